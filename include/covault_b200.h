@@ -1,0 +1,88 @@
+/*
+ * covault_b200.h -- C ABI of the B200-native hot path of arXiv 2103.16898 (reference: covault).
+ *
+ * Plain pointers and sizes only.  Status codes: 0 ok, 1 authentication failure,
+ * <0 error (cvb_last_error() gives a message).  Device pointers are CUDA global memory;
+ * `stream` is a cudaStream_t (pass torch.cuda.current_stream().cuda_stream).
+ *
+ * The reference exposes these operations as Python functions (it has no FFI); each entry
+ * below names the reference interface it replaces.  INTEGRATION.md shows the ctypes
+ * binding a maintainer adds on the reference side.
+ */
+#ifndef COVAULT_B200_H
+#define COVAULT_B200_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CVB_OK 0
+#define CVB_AUTH_FAIL 1
+#define CVB_EINVAL (-1)
+#define CVB_ECUDA (-2)
+#define CVB_ENOMEM (-3)
+
+int cvb_version(void);
+const char* cvb_last_error(void);
+int cvb_set_device(int device);
+int cvb_device_sync(void);
+
+/* ---- AEAD: AES-256-GCM, NIST SP 800-38D, 96-bit nonce, 128-bit tag ------------------- */
+
+/* Replaces covault.crypto.aead_open (pkg/src/covault/crypto.py:265-272).
+ * blob = C || T (blob_len >= 16; shorter -> CVB_AUTH_FAIL like cryptography's InvalidTag).
+ * On success writes blob_len-16 plaintext bytes to `out` (host memory).  On CVB_AUTH_FAIL
+ * `out` is not written.  Synchronous; host buffers. */
+int cvb_aead_open(const uint8_t key[32], const uint8_t nonce[12], const uint8_t* aad, size_t aad_len,
+                  const uint8_t* blob, size_t blob_len, uint8_t* out);
+
+/* Replaces covault.crypto.aead_seal (pkg/src/covault/crypto.py:258-262): out gets len+16
+ * bytes C || T.  Synchronous; host buffers. */
+int cvb_aead_seal(const uint8_t key[32], const uint8_t nonce[12], const uint8_t* aad, size_t aad_len,
+                  const uint8_t* pt, size_t len, uint8_t* out);
+
+/* FIPS-197 single block (host) -- self test of the key schedule the kernels use. */
+int cvb_aes256_encrypt_block_host(const uint8_t key[32], const uint8_t in[16], uint8_t out[16]);
+
+/* Device-resident per-key context (expanded key + GHASH power tables in HBM).
+ * Used by covault.volume.Volume.get's B200 path (pkg/src/covault/volume.py:185-197). */
+typedef struct cvb_gcm_ctx cvb_gcm_ctx;
+int cvb_gcm_ctx_create(const uint8_t key[32], cvb_gcm_ctx** out);
+void cvb_gcm_ctx_destroy(cvb_gcm_ctx* ctx);
+
+/* Asynchronous, stream-ordered open of a blob already in HBM.  work: >= 8 zeroed uint32
+ * device words private to this call; status (0 ok / 1 tag mismatch) lands in work[4].
+ * On mismatch `out_dev` is zeroed on the stream before later work can read it. */
+int cvb_gcm_open_dev(cvb_gcm_ctx* ctx, const uint8_t nonce[12], const uint8_t* aad_dev, size_t aad_len,
+                     const uint8_t* blob_dev, size_t blob_len, uint8_t* out_dev, uint32_t* work_dev,
+                     void* stream);
+
+/* Asynchronous seal: out_dev receives len + 16 bytes (C || T).  Replaces the AEAD inside
+ * covault.volume.Volume.put (pkg/src/covault/volume.py:161-183). */
+int cvb_gcm_seal_dev(cvb_gcm_ctx* ctx, const uint8_t nonce[12], const uint8_t* aad_dev, size_t aad_len,
+                     const uint8_t* pt_dev, size_t len, uint8_t* out_dev, uint32_t* work_dev, void* stream);
+
+/* ---- loader: verified plaintext records -> normalised NHWC input tile ------------------ */
+
+/* Replaces Volume.get(...).decode + parse_dataset (pkg/src/covault/workload.py:24-41) for
+ * the binary record payload (1 label byte + C*H*W CHW bytes per record).  Output NHWC with
+ * channels padded to 8, value (x/255 - mean_c)/std_c; dtype 0 = bf16, 1 = fp32; labels
+ * int32.  Asynchronous. */
+int cvb_records_to_nhwc(const uint8_t* pt_dev, int64_t nrec, int64_t rec_bytes, int64_t c, int64_t h,
+                        int64_t w, const float* mean, const float* std, int dtype, void* out_dev,
+                        int32_t* labels_dev, void* stream);
+
+/* ---- reference trainer ---------------------------------------------------------------- */
+
+/* Numeric core of covault.workload.run_training (pkg/src/covault/workload.py:48-71).
+ * X: n x f row-major binary64 (host), y: n labels (host).  mode 0 = bit-exact reference
+ * order (reproduces the golden model digest), 1 = parallel reductions.  Synchronous. */
+int cvb_logistic_train(const double* X, const double* y, int64_t n, int64_t f, double lr, int64_t epochs,
+                       int mode, double* w_out, double* b_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,105 @@
+"""Loader for the in-tree C-ABI library ``libcovault_b200.so`` (sm_100a kernels).
+
+There is no fallback: if the library is missing or cannot be loaded the import of any
+compute entry point raises :class:`NativeLibraryMissing`.  Build it with
+``python -c "import __graft_entry__ as g; g.build()"`` (or ``make -C
+paper_2103_16898_b200/csrc``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("CVB_LIB", _HERE / "libcovault_b200.so"))
+
+_lock = threading.Lock()
+_lib = None
+
+# status codes (include/covault_b200.h)
+CVB_OK = 0
+CVB_AUTH_FAIL = 1
+CVB_EINVAL = -1
+CVB_ECUDA = -2
+CVB_ENOMEM = -3
+
+_c = ctypes
+_P = _c.c_void_p
+_SZ = _c.c_size_t
+_I64 = _c.c_int64
+_INT = _c.c_int
+
+# name -> (restype, argtypes); every symbol declared in include/*.h is listed here
+SIGNATURES = {
+    "cvb_version": (_INT, []),
+    "cvb_last_error": (_c.c_char_p, []),
+    "cvb_set_device": (_INT, [_INT]),
+    "cvb_device_sync": (_INT, []),
+    "cvb_aes256_encrypt_block_host": (_INT, [_P, _P, _P]),
+    "cvb_aead_open": (_INT, [_P, _P, _P, _SZ, _P, _SZ, _P]),
+    "cvb_aead_seal": (_INT, [_P, _P, _P, _SZ, _P, _SZ, _P]),
+    "cvb_gcm_ctx_create": (_INT, [_P, _c.POINTER(_P)]),
+    "cvb_gcm_ctx_destroy": (None, [_P]),
+    "cvb_gcm_open_dev": (_INT, [_P, _P, _P, _SZ, _P, _SZ, _P, _P, _P]),
+    "cvb_gcm_seal_dev": (_INT, [_P, _P, _P, _SZ, _P, _SZ, _P, _P, _P]),
+    "cvb_records_to_nhwc": (_INT, [_P, _I64, _I64, _I64, _I64, _I64, _P, _P, _INT, _P, _P, _P]),
+    "cvb_logistic_train": (_INT, [_P, _P, _I64, _I64, _c.c_double, _I64, _INT, _P, _P]),
+}
+
+
+class NativeLibraryMissing(RuntimeError):
+    pass
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def load():
+    """Return the loaded ctypes library (raises NativeLibraryMissing if absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise NativeLibraryMissing(
+                f"{LIB_PATH} not built; run `make -C {_HERE / 'csrc'}` (no CPU fallback exists)")
+        lib = ctypes.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def check(rc: int, what: str) -> int:
+    if rc < 0:
+        msg = load().cvb_last_error().decode("utf-8", "replace")
+        raise NativeError(f"{what} failed ({rc}): {msg}")
+    return rc
+
+
+_device_bound = set()
+
+
+def bind_device(dev: int | None = None) -> None:
+    """Point the library's CUDA runtime at torch's current device (once per device)."""
+    import torch
+
+    if dev is None:
+        dev = torch.cuda.current_device()
+    if dev not in _device_bound:
+        check(load().cvb_set_device(int(dev)), "cvb_set_device")
+        _device_bound.add(dev)
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)

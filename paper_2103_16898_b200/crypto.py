@@ -1,0 +1,164 @@
+"""GPU AES-256-GCM behind the reference's AEAD API.
+
+Same signatures, argument meaning and exceptions as
+  covault.crypto.aead_seal(key, nonce, aad, plaintext) -> bytes   crypto.py:258-262
+  covault.crypto.aead_open(key, nonce, aad, ciphertext) -> bytes  crypto.py:265-272
+  covault.crypto.SymmetricKey                                     crypto.py:213-255
+When the reference package is importable its exception classes are used, so these
+functions can be monkeypatched into ``covault.crypto`` and the reference's own tests keep
+catching the same types.  The device-side API (``GcmContext``) keeps
+ciphertext and plaintext in HBM for the training loader.
+"""
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import secrets
+
+from . import _lib
+
+AEAD_NONCE_SIZE = 12
+SYMMETRIC_KEY_SIZE = 32
+KEY_COMMITMENT_TAG = b"covault.key-commitment.v1"   # crypto.py:38
+
+try:  # share exception identity with the reference when it is installed
+    from covault.crypto import AuthenticationFailure, CryptoError, DecodeError  # type: ignore
+except Exception:  # pragma: no cover - standalone use
+    class CryptoError(Exception):
+        """Base class for failures in this module (crypto.py:42-43)."""
+
+    class DecodeError(CryptoError):
+        """Malformed key or nonce (crypto.py:46-47)."""
+
+    class AuthenticationFailure(CryptoError):
+        """AEAD open failed (crypto.py:50-51)."""
+
+
+class SymmetricKey:
+    """32 bytes of key material plus its commitment key_id = SHA-256(key || tag)."""
+
+    __slots__ = ("_bytes", "key_id")
+
+    def __init__(self, raw: bytes) -> None:
+        if len(raw) != SYMMETRIC_KEY_SIZE:
+            raise DecodeError(f"symmetric key must be {SYMMETRIC_KEY_SIZE} bytes")
+        self._bytes = bytes(raw)
+        self.key_id = hashlib.sha256(self._bytes + KEY_COMMITMENT_TAG).digest()
+
+    @classmethod
+    def from_hex(cls, text: str) -> "SymmetricKey":
+        try:
+            return cls(bytes.fromhex(text))
+        except ValueError as e:
+            raise DecodeError(f"bad key hex: {e}") from e
+
+    @classmethod
+    def generate(cls) -> "SymmetricKey":
+        return cls(secrets.token_bytes(SYMMETRIC_KEY_SIZE))
+
+    def reveal_bytes(self) -> bytes:
+        return self._bytes
+
+    def __repr__(self) -> str:
+        return f"SymmetricKey(id={self.key_id.hex()[:12]}…)"
+
+
+def _key_bytes(key) -> bytes:
+    raw = key.reveal_bytes() if hasattr(key, "reveal_bytes") else bytes(key)
+    if len(raw) != SYMMETRIC_KEY_SIZE:
+        raise DecodeError(f"symmetric key must be {SYMMETRIC_KEY_SIZE} bytes")
+    return raw
+
+
+def aead_seal(key, nonce: bytes, aad: bytes, plaintext: bytes) -> bytes:
+    """AES-256-GCM seal on the GPU -> C || T (crypto.py:258-262)."""
+    if len(nonce) != AEAD_NONCE_SIZE:
+        raise DecodeError(f"nonce must be {AEAD_NONCE_SIZE} bytes")
+    lib = _lib.load()
+    kb = _key_bytes(key)
+    out = ctypes.create_string_buffer(len(plaintext) + 16)
+    rc = lib.cvb_aead_seal(kb, bytes(nonce), bytes(aad), len(aad), bytes(plaintext), len(plaintext), out)
+    _lib.check(rc, "aead_seal")
+    return out.raw
+
+
+def aead_open(key, nonce: bytes, aad: bytes, ciphertext: bytes) -> bytes:
+    """AES-256-GCM open on the GPU; raises AuthenticationFailure on any mismatch."""
+    if len(nonce) != AEAD_NONCE_SIZE:
+        raise DecodeError(f"nonce must be {AEAD_NONCE_SIZE} bytes")
+    lib = _lib.load()
+    kb = _key_bytes(key)
+    n = len(ciphertext)
+    out = ctypes.create_string_buffer(max(1, n - 16))
+    rc = lib.cvb_aead_open(kb, bytes(nonce), bytes(aad), len(aad), bytes(ciphertext), n, out)
+    _lib.check(rc, "aead_open")
+    if rc == _lib.CVB_AUTH_FAIL:
+        raise AuthenticationFailure("AEAD authentication failed")
+    return out.raw[: n - 16]
+
+
+def fresh_nonce() -> bytes:
+    return secrets.token_bytes(AEAD_NONCE_SIZE)
+
+
+class GcmContext:
+    """Per-key device context: expanded key + GHASH power tables resident in HBM.
+
+    ``open_device`` / ``seal_device`` are stream-ordered and never synchronise; the tag
+    verdict lands in a device status word (``status_tensor``) and, on a mismatch, the
+    plaintext is zeroed on-stream before any later kernel can read it.
+    """
+
+    def __init__(self, key):
+        import torch
+
+        _lib.bind_device()
+        self._lib = _lib.load()
+        self._ptr = ctypes.c_void_p()
+        _lib.check(self._lib.cvb_gcm_ctx_create(_key_bytes(key), ctypes.byref(self._ptr)), "gcm_ctx_create")
+        self._torch = torch
+
+    def close(self):
+        if self._ptr:
+            self._lib.cvb_gcm_ctx_destroy(self._ptr)
+            self._ptr = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def new_workspace(self, device=None):
+        """8 zeroed uint32 words: GHASH accumulator [0:4] + status [4]."""
+        return self._torch.zeros(8, dtype=self._torch.int32, device=device or "cuda")
+
+    def open_device(self, nonce: bytes, aad_dev, blob_dev, out_dev, work, stream=None):
+        """blob_dev: uint8 CUDA tensor C||T; out_dev: uint8 CUDA tensor of len(C)."""
+        if len(nonce) != AEAD_NONCE_SIZE:
+            raise DecodeError(f"nonce must be {AEAD_NONCE_SIZE} bytes")
+        n = blob_dev.numel()
+        if out_dev.numel() < n - 16:
+            raise ValueError("output buffer too small")
+        aad_ptr = aad_dev.data_ptr() if aad_dev is not None and aad_dev.numel() else None
+        aad_len = aad_dev.numel() if aad_dev is not None else 0
+        rc = self._lib.cvb_gcm_open_dev(self._ptr, bytes(nonce), aad_ptr, aad_len, blob_dev.data_ptr(), n,
+                                        out_dev.data_ptr(), work.data_ptr(), _lib.stream_ptr(stream))
+        _lib.check(rc, "gcm_open_dev")
+
+    def seal_device(self, nonce: bytes, aad_dev, pt_dev, out_dev, work, stream=None):
+        if len(nonce) != AEAD_NONCE_SIZE:
+            raise DecodeError(f"nonce must be {AEAD_NONCE_SIZE} bytes")
+        n = pt_dev.numel()
+        if out_dev.numel() < n + 16:
+            raise ValueError("output buffer too small")
+        aad_ptr = aad_dev.data_ptr() if aad_dev is not None and aad_dev.numel() else None
+        aad_len = aad_dev.numel() if aad_dev is not None else 0
+        rc = self._lib.cvb_gcm_seal_dev(self._ptr, bytes(nonce), aad_ptr, aad_len, pt_dev.data_ptr() if n else None,
+                                        n, out_dev.data_ptr(), work.data_ptr(), _lib.stream_ptr(stream))
+        _lib.check(rc, "gcm_seal_dev")
+
+    @staticmethod
+    def status_ok(work) -> bool:
+        """Host check of the tag verdict (synchronises on the work tensor)."""
+        return int(work[4].item()) == 0
