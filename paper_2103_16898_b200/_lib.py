@@ -46,6 +46,13 @@ SIGNATURES = {
     "cvb_gcm_seal_dev": (_INT, [_P, _P, _P, _SZ, _P, _SZ, _P, _P, _P]),
     "cvb_records_to_nhwc": (_INT, [_P, _I64, _I64, _I64, _I64, _I64, _P, _P, _INT, _P, _P, _P]),
     "cvb_logistic_train": (_INT, [_P, _P, _I64, _I64, _c.c_double, _I64, _INT, _P, _P]),
+    # tcgen05 implicit-GEMM engine (include/cvb_nn.h)
+    "cvb_conv2d_fwd": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT,
+                              _INT, _INT, _P, _INT, _P]),
+    "cvb_conv2d_wgrad": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT, _INT, _INT, _INT, _INT, _INT,
+                                _INT, _P, _INT, _c.POINTER(_INT), _P]),
+    "cvb_gemm": (_INT, [_P, _INT, _I64, _P, _INT, _I64, _INT, _INT, _INT, _P, _I64, _INT, _P, _INT, _P]),
+    "cvb_gemm_splits_used": (_INT, [_INT, _INT]),
 }
 
 

@@ -1,0 +1,683 @@
+// tcgen05 implicit-GEMM engine for conv / dense layers (K5 of DESIGN.md).
+//
+// No reference code exists for this layer type (the reference trainer is a logistic toy,
+// pkg/src/covault/workload.py:48-71); the CNN is defined from the paper's prose
+// -- see DESIGN.md.
+//
+// One persistent, warp-specialised kernel serves every GEMM of a training step:
+//   warp 0      TMA producer: per K-block, G boxes per operand, loaded straight from the
+//               NHWC activation (4-D tensor map; conv padding = TMA out-of-bounds zero
+//               fill) or from 2-D weight / dense maps, into a multi-stage smem ring.
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (kind::f16, bf16 in,
+//               fp32 accumulate in TMEM, 128 x BN tile, 4 MMAs of K=16 per 64-wide K-block),
+//               double-buffered accumulators so the epilogue of tile i overlaps tile i+1.
+//   warps 2..5  epilogue: tcgen05.ld 32x32b -> bias -> bf16/fp32 -> global (NHWC rows,
+//               dense rows or fp32 split-K partials).
+// Modes:
+//   FWD   A = gathered activation (K-major, K = taps x Cin), B = weights [Cout][K] (K-major).
+//         Used for conv forward and for dgrad (input dY or its zero-upsampled copy, weights
+//         flipped/transposed).  Stride-2 convs read the input through 4 parity views.
+//   WGRAD A = dY (MN-major, M = Cout), B = gathered input (MN-major, N = taps x Cin),
+//         K = output pixels in 64-pixel boxes, split over CTAs, fp32 partials.
+//   DENSE 2-D operands, each K-major or MN-major (FC fwd/dgrad/wgrad).
+#include "cvb_common.cuh"
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+
+namespace {
+
+enum { MODE_FWD = 0, MODE_WGRAD = 1, MODE_DENSE = 2 };
+enum { OUT_NHWC = 0, OUT_ROWS = 1, OUT_PARTIAL = 2 };
+
+constexpr int BM = 128;          // UMMA M (cta_group::1)
+constexpr int BK = 64;           // K elements per pipeline stage
+constexpr int NUM_THREADS = 192; // 6 warps
+
+struct GemmParams {
+  CUtensorMap mapA[4];
+  CUtensorMap mapB[4];
+  int mode;
+  int a_major, b_major;     // 0 = K-major, 1 = MN-major
+  int a_cel, b_cel;         // channels / elements per box row (8,16,32,64)
+  int BN;
+  int M, N;                 // logical GEMM extents (rows, cols)
+  int m_tiles, n_tiles, splits;
+  int num_kb;               // total K-blocks of the full K range
+  int kb_per_split;
+  int a_box_rows;           // rows TMA writes per A box (FWD/DENSE-K: <=128)
+  uint32_t tx_bytes;
+  uint32_t idesc;
+  int stages;
+  // conv geometry
+  int tw, th, tn;           // pixel-box extents (FWD: the M tile; WGRAD: the K chunk)
+  int ptiles_w, ptiles_h;   // tile counts along w, h of the pixel space
+  int OH, OW, NIMG;         // pixel space (FWD: output; WGRAD: dY)
+  int KH, KW, pad, stride;  // gathered operand geometry
+  int cin;                  // channels of the gathered operand (padded, multiple of cel)
+  int ntaps;
+  // epilogue
+  int out_mode, out_f32;
+  void* out;
+  int64_t ldc;              // row stride of the output in elements
+  int col_off;
+  const float* bias;
+  int part_rows;            // OUT_PARTIAL: rows per split slab
+};
+
+// ---------------------------------------------------------------------------------------
+// PTX helpers
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, void* dst, uint64_t* bar, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)),
+        "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, void* dst, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc) : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor (sm_100: version 1 at bits 46-47).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)layout << 61;
+  return d;
+}
+__device__ __forceinline__ uint32_t layout_of(int rowbytes) {
+  return rowbytes == 128 ? 2u : rowbytes == 64 ? 4u : rowbytes == 32 ? 6u : 0u;
+}
+
+// Descriptor of MMA k-step s (16 K elements) of one operand stage.
+//   K-major : `rows` rows per box, boxes of cel K-elements at stride rows*R
+//   MN-major: boxes of cel MN-elements x 64 K-rows at stride 64*R
+__device__ __forceinline__ uint64_t operand_desc(uint32_t base, int major, int cel, int rows, int s) {
+  const int R = cel * 2;
+  if (major == 0) {
+    if (R == 16) return make_desc(base + 2 * s * rows * 16, rows * 16, 128, 0);
+    const int kb = 32 * s;  // byte offset of the k-step along K
+    return make_desc(base + (kb / R) * rows * R + (kb % R), 16, 8 * R, layout_of(R));
+  }
+  if (R == 16) return make_desc(base + s * 256, 128, 64 * 16, 0);
+  return make_desc(base + s * 16 * R, 64 * R, 8 * R, layout_of(R));
+}
+
+// ---------------------------------------------------------------------------------------
+// The kernel
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_constant__ GemmParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t a_stage = BM * BK * 2;            // 16 KB
+  const uint32_t b_stage = p.BN * BK * 2;
+  const uint32_t stage_bytes = a_stage + b_stage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes);
+  uint64_t* empty = full + p.stages;
+  uint64_t* tfull = empty + p.stages;       // [2]
+  uint64_t* tempty = tfull + 2;             // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tmem_cols = (2 * p.BN <= 32) ? 32 : (2 * p.BN <= 64) ? 64 : (2 * p.BN <= 128) ? 128 : (2 * p.BN <= 256) ? 256 : 512;
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < 4; i++) { prefetch_map(&p.mapA[i]); prefetch_map(&p.mapB[i]); }
+    for (int i = 0; i < p.stages; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int units = p.m_tiles * p.n_tiles * p.splits;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===================== TMA producer =====================
+      int it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int mt = u % p.m_tiles, rest = u / p.m_tiles;
+        const int nt = rest % p.n_tiles, sp = rest / p.n_tiles;
+        const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+        // FWD: tile mt is a pixel box of the output
+        int tw0 = 0, th0 = 0, tn0 = 0;
+        if (p.mode == MODE_FWD) {
+          tw0 = (mt % p.ptiles_w) * p.tw;
+          int r2 = mt / p.ptiles_w;
+          th0 = (r2 % p.ptiles_h) * p.th;
+          tn0 = (r2 / p.ptiles_h) * p.tn;
+        }
+        const int m0 = mt * BM, n0 = nt * p.BN;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % p.stages;
+          const uint32_t ph = (it / p.stages) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], p.tx_bytes);
+          uint8_t* sa = smem + s * stage_bytes;
+          uint8_t* sb = sa + a_stage;
+          if (p.mode == MODE_FWD) {
+            const int ga = BK / p.a_cel;
+            for (int g = 0; g < ga; g++) {
+              const int k = kb * BK + g * p.a_cel;
+              const int tap = k / p.cin, ci = k - tap * p.cin;
+              int mi = 0, cw = tw0, ch = th0, cc = ci;
+              if (tap < p.ntaps) {
+                const int kh = tap / p.KW, kw = tap - kh * p.KW;
+                const int dh = kh - p.pad, dw = kw - p.pad;
+                if (p.stride == 1) { cw = tw0 + dw; ch = th0 + dh; }
+                else { mi = ((dh & 1) << 1) | (dw & 1); cw = tw0 + (dw >> 1); ch = th0 + (dh >> 1); }
+              } else {
+                cc = p.cin;  // fully out of bounds -> zeros
+              }
+              tma_load_4d(&p.mapA[mi], sa + g * BM * p.a_cel * 2, &full[s], cc, cw, ch, tn0);
+            }
+            const int gb = BK / p.b_cel;
+            for (int g = 0; g < gb; g++)
+              tma_load_2d(&p.mapB[0], sb + g * p.BN * p.b_cel * 2, &full[s], kb * BK + g * p.b_cel, n0);
+          } else if (p.mode == MODE_WGRAD) {
+            // K chunk kb = a pixel box of the dY space
+            const int pw = (kb % p.ptiles_w) * p.tw;
+            const int r2 = kb / p.ptiles_w;
+            const int ph0 = (r2 % p.ptiles_h) * p.th;
+            const int pn = (r2 / p.ptiles_h) * p.tn;
+            const int ga = BM / p.a_cel;
+            for (int b = 0; b < ga; b++)
+              tma_load_4d(&p.mapA[0], sa + b * BK * p.a_cel * 2, &full[s], m0 + b * p.a_cel, pw, ph0, pn);
+            const int gb = p.BN / p.b_cel;
+            for (int j = 0; j < gb; j++) {
+              const int col = n0 + j * p.b_cel;
+              const int tap = col / p.cin, ci = col - tap * p.cin;
+              int mi = 0, cw = pw, ch = ph0, cc = ci;
+              if (tap < p.ntaps) {
+                const int kh = tap / p.KW, kw = tap - kh * p.KW;
+                const int dh = kh - p.pad, dw = kw - p.pad;
+                if (p.stride == 1) { cw = pw + dw; ch = ph0 + dh; }
+                else { mi = ((dh & 1) << 1) | (dw & 1); cw = pw + (dw >> 1); ch = ph0 + (dh >> 1); }
+              } else {
+                cc = p.cin;
+              }
+              tma_load_4d(&p.mapB[mi], sb + j * BK * p.b_cel * 2, &full[s], cc, cw, ch, pn);
+            }
+          } else {  // DENSE
+            if (p.a_major == 0) {
+              for (int g = 0; g < BK / p.a_cel; g++)
+                tma_load_2d(&p.mapA[0], sa + g * BM * p.a_cel * 2, &full[s], kb * BK + g * p.a_cel, m0);
+            } else {
+              for (int b = 0; b < BM / p.a_cel; b++)
+                tma_load_2d(&p.mapA[0], sa + b * BK * p.a_cel * 2, &full[s], m0 + b * p.a_cel, kb * BK);
+            }
+            if (p.b_major == 0) {
+              for (int g = 0; g < BK / p.b_cel; g++)
+                tma_load_2d(&p.mapB[0], sb + g * p.BN * p.b_cel * 2, &full[s], kb * BK + g * p.b_cel, n0);
+            } else {
+              for (int j = 0; j < p.BN / p.b_cel; j++)
+                tma_load_2d(&p.mapB[0], sb + j * BK * p.b_cel * 2, &full[s], n0 + j * p.b_cel, kb * BK);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===================== MMA issuer =====================
+      int it = 0, lt = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
+        const int sp = u / (p.m_tiles * p.n_tiles);
+        const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+        const int acc = lt & 1;
+        mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * p.BN;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % p.stages;
+          const uint32_t ph = (it / p.stages) & 1;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * stage_bytes);
+          const uint32_t sb = sa + a_stage;
+#pragma unroll
+          for (int k = 0; k < BK / 16; k++) {
+            uint64_t ad = operand_desc(sa, p.a_major, p.a_cel, BM, k);
+            uint64_t bd = operand_desc(sb, p.b_major, p.b_cel, p.BN, k);
+            umma_bf16(tmem_d, ad, bd, p.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // ===================== epilogue (warps 2..5) =====================
+    const int quarter = warp & 3;              // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;       // accumulator row (0..127)
+    int lt = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
+      const int mt = u % p.m_tiles, rest = u / p.m_tiles;
+      const int nt = rest % p.n_tiles, sp = rest / p.n_tiles;
+      const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+      const int acc = lt & 1;
+      mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      tc_fence_after();
+      // destination row
+      bool valid = true;
+      int64_t dst_row = 0;
+      if (p.out_mode == OUT_NHWC) {
+        const int wb = row % p.tw, r2 = row / p.tw, hb = r2 % p.th, nb = r2 / p.th;
+        const int ow = (mt % p.ptiles_w) * p.tw + wb;
+        const int q = mt / p.ptiles_w;
+        const int oh = (q % p.ptiles_h) * p.th + hb;
+        const int n = (q / p.ptiles_h) * p.tn + nb;
+        valid = (row < p.tw * p.th * p.tn) && ow < p.OW && oh < p.OH && n < p.NIMG;
+        dst_row = (((int64_t)n * p.OH + oh) * p.OW + ow);
+      } else if (p.out_mode == OUT_ROWS) {
+        const int m = mt * BM + row;
+        valid = m < p.M;
+        dst_row = m;
+      } else {
+        const int m = mt * BM + row;
+        valid = m < p.part_rows;
+        dst_row = (int64_t)sp * p.part_rows + m;
+      }
+      const bool has_k = kb1 > kb0;
+      const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * p.BN;
+      for (int c = 0; c < p.BN; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(tbase + c, r);
+        const int col = nt * p.BN + c;
+        if (!valid) continue;
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+          v[j] = has_k ? __uint_as_float(r[j]) : 0.f;
+          if (p.bias && col + j < p.N) v[j] += p.bias[col + j];
+        }
+        const int64_t off = dst_row * p.ldc + p.col_off + col;
+        if (col + 16 <= p.N) {
+          if (p.out_f32) {
+            float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + off);
+#pragma unroll
+            for (int j = 0; j < 4; j++) d[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          } else {
+            uint32_t pk[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+              __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+              pk[j] = *reinterpret_cast<uint32_t*>(&h);
+            }
+            uint4* d = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + off);
+            d[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            d[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
+        } else {
+          for (int j = 0; j < 16 && col + j < p.N; j++) {
+            if (p.out_f32) reinterpret_cast<float*>(p.out)[off + j] = v[j];
+            else reinterpret_cast<__nv_bfloat16*>(p.out)[off + j] = __float2bfloat16_rn(v[j]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncwarp();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Host side: tensor maps and launch planning
+// ---------------------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+int get_encoder() {
+  if (g_encode) return CVB_OK;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  CVB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) { cvb_set_error("cuTensorMapEncodeTiled unavailable"); return CVB_ECUDA; }
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return CVB_OK;
+}
+
+CUtensorMapSwizzle swz_of(int rowbytes) {
+  return rowbytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : rowbytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+       : rowbytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
+}
+
+int encode(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+           const uint32_t* box, int rowbytes) {
+  uint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims, strides_bytes, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz_of(rowbytes), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    cvb_set_error("cuTensorMapEncodeTiled failed (%d) rank=%d dims=%llu,%llu,%llu,%llu box=%u,%u,%u,%u", (int)r, rank,
+                  (unsigned long long)dims[0], (unsigned long long)(rank > 1 ? dims[1] : 0),
+                  (unsigned long long)(rank > 2 ? dims[2] : 0), (unsigned long long)(rank > 3 ? dims[3] : 0), box[0],
+                  rank > 1 ? box[1] : 0, rank > 2 ? box[2] : 0, rank > 3 ? box[3] : 0);
+    return CVB_EINVAL;
+  }
+  return CVB_OK;
+}
+
+// NHWC activation map (channel stride cstride, using channels [0, c)), box (cel, bw, bh, bn).
+// parity (rh, rw) >= 0 builds the stride-2 view of rows rh::2 and cols rw::2.
+int encode_nhwc(CUtensorMap* m, const void* base, int n, int h, int w, int c, int cstride, int cel, int bw, int bh,
+                int bn, int rh = -1, int rw = -1) {
+  const uint64_t es = 2;
+  if (rh < 0) {
+    uint64_t dims[4] = {(uint64_t)c, (uint64_t)w, (uint64_t)h, (uint64_t)n};
+    uint64_t st[3] = {cstride * es, (uint64_t)w * cstride * es, (uint64_t)h * w * cstride * es};
+    uint32_t box[4] = {(uint32_t)cel, (uint32_t)bw, (uint32_t)bh, (uint32_t)bn};
+    return encode(m, base, 4, dims, st, box, cel * 2);
+  }
+  const char* b = reinterpret_cast<const char*>(base) + ((int64_t)rh * w + rw) * cstride * es;
+  uint64_t w2 = (uint64_t)(w - rw + 1) / 2, h2 = (uint64_t)(h - rh + 1) / 2;
+  if (w2 == 0) w2 = 1;
+  if (h2 == 0) h2 = 1;
+  uint64_t dims[4] = {(uint64_t)c, w2, h2, (uint64_t)n};
+  uint64_t st[3] = {2 * cstride * es, 2 * (uint64_t)w * cstride * es, (uint64_t)h * w * cstride * es};
+  uint32_t box[4] = {(uint32_t)cel, (uint32_t)bw, (uint32_t)bh, (uint32_t)bn};
+  return encode(m, b, 4, dims, st, box, cel * 2);
+}
+
+// 2-D row-major [rows][cols] (ld elements per row), box (cel, brows)
+int encode_2d(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld, int cel, int brows) {
+  uint64_t dims[2] = {(uint64_t)cols, (uint64_t)rows};
+  uint64_t st[1] = {(uint64_t)ld * 2};
+  uint32_t box[2] = {(uint32_t)cel, (uint32_t)brows};
+  return encode(m, base, 2, dims, st, box, cel * 2);
+}
+
+int pick_cel(int c) {
+  if (c % 64 == 0) return 64;
+  if (c % 32 == 0) return 32;
+  if (c % 16 == 0) return 16;
+  if (c % 8 == 0) return 8;
+  return 0;
+}
+
+uint32_t make_idesc(int a_major, int b_major, int bn) {
+  uint32_t d = 0;
+  d |= 1u << 4;                    // D = f32
+  d |= 1u << 7;                    // A = bf16
+  d |= 1u << 10;                   // B = bf16
+  d |= (uint32_t)a_major << 15;
+  d |= (uint32_t)b_major << 16;
+  d |= (uint32_t)(bn >> 3) << 17;
+  d |= (uint32_t)(BM >> 4) << 24;
+  return d;
+}
+
+int g_num_sms = 0;
+bool g_attr_done = false;
+
+int launch(GemmParams& p, cudaStream_t stream) {
+  if (!g_num_sms) g_num_sms = cvb_num_sms();
+  const uint32_t stage_bytes = (BM + p.BN) * BK * 2;
+  p.stages = (int)((200u * 1024u) / stage_bytes);
+  if (p.stages > 8) p.stages = 8;
+  if (p.stages < 2) { cvb_set_error("BN too large"); return CVB_EINVAL; }
+  size_t smem = (size_t)p.stages * stage_bytes + 1024 + 256;
+  if (!g_attr_done) {
+    CVB_CUDA(cudaFuncSetAttribute(umma_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    g_attr_done = true;
+  }
+  p.idesc = make_idesc(p.a_major, p.b_major, p.BN);
+  const int units = p.m_tiles * p.n_tiles * p.splits;
+  const int grid = units < g_num_sms ? units : g_num_sms;
+  umma_gemm_kernel<<<grid, NUM_THREADS, smem, stream>>>(p);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+int pick_bn(int n) {
+  if (n <= 256) return (n + 15) / 16 * 16;
+  // split N into near-equal tiles that are multiples of 16 and <= 256
+  int tiles = (n + 255) / 256;
+  int bn = ((n + tiles - 1) / tiles + 15) / 16 * 16;
+  return bn;
+}
+
+// pixel box for an M tile of 128 output rows
+void pick_mbox(int n, int oh, int ow, int& bw, int& bh, int& bn) {
+  if (ow >= BM) { bw = BM; bh = 1; bn = 1; return; }
+  bw = ow;
+  int hmax = BM / ow;
+  if (hmax >= oh) {
+    bh = oh;
+    bn = BM / (ow * oh);
+    if (bn > n) bn = n;
+    return;
+  }
+  int ht = (oh + hmax - 1) / hmax;
+  bh = (oh + ht - 1) / ht;
+  bn = 1;
+}
+
+int next_pow2(int x) { int p = 1; while (p < x) p <<= 1; return p; }
+
+// pixel box for a 64-pixel K chunk (wgrad): exact 64 rows, OOB rows zero-filled by TMA
+void pick_kbox(int n, int oh, int ow, int& bw, int& bh, int& bn) {
+  bw = min(64, next_pow2(ow));
+  bh = min(64 / bw, next_pow2(oh));
+  bn = 64 / (bw * bh);
+  (void)n;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------------------
+
+// Convolution forward as implicit GEMM (also serves dgrad):
+//   y[n,oh,ow, yoff+co] = bias[co] + sum_{kh,kw,ci} x[n, oh*s-pad+kh, ow*s-pad+kw, ci] * w[co][kh][kw][ci]
+// x: NHWC bf16 (channel stride xcs, channels [0,cin)), cin multiple of 8.
+// w: bf16 [cout][kh*kw*cin] (K-major).  y: NHWC (bf16, or fp32 if y_f32) with channel stride ycs.
+CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs, const void* wt, int cout, int kh,
+                           int kw, int stride, int pad, void* y, int oh, int ow, int ycs, int yoff, const float* bias,
+                           int y_f32, void* stream) {
+  if (get_encoder()) return CVB_ECUDA;
+  const int acel = pick_cel(cin);
+  if (!acel || (stride != 1 && stride != 2) || cout % 8) { cvb_set_error("conv2d_fwd: unsupported shape"); return CVB_EINVAL; }
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.mode = MODE_FWD;
+  p.a_major = 0; p.b_major = 0;
+  p.a_cel = acel;
+  const int K = kh * kw * cin;
+  p.b_cel = 64;   // weights [cout][K]: 128-byte rows, K tail zero-filled by TMA
+  p.BN = pick_bn(cout);
+  p.M = n * oh * ow;
+  p.N = cout;
+  int bw, bh, bnn;
+  pick_mbox(n, oh, ow, bw, bh, bnn);
+  p.tw = bw; p.th = bh; p.tn = bnn;
+  p.ptiles_w = (ow + bw - 1) / bw;
+  p.ptiles_h = (oh + bh - 1) / bh;
+  const int ptiles_n = (n + bnn - 1) / bnn;
+  p.m_tiles = p.ptiles_w * p.ptiles_h * ptiles_n;
+  p.n_tiles = (cout + p.BN - 1) / p.BN;
+  p.splits = 1;
+  p.num_kb = (K + BK - 1) / BK;
+  p.kb_per_split = p.num_kb;
+  p.a_box_rows = bw * bh * bnn;
+  p.OH = oh; p.OW = ow; p.NIMG = n;
+  p.KH = kh; p.KW = kw; p.pad = pad; p.stride = stride;
+  p.cin = cin; p.ntaps = kh * kw;
+  p.tx_bytes = (BK / p.a_cel) * p.a_box_rows * p.a_cel * 2 + (BK / p.b_cel) * p.BN * p.b_cel * 2;
+  int rc;
+  if (stride == 1) {
+    if ((rc = encode_nhwc(&p.mapA[0], x, n, h, w, cin, xcs, acel, bw, bh, bnn))) return rc;
+  } else {
+    for (int rh = 0; rh < 2; rh++)
+      for (int rw = 0; rw < 2; rw++)
+        if ((rc = encode_nhwc(&p.mapA[rh * 2 + rw], x, n, h, w, cin, xcs, acel, bw, bh, bnn, rh, rw))) return rc;
+  }
+  if ((rc = encode_2d(&p.mapB[0], wt, cout, K, K, p.b_cel, p.BN))) return rc;
+  p.out_mode = OUT_NHWC; p.out_f32 = y_f32; p.out = y; p.ldc = ycs; p.col_off = yoff; p.bias = bias;
+  return launch(p, (cudaStream_t)stream);
+}
+
+// Weight gradient, fp32 partials: part[split][cout_rows][kh*kw*cin] (caller reduces with
+// cvb_reduce_splits).  dy: NHWC bf16 [n][oh][ow][cout] (stride dycs); x: NHWC input.
+// Returns the number of splits used through *splits_out (<= max_splits).
+CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, int dycs, const void* x, int h, int w,
+                             int cin, int xcs, int kh, int kw, int stride, int pad, float* part, int max_splits,
+                             int* splits_out, void* stream) {
+  if (get_encoder()) return CVB_ECUDA;
+  const int acel = pick_cel(cout), bcel = pick_cel(cin);
+  if (!acel || !bcel || (stride != 1 && stride != 2)) { cvb_set_error("conv2d_wgrad: unsupported shape"); return CVB_EINVAL; }
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.mode = MODE_WGRAD;
+  p.a_major = 1; p.b_major = 1;
+  p.a_cel = acel; p.b_cel = bcel;
+  const int Ncols = kh * kw * cin;
+  int bn = pick_bn(Ncols);
+  // an N tile must be a whole number of B boxes
+  bn = (bn + bcel - 1) / bcel * bcel;
+  if (bn > 256) bn = 256 / bcel * bcel;
+  p.BN = bn;
+  p.M = cout; p.N = Ncols;
+  int bw, bh, bnn;
+  pick_kbox(n, oh, ow, bw, bh, bnn);
+  p.tw = bw; p.th = bh; p.tn = bnn;
+  p.ptiles_w = (ow + bw - 1) / bw;
+  p.ptiles_h = (oh + bh - 1) / bh;
+  const int ptiles_n = (n + bnn - 1) / bnn;
+  p.num_kb = p.ptiles_w * p.ptiles_h * ptiles_n;
+  p.m_tiles = (cout + BM - 1) / BM;
+  p.n_tiles = (Ncols + p.BN - 1) / p.BN;
+  if (!g_num_sms) g_num_sms = cvb_num_sms();
+  int tiles = p.m_tiles * p.n_tiles;
+  int splits = (g_num_sms + tiles - 1) / tiles;
+  if (splits > max_splits) splits = max_splits;
+  if (splits > p.num_kb) splits = p.num_kb;
+  if (splits < 1) splits = 1;
+  p.kb_per_split = (p.num_kb + splits - 1) / splits;
+  splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
+  p.splits = splits;
+  p.OH = oh; p.OW = ow; p.NIMG = n;
+  p.KH = kh; p.KW = kw; p.pad = pad; p.stride = stride;
+  p.cin = cin; p.ntaps = kh * kw;
+  p.tx_bytes = (BM / acel) * BK * acel * 2 + (p.BN / bcel) * BK * bcel * 2;
+  int rc;
+  if ((rc = encode_nhwc(&p.mapA[0], dy, n, oh, ow, cout, dycs, acel, bw, bh, bnn))) return rc;
+  if (stride == 1) {
+    if ((rc = encode_nhwc(&p.mapB[0], x, n, h, w, cin, xcs, bcel, bw, bh, bnn))) return rc;
+  } else {
+    for (int rh = 0; rh < 2; rh++)
+      for (int rw = 0; rw < 2; rw++)
+        if ((rc = encode_nhwc(&p.mapB[rh * 2 + rw], x, n, h, w, cin, xcs, bcel, bw, bh, bnn, rh, rw))) return rc;
+  }
+  p.out_mode = OUT_PARTIAL; p.out_f32 = 1; p.out = part; p.ldc = Ncols; p.col_off = 0; p.part_rows = cout;
+  *splits_out = splits;
+  return launch(p, (cudaStream_t)stream);
+}
+
+// Dense GEMM: C[m][n] (+bias[n]) = sum_k A(m,k) B(n,k)
+//   A: a_major 0 -> row-major [M][K] (lda), 1 -> row-major [K][M] (lda)
+//   B: b_major 0 -> row-major [N][K] (ldb), 1 -> row-major [K][N] (ldb)
+// C row-major [M][ldc] bf16 or fp32; split-K > 1 writes fp32 partials [split][M][ldc].
+CVB_API int cvb_gemm(const void* a, int a_major, int64_t lda, const void* b, int b_major, int64_t ldb, int M, int N,
+                     int K, void* c, int64_t ldc, int c_f32, const float* bias, int splits, void* stream) {
+  if (get_encoder()) return CVB_ECUDA;
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.mode = MODE_DENSE;
+  p.a_major = a_major; p.b_major = b_major;
+  p.a_cel = 64; p.b_cel = 64;
+  if (K % 8 || (a_major && M % 8) || (b_major && N % 8)) { cvb_set_error("gemm: unsupported shape"); return CVB_EINVAL; }
+  if (a_major == 0) p.a_cel = pick_cel(K) ? min(64, pick_cel(K)) : 8;
+  if (b_major == 0) p.b_cel = pick_cel(K) ? min(64, pick_cel(K)) : 8;
+  p.BN = pick_bn(N);
+  if (b_major == 1) { p.BN = (p.BN + 63) / 64 * 64; if (p.BN > 256) p.BN = 256; }
+  p.M = M; p.N = N;
+  p.m_tiles = (M + BM - 1) / BM;
+  p.n_tiles = (N + p.BN - 1) / p.BN;
+  p.num_kb = (K + BK - 1) / BK;
+  if (splits < 1) splits = 1;
+  if (splits > p.num_kb) splits = p.num_kb;
+  p.kb_per_split = (p.num_kb + splits - 1) / splits;
+  p.splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
+  int rc;
+  if (a_major == 0) { if ((rc = encode_2d(&p.mapA[0], a, M, K, lda, p.a_cel, BM))) return rc; }
+  else { if ((rc = encode_2d(&p.mapA[0], a, K, M, lda, p.a_cel, BK))) return rc; }
+  if (b_major == 0) { if ((rc = encode_2d(&p.mapB[0], b, N, K, ldb, p.b_cel, p.BN))) return rc; }
+  else { if ((rc = encode_2d(&p.mapB[0], b, K, N, ldb, p.b_cel, BK))) return rc; }
+  p.tx_bytes = (a_major == 0 ? (BK / p.a_cel) * BM * p.a_cel * 2 : (BM / p.a_cel) * BK * p.a_cel * 2) +
+               (b_major == 0 ? (BK / p.b_cel) * p.BN * p.b_cel * 2 : (p.BN / p.b_cel) * BK * p.b_cel * 2);
+  if (p.splits > 1) { p.out_mode = OUT_PARTIAL; p.out_f32 = 1; p.part_rows = M; }
+  else { p.out_mode = OUT_ROWS; p.out_f32 = c_f32; }
+  p.out = c; p.ldc = ldc; p.bias = p.splits > 1 ? nullptr : bias;
+  return launch(p, (cudaStream_t)stream);
+}
+
+CVB_API int cvb_gemm_splits_used(int K, int splits) {
+  int num_kb = (K + BK - 1) / BK;
+  if (splits < 1) splits = 1;
+  if (splits > num_kb) splits = num_kb;
+  int per = (num_kb + splits - 1) / splits;
+  return (num_kb + per - 1) / per;
+}

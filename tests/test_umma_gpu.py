@@ -1,0 +1,101 @@
+"""tcgen05 implicit-GEMM engine vs a torch fp32 reference of the same op (bf16-rounded
+operands, fp32 accumulation on both sides; tolerance 2e-3 relative to the output scale)."""
+import pytest
+import torch
+import torch.nn.functional as F
+
+from paper_2103_16898_b200 import kernels as K
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-3
+
+
+def _close(got, want, tol=TOL):
+    got, want = got.float(), want.float()
+    scale = want.abs().max().item() + 1e-6
+    err = (got - want).abs().max().item()
+    assert err <= tol * scale, f"max err {err:.3e} vs scale {scale:.3e}"
+
+
+def _ref_conv(x, w, stride, pad):
+    # x NHWC bf16, w [co,kh,kw,ci] -> NHWC fp32
+    y = F.conv2d(x.permute(0, 3, 1, 2).float(), w.permute(0, 3, 1, 2).float(), stride=stride, padding=pad)
+    return y.permute(0, 2, 3, 1)
+
+
+CONV_CASES = [
+    # n, h, w, cin, cout, k, stride, pad
+    (2, 32, 32, 8, 32, 3, 1, 1),
+    (2, 32, 32, 32, 32, 3, 1, 1),
+    (2, 16, 16, 32, 64, 3, 1, 1),
+    (3, 16, 16, 64, 64, 3, 1, 1),
+    (4, 8, 8, 64, 128, 3, 2, 1),
+    (4, 8, 8, 64, 128, 1, 2, 0),
+    (2, 14, 14, 96, 128, 1, 1, 0),
+    (3, 7, 7, 128, 32, 3, 1, 1),
+    (2, 28, 28, 16, 48, 3, 1, 1),
+    (1, 56, 56, 8, 64, 7, 2, 3),
+    (8, 4, 4, 256, 512, 3, 1, 1),
+    (2, 32, 32, 64, 256, 3, 1, 1),
+]
+
+
+@pytest.mark.parametrize("n,h,w,cin,cout,k,s,p", CONV_CASES)
+def test_conv_fwd(n, h, w, cin, cout, k, s, p):
+    g = torch.Generator(device="cuda").manual_seed(n * 1000 + h + cin + cout)
+    x = torch.randn(n, h, w, cin, device="cuda", generator=g).to(torch.bfloat16)
+    wt = (torch.randn(cout, k, k, cin, device="cuda", generator=g) / (k * k * cin) ** 0.5).to(torch.bfloat16)
+    bias = torch.randn(cout, device="cuda", generator=g)
+    y = K.conv2d_fwd(x, wt, s, p, bias=bias, out_f32=True)
+    _close(y, _ref_conv(x, wt, s, p) + bias)
+    yb = K.conv2d_fwd(x, wt, s, p)   # bf16 output path
+    _close(yb, _ref_conv(x, wt, s, p), tol=1e-2)
+
+
+def test_conv_fwd_channel_slices():
+    # DenseNet-style: read channels [0,cin) of a wider buffer, write at an offset of another
+    x_full = torch.randn(2, 8, 8, 160, device="cuda").to(torch.bfloat16)
+    wt = (torch.randn(32, 3, 3, 96, device="cuda") * 0.1).to(torch.bfloat16)
+    out = torch.zeros(2, 8, 8, 256, device="cuda", dtype=torch.bfloat16)
+    K.conv2d_fwd(x_full, wt, 1, 1, out=out, cin=96, out_coff=64)
+    _close(out[..., 64:96], _ref_conv(x_full[..., :96].contiguous(), wt, 1, 1), tol=1e-2)
+    assert out[..., :64].abs().max().item() == 0 and out[..., 96:].abs().max().item() == 0
+
+
+@pytest.mark.parametrize("n,h,w,cin,cout,k,s,p", CONV_CASES)
+def test_conv_wgrad(n, h, w, cin, cout, k, s, p):
+    g = torch.Generator(device="cuda").manual_seed(7 + n + h + cin + cout)
+    x = torch.randn(n, h, w, cin, device="cuda", generator=g).to(torch.bfloat16)
+    oh, ow = K.conv_out_hw(h, w, k, s, p)
+    dy = torch.randn(n, oh, ow, cout, device="cuda", generator=g).to(torch.bfloat16)
+    part, used = K.conv2d_wgrad_partials(dy, x, k, k, s, p)
+    dw = part[:used].sum(0).view(cout, k, k, cin)
+    xr = x.permute(0, 3, 1, 2).float().requires_grad_(True)
+    wr = torch.zeros(cout, cin, k, k, device="cuda", requires_grad=True)
+    yr = F.conv2d(xr, wr, stride=s, padding=p)
+    yr.backward(dy.permute(0, 3, 1, 2).float())
+    _close(dw, wr.grad.permute(0, 2, 3, 1))
+
+
+@pytest.mark.parametrize("M,N,Kd,am,bm,splits", [
+    (512, 256, 4096, 0, 0, 1), (512, 10, 256, 0, 0, 1), (512, 4096, 256, 0, 1, 1),
+    (256, 4096, 512, 1, 1, 4), (10, 256, 512, 1, 1, 2), (300, 200, 136, 0, 0, 1),
+])
+def test_dense(M, N, Kd, am, bm, splits):
+    g = torch.Generator(device="cuda").manual_seed(M + N + Kd)
+    A = torch.randn(M, Kd, device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randn(N, Kd, device="cuda", generator=g).to(torch.bfloat16)
+    a = A if am == 0 else A.t().contiguous()
+    if bm == 1 and N % 8:
+        pytest.skip("MN-major operand needs N % 8 == 0")
+    b = B if bm == 0 else B.t().contiguous()
+    if am == 1 and M % 8:
+        pytest.skip("MN-major operand needs M % 8 == 0")
+    bias = torch.randn(N, device="cuda", generator=g)
+    out = K.gemm(a, b, M, N, Kd, am, bm, out_f32=True, bias=None if splits > 1 else bias, splits=splits)
+    want = A.float() @ B.float().t()
+    if out.dim() == 3:
+        out = out.sum(0)
+    else:
+        want = want + bias
+    _close(out, want)
