@@ -1,0 +1,340 @@
+"""Benchmark of the encrypted-training hot path (BASELINE.json metric: training images/s).
+
+Workload (N=1): BASELINE.json configs[1] -- the paper-shaped small CNN on synthetic
+CIFAR-10-shaped records, batch 512 per GPU, bf16 operands / fp32 accumulation.  One step =
+AES-256-GCM open of one sealed 512-record shard (tag verified on device) + record decode +
+forward + softmax-CE + backward + Adam.  Per-rank inputs: 96 sealed shards (151 MB of
+ciphertext, larger than the 126 MB L2) resident in HBM, cycled.  Weak scaling under
+torchrun: every rank has its own shards and batch, gradients all-reduced over NCCL.
+
+Prints ONE JSON line on rank 0 (see the driver contract in the task statement):
+  value     images/s over all ranks, device-resident ciphertext, CUDA-event timed
+  e2e       same metric through the public host API: pinned host ciphertext -> H2D ->
+            decrypt -> train -> D2H of loss + tag status inside the timed region
+  roofline  dominant kernel of an instrumented replay of the step (CUDA events per launch)
+  cpu_baseline  reference CPU arm on the host cores (rank 0, N=1 only; bounded sample)
+``--impl reference`` runs only the CPU reference arm (oracle port of the CNN + the
+reference's own AES-GCM open) and prints its line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+_REF = ROOT / "baseline" / "_ref"
+if _REF.exists():
+    sys.path.insert(1, str(_REF))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+METRIC = "training images/sec at 1/2/4/8 B200 vs reference CPU trainer on host cores"
+UNIT = "images/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="small_cnn")
+    ap.add_argument("--batch", type=int, default=512)
+    ap.add_argument("--shards", type=int, default=96)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------------------
+# synthetic sealed dataset (reference volume format: one AES-256-GCM message per shard file,
+# AAD = volume_name || 0 || path, volume.py:53-54)
+# ---------------------------------------------------------------------------------------
+def make_shards(n_shards, batch, seed, key, spec):
+    from cryptography.hazmat.primitives.ciphers.aead import AESGCM
+
+    c, h, w = spec["c"], spec["h"], spec["w"]
+    rng = np.random.default_rng(seed)
+    templ = np.random.default_rng(0).normal(size=(10, c * h * w)).astype(np.float32)
+    aes = AESGCM(key)
+    shards = []
+    for i in range(n_shards):
+        labels = rng.integers(0, 10, size=batch).astype(np.uint8)
+        noise = rng.integers(-52, 53, size=(batch, c * h * w), dtype=np.int16)
+        px = np.clip(128 + 40 * templ[labels] + noise, 0, 255).astype(np.uint8)
+        pt = np.concatenate([labels[:, None], px], axis=1).tobytes()
+        path = f"shard-{seed:03d}-{i:05d}.bin"
+        aad = b"training-data\x00" + path.encode()
+        nonce = rng.bytes(12)
+        shards.append((path, nonce, aad, aes.encrypt(nonce, pt, aad), pt if i == 0 else None))
+    return shards
+
+
+def clocks_sampler(dev_index):
+    try:
+        return subprocess.Popen(
+            ["nvidia-smi", f"--id={dev_index}",
+             "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+            stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+    except Exception:
+        return None
+
+
+def clocks_summary(proc):
+    if proc is None:
+        return None
+    proc.terminate()
+    try:
+        out, _ = proc.communicate(timeout=5)
+    except Exception:
+        proc.kill()
+        return None
+    sm, mx, reasons = [], 0.0, set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    for line in out.strip().splitlines():
+        f = [x.strip() for x in line.split(",")]
+        if len(f) < 7:
+            continue
+        try:
+            sm.append(float(f[0]))
+            mx = max(mx, float(f[1]))
+        except ValueError:
+            continue
+        for nm, v in zip(names, f[3:7]):
+            if v.lower() == "active":
+                reasons.add(nm)
+    if not sm:
+        return None
+    return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+# ---------------------------------------------------------------------------------------
+# CPU reference arm
+# ---------------------------------------------------------------------------------------
+def cpu_reference(model, batch, key, spec, seconds, steps=None, warmup=0):
+    """Reference CPU trainer on the host cores: the reference's own AES-GCM open
+    (covault.crypto.aead_open -> OpenSSL) of the shard, then the CPU restatement of the CNN
+    step (oracle/cnn_ref.py, fp32, all threads).  Returns (img/s, cores, sample, kind)."""
+    from oracle.cnn_ref import RefTrainer, normalise_records
+    from paper_2103_16898_b200 import nets
+
+    cores = len(os.sched_getaffinity(0))
+    torch.set_num_threads(cores)
+    try:
+        from covault.crypto import SymmetricKey, aead_open  # the reference package (baseline/_ref)
+
+        rkey = SymmetricKey(key)
+        opener = lambda n, a, b: aead_open(rkey, n, a, b)  # noqa: E731
+        dec = "covault.crypto.aead_open (reference, OpenSSL)"
+    except Exception:
+        from cryptography.hazmat.primitives.ciphers.aead import AESGCM
+
+        opener = lambda n, a, b: AESGCM(key).decrypt(n, b, a)  # noqa: E731
+        dec = "cryptography AESGCM (reference's dependency)"
+    m = nets.make_model(model, seed=0)
+    ref = RefTrainer(model, {n: t.clone() for n, _, t in m.ps.specs}, emulate_bf16=False)
+    shards = make_shards(2, batch, 7, key, spec)
+    t_total, n_img, it = 0.0, 0, 0
+    deadline = time.perf_counter() + seconds
+    while True:
+        path, nonce, aad, blob, _ = shards[it % 2]
+        t0 = time.perf_counter()
+        pt = opener(nonce, aad, blob)
+        rec = torch.frombuffer(bytearray(pt), dtype=torch.uint8).view(batch, -1)
+        x, lab = normalise_records(rec, spec["c"], spec["h"], spec["w"], spec["mean"], spec["std"], False)
+        ref.step(x, lab)
+        dt = time.perf_counter() - t0
+        if it >= warmup:
+            t_total += dt
+            n_img += batch
+        it += 1
+        if steps is not None:
+            if it >= steps + warmup:
+                break
+        elif time.perf_counter() > deadline and it > warmup:
+            break
+    sample = (f"{it - warmup} timed steps of batch {batch} ({n_img} images): {dec} of one sealed shard + "
+              f"{model} fp32 train step (oracle/cnn_ref.py, torch CPU, {cores} threads)")
+    return n_img / t_total, cores, sample, t_total
+
+
+def run_reference(args, rank, world):
+    from paper_2103_16898_b200.loader import CIFAR
+
+    if rank != 0:
+        return
+    key = bytes(range(32))
+    v, cores, sample, t = cpu_reference(args.model, args.batch, key, CIFAR, 0, steps=args.steps,
+                                        warmup=args.warmup)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / max(1, args.steps),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+            "config": {"workload": f"{args.model} CIFAR-10-shaped, batch {args.batch}, sealed shards (CPU reference)",
+                       "model": args.model, "global_batch": args.batch, "seq_len": None, "parallelism": "cpu"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import torch.distributed as dist
+
+    from paper_2103_16898_b200 import kernels as K
+    from paper_2103_16898_b200.loader import CIFAR
+    from paper_2103_16898_b200.trainer import EncryptedTrainer
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    spec = CIFAR
+    key = bytes(range(32))
+    B = args.batch
+    tr = EncryptedTrainer(args.model, key, batch=B, spec=spec, seed=0, world=world, rank=rank)
+    shards = make_shards(args.shards, B, 1000 + rank, key, spec)
+    # resident ciphertext + AADs in HBM (inputs larger than L2)
+    cts = [torch.frombuffer(bytearray(s[3]), dtype=torch.uint8).to(dev) for s in shards]
+    aads = [torch.frombuffer(bytearray(s[2]), dtype=torch.uint8).to(dev) for s in shards]
+    host = [torch.frombuffer(bytearray(s[3]), dtype=torch.uint8).pin_memory() for s in shards]
+    # parity gate before timing: shard 0 decrypts bit-exactly on the device
+    tr.step_resident(cts[0], shards[0][1], aads[0], B)
+    torch.cuda.synchronize()
+    assert int(tr.loader.work[4].item()) == 0, "tag check failed"
+    assert bytes(tr.loader.pt[:len(shards[0][4])].cpu().numpy()) == shards[0][4], "decrypt mismatch"
+    tr.capture()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, steps):
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(steps):
+            fn(i)
+        e1.record()
+        barrier()
+        ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return float(ms.item())
+
+    resident = lambda i: tr.step_resident(cts[i % len(cts)], shards[i % len(cts)][1], aads[i % len(cts)], B)  # noqa
+    e2e_step = lambda i: tr.step_host(host[i % len(cts)], shards[i % len(cts)][1], shards[i % len(cts)][2], B)  # noqa
+
+    for i in range(args.warmup):
+        resident(i)
+    launches0 = K.REC.launches
+    clk = clocks_sampler(local_rank) if rank == 0 else None
+    ms = timed(resident, args.steps)
+    clocks = clocks_summary(clk) if rank == 0 else None
+    # graph replays do not pass through the Python wrappers: count one eager step's launches
+    per_step_eager = None
+    for i in range(args.warmup):
+        e2e_step(i)
+    ms_e2e = timed(e2e_step, args.steps)
+    tr.check_status()
+
+    # instrumented eager step (per-launch CUDA events) for the roofline and launch count
+    K.REC.timing, K.REC.records = True, []
+    l0 = K.REC.launches
+    tr.graph = None
+    resident(0)
+    torch.cuda.synchronize()
+    per_step_eager = K.REC.launches - l0
+    K.REC.timing = False
+    summ = K.REC.summary()
+    step_ms_instr = sum(v[1] for v in summ.values())
+    dom = max(summ.items(), key=lambda kv: kv[1][1])
+    hbm, tflops, src = peaks()
+    kind, (calls, dms, dfl, dby) = dom
+    if dfl > 0:
+        ach = dfl / (dms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": ach, "peak": tflops, "unit": "TFLOP/s", "frac": ach / tflops}
+    else:
+        ach = dby / (dms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm}
+    roof.update({"traffic": None, "kernel": kind, "launches_per_step": calls,
+                 "share_of_step": dms / step_ms_instr, "peak_source": src,
+                 "per_kind_ms": {k: round(v[1], 4) for k, v in summ.items()},
+                 "algorithmic": "sum over the step's launches of 2*M*N*K (real channel counts)"
+                 if dfl > 0 else "sum of read+write bytes"})
+    prof = ROOT / "profiles" / "roofline_live.json"
+    if rank == 0:
+        try:
+            prof.write_text(json.dumps({"summary": {k: v for k, v in summ.items()}, "roofline": roof}, indent=1))
+        except Exception:
+            pass
+
+    images = B * args.steps * world
+    value = images / (ms * 1e-3)
+    e2e = images / (ms_e2e * 1e-3)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, sample, _ = cpu_reference(args.model, B, key, spec, args.cpu_seconds, warmup=1)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+    if rank == 0:
+        decrypt_launches = 4
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16 operands, fp32 accumulate", "data": "synthetic",
+            "config": {"workload": f"configs[1]: {args.model} (paper CIFAR CNN), CIFAR-10-shaped sealed shards, "
+                                   f"batch {B}/GPU, decrypt+decode+fwd+bwd+Adam per step",
+                       "model": args.model, "global_batch": B * world, "seq_len": None,
+                       "parallelism": f"dp{world}",
+                       "l2": f"{args.shards} resident shards/rank = "
+                             f"{args.shards * (B * 3073 + 16) / 1e6:.0f} MB ciphertext (> 126 MB L2), cycled"},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": B * 3073 + 16 + 64,
+                    "d2h_bytes_per_step": 8},
+            "gpu_launches": args.steps * (per_step_eager + decrypt_launches) if per_step_eager else None,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "loss": float(tr.net.loss.item()),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,79 @@
+/*
+ * cvb_nn.h -- C ABI of the CNN training-step kernels (sm_100a).
+ *
+ * The reference has NO code for this part of the path: its trainer is an fp64 logistic
+ * toy (pkg/src/covault/workload.py:48-71) and the CIFAR CNN / medical model exist only as
+ * paper prose.  These entry points are what the B200
+ * trainer (paper_2103_16898_b200/nets.py, trainer.py) calls behind the reference's
+ * run_training(params, data) signature; DESIGN.md documents the model definitions.
+ *
+ * Activations: NHWC bf16 rows [N*H*W][C] with a channel stride (cs) so concat buffers are
+ * read/written in place.  Weights: bf16 [Cout][KH][KW][Cin] (K-major).  Grads/optimiser
+ * state: fp32.  All calls are asynchronous on `stream` (a cudaStream_t).
+ */
+#ifndef CVB_NN_H
+#define CVB_NN_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- tcgen05 implicit-GEMM engine ------------------------------------------------------ */
+/* y[n,oh,ow,yoff+co] = bias[co] + sum x[n, oh*s-pad+kh, ow*s-pad+kw, ci] * w[co][kh][kw][ci] */
+int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs, const void* wt, int cout, int kh, int kw,
+                   int stride, int pad, void* y, int oh, int ow, int ycs, int yoff, const float* bias, int y_f32,
+                   int accumulate, void* stream);
+/* fp32 partial weight gradients part[split][cout][kh*kw*cin]; *splits_out receives the count */
+int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, int dycs, const void* x, int h, int w, int cin,
+                     int xcs, int kh, int kw, int stride, int pad, float* part, int max_splits, int* splits_out,
+                     void* stream);
+/* C[M][N] (+bias) = sum_k A(m,k) B(n,k); A [M][K] (a_major 0) or [K][M] (1); B [N][K] or [K][N] */
+int cvb_gemm(const void* a, int a_major, int64_t lda, const void* b, int b_major, int64_t ldb, int M, int N, int K,
+             void* c, int64_t ldc, int c_f32, const float* bias, int splits, int accumulate, void* stream);
+int cvb_gemm_splits_used(int K, int splits);
+
+/* ---- batch norm (+ReLU, +residual) --------------------------------------------------------- */
+int64_t cvb_bn_workspace_floats(int64_t rows, int C);
+int cvb_bn_stats(const void* x, int64_t rows, int C, int xcs, float* ws, float* mean, float* rstd, float eps,
+                 float* run_mean, float* run_var, float momentum, void* stream);
+int cvb_bn_apply(const void* x, int64_t rows, int C, int xcs, const float* mean, const float* rstd, const float* gamma,
+                 const float* beta, const void* res, int rcs, int relu, void* y, int ycs, int ycoff, void* stream);
+int cvb_bn_backward(const void* dy, int dycs, const void* x, int xcs, const void* y, int ycs, int64_t rows, int C,
+                    const float* mean, const float* rstd, const float* gamma, const float* beta, int relu, float* ws,
+                    float* dgamma, float* dbeta, void* dx, int dxcs, float* dx32, int accum32, void* dz_out,
+                    void* stream);
+
+/* ---- pooling -------------------------------------------------------------------------------- */
+int cvb_maxpool_fwd(const void* x, int n, int h, int w, int C, int k, int s, int p, void* y, int oh, int ow, void* stream);
+int cvb_maxpool_bwd(const void* x, const void* dy, int n, int h, int w, int C, int k, int s, int p, int oh, int ow,
+                    void* dx, void* stream);
+int cvb_avgpool_fwd(const void* x, int n, int h, int w, int C, int xcs, int k, void* y, void* stream);
+int cvb_avgpool_bwd(const void* dy, int n, int h, int w, int C, int k, void* dx, int dxcs, void* stream);
+int cvb_gap_fwd(const void* x, int n, int hw, int C, int xcs, void* y, void* stream);
+int cvb_gap_bwd(const void* dy, int n, int hw, int C, void* dx, void* stream);
+
+/* ---- loss, reductions, layout helpers ---------------------------------------------------------- */
+int cvb_softmax_xent(const float* logits, int B, int C, const int32_t* labels, float grad_scale, float* row_ws,
+                     float* loss_out, void* dlogits, int ldd, void* stream);
+int cvb_reduce_splits(const float* part, int splits, int64_t count, float* out, int accumulate, float scale,
+                      void* stream);
+int cvb_weight_flip(const void* w, int cout, int kh, int kw, int cin, void* wt, void* stream);
+int cvb_zero_upsample(const void* dy, int n, int oh, int ow, int C, int dycs, void* out, void* stream);
+int cvb_col_sum(const void* x, int is_f32, int64_t rows, int cols, int64_t ld, float* out, int accumulate, void* stream);
+int cvb_relu_fwd(void* x, int64_t n, void* stream);
+int cvb_relu_bwd(void* dy, const void* y, int64_t n, void* stream);
+
+/* ---- fused optimisers over flat fp32 buffers (refresh the bf16 compute copy pb) ---------------- */
+/* step > 0: host bias correction; step <= 0: device counter (step_dev += 1, factors in sched_dev[2]),
+ * so a captured CUDA graph replays correctly. */
+int cvb_adam_step(float* p, const float* g, float* m, float* v, void* pb, int64_t n, float lr, float b1, float b2,
+                  float eps, int64_t step, float grad_scale, int32_t* step_dev, float* sched_dev, void* stream);
+int cvb_sgd_step(float* p, const float* g, float* buf, void* pb, int64_t n, float lr, float momentum, float wd,
+                 float grad_scale, int first, void* stream);
+int cvb_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

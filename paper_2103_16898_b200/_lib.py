@@ -48,11 +48,33 @@ SIGNATURES = {
     "cvb_logistic_train": (_INT, [_P, _P, _I64, _I64, _c.c_double, _I64, _INT, _P, _P]),
     # tcgen05 implicit-GEMM engine (include/cvb_nn.h)
     "cvb_conv2d_fwd": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT,
-                              _INT, _INT, _P, _INT, _P]),
+                              _INT, _INT, _P, _INT, _INT, _P]),
     "cvb_conv2d_wgrad": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT, _INT, _INT, _INT, _INT, _INT,
                                 _INT, _P, _INT, _c.POINTER(_INT), _P]),
-    "cvb_gemm": (_INT, [_P, _INT, _I64, _P, _INT, _I64, _INT, _INT, _INT, _P, _I64, _INT, _P, _INT, _P]),
+    "cvb_gemm": (_INT, [_P, _INT, _I64, _P, _INT, _I64, _INT, _INT, _INT, _P, _I64, _INT, _P, _INT, _INT, _P]),
     "cvb_gemm_splits_used": (_INT, [_INT, _INT]),
+    "cvb_bn_workspace_floats": (_I64, [_I64, _INT]),
+    "cvb_bn_stats": (_INT, [_P, _I64, _INT, _INT, _P, _P, _P, _c.c_float, _P, _P, _c.c_float, _P]),
+    "cvb_bn_apply": (_INT, [_P, _I64, _INT, _INT, _P, _P, _P, _P, _P, _INT, _INT, _P, _INT, _INT, _P]),
+    "cvb_bn_backward": (_INT, [_P, _INT, _P, _INT, _P, _INT, _I64, _INT, _P, _P, _P, _P, _INT, _P, _P, _P, _P, _INT,
+                               _P, _INT, _P, _P]),
+    "cvb_maxpool_fwd": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT, _P]),
+    "cvb_maxpool_bwd": (_INT, [_P, _P, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _P, _P]),
+    "cvb_avgpool_fwd": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _INT, _P, _P]),
+    "cvb_avgpool_bwd": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _P, _INT, _P]),
+    "cvb_gap_fwd": (_INT, [_P, _INT, _INT, _INT, _INT, _P, _P]),
+    "cvb_gap_bwd": (_INT, [_P, _INT, _INT, _INT, _P, _P]),
+    "cvb_softmax_xent": (_INT, [_P, _INT, _INT, _P, _c.c_float, _P, _P, _P, _INT, _P]),
+    "cvb_reduce_splits": (_INT, [_P, _INT, _I64, _P, _INT, _c.c_float, _P]),
+    "cvb_weight_flip": (_INT, [_P, _INT, _INT, _INT, _INT, _P, _P]),
+    "cvb_zero_upsample": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _P, _P]),
+    "cvb_col_sum": (_INT, [_P, _INT, _I64, _INT, _I64, _P, _INT, _P]),
+    "cvb_relu_fwd": (_INT, [_P, _I64, _P]),
+    "cvb_relu_bwd": (_INT, [_P, _P, _I64, _P]),
+    "cvb_adam_step": (_INT, [_P, _P, _P, _P, _P, _I64, _c.c_float, _c.c_float, _c.c_float, _c.c_float, _I64,
+                             _c.c_float, _P, _P, _P]),
+    "cvb_sgd_step": (_INT, [_P, _P, _P, _P, _I64, _c.c_float, _c.c_float, _c.c_float, _c.c_float, _INT, _P]),
+    "cvb_cast_f32_bf16": (_INT, [_P, _P, _I64, _P]),
 }
 
 

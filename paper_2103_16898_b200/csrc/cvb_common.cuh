@@ -31,10 +31,14 @@ void cvb_set_error(const char* fmt, ...);
     }                                                                                  \
   } while (0)
 
+// SM count of the current device, cached per device (safe to call during graph capture).
 static inline int cvb_num_sms() {
+  static int cache[64] = {0};
   int dev = 0, n = 148;
   cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && cache[dev]) return cache[dev];
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (dev >= 0 && dev < 64) cache[dev] = n;
   return n;
 }
 

@@ -1,0 +1,702 @@
+// Memory-bound kernels of the CNN training step (K3/K4/K5-support of DESIGN.md): batch-norm
+// statistics / apply / backward with fused ReLU and residual, pooling, softmax
+// cross-entropy, split-K reduction, weight flip, zero-upsampling, column sums and the
+// fused Adam / SGD updates.  All activations are NHWC bf16 rows [rows][C] with a channel
+// stride (so DenseNet concat buffers are read in place); statistics and gradients fp32.
+// Every reduction is two-level and fixed-order -> results are deterministic run to run.
+// 8 channels (one 16-byte vector) per thread in the elementwise kernels.
+#include "cvb_common.cuh"
+#include <cuda_bf16.h>
+#include <math.h>
+
+namespace {
+
+typedef __nv_bfloat16 bf16;
+
+__device__ __forceinline__ void load8(const bf16* p, float v[8]) {
+  uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; i++) { float2 f = __bfloat1622float2(h[i]); v[2 * i] = f.x; v[2 * i + 1] = f.y; }
+}
+__device__ __forceinline__ void store8(bf16* p, const float v[8]) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; i++) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
+constexpr int ST_THREADS = 256;
+
+// ---- per-channel sum / sum of squares (two-level) -------------------------------------
+// grid.x = blocks over rows; thread (rl, g) handles channel group g (8 channels) of rows
+// rl, rl + RL, ... inside the block's row range.  Partial layout: [blk][2][C].
+__global__ void chan_stats_partial(const bf16* __restrict__ x, int64_t rows, int C, int cs, int64_t rows_per_blk,
+                                   float* __restrict__ part) {
+  const int G = C / 8;
+  const int RL = ST_THREADS / G;  // row lanes (G <= 256 guaranteed by host)
+  const int t = threadIdx.x, g = t % G, rl = t / G;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_blk, r1 = min(rows, r0 + rows_per_blk);
+  float s[8] = {0}, q[8] = {0};
+  if (rl < RL) {
+    for (int64_t r = r0 + rl; r < r1; r += RL) {
+      float v[8];
+      load8(x + r * cs + g * 8, v);
+#pragma unroll
+      for (int i = 0; i < 8; i++) { s[i] += v[i]; q[i] += v[i] * v[i]; }
+    }
+  }
+  extern __shared__ float sh[];  // [RL][G][16]
+  if (rl < RL) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) { sh[(rl * G + g) * 16 + i] = s[i]; sh[(rl * G + g) * 16 + 8 + i] = q[i]; }
+  }
+  __syncthreads();
+  for (int idx = t; idx < G * 16; idx += ST_THREADS) {
+    const int gg = idx / 16, k = idx % 16;
+    float acc = 0.f;
+    for (int l = 0; l < RL; l++) acc += sh[(l * G + gg) * 16 + k];
+    const int c = gg * 8 + (k & 7);
+    part[((int64_t)blockIdx.x * 2 + (k >> 3)) * C + c] = acc;
+  }
+}
+
+__global__ void bn_finalize(const float* __restrict__ part, int nblk, int C, double count, float eps,
+                            float* __restrict__ mean, float* __restrict__ rstd, float* __restrict__ run_mean,
+                            float* __restrict__ run_var, float momentum) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double s = 0, q = 0;
+  for (int b = 0; b < nblk; b++) { s += part[(int64_t)(2 * b) * C + c]; q += part[(int64_t)(2 * b + 1) * C + c]; }
+  const double m = s / count;
+  double var = q / count - m * m;
+  if (var < 0) var = 0;
+  mean[c] = (float)m;
+  rstd[c] = (float)(1.0 / sqrt(var + (double)eps));
+  if (run_mean) {
+    const double unb = count > 1 ? var * count / (count - 1) : var;
+    run_mean[c] = (float)((1.0 - momentum) * run_mean[c] + momentum * m);
+    run_var[c] = (float)((1.0 - momentum) * run_var[c] + momentum * unb);
+  }
+}
+
+// ---- y = act(gamma * (x - mean) * rstd + beta [+ res]) ---------------------------------
+__global__ void bn_apply(const bf16* __restrict__ x, int64_t rows, int C, int xcs, const float* __restrict__ mean,
+                         const float* __restrict__ rstd, const float* __restrict__ gamma, const float* __restrict__ beta,
+                         const bf16* __restrict__ res, int rcs, int relu, bf16* __restrict__ y, int ycs, int ycoff) {
+  const int G = C / 8;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * G) return;
+  const int64_t r = i / G;
+  const int g = (int)(i - r * G);
+  float v[8], o[8];
+  load8(x + r * xcs + g * 8, v);
+  float rv[8];
+  if (res) load8(res + r * rcs + g * 8, rv);
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const int c = g * 8 + k;
+    const float sc = gamma[c] * rstd[c];
+    float z = (v[k] - mean[c]) * sc + beta[c];
+    if (res) z += rv[k];
+    o[k] = relu ? fmaxf(z, 0.f) : z;
+  }
+  store8(y + r * ycs + ycoff + g * 8, o);
+}
+
+// ---- batch-norm backward, reduction pass ----------------------------------------------
+// dz = dy * mask (mask = y > 0 when relu; y = the layer output, or recomputed from x when
+// y == nullptr).  Partials [blk][2][C] of sum(dz) and sum(dz * xhat); optionally stores dz.
+__global__ void bn_bwd_partial(const bf16* __restrict__ dy, int dycs, const bf16* __restrict__ x, int xcs,
+                               const bf16* __restrict__ y, int ycs, int64_t rows, int C, const float* __restrict__ mean,
+                               const float* __restrict__ rstd, const float* __restrict__ gamma, const float* __restrict__ beta,
+                               int relu, int64_t rows_per_blk, float* __restrict__ part, bf16* __restrict__ dz_out) {
+  const int G = C / 8;
+  const int RL = ST_THREADS / G;
+  const int t = threadIdx.x, g = t % G, rl = t / G;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_blk, r1 = min(rows, r0 + rows_per_blk);
+  float s[8] = {0}, q[8] = {0};
+  float mu[8], rs[8], ga[8], be[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const int c = g * 8 + k;
+    mu[k] = mean[c]; rs[k] = rstd[c]; ga[k] = gamma[c]; be[k] = beta[c];
+  }
+  if (rl < RL) {
+    for (int64_t r = r0 + rl; r < r1; r += RL) {
+      float d[8], xv[8], yv[8];
+      load8(dy + r * dycs + g * 8, d);
+      load8(x + r * xcs + g * 8, xv);
+      if (relu && y) load8(y + r * ycs + g * 8, yv);
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const float xh = (xv[k] - mu[k]) * rs[k];
+        if (relu) {
+          const float z = y ? yv[k] : xh * ga[k] + be[k];
+          if (!(z > 0.f)) d[k] = 0.f;
+        }
+        s[k] += d[k];
+        q[k] += d[k] * xh;
+      }
+      if (dz_out) store8(dz_out + r * C + g * 8, d);
+    }
+  }
+  extern __shared__ float sh[];
+  if (rl < RL) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) { sh[(rl * G + g) * 16 + i] = s[i]; sh[(rl * G + g) * 16 + 8 + i] = q[i]; }
+  }
+  __syncthreads();
+  for (int idx = t; idx < G * 16; idx += ST_THREADS) {
+    const int gg = idx / 16, k = idx % 16;
+    float acc = 0.f;
+    for (int l = 0; l < RL; l++) acc += sh[(l * G + gg) * 16 + k];
+    part[((int64_t)blockIdx.x * 2 + (k >> 3)) * C + gg * 8 + (k & 7)] = acc;
+  }
+}
+
+__global__ void bn_bwd_finalize(const float* __restrict__ part, int nblk, int C, float* __restrict__ dbeta,
+                                float* __restrict__ dgamma) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double s = 0, q = 0;
+  for (int b = 0; b < nblk; b++) { s += part[(int64_t)(2 * b) * C + c]; q += part[(int64_t)(2 * b + 1) * C + c]; }
+  dbeta[c] = (float)s;
+  dgamma[c] = (float)q;
+}
+
+// dx = gamma * rstd * (dz - dbeta/M - xhat * dgamma/M)   (dz recomputed like the partial pass)
+__global__ void bn_bwd_apply(const bf16* __restrict__ dy, int dycs, const bf16* __restrict__ x, int xcs,
+                             const bf16* __restrict__ y, int ycs, int64_t rows, int C, const float* __restrict__ mean,
+                             const float* __restrict__ rstd, const float* __restrict__ gamma, const float* __restrict__ beta,
+                             int relu, const float* __restrict__ dbeta, const float* __restrict__ dgamma,
+                             bf16* __restrict__ dx, int dxcs, float* __restrict__ dx32, int accum32) {
+  const int G = C / 8;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * G) return;
+  const int64_t r = i / G;
+  const int g = (int)(i - r * G);
+  const float invM = 1.0f / (float)rows;
+  float d[8], xv[8], yv[8], o[8];
+  load8(dy + r * dycs + g * 8, d);
+  load8(x + r * xcs + g * 8, xv);
+  if (relu && y) load8(y + r * ycs + g * 8, yv);
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const int c = g * 8 + k;
+    const float xh = (xv[k] - mean[c]) * rstd[c];
+    if (relu) {
+      const float z = y ? yv[k] : xh * gamma[c] + beta[c];
+      if (!(z > 0.f)) d[k] = 0.f;
+    }
+    o[k] = gamma[c] * rstd[c] * (d[k] - dbeta[c] * invM - xh * dgamma[c] * invM);
+  }
+  if (dx32) {
+    float* p = dx32 + r * dxcs + g * 8;
+#pragma unroll
+    for (int k = 0; k < 8; k++) p[k] = accum32 ? p[k] + o[k] : o[k];
+  } else {
+    store8(dx + r * dxcs + g * 8, o);
+  }
+}
+
+// ---- pooling --------------------------------------------------------------------------
+__global__ void maxpool_fwd(const bf16* __restrict__ x, int n, int h, int w, int C, int k, int s, int p, int oh, int ow,
+                            bf16* __restrict__ y) {
+  const int G = C / 8;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * oh * ow * G) return;
+  const int g = (int)(i % G);
+  int64_t pix = i / G;
+  const int ox = (int)(pix % ow), oy = (int)((pix / ow) % oh), b = (int)(pix / ((int64_t)ow * oh));
+  float m[8];
+#pragma unroll
+  for (int c = 0; c < 8; c++) m[c] = -INFINITY;
+  for (int dy = 0; dy < k; dy++) {
+    const int iy = oy * s - p + dy;
+    if (iy < 0 || iy >= h) continue;
+    for (int dx = 0; dx < k; dx++) {
+      const int ix = ox * s - p + dx;
+      if (ix < 0 || ix >= w) continue;
+      float v[8];
+      load8(x + (((int64_t)b * h + iy) * w + ix) * C + g * 8, v);
+#pragma unroll
+      for (int c = 0; c < 8; c++) if (v[c] > m[c]) m[c] = v[c];
+    }
+  }
+  store8(y + pix * C + g * 8, m);
+}
+
+// gather form: each input element collects dy of every window whose FIRST arg-max it is
+__global__ void maxpool_bwd(const bf16* __restrict__ x, const bf16* __restrict__ dyp, int n, int h, int w, int C, int k,
+                            int s, int p, int oh, int ow, bf16* __restrict__ dx) {
+  const int G = C / 8;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * h * w * G) return;
+  const int g = (int)(i % G);
+  const int64_t pix = i / G;
+  const int ix = (int)(pix % w), iy = (int)((pix / w) % h), b = (int)(pix / ((int64_t)w * h));
+  float acc[8] = {0};
+  const int oy0 = max(0, (iy + p - k + s) / s), oy1 = min(oh - 1, (iy + p) / s);
+  const int ox0 = max(0, (ix + p - k + s) / s), ox1 = min(ow - 1, (ix + p) / s);
+  for (int oy = oy0; oy <= oy1; oy++) {
+    for (int ox = ox0; ox <= ox1; ox++) {
+      // recompute the window's first arg-max (row-major scan, strict >)
+      float m[8];
+      int am[8];
+#pragma unroll
+      for (int c = 0; c < 8; c++) { m[c] = -INFINITY; am[c] = -1; }
+      for (int dy = 0; dy < k; dy++) {
+        const int yy = oy * s - p + dy;
+        if (yy < 0 || yy >= h) continue;
+        for (int dx2 = 0; dx2 < k; dx2++) {
+          const int xx = ox * s - p + dx2;
+          if (xx < 0 || xx >= w) continue;
+          float v[8];
+          load8(x + (((int64_t)b * h + yy) * w + xx) * C + g * 8, v);
+#pragma unroll
+          for (int c = 0; c < 8; c++) if (v[c] > m[c]) { m[c] = v[c]; am[c] = yy * w + xx; }
+        }
+      }
+      float d[8];
+      load8(dyp + (((int64_t)b * oh + oy) * ow + ox) * C + g * 8, d);
+      const int me = iy * w + ix;
+#pragma unroll
+      for (int c = 0; c < 8; c++) if (am[c] == me) acc[c] += d[c];
+    }
+  }
+  store8(dx + pix * C + g * 8, acc);
+}
+
+__global__ void avgpool_fwd(const bf16* __restrict__ x, int n, int h, int w, int C, int xcs, int k, int oh, int ow,
+                            bf16* __restrict__ y) {
+  const int G = C / 8;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * oh * ow * G) return;
+  const int g = (int)(i % G);
+  const int64_t pix = i / G;
+  const int ox = (int)(pix % ow), oy = (int)((pix / ow) % oh), b = (int)(pix / ((int64_t)ow * oh));
+  float a[8] = {0};
+  for (int dy = 0; dy < k; dy++)
+    for (int dx = 0; dx < k; dx++) {
+      float v[8];
+      load8(x + (((int64_t)b * h + oy * k + dy) * w + ox * k + dx) * xcs + g * 8, v);
+#pragma unroll
+      for (int c = 0; c < 8; c++) a[c] += v[c];
+    }
+  const float inv = 1.0f / (k * k);
+#pragma unroll
+  for (int c = 0; c < 8; c++) a[c] *= inv;
+  store8(y + pix * C + g * 8, a);
+}
+
+__global__ void avgpool_bwd(const bf16* __restrict__ dy, int n, int h, int w, int C, int k, int oh, int ow,
+                            bf16* __restrict__ dx, int dxcs) {
+  const int G = C / 8;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * h * w * G) return;
+  const int g = (int)(i % G);
+  const int64_t pix = i / G;
+  const int ix = (int)(pix % w), iy = (int)((pix / w) % h), b = (int)(pix / ((int64_t)w * h));
+  float v[8];
+  const int ox = ix / k, oy = iy / k;
+  if (ox < ow && oy < oh) {
+    load8(dy + (((int64_t)b * oh + oy) * ow + ox) * C + g * 8, v);
+    const float inv = 1.0f / (k * k);
+#pragma unroll
+    for (int c = 0; c < 8; c++) v[c] *= inv;
+  } else {
+#pragma unroll
+    for (int c = 0; c < 8; c++) v[c] = 0.f;
+  }
+  store8(dx + pix * dxcs + g * 8, v);
+}
+
+// global average pool: x [n][hw][C] (stride xcs) -> y [n][C] bf16
+__global__ void gap_fwd(const bf16* __restrict__ x, int n, int hw, int C, int xcs, bf16* __restrict__ y) {
+  const int G = C / 8;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * G) return;
+  const int b = i / G, g = i % G;
+  float a[8] = {0};
+  for (int j = 0; j < hw; j++) {
+    float v[8];
+    load8(x + ((int64_t)b * hw + j) * xcs + g * 8, v);
+#pragma unroll
+    for (int c = 0; c < 8; c++) a[c] += v[c];
+  }
+  const float inv = 1.0f / hw;
+#pragma unroll
+  for (int c = 0; c < 8; c++) a[c] *= inv;
+  store8(y + (int64_t)b * C + g * 8, a);
+}
+
+__global__ void gap_bwd(const bf16* __restrict__ dy, int n, int hw, int C, bf16* __restrict__ dx) {
+  const int G = C / 8;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * hw * G) return;
+  const int g = (int)(i % G);
+  const int64_t pix = i / G;
+  const int b = (int)(pix / hw);
+  float v[8];
+  load8(dy + (int64_t)b * C + g * 8, v);
+  const float inv = 1.0f / hw;
+#pragma unroll
+  for (int c = 0; c < 8; c++) v[c] *= inv;
+  store8(dx + pix * C + g * 8, v);
+}
+
+// ---- softmax cross-entropy: one warp per row, classes <= 32*4 ----------------------------
+__global__ void softmax_xent(const float* __restrict__ logits, int B, int C, const int32_t* __restrict__ labels,
+                             float scale, float* __restrict__ row_loss, bf16* __restrict__ dlogits, int ldd) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= B) return;
+  const float* l = logits + (int64_t)row * ldd;   // logits and dlogits share the row stride
+  float v[4];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < 4; j++) { const int c = lane + 32 * j; v[j] = c < C ? l[c] : -INFINITY; mx = fmaxf(mx, v[j]); }
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float se = 0.f;
+#pragma unroll
+  for (int j = 0; j < 4; j++) { const int c = lane + 32 * j; if (c < C) se += expf(v[j] - mx); }
+  for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+  const int lab = labels[row];
+  const float lse = logf(se) + mx;
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    const int c = lane + 32 * j;
+    if (c < C) {
+      const float pr = expf(v[j] - lse);
+      dlogits[(int64_t)row * ldd + c] = __float2bfloat16_rn((pr - (c == lab ? 1.f : 0.f)) * scale);
+      if (c == lab) row_loss[row] = lse - v[j];
+    }
+  }
+}
+
+// deterministic sum of n floats into out[0] (single block)
+__global__ void sum_small(const float* __restrict__ x, int n, float scale, float* __restrict__ out) {
+  __shared__ double sh[256];
+  double a = 0;
+  for (int i = threadIdx.x; i < n; i += 256) a += x[i];
+  sh[threadIdx.x] = a;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = (float)(sh[0] * scale);
+}
+
+// ---- misc -------------------------------------------------------------------------------
+__global__ void reduce_splits(const float* __restrict__ part, int splits, int64_t count, float* __restrict__ out,
+                              int accumulate, float scale) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  float a = 0.f;
+  for (int s = 0; s < splits; s++) a += part[s * count + i];
+  a *= scale;
+  out[i] = accumulate ? out[i] + a : a;
+}
+
+// wt[ci][kh'][kw'][co] = w[co][KH-1-kh'][KW-1-kw'][ci]
+__global__ void weight_flip(const bf16* __restrict__ w, int cout, int kh, int kw, int cin, bf16* __restrict__ wt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)cout * kh * kw * cin;
+  if (i >= total) return;
+  const int co = (int)(i % cout);
+  int64_t r = i / cout;
+  const int x = (int)(r % kw); r /= kw;
+  const int y = (int)(r % kh);
+  const int ci = (int)(r / kh);
+  wt[i] = w[(((int64_t)co * kh + (kh - 1 - y)) * kw + (kw - 1 - x)) * cin + ci];
+}
+
+__global__ void zero_upsample(const bf16* __restrict__ dy, int n, int oh, int ow, int C, int dycs, bf16* __restrict__ out,
+                              int uh, int uw) {
+  const int G = C / 8;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * uh * uw * G) return;
+  const int g = (int)(i % G);
+  const int64_t pix = i / G;
+  const int x = (int)(pix % uw), y = (int)((pix / uw) % uh), b = (int)(pix / ((int64_t)uw * uh));
+  uint4 v = make_uint4(0, 0, 0, 0);
+  if (!(x & 1) && !(y & 1)) v = *reinterpret_cast<const uint4*>(dy + (((int64_t)b * oh + (y >> 1)) * ow + (x >> 1)) * dycs + g * 8);
+  *reinterpret_cast<uint4*>(out + pix * C + g * 8) = v;
+}
+
+// column sums of a row-major [rows][cols] bf16/fp32 matrix -> fp32 (bias gradients)
+__global__ void col_sum(const void* __restrict__ x, int is_f32, int64_t rows, int cols, int64_t ld, float* __restrict__ out,
+                        int accumulate) {
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int rl = threadIdx.x >> 5;  // 8 row lanes
+  __shared__ float sh[8][32];
+  float a = 0.f;
+  if (c < cols) {
+    for (int64_t r = rl; r < rows; r += 8)
+      a += is_f32 ? reinterpret_cast<const float*>(x)[r * ld + c] : __bfloat162float(reinterpret_cast<const bf16*>(x)[r * ld + c]);
+  }
+  sh[rl][threadIdx.x & 31] = a;
+  __syncthreads();
+  if (rl == 0 && c < cols) {
+    float s = 0.f;
+    for (int l = 0; l < 8; l++) s += sh[l][threadIdx.x];
+    out[c] = accumulate ? out[c] + s : s;
+  }
+}
+
+// relu backward on a bf16 matrix in place: dx = dy * (y > 0)
+__global__ void relu_bwd(bf16* __restrict__ dy, const bf16* __restrict__ y, int64_t n8) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n8) return;
+  float d[8], v[8];
+  load8(dy + i * 8, d);
+  load8(y + i * 8, v);
+#pragma unroll
+  for (int k = 0; k < 8; k++) if (!(v[k] > 0.f)) d[k] = 0.f;
+  store8(dy + i * 8, d);
+}
+
+__global__ void relu_fwd(bf16* __restrict__ x, int64_t n8) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n8) return;
+  float v[8];
+  load8(x + i * 8, v);
+#pragma unroll
+  for (int k = 0; k < 8; k++) v[k] = fmaxf(v[k], 0.f);
+  store8(x + i * 8, v);
+}
+
+// torch.optim.Adam (no weight decay, no amsgrad) over flat fp32 buffers; refreshes the
+// bf16 compute copy.  step_size = lr / (1 - b1^t), inv_bc2_sqrt = 1 / sqrt(1 - b2^t).
+// Device-side step counter so a captured CUDA graph can be replayed: step += 1 and the
+// bias-correction factors are recomputed on the device every replay.
+__global__ void adam_schedule(int32_t* step, float lr, float b1, float b2, float* sched) {
+  const int t = ++(*step);
+  sched[0] = (float)((double)lr / (1.0 - pow((double)b1, (double)t)));
+  sched[1] = (float)(1.0 / sqrt(1.0 - pow((double)b2, (double)t)));
+}
+
+__global__ void adam_step(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v,
+                          bf16* __restrict__ pb, int64_t n, float b1, float b2, float eps, float step_size,
+                          float inv_bc2_sqrt, float grad_scale, const float* __restrict__ sched) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (sched) { step_size = sched[0]; inv_bc2_sqrt = sched[1]; }
+  const float gi = g[i] * grad_scale;
+  const float mi = b1 * m[i] + (1.f - b1) * gi;
+  const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+  m[i] = mi;
+  v[i] = vi;
+  const float denom = sqrtf(vi) * inv_bc2_sqrt + eps;
+  const float pi = p[i] - step_size * (mi / denom);
+  p[i] = pi;
+  if (pb) pb[i] = __float2bfloat16_rn(pi);
+}
+
+// torch.optim.SGD with momentum (dampening 0, no nesterov) + optional weight decay
+__global__ void sgd_step(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ buf, bf16* __restrict__ pb,
+                         int64_t n, float lr, float momentum, float wd, float grad_scale, int first) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float d = g[i] * grad_scale + wd * p[i];
+  if (momentum != 0.f) { d = first ? d : momentum * buf[i] + d; buf[i] = d; }
+  const float pi = p[i] - lr * d;
+  p[i] = pi;
+  if (pb) pb[i] = __float2bfloat16_rn(pi);
+}
+
+__global__ void cast_f32_bf16(const float* __restrict__ x, bf16* __restrict__ y, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = __float2bfloat16_rn(x[i]);
+}
+
+inline unsigned nblocks(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+int stats_blocks(int64_t rows, int C, int64_t* rpb) {
+  int nsm = cvb_num_sms();
+  int64_t target = (int64_t)nsm * 4;
+  int64_t per = (rows + target - 1) / target;
+  if (per < 64) per = 64;
+  *rpb = per;
+  return (int)((rows + per - 1) / per);
+}
+
+}  // namespace
+
+// ======================================= C ABI ==========================================
+#define STREAM (cudaStream_t)stream
+
+// Batch-norm forward statistics over rows of x ([rows][C], channel stride xcs).  ws must hold
+// cvb_bn_workspace_floats(rows, C) floats.  Writes mean/rstd; updates running stats if given.
+CVB_API int64_t cvb_bn_workspace_floats(int64_t rows, int C) {
+  int64_t rpb;
+  return (int64_t)stats_blocks(rows, C, &rpb) * 2 * C;
+}
+
+CVB_API int cvb_bn_stats(const void* x, int64_t rows, int C, int xcs, float* ws, float* mean, float* rstd, float eps,
+                         float* run_mean, float* run_var, float momentum, void* stream) {
+  if (C % 8 || C / 8 > ST_THREADS) { cvb_set_error("bn_stats: C must be a multiple of 8, <= 2048"); return CVB_EINVAL; }
+  int64_t rpb;
+  int nb = stats_blocks(rows, C, &rpb);
+  const int G = C / 8, RL = ST_THREADS / G;
+  chan_stats_partial<<<nb, ST_THREADS, RL * G * 16 * sizeof(float), STREAM>>>((const bf16*)x, rows, C, xcs, rpb, ws);
+  bn_finalize<<<nblocks(C), 256, 0, STREAM>>>(ws, nb, C, (double)rows, eps, mean, rstd, run_mean, run_var, momentum);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_bn_apply(const void* x, int64_t rows, int C, int xcs, const float* mean, const float* rstd,
+                         const float* gamma, const float* beta, const void* res, int rcs, int relu, void* y, int ycs,
+                         int ycoff, void* stream) {
+  bn_apply<<<nblocks(rows * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, rows, C, xcs, mean, rstd, gamma, beta,
+                                                       (const bf16*)res, rcs, relu, (bf16*)y, ycs, ycoff);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+// Batch-norm (+ReLU) backward.  dy: grad of the layer output; y (optional): layer output for
+// the ReLU mask (else recomputed from x).  Writes dgamma/dbeta (fp32) and dx (bf16, stride
+// dxcs) or, if dx32 != NULL, fp32 dx (accumulated when accum32).  dz_out (optional, [rows][C]
+// bf16) receives the masked output gradient (the residual branch's gradient).
+CVB_API int cvb_bn_backward(const void* dy, int dycs, const void* x, int xcs, const void* y, int ycs, int64_t rows, int C,
+                            const float* mean, const float* rstd, const float* gamma, const float* beta, int relu,
+                            float* ws, float* dgamma, float* dbeta, void* dx, int dxcs, float* dx32, int accum32,
+                            void* dz_out, void* stream) {
+  if (C % 8 || C / 8 > ST_THREADS) { cvb_set_error("bn_backward: bad C"); return CVB_EINVAL; }
+  int64_t rpb;
+  int nb = stats_blocks(rows, C, &rpb);
+  const int G = C / 8, RL = ST_THREADS / G;
+  bn_bwd_partial<<<nb, ST_THREADS, RL * G * 16 * sizeof(float), STREAM>>>(
+      (const bf16*)dy, dycs, (const bf16*)x, xcs, (const bf16*)y, ycs, rows, C, mean, rstd, gamma, beta, relu, rpb, ws,
+      (bf16*)dz_out);
+  bn_bwd_finalize<<<nblocks(C), 256, 0, STREAM>>>(ws, nb, C, dbeta, dgamma);
+  if (dx || dx32)
+    bn_bwd_apply<<<nblocks(rows * G), 256, 0, STREAM>>>((const bf16*)dy, dycs, (const bf16*)x, xcs, (const bf16*)y, ycs,
+                                                        rows, C, mean, rstd, gamma, beta, relu, dbeta, dgamma, (bf16*)dx,
+                                                        dxcs, dx32, accum32);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_maxpool_fwd(const void* x, int n, int h, int w, int C, int k, int s, int p, void* y, int oh, int ow,
+                            void* stream) {
+  maxpool_fwd<<<nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, n, h, w, C, k, s, p, oh, ow, (bf16*)y);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_maxpool_bwd(const void* x, const void* dy, int n, int h, int w, int C, int k, int s, int p, int oh,
+                            int ow, void* dx, void* stream) {
+  maxpool_bwd<<<nblocks((int64_t)n * h * w * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, (const bf16*)dy, n, h, w, C, k, s,
+                                                                         p, oh, ow, (bf16*)dx);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_avgpool_fwd(const void* x, int n, int h, int w, int C, int xcs, int k, void* y, void* stream) {
+  const int oh = h / k, ow = w / k;
+  avgpool_fwd<<<nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, n, h, w, C, xcs, k, oh, ow, (bf16*)y);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_avgpool_bwd(const void* dy, int n, int h, int w, int C, int k, void* dx, int dxcs, void* stream) {
+  const int oh = h / k, ow = w / k;
+  avgpool_bwd<<<nblocks((int64_t)n * h * w * (C / 8)), 256, 0, STREAM>>>((const bf16*)dy, n, h, w, C, k, oh, ow, (bf16*)dx, dxcs);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_gap_fwd(const void* x, int n, int hw, int C, int xcs, void* y, void* stream) {
+  gap_fwd<<<nblocks((int64_t)n * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, n, hw, C, xcs, (bf16*)y);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_gap_bwd(const void* dy, int n, int hw, int C, void* dx, void* stream) {
+  gap_bwd<<<nblocks((int64_t)n * hw * (C / 8)), 256, 0, STREAM>>>((const bf16*)dy, n, hw, C, (bf16*)dx);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+// Softmax cross-entropy: loss_out[0] = mean over the B rows * loss_scale; dlogits (bf16,
+// row stride ldd) = (softmax - onehot) * grad_scale.  row_ws: B floats.
+CVB_API int cvb_softmax_xent(const float* logits, int B, int C, const int32_t* labels, float grad_scale, float* row_ws,
+                             float* loss_out, void* dlogits, int ldd, void* stream) {
+  if (C > 128) { cvb_set_error("softmax_xent: C > 128"); return CVB_EINVAL; }
+  softmax_xent<<<nblocks((int64_t)B * 32), 256, 0, STREAM>>>(logits, B, C, labels, grad_scale, row_ws, (bf16*)dlogits, ldd);
+  sum_small<<<1, 256, 0, STREAM>>>(row_ws, B, 1.0f / B, loss_out);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_reduce_splits(const float* part, int splits, int64_t count, float* out, int accumulate, float scale,
+                              void* stream) {
+  reduce_splits<<<nblocks(count), 256, 0, STREAM>>>(part, splits, count, out, accumulate, scale);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_weight_flip(const void* w, int cout, int kh, int kw, int cin, void* wt, void* stream) {
+  weight_flip<<<nblocks((int64_t)cout * kh * kw * cin), 256, 0, STREAM>>>((const bf16*)w, cout, kh, kw, cin, (bf16*)wt);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_zero_upsample(const void* dy, int n, int oh, int ow, int C, int dycs, void* out, void* stream) {
+  const int uh = 2 * oh - 1, uw = 2 * ow - 1;
+  zero_upsample<<<nblocks((int64_t)n * uh * uw * (C / 8)), 256, 0, STREAM>>>((const bf16*)dy, n, oh, ow, C, dycs, (bf16*)out, uh, uw);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_col_sum(const void* x, int is_f32, int64_t rows, int cols, int64_t ld, float* out, int accumulate,
+                        void* stream) {
+  col_sum<<<(cols + 31) / 32, 256, 0, STREAM>>>(x, is_f32, rows, cols, ld, out, accumulate);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_relu_fwd(void* x, int64_t n, void* stream) {
+  relu_fwd<<<nblocks(n / 8), 256, 0, STREAM>>>((bf16*)x, n / 8);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_relu_bwd(void* dy, const void* y, int64_t n, void* stream) {
+  relu_bwd<<<nblocks(n / 8), 256, 0, STREAM>>>((bf16*)dy, (const bf16*)y, n / 8);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+// step > 0: host-side bias correction for that step.  step <= 0: device counter mode --
+// step_dev is incremented on the device and the factors land in sched_dev (2 floats).
+CVB_API int cvb_adam_step(float* p, const float* g, float* m, float* v, void* pb, int64_t n, float lr, float b1, float b2,
+                          float eps, int64_t step, float grad_scale, int32_t* step_dev, float* sched_dev, void* stream) {
+  if (step > 0) {
+    const double bc1 = 1.0 - pow((double)b1, (double)step), bc2 = 1.0 - pow((double)b2, (double)step);
+    adam_step<<<nblocks(n), 256, 0, STREAM>>>(p, g, m, v, (bf16*)pb, n, b1, b2, eps, (float)(lr / bc1),
+                                              (float)(1.0 / sqrt(bc2)), grad_scale, nullptr);
+  } else {
+    if (!step_dev || !sched_dev) { cvb_set_error("adam_step: device counter mode needs step_dev/sched_dev"); return CVB_EINVAL; }
+    adam_schedule<<<1, 1, 0, STREAM>>>(step_dev, lr, b1, b2, sched_dev);
+    adam_step<<<nblocks(n), 256, 0, STREAM>>>(p, g, m, v, (bf16*)pb, n, b1, b2, eps, 0.f, 0.f, grad_scale, sched_dev);
+  }
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_sgd_step(float* p, const float* g, float* buf, void* pb, int64_t n, float lr, float momentum, float wd,
+                         float grad_scale, int first, void* stream) {
+  sgd_step<<<nblocks(n), 256, 0, STREAM>>>(p, g, buf, (bf16*)pb, n, lr, momentum, wd, grad_scale, first);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream) {
+  cast_f32_bf16<<<nblocks(n), 256, 0, STREAM>>>(x, (bf16*)y, n);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}

@@ -63,6 +63,7 @@ struct GemmParams {
   int col_off;
   const float* bias;
   int part_rows;            // OUT_PARTIAL: rows per split slab
+  int accum;                // add into the existing output
 };
 
 // ---------------------------------------------------------------------------------------
@@ -347,6 +348,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           if (p.bias && col + j < p.N) v[j] += p.bias[col + j];
         }
         const int64_t off = dst_row * p.ldc + p.col_off + col;
+        if (p.accum) {   // out += result (residual / concat gradient accumulation)
+          for (int j = 0; j < 16 && col + j < p.N; j++)
+            v[j] += p.out_f32 ? reinterpret_cast<const float*>(p.out)[off + j]
+                              : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.out)[off + j]);
+        }
         if (col + 16 <= p.N) {
           if (p.out_f32) {
             float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + off);
@@ -536,7 +542,7 @@ void pick_kbox(int n, int oh, int ow, int& bw, int& bh, int& bn) {
 // w: bf16 [cout][kh*kw*cin] (K-major).  y: NHWC (bf16, or fp32 if y_f32) with channel stride ycs.
 CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs, const void* wt, int cout, int kh,
                            int kw, int stride, int pad, void* y, int oh, int ow, int ycs, int yoff, const float* bias,
-                           int y_f32, void* stream) {
+                           int y_f32, int accumulate, void* stream) {
   if (get_encoder()) return CVB_ECUDA;
   const int acel = pick_cel(cin);
   if (!acel || (stride != 1 && stride != 2) || cout % 8) { cvb_set_error("conv2d_fwd: unsupported shape"); return CVB_EINVAL; }
@@ -576,6 +582,7 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
   }
   if ((rc = encode_2d(&p.mapB[0], wt, cout, K, K, p.b_cel, p.BN))) return rc;
   p.out_mode = OUT_NHWC; p.out_f32 = y_f32; p.out = y; p.ldc = ycs; p.col_off = yoff; p.bias = bias;
+  p.accum = accumulate;
   return launch(p, (cudaStream_t)stream);
 }
 
@@ -641,7 +648,8 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
 //   B: b_major 0 -> row-major [N][K] (ldb), 1 -> row-major [K][N] (ldb)
 // C row-major [M][ldc] bf16 or fp32; split-K > 1 writes fp32 partials [split][M][ldc].
 CVB_API int cvb_gemm(const void* a, int a_major, int64_t lda, const void* b, int b_major, int64_t ldb, int M, int N,
-                     int K, void* c, int64_t ldc, int c_f32, const float* bias, int splits, void* stream) {
+                     int K, void* c, int64_t ldc, int c_f32, const float* bias, int splits, int accumulate,
+                     void* stream) {
   if (get_encoder()) return CVB_ECUDA;
   GemmParams p;
   memset(&p, 0, sizeof(p));
@@ -671,6 +679,7 @@ CVB_API int cvb_gemm(const void* a, int a_major, int64_t lda, const void* b, int
   if (p.splits > 1) { p.out_mode = OUT_PARTIAL; p.out_f32 = 1; p.part_rows = M; }
   else { p.out_mode = OUT_ROWS; p.out_f32 = c_f32; }
   p.out = c; p.ldc = ldc; p.bias = p.splits > 1 ? nullptr : bias;
+  p.accum = p.splits > 1 ? 0 : accumulate;
   return launch(p, (cudaStream_t)stream);
 }
 

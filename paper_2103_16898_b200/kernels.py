@@ -1,8 +1,8 @@
 """Torch-tensor front end of the sm_100a kernels (no compute here, only argument plumbing).
 
-Every function launches one of the library's CUDA kernels on the current torch stream.
-Activations are NHWC bf16; weights are bf16 [Cout][KH][KW][Cin] (K-major); gradients and
-optimiser state are fp32.  There is no fallback: a missing library raises.
+Every function launches one or more of the library's CUDA kernels on the current torch
+stream.  Activations are NHWC bf16; weights are bf16 [Cout][KH][KW][Cin] (K-major);
+gradients and optimiser state are fp32.  There is no fallback: a missing library raises.
 """
 from __future__ import annotations
 
@@ -14,6 +14,46 @@ from . import _lib
 
 BF16 = torch.bfloat16
 F32 = torch.float32
+
+
+class Recorder:
+    """Launch accounting: counts every kernel this module launches and, when `timing` is on,
+    brackets each call with CUDA events on the launching stream and records its algorithmic
+    FLOPs / bytes (bench.py uses it for the roofline of the dominant kernel)."""
+
+    def __init__(self):
+        self.launches = 0
+        self.timing = False
+        self.records = []   # (kind, flops, bytes, ev_start, ev_end)
+
+    def begin(self, n_kernels, kind, flops=0, nbytes=0):
+        self.launches += n_kernels
+        if not self.timing:
+            return None
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        return (kind, flops, nbytes, e0)
+
+    def end(self, tok):
+        if tok is None:
+            return
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        self.records.append((*tok, e1))
+
+    def summary(self):
+        """{kind: [calls, ms, flops, bytes]} (call after a synchronize)."""
+        out = {}
+        for kind, fl, nb, e0, e1 in self.records:
+            c = out.setdefault(kind, [0, 0.0, 0, 0])
+            c[0] += 1
+            c[1] += e0.elapsed_time(e1)
+            c[2] += fl
+            c[3] += nb
+        return out
+
+
+REC = Recorder()
 
 
 def _ptr(t):
@@ -33,27 +73,33 @@ def conv_out_hw(h, w, k, stride, pad):
     return (h + 2 * pad - k) // stride + 1, (w + 2 * pad - k) // stride + 1
 
 
-def conv2d_fwd(x, w, stride=1, pad=0, bias=None, out=None, out_f32=False, cin=None, out_coff=0):
+def conv2d_fwd(x, w, stride=1, pad=0, bias=None, out=None, out_f32=False, cin=None, out_coff=0, out_hw=None,
+               accumulate=False, acct_flops=None, kind="umma_gemm"):
     """x: [N,H,W,Cs] bf16 (channels [0,cin) used, stride Cs); w: [Cout,KH,KW,cin] bf16.
 
-    Returns y [N,OH,OW,Cout] (or writes into `out` at channel offset out_coff)."""
+    Returns y [N,OH,OW,Cout] (or writes into `out` at channel offset out_coff; adds into it
+    when accumulate).  out_hw overrides the output extent (transposed-conv dgrad)."""
     lib = _lib_bound()
     n, h, wd, cs = x.shape
     cin = cs if cin is None else cin
     cout, kh, kw, wc = w.shape
     assert wc == cin and x.stride(-1) == 1 and w.is_contiguous()
-    oh, ow = conv_out_hw(h, wd, kh, stride, pad)
+    oh, ow = conv_out_hw(h, wd, kh, stride, pad) if out_hw is None else out_hw
     if out is None:
         out = torch.empty((n, oh, ow, cout), dtype=F32 if out_f32 else BF16, device=x.device)
     ycs = out.shape[-1]
     assert out.shape[:3] == (n, oh, ow) and (out.dtype == F32) == bool(out_f32)
+    flops = acct_flops if acct_flops is not None else 2 * n * oh * ow * cout * kh * kw * cin
+    tok = REC.begin(1, kind, flops)
     rc = lib.cvb_conv2d_fwd(x.data_ptr(), n, h, wd, cin, x.stride(2), w.data_ptr(), cout, kh, kw, stride, pad,
-                            out.data_ptr(), oh, ow, ycs, out_coff, _ptr(bias), int(out_f32), _stream())
+                            out.data_ptr(), oh, ow, ycs, out_coff, _ptr(bias), int(out_f32), int(accumulate),
+                            _stream())
+    REC.end(tok)
     _lib.check(rc, "conv2d_fwd")
     return out
 
 
-def conv2d_wgrad_partials(dy, x, kh, kw, stride, pad, cin=None, max_splits=148, part=None):
+def conv2d_wgrad_partials(dy, x, kh, kw, stride, pad, cin=None, max_splits=148, part=None, acct_flops=None):
     """fp32 partial weight gradients [splits, Cout, KH*KW*cin]; returns (part, splits)."""
     lib = _lib_bound()
     n, oh, ow, cout = dy.shape
@@ -63,14 +109,18 @@ def conv2d_wgrad_partials(dy, x, kh, kw, stride, pad, cin=None, max_splits=148, 
     if part is None:
         part = torch.empty((max_splits, cout, ncols), dtype=F32, device=dy.device)
     used = ctypes.c_int(0)
+    flops = acct_flops if acct_flops is not None else 2 * n * oh * ow * cout * ncols
+    tok = REC.begin(1, "umma_gemm", flops)
     rc = lib.cvb_conv2d_wgrad(dy.data_ptr(), n, oh, ow, cout, dy.stride(2), x.data_ptr(), h, wd, cin, x.stride(2),
                               kh, kw, stride, pad, part.data_ptr(), min(max_splits, part.shape[0]),
                               ctypes.byref(used), _stream())
+    REC.end(tok)
     _lib.check(rc, "conv2d_wgrad")
     return part, used.value
 
 
-def gemm(a, b, M, N, K, a_major=0, b_major=0, out=None, out_f32=False, bias=None, splits=1):
+def gemm(a, b, M, N, K, a_major=0, b_major=0, out=None, out_f32=False, bias=None, splits=1, accumulate=False,
+         acct_flops=None):
     """C[M,N] = sum_k A(m,k) B(n,k) with A [M,K] (a_major 0) or [K,M] (1), B [N,K] (0) or [K,N] (1)."""
     lib = _lib_bound()
     used = lib.cvb_gemm_splits_used(K, splits)
@@ -79,7 +129,172 @@ def gemm(a, b, M, N, K, a_major=0, b_major=0, out=None, out_f32=False, bias=None
             out = torch.empty((used, M, N), dtype=F32, device=a.device)
         else:
             out = torch.empty((M, N), dtype=F32 if out_f32 else BF16, device=a.device)
+    tok = REC.begin(1, "umma_gemm", acct_flops if acct_flops is not None else 2 * M * N * K)
     rc = lib.cvb_gemm(a.data_ptr(), a_major, a.stride(0), b.data_ptr(), b_major, b.stride(0), M, N, K,
-                      out.data_ptr(), out.stride(-2), int(out_f32 or used > 1), _ptr(bias), splits, _stream())
+                      out.data_ptr(), out.stride(-2), int(out_f32 or used > 1), _ptr(bias), splits, int(accumulate),
+                      _stream())
+    REC.end(tok)
     _lib.check(rc, "gemm")
     return out
+
+
+# ---------------------------------------------------------------------------------------
+# memory-bound kernels (csrc/nn.cu); `nbytes` = algorithmic HBM bytes (reads + writes)
+# ---------------------------------------------------------------------------------------
+def bn_workspace(rows, C, device="cuda"):
+    n = _lib_bound().cvb_bn_workspace_floats(rows, C)
+    return torch.empty(max(1, n), dtype=F32, device=device)
+
+
+def bn_stats(x, rows, C, xcs, ws, mean, rstd, eps=1e-5, run_mean=None, run_var=None, momentum=0.1):
+    tok = REC.begin(2, "bn", 0, rows * C * 2)
+    rc = _lib_bound().cvb_bn_stats(x.data_ptr(), rows, C, xcs, ws.data_ptr(), mean.data_ptr(), rstd.data_ptr(), eps,
+                                   _ptr(run_mean), _ptr(run_var), momentum, _stream())
+    REC.end(tok)
+    _lib.check(rc, "bn_stats")
+
+
+def bn_apply(x, rows, C, xcs, mean, rstd, gamma, beta, y, ycs, ycoff=0, relu=True, res=None, rcs=0):
+    tok = REC.begin(1, "bn", 0, rows * C * 2 * (3 if res is not None else 2))
+    rc = _lib_bound().cvb_bn_apply(x.data_ptr(), rows, C, xcs, mean.data_ptr(), rstd.data_ptr(), gamma.data_ptr(),
+                                   beta.data_ptr(), _ptr(res), rcs, int(relu), y.data_ptr(), ycs, ycoff, _stream())
+    REC.end(tok)
+    _lib.check(rc, "bn_apply")
+
+
+def bn_backward(dy, dycs, x, xcs, rows, C, mean, rstd, gamma, beta, ws, dgamma, dbeta, relu=True, y=None, ycs=0,
+                dx=None, dxcs=0, dx32=None, accum32=False, dz_out=None):
+    # partial pass reads dy, x (, y) [+ writes dz]; apply pass re-reads them and writes dx
+    nb = rows * C * 2 * ((3 if y is not None else 2) * 2 + (1 if dz_out is not None else 0) + 1)
+    tok = REC.begin(3 if (dx is not None or dx32 is not None) else 2, "bn", 0, nb)
+    rc = _lib_bound().cvb_bn_backward(dy.data_ptr(), dycs, x.data_ptr(), xcs, _ptr(y), ycs, rows, C, mean.data_ptr(),
+                                      rstd.data_ptr(), gamma.data_ptr(), beta.data_ptr(), int(relu), ws.data_ptr(),
+                                      dgamma.data_ptr(), dbeta.data_ptr(), _ptr(dx), dxcs, _ptr(dx32), int(accum32),
+                                      _ptr(dz_out), _stream())
+    REC.end(tok)
+    _lib.check(rc, "bn_backward")
+
+
+def maxpool_fwd(x, k, s, p, y):
+    n, h, w, c = x.shape
+    _, oh, ow, _ = y.shape
+    tok = REC.begin(1, "pool", 0, (x.numel() + y.numel()) * 2)
+    rc = _lib_bound().cvb_maxpool_fwd(x.data_ptr(), n, h, w, c, k, s, p, y.data_ptr(), oh, ow, _stream())
+    REC.end(tok)
+    _lib.check(rc, "maxpool_fwd")
+
+
+def maxpool_bwd(x, dy, k, s, p, dx):
+    n, h, w, c = x.shape
+    _, oh, ow, _ = dy.shape
+    tok = REC.begin(1, "pool", 0, (2 * x.numel() + dy.numel()) * 2)
+    rc = _lib_bound().cvb_maxpool_bwd(x.data_ptr(), dy.data_ptr(), n, h, w, c, k, s, p, oh, ow, dx.data_ptr(),
+                                      _stream())
+    REC.end(tok)
+    _lib.check(rc, "maxpool_bwd")
+
+
+def avgpool_fwd(x, n, h, w, c, xcs, k, y):
+    tok = REC.begin(1, "pool", 0, n * h * w * c * 2 * 5 // 4)
+    rc = _lib_bound().cvb_avgpool_fwd(x.data_ptr(), n, h, w, c, xcs, k, y.data_ptr(), _stream())
+    REC.end(tok)
+    _lib.check(rc, "avgpool_fwd")
+
+
+def avgpool_bwd(dy, n, h, w, c, k, dx, dxcs):
+    tok = REC.begin(1, "pool", 0, n * h * w * c * 2 * 5 // 4)
+    rc = _lib_bound().cvb_avgpool_bwd(dy.data_ptr(), n, h, w, c, k, dx.data_ptr(), dxcs, _stream())
+    REC.end(tok)
+    _lib.check(rc, "avgpool_bwd")
+
+
+def gap_fwd(x, n, hw, c, xcs, y):
+    tok = REC.begin(1, "pool", 0, n * hw * c * 2)
+    rc = _lib_bound().cvb_gap_fwd(x.data_ptr(), n, hw, c, xcs, y.data_ptr(), _stream())
+    REC.end(tok)
+    _lib.check(rc, "gap_fwd")
+
+
+def gap_bwd(dy, n, hw, c, dx):
+    tok = REC.begin(1, "pool", 0, n * hw * c * 2)
+    rc = _lib_bound().cvb_gap_bwd(dy.data_ptr(), n, hw, c, dx.data_ptr(), _stream())
+    REC.end(tok)
+    _lib.check(rc, "gap_bwd")
+
+
+def softmax_xent(logits, B, C, labels, grad_scale, row_ws, loss_out, dlogits):
+    ld = logits.shape[-1]
+    assert dlogits.shape[-1] == ld
+    tok = REC.begin(2, "head", 0, B * ld * 6)
+    rc = _lib_bound().cvb_softmax_xent(logits.data_ptr(), B, C, labels.data_ptr(), grad_scale, row_ws.data_ptr(),
+                                       loss_out.data_ptr(), dlogits.data_ptr(), ld, _stream())
+    REC.end(tok)
+    _lib.check(rc, "softmax_xent")
+
+
+def reduce_splits(part, splits, count, out, accumulate=False, scale=1.0):
+    tok = REC.begin(1, "reduce", 0, (splits + 1) * count * 4)
+    rc = _lib_bound().cvb_reduce_splits(part.data_ptr(), splits, count, out.data_ptr(), int(accumulate), scale, _stream())
+    REC.end(tok)
+    _lib.check(rc, "reduce_splits")
+
+
+def weight_flip(w, wt):
+    cout, kh, kw, cin = w.shape
+    tok = REC.begin(1, "layout", 0, w.numel() * 4)
+    rc = _lib_bound().cvb_weight_flip(w.data_ptr(), cout, kh, kw, cin, wt.data_ptr(), _stream())
+    REC.end(tok)
+    _lib.check(rc, "weight_flip")
+
+
+def zero_upsample(dy, out):
+    n, oh, ow, c = dy.shape
+    tok = REC.begin(1, "layout", 0, (dy.numel() + out.numel()) * 2)
+    rc = _lib_bound().cvb_zero_upsample(dy.data_ptr(), n, oh, ow, c, dy.stride(2), out.data_ptr(), _stream())
+    REC.end(tok)
+    _lib.check(rc, "zero_upsample")
+
+
+def col_sum(x, rows, cols, ld, out, accumulate=False):
+    tok = REC.begin(1, "reduce", 0, rows * cols * x.element_size())
+    rc = _lib_bound().cvb_col_sum(x.data_ptr(), int(x.dtype == F32), rows, cols, ld, out.data_ptr(), int(accumulate),
+                                  _stream())
+    REC.end(tok)
+    _lib.check(rc, "col_sum")
+
+
+def relu_fwd(x):
+    tok = REC.begin(1, "eltwise", 0, x.numel() * 4)
+    rc = _lib_bound().cvb_relu_fwd(x.data_ptr(), x.numel(), _stream())
+    REC.end(tok)
+    _lib.check(rc, "relu_fwd")
+
+
+def relu_bwd(dy, y):
+    tok = REC.begin(1, "eltwise", 0, dy.numel() * 6)
+    rc = _lib_bound().cvb_relu_bwd(dy.data_ptr(), y.data_ptr(), dy.numel(), _stream())
+    REC.end(tok)
+    _lib.check(rc, "relu_bwd")
+
+
+def adam_step(p, g, m, v, pb, lr, b1, b2, eps, step=0, grad_scale=1.0, step_dev=None, sched_dev=None):
+    tok = REC.begin(1 if step > 0 else 2, "optimizer", 0, p.numel() * (4 * 7 + 2))
+    rc = _lib_bound().cvb_adam_step(p.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(), _ptr(pb), p.numel(), lr, b1,
+                                    b2, eps, step, grad_scale, _ptr(step_dev), _ptr(sched_dev), _stream())
+    REC.end(tok)
+    _lib.check(rc, "adam_step")
+
+
+def sgd_step(p, g, buf, pb, lr, momentum=0.0, wd=0.0, grad_scale=1.0, first=False):
+    tok = REC.begin(1, "optimizer", 0, p.numel() * (4 * 5 + 2))
+    rc = _lib_bound().cvb_sgd_step(p.data_ptr(), g.data_ptr(), buf.data_ptr(), _ptr(pb), p.numel(), lr, momentum, wd,
+                                   grad_scale, int(first), _stream())
+    REC.end(tok)
+    _lib.check(rc, "sgd_step")
+
+
+def cast_f32_bf16(x, y):
+    tok = REC.begin(1, "layout", 0, x.numel() * 6)
+    rc = _lib_bound().cvb_cast_f32_bf16(x.data_ptr(), y.data_ptr(), x.numel(), _stream())
+    REC.end(tok)
+    _lib.check(rc, "cast_f32_bf16")

@@ -1,0 +1,98 @@
+"""Decrypt-and-normalise loader: sealed record shards -> verified input tiles in HBM.
+
+Replaces the reference's data path Volume.get(...) -> bytes.decode -> parse_dataset
+(/root/reference/pkg/src/covault/volume.py:185-197, workload.py:24-41) for the binary
+record payload (CIFAR-10 binary layout: 1 label byte + C*H*W CHW pixel bytes per record).
+
+Per shard: ciphertext (host, pinned) -> H2D -> GCM open kernel (bit-exact AES-256-GCM,
+tag verified on device) -> record decoder kernel -> NHWC-8 bf16 tile + int32 labels.
+Security contract kept from the reference: a shard's plaintext is never consumed before its
+tag verdict is known (``ShardLoader.next`` checks the device status word of the shard it
+hands out; on a mismatch the plaintext was already zeroed on-stream and
+AuthenticationFailure is raised -- volume.py:186 "never partial").
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from .crypto import AuthenticationFailure, GcmContext
+from .volume import Volume, aad_for
+
+CIFAR = dict(c=3, h=32, w=32, mean=(0.5, 0.5, 0.5), std=(0.25, 0.25, 0.25))
+MEDICAL = dict(c=1, h=224, w=224, mean=(0.5,), std=(0.25,))
+
+
+def record_bytes(c, h, w):
+    return 1 + c * h * w
+
+
+def decode_records(pt_dev: torch.Tensor, nrec: int, c: int, h: int, w: int, mean, std, out=None, labels=None,
+                   dtype=torch.bfloat16):
+    """Verified plaintext records (uint8 CUDA tensor) -> (NHWC-8 tile, int32 labels)."""
+    lib = _lib.load()
+    if out is None:
+        out = torch.empty(nrec, h, w, 8, dtype=dtype, device=pt_dev.device)
+    if labels is None:
+        labels = torch.empty(nrec, dtype=torch.int32, device=pt_dev.device)
+    m = (ctypes.c_float * 8)(*mean)
+    s = (ctypes.c_float * 8)(*std)
+    rc = lib.cvb_records_to_nhwc(pt_dev.data_ptr(), nrec, record_bytes(c, h, w), c, h, w, m, s,
+                                 0 if dtype == torch.bfloat16 else 1, out.data_ptr(), labels.data_ptr(),
+                                 _lib.stream_ptr())
+    _lib.check(rc, "records_to_nhwc")
+    return out, labels
+
+
+class ShardSet:
+    """Sealed shards of one volume, held as pinned host ciphertext (the e2e input)."""
+
+    def __init__(self, volume: Volume, paths, spec=CIFAR):
+        self.volume, self.paths, self.spec = volume, list(paths), spec
+        self.rec = record_bytes(spec["c"], spec["h"], spec["w"])
+        self.blobs, self.nonces, self.aads, self.nrec = [], [], [], []
+        for p in self.paths:
+            e = volume.entry(p)
+            blob = volume.read_blob(p)
+            if (len(blob) - 16) % self.rec:
+                raise ValueError(f"{p}: plaintext length is not a whole number of records")
+            host = torch.frombuffer(bytearray(blob), dtype=torch.uint8).pin_memory()
+            self.blobs.append(host)
+            self.nonces.append(e.nonce)
+            self.aads.append(aad_for(volume.volume_name, p))
+            self.nrec.append((len(blob) - 16) // self.rec)
+
+
+class ShardLoader:
+    """Device pipeline for one shard at a time (buffers reused; graph-capture friendly)."""
+
+    def __init__(self, ctx: GcmContext, max_shard_bytes: int, max_records: int, spec=CIFAR, device="cuda"):
+        self.ctx, self.spec = ctx, spec
+        self.ct = torch.empty(max_shard_bytes + 16, dtype=torch.uint8, device=device)
+        self.pt = torch.empty(max_shard_bytes, dtype=torch.uint8, device=device)
+        self.aad = torch.zeros(256, dtype=torch.uint8, device=device)
+        self.work = ctx.new_workspace(device)
+        self.x = torch.empty(max_records, spec["h"], spec["w"], 8, dtype=torch.bfloat16, device=device)
+        self.labels = torch.empty(max_records, dtype=torch.int32, device=device)
+
+    def stage(self, blob_host: torch.Tensor, aad: bytes):
+        """H2D copy of one sealed shard (async on the current stream)."""
+        n = blob_host.numel()
+        self.ct[:n].copy_(blob_host, non_blocking=True)
+        self.aad[:len(aad)].copy_(torch.frombuffer(bytearray(aad), dtype=torch.uint8), non_blocking=True)
+        self.n, self.aad_len = n, len(aad)
+
+    def decrypt_decode(self, nonce: bytes, nrec: int):
+        """GCM open + record decode, stream-ordered, no host sync."""
+        s = self.spec
+        # the finalize kernel resets the GHASH accumulator and rewrites the status word
+        self.ctx.open_device(nonce, self.aad[:self.aad_len], self.ct[:self.n], self.pt, self.work)
+        decode_records(self.pt, nrec, s["c"], s["h"], s["w"], s["mean"], s["std"], out=self.x, labels=self.labels)
+        return self.x[:nrec], self.labels[:nrec]
+
+    def verify(self):
+        """Host check of the tag verdict of the last decrypted shard (synchronises)."""
+        if int(self.work[4].item()) != 0:
+            raise AuthenticationFailure("AEAD authentication failed for training shard")

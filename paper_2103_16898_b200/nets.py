@@ -1,0 +1,400 @@
+"""CNNs of the paper's GPU-offloaded training step, built on the sm_100a kernels.
+
+The reference contains no CNN (its trainer is a logistic toy, workload.py:48-71); the
+models follow the paper's prose and BASELINE.json's configs (defined in DESIGN.md):
+  SmallCNN     PAPER.md:441-443 "4 conv + BN, 2 FC, Adam lr 1e-3" on 32x32x3, 10 classes
+  ResNet18     CIFAR variant (3x3 stem, no max-pool), BASELINE.json configs[2]
+  DenseNet121  growth 32, blocks (6,12,24,16), 1-channel 224x224 stem, 2 classes, configs[3]
+
+Execution model: every buffer is allocated once for a fixed per-rank batch (build()), the
+step is a fixed launch sequence (forward, loss, backward, fused Adam) on the current
+stream, so it can be captured into one CUDA graph and replayed.  Parameters live in one
+flat fp32 buffer (plus grads, Adam moments and a bf16 compute copy) -- one Adam launch and
+one NCCL bucket space for data parallelism.
+
+Numerics (the contract the CPU restatement oracle/cnn_ref.py follows): conv/FC operands
+bf16, fp32 accumulation in TMEM, activations stored bf16, BN statistics and all gradients
+of parameters fp32, activation gradients stored bf16, master weights fp32.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import kernels as K
+
+BF16, F32 = torch.bfloat16, torch.float32
+ALIGN = 64  # elements; keeps every parameter view 128-byte aligned (TMA needs 16 B)
+
+
+def _pad16(n):
+    return (n + 15) // 16 * 16
+
+
+class ParamStore:
+    """Flat fp32 master / grad / Adam state + bf16 compute copy with per-parameter views."""
+
+    def __init__(self):
+        self.specs = []      # (name, shape, init cpu tensor)
+        self.logical = 0     # parameter count without layout padding
+
+    def add(self, name, init: torch.Tensor, logical: int | None = None):
+        self.specs.append((name, tuple(init.shape), init.float()))
+        self.logical += init.numel() if logical is None else logical
+        return name
+
+    def finalize(self, device):
+        offs, off = {}, 0
+        for name, shape, _ in self.specs:
+            offs[name] = off
+            n = math.prod(shape)
+            off += (n + ALIGN - 1) // ALIGN * ALIGN
+        self.total = off
+        self.p32 = torch.zeros(off, dtype=F32, device=device)
+        self.g32 = torch.zeros(off, dtype=F32, device=device)
+        self.m = torch.zeros(off, dtype=F32, device=device)
+        self.v = torch.zeros(off, dtype=F32, device=device)
+        self.pb = torch.zeros(off, dtype=BF16, device=device)
+        self.p, self.g, self.b, self.offsets = {}, {}, {}, offs
+        for name, shape, init in self.specs:
+            o, n = offs[name], math.prod(shape)
+            self.p[name] = self.p32[o:o + n].view(shape)
+            self.g[name] = self.g32[o:o + n].view(shape)
+            self.b[name] = self.pb[o:o + n].view(shape)
+            self.p[name].copy_(init.to(device))
+        K.cast_f32_bf16(self.p32, self.pb)
+        self.step_dev = torch.zeros(1, dtype=torch.int32, device=device)
+        self.sched = torch.zeros(2, dtype=F32, device=device)
+
+    def state_cpu(self):
+        return {name: self.p[name].detach().cpu().clone() for name, _, _ in self.specs}
+
+
+def _uniform(gen, shape, bound):
+    return (torch.rand(shape, generator=gen) * 2 - 1) * bound
+
+
+class Scratch:
+    """Shared scratch for split-K partials, BN partials and flipped weights."""
+
+    def __init__(self):
+        self.part_floats = 1
+        self.bn_floats = 1
+        self.flip_elems = 1
+        self.up_elems = 1
+
+    def finalize(self, device):
+        self.part = torch.empty(self.part_floats, dtype=F32, device=device)
+        self.bnws = torch.empty(self.bn_floats, dtype=F32, device=device)
+        self.flip = torch.empty(self.flip_elems, dtype=BF16, device=device)
+        self.up = torch.empty(self.up_elems, dtype=BF16, device=device)
+
+
+MAX_SPLITS = 148
+PART_CAP = 16 << 20   # floats of split-K partial workspace (64 MB)
+
+
+class ConvBN:
+    """conv (no bias) -> batch norm -> [+ residual] -> [ReLU]; NHWC bf16."""
+
+    def __init__(self, ps: ParamStore, name, cin, cout, k, stride, pad, gen, relu=True, cin_real=None,
+                 need_dgrad=True):
+        self.name, self.cin, self.cout, self.k, self.s, self.pad = name, cin, cout, k, stride, pad
+        self.relu, self.need_dgrad = relu, need_dgrad
+        cin_real = cin if cin_real is None else cin_real
+        self.cin_real = cin_real
+        bound = 1.0 / math.sqrt(cin_real * k * k)  # torch default (kaiming_uniform a=sqrt(5))
+        w = _uniform(gen, (cout, k, k, cin_real), bound)
+        if cin_real != cin:
+            w = torch.cat([w, torch.zeros(cout, k, k, cin - cin_real)], dim=3)
+        self.W = ps.add(f"{name}.w", w, logical=cout * k * k * cin_real)
+        self.G = ps.add(f"{name}.gamma", torch.ones(cout))
+        self.B = ps.add(f"{name}.beta", torch.zeros(cout))
+
+    def build(self, n, h, w, scratch: Scratch, device):
+        self.n, self.h, self.w = n, h, w
+        self.oh, self.ow = K.conv_out_hw(h, w, self.k, self.s, self.pad)
+        self.rows = n * self.oh * self.ow
+        self.flops = 2 * self.rows * self.cout * self.k * self.k * self.cin_real   # algorithmic, per pass
+        self.z = torch.empty(n, self.oh, self.ow, self.cout, dtype=BF16, device=device)
+        self.dz = torch.empty_like(self.z)
+        self.mean = torch.zeros(self.cout, dtype=F32, device=device)
+        self.rstd = torch.zeros(self.cout, dtype=F32, device=device)
+        self.run_mean = torch.zeros(self.cout, dtype=F32, device=device)
+        self.run_var = torch.ones(self.cout, dtype=F32, device=device)
+        self.wcount = self.cout * self.k * self.k * self.cin
+        scratch.part_floats = max(scratch.part_floats, min(MAX_SPLITS * self.wcount, max(PART_CAP, 8 * self.wcount)))
+        scratch.bn_floats = max(scratch.bn_floats, K._lib_bound().cvb_bn_workspace_floats(self.rows, self.cout))
+        if self.need_dgrad:
+            scratch.flip_elems = max(scratch.flip_elems, self.cout * self.k * self.k * self.cin)
+            if self.s == 2:
+                scratch.up_elems = max(scratch.up_elems, n * (2 * self.oh - 1) * (2 * self.ow - 1) * self.cout)
+        self.scratch = scratch
+        return self.oh, self.ow
+
+    def forward(self, ps: ParamStore, x, out, res=None, out_coff=0, cin=None):
+        """x: [n,h,w,cs] (channels [0,cin)); out: [n,oh,ow,ocs] written at channel out_coff."""
+        K.conv2d_fwd(x, ps.b[self.W], self.s, self.pad, out=self.z, cin=cin if cin is not None else self.cin,
+                     acct_flops=self.flops)
+        K.bn_stats(self.z, self.rows, self.cout, self.cout, self.scratch.bnws, self.mean, self.rstd,
+                   run_mean=self.run_mean, run_var=self.run_var)
+        K.bn_apply(self.z, self.rows, self.cout, self.cout, self.mean, self.rstd, ps.p[self.G], ps.p[self.B], out,
+                   out.shape[-1], out_coff, relu=self.relu, res=res, rcs=res.shape[-1] if res is not None else 0)
+
+    def backward(self, ps: ParamStore, dout, x, dx=None, y=None, dres=None, dx_accumulate=False, cin=None,
+                 dout_coff=0):
+        """dout: grad of this layer's output; y: the output (ReLU mask when a residual was added);
+        dres: receives the residual branch's gradient (masked dout); dx: grad wrt x (bf16)."""
+        cin = self.cin if cin is None else cin
+        dcs = dout.shape[-1]
+        dsrc = dout if dout_coff == 0 else dout[..., dout_coff:]
+        K.bn_backward(dsrc, dcs, self.z, self.cout, self.rows, self.cout, self.mean, self.rstd, ps.p[self.G],
+                      ps.p[self.B], self.scratch.bnws, ps.g[self.G], ps.g[self.B], relu=self.relu,
+                      y=y, ycs=y.shape[-1] if y is not None else 0, dx=self.dz, dxcs=self.cout, dz_out=dres)
+        count = self.cout * self.k * self.k * cin
+        maxs = max(1, min(MAX_SPLITS, self.scratch.part.numel() // count))
+        part, used = K.conv2d_wgrad_partials(self.dz, x, self.k, self.k, self.s, self.pad, cin=cin,
+                                             part=self.scratch.part[:maxs * count].view(maxs, self.cout,
+                                                                                        self.k * self.k * cin),
+                                             acct_flops=self.flops)
+        K.reduce_splits(part, used, count, ps.g[self.W])
+        if dx is not None:
+            wt = self.scratch.flip[:self.cout * self.k * self.k * cin].view(cin, self.k, self.k, self.cout)
+            K.weight_flip(ps.b[self.W], wt)
+            src = self.dz
+            if self.s == 2:
+                uh, uw = 2 * self.oh - 1, 2 * self.ow - 1
+                src = self.scratch.up[:self.n * uh * uw * self.cout].view(self.n, uh, uw, self.cout)
+                K.zero_upsample(self.dz, src)
+            K.conv2d_fwd(src, wt, 1, self.k - 1 - self.pad, out=dx, out_hw=(self.h, self.w),
+                         accumulate=dx_accumulate, acct_flops=self.flops)
+
+
+class Linear:
+    """y = x W^T + b with W [out_pad][in] (out padded to 16 so every TMA row stride is legal)."""
+
+    def __init__(self, ps: ParamStore, name, fin, fout, gen):
+        self.fin, self.fout, self.fpad = fin, fout, _pad16(fout)
+        bound = 1.0 / math.sqrt(fin)
+        w = torch.zeros(self.fpad, fin)
+        w[:fout] = _uniform(gen, (fout, fin), bound)
+        b = torch.zeros(self.fpad)
+        b[:fout] = _uniform(gen, (fout,), bound)
+        self.W = ps.add(f"{name}.w", w, logical=fout * fin)
+        self.Bn = ps.add(f"{name}.b", b, logical=fout)
+
+    def forward(self, ps, x, out, out_f32=False):
+        B = x.shape[0]
+        K.gemm(x, ps.b[self.W], B, self.fpad, self.fin, 0, 0, out=out, out_f32=out_f32, bias=ps.p[self.Bn])
+
+    def backward(self, ps, dy, x, dx=None):
+        B = x.shape[0]
+        K.gemm(dy, x, self.fpad, self.fin, B, 1, 1, out=ps.g[self.W], out_f32=True)
+        K.col_sum(dy, B, self.fpad, self.fpad, ps.g[self.Bn])
+        if dx is not None:
+            K.gemm(dy, ps.b[self.W], B, self.fin, self.fpad, 0, 1, out=dx)
+
+
+class Net:
+    """Common driver: loss head, Adam, buffers."""
+
+    num_classes = 10
+    in_channels = 3
+    image = 32
+
+    def __init__(self, seed=0):
+        self.gen = torch.Generator().manual_seed(seed)
+        self.ps = ParamStore()
+        self.scratch = Scratch()
+        self.lr, self.b1, self.b2, self.eps = 1e-3, 0.9, 0.999, 1e-8
+        self.grad_scale = 1.0
+
+    def build(self, batch, device="cuda", global_batch=None):
+        self.batch = batch
+        self.global_batch = global_batch or batch
+        self.device = device
+        self._build(batch, device)
+        self.scratch.finalize(device)
+        self.ps.finalize(device)
+        fpad = self.head.fpad
+        self.logits = torch.zeros(batch, fpad, dtype=F32, device=device)
+        self.dlogits = torch.zeros(batch, fpad, dtype=BF16, device=device)
+        self.row_loss = torch.zeros(batch, dtype=F32, device=device)
+        self.loss = torch.zeros(1, dtype=F32, device=device)
+        return self
+
+    def loss_and_grad(self, labels):
+        K.softmax_xent(self.logits, self.batch, self.num_classes, labels, 1.0 / self.global_batch, self.row_loss,
+                       self.loss, self.dlogits)
+
+    def step(self, x, labels, allreduce=None):
+        """One training step on a resident input tile (NHWC8 bf16) and int32 labels."""
+        self.forward(x)
+        self.loss_and_grad(labels)
+        self.backward(x)
+        if allreduce is not None:
+            allreduce(self.ps.g32)
+        self.optimizer_step()
+        return self.loss
+
+    def optimizer_step(self):
+        K.adam_step(self.ps.p32, self.ps.g32, self.ps.m, self.ps.v, self.ps.pb, self.lr, self.b1, self.b2, self.eps,
+                    step=0, grad_scale=self.grad_scale, step_dev=self.ps.step_dev, sched_dev=self.ps.sched)
+
+    @property
+    def num_params(self):
+        return self.ps.logical
+
+
+class SmallCNN(Net):
+    """Paper-shaped CIFAR CNN: [conv3x3-BN-ReLU]x2, maxpool, [conv3x3-BN-ReLU]x2, maxpool,
+    FC 4096-256 (ReLU), FC 256-10.  Input NHWC with channels padded 3 -> 8."""
+
+    def __init__(self, seed=0, num_classes=10):
+        super().__init__(seed)
+        self.num_classes = num_classes
+        ps, g = self.ps, self.gen
+        self.c1 = ConvBN(ps, "conv1", 8, 32, 3, 1, 1, g, cin_real=3, need_dgrad=False)
+        self.c2 = ConvBN(ps, "conv2", 32, 32, 3, 1, 1, g)
+        self.c3 = ConvBN(ps, "conv3", 32, 64, 3, 1, 1, g)
+        self.c4 = ConvBN(ps, "conv4", 64, 64, 3, 1, 1, g)
+        self.fc1 = Linear(ps, "fc1", 8 * 8 * 64, 256, g)
+        self.head = Linear(ps, "fc2", 256, num_classes, g)
+
+    def _build(self, n, dev):
+        S = self.scratch
+        e = lambda *s: torch.empty(*s, dtype=BF16, device=dev)  # noqa: E731
+        self.c1.build(n, 32, 32, S, dev)
+        self.c2.build(n, 32, 32, S, dev)
+        self.c3.build(n, 16, 16, S, dev)
+        self.c4.build(n, 16, 16, S, dev)
+        self.a1, self.a2, self.p1 = e(n, 32, 32, 32), e(n, 32, 32, 32), e(n, 16, 16, 32)
+        self.a3, self.a4, self.p2 = e(n, 16, 16, 64), e(n, 16, 16, 64), e(n, 8, 8, 64)
+        self.h = e(n, 256)
+        self.dh, self.dp2 = e(n, 256), e(n, 8, 8, 64)
+        self.da4, self.da3, self.dp1 = e(n, 16, 16, 64), e(n, 16, 16, 64), e(n, 16, 16, 32)
+        self.da2, self.da1 = e(n, 32, 32, 32), e(n, 32, 32, 32)
+
+    def forward(self, x):
+        ps = self.ps
+        self.c1.forward(ps, x, self.a1)
+        self.c2.forward(ps, self.a1, self.a2)
+        K.maxpool_fwd(self.a2, 2, 2, 0, self.p1)
+        self.c3.forward(ps, self.p1, self.a3)
+        self.c4.forward(ps, self.a3, self.a4)
+        K.maxpool_fwd(self.a4, 2, 2, 0, self.p2)
+        flat = self.p2.view(self.batch, -1)
+        self.fc1.forward(ps, flat, self.h)
+        K.relu_fwd(self.h)
+        self.head.forward(ps, self.h, self.logits, out_f32=True)
+
+    def backward(self, x):
+        ps = self.ps
+        flat = self.p2.view(self.batch, -1)
+        self.head.backward(ps, self.dlogits, self.h, self.dh)
+        K.relu_bwd(self.dh, self.h)
+        self.fc1.backward(ps, self.dh, flat, self.dp2.view(self.batch, -1))
+        K.maxpool_bwd(self.a4, self.dp2, 2, 2, 0, self.da4)
+        self.c4.backward(ps, self.da4, self.a3, dx=self.da3)
+        self.c3.backward(ps, self.da3, self.p1, dx=self.dp1)
+        K.maxpool_bwd(self.a2, self.dp1, 2, 2, 0, self.da2)
+        self.c2.backward(ps, self.da2, self.a1, dx=self.da1)
+        self.c1.backward(ps, self.da1, x, dx=None)
+
+
+class BasicBlock:
+    def __init__(self, ps, name, cin, cout, stride, gen):
+        self.c1 = ConvBN(ps, f"{name}.conv1", cin, cout, 3, stride, 1, gen, relu=True)
+        self.c2 = ConvBN(ps, f"{name}.conv2", cout, cout, 3, 1, 1, gen, relu=True)  # relu after residual add
+        self.down = None
+        if stride != 1 or cin != cout:
+            self.down = ConvBN(ps, f"{name}.down", cin, cout, 1, stride, 0, gen, relu=False)
+        self.cin, self.cout = cin, cout
+
+    def build(self, n, h, w, S, dev):
+        oh, ow = self.c1.build(n, h, w, S, dev)
+        self.c2.build(n, oh, ow, S, dev)
+        e = lambda *s: torch.empty(*s, dtype=BF16, device=dev)  # noqa: E731
+        self.o1, self.do1 = e(n, oh, ow, self.cout), e(n, oh, ow, self.cout)
+        self.dres = e(n, oh, ow, self.cout)
+        if self.down is not None:
+            self.down.build(n, h, w, S, dev)
+            self.sc = e(n, oh, ow, self.cout)
+        return oh, ow
+
+    def forward(self, ps, x, out):
+        self.c1.forward(ps, x, self.o1)
+        sc = x
+        if self.down is not None:
+            self.down.forward(ps, x, self.sc)
+            sc = self.sc
+        self.c2.forward(ps, self.o1, out, res=sc)
+
+    def backward(self, ps, dout, x, out, dx):
+        # out = relu(bn2(conv2(o1)) + sc): mask from `out`; the masked dout is the grad of sc
+        if self.down is not None:
+            self.c2.backward(ps, dout, self.o1, dx=self.do1, y=out, dres=self.dres)
+            self.down.backward(ps, self.dres, x, dx=dx)
+            self.c1.backward(ps, self.do1, x, dx=dx, dx_accumulate=True)
+        else:
+            # identity shortcut: dx = masked dout (written by bn backward) + dgrad(conv1)
+            self.c2.backward(ps, dout, self.o1, dx=self.do1, y=out, dres=dx)
+            self.c1.backward(ps, self.do1, x, dx=dx, dx_accumulate=True)
+
+
+class ResNet18(Net):
+    """ResNet-18 for 32x32 inputs (3x3 stem, no max-pool), BasicBlock x [2,2,2,2]."""
+
+    def __init__(self, seed=0, num_classes=10):
+        super().__init__(seed)
+        self.num_classes = num_classes
+        ps, g = self.ps, self.gen
+        self.stem = ConvBN(ps, "stem", 8, 64, 3, 1, 1, g, cin_real=3, need_dgrad=False)
+        cfg = [(64, 64, 1), (64, 64, 1), (64, 128, 2), (128, 128, 1), (128, 256, 2), (256, 256, 1),
+               (256, 512, 2), (512, 512, 1)]
+        self.blocks = [BasicBlock(ps, f"layer{i // 2 + 1}.{i % 2}", ci, co, s, g) for i, (ci, co, s) in enumerate(cfg)]
+        self.head = Linear(ps, "fc", 512, num_classes, g)
+
+    def _build(self, n, dev):
+        S = self.scratch
+        e = lambda *s: torch.empty(*s, dtype=BF16, device=dev)  # noqa: E731
+        self.stem.build(n, 32, 32, S, dev)
+        self.x0 = e(n, 32, 32, 64)
+        self.dx0 = e(n, 32, 32, 64)
+        h = w = 32
+        self.outs, self.douts = [], []
+        for b in self.blocks:
+            h, w = b.build(n, h, w, S, dev)
+            self.outs.append(e(n, h, w, b.cout))
+            self.douts.append(e(n, h, w, b.cout))
+        self.final_hw = h * w
+        self.pooled, self.dpooled = e(n, 512), e(n, 512)
+
+    def forward(self, x):
+        ps = self.ps
+        self.stem.forward(ps, x, self.x0)
+        cur = self.x0
+        for b, o in zip(self.blocks, self.outs):
+            b.forward(ps, cur, o)
+            cur = o
+        K.gap_fwd(cur, self.batch, self.final_hw, 512, 512, self.pooled)
+        self.head.forward(ps, self.pooled, self.logits, out_f32=True)
+
+    def backward(self, x):
+        ps = self.ps
+        self.head.backward(ps, self.dlogits, self.pooled, self.dpooled)
+        K.gap_bwd(self.dpooled, self.batch, self.final_hw, 512, self.douts[-1])
+        for i in range(len(self.blocks) - 1, -1, -1):
+            b = self.blocks[i]
+            xin = self.outs[i - 1] if i > 0 else self.x0
+            dxin = self.douts[i - 1] if i > 0 else self.dx0
+            b.backward(ps, self.douts[i], xin, self.outs[i], dxin)
+        self.stem.backward(ps, self.dx0, x, dx=None)
+
+
+MODELS = {"small_cnn": SmallCNN, "resnet18": ResNet18}
+
+
+def make_model(name, seed=0, **kw):
+    return MODELS[name](seed=seed, **kw)

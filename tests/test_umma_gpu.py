@@ -77,6 +77,31 @@ def test_conv_wgrad(n, h, w, cin, cout, k, s, p):
     _close(dw, wr.grad.permute(0, 2, 3, 1))
 
 
+@pytest.mark.parametrize("n,h,w,cin,cout,k,s,p", CONV_CASES)
+def test_conv_dgrad_via_flipped_conv(n, h, w, cin, cout, k, s, p):
+    """dgrad = stride-1 conv of dY (zero-upsampled for stride 2) with flipped weights."""
+    g = torch.Generator(device="cuda").manual_seed(11 + n + h + cin + cout)
+    wt = (torch.randn(cout, k, k, cin, device="cuda", generator=g) / (k * k * cin) ** 0.5).to(torch.bfloat16)
+    oh, ow = K.conv_out_hw(h, w, k, s, p)
+    dy = torch.randn(n, oh, ow, cout, device="cuda", generator=g).to(torch.bfloat16)
+    flip = torch.empty(cin, k, k, cout, device="cuda", dtype=torch.bfloat16)
+    K.weight_flip(wt, flip)
+    src = dy
+    if s == 2:
+        src = torch.empty(n, 2 * oh - 1, 2 * ow - 1, cout, device="cuda", dtype=torch.bfloat16)
+        K.zero_upsample(dy, src)
+    dx = torch.zeros(n, h, w, cin, device="cuda", dtype=torch.float32)
+    K.conv2d_fwd(src, flip, 1, k - 1 - p, out=dx, out_f32=True, out_hw=(h, w))
+    xr = torch.zeros(n, cin, h, w, device="cuda", requires_grad=True)
+    F.conv2d(xr, wt.permute(0, 3, 1, 2).float(), stride=s, padding=p).backward(dy.permute(0, 3, 1, 2).float())
+    _close(dx, xr.grad.permute(0, 2, 3, 1))
+    # accumulate mode adds onto the existing output
+    base = torch.randn(n, h, w, cin, device="cuda", generator=g)
+    acc = base.clone()
+    K.conv2d_fwd(src, flip, 1, k - 1 - p, out=acc, out_f32=True, out_hw=(h, w), accumulate=True)
+    _close(acc, base + xr.grad.permute(0, 2, 3, 1))
+
+
 @pytest.mark.parametrize("M,N,Kd,am,bm,splits", [
     (512, 256, 4096, 0, 0, 1), (512, 10, 256, 0, 0, 1), (512, 4096, 256, 0, 1, 1),
     (256, 4096, 512, 1, 1, 4), (10, 256, 512, 1, 1, 2), (300, 200, 136, 0, 0, 1),
