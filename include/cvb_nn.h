@@ -32,6 +32,10 @@ int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, int dycs, 
 int cvb_gemm(const void* a, int a_major, int64_t lda, const void* b, int b_major, int64_t ldb, int M, int N, int K,
              void* c, int64_t ldc, int c_f32, const float* bias, int splits, int accumulate, void* stream);
 int cvb_gemm_splits_used(int K, int splits);
+/* profiling aids (not on the hot path): raw tcgen05.mma issue rate; CTA-0 pipeline timeline
+ * of the last GEMM launched with CVB_GEMM_DBG=4 (5 x 4096 clock64 stamps) */
+long long cvb_debug_mma_cycles(int n_mma, int bn, int commit_every);
+int cvb_debug_trace(long long* host_out);
 
 /* ---- batch norm (+ReLU, +residual) --------------------------------------------------------- */
 int64_t cvb_bn_workspace_floats(int64_t rows, int C);
@@ -58,6 +62,9 @@ int cvb_softmax_xent(const float* logits, int B, int C, const int32_t* labels, f
                      float* loss_out, void* dlogits, int ldd, void* stream);
 int cvb_reduce_splits(const float* part, int splits, int64_t count, float* out, int accumulate, float scale,
                       void* stream);
+/* split-K epilogue of a dense layer: out[r][c] = act(sum_s part[s][r][c] + bias[c]) */
+int cvb_reduce_splits_act(const float* part, int splits, int rows, int cols, const float* bias, int relu, void* out,
+                          int out_f32, int64_t ldo, void* stream);
 int cvb_weight_flip(const void* w, int cout, int kh, int kw, int cin, void* wt, void* stream);
 int cvb_zero_upsample(const void* dy, int n, int oh, int ow, int C, int dycs, void* out, void* stream);
 int cvb_col_sum(const void* x, int is_f32, int64_t rows, int cols, int64_t ld, float* out, int accumulate, void* stream);

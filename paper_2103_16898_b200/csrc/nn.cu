@@ -62,13 +62,36 @@ __global__ void chan_stats_partial(const bf16* __restrict__ x, int64_t rows, int
   }
 }
 
-__global__ void bn_finalize(const float* __restrict__ part, int nblk, int C, double count, float eps,
+// Sum the [nblk][2][C] partials: block = 32 channels x 32 warps; warp w sums blocks w, w+32,
+// ... (coalesced across the 32 channels, independent loads), then a fixed-order smem
+// combine -> deterministic.
+constexpr int FIN_WARPS = 32;
+__device__ __forceinline__ void sum_partials(const float* __restrict__ part, int nblk, int C, int c, double& s,
+                                             double& q) {
+  __shared__ double sh[2][FIN_WARPS][32];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  double a = 0, b2 = 0;
+  if (c < C) {
+#pragma unroll 4
+    for (int b = w; b < nblk; b += FIN_WARPS) {
+      a += part[(int64_t)(2 * b) * C + c];
+      b2 += part[(int64_t)(2 * b + 1) * C + c];
+    }
+  }
+  sh[0][w][l] = a;
+  sh[1][w][l] = b2;
+  __syncthreads();
+  s = 0; q = 0;
+  for (int k = 0; k < FIN_WARPS; k++) { s += sh[0][k][l]; q += sh[1][k][l]; }
+}
+
+__global__ void __launch_bounds__(FIN_WARPS * 32) bn_finalize(const float* __restrict__ part, int nblk, int C, double count, float eps,
                             float* __restrict__ mean, float* __restrict__ rstd, float* __restrict__ run_mean,
                             float* __restrict__ run_var, float momentum) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  double s = 0, q = 0;
-  for (int b = 0; b < nblk; b++) { s += part[(int64_t)(2 * b) * C + c]; q += part[(int64_t)(2 * b + 1) * C + c]; }
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  double s, q;
+  sum_partials(part, nblk, C, c, s, q);
+  if (threadIdx.x >= 32 || c >= C) return;
   const double m = s / count;
   double var = q / count - m * m;
   if (var < 0) var = 0;
@@ -156,12 +179,12 @@ __global__ void bn_bwd_partial(const bf16* __restrict__ dy, int dycs, const bf16
   }
 }
 
-__global__ void bn_bwd_finalize(const float* __restrict__ part, int nblk, int C, float* __restrict__ dbeta,
+__global__ void __launch_bounds__(FIN_WARPS * 32) bn_bwd_finalize(const float* __restrict__ part, int nblk, int C, float* __restrict__ dbeta,
                                 float* __restrict__ dgamma) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  double s = 0, q = 0;
-  for (int b = 0; b < nblk; b++) { s += part[(int64_t)(2 * b) * C + c]; q += part[(int64_t)(2 * b + 1) * C + c]; }
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  double s, q;
+  sum_partials(part, nblk, C, c, s, q);
+  if (threadIdx.x >= 32 || c >= C) return;
   dbeta[c] = (float)s;
   dgamma[c] = (float)q;
 }
@@ -267,6 +290,38 @@ __global__ void maxpool_bwd(const bf16* __restrict__ x, const bf16* __restrict__
     }
   }
   store8(dx + pix * C + g * 8, acc);
+}
+
+// 2x2 / stride-2 windows do not overlap: one thread per output pixel and 8-channel group
+// routes dy to the window's first arg-max and writes zeros to the other three inputs.
+__global__ void maxpool2_bwd(const bf16* __restrict__ x, const bf16* __restrict__ dyp, int n, int h, int w, int C,
+                             int oh, int ow, bf16* __restrict__ dx) {
+  const int G = C / 8;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * oh * ow * G) return;
+  const int g = (int)(i % G);
+  const int64_t pix = i / G;
+  const int ox = (int)(pix % ow), oy = (int)((pix / ow) % oh), b = (int)(pix / ((int64_t)ow * oh));
+  float v[4][8], d[8];
+  int64_t base[4];
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    base[q] = (((int64_t)b * h + 2 * oy + (q >> 1)) * w + 2 * ox + (q & 1)) * C + g * 8;
+    load8(x + base[q], v[q]);
+  }
+  load8(dyp + pix * C + g * 8, d);
+  float o[4][8];
+#pragma unroll
+  for (int c = 0; c < 8; c++) {
+    int am = 0;
+    float m = v[0][c];
+#pragma unroll
+    for (int q = 1; q < 4; q++) if (v[q][c] > m) { m = v[q][c]; am = q; }
+#pragma unroll
+    for (int q = 0; q < 4; q++) o[q][c] = (q == am) ? d[c] : 0.f;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; q++) store8(dx + base[q], o[q]);
 }
 
 __global__ void avgpool_fwd(const bf16* __restrict__ x, int n, int h, int w, int C, int xcs, int k, int oh, int ow,
@@ -400,6 +455,22 @@ __global__ void reduce_splits(const float* __restrict__ part, int splits, int64_
   out[i] = accumulate ? out[i] + a : a;
 }
 
+// split-K epilogue of a dense layer: out[r][c] = act(sum_s part[s][r][c] + bias[c])
+__global__ void reduce_splits_act(const float* __restrict__ part, int splits, int rows, int cols,
+                                  const float* __restrict__ bias, int relu, void* __restrict__ out, int out_f32,
+                                  int64_t ldo) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t count = (int64_t)rows * cols;
+  if (i >= count) return;
+  const int r = (int)(i / cols), c = (int)(i - (int64_t)r * cols);
+  float a = 0.f;
+  for (int s = 0; s < splits; s++) a += part[s * count + i];
+  if (bias) a += bias[c];
+  if (relu) a = fmaxf(a, 0.f);
+  if (out_f32) reinterpret_cast<float*>(out)[(int64_t)r * ldo + c] = a;
+  else reinterpret_cast<bf16*>(out)[(int64_t)r * ldo + c] = __float2bfloat16_rn(a);
+}
+
 // wt[ci][kh'][kw'][co] = w[co][KH-1-kh'][KW-1-kw'][ci]
 __global__ void weight_flip(const bf16* __restrict__ w, int cout, int kh, int kw, int cin, bf16* __restrict__ wt) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -516,7 +587,7 @@ inline unsigned nblocks(int64_t n, int t = 256) { return (unsigned)((n + t - 1) 
 
 int stats_blocks(int64_t rows, int C, int64_t* rpb) {
   int nsm = cvb_num_sms();
-  int64_t target = (int64_t)nsm * 4;
+  int64_t target = (int64_t)nsm * 2;
   int64_t per = (rows + target - 1) / target;
   if (per < 64) per = 64;
   *rpb = per;
@@ -542,7 +613,8 @@ CVB_API int cvb_bn_stats(const void* x, int64_t rows, int C, int xcs, float* ws,
   int nb = stats_blocks(rows, C, &rpb);
   const int G = C / 8, RL = ST_THREADS / G;
   chan_stats_partial<<<nb, ST_THREADS, RL * G * 16 * sizeof(float), STREAM>>>((const bf16*)x, rows, C, xcs, rpb, ws);
-  bn_finalize<<<nblocks(C), 256, 0, STREAM>>>(ws, nb, C, (double)rows, eps, mean, rstd, run_mean, run_var, momentum);
+  bn_finalize<<<(C + 31) / 32, FIN_WARPS * 32, 0, STREAM>>>(ws, nb, C, (double)rows, eps, mean, rstd, run_mean,
+                                                             run_var, momentum);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
@@ -571,7 +643,7 @@ CVB_API int cvb_bn_backward(const void* dy, int dycs, const void* x, int xcs, co
   bn_bwd_partial<<<nb, ST_THREADS, RL * G * 16 * sizeof(float), STREAM>>>(
       (const bf16*)dy, dycs, (const bf16*)x, xcs, (const bf16*)y, ycs, rows, C, mean, rstd, gamma, beta, relu, rpb, ws,
       (bf16*)dz_out);
-  bn_bwd_finalize<<<nblocks(C), 256, 0, STREAM>>>(ws, nb, C, dbeta, dgamma);
+  bn_bwd_finalize<<<(C + 31) / 32, FIN_WARPS * 32, 0, STREAM>>>(ws, nb, C, dbeta, dgamma);
   if (dx || dx32)
     bn_bwd_apply<<<nblocks(rows * G), 256, 0, STREAM>>>((const bf16*)dy, dycs, (const bf16*)x, xcs, (const bf16*)y, ycs,
                                                         rows, C, mean, rstd, gamma, beta, relu, dbeta, dgamma, (bf16*)dx,
@@ -589,8 +661,12 @@ CVB_API int cvb_maxpool_fwd(const void* x, int n, int h, int w, int C, int k, in
 
 CVB_API int cvb_maxpool_bwd(const void* x, const void* dy, int n, int h, int w, int C, int k, int s, int p, int oh,
                             int ow, void* dx, void* stream) {
-  maxpool_bwd<<<nblocks((int64_t)n * h * w * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, (const bf16*)dy, n, h, w, C, k, s,
-                                                                         p, oh, ow, (bf16*)dx);
+  if (k == 2 && s == 2 && p == 0 && h == 2 * oh && w == 2 * ow)
+    maxpool2_bwd<<<nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, (const bf16*)dy, n, h, w,
+                                                                              C, oh, ow, (bf16*)dx);
+  else
+    maxpool_bwd<<<nblocks((int64_t)n * h * w * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, (const bf16*)dy, n, h, w, C,
+                                                                           k, s, p, oh, ow, (bf16*)dx);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
@@ -635,6 +711,14 @@ CVB_API int cvb_softmax_xent(const float* logits, int B, int C, const int32_t* l
 CVB_API int cvb_reduce_splits(const float* part, int splits, int64_t count, float* out, int accumulate, float scale,
                               void* stream) {
   reduce_splits<<<nblocks(count), 256, 0, STREAM>>>(part, splits, count, out, accumulate, scale);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_reduce_splits_act(const float* part, int splits, int rows, int cols, const float* bias, int relu,
+                                  void* out, int out_f32, int64_t ldo, void* stream) {
+  reduce_splits_act<<<nblocks((int64_t)rows * cols), 256, 0, STREAM>>>(part, splits, rows, cols, bias, relu, out, out_f32,
+                                                                      ldo);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }

@@ -8,11 +8,15 @@
 //   warp 0      TMA producer: per K-block, G boxes per operand, loaded straight from the
 //               NHWC activation (4-D tensor map; conv padding = TMA out-of-bounds zero
 //               fill) or from 2-D weight / dense maps, into a multi-stage smem ring.
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (kind::f16, bf16 in,
-//               fp32 accumulate in TMEM, 128 x BN tile, 4 MMAs of K=16 per 64-wide K-block),
-//               double-buffered accumulators so the epilogue of tile i overlaps tile i+1.
+//   warp 1      TMEM allocator + tcgen05.mma issuer (kind::f16, bf16 in, fp32 accumulate in
+//               TMEM, 128 x BN tile, 4 MMAs of K=16 per 64-wide K-block), double-buffered
+//               accumulators so the epilogue of tile i overlaps the MMAs of tile i+1.
 //   warps 2..5  epilogue: tcgen05.ld 32x32b -> bias -> bf16/fp32 -> global (NHWC rows,
 //               dense rows or fp32 split-K partials).
+// All per-K-block box coordinates and all UMMA smem descriptors are precomputed on the host
+// (box table + descriptor templates in the parameter bank), so the single-thread issue
+// loops are a handful of uniform instructions per TMA / MMA (measured: without this the
+// issue loops, not the tensor core, bounded the kernel).
 // Modes:
 //   FWD   A = gathered activation (K-major, K = taps x Cin), B = weights [Cout][K] (K-major).
 //         Used for conv forward and for dgrad (input dY or its zero-upsampled copy, weights
@@ -24,6 +28,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
+#include <stdlib.h>
 
 namespace {
 
@@ -33,19 +38,22 @@ enum { OUT_NHWC = 0, OUT_ROWS = 1, OUT_PARTIAL = 2 };
 constexpr int BM = 128;          // UMMA M (cta_group::1)
 constexpr int BK = 64;           // K elements per pipeline stage
 constexpr int NUM_THREADS = 192; // 6 warps
+constexpr int MAX_BOXES = 512;   // box-table entries
 
 struct GemmParams {
   CUtensorMap mapA[4];
   CUtensorMap mapB[4];
+  uint64_t adesc[4], bdesc[4];   // UMMA descriptor templates, start address relative to the stage
   int mode;
   int a_major, b_major;     // 0 = K-major, 1 = MN-major
-  int a_cel, b_cel;         // channels / elements per box row (8,16,32,64)
+  int a_cel, b_cel;         // elements per box row (8,16,32,64)
+  int ga, gb;               // boxes per stage (A, B)
+  uint32_t a_box_stride, b_box_stride;   // smem bytes between boxes
   int BN;
   int M, N;                 // logical GEMM extents (rows, cols)
   int m_tiles, n_tiles, splits;
   int num_kb;               // total K-blocks of the full K range
   int kb_per_split;
-  int a_box_rows;           // rows TMA writes per A box (FWD/DENSE-K: <=128)
   uint32_t tx_bytes;
   uint32_t idesc;
   int stages;
@@ -53,9 +61,6 @@ struct GemmParams {
   int tw, th, tn;           // pixel-box extents (FWD: the M tile; WGRAD: the K chunk)
   int ptiles_w, ptiles_h;   // tile counts along w, h of the pixel space
   int OH, OW, NIMG;         // pixel space (FWD: output; WGRAD: dY)
-  int KH, KW, pad, stride;  // gathered operand geometry
-  int cin;                  // channels of the gathered operand (padded, multiple of cel)
-  int ntaps;
   // epilogue
   int out_mode, out_f32;
   void* out;
@@ -64,7 +69,20 @@ struct GemmParams {
   const float* bias;
   int part_rows;            // OUT_PARTIAL: rows per split slab
   int accum;                // add into the existing output
+  int dbg;                  // profiling knobs: 1 = skip MMA, 2 = skip TMA (results invalid)
+  long long* trace;         // debug: clock64 timeline of CTA 0 (5 x 4096 slots) or null
+  int nbox;
+  uint32_t boxtab[MAX_BOXES];   // packed (map, channel, dw, dh) per gathered box
 };
+
+#define TRACE(type, idx)                                                                        \
+  do {                                                                                          \
+    if (p.trace && blockIdx.x == 0 && (idx) < 4096) p.trace[(type) * 4096 + (idx)] = clock64(); \
+  } while (0)
+
+__host__ __device__ inline uint32_t pack_box(int mi, int cc, int dw, int dh) {
+  return (uint32_t)mi | ((uint32_t)cc << 2) | ((uint32_t)(dw + 64) << 18) | ((uint32_t)(dh + 64) << 25);
+}
 
 // ---------------------------------------------------------------------------------------
 // PTX helpers
@@ -88,19 +106,29 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }
-__device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, void* dst, uint64_t* bar, int c0, int c1, int c2, int c3) {
+__device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, uint32_t dst, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
   asm volatile(
       "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];"
-      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)),
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)),
         "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
 }
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, void* dst, uint64_t* bar, int c0, int c1) {
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint32_t dst, uint64_t* bar, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
-      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1) : "memory");
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1) : "memory");
 }
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "elect.sync _|P1, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "+r"(pred));
+  return pred != 0;
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -115,46 +143,73 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint6
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+// 32 consecutive fp32 columns of this thread's TMEM lane; caller waits with tmem_wait()
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-
-// UMMA shared-memory descriptor (sm_100: version 1 at bits 46-47).
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)layout << 61;
-  return d;
-}
-__device__ __forceinline__ uint32_t layout_of(int rowbytes) {
-  return rowbytes == 128 ? 2u : rowbytes == 64 ? 4u : rowbytes == 32 ? 6u : 0u;
-}
-
-// Descriptor of MMA k-step s (16 K elements) of one operand stage.
-//   K-major : `rows` rows per box, boxes of cel K-elements at stride rows*R
-//   MN-major: boxes of cel MN-elements x 64 K-rows at stride 64*R
-__device__ __forceinline__ uint64_t operand_desc(uint32_t base, int major, int cel, int rows, int s) {
-  const int R = cel * 2;
-  if (major == 0) {
-    if (R == 16) return make_desc(base + 2 * s * rows * 16, rows * 16, 128, 0);
-    const int kb = 32 * s;  // byte offset of the k-step along K
-    return make_desc(base + (kb / R) * rows * R + (kb % R), 16, 8 * R, layout_of(R));
-  }
-  if (R == 16) return make_desc(base + s * 256, 128, 64 * 16, 0);
-  return make_desc(base + s * 16 * R, 64 * R, 8 * R, layout_of(R));
-}
+__device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------------------
 // The kernel
 // ---------------------------------------------------------------------------------------
+// Store 16 fp32 accumulator values of one output row (bias / accumulate / bf16 pack).
+__device__ __forceinline__ void store16(const GemmParams& p, int64_t off, int col, const uint32_t* r, bool has_k) {
+  float v[16];
+#pragma unroll
+  for (int j = 0; j < 16; j++) v[j] = has_k ? __uint_as_float(r[j]) : 0.f;
+  if (p.bias) {
+#pragma unroll
+    for (int j = 0; j < 16; j++) v[j] += (col + j < p.N) ? __ldg(p.bias + col + j) : 0.f;
+  }
+  const bool full = col + 16 <= p.N;
+  if (p.accum) {
+#pragma unroll
+    for (int j = 0; j < 16; j++)
+      if (full || col + j < p.N)
+        v[j] += p.out_f32 ? reinterpret_cast<const float*>(p.out)[off + j]
+                          : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.out)[off + j]);
+  }
+  if (full) {
+    if (p.out_f32) {
+      float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + off);
+#pragma unroll
+      for (int j = 0; j < 4; j++) d[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    } else {
+      uint32_t pk[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+        pk[j] = *reinterpret_cast<uint32_t*>(&h);
+      }
+      uint4* d = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + off);
+      d[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      d[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+      if (col + j < p.N) {
+        if (p.out_f32) reinterpret_cast<float*>(p.out)[off + j] = v[j];
+        else reinterpret_cast<__nv_bfloat16*>(p.out)[off + j] = __float2bfloat16_rn(v[j]);
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_constant__ GemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -184,128 +239,128 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const uint32_t smem0 = smem_u32(smem);
 
   const int units = p.m_tiles * p.n_tiles * p.splits;
 
+  // Role loops run on whole, converged warps; only the issuing instructions are predicated on
+  // one elected lane.  Stage / phase counters are incremental (no divisions in the loops).
   if (warp == 0) {
-    if (lane == 0) {
-      // ===================== TMA producer =====================
-      int it = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int mt = u % p.m_tiles, rest = u / p.m_tiles;
-        const int nt = rest % p.n_tiles, sp = rest / p.n_tiles;
-        const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
-        // FWD: tile mt is a pixel box of the output
-        int tw0 = 0, th0 = 0, tn0 = 0;
-        if (p.mode == MODE_FWD) {
-          tw0 = (mt % p.ptiles_w) * p.tw;
-          int r2 = mt / p.ptiles_w;
-          th0 = (r2 % p.ptiles_h) * p.th;
-          tn0 = (r2 / p.ptiles_h) * p.tn;
-        }
-        const int m0 = mt * BM, n0 = nt * p.BN;
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          const int s = it % p.stages;
-          const uint32_t ph = (it / p.stages) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], p.tx_bytes);
-          uint8_t* sa = smem + s * stage_bytes;
-          uint8_t* sb = sa + a_stage;
-          if (p.mode == MODE_FWD) {
-            const int ga = BK / p.a_cel;
-            for (int g = 0; g < ga; g++) {
-              const int k = kb * BK + g * p.a_cel;
-              const int tap = k / p.cin, ci = k - tap * p.cin;
-              int mi = 0, cw = tw0, ch = th0, cc = ci;
-              if (tap < p.ntaps) {
-                const int kh = tap / p.KW, kw = tap - kh * p.KW;
-                const int dh = kh - p.pad, dw = kw - p.pad;
-                if (p.stride == 1) { cw = tw0 + dw; ch = th0 + dh; }
-                else { mi = ((dh & 1) << 1) | (dw & 1); cw = tw0 + (dw >> 1); ch = th0 + (dh >> 1); }
-              } else {
-                cc = p.cin;  // fully out of bounds -> zeros
+    const bool leader = elect_one();
+    int s = 0;
+    uint32_t ph = 0;
+    int it = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int mt = u % p.m_tiles, rest = u / p.m_tiles;
+      const int nt = rest % p.n_tiles, sp = rest / p.n_tiles;
+      const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+      int tw0 = 0, th0 = 0, tn0 = 0;
+      if (p.mode == MODE_FWD) {
+        tw0 = (mt % p.ptiles_w) * p.tw;
+        const int r2 = mt / p.ptiles_w;
+        th0 = (r2 % p.ptiles_h) * p.th;
+        tn0 = (r2 / p.ptiles_h) * p.tn;
+      }
+      // WGRAD: K-block kb is a pixel box; walk it incrementally
+      int pw = 0, ph0 = 0, pn = 0;
+      if (p.mode == MODE_WGRAD) {
+        pw = (kb0 % p.ptiles_w) * p.tw;
+        const int r2 = kb0 / p.ptiles_w;
+        ph0 = (r2 % p.ptiles_h) * p.th;
+        pn = (r2 / p.ptiles_h) * p.tn;
+      }
+      const int m0 = mt * BM, n0 = nt * p.BN;
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        mbar_wait(&empty[s], ph ^ 1);
+        if (leader) {
+          TRACE(0, it);
+          const uint32_t sa = smem0 + s * stage_bytes, sb = sa + a_stage;
+          if (p.dbg & 2) {
+            mbar_arrive(&full[s]);
+          } else {
+            mbar_expect_tx(&full[s], p.tx_bytes);
+            if (p.mode == MODE_FWD) {
+              const uint32_t* tab = p.boxtab + kb * p.ga;
+              for (int g = 0; g < p.ga; g++) {
+                const uint32_t e = tab[g];
+                tma_load_4d(&p.mapA[e & 3], sa + g * p.a_box_stride, &full[s], (int)((e >> 2) & 0xFFFF),
+                            tw0 + (int)((e >> 18) & 127) - 64, th0 + (int)(e >> 25) - 64, tn0);
               }
-              tma_load_4d(&p.mapA[mi], sa + g * BM * p.a_cel * 2, &full[s], cc, cw, ch, tn0);
-            }
-            const int gb = BK / p.b_cel;
-            for (int g = 0; g < gb; g++)
-              tma_load_2d(&p.mapB[0], sb + g * p.BN * p.b_cel * 2, &full[s], kb * BK + g * p.b_cel, n0);
-          } else if (p.mode == MODE_WGRAD) {
-            // K chunk kb = a pixel box of the dY space
-            const int pw = (kb % p.ptiles_w) * p.tw;
-            const int r2 = kb / p.ptiles_w;
-            const int ph0 = (r2 % p.ptiles_h) * p.th;
-            const int pn = (r2 / p.ptiles_h) * p.tn;
-            const int ga = BM / p.a_cel;
-            for (int b = 0; b < ga; b++)
-              tma_load_4d(&p.mapA[0], sa + b * BK * p.a_cel * 2, &full[s], m0 + b * p.a_cel, pw, ph0, pn);
-            const int gb = p.BN / p.b_cel;
-            for (int j = 0; j < gb; j++) {
-              const int col = n0 + j * p.b_cel;
-              const int tap = col / p.cin, ci = col - tap * p.cin;
-              int mi = 0, cw = pw, ch = ph0, cc = ci;
-              if (tap < p.ntaps) {
-                const int kh = tap / p.KW, kw = tap - kh * p.KW;
-                const int dh = kh - p.pad, dw = kw - p.pad;
-                if (p.stride == 1) { cw = pw + dw; ch = ph0 + dh; }
-                else { mi = ((dh & 1) << 1) | (dw & 1); cw = pw + (dw >> 1); ch = ph0 + (dh >> 1); }
-              } else {
-                cc = p.cin;
+              for (int g = 0; g < p.gb; g++)
+                tma_load_2d(&p.mapB[0], sb + g * p.b_box_stride, &full[s], kb * BK + g * p.b_cel, n0);
+            } else if (p.mode == MODE_WGRAD) {
+              for (int b = 0; b < p.ga; b++)
+                tma_load_4d(&p.mapA[0], sa + b * p.a_box_stride, &full[s], m0 + b * p.a_cel, pw, ph0, pn);
+              const uint32_t* tab = p.boxtab + nt * p.gb;
+              for (int j = 0; j < p.gb; j++) {
+                const uint32_t e = tab[j];
+                tma_load_4d(&p.mapB[e & 3], sb + j * p.b_box_stride, &full[s], (int)((e >> 2) & 0xFFFF),
+                            pw + (int)((e >> 18) & 127) - 64, ph0 + (int)(e >> 25) - 64, pn);
               }
-              tma_load_4d(&p.mapB[mi], sb + j * BK * p.b_cel * 2, &full[s], cc, cw, ch, pn);
-            }
-          } else {  // DENSE
-            if (p.a_major == 0) {
-              for (int g = 0; g < BK / p.a_cel; g++)
-                tma_load_2d(&p.mapA[0], sa + g * BM * p.a_cel * 2, &full[s], kb * BK + g * p.a_cel, m0);
-            } else {
-              for (int b = 0; b < BM / p.a_cel; b++)
-                tma_load_2d(&p.mapA[0], sa + b * BK * p.a_cel * 2, &full[s], m0 + b * p.a_cel, kb * BK);
-            }
-            if (p.b_major == 0) {
-              for (int g = 0; g < BK / p.b_cel; g++)
-                tma_load_2d(&p.mapB[0], sb + g * p.BN * p.b_cel * 2, &full[s], kb * BK + g * p.b_cel, n0);
-            } else {
-              for (int j = 0; j < p.BN / p.b_cel; j++)
-                tma_load_2d(&p.mapB[0], sb + j * BK * p.b_cel * 2, &full[s], n0 + j * p.b_cel, kb * BK);
+            } else {  // DENSE
+              for (int g = 0; g < p.ga; g++) {
+                if (p.a_major == 0) tma_load_2d(&p.mapA[0], sa + g * p.a_box_stride, &full[s], kb * BK + g * p.a_cel, m0);
+                else tma_load_2d(&p.mapA[0], sa + g * p.a_box_stride, &full[s], m0 + g * p.a_cel, kb * BK);
+              }
+              for (int g = 0; g < p.gb; g++) {
+                if (p.b_major == 0) tma_load_2d(&p.mapB[0], sb + g * p.b_box_stride, &full[s], kb * BK + g * p.b_cel, n0);
+                else tma_load_2d(&p.mapB[0], sb + g * p.b_box_stride, &full[s], n0 + g * p.b_cel, kb * BK);
+              }
             }
           }
         }
+        __syncwarp();
+        if (p.mode == MODE_WGRAD) {
+          pw += p.tw;
+          if (pw >= p.ptiles_w * p.tw) {
+            pw = 0;
+            ph0 += p.th;
+            if (ph0 >= p.ptiles_h * p.th) { ph0 = 0; pn += p.tn; }
+          }
+        }
+        if (++s == p.stages) { s = 0; ph ^= 1; }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===================== MMA issuer =====================
-      int it = 0, lt = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
-        const int sp = u / (p.m_tiles * p.n_tiles);
-        const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
-        const int acc = lt & 1;
-        mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+    const bool leader = elect_one();
+    int s = 0;
+    uint32_t ph = 0;
+    int it = 0, lt = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
+      const int sp = u / (p.m_tiles * p.n_tiles);
+      const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+      const int acc = lt & 1;
+      mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t tmem_d = tmem_base + acc * p.BN;
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        mbar_wait(&full[s], ph);
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * p.BN;
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          const int s = it % p.stages;
-          const uint32_t ph = (it / p.stages) & 1;
-          mbar_wait(&full[s], ph);
-          tc_fence_after();
-          const uint32_t sa = smem_u32(smem + s * stage_bytes);
-          const uint32_t sb = sa + a_stage;
+        if (leader) {
+          TRACE(1, it);
+          if (p.dbg & 1) {
+            mbar_arrive(&empty[s]);
+          } else {
+            const uint64_t sa = (smem0 + s * stage_bytes) >> 4, sb = sa + (a_stage >> 4);
 #pragma unroll
-          for (int k = 0; k < BK / 16; k++) {
-            uint64_t ad = operand_desc(sa, p.a_major, p.a_cel, BM, k);
-            uint64_t bd = operand_desc(sb, p.b_major, p.b_cel, p.BN, k);
-            umma_bf16(tmem_d, ad, bd, p.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < BK / 16; k++)
+              umma_bf16(tmem_d, p.adesc[k] + sa, p.bdesc[k] + sb, p.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            umma_commit(&empty[s]);
           }
-          umma_commit(&empty[s]);
+          TRACE(2, it);
         }
-        umma_commit(&tfull[acc]);
+        __syncwarp();
+        if (++s == p.stages) { s = 0; ph ^= 1; }
       }
+      if (leader) umma_commit(&tfull[acc]);
+      __syncwarp();
     }
   } else {
     // ===================== epilogue (warps 2..5) =====================
     const int quarter = warp & 3;              // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;       // accumulator row (0..127)
+    // row -> pixel offsets inside an NHWC M-tile (constant over tiles)
+    const int wb = row % p.tw, r2 = row / p.tw, hb = r2 % p.th, nb = r2 / p.th;
     int lt = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
       const int mt = u % p.m_tiles, rest = u / p.m_tiles;
@@ -313,12 +368,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
       const int acc = lt & 1;
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      if (warp == 2 && lane == 0) TRACE(3, lt);
       tc_fence_after();
-      // destination row
       bool valid = true;
       int64_t dst_row = 0;
       if (p.out_mode == OUT_NHWC) {
-        const int wb = row % p.tw, r2 = row / p.tw, hb = r2 % p.th, nb = r2 / p.th;
         const int ow = (mt % p.ptiles_w) * p.tw + wb;
         const int q = mt / p.ptiles_w;
         const int oh = (q % p.ptiles_h) * p.th + hb;
@@ -336,49 +390,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       }
       const bool has_k = kb1 > kb0;
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * p.BN;
-      for (int c = 0; c < p.BN; c += 16) {
+      const int64_t rowoff = dst_row * p.ldc + p.col_off + nt * p.BN;
+      int c = 0;
+      for (; c + 32 <= p.BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tbase + c, r);
+        tmem_wait();
+        if (valid) {
+          store16(p, rowoff + c, nt * p.BN + c, r, has_k);
+          store16(p, rowoff + c + 16, nt * p.BN + c + 16, r + 16, has_k);
+        }
+      }
+      if (c < p.BN) {
         uint32_t r[16];
         tmem_ld16(tbase + c, r);
-        const int col = nt * p.BN + c;
-        if (!valid) continue;
-        float v[16];
-#pragma unroll
-        for (int j = 0; j < 16; j++) {
-          v[j] = has_k ? __uint_as_float(r[j]) : 0.f;
-          if (p.bias && col + j < p.N) v[j] += p.bias[col + j];
-        }
-        const int64_t off = dst_row * p.ldc + p.col_off + col;
-        if (p.accum) {   // out += result (residual / concat gradient accumulation)
-          for (int j = 0; j < 16 && col + j < p.N; j++)
-            v[j] += p.out_f32 ? reinterpret_cast<const float*>(p.out)[off + j]
-                              : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.out)[off + j]);
-        }
-        if (col + 16 <= p.N) {
-          if (p.out_f32) {
-            float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + off);
-#pragma unroll
-            for (int j = 0; j < 4; j++) d[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          } else {
-            uint32_t pk[8];
-#pragma unroll
-            for (int j = 0; j < 8; j++) {
-              __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
-              pk[j] = *reinterpret_cast<uint32_t*>(&h);
-            }
-            uint4* d = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + off);
-            d[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            d[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-          }
-        } else {
-          for (int j = 0; j < 16 && col + j < p.N; j++) {
-            if (p.out_f32) reinterpret_cast<float*>(p.out)[off + j] = v[j];
-            else reinterpret_cast<__nv_bfloat16*>(p.out)[off + j] = __float2bfloat16_rn(v[j]);
-          }
-        }
+        tmem_wait();
+        if (valid) store16(p, rowoff + c, nt * p.BN + c, r, has_k);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (warp == 2 && lane == 0) TRACE(4, lt);
     }
   }
   __syncwarp();
@@ -390,7 +422,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
 }
 
 // ---------------------------------------------------------------------------------------
-// Host side: tensor maps and launch planning
+// Host side: tensor maps, descriptor templates, box tables, launch planning
 // ---------------------------------------------------------------------------------------
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
@@ -474,14 +506,58 @@ uint32_t make_idesc(int a_major, int b_major, int bn) {
   return d;
 }
 
+// UMMA shared-memory descriptor (sm_100: version 1 at bits 46-47); start address relative.
+uint64_t desc_tmpl(uint32_t rel_addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((rel_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)layout << 61;
+  return d;
+}
+uint32_t layout_of(int rowbytes) { return rowbytes == 128 ? 2u : rowbytes == 64 ? 4u : rowbytes == 32 ? 6u : 0u; }
+
+// Descriptor template of MMA k-step s (16 K elements) of one operand stage.
+//   K-major : `rows` rows per box, boxes of cel K-elements at stride rows*R
+//   MN-major: boxes of cel MN-elements x 64 K-rows at stride 64*R
+uint64_t operand_desc(int major, int cel, int rows, int s) {
+  const int R = cel * 2;
+  if (major == 0) {
+    if (R == 16) return desc_tmpl(2 * s * rows * 16, rows * 16, 128, 0);
+    const int kb = 32 * s;
+    return desc_tmpl((kb / R) * rows * R + (kb % R), 16, 8 * R, layout_of(R));
+  }
+  if (R == 16) return desc_tmpl(s * 256, 128, 64 * 16, 0);
+  return desc_tmpl(s * 16 * R, 64 * R, 8 * R, layout_of(R));
+}
+
 int g_num_sms = 0;
 bool g_attr_done = false;
+long long* g_trace = nullptr;
 
 int launch(GemmParams& p, cudaStream_t stream) {
   if (!g_num_sms) g_num_sms = cvb_num_sms();
   const uint32_t stage_bytes = (BM + p.BN) * BK * 2;
   p.stages = (int)((200u * 1024u) / stage_bytes);
   if (p.stages > 8) p.stages = 8;
+  static int env_stages = -1, env_dbg = -1;
+  if (env_stages < 0) {
+    const char* e = getenv("CVB_STAGES");
+    env_stages = e ? atoi(e) : 0;
+    const char* d = getenv("CVB_GEMM_DBG");
+    env_dbg = d ? atoi(d) : 0;
+  }
+  if (env_stages > 0 && env_stages < p.stages) p.stages = env_stages;
+  p.dbg = env_dbg;
+  p.trace = nullptr;
+  if (env_dbg & 4) {
+    static long long* tr = nullptr;
+    if (!tr) cudaMalloc(&tr, 5 * 4096 * sizeof(long long));
+    cudaMemsetAsync(tr, 0, 5 * 4096 * sizeof(long long), stream);
+    p.trace = tr;
+    g_trace = tr;
+  }
   if (p.stages < 2) { cvb_set_error("BN too large"); return CVB_EINVAL; }
   size_t smem = (size_t)p.stages * stage_bytes + 1024 + 256;
   if (!g_attr_done) {
@@ -489,6 +565,13 @@ int launch(GemmParams& p, cudaStream_t stream) {
     g_attr_done = true;
   }
   p.idesc = make_idesc(p.a_major, p.b_major, p.BN);
+  // smem box strides and descriptor templates
+  p.a_box_stride = p.a_major == 0 ? BM * p.a_cel * 2 : BK * p.a_cel * 2;
+  p.b_box_stride = p.b_major == 0 ? p.BN * p.b_cel * 2 : BK * p.b_cel * 2;
+  for (int k = 0; k < 4; k++) {
+    p.adesc[k] = operand_desc(p.a_major, p.a_cel, BM, k);
+    p.bdesc[k] = operand_desc(p.b_major, p.b_cel, p.BN, k);
+  }
   const int units = p.m_tiles * p.n_tiles * p.splits;
   const int grid = units < g_num_sms ? units : g_num_sms;
   umma_gemm_kernel<<<grid, NUM_THREADS, smem, stream>>>(p);
@@ -498,10 +581,8 @@ int launch(GemmParams& p, cudaStream_t stream) {
 
 int pick_bn(int n) {
   if (n <= 256) return (n + 15) / 16 * 16;
-  // split N into near-equal tiles that are multiples of 16 and <= 256
   int tiles = (n + 255) / 256;
-  int bn = ((n + tiles - 1) / tiles + 15) / 16 * 16;
-  return bn;
+  return ((n + tiles - 1) / tiles + 15) / 16 * 16;
 }
 
 // pixel box for an M tile of 128 output rows
@@ -520,14 +601,24 @@ void pick_mbox(int n, int oh, int ow, int& bw, int& bh, int& bn) {
   bn = 1;
 }
 
-int next_pow2(int x) { int p = 1; while (p < x) p <<= 1; return p; }
+int next_pow2(int x) { int q = 1; while (q < x) q <<= 1; return q; }
 
 // pixel box for a 64-pixel K chunk (wgrad): exact 64 rows, OOB rows zero-filled by TMA
-void pick_kbox(int n, int oh, int ow, int& bw, int& bh, int& bn) {
-  bw = min(64, next_pow2(ow));
-  bh = min(64 / bw, next_pow2(oh));
+void pick_kbox(int oh, int ow, int& bw, int& bh, int& bn) {
+  bw = next_pow2(ow) < 64 ? next_pow2(ow) : 64;
+  bh = 64 / bw < next_pow2(oh) ? 64 / bw : next_pow2(oh);
   bn = 64 / (bw * bh);
-  (void)n;
+}
+
+// gathered-operand box: tap -> (parity map, dw, dh) for the conv geometry
+uint32_t gather_entry(int k_elem, int cin, int ntaps, int KW, int pad, int stride) {
+  const int tap = k_elem / cin, ci = k_elem - tap * cin;
+  if (tap >= ntaps) return pack_box(0, cin, 0, 0);   // fully out of bounds -> zeros
+  const int kh = tap / KW, kw = tap - kh * KW;
+  const int dh = kh - pad, dw = kw - pad;
+  if (stride == 1) return pack_box(0, ci, dw, dh);
+  const int mi = ((dh & 1) << 1) | (dw & 1);
+  return pack_box(mi, ci, dw >> 1, dh >> 1);
 }
 
 }  // namespace
@@ -546,13 +637,15 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
   if (get_encoder()) return CVB_ECUDA;
   const int acel = pick_cel(cin);
   if (!acel || (stride != 1 && stride != 2) || cout % 8) { cvb_set_error("conv2d_fwd: unsupported shape"); return CVB_EINVAL; }
-  GemmParams p;
+  static GemmParams p;   // large (boxes table): keep off the stack
   memset(&p, 0, sizeof(p));
   p.mode = MODE_FWD;
   p.a_major = 0; p.b_major = 0;
   p.a_cel = acel;
   const int K = kh * kw * cin;
   p.b_cel = 64;   // weights [cout][K]: 128-byte rows, K tail zero-filled by TMA
+  p.ga = BK / p.a_cel;
+  p.gb = BK / p.b_cel;
   p.BN = pick_bn(cout);
   p.M = n * oh * ow;
   p.N = cout;
@@ -567,11 +660,11 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
   p.splits = 1;
   p.num_kb = (K + BK - 1) / BK;
   p.kb_per_split = p.num_kb;
-  p.a_box_rows = bw * bh * bnn;
   p.OH = oh; p.OW = ow; p.NIMG = n;
-  p.KH = kh; p.KW = kw; p.pad = pad; p.stride = stride;
-  p.cin = cin; p.ntaps = kh * kw;
-  p.tx_bytes = (BK / p.a_cel) * p.a_box_rows * p.a_cel * 2 + (BK / p.b_cel) * p.BN * p.b_cel * 2;
+  p.nbox = p.num_kb * p.ga;
+  if (p.nbox > MAX_BOXES) { cvb_set_error("conv2d_fwd: K too large for the box table"); return CVB_EINVAL; }
+  for (int i = 0; i < p.nbox; i++) p.boxtab[i] = gather_entry((i / p.ga) * BK + (i % p.ga) * acel, cin, kh * kw, kw, pad, stride);
+  p.tx_bytes = p.ga * bw * bh * bnn * p.a_cel * 2 + p.gb * p.BN * p.b_cel * 2;
   int rc;
   if (stride == 1) {
     if ((rc = encode_nhwc(&p.mapA[0], x, n, h, w, cin, xcs, acel, bw, bh, bnn))) return rc;
@@ -595,20 +688,21 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
   if (get_encoder()) return CVB_ECUDA;
   const int acel = pick_cel(cout), bcel = pick_cel(cin);
   if (!acel || !bcel || (stride != 1 && stride != 2)) { cvb_set_error("conv2d_wgrad: unsupported shape"); return CVB_EINVAL; }
-  GemmParams p;
+  static GemmParams p;
   memset(&p, 0, sizeof(p));
   p.mode = MODE_WGRAD;
   p.a_major = 1; p.b_major = 1;
   p.a_cel = acel; p.b_cel = bcel;
   const int Ncols = kh * kw * cin;
   int bn = pick_bn(Ncols);
-  // an N tile must be a whole number of B boxes
-  bn = (bn + bcel - 1) / bcel * bcel;
+  bn = (bn + bcel - 1) / bcel * bcel;      // an N tile is a whole number of B boxes
   if (bn > 256) bn = 256 / bcel * bcel;
   p.BN = bn;
+  p.ga = BM / p.a_cel;
+  p.gb = p.BN / p.b_cel;
   p.M = cout; p.N = Ncols;
   int bw, bh, bnn;
-  pick_kbox(n, oh, ow, bw, bh, bnn);
+  pick_kbox(oh, ow, bw, bh, bnn);
   p.tw = bw; p.th = bh; p.tn = bnn;
   p.ptiles_w = (ow + bw - 1) / bw;
   p.ptiles_h = (oh + bh - 1) / bh;
@@ -626,9 +720,10 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
   splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
   p.splits = splits;
   p.OH = oh; p.OW = ow; p.NIMG = n;
-  p.KH = kh; p.KW = kw; p.pad = pad; p.stride = stride;
-  p.cin = cin; p.ntaps = kh * kw;
-  p.tx_bytes = (BM / acel) * BK * acel * 2 + (p.BN / bcel) * BK * bcel * 2;
+  p.nbox = p.n_tiles * p.gb;
+  if (p.nbox > MAX_BOXES) { cvb_set_error("conv2d_wgrad: N too large for the box table"); return CVB_EINVAL; }
+  for (int i = 0; i < p.nbox; i++) p.boxtab[i] = gather_entry(i * bcel, cin, kh * kw, kw, pad, stride);
+  p.tx_bytes = p.ga * BK * acel * 2 + p.gb * BK * bcel * 2;
   int rc;
   if ((rc = encode_nhwc(&p.mapA[0], dy, n, oh, ow, cout, dycs, acel, bw, bh, bnn))) return rc;
   if (stride == 1) {
@@ -651,16 +746,18 @@ CVB_API int cvb_gemm(const void* a, int a_major, int64_t lda, const void* b, int
                      int K, void* c, int64_t ldc, int c_f32, const float* bias, int splits, int accumulate,
                      void* stream) {
   if (get_encoder()) return CVB_ECUDA;
-  GemmParams p;
+  static GemmParams p;
   memset(&p, 0, sizeof(p));
   p.mode = MODE_DENSE;
   p.a_major = a_major; p.b_major = b_major;
   p.a_cel = 64; p.b_cel = 64;
   if (K % 8 || (a_major && M % 8) || (b_major && N % 8)) { cvb_set_error("gemm: unsupported shape"); return CVB_EINVAL; }
-  if (a_major == 0) p.a_cel = pick_cel(K) ? min(64, pick_cel(K)) : 8;
-  if (b_major == 0) p.b_cel = pick_cel(K) ? min(64, pick_cel(K)) : 8;
+  if (a_major == 0) p.a_cel = pick_cel(K) ? (pick_cel(K) < 64 ? pick_cel(K) : 64) : 8;
+  if (b_major == 0) p.b_cel = pick_cel(K) ? (pick_cel(K) < 64 ? pick_cel(K) : 64) : 8;
   p.BN = pick_bn(N);
   if (b_major == 1) { p.BN = (p.BN + 63) / 64 * 64; if (p.BN > 256) p.BN = 256; }
+  p.ga = a_major == 0 ? BK / p.a_cel : BM / p.a_cel;
+  p.gb = b_major == 0 ? BK / p.b_cel : p.BN / p.b_cel;
   p.M = M; p.N = N;
   p.m_tiles = (M + BM - 1) / BM;
   p.n_tiles = (N + p.BN - 1) / p.BN;
@@ -669,18 +766,78 @@ CVB_API int cvb_gemm(const void* a, int a_major, int64_t lda, const void* b, int
   if (splits > p.num_kb) splits = p.num_kb;
   p.kb_per_split = (p.num_kb + splits - 1) / splits;
   p.splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
+  p.tw = 1; p.th = 1; p.tn = 1; p.ptiles_w = 1; p.ptiles_h = 1;
   int rc;
   if (a_major == 0) { if ((rc = encode_2d(&p.mapA[0], a, M, K, lda, p.a_cel, BM))) return rc; }
   else { if ((rc = encode_2d(&p.mapA[0], a, K, M, lda, p.a_cel, BK))) return rc; }
   if (b_major == 0) { if ((rc = encode_2d(&p.mapB[0], b, N, K, ldb, p.b_cel, p.BN))) return rc; }
   else { if ((rc = encode_2d(&p.mapB[0], b, K, N, ldb, p.b_cel, BK))) return rc; }
-  p.tx_bytes = (a_major == 0 ? (BK / p.a_cel) * BM * p.a_cel * 2 : (BM / p.a_cel) * BK * p.a_cel * 2) +
-               (b_major == 0 ? (BK / p.b_cel) * p.BN * p.b_cel * 2 : (p.BN / p.b_cel) * BK * p.b_cel * 2);
+  p.tx_bytes = (a_major == 0 ? p.ga * BM * p.a_cel * 2 : p.ga * BK * p.a_cel * 2) +
+               (b_major == 0 ? p.gb * p.BN * p.b_cel * 2 : p.gb * BK * p.b_cel * 2);
   if (p.splits > 1) { p.out_mode = OUT_PARTIAL; p.out_f32 = 1; p.part_rows = M; }
   else { p.out_mode = OUT_ROWS; p.out_f32 = c_f32; }
   p.out = c; p.ldc = ldc; p.bias = p.splits > 1 ? nullptr : bias;
   p.accum = p.splits > 1 ? 0 : accumulate;
   return launch(p, (cudaStream_t)stream);
+}
+
+// ---- microbenchmark of the raw tcgen05.mma issue rate (debug aid, not on the hot path) ---
+__global__ void __launch_bounds__(128, 1) mma_rate_kernel(int n_mma, int bn, int commit_every, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&slot)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (warp == 0) {
+    const bool leader = elect_one();
+    const uint64_t sa = smem_u32(smem) >> 4, sb = sa + (16384 >> 4);
+    const uint64_t d0 = (uint64_t)1 | ((uint64_t)64 << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(bn >> 3) << 17) | (8u << 24);
+    long long t0 = clock64();
+    int phase = 0;
+    for (int i = 0; i < n_mma; i++) {
+      if (leader) {
+        umma_bf16(tmem, d0 + sa + (i & 3) * 2, d0 + sb + (i & 3) * 2, idesc, 1u);
+        if (commit_every && (i % commit_every) == commit_every - 1) umma_commit(&bar);
+      }
+      __syncwarp();
+      if (commit_every && (i % commit_every) == commit_every - 1) { mbar_wait(&bar, phase); phase ^= 1; }
+    }
+    if (leader) umma_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, phase);
+    long long t1 = clock64();
+    if (leader) *out = t1 - t0;
+  }
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
+CVB_API long long cvb_debug_mma_cycles(int n_mma, int bn, int commit_every) {
+  long long* d = nullptr;
+  long long h = -1;
+  cudaMalloc(&d, 8);
+  cudaFuncSetAttribute(mma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  mma_rate_kernel<<<1, 128, 64 * 1024>>>(n_mma, bn, commit_every, d);
+  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return h;
+}
+
+CVB_API int cvb_debug_trace(long long* host_out) {
+  if (!g_trace) return -1;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host_out, g_trace, 5 * 4096 * sizeof(long long), cudaMemcpyDeviceToHost);
+  return 0;
 }
 
 CVB_API int cvb_gemm_splits_used(int K, int splits) {

@@ -119,6 +119,10 @@ def conv2d_wgrad_partials(dy, x, kh, kw, stride, pad, cin=None, max_splits=148, 
     return part, used.value
 
 
+def splits_used(K, splits):
+    return _lib_bound().cvb_gemm_splits_used(K, splits)
+
+
 def gemm(a, b, M, N, K, a_major=0, b_major=0, out=None, out_f32=False, bias=None, splits=1, accumulate=False,
          acct_flops=None):
     """C[M,N] = sum_k A(m,k) B(n,k) with A [M,K] (a_major 0) or [K,M] (1), B [N,K] (0) or [K,N] (1)."""
@@ -237,6 +241,14 @@ def reduce_splits(part, splits, count, out, accumulate=False, scale=1.0):
     rc = _lib_bound().cvb_reduce_splits(part.data_ptr(), splits, count, out.data_ptr(), int(accumulate), scale, _stream())
     REC.end(tok)
     _lib.check(rc, "reduce_splits")
+
+
+def reduce_splits_act(part, splits, rows, cols, out, bias=None, relu=False):
+    tok = REC.begin(1, "reduce", 0, (splits * 4 + out.element_size()) * rows * cols)
+    rc = _lib_bound().cvb_reduce_splits_act(part.data_ptr(), splits, rows, cols, _ptr(bias), int(relu), out.data_ptr(),
+                                            int(out.dtype == F32), out.stride(0), _stream())
+    REC.end(tok)
+    _lib.check(rc, "reduce_splits_act")
 
 
 def weight_flip(w, wt):

@@ -184,16 +184,47 @@ class Linear:
         self.W = ps.add(f"{name}.w", w, logical=fout * fin)
         self.Bn = ps.add(f"{name}.b", b, logical=fout)
 
-    def forward(self, ps, x, out, out_f32=False):
+    @staticmethod
+    def _splits(M, N, Kd, bn_cap=256):
+        """split-K factor so that the (m, n, split) work units cover the 148 SMs."""
+        tiles = -(-M // 128) * -(-N // min(bn_cap, _pad16(N)))
+        return max(1, min(-(-Kd // 64), 148 // max(1, tiles)))
+
+    def build(self, batch, scratch):
+        B = batch
+        self.s_fwd = self._splits(B, self.fpad, self.fin)
+        self.s_wg = self._splits(self.fpad, self.fin, B)
+        need = max(self.s_fwd * B * self.fpad, self.s_wg * self.fpad * self.fin if self.s_wg > 1 else 0)
+        scratch.part_floats = max(scratch.part_floats, need)
+        self.scratch = scratch
+
+    def forward(self, ps, x, out, out_f32=False, relu=False):
         B = x.shape[0]
-        K.gemm(x, ps.b[self.W], B, self.fpad, self.fin, 0, 0, out=out, out_f32=out_f32, bias=ps.p[self.Bn])
+        fl = 2 * B * self.fout * self.fin
+        if self.s_fwd > 1:
+            part = self.scratch.part[:self.s_fwd * B * self.fpad].view(self.s_fwd, B, self.fpad)
+            K.gemm(x, ps.b[self.W], B, self.fpad, self.fin, 0, 0, out=part, splits=self.s_fwd, acct_flops=fl)
+            used = K.splits_used(self.fin, self.s_fwd)
+            K.reduce_splits_act(part, used, B, self.fpad, out, bias=ps.p[self.Bn], relu=relu)
+        else:
+            K.gemm(x, ps.b[self.W], B, self.fpad, self.fin, 0, 0, out=out, out_f32=out_f32, bias=ps.p[self.Bn],
+                   acct_flops=fl)
+            if relu:
+                K.relu_fwd(out)
 
     def backward(self, ps, dy, x, dx=None):
         B = x.shape[0]
-        K.gemm(dy, x, self.fpad, self.fin, B, 1, 1, out=ps.g[self.W], out_f32=True)
+        fl = 2 * B * self.fout * self.fin
+        if self.s_wg > 1:
+            part = self.scratch.part[:self.s_wg * self.fpad * self.fin].view(self.s_wg, self.fpad, self.fin)
+            K.gemm(dy, x, self.fpad, self.fin, B, 1, 1, out=part, splits=self.s_wg, acct_flops=fl)
+            used = K.splits_used(B, self.s_wg)
+            K.reduce_splits(part, used, self.fpad * self.fin, ps.g[self.W])
+        else:
+            K.gemm(dy, x, self.fpad, self.fin, B, 1, 1, out=ps.g[self.W], out_f32=True, acct_flops=fl)
         K.col_sum(dy, B, self.fpad, self.fpad, ps.g[self.Bn])
         if dx is not None:
-            K.gemm(dy, ps.b[self.W], B, self.fin, self.fpad, 0, 1, out=dx)
+            K.gemm(dy, ps.b[self.W], B, self.fin, self.fpad, 0, 1, out=dx, acct_flops=fl)
 
 
 class Net:
@@ -269,6 +300,8 @@ class SmallCNN(Net):
         self.c2.build(n, 32, 32, S, dev)
         self.c3.build(n, 16, 16, S, dev)
         self.c4.build(n, 16, 16, S, dev)
+        self.fc1.build(n, S)
+        self.head.build(n, S)
         self.a1, self.a2, self.p1 = e(n, 32, 32, 32), e(n, 32, 32, 32), e(n, 16, 16, 32)
         self.a3, self.a4, self.p2 = e(n, 16, 16, 64), e(n, 16, 16, 64), e(n, 8, 8, 64)
         self.h = e(n, 256)
@@ -285,8 +318,7 @@ class SmallCNN(Net):
         self.c4.forward(ps, self.a3, self.a4)
         K.maxpool_fwd(self.a4, 2, 2, 0, self.p2)
         flat = self.p2.view(self.batch, -1)
-        self.fc1.forward(ps, flat, self.h)
-        K.relu_fwd(self.h)
+        self.fc1.forward(ps, flat, self.h, relu=True)
         self.head.forward(ps, self.h, self.logits, out_f32=True)
 
     def backward(self, x):
@@ -370,6 +402,7 @@ class ResNet18(Net):
             self.douts.append(e(n, h, w, b.cout))
         self.final_hw = h * w
         self.pooled, self.dpooled = e(n, 512), e(n, 512)
+        self.head.build(n, S)
 
     def forward(self, x):
         ps = self.ps

@@ -23,7 +23,12 @@ from oracle.cnn_ref import RefTrainer, normalise_records
 from paper_2103_16898_b200 import loader, nets
 
 LOSS_TOL = 1e-3
-CURVE_TOL = 5e-2
+CURVE_TOL = 2e-2
+# Adam's first steps move every weight by ~lr; at the paper's lr=1e-3 the loss jumps from
+# 2.3 to ~3.8 on these synthetic batches, which turns rounding noise into trajectory
+# divergence.  Parity of the multi-step update is therefore checked at lr=1e-4 (same code
+# path; lr is a kernel argument); the bench and the loss-decrease test use 1e-3.
+PARITY_LR = 1e-4
 COS_MIN = {"small_cnn": 0.99, "resnet18": 0.95}   # 17 BN/ReLU layers amplify the flips
 GRAD_TOL = {"small_cnn": 0.15, "resnet18": 0.40}
 W_TOL = 1e-2
@@ -49,11 +54,12 @@ def rel(a, b):
     return (a - b).norm().item() / max(b.norm().item(), 1e-12)
 
 
-def run_parity(model="small_cnn", batch=32, steps=3, seed=0, emulate=True):
+def run_parity(model="small_cnn", batch=32, steps=3, seed=0, emulate=True, lr=PARITY_LR):
     spec = loader.CIFAR
     net = nets.make_model(model, seed=seed).build(batch)
+    net.lr = lr
     state0 = net.ps.state_cpu()
-    ref = RefTrainer(model, state0, emulate_bf16=emulate)
+    ref = RefTrainer(model, state0, emulate_bf16=emulate, lr=lr)
     report = []
     for s in range(steps):
         rec = make_records(batch, seed * 100 + s)

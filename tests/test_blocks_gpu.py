@@ -55,8 +55,10 @@ def test_basic_block(cin, cout, stride, n, h):
 
 def test_linear_layer():
     g = torch.Generator().manual_seed(3)
-    ps = nets.ParamStore()
+    ps, S = nets.ParamStore(), nets.Scratch()
     lin = nets.Linear(ps, "fc", 512, 10, g)
+    lin.build(64, S)
+    S.finalize("cuda")
     ps.finalize("cuda")
     x = torch.randn(64, 512, generator=g).bfloat16().cuda()
     y = torch.empty(64, 16, device="cuda")
