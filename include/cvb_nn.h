@@ -49,10 +49,11 @@ int cvb_bn_backward(const void* dy, int dycs, const void* x, int xcs, const void
                     void* stream);
 
 /* ---- pooling -------------------------------------------------------------------------------- */
-int cvb_maxpool_fwd(const void* x, int n, int h, int w, int C, int k, int s, int p, void* y, int oh, int ow, void* stream);
+int cvb_maxpool_fwd(const void* x, int n, int h, int w, int C, int k, int s, int p, void* y, int oh, int ow, int ycs,
+                    void* stream);
 int cvb_maxpool_bwd(const void* x, const void* dy, int n, int h, int w, int C, int k, int s, int p, int oh, int ow,
                     void* dx, void* stream);
-int cvb_avgpool_fwd(const void* x, int n, int h, int w, int C, int xcs, int k, void* y, void* stream);
+int cvb_avgpool_fwd(const void* x, int n, int h, int w, int C, int xcs, int k, void* y, int ycs, void* stream);
 int cvb_avgpool_bwd(const void* dy, int n, int h, int w, int C, int k, void* dx, int dxcs, void* stream);
 int cvb_gap_fwd(const void* x, int n, int hw, int C, int xcs, void* y, void* stream);
 int cvb_gap_bwd(const void* dy, int n, int hw, int C, void* dx, void* stream);
@@ -79,6 +80,8 @@ int cvb_adam_step(float* p, const float* g, float* m, float* v, void* pb, int64_
 int cvb_sgd_step(float* p, const float* g, float* buf, void* pb, int64_t n, float lr, float momentum, float wd,
                  float grad_scale, int first, void* stream);
 int cvb_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream);
+/* y[r][c] = bf16(x[r][c]) with row strides (concat-gradient slices) */
+int cvb_cast_rows(const float* x, int64_t ldx, void* y, int64_t ldy, int64_t rows, int cols, void* stream);
 
 #ifdef __cplusplus
 }

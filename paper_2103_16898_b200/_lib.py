@@ -58,9 +58,9 @@ SIGNATURES = {
     "cvb_bn_apply": (_INT, [_P, _I64, _INT, _INT, _P, _P, _P, _P, _P, _INT, _INT, _P, _INT, _INT, _P]),
     "cvb_bn_backward": (_INT, [_P, _INT, _P, _INT, _P, _INT, _I64, _INT, _P, _P, _P, _P, _INT, _P, _P, _P, _P, _INT,
                                _P, _INT, _P, _P]),
-    "cvb_maxpool_fwd": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT, _P]),
+    "cvb_maxpool_fwd": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT, _INT, _P]),
     "cvb_maxpool_bwd": (_INT, [_P, _P, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _P, _P]),
-    "cvb_avgpool_fwd": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _INT, _P, _P]),
+    "cvb_avgpool_fwd": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _INT, _P, _INT, _P]),
     "cvb_avgpool_bwd": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _P, _INT, _P]),
     "cvb_gap_fwd": (_INT, [_P, _INT, _INT, _INT, _INT, _P, _P]),
     "cvb_gap_bwd": (_INT, [_P, _INT, _INT, _INT, _P, _P]),
@@ -78,6 +78,7 @@ SIGNATURES = {
                              _c.c_float, _P, _P, _P]),
     "cvb_sgd_step": (_INT, [_P, _P, _P, _P, _I64, _c.c_float, _c.c_float, _c.c_float, _c.c_float, _INT, _P]),
     "cvb_cast_f32_bf16": (_INT, [_P, _P, _I64, _P]),
+    "cvb_cast_rows": (_INT, [_P, _I64, _P, _I64, _I64, _INT, _P]),
 }
 
 

@@ -226,7 +226,7 @@ __global__ void bn_bwd_apply(const bf16* __restrict__ dy, int dycs, const bf16* 
 
 // ---- pooling --------------------------------------------------------------------------
 __global__ void maxpool_fwd(const bf16* __restrict__ x, int n, int h, int w, int C, int k, int s, int p, int oh, int ow,
-                            bf16* __restrict__ y) {
+                            bf16* __restrict__ y, int ycs) {
   const int G = C / 8;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)n * oh * ow * G) return;
@@ -248,7 +248,7 @@ __global__ void maxpool_fwd(const bf16* __restrict__ x, int n, int h, int w, int
       for (int c = 0; c < 8; c++) if (v[c] > m[c]) m[c] = v[c];
     }
   }
-  store8(y + pix * C + g * 8, m);
+  store8(y + pix * ycs + g * 8, m);
 }
 
 // gather form: each input element collects dy of every window whose FIRST arg-max it is
@@ -325,7 +325,7 @@ __global__ void maxpool2_bwd(const bf16* __restrict__ x, const bf16* __restrict_
 }
 
 __global__ void avgpool_fwd(const bf16* __restrict__ x, int n, int h, int w, int C, int xcs, int k, int oh, int ow,
-                            bf16* __restrict__ y) {
+                            bf16* __restrict__ y, int ycs) {
   const int G = C / 8;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)n * oh * ow * G) return;
@@ -343,7 +343,7 @@ __global__ void avgpool_fwd(const bf16* __restrict__ x, int n, int h, int w, int
   const float inv = 1.0f / (k * k);
 #pragma unroll
   for (int c = 0; c < 8; c++) a[c] *= inv;
-  store8(y + pix * C + g * 8, a);
+  store8(y + pix * ycs + g * 8, a);
 }
 
 __global__ void avgpool_bwd(const bf16* __restrict__ dy, int n, int h, int w, int C, int k, int oh, int ow,
@@ -578,6 +578,20 @@ __global__ void sgd_step(float* __restrict__ p, const float* __restrict__ g, flo
   if (pb) pb[i] = __float2bfloat16_rn(pi);
 }
 
+// strided 2-D cast: y[r][c] = bf16(x[r][c]) with row strides (DenseNet concat-gradient slices)
+__global__ void cast_rows(const float* __restrict__ x, int64_t ldx, bf16* __restrict__ y, int64_t ldy, int64_t rows,
+                          int cols) {
+  const int G = cols / 8;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * G) return;
+  const int64_t r = i / G;
+  const int g = (int)(i - r * G);
+  const float4* s = reinterpret_cast<const float4*>(x + r * ldx + g * 8);
+  float4 a = s[0], b = s[1];
+  float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  store8(y + r * ldy + g * 8, v);
+}
+
 __global__ void cast_f32_bf16(const float* __restrict__ x, bf16* __restrict__ y, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = __float2bfloat16_rn(x[i]);
@@ -653,8 +667,9 @@ CVB_API int cvb_bn_backward(const void* dy, int dycs, const void* x, int xcs, co
 }
 
 CVB_API int cvb_maxpool_fwd(const void* x, int n, int h, int w, int C, int k, int s, int p, void* y, int oh, int ow,
-                            void* stream) {
-  maxpool_fwd<<<nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, n, h, w, C, k, s, p, oh, ow, (bf16*)y);
+                            int ycs, void* stream) {
+  maxpool_fwd<<<nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, n, h, w, C, k, s, p, oh, ow,
+                                                                          (bf16*)y, ycs);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
@@ -671,9 +686,10 @@ CVB_API int cvb_maxpool_bwd(const void* x, const void* dy, int n, int h, int w, 
   return CVB_OK;
 }
 
-CVB_API int cvb_avgpool_fwd(const void* x, int n, int h, int w, int C, int xcs, int k, void* y, void* stream) {
+CVB_API int cvb_avgpool_fwd(const void* x, int n, int h, int w, int C, int xcs, int k, void* y, int ycs, void* stream) {
   const int oh = h / k, ow = w / k;
-  avgpool_fwd<<<nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, n, h, w, C, xcs, k, oh, ow, (bf16*)y);
+  avgpool_fwd<<<nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, n, h, w, C, xcs, k, oh, ow,
+                                                                          (bf16*)y, ycs);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
@@ -775,6 +791,13 @@ CVB_API int cvb_adam_step(float* p, const float* g, float* m, float* v, void* pb
 CVB_API int cvb_sgd_step(float* p, const float* g, float* buf, void* pb, int64_t n, float lr, float momentum, float wd,
                          float grad_scale, int first, void* stream) {
   sgd_step<<<nblocks(n), 256, 0, STREAM>>>(p, g, buf, (bf16*)pb, n, lr, momentum, wd, grad_scale, first);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_cast_rows(const float* x, int64_t ldx, void* y, int64_t ldy, int64_t rows, int cols, void* stream) {
+  if (cols % 8) { cvb_set_error("cast_rows: cols must be a multiple of 8"); return CVB_EINVAL; }
+  cast_rows<<<nblocks(rows * (cols / 8)), 256, 0, STREAM>>>(x, ldx, (bf16*)y, ldy, rows, cols);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }

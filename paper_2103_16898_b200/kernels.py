@@ -183,7 +183,7 @@ def maxpool_fwd(x, k, s, p, y):
     n, h, w, c = x.shape
     _, oh, ow, _ = y.shape
     tok = REC.begin(1, "pool", 0, (x.numel() + y.numel()) * 2)
-    rc = _lib_bound().cvb_maxpool_fwd(x.data_ptr(), n, h, w, c, k, s, p, y.data_ptr(), oh, ow, _stream())
+    rc = _lib_bound().cvb_maxpool_fwd(x.data_ptr(), n, h, w, c, k, s, p, y.data_ptr(), oh, ow, y.stride(2), _stream())
     REC.end(tok)
     _lib.check(rc, "maxpool_fwd")
 
@@ -198,9 +198,10 @@ def maxpool_bwd(x, dy, k, s, p, dx):
     _lib.check(rc, "maxpool_bwd")
 
 
-def avgpool_fwd(x, n, h, w, c, xcs, k, y):
+def avgpool_fwd(x, n, h, w, c, xcs, k, y, ycs=None):
     tok = REC.begin(1, "pool", 0, n * h * w * c * 2 * 5 // 4)
-    rc = _lib_bound().cvb_avgpool_fwd(x.data_ptr(), n, h, w, c, xcs, k, y.data_ptr(), _stream())
+    rc = _lib_bound().cvb_avgpool_fwd(x.data_ptr(), n, h, w, c, xcs, k, y.data_ptr(), c if ycs is None else ycs,
+                                      _stream())
     REC.end(tok)
     _lib.check(rc, "avgpool_fwd")
 
@@ -303,6 +304,13 @@ def sgd_step(p, g, buf, pb, lr, momentum=0.0, wd=0.0, grad_scale=1.0, first=Fals
                                    grad_scale, int(first), _stream())
     REC.end(tok)
     _lib.check(rc, "sgd_step")
+
+
+def cast_rows(x, ldx, y, ldy, rows, cols):
+    tok = REC.begin(1, "layout", 0, rows * cols * 6)
+    rc = _lib_bound().cvb_cast_rows(x.data_ptr(), ldx, y.data_ptr(), ldy, rows, cols, _stream())
+    REC.end(tok)
+    _lib.check(rc, "cast_rows")
 
 
 def cast_f32_bf16(x, y):

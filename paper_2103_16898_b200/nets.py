@@ -426,7 +426,250 @@ class ResNet18(Net):
         self.stem.backward(ps, self.dx0, x, dx=None)
 
 
-MODELS = {"small_cnn": SmallCNN, "resnet18": ResNet18}
+class BNAct:
+    """Pre-activation batch norm (+ReLU) over channels [0, C) of an NHWC buffer with a channel
+    stride (DenseNet reads its concat buffer in place).  Backward accumulates the input
+    gradient in fp32 (the concat gradient receives one contribution per later layer)."""
+
+    def __init__(self, ps, name, C, relu=True):
+        self.C, self.relu = C, relu
+        self.G = ps.add(f"{name}.gamma", torch.ones(C))
+        self.B = ps.add(f"{name}.beta", torch.zeros(C))
+
+    def build(self, rows, scratch, device):
+        self.rows = rows
+        self.mean = torch.zeros(self.C, dtype=F32, device=device)
+        self.rstd = torch.zeros(self.C, dtype=F32, device=device)
+        self.run_mean = torch.zeros(self.C, dtype=F32, device=device)
+        self.run_var = torch.ones(self.C, dtype=F32, device=device)
+        scratch.bn_floats = max(scratch.bn_floats, K._lib_bound().cvb_bn_workspace_floats(rows, self.C))
+        self.scratch = scratch
+
+    def forward(self, ps, x, xcs, y, ycs, stats=True):
+        if stats:
+            K.bn_stats(x, self.rows, self.C, xcs, self.scratch.bnws, self.mean, self.rstd, run_mean=self.run_mean,
+                       run_var=self.run_var)
+        K.bn_apply(x, self.rows, self.C, xcs, self.mean, self.rstd, ps.p[self.G], ps.p[self.B], y, ycs,
+                   relu=self.relu)
+
+    def backward(self, ps, dy, dycs, x, xcs, dx32, dx32cs, accumulate):
+        K.bn_backward(dy, dycs, x, xcs, self.rows, self.C, self.mean, self.rstd, ps.p[self.G], ps.p[self.B],
+                      self.scratch.bnws, ps.g[self.G], ps.g[self.B], relu=self.relu, dx32=dx32, dxcs=dx32cs,
+                      accum32=accumulate)
+
+
+class Conv:
+    """Convolution without a following BN (DenseNet's pre-activation units): bf16 output
+    into a channel slice of the destination; backward = split-K wgrad + flipped-weight dgrad."""
+
+    def __init__(self, ps, name, cin, cout, k, stride, pad, gen):
+        self.cin, self.cout, self.k, self.s, self.pad = cin, cout, k, stride, pad
+        bound = 1.0 / math.sqrt(cin * k * k)
+        self.W = ps.add(f"{name}.w", _uniform(gen, (cout, k, k, cin), bound))
+
+    def build(self, n, h, w, scratch):
+        self.n, self.h, self.w = n, h, w
+        self.oh, self.ow = K.conv_out_hw(h, w, self.k, self.s, self.pad)
+        self.flops = 2 * n * self.oh * self.ow * self.cout * self.k * self.k * self.cin
+        count = self.cout * self.k * self.k * self.cin
+        scratch.part_floats = max(scratch.part_floats, min(MAX_SPLITS * count, max(PART_CAP, 8 * count)))
+        scratch.flip_elems = max(scratch.flip_elems, count)
+        self.scratch = scratch
+        return self.oh, self.ow
+
+    def forward(self, ps, x, out, out_coff=0):
+        K.conv2d_fwd(x, ps.b[self.W], self.s, self.pad, out=out, cin=self.cin, out_coff=out_coff,
+                     acct_flops=self.flops)
+
+    def backward(self, ps, dz, x, dx=None):
+        count = self.cout * self.k * self.k * self.cin
+        maxs = max(1, min(MAX_SPLITS, self.scratch.part.numel() // count))
+        part, used = K.conv2d_wgrad_partials(dz, x, self.k, self.k, self.s, self.pad, cin=self.cin,
+                                             part=self.scratch.part[:maxs * count].view(maxs, self.cout,
+                                                                                        self.k * self.k * self.cin),
+                                             acct_flops=self.flops)
+        K.reduce_splits(part, used, count, ps.g[self.W])
+        if dx is not None:
+            wt = self.scratch.flip[:count].view(self.cin, self.k, self.k, self.cout)
+            K.weight_flip(ps.b[self.W], wt)
+            K.conv2d_fwd(dz, wt, 1, self.k - 1 - self.pad, out=dx, out_hw=(self.h, self.w), acct_flops=self.flops)
+
+
+class DenseLayer:
+    """BN-ReLU-conv1x1(4g) -> BN-ReLU-conv3x3(g), output appended to the block buffer."""
+
+    def __init__(self, ps, name, cin, growth, bn_size, gen):
+        self.cin, self.growth, self.mid = cin, growth, bn_size * growth
+        self.bn1 = BNAct(ps, f"{name}.norm1", cin)
+        self.conv1 = Conv(ps, f"{name}.conv1", cin, self.mid, 1, 1, 0, gen)
+        self.bn2 = BNAct(ps, f"{name}.norm2", self.mid)
+        self.conv2 = Conv(ps, f"{name}.conv2", self.mid, growth, 3, 1, 1, gen)
+
+    def build(self, n, h, w, S, dev):
+        rows = n * h * w
+        self.bn1.build(rows, S, dev)
+        self.conv1.build(n, h, w, S)
+        self.bn2.build(rows, S, dev)
+        self.conv2.build(n, h, w, S)
+        self.z1 = torch.empty(n, h, w, self.mid, dtype=BF16, device=dev)   # kept for backward
+
+    def forward(self, ps, blk, y1, y2):
+        cs = blk.shape[-1]
+        self.bn1.forward(ps, blk, cs, y1, self.cin)
+        self.conv1.forward(ps, y1, self.z1)
+        self.bn2.forward(ps, self.z1, self.mid, y2, self.mid)
+        self.conv2.forward(ps, y2, blk, out_coff=self.cin)
+
+    def backward(self, ps, blk, dblk32, y1, y2, dz2, dy2, dz1, dy1):
+        cs = blk.shape[-1]
+        rows = self.bn1.rows
+        # gradient of this layer's output slice is complete (later layers already added)
+        K.cast_rows(dblk32[..., self.cin:], cs, dz2, self.growth, rows, self.growth)
+        self.bn2.forward(ps, self.z1, self.mid, y2, self.mid, stats=False)     # recompute y2
+        self.conv2.backward(ps, dz2, y2, dx=dy2)
+        K.bn_backward(dy2, self.mid, self.z1, self.mid, rows, self.mid, self.bn2.mean, self.bn2.rstd,
+                      ps.p[self.bn2.G], ps.p[self.bn2.B], self.bn2.scratch.bnws, ps.g[self.bn2.G], ps.g[self.bn2.B],
+                      relu=True, dx=dz1, dxcs=self.mid)
+        self.bn1.forward(ps, blk, cs, y1, self.cin, stats=False)               # recompute y1
+        self.conv1.backward(ps, dz1, y1, dx=dy1)
+        self.bn1.backward(ps, dy1, self.cin, blk, cs, dblk32, cs, accumulate=True)
+
+
+class DenseNet121(Net):
+    """DenseNet-121-style (growth 32, blocks 6/12/24/16, bn_size 4, compression 0.5) for the
+    medical config: 224x224x1 input (padded to 8 channels), 2 classes."""
+
+    num_classes = 2
+    in_channels = 1
+    image = 224
+
+    def __init__(self, seed=0, num_classes=2, blocks=(6, 12, 24, 16), growth=32, bn_size=4, init_ch=64):
+        super().__init__(seed)
+        self.num_classes = num_classes
+        ps, g = self.ps, self.gen
+        self.stem = ConvBN(ps, "features.conv0", 8, init_ch, 7, 2, 3, g, cin_real=1, need_dgrad=False)
+        self.blocks, self.trans = [], []
+        c = init_ch
+        for bi, nl in enumerate(blocks):
+            layers = [DenseLayer(ps, f"features.denseblock{bi + 1}.denselayer{li + 1}", c + li * growth, growth,
+                                 bn_size, g) for li in range(nl)]
+            self.blocks.append((c, c + nl * growth, layers))
+            c = c + nl * growth
+            if bi != len(blocks) - 1:
+                t = (BNAct(ps, f"features.transition{bi + 1}.norm", c),
+                     Conv(ps, f"features.transition{bi + 1}.conv", c, c // 2, 1, 1, 0, g))
+                self.trans.append(t)
+                c //= 2
+        self.norm5 = BNAct(ps, "features.norm5", c)
+        self.final_c = c
+        self.head = Linear(ps, "classifier", c, num_classes, g)
+
+    def _build(self, n, dev):
+        S = self.scratch
+        e = lambda *s: torch.empty(*s, dtype=BF16, device=dev)  # noqa: E731
+        oh, ow = self.stem.build(n, 224, 224, S, dev)
+        self.a0 = e(n, oh, ow, self.stem.cout)
+        self.da0 = e(n, oh, ow, self.stem.cout)
+        h, w = (oh + 2 - 3) // 2 + 1, (ow + 2 - 3) // 2 + 1
+        self.geo, self.bufs, self.dbufs = [], [], []
+        ymax = 0
+        for bi, (c0, c1, layers) in enumerate(self.blocks):
+            for L in layers:
+                L.build(n, h, w, S, dev)
+            self.geo.append((h, w))
+            self.bufs.append(e(n, h, w, c1))
+            self.dbufs.append(torch.empty(n, h, w, c1, dtype=F32, device=dev))
+            ymax = max(ymax, n * h * w * c1)
+            if bi < len(self.trans):
+                bn, conv = self.trans[bi]
+                bn.build(n * h * w, S, dev)
+                conv.build(n, h, w, S)
+                h, w = h // 2, w // 2
+        self.norm5.build(n * h * w, S, dev)
+        self.head.build(n, S)
+        # shared scratch (largest use wins)
+        mid = max(L.mid for _, _, ls in self.blocks for L in ls)
+        rows_max = max(n * gh * gw for gh, gw in self.geo)
+        self.y1 = e(ymax)
+        self.y2 = e(rows_max * mid)
+        self.dz2 = e(rows_max * 32)
+        self.dy2 = e(rows_max * mid)
+        self.dz1 = e(rows_max * mid)
+        self.dy1 = e(ymax)
+        self.t = e(ymax // 2)
+        self.dt = e(ymax // 2)
+        self.y5 = e(n * h * w * self.final_c)
+        self.dy5 = e(n * h * w * self.final_c)
+        self.final_hw = h * w
+        self.pooled, self.dpooled = e(n, self.final_c), e(n, self.final_c)
+        self.dcast = e(ymax)
+
+    def _v(self, buf, *shape):
+        return buf[:math.prod(shape)].view(*shape)
+
+    def forward(self, x):
+        ps, n = self.ps, self.batch
+        self.stem.forward(ps, x, self.a0)
+        K.maxpool_fwd(self.a0, 3, 2, 1, self.bufs[0][..., :self.stem.cout])
+        for bi, (c0, c1, layers) in enumerate(self.blocks):
+            h, w = self.geo[bi]
+            blk = self.bufs[bi]
+            for L in layers:
+                L.forward(ps, blk, self._v(self.y1, n, h, w, L.cin), self._v(self.y2, n, h, w, L.mid))
+            if bi < len(self.trans):
+                bn, conv = self.trans[bi]
+                y = self._v(self.y1, n, h, w, c1)
+                bn.forward(ps, blk, c1, y, c1)
+                t = self._v(self.t, n, h, w, c1 // 2)
+                conv.forward(ps, y, t)
+                nxt = self.bufs[bi + 1]
+                K.avgpool_fwd(t, n, h, w, c1 // 2, c1 // 2, 2, nxt, nxt.shape[-1])
+        h, w = self.geo[-1]
+        c = self.final_c
+        self.norm5.forward(ps, self.bufs[-1], c, self._v(self.y5, n, h, w, c), c)
+        K.gap_fwd(self._v(self.y5, n, h, w, c), n, h * w, c, c, self.pooled)
+        self.head.forward(ps, self.pooled, self.logits, out_f32=True)
+
+    def backward(self, x):
+        ps, n = self.ps, self.batch
+        c = self.final_c
+        self.head.backward(ps, self.dlogits, self.pooled, self.dpooled)
+        h, w = self.geo[-1]
+        dy5 = self._v(self.dy5, n, h, w, c)
+        K.gap_bwd(self.dpooled, n, h * w, c, dy5)
+        self.norm5.backward(ps, dy5, c, self.bufs[-1], c, self.dbufs[-1], c, accumulate=False)
+        for bi in range(len(self.blocks) - 1, -1, -1):
+            c0, c1, layers = self.blocks[bi]
+            h, w = self.geo[bi]
+            blk, dblk = self.bufs[bi], self.dbufs[bi]
+            if bi < len(self.trans):
+                # transition: its input gradient initialises this block's fp32 concat gradient
+                bn, conv = self.trans[bi]
+                nxt_d = self.dbufs[bi + 1]
+                oh, ow = h // 2, w // 2
+                dp = self._v(self.dcast, n, oh, ow, c1 // 2)
+                K.cast_rows(nxt_d, nxt_d.shape[-1], dp, c1 // 2, n * oh * ow, c1 // 2)
+                dt = self._v(self.dt, n, h, w, c1 // 2)
+                K.avgpool_bwd(dp, n, h, w, c1 // 2, 2, dt, c1 // 2)
+                y = self._v(self.y1, n, h, w, c1)
+                bn.forward(ps, blk, c1, y, c1, stats=False)
+                dy = self._v(self.dy1, n, h, w, c1)
+                conv.backward(ps, dt, y, dx=dy)
+                bn.backward(ps, dy, c1, blk, c1, dblk, c1, accumulate=False)
+            for L in reversed(layers):
+                rows = n * h * w
+                L.backward(ps, blk, dblk, self._v(self.y1, n, h, w, L.cin), self._v(self.y2, n, h, w, L.mid),
+                           self._v(self.dz2, n, h, w, L.growth), self._v(self.dy2, n, h, w, L.mid),
+                           self._v(self.dz1, n, h, w, L.mid), self._v(self.dy1, n, h, w, L.cin))
+        # stem: max-pool backward from the first 64 channels of block 1's gradient
+        h, w = self.geo[0]
+        d0 = self._v(self.dcast, n, h, w, self.stem.cout)
+        K.cast_rows(self.dbufs[0], self.dbufs[0].shape[-1], d0, self.stem.cout, n * h * w, self.stem.cout)
+        K.maxpool_bwd(self.a0, d0, 3, 2, 1, self.da0)
+        self.stem.backward(ps, self.da0, x, dx=None)
+
+
+MODELS = {"small_cnn": SmallCNN, "resnet18": ResNet18, "densenet121": DenseNet121}
 
 
 def make_model(name, seed=0, **kw):
