@@ -147,7 +147,51 @@ class ResNet18Ref(RefModel):
         return self.linear(pooled, "fc", self.num_classes, out_f32=True)
 
 
-REF_MODELS = {"small_cnn": SmallCNNRef, "resnet18": ResNet18Ref}
+class DenseNet121Ref(RefModel):
+    """DenseNet-121-style, 1-channel 224x224 stem, 2 classes (nets.DenseNet121).  Rounding
+    points: BN outputs, conv outputs and pool outputs are bf16; the concat gradient is fp32
+    (autograd sums the per-layer contributions) and is rounded where the GPU casts it."""
+
+    num_classes = 2
+    blocks = (6, 12, 24, 16)
+    growth, bn_size, init_ch = 32, 4, 64
+
+    def bn_relu(self, x, name, relu=True):
+        rm = self.running.setdefault(name + ".rm", torch.zeros(x.shape[1]))
+        rv = self.running.setdefault(name + ".rv", torch.ones(x.shape[1]))
+        y = F.batch_norm(x, rm, rv, self.P(f"{name}.gamma"), self.P(f"{name}.beta"), training=True, momentum=0.1,
+                         eps=1e-5)
+        return self.R.rb(F.relu(y) if relu else y)
+
+    def conv(self, x, name, stride, pad):
+        w = self.P(f"{name}.w")
+        wt = nhwc_conv_weight(_bf16_param(w) if self.R.on else w)
+        return self.R.rb(F.conv2d(x, wt, stride=stride, padding=pad))
+
+    def forward(self, x):
+        R = self.R
+        a = self.conv_bn(x, "features.conv0", 2, 3, cin_real=1)
+        a = R.rb(F.max_pool2d(a, 3, 2, 1))
+        feats = [a]
+        for bi, nl in enumerate(self.blocks):
+            for li in range(nl):
+                nm = f"features.denseblock{bi + 1}.denselayer{li + 1}"
+                cat = torch.cat(feats, dim=1)
+                y1 = self.bn_relu(cat, f"{nm}.norm1")
+                z1 = self.conv(y1, f"{nm}.conv1", 1, 0)
+                y2 = self.bn_relu(z1, f"{nm}.norm2")
+                feats.append(self.conv(y2, f"{nm}.conv2", 1, 1))
+            cat = torch.cat(feats, dim=1)
+            if bi != len(self.blocks) - 1:
+                y = self.bn_relu(cat, f"features.transition{bi + 1}.norm")
+                t = self.conv(y, f"features.transition{bi + 1}.conv", 1, 0)
+                feats = [R.rb(F.avg_pool2d(t, 2))]
+        y5 = self.bn_relu(cat, "features.norm5")
+        pooled = R.rb(y5.mean(dim=(2, 3)))
+        return self.linear(pooled, "classifier", self.num_classes, out_f32=True)
+
+
+REF_MODELS = {"small_cnn": SmallCNNRef, "resnet18": ResNet18Ref, "densenet121": DenseNet121Ref}
 
 
 def normalise_records(records_u8: torch.Tensor, c: int, h: int, w: int, mean, std, emulate_bf16=True):

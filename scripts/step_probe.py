@@ -12,8 +12,9 @@ from paper_2103_16898_b200 import loader
 model = sys.argv[1] if len(sys.argv) > 1 else "small_cnn"
 batch = int(sys.argv[2]) if len(sys.argv) > 2 else 512
 net = nets.make_model(model, seed=0).build(batch)
-rec = make_records(batch, 3)
-x, lab = gpu_inputs(rec, loader.CIFAR)
+spec = loader.MEDICAL if model == "densenet121" else loader.CIFAR
+rec = make_records(batch, 3, c=spec["c"], h=spec["h"], w=spec["w"], classes=net.num_classes)
+x, lab = gpu_inputs(rec, spec)
 for _ in range(3):
     net.step(x, lab)
 torch.cuda.synchronize()

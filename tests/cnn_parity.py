@@ -29,8 +29,11 @@ CURVE_TOL = 2e-2
 # divergence.  Parity of the multi-step update is therefore checked at lr=1e-4 (same code
 # path; lr is a kernel argument); the bench and the loss-decrease test use 1e-3.
 PARITY_LR = 1e-4
-COS_MIN = {"small_cnn": 0.99, "resnet18": 0.95}   # 17 BN/ReLU layers amplify the flips
-GRAD_TOL = {"small_cnn": 0.15, "resnet18": 0.40}
+# deep BN/ReLU stacks amplify the flips: 17 layers (ResNet-18) -> cos 0.97, 121 layers at
+# batch 8 (DenseNet-121) -> cos 0.86; the layer compositions themselves are checked on
+# identical inputs in tests/test_blocks_gpu.py (<= 5% per gradient).
+COS_MIN = {"small_cnn": 0.99, "resnet18": 0.95, "densenet121": 0.80}
+GRAD_TOL = {"small_cnn": 0.15, "resnet18": 0.40, "densenet121": 0.80}
 W_TOL = 1e-2
 FP32_LOSS_TOL = 2e-2
 
@@ -55,14 +58,15 @@ def rel(a, b):
 
 
 def run_parity(model="small_cnn", batch=32, steps=3, seed=0, emulate=True, lr=PARITY_LR):
-    spec = loader.CIFAR
+    spec = loader.MEDICAL if model == "densenet121" else loader.CIFAR
+    classes = 2 if model == "densenet121" else 10
     net = nets.make_model(model, seed=seed).build(batch)
     net.lr = lr
     state0 = net.ps.state_cpu()
     ref = RefTrainer(model, state0, emulate_bf16=emulate, lr=lr)
     report = []
     for s in range(steps):
-        rec = make_records(batch, seed * 100 + s)
+        rec = make_records(batch, seed * 100 + s, c=spec["c"], h=spec["h"], w=spec["w"], classes=classes)
         x, lab = gpu_inputs(rec, spec)
         xr, labr = normalise_records(torch.from_numpy(rec), spec["c"], spec["h"], spec["w"], spec["mean"],
                                      spec["std"], emulate_bf16=emulate)

@@ -53,6 +53,66 @@ def test_basic_block(cin, cout, stride, n, h):
         assert rel(ps.g[name].cpu(), p.grad) < 5e-2, (name, rel(ps.g[name].cpu(), p.grad))
 
 
+def test_dense_block_and_transition():
+    """3 DenseNet layers on a 64-channel block input + a transition, identical inputs."""
+    g = torch.Generator().manual_seed(5)
+    n, h, w, c0, gr = 8, 8, 8, 64, 32
+    ps, S = nets.ParamStore(), nets.Scratch()
+    layers = [nets.DenseLayer(ps, f"b.l{i}", c0 + i * gr, gr, 4, g) for i in range(3)]
+    c1 = c0 + 3 * gr
+    tbn = nets.BNAct(ps, "t.norm", c1)
+    tconv = nets.Conv(ps, "t.conv", c1, c1 // 2, 1, 1, 0, g)
+    for L in layers:
+        L.build(n, h, w, S, "cuda")
+    tbn.build(n * h * w, S, "cuda")
+    tconv.build(n, h, w, S)
+    S.finalize("cuda")
+    ps.finalize("cuda")
+    e = lambda *s: torch.empty(*s, dtype=torch.bfloat16, device="cuda")  # noqa: E731
+    x0 = torch.randn(n, h, w, c0, generator=g).bfloat16()
+    blk = torch.zeros(n, h, w, c1, dtype=torch.bfloat16, device="cuda")
+    blk[..., :c0] = x0.cuda()
+    y1, y2 = e(n * h * w * c1), e(n * h * w * 128)
+    for L in layers:
+        L.forward(ps, blk, y1[:n * h * w * L.cin].view(n, h, w, L.cin), y2.view(n, h, w, 128))
+    y = e(n, h, w, c1)
+    tbn.forward(ps, blk, c1, y, c1)
+    t = e(n, h, w, c1 // 2)
+    tconv.forward(ps, y, t)
+    dt = torch.randn(n, h, w, c1 // 2, generator=g).bfloat16()
+    dblk = torch.empty(n, h, w, c1, dtype=torch.float32, device="cuda")
+    dy = e(n, h, w, c1)
+    tbn.forward(ps, blk, c1, y, c1, stats=False)
+    tconv.backward(ps, dt.cuda(), y, dx=dy)
+    tbn.backward(ps, dy, c1, blk, c1, dblk, c1, accumulate=False)
+    dz2, dy2, dz1, dy1 = e(n * h * w * gr), e(n * h * w * 128), e(n * h * w * 128), e(n * h * w * c1)
+    for L in reversed(layers):
+        L.backward(ps, blk, dblk, y1[:n * h * w * L.cin].view(n, h, w, L.cin), y2.view(n, h, w, 128),
+                   dz2.view(n, h, w, gr), dy2.view(n, h, w, 128), dz1.view(n, h, w, 128),
+                   dy1[:n * h * w * L.cin].view(n, h, w, L.cin))
+    torch.cuda.synchronize()
+
+    from oracle.cnn_ref import DenseNet121Ref
+    ref = DenseNet121Ref(ps.state_cpu())
+    xr = nchw(x0).requires_grad_(True)
+    feats = [xr]
+    for i, L in enumerate(layers):
+        cat = torch.cat(feats, 1)
+        yy1 = ref.bn_relu(cat, f"b.l{i}.norm1")
+        z1 = ref.conv(yy1, f"b.l{i}.conv1", 1, 0)
+        yy2 = ref.bn_relu(z1, f"b.l{i}.norm2")
+        feats.append(ref.conv(yy2, f"b.l{i}.conv2", 1, 1))
+    cat = torch.cat(feats, 1)
+    tt = ref.conv(ref.bn_relu(cat, "t.norm"), "t.conv", 1, 0)
+    assert rel(nchw(blk), cat.detach()) < 1e-2
+    assert rel(nchw(t), tt.detach()) < 1e-2
+    tt.backward(nchw(dt))
+    assert rel(nchw(dblk[..., :c0]), xr.grad) < 3e-2, rel(nchw(dblk[..., :c0]), xr.grad)
+    for k, p in ref.params.items():
+        name = k.replace("__", ".")
+        assert rel(ps.g[name].cpu(), p.grad) < 5e-2, (name, rel(ps.g[name].cpu(), p.grad))
+
+
 def test_linear_layer():
     g = torch.Generator().manual_seed(3)
     ps, S = nets.ParamStore(), nets.Scratch()

@@ -7,7 +7,7 @@ from tests import cnn_parity as P
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("model,batch", [("small_cnn", 32), ("small_cnn", 64), ("resnet18", 16)])
+@pytest.mark.parametrize("model,batch", [("small_cnn", 32), ("small_cnn", 64), ("resnet18", 16), ("densenet121", 8)])
 def test_train_steps_match_bf16_emulating_oracle(model, batch):
     report, wrel = P.run_parity(model, batch=batch, steps=3)
     P.check(report, wrel, model)
