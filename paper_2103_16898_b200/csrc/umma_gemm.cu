@@ -32,7 +32,12 @@
 
 namespace {
 
-enum { MODE_FWD = 0, MODE_WGRAD = 1, MODE_DENSE = 2 };
+enum { MODE_FWD = 0, MODE_WGRAD = 1, MODE_DENSE = 2, MODE_HALO = 3 };
+// MODE_HALO (stride-1 conv, 8x16 output tiles): a K-block is one channel group of the input
+// *halo* tile ((8+KW-1) x (16+KH-1) pixels), loaded once as 8-channel no-swizzle planes; each
+// tap is just a different UMMA descriptor start row into the same smem (core matrices are 8
+// consecutive pixels = 128 contiguous bytes, 8-row groups one halo row apart).  9x fewer L2
+// reads and TMA issues than one box per tap; the weights stay resident in smem.
 enum { OUT_NHWC = 0, OUT_ROWS = 1, OUT_PARTIAL = 2 };
 
 constexpr int BM = 128;          // UMMA M (cta_group::1)
@@ -55,6 +60,11 @@ struct GemmParams {
   int num_kb;               // total K-blocks of the full K range
   int kb_per_split;
   uint32_t tx_bytes;
+  uint32_t a_box_bytes;     // bytes TMA writes per A box (WGRAD: per-tile A box count varies)
+  uint32_t a_stage_bytes;   // smem bytes of the A part of one pipeline stage
+  int b_res;                // 1: the whole B operand (one N tile, all K) is loaded once per CTA
+  uint32_t b_res_bytes;     // size of the resident B region
+  int b_slabs;              // 64-wide K slabs of the resident B
   uint32_t idesc;
   int stages;
   // conv geometry
@@ -72,6 +82,10 @@ struct GemmParams {
   int dbg;                  // profiling knobs: 1 = skip MMA, 2 = skip TMA (results invalid)
   long long* trace;         // debug: clock64 timeline of CTA 0 (5 x 4096 slots) or null
   int nbox;
+  // MODE_HALO geometry
+  int h_cin, h_cg, h_planes, h_pitch, h_pad, h_kh, h_kw;
+  uint32_t h_plane_stride;      // bytes between 8-channel planes (>= halo pixels * 16, 128-aligned)
+  uint32_t h_box_bytes;         // bytes TMA writes per plane
   uint32_t boxtab[MAX_BOXES];   // packed (map, channel, dw, dh) per gathered box
 };
 
@@ -213,14 +227,16 @@ __device__ __forceinline__ void store16(const GemmParams& p, int64_t off, int co
 __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_constant__ GemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t a_stage = BM * BK * 2;            // 16 KB
-  const uint32_t b_stage = p.BN * BK * 2;
+  const uint32_t a_stage = p.a_stage_bytes;         // 16 KB (halo mode: planes * plane stride)
+  const uint32_t b_stage = p.b_res ? 0u : p.BN * BK * 2;
   const uint32_t stage_bytes = a_stage + b_stage;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes);
+  const uint32_t b_kb_bytes = p.BN * BK * 2;        // resident B: one K-block slab
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes + p.b_res_bytes);
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;       // [2]
   uint64_t* tempty = tfull + 2;             // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bres_full = tempty + 2;         // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tmem_cols = (2 * p.BN <= 32) ? 32 : (2 * p.BN <= 64) ? 64 : (2 * p.BN <= 128) ? 128 : (2 * p.BN <= 256) ? 256 : 512;
@@ -229,6 +245,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
     for (int i = 0; i < 4; i++) { prefetch_map(&p.mapA[i]); prefetch_map(&p.mapB[i]); }
     for (int i = 0; i < p.stages; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    mbar_init(bres_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -245,17 +262,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
 
   // Role loops run on whole, converged warps; only the issuing instructions are predicated on
   // one elected lane.  Stage / phase counters are incremental (no divisions in the loops).
+  const uint32_t bres = smem0 + p.stages * stage_bytes;   // resident B region (if any)
   if (warp == 0) {
     const bool leader = elect_one();
     int s = 0;
     uint32_t ph = 0;
     int it = 0;
+    if (p.b_res && leader && blockIdx.x < units) {
+      // whole B operand (single N tile): b_slabs slabs of BN x 64, loaded once per CTA
+      mbar_expect_tx(bres_full, p.b_slabs * p.gb * p.BN * p.b_cel * 2);
+      for (int kb = 0; kb < p.b_slabs; kb++)
+        for (int g = 0; g < p.gb; g++)
+          tma_load_2d(&p.mapB[0], bres + kb * b_kb_bytes + g * p.b_box_stride, bres_full, kb * BK + g * p.b_cel, 0);
+    }
+    __syncwarp();
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int mt = u % p.m_tiles, rest = u / p.m_tiles;
       const int nt = rest % p.n_tiles, sp = rest / p.n_tiles;
       const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
       int tw0 = 0, th0 = 0, tn0 = 0;
-      if (p.mode == MODE_FWD) {
+      if (p.mode == MODE_FWD || p.mode == MODE_HALO) {
         tw0 = (mt % p.ptiles_w) * p.tw;
         const int r2 = mt / p.ptiles_w;
         th0 = (r2 % p.ptiles_h) * p.th;
@@ -270,6 +296,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
         pn = (r2 / p.ptiles_h) * p.tn;
       }
       const int m0 = mt * BM, n0 = nt * p.BN;
+      // WGRAD: A boxes past M (Cout) would be all zero fill -- skip them; their accumulator
+      // rows are never stored.
+      int ga_eff = p.ga;
+      uint32_t tx = p.tx_bytes;
+      if (p.mode == MODE_WGRAD) {
+        ga_eff = min(p.ga, (p.M - m0 + p.a_cel - 1) / p.a_cel);
+        tx = p.tx_bytes - (uint32_t)(p.ga - ga_eff) * p.a_box_bytes;
+      }
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
         mbar_wait(&empty[s], ph ^ 1);
         if (leader) {
@@ -278,18 +312,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           if (p.dbg & 2) {
             mbar_arrive(&full[s]);
           } else {
-            mbar_expect_tx(&full[s], p.tx_bytes);
-            if (p.mode == MODE_FWD) {
+            mbar_expect_tx(&full[s], tx);
+            if (p.mode == MODE_HALO) {
+              for (int j = 0; j < p.h_planes; j++)
+                tma_load_4d(&p.mapA[0], sa + j * p.h_plane_stride, &full[s], kb * p.h_cg + 8 * j, tw0 - p.h_pad,
+                            th0 - p.h_pad, tn0);
+            } else if (p.mode == MODE_FWD) {
               const uint32_t* tab = p.boxtab + kb * p.ga;
               for (int g = 0; g < p.ga; g++) {
                 const uint32_t e = tab[g];
                 tma_load_4d(&p.mapA[e & 3], sa + g * p.a_box_stride, &full[s], (int)((e >> 2) & 0xFFFF),
                             tw0 + (int)((e >> 18) & 127) - 64, th0 + (int)(e >> 25) - 64, tn0);
               }
-              for (int g = 0; g < p.gb; g++)
-                tma_load_2d(&p.mapB[0], sb + g * p.b_box_stride, &full[s], kb * BK + g * p.b_cel, n0);
+              if (!p.b_res)
+                for (int g = 0; g < p.gb; g++)
+                  tma_load_2d(&p.mapB[0], sb + g * p.b_box_stride, &full[s], kb * BK + g * p.b_cel, n0);
             } else if (p.mode == MODE_WGRAD) {
-              for (int b = 0; b < p.ga; b++)
+              for (int b = 0; b < ga_eff; b++)
                 tma_load_4d(&p.mapA[0], sa + b * p.a_box_stride, &full[s], m0 + b * p.a_cel, pw, ph0, pn);
               const uint32_t* tab = p.boxtab + nt * p.gb;
               for (int j = 0; j < p.gb; j++) {
@@ -330,6 +369,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       const int sp = u / (p.m_tiles * p.n_tiles);
       const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
       const int acc = lt & 1;
+      if (lt == 0 && p.b_res) mbar_wait(bres_full, 0);
       mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
       tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * p.BN;
@@ -341,10 +381,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           if (p.dbg & 1) {
             mbar_arrive(&empty[s]);
           } else {
-            const uint64_t sa = (smem0 + s * stage_bytes) >> 4, sb = sa + (a_stage >> 4);
+            const uint64_t sa = (smem0 + s * stage_bytes) >> 4;
+            if (p.mode == MODE_HALO) {
+              // every tap of this channel group reads the same halo planes at a row offset
+              const uint32_t ps16 = p.h_plane_stride >> 4, nj = p.h_cg >> 4;
+              int t = 0;
+              for (int kh = 0; kh < p.h_kh; kh++) {
+                for (int kw = 0; kw < p.h_kw; kw++, t++) {
+                  const uint64_t arow = sa + (uint64_t)(kh * p.h_pitch + kw);
+                  for (uint32_t j = 0; j < nj; j++) {
+                    const int k = t * p.h_cin + kb * p.h_cg + 16 * (int)j;
+                    const uint64_t bd = p.bdesc[(k >> 4) & 3] + ((bres + (uint32_t)(k >> 6) * b_kb_bytes) >> 4);
+                    umma_bf16(tmem_d, p.adesc[0] + arow + 2 * j * ps16, bd, p.idesc,
+                              (kb > kb0 || t > 0 || j > 0) ? 1u : 0u);
+                  }
+                }
+              }
+            } else {
+              const uint64_t sb = p.b_res ? (uint64_t)((bres + kb * b_kb_bytes) >> 4) : sa + (a_stage >> 4);
 #pragma unroll
-            for (int k = 0; k < BK / 16; k++)
-              umma_bf16(tmem_d, p.adesc[k] + sa, p.bdesc[k] + sb, p.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+              for (int k = 0; k < BK / 16; k++)
+                umma_bf16(tmem_d, p.adesc[k] + sa, p.bdesc[k] + sb, p.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            }
             umma_commit(&empty[s]);
           }
           TRACE(2, it);
@@ -538,8 +596,9 @@ long long* g_trace = nullptr;
 
 int launch(GemmParams& p, cudaStream_t stream) {
   if (!g_num_sms) g_num_sms = cvb_num_sms();
-  const uint32_t stage_bytes = (BM + p.BN) * BK * 2;
-  p.stages = (int)((200u * 1024u) / stage_bytes);
+  if (!p.a_stage_bytes) p.a_stage_bytes = BM * BK * 2;
+  const uint32_t stage_bytes = p.a_stage_bytes + (p.b_res ? 0u : (uint32_t)p.BN * BK * 2);
+  p.stages = (int)((200u * 1024u - p.b_res_bytes) / stage_bytes);
   if (p.stages > 8) p.stages = 8;
   static int env_stages = -1, env_dbg = -1;
   if (env_stages < 0) {
@@ -559,7 +618,7 @@ int launch(GemmParams& p, cudaStream_t stream) {
     g_trace = tr;
   }
   if (p.stages < 2) { cvb_set_error("BN too large"); return CVB_EINVAL; }
-  size_t smem = (size_t)p.stages * stage_bytes + 1024 + 256;
+  size_t smem = (size_t)p.stages * stage_bytes + p.b_res_bytes + 1024 + 256;
   if (!g_attr_done) {
     CVB_CUDA(cudaFuncSetAttribute(umma_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     g_attr_done = true;
@@ -572,6 +631,8 @@ int launch(GemmParams& p, cudaStream_t stream) {
     p.adesc[k] = operand_desc(p.a_major, p.a_cel, BM, k);
     p.bdesc[k] = operand_desc(p.b_major, p.b_cel, p.BN, k);
   }
+  if (p.mode == MODE_HALO)   // no-swizzle K-major: LBO = next 8-channel plane, SBO = one halo row
+    p.adesc[0] = desc_tmpl(0, p.h_plane_stride, (uint32_t)p.h_pitch * 16, 0);
   const int units = p.m_tiles * p.n_tiles * p.splits;
   const int grid = units < g_num_sms ? units : g_num_sms;
   umma_gemm_kernel<<<grid, NUM_THREADS, smem, stream>>>(p);
@@ -639,6 +700,48 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
   if (!acel || (stride != 1 && stride != 2) || cout % 8) { cvb_set_error("conv2d_fwd: unsupported shape"); return CVB_EINVAL; }
   static GemmParams p;   // large (boxes table): keep off the stack
   memset(&p, 0, sizeof(p));
+  {
+    // ---- halo path: stride 1, 16-channel multiples, resident weights ----
+    static int no_halo = -1;
+    if (no_halo < 0) no_halo = getenv("CVB_NO_HALO") ? 1 : 0;
+    const int K = kh * kw * cin;
+    const int BN = pick_bn(cout);
+    const uint32_t b_all = (uint32_t)((K + BK - 1) / BK) * BN * BK * 2;
+    const int cg = cin % 64 == 0 ? 64 : cin % 32 == 0 ? 32 : cin % 16 == 0 ? 16 : 0;
+    if (!no_halo && stride == 1 && cg && cout <= 256 && b_all <= 96u * 1024u && kh <= 7 && kw <= 7) {
+      p.mode = MODE_HALO;
+      p.a_major = 0; p.b_major = 0;
+      p.a_cel = 8; p.b_cel = 64;
+      p.gb = 1;
+      p.BN = BN;
+      p.M = n * oh * ow; p.N = cout;
+      p.tw = 8; p.th = 16; p.tn = 1;
+      p.ptiles_w = (ow + 7) / 8;
+      p.ptiles_h = (oh + 15) / 16;
+      p.m_tiles = p.ptiles_w * p.ptiles_h * n;
+      p.n_tiles = 1;
+      p.splits = 1;
+      p.h_cin = cin; p.h_cg = cg; p.h_planes = cg / 8; p.h_pad = pad; p.h_kh = kh; p.h_kw = kw;
+      p.h_pitch = 8 + kw - 1;
+      const int hrows = 16 + kh - 1;
+      p.h_box_bytes = (uint32_t)p.h_pitch * hrows * 16;
+      p.h_plane_stride = (p.h_box_bytes + 127) / 128 * 128;
+      p.a_stage_bytes = (p.h_planes * p.h_plane_stride + 1023) / 1024 * 1024;
+      p.num_kb = cin / cg;
+      p.kb_per_split = p.num_kb;
+      p.OH = oh; p.OW = ow; p.NIMG = n;
+      p.b_res = 1;
+      p.b_res_bytes = b_all;
+      p.b_slabs = (K + BK - 1) / BK;
+      p.tx_bytes = p.h_planes * p.h_box_bytes;
+      int rc;
+      if ((rc = encode_nhwc(&p.mapA[0], x, n, h, w, cin, xcs, 8, p.h_pitch, hrows, 1))) return rc;
+      if ((rc = encode_2d(&p.mapB[0], wt, cout, K, K, p.b_cel, p.BN))) return rc;
+      p.out_mode = OUT_NHWC; p.out_f32 = y_f32; p.out = y; p.ldc = ycs; p.col_off = yoff; p.bias = bias;
+      p.accum = accumulate;
+      return launch(p, (cudaStream_t)stream);
+    }
+  }
   p.mode = MODE_FWD;
   p.a_major = 0; p.b_major = 0;
   p.a_cel = acel;
@@ -664,7 +767,12 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
   p.nbox = p.num_kb * p.ga;
   if (p.nbox > MAX_BOXES) { cvb_set_error("conv2d_fwd: K too large for the box table"); return CVB_EINVAL; }
   for (int i = 0; i < p.nbox; i++) p.boxtab[i] = gather_entry((i / p.ga) * BK + (i % p.ga) * acel, cin, kh * kw, kw, pad, stride);
-  p.tx_bytes = p.ga * bw * bh * bnn * p.a_cel * 2 + p.gb * p.BN * p.b_cel * 2;
+  // small weight operands stay resident in smem for the CTA's whole tile loop
+  const uint32_t b_all = (uint32_t)p.num_kb * p.BN * BK * 2;
+  p.b_res = (p.n_tiles == 1 && b_all <= 96u * 1024u) ? 1 : 0;
+  p.b_res_bytes = p.b_res ? b_all : 0;
+  p.b_slabs = p.num_kb;
+  p.tx_bytes = p.ga * bw * bh * bnn * p.a_cel * 2 + (p.b_res ? 0 : p.gb * p.BN * p.b_cel * 2);
   int rc;
   if (stride == 1) {
     if ((rc = encode_nhwc(&p.mapA[0], x, n, h, w, cin, xcs, acel, bw, bh, bnn))) return rc;
@@ -724,6 +832,7 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
   if (p.nbox > MAX_BOXES) { cvb_set_error("conv2d_wgrad: N too large for the box table"); return CVB_EINVAL; }
   for (int i = 0; i < p.nbox; i++) p.boxtab[i] = gather_entry(i * bcel, cin, kh * kw, kw, pad, stride);
   p.tx_bytes = p.ga * BK * acel * 2 + p.gb * BK * bcel * 2;
+  p.a_box_bytes = BK * acel * 2;
   int rc;
   if ((rc = encode_nhwc(&p.mapA[0], dy, n, oh, ow, cout, dycs, acel, bw, bh, bnn))) return rc;
   if (stride == 1) {
@@ -831,6 +940,55 @@ CVB_API long long cvb_debug_mma_cycles(int n_mma, int bn, int commit_every) {
   cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
   cudaFree(d);
   return h;
+}
+
+// ---- microbenchmark of the TMA issue rate (debug aid) -----------------------------------
+struct TmaProbe { CUtensorMap map; };
+__global__ void __launch_bounds__(32, 1) tma_rate_kernel(const __grid_constant__ TmaProbe tp, int n_tma, int dims,
+                                                        int box_bytes, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+  __syncwarp();
+  const bool leader = elect_one();
+  long long t0 = clock64();
+  if (leader) {
+    prefetch_map(&tp.map);
+    mbar_expect_tx(&bar, (uint32_t)n_tma * box_bytes);
+    for (int i = 0; i < n_tma; i++) {
+      const uint32_t dst = smem_u32(smem) + (i & 7) * box_bytes;
+      if (dims == 4) tma_load_4d(&tp.map, dst, &bar, 0, (i & 3), (i >> 2) & 3, 0);
+      else tma_load_2d(&tp.map, dst, &bar, 0, (i & 15) * 8);
+    }
+  }
+  __syncwarp();
+  long long t1 = clock64();
+  mbar_wait(&bar, 0);
+  long long t2 = clock64();
+  if (leader) { out[0] = t1 - t0; out[1] = t2 - t0; }
+}
+
+// returns issue cycles for n_tma loads (low 32 bits: issue, high: until all landed)
+CVB_API long long cvb_debug_tma_cycles(int n_tma, int dims, int cel) {
+  if (get_encoder()) return -1;
+  TmaProbe tp;
+  void* buf = nullptr;
+  cudaMalloc(&buf, 64 << 20);
+  int rc;
+  if (dims == 4) rc = encode_nhwc(&tp.map, buf, 4, 64, 64, 64, 64, cel, 32, 4, 1);
+  else rc = encode_2d(&tp.map, buf, 4096, 4096, 4096, cel, 128);
+  if (rc) { cudaFree(buf); return -2; }
+  const int box_bytes = dims == 4 ? 128 * cel * 2 : 128 * cel * 2;
+  long long* d = nullptr;
+  long long h[2] = {-1, -1};
+  cudaMalloc(&d, 16);
+  cudaFuncSetAttribute(tma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  tma_rate_kernel<<<1, 32, 8 * box_bytes + 1024>>>(tp, n_tma, dims, box_bytes, d);
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  cudaFree(buf);
+  return (h[1] << 32) | (h[0] & 0xffffffff);
 }
 
 CVB_API int cvb_debug_trace(long long* host_out) {
