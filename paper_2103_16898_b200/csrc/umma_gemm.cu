@@ -84,6 +84,7 @@ struct GemmParams {
   int nbox;
   // MODE_HALO geometry
   int h_cin, h_cg, h_planes, h_pitch, h_pad, h_kh, h_kw;
+  int h_mps;                    // MMAs per stage (taps * cg/16); boxtab holds their offsets
   uint32_t h_plane_stride;      // bytes between 8-channel planes (>= halo pixels * 16, 128-aligned)
   uint32_t h_box_bytes;         // bytes TMA writes per plane
   uint32_t boxtab[MAX_BOXES];   // packed (map, channel, dw, dh) per gathered box
@@ -383,19 +384,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           } else {
             const uint64_t sa = (smem0 + s * stage_bytes) >> 4;
             if (p.mode == MODE_HALO) {
-              // every tap of this channel group reads the same halo planes at a row offset
-              const uint32_t ps16 = p.h_plane_stride >> 4, nj = p.h_cg >> 4;
-              int t = 0;
-              for (int kh = 0; kh < p.h_kh; kh++) {
-                for (int kw = 0; kw < p.h_kw; kw++, t++) {
-                  const uint64_t arow = sa + (uint64_t)(kh * p.h_pitch + kw);
-                  for (uint32_t j = 0; j < nj; j++) {
-                    const int k = t * p.h_cin + kb * p.h_cg + 16 * (int)j;
-                    const uint64_t bd = p.bdesc[(k >> 4) & 3] + ((bres + (uint32_t)(k >> 6) * b_kb_bytes) >> 4);
-                    umma_bf16(tmem_d, p.adesc[0] + arow + 2 * j * ps16, bd, p.idesc,
-                              (kb > kb0 || t > 0 || j > 0) ? 1u : 0u);
-                  }
-                }
+              // every tap of this channel group reads the same halo planes at a row offset;
+              // per-MMA (A row offset, B slab offset) pairs are precomputed on the host
+              const uint32_t* tab = p.boxtab + kb * p.h_mps;
+              const uint64_t a0 = p.adesc[0] + sa, b0 = p.bdesc[0] + (bres >> 4);
+              for (int i = 0; i < p.h_mps; i++) {
+                const uint32_t e = tab[i];
+                umma_bf16(tmem_d, a0 + (e & 0xFFFFu), b0 + (e >> 16), p.idesc, (kb > kb0 || i > 0) ? 1u : 0u);
               }
             } else {
               const uint64_t sb = p.b_res ? (uint64_t)((bres + kb * b_kb_bytes) >> 4) : sa + (a_stage >> 4);
@@ -733,6 +728,19 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
       p.b_res = 1;
       p.b_res_bytes = b_all;
       p.b_slabs = (K + BK - 1) / BK;
+      // per-MMA descriptor offsets (16-byte units): A = tap row offset + 8-channel plane pair,
+      // B = 64-wide K slab + 32-byte step inside the 128-byte swizzled row
+      const int nj = cg / 16;
+      p.h_mps = kh * kw * nj;
+      if (p.num_kb * p.h_mps > MAX_BOXES) { cvb_set_error("conv2d_fwd: halo MMA table overflow"); return CVB_EINVAL; }
+      for (int g = 0; g < p.num_kb; g++)
+        for (int t = 0; t < kh * kw; t++)
+          for (int j = 0; j < nj; j++) {
+            const int kk = t * cin + g * cg + 16 * j;
+            const uint32_t aoff = (uint32_t)((t / kw) * p.h_pitch + (t % kw)) + 2u * j * (p.h_plane_stride >> 4);
+            const uint32_t boff = (uint32_t)(kk >> 6) * (uint32_t)(BN * BK * 2 / 16) + 2u * ((kk >> 4) & 3);
+            p.boxtab[g * p.h_mps + t * nj + j] = aoff | (boff << 16);
+          }
       p.tx_bytes = p.h_planes * p.h_box_bytes;
       int rc;
       if ((rc = encode_nhwc(&p.mapA[0], x, n, h, w, cin, xcs, 8, p.h_pitch, hrows, 1))) return rc;
@@ -905,8 +913,9 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int n_mma, int bn, int
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = slot;
-  if (warp == 0) {
+  const uint32_t tmem = slot + (commit_every < 0 && warp == 4 ? 128u : 0u);
+  if (commit_every < 0) commit_every = 0;
+  if (warp == 0 || (blockDim.x > 128 && warp == 4)) {
     const bool leader = elect_one();
     const uint64_t sa = smem_u32(smem) >> 4, sb = sa + (16384 >> 4);
     const uint64_t d0 = (uint64_t)1 | ((uint64_t)64 << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
@@ -925,18 +934,19 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int n_mma, int bn, int
     __syncwarp();
     mbar_wait(&bar, phase);
     long long t1 = clock64();
-    if (leader) *out = t1 - t0;
+    if (leader && warp == 0) *out = t1 - t0;
   }
   __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(slot), "r"(256));
 }
 
+// commit_every < 0: two issuing warps (0 and 4), each with its own accumulator
 CVB_API long long cvb_debug_mma_cycles(int n_mma, int bn, int commit_every) {
   long long* d = nullptr;
   long long h = -1;
   cudaMalloc(&d, 8);
   cudaFuncSetAttribute(mma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-  mma_rate_kernel<<<1, 128, 64 * 1024>>>(n_mma, bn, commit_every, d);
+  mma_rate_kernel<<<1, commit_every < 0 ? 160 : 128, 64 * 1024>>>(n_mma, bn, commit_every, d);
   cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
   cudaFree(d);
   return h;
