@@ -62,11 +62,12 @@ def make_shards(n_shards, batch, seed, key, spec):
 
     c, h, w = spec["c"], spec["h"], spec["w"]
     rng = np.random.default_rng(seed)
-    templ = np.random.default_rng(0).normal(size=(10, c * h * w)).astype(np.float32)
+    classes = 2 if c == 1 else 10     # medical: binary diagnosis; CIFAR: 10 classes
+    templ = np.random.default_rng(0).normal(size=(classes, c * h * w)).astype(np.float32)
     aes = AESGCM(key)
     shards = []
     for i in range(n_shards):
-        labels = rng.integers(0, 10, size=batch).astype(np.uint8)
+        labels = rng.integers(0, classes, size=batch).astype(np.uint8)
         noise = rng.integers(-52, 53, size=(batch, c * h * w), dtype=np.int16)
         px = np.clip(128 + 40 * templ[labels] + noise, 0, 255).astype(np.uint8)
         pt = np.concatenate([labels[:, None], px], axis=1).tobytes()
@@ -208,7 +209,8 @@ def run_ours(args, rank, world, local_rank):
     spec = CIFAR
     key = bytes(range(32))
     B = args.batch
-    tr = EncryptedTrainer(args.model, key, batch=B, spec=spec, seed=0, world=world, rank=rank)
+    tr = EncryptedTrainer(args.model, key, batch=B, spec=spec, seed=0, world=world, rank=rank,
+                          force_allreduce=bool(os.environ.get("CVB_FORCE_DIST")))
     shards = make_shards(args.shards, B, 1000 + rank, key, spec)
     # resident ciphertext + AADs in HBM (inputs larger than L2)
     cts = [torch.frombuffer(bytearray(s[3]), dtype=torch.uint8).to(dev) for s in shards]
@@ -324,13 +326,14 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if world > 1:
+    force = bool(os.environ.get("CVB_FORCE_DIST"))   # exercise the NCCL path even at world 1
+    if world > 1 or force:
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     run_ours(args, rank, world, local_rank)
-    if world > 1:
+    if world > 1 or force:
         import torch.distributed as dist
 
         dist.destroy_process_group()

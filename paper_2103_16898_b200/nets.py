@@ -445,8 +445,14 @@ class BNAct:
         scratch.bn_floats = max(scratch.bn_floats, K._lib_bound().cvb_bn_workspace_floats(rows, self.C))
         self.scratch = scratch
 
+    def use_stats(self, mean, rstd):
+        """Share precomputed per-channel batch statistics (DenseNet: every BN over a concat
+        prefix sees the same per-channel mean/var -- computed once per produced slice)."""
+        self.mean, self.rstd = mean, rstd
+        self.shared = True
+
     def forward(self, ps, x, xcs, y, ycs, stats=True):
-        if stats:
+        if stats and not getattr(self, "shared", False):
             K.bn_stats(x, self.rows, self.C, xcs, self.scratch.bnws, self.mean, self.rstd, run_mean=self.run_mean,
                        run_var=self.run_var)
         K.bn_apply(x, self.rows, self.C, xcs, self.mean, self.rstd, ps.p[self.G], ps.p[self.B], y, ycs,
@@ -511,26 +517,31 @@ class DenseLayer:
         self.conv1.build(n, h, w, S)
         self.bn2.build(rows, S, dev)
         self.conv2.build(n, h, w, S)
-        self.z1 = torch.empty(n, h, w, self.mid, dtype=BF16, device=dev)   # kept for backward
+        # kept for backward (no recompute): BN1/BN2 outputs and the 1x1 conv output
+        self.z1 = torch.empty(n, h, w, self.mid, dtype=BF16, device=dev)
+        self.y1 = torch.empty(n, h, w, self.cin, dtype=BF16, device=dev)
+        self.y2 = torch.empty(n, h, w, self.mid, dtype=BF16, device=dev)
 
-    def forward(self, ps, blk, y1, y2):
+    def forward(self, ps, blk, y1=None, y2=None):
         cs = blk.shape[-1]
-        self.bn1.forward(ps, blk, cs, y1, self.cin)
-        self.conv1.forward(ps, y1, self.z1)
-        self.bn2.forward(ps, self.z1, self.mid, y2, self.mid)
-        self.conv2.forward(ps, y2, blk, out_coff=self.cin)
+        self.bn1.forward(ps, blk, cs, self.y1, self.cin)
+        self.conv1.forward(ps, self.y1, self.z1)
+        self.bn2.forward(ps, self.z1, self.mid, self.y2, self.mid)
+        self.conv2.forward(ps, self.y2, blk, out_coff=self.cin)
+        # batch statistics of the 32 new channels, shared by every later BN over this block
+        m, r = self.slice_stats
+        K.bn_stats(blk[..., self.cin:], self.bn1.rows, self.growth, cs, self.bn1.scratch.bnws, m, r)
 
     def backward(self, ps, blk, dblk32, y1, y2, dz2, dy2, dz1, dy1):
         cs = blk.shape[-1]
         rows = self.bn1.rows
+        y1, y2 = self.y1, self.y2
         # gradient of this layer's output slice is complete (later layers already added)
         K.cast_rows(dblk32[..., self.cin:], cs, dz2, self.growth, rows, self.growth)
-        self.bn2.forward(ps, self.z1, self.mid, y2, self.mid, stats=False)     # recompute y2
         self.conv2.backward(ps, dz2, y2, dx=dy2)
         K.bn_backward(dy2, self.mid, self.z1, self.mid, rows, self.mid, self.bn2.mean, self.bn2.rstd,
                       ps.p[self.bn2.G], ps.p[self.bn2.B], self.bn2.scratch.bnws, ps.g[self.bn2.G], ps.g[self.bn2.B],
                       relu=True, dx=dz1, dxcs=self.mid)
-        self.bn1.forward(ps, blk, cs, y1, self.cin, stats=False)               # recompute y1
         self.conv1.backward(ps, dz1, y1, dx=dy1)
         self.bn1.backward(ps, dy1, self.cin, blk, cs, dblk32, cs, accumulate=True)
 
@@ -572,10 +583,17 @@ class DenseNet121(Net):
         self.da0 = e(n, oh, ow, self.stem.cout)
         h, w = (oh + 2 - 3) // 2 + 1, (ow + 2 - 3) // 2 + 1
         self.geo, self.bufs, self.dbufs = [], [], []
+        self.bmean, self.brstd, self.ty = [], [], []
         ymax = 0
         for bi, (c0, c1, layers) in enumerate(self.blocks):
+            bm = torch.zeros(c1, dtype=F32, device=dev)
+            br = torch.zeros(c1, dtype=F32, device=dev)
+            self.bmean.append(bm)
+            self.brstd.append(br)
             for L in layers:
                 L.build(n, h, w, S, dev)
+                L.bn1.use_stats(bm[:L.cin], br[:L.cin])
+                L.slice_stats = (bm[L.cin:L.cin + L.growth], br[L.cin:L.cin + L.growth])
             self.geo.append((h, w))
             self.bufs.append(e(n, h, w, c1))
             self.dbufs.append(torch.empty(n, h, w, c1, dtype=F32, device=dev))
@@ -583,9 +601,12 @@ class DenseNet121(Net):
             if bi < len(self.trans):
                 bn, conv = self.trans[bi]
                 bn.build(n * h * w, S, dev)
+                bn.use_stats(bm, br)
                 conv.build(n, h, w, S)
+                self.ty.append(e(n, h, w, c1))            # transition BN output, kept for backward
                 h, w = h // 2, w // 2
         self.norm5.build(n * h * w, S, dev)
+        self.norm5.use_stats(self.bmean[-1], self.brstd[-1])
         self.head.build(n, S)
         # shared scratch (largest use wins)
         mid = max(L.mid for _, _, ls in self.blocks for L in ls)
@@ -610,20 +631,26 @@ class DenseNet121(Net):
     def forward(self, x):
         ps, n = self.ps, self.batch
         self.stem.forward(ps, x, self.a0)
-        K.maxpool_fwd(self.a0, 3, 2, 1, self.bufs[0][..., :self.stem.cout])
+        c0 = self.stem.cout
+        K.maxpool_fwd(self.a0, 3, 2, 1, self.bufs[0][..., :c0])
+        h, w = self.geo[0]
+        K.bn_stats(self.bufs[0], n * h * w, c0, self.bufs[0].shape[-1], self.scratch.bnws, self.bmean[0][:c0],
+                   self.brstd[0][:c0])
         for bi, (c0, c1, layers) in enumerate(self.blocks):
             h, w = self.geo[bi]
             blk = self.bufs[bi]
             for L in layers:
-                L.forward(ps, blk, self._v(self.y1, n, h, w, L.cin), self._v(self.y2, n, h, w, L.mid))
+                L.forward(ps, blk)
             if bi < len(self.trans):
                 bn, conv = self.trans[bi]
-                y = self._v(self.y1, n, h, w, c1)
+                y = self.ty[bi]
                 bn.forward(ps, blk, c1, y, c1)
                 t = self._v(self.t, n, h, w, c1 // 2)
                 conv.forward(ps, y, t)
                 nxt = self.bufs[bi + 1]
                 K.avgpool_fwd(t, n, h, w, c1 // 2, c1 // 2, 2, nxt, nxt.shape[-1])
+                K.bn_stats(nxt, n * (h // 2) * (w // 2), c1 // 2, nxt.shape[-1], self.scratch.bnws,
+                           self.bmean[bi + 1][:c1 // 2], self.brstd[bi + 1][:c1 // 2])
         h, w = self.geo[-1]
         c = self.final_c
         self.norm5.forward(ps, self.bufs[-1], c, self._v(self.y5, n, h, w, c), c)
@@ -651,8 +678,7 @@ class DenseNet121(Net):
                 K.cast_rows(nxt_d, nxt_d.shape[-1], dp, c1 // 2, n * oh * ow, c1 // 2)
                 dt = self._v(self.dt, n, h, w, c1 // 2)
                 K.avgpool_bwd(dp, n, h, w, c1 // 2, 2, dt, c1 // 2)
-                y = self._v(self.y1, n, h, w, c1)
-                bn.forward(ps, blk, c1, y, c1, stats=False)
+                y = self.ty[bi]
                 dy = self._v(self.dy1, n, h, w, c1)
                 conv.backward(ps, dt, y, dx=dy)
                 bn.backward(ps, dy, c1, blk, c1, dblk, c1, accumulate=False)

@@ -48,14 +48,14 @@ class GradAllReduce:
 
 class EncryptedTrainer:
     def __init__(self, model="small_cnn", key: bytes = bytes(range(32)), batch=512, spec=CIFAR, seed=0,
-                 world=1, rank=0, max_shard_bytes=None, lr=1e-3):
+                 world=1, rank=0, max_shard_bytes=None, lr=1e-3, force_allreduce=False):
         self.spec, self.batch, self.world, self.rank = spec, batch, world, rank
         self.net = make_model(model, seed=seed).build(batch, global_batch=batch * world)
         self.net.lr = lr
         self.ctx = GcmContext(key)
         rec = record_bytes(spec["c"], spec["h"], spec["w"])
         self.loader = ShardLoader(self.ctx, max_shard_bytes or batch * rec, batch, spec)
-        self.allreduce = GradAllReduce(self.net.ps.g32) if world > 1 else None
+        self.allreduce = GradAllReduce(self.net.ps.g32) if (world > 1 or force_allreduce) else None
         self.graph = None
         self.status_host = torch.zeros(8, dtype=torch.int32).pin_memory()
         self.loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()

@@ -13,9 +13,12 @@ from bench import make_shards  # noqa: E402
 
 model = sys.argv[1] if len(sys.argv) > 1 else "small_cnn"
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 512
+from paper_2103_16898_b200.loader import MEDICAL  # noqa: E402
+
+spec = MEDICAL if model == "densenet121" else CIFAR
 key = bytes(range(32))
-tr = EncryptedTrainer(model, key, batch=B, spec=CIFAR)
-sh = make_shards(2, B, 1, key, CIFAR)
+tr = EncryptedTrainer(model, key, batch=B, spec=spec)
+sh = make_shards(2, B, 1, key, spec)
 ct = [torch.frombuffer(bytearray(s[3]), dtype=torch.uint8).cuda() for s in sh]
 aad = [torch.frombuffer(bytearray(s[2]), dtype=torch.uint8).cuda() for s in sh]
 for i in range(3):

@@ -72,6 +72,14 @@ def test_dense_block_and_transition():
     x0 = torch.randn(n, h, w, c0, generator=g).bfloat16()
     blk = torch.zeros(n, h, w, c1, dtype=torch.bfloat16, device="cuda")
     blk[..., :c0] = x0.cuda()
+    from paper_2103_16898_b200 import kernels as K
+
+    bm, br = torch.zeros(c1, device="cuda"), torch.zeros(c1, device="cuda")
+    for L in layers:
+        L.bn1.use_stats(bm[:L.cin], br[:L.cin])
+        L.slice_stats = (bm[L.cin:L.cin + gr], br[L.cin:L.cin + gr])
+    tbn.use_stats(bm, br)
+    K.bn_stats(blk, n * h * w, c0, c1, S.bnws, bm[:c0], br[:c0])
     y1, y2 = e(n * h * w * c1), e(n * h * w * 128)
     for L in layers:
         L.forward(ps, blk, y1[:n * h * w * L.cin].view(n, h, w, L.cin), y2.view(n, h, w, 128))
@@ -82,7 +90,6 @@ def test_dense_block_and_transition():
     dt = torch.randn(n, h, w, c1 // 2, generator=g).bfloat16()
     dblk = torch.empty(n, h, w, c1, dtype=torch.float32, device="cuda")
     dy = e(n, h, w, c1)
-    tbn.forward(ps, blk, c1, y, c1, stats=False)
     tconv.backward(ps, dt.cuda(), y, dx=dy)
     tbn.backward(ps, dy, c1, blk, c1, dblk, c1, accumulate=False)
     dz2, dy2, dz1, dy1 = e(n * h * w * gr), e(n * h * w * 128), e(n * h * w * 128), e(n * h * w * c1)
