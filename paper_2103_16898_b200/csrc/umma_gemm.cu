@@ -48,7 +48,8 @@ constexpr int MAX_BOXES = 512;   // box-table entries
 struct GemmParams {
   CUtensorMap mapA[4];
   CUtensorMap mapB[4];
-  uint64_t adesc[4], bdesc[4];   // UMMA descriptor templates, start address relative to the stage
+  uint64_t adesc[8], bdesc[8];   // UMMA descriptor templates, start address relative to the stage
+  int kr, ksteps;                // K rows per stage of MN-major operands (64 / 128), MMAs per stage
   int mode;
   int a_major, b_major;     // 0 = K-major, 1 = MN-major
   int a_cel, b_cel;         // elements per box row (8,16,32,64)
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t a_stage = p.a_stage_bytes;         // 16 KB (halo mode: planes * plane stride)
-  const uint32_t b_stage = p.b_res ? 0u : p.BN * BK * 2;
+  const uint32_t b_stage = p.b_res ? 0u : p.BN * p.kr * 2;
   const uint32_t stage_bytes = a_stage + b_stage;
   const uint32_t b_kb_bytes = p.BN * BK * 2;        // resident B: one K-block slab
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes + p.b_res_bytes);
@@ -395,7 +396,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
             } else {
               const uint64_t sb = p.b_res ? (uint64_t)((bres + kb * b_kb_bytes) >> 4) : sa + (a_stage >> 4);
 #pragma unroll
-              for (int k = 0; k < BK / 16; k++)
+              for (int k = 0; k < p.ksteps; k++)
                 umma_bf16(tmem_d, p.adesc[k] + sa, p.bdesc[k] + sb, p.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
             }
             umma_commit(&empty[s]);
@@ -574,15 +575,15 @@ uint32_t layout_of(int rowbytes) { return rowbytes == 128 ? 2u : rowbytes == 64 
 // Descriptor template of MMA k-step s (16 K elements) of one operand stage.
 //   K-major : `rows` rows per box, boxes of cel K-elements at stride rows*R
 //   MN-major: boxes of cel MN-elements x 64 K-rows at stride 64*R
-uint64_t operand_desc(int major, int cel, int rows, int s) {
+uint64_t operand_desc(int major, int cel, int rows, int s, int krows = 64) {
   const int R = cel * 2;
   if (major == 0) {
     if (R == 16) return desc_tmpl(2 * s * rows * 16, rows * 16, 128, 0);
     const int kb = 32 * s;
     return desc_tmpl((kb / R) * rows * R + (kb % R), 16, 8 * R, layout_of(R));
   }
-  if (R == 16) return desc_tmpl(s * 256, 128, 64 * 16, 0);
-  return desc_tmpl(s * 16 * R, 64 * R, 8 * R, layout_of(R));
+  if (R == 16) return desc_tmpl(s * 256, 128, krows * 16, 0);
+  return desc_tmpl(s * 16 * R, krows * R, 8 * R, layout_of(R));
 }
 
 int g_num_sms = 0;
@@ -591,9 +592,11 @@ long long* g_trace = nullptr;
 
 int launch(GemmParams& p, cudaStream_t stream) {
   if (!g_num_sms) g_num_sms = cvb_num_sms();
-  if (!p.a_stage_bytes) p.a_stage_bytes = BM * BK * 2;
-  const uint32_t stage_bytes = p.a_stage_bytes + (p.b_res ? 0u : (uint32_t)p.BN * BK * 2);
-  p.stages = (int)((200u * 1024u - p.b_res_bytes) / stage_bytes);
+  if (!p.kr) p.kr = BK;
+  p.ksteps = p.kr / 16;
+  if (!p.a_stage_bytes) p.a_stage_bytes = BM * p.kr * 2;
+  const uint32_t stage_bytes = p.a_stage_bytes + (p.b_res ? 0u : (uint32_t)p.BN * p.kr * 2);
+  p.stages = (int)((220u * 1024u - p.b_res_bytes) / stage_bytes);
   if (p.stages > 8) p.stages = 8;
   static int env_stages = -1, env_dbg = -1;
   if (env_stages < 0) {
@@ -620,11 +623,11 @@ int launch(GemmParams& p, cudaStream_t stream) {
   }
   p.idesc = make_idesc(p.a_major, p.b_major, p.BN);
   // smem box strides and descriptor templates
-  p.a_box_stride = p.a_major == 0 ? BM * p.a_cel * 2 : BK * p.a_cel * 2;
-  p.b_box_stride = p.b_major == 0 ? p.BN * p.b_cel * 2 : BK * p.b_cel * 2;
-  for (int k = 0; k < 4; k++) {
-    p.adesc[k] = operand_desc(p.a_major, p.a_cel, BM, k);
-    p.bdesc[k] = operand_desc(p.b_major, p.b_cel, p.BN, k);
+  p.a_box_stride = p.a_major == 0 ? BM * p.a_cel * 2 : p.kr * p.a_cel * 2;
+  p.b_box_stride = p.b_major == 0 ? p.BN * p.b_cel * 2 : p.kr * p.b_cel * 2;
+  for (int k = 0; k < p.ksteps; k++) {
+    p.adesc[k] = operand_desc(p.a_major, p.a_cel, BM, k, p.kr);
+    p.bdesc[k] = operand_desc(p.b_major, p.b_cel, p.BN, k, p.kr);
   }
   if (p.mode == MODE_HALO)   // no-swizzle K-major: LBO = next 8-channel plane, SBO = one halo row
     p.adesc[0] = desc_tmpl(0, p.h_plane_stride, (uint32_t)p.h_pitch * 16, 0);
@@ -660,10 +663,11 @@ void pick_mbox(int n, int oh, int ow, int& bw, int& bh, int& bn) {
 int next_pow2(int x) { int q = 1; while (q < x) q <<= 1; return q; }
 
 // pixel box for a 64-pixel K chunk (wgrad): exact 64 rows, OOB rows zero-filled by TMA
-void pick_kbox(int oh, int ow, int& bw, int& bh, int& bn) {
-  bw = next_pow2(ow) < 64 ? next_pow2(ow) : 64;
-  bh = 64 / bw < next_pow2(oh) ? 64 / bw : next_pow2(oh);
-  bn = 64 / (bw * bh);
+void pick_kbox(int oh, int ow, int rows, int& bw, int& bh, int& bn) {
+  bw = next_pow2(ow) < rows ? next_pow2(ow) : rows;
+  if (bw > 256) bw = 256;
+  bh = rows / bw < next_pow2(oh) ? rows / bw : next_pow2(oh);
+  bn = rows / (bw * bh);
 }
 
 // gathered-operand box: tap -> (parity map, dw, dh) for the conv geometry
@@ -817,8 +821,14 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
   p.ga = BM / p.a_cel;
   p.gb = p.BN / p.b_cel;
   p.M = cout; p.N = Ncols;
+  // 128 pixels per K-block halves the TMA issues per pixel (TMA issue, not the tensor core,
+  // bounds these wgrads); measured better even when only 2 stages fit
+  static int env_kr = -1;
+  if (env_kr < 0) { const char* e = getenv("CVB_WGRAD_KR"); env_kr = e ? atoi(e) : 0; }
+  p.kr = (BM + p.BN) * 128 * 2 * 2 <= 220 * 1024 ? 128 : 64;
+  if (env_kr == 64 || env_kr == 128) p.kr = env_kr;
   int bw, bh, bnn;
-  pick_kbox(oh, ow, bw, bh, bnn);
+  pick_kbox(oh, ow, p.kr, bw, bh, bnn);
   p.tw = bw; p.th = bh; p.tn = bnn;
   p.ptiles_w = (ow + bw - 1) / bw;
   p.ptiles_h = (oh + bh - 1) / bh;
@@ -839,8 +849,8 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
   p.nbox = p.n_tiles * p.gb;
   if (p.nbox > MAX_BOXES) { cvb_set_error("conv2d_wgrad: N too large for the box table"); return CVB_EINVAL; }
   for (int i = 0; i < p.nbox; i++) p.boxtab[i] = gather_entry(i * bcel, cin, kh * kw, kw, pad, stride);
-  p.tx_bytes = p.ga * BK * acel * 2 + p.gb * BK * bcel * 2;
-  p.a_box_bytes = BK * acel * 2;
+  p.tx_bytes = p.ga * p.kr * acel * 2 + p.gb * p.kr * bcel * 2;
+  p.a_box_bytes = p.kr * acel * 2;
   int rc;
   if ((rc = encode_nhwc(&p.mapA[0], dy, n, oh, ow, cout, dycs, acel, bw, bh, bnn))) return rc;
   if (stride == 1) {
