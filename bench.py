@@ -46,11 +46,32 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--model", default="small_cnn")
-    ap.add_argument("--batch", type=int, default=512)
-    ap.add_argument("--shards", type=int, default=96)
+    ap.add_argument("--batch", type=int, default=None, help="per-GPU batch (default: 512, DenseNet 128)")
+    ap.add_argument("--shards", type=int, default=None, help="resident shards per rank (default: > 150 MB)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.batch is None:
+        a.batch = 128 if a.model == "densenet121" else 512
+    return a
+
+
+# BASELINE.json configs each model is the bench line of
+WORKLOADS = {
+    "small_cnn": ("configs[1]", "paper-shaped small CNN (4 conv+BN, 2 FC, Adam)", "CIFAR-10-shaped 32x32x3, 10 classes"),
+    "resnet18": ("configs[2]", "ResNet-18 (CIFAR variant)", "CIFAR-10-shaped 32x32x3, 10 classes"),
+    "densenet121": ("configs[3]", "DenseNet-121-style CNN (1-channel stem)", "medical-imaging-shaped 224x224x1, binary"),
+}
+
+
+def spec_for(model):
+    from paper_2103_16898_b200.loader import CIFAR, MEDICAL
+
+    return MEDICAL if model == "densenet121" else CIFAR
+
+
+def rec_bytes(spec):
+    return 1 + spec["c"] * spec["h"] * spec["w"]
 
 
 # ---------------------------------------------------------------------------------------
@@ -78,44 +99,53 @@ def make_shards(n_shards, batch, seed, key, spec):
     return shards
 
 
-def clocks_sampler(dev_index):
-    try:
-        return subprocess.Popen(
-            ["nvidia-smi", f"--id={dev_index}",
-             "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
-            stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-    except Exception:
-        return None
+class ClockSampler:
+    """NVML clock + throttle-reason sampling in a background thread (every ~5 ms) while the
+    timed region runs (nvidia-smi's 200 ms floor is longer than a small-CNN timed region)."""
 
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
-def clocks_summary(proc):
-    if proc is None:
-        return None
-    proc.terminate()
-    try:
-        out, _ = proc.communicate(timeout=5)
-    except Exception:
-        proc.kill()
-        return None
-    sm, mx, reasons = [], 0.0, set()
-    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-    for line in out.strip().splitlines():
-        f = [x.strip() for x in line.split(",")]
-        if len(f) < 7:
-            continue
+    def __init__(self, dev_index, period=0.005):
+        import threading
+
+        self.sm, self.reasons, self.mx, self.ok = [], set(), 0.0, False
         try:
-            sm.append(float(f[0]))
-            mx = max(mx, float(f[1]))
-        except ValueError:
-            continue
-        for nm, v in zip(names, f[3:7]):
-            if v.lower() == "active":
-                reasons.add(nm)
-    if not sm:
-        return None
-    return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self.ok = True
+        except Exception:
+            return
+        self.period, self.stop_ev = period, threading.Event()
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop_ev.is_set():
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for nm, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(nm)
+            except Exception:
+                pass
+            self.stop_ev.wait(self.period)
+
+    def summary(self):
+        if not self.ok:
+            return None
+        self.stop_ev.set()
+        self.th.join(timeout=2)
+        if not self.sm:
+            return None
+        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": self.mx, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": "nvml, sampled during the timed region"}
 
 
 def peaks():
@@ -177,17 +207,16 @@ def cpu_reference(model, batch, key, spec, seconds, steps=None, warmup=0):
 
 
 def run_reference(args, rank, world):
-    from paper_2103_16898_b200.loader import CIFAR
-
     if rank != 0:
         return
     key = bytes(range(32))
-    v, cores, sample, t = cpu_reference(args.model, args.batch, key, CIFAR, 0, steps=args.steps,
+    cfg, mname, dname = WORKLOADS[args.model]
+    v, cores, sample, t = cpu_reference(args.model, args.batch, key, spec_for(args.model), 0, steps=args.steps,
                                         warmup=args.warmup)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / max(1, args.steps),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-            "config": {"workload": f"{args.model} CIFAR-10-shaped, batch {args.batch}, sealed shards (CPU reference)",
+            "config": {"workload": f"{cfg}: {mname}, {dname} sealed shards, batch {args.batch} (CPU reference)",
                        "model": args.model, "global_batch": args.batch, "seq_len": None, "parallelism": "cpu"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -201,14 +230,17 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
 
     from paper_2103_16898_b200 import kernels as K
-    from paper_2103_16898_b200.loader import CIFAR
     from paper_2103_16898_b200.trainer import EncryptedTrainer
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    spec = CIFAR
+    spec = spec_for(args.model)
     key = bytes(range(32))
     B = args.batch
+    rb = rec_bytes(spec)
+    if args.shards is None:   # enough resident ciphertext to exceed the 126 MB L2
+        args.shards = max(4, -(-160_000_000 // (B * rb + 16)))
+    cfg, mname, dname = WORKLOADS[args.model]
     tr = EncryptedTrainer(args.model, key, batch=B, spec=spec, seed=0, world=world, rank=rank,
                           force_allreduce=bool(os.environ.get("CVB_FORCE_DIST")))
     shards = make_shards(args.shards, B, 1000 + rank, key, spec)
@@ -247,9 +279,9 @@ def run_ours(args, rank, world, local_rank):
     for i in range(args.warmup):
         resident(i)
     launches0 = K.REC.launches
-    clk = clocks_sampler(local_rank) if rank == 0 else None
+    clk = ClockSampler(local_rank) if rank == 0 else None
     ms = timed(resident, args.steps)
-    clocks = clocks_summary(clk) if rank == 0 else None
+    clocks = clk.summary() if rank == 0 else None
     # graph replays do not pass through the Python wrappers: count one eager step's launches
     per_step_eager = None
     for i in range(args.warmup):
@@ -301,13 +333,13 @@ def run_ours(args, rank, world, local_rank):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16 operands, fp32 accumulate", "data": "synthetic",
-            "config": {"workload": f"configs[1]: {args.model} (paper CIFAR CNN), CIFAR-10-shaped sealed shards, "
-                                   f"batch {B}/GPU, decrypt+decode+fwd+bwd+Adam per step",
+            "config": {"workload": f"{cfg}: {mname}, {dname} sealed shards, batch {B}/GPU, "
+                                   f"decrypt+decode+fwd+bwd+Adam per step",
                        "model": args.model, "global_batch": B * world, "seq_len": None,
                        "parallelism": f"dp{world}",
                        "l2": f"{args.shards} resident shards/rank = "
-                             f"{args.shards * (B * 3073 + 16) / 1e6:.0f} MB ciphertext (> 126 MB L2), cycled"},
-            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": B * 3073 + 16 + 64,
+                             f"{args.shards * (B * rb + 16) / 1e6:.0f} MB ciphertext (> 126 MB L2), cycled"},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": B * rb + 16 + 64,
                     "d2h_bytes_per_step": 8},
             "gpu_launches": args.steps * (per_step_eager + decrypt_launches) if per_step_eager else None,
             "roofline": roof,

