@@ -25,6 +25,12 @@ int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs, const v
                    int stride, int pad, void* y, int oh, int ow, int ycs, int yoff, const float* bias, int y_f32,
                    int accumulate, void* stream);
 /* fp32 partial weight gradients part[split][cout][kh*kw*cin]; *splits_out receives the count */
+/* dX of a stride-2 conv by output-parity classes (no zero-upsampled dY): 4 gather convs of dY
+   through parity views of dx; wscratch = cout*kh*kw*cin bf16.  Returns CVB_EINVAL (nothing
+   launched) for unsupported geometry; classes without taps need accumulate=1. */
+int cvb_conv2d_dgrad_s2(const void* dy, int n, int oh, int ow, int cout, int dycs, const void* w, int cin, int kh,
+                        int kw, int pad, void* dx, int h, int wd, int dxcs, int accumulate, void* wscratch,
+                        void* stream);
 int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, int dycs, const void* x, int h, int w, int cin,
                      int xcs, int kh, int kw, int stride, int pad, float* part, int max_splits, int* splits_out,
                      void* stream);
@@ -47,6 +53,16 @@ int cvb_bn_backward(const void* dy, int dycs, const void* x, int xcs, const void
                     const float* mean, const float* rstd, const float* gamma, const float* beta, int relu, float* ws,
                     float* dgamma, float* dbeta, void* dx, int dxcs, float* dx32, int accum32, void* dz_out,
                     void* stream);
+/* single-launch (cooperative, grid-barrier) forms of the above: statistics + finalisation +
+   elementwise pass in one kernel; y == NULL in cvb_bn_forward computes statistics only */
+int64_t cvb_bn_fused_workspace_floats(int C);
+int cvb_bn_forward(const void* x, int64_t rows, int C, int xcs, float* ws, float* mean, float* rstd, float eps,
+                   float* run_mean, float* run_var, float momentum, const float* gamma, const float* beta,
+                   const void* res, int rcs, int relu, void* y, int ycs, int ycoff, void* stream);
+int cvb_bn_backward_fused(const void* dy, int dycs, const void* x, int xcs, const void* y, int ycs, int64_t rows,
+                          int C, const float* mean, const float* rstd, const float* gamma, const float* beta, int relu,
+                          float* ws, float* dgamma, float* dbeta, void* dx, int dxcs, float* dx32, int accum32,
+                          void* dz_out, void* stream);
 
 /* ---- pooling -------------------------------------------------------------------------------- */
 int cvb_maxpool_fwd(const void* x, int n, int h, int w, int C, int k, int s, int p, void* y, int oh, int ow, int ycs,

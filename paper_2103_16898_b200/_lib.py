@@ -58,6 +58,13 @@ SIGNATURES = {
     "cvb_bn_apply": (_INT, [_P, _I64, _INT, _INT, _P, _P, _P, _P, _P, _INT, _INT, _P, _INT, _INT, _P]),
     "cvb_bn_backward": (_INT, [_P, _INT, _P, _INT, _P, _INT, _I64, _INT, _P, _P, _P, _P, _INT, _P, _P, _P, _P, _INT,
                                _P, _INT, _P, _P]),
+    "cvb_bn_fused_workspace_floats": (_I64, [_INT]),
+    "cvb_conv2d_dgrad_s2": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT, _INT, _INT, _P, _INT, _INT, _INT,
+                                   _INT, _P, _P]),
+    "cvb_bn_forward": (_INT, [_P, _I64, _INT, _INT, _P, _P, _P, _c.c_float, _P, _P, _c.c_float, _P, _P, _P, _INT, _INT,
+                              _P, _INT, _INT, _P]),
+    "cvb_bn_backward_fused": (_INT, [_P, _INT, _P, _INT, _P, _INT, _I64, _INT, _P, _P, _P, _P, _INT, _P, _P, _P, _P,
+                                     _INT, _P, _INT, _P, _P]),
     "cvb_maxpool_fwd": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT, _INT, _P]),
     "cvb_maxpool_bwd": (_INT, [_P, _P, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _P, _P]),
     "cvb_avgpool_fwd": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _INT, _P, _INT, _P]),

@@ -1,0 +1,396 @@
+// Single-launch batch norm (K5-support of DESIGN.md): statistics, finalisation and the
+// elementwise pass of a BN layer in ONE persistent cooperative kernel.
+//
+//   forward : pass 1 per-channel sum / sum-of-squares of the CTA's rows -> partials
+//             grid barrier -> channel finalisation (mean, rstd, running stats)
+//             grid barrier -> pass 2 y = act(gamma*(x-mean)*rstd + beta [+ res])
+//   backward: pass 1 dz = dy * relu-mask, partials of sum(dz) and sum(dz*xhat) [dz stored]
+//             grid barrier -> dbeta/dgamma
+//             grid barrier -> pass 2 dx = gamma*rstd*(dz - dbeta/M - xhat*dgamma/M)
+//
+// Why one launch: the three-kernel form (partial / finalize / apply) paid two launch tails
+// and a serial finalize per layer, and its apply pass re-read the tensors from HBM after the
+// L2 had been flushed by other CTAs.  Here each CTA re-reads exactly the rows it reduced in
+// pass 1 (L2-hot for all but the largest tensors).  Every reduction is fixed-order (thread ->
+// smem in row-lane order -> partial per CTA -> channel sum over CTAs in index order), so
+// results are bit-identical run to run and identical to the three-kernel numerics up to the
+// summation tree.
+//
+// Co-residency for the grid barrier is guaranteed by a cooperative launch (capturable into
+// CUDA graphs); the barrier is a generation counter in global memory that returns to zero.
+#include "cvb_common.cuh"
+#include <cuda_bf16.h>
+#include <math.h>
+
+namespace {
+
+typedef __nv_bfloat16 bf16;
+constexpr int THREADS = 512;
+constexpr int MAX_OCC = 2;        // CTAs per SM (partials workspace = grid * 2 * C floats)
+constexpr int UNROLL = 4;
+
+__device__ __forceinline__ void ld8(const bf16* p, float v[8]) {
+  uint4 u = __ldcg(reinterpret_cast<const uint4*>(p));
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; i++) { float2 f = __bfloat1622float2(h[i]); v[2 * i] = f.x; v[2 * i + 1] = f.y; }
+}
+__device__ __forceinline__ void st8(bf16* p, const float v[8]) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; i++) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
+// bar[0] = arrivals, bar[1] = generation.  All CTAs are co-resident (cooperative launch).
+__device__ __forceinline__ void grid_sync(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = bar + 1;
+    const unsigned g = *vgen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*vgen == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Fixed-order block reduction of per-thread (s[8], q[8]) for channel group g, row lane rl
+// into part[blk][2][C].
+__device__ __forceinline__ void block_partials(const float s[8], const float q[8], int G, int RL, int g, int rl,
+                                               int C, float* __restrict__ part, float* sh) {
+  if (rl < RL) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) { sh[(rl * G + g) * 16 + i] = s[i]; sh[(rl * G + g) * 16 + 8 + i] = q[i]; }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < G * 16; idx += THREADS) {
+    const int gg = idx >> 4, k = idx & 15;
+    float acc = 0.f;
+    for (int l = 0; l < RL; l++) acc += sh[(l * G + gg) * 16 + k];
+    part[((int64_t)blockIdx.x * 2 + (k >> 3)) * C + gg * 8 + (k & 7)] = acc;
+  }
+}
+
+// Channel c's totals over all CTAs' partials, fixed order (warp-strided, then smem in warp
+// order).  Called by a whole CTA for one channel; result valid in thread 0.
+__device__ __forceinline__ void channel_total(const float* __restrict__ part, int C, int c, double& s, double& q,
+                                              double* shd) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = THREADS / 32;
+  double a = 0, b = 0;
+  for (int k = threadIdx.x; k < (int)gridDim.x; k += THREADS) {
+    a += __ldcg(part + (int64_t)(2 * k) * C + c);
+    b += __ldcg(part + (int64_t)(2 * k + 1) * C + c);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) { a += __shfl_down_sync(0xffffffffu, a, o); b += __shfl_down_sync(0xffffffffu, b, o); }
+  if (l == 0) { shd[w] = a; shd[nw + w] = b; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s = 0; q = 0;
+    for (int k = 0; k < nw; k++) { s += shd[k]; q += shd[nw + k]; }
+  }
+  __syncthreads();
+}
+
+struct FwdArgs {
+  const bf16* x; int64_t rows; int C, xcs;
+  float* part; unsigned* bar;
+  float* mean; float* rstd; float eps; float* run_mean; float* run_var; float momentum;
+  const float* gamma; const float* beta; const bf16* res; int rcs; int relu;
+  bf16* y; int ycs, ycoff;   // y == nullptr: statistics only
+};
+
+__global__ void __launch_bounds__(THREADS) bn_fwd_fused(const FwdArgs a) {
+  extern __shared__ float sh[];
+  __shared__ double shd[2 * THREADS / 32];
+  __shared__ float s_scale[2048], s_shift[2048];
+  const int C = a.C, G = C / 8, RL = THREADS / G;
+  const int g = threadIdx.x % G, rl = threadIdx.x / G;
+  const int64_t per = (a.rows + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(a.rows, r0 + per);
+  // ---- pass 1: partial statistics ----
+  float s[8] = {0}, q[8] = {0};
+  if (rl < RL) {
+    int64_t r = r0 + rl;
+    for (; r + (UNROLL - 1) * RL < r1; r += UNROLL * RL) {
+      float v[UNROLL][8];
+#pragma unroll
+      for (int u = 0; u < UNROLL; u++) ld8(a.x + (r + u * RL) * a.xcs + g * 8, v[u]);
+#pragma unroll
+      for (int u = 0; u < UNROLL; u++)
+#pragma unroll
+        for (int i = 0; i < 8; i++) { s[i] += v[u][i]; q[i] += v[u][i] * v[u][i]; }
+    }
+    for (; r < r1; r += RL) {
+      float v[8];
+      ld8(a.x + r * a.xcs + g * 8, v);
+#pragma unroll
+      for (int i = 0; i < 8; i++) { s[i] += v[i]; q[i] += v[i] * v[i]; }
+    }
+  }
+  block_partials(s, q, G, RL, g, rl, C, a.part, sh);
+  grid_sync(a.bar);
+  // ---- finalisation: CTA b owns channels b, b + grid, ... ----
+  for (int c = blockIdx.x; c < C; c += gridDim.x) {
+    double ts, tq;
+    channel_total(a.part, C, c, ts, tq, shd);
+    if (threadIdx.x == 0) {
+      const double cnt = (double)a.rows;
+      const double m = ts / cnt;
+      double var = tq / cnt - m * m;
+      if (var < 0) var = 0;
+      a.mean[c] = (float)m;
+      a.rstd[c] = (float)(1.0 / sqrt(var + (double)a.eps));
+      if (a.run_mean) {
+        const double unb = cnt > 1 ? var * cnt / (cnt - 1) : var;
+        a.run_mean[c] = (float)((1.0 - a.momentum) * a.run_mean[c] + a.momentum * m);
+        a.run_var[c] = (float)((1.0 - a.momentum) * a.run_var[c] + a.momentum * unb);
+      }
+    }
+  }
+  if (!a.y) return;
+  grid_sync(a.bar);
+  // ---- pass 2: normalise the same rows ----
+  for (int c = threadIdx.x; c < C; c += THREADS) {
+    s_scale[c] = a.gamma[c] * __ldcg(a.rstd + c);
+    s_shift[c] = __ldcg(a.mean + c);
+  }
+  __syncthreads();
+  if (rl >= RL) return;
+  float sc[8], mu[8], be[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) { sc[k] = s_scale[g * 8 + k]; mu[k] = s_shift[g * 8 + k]; be[k] = a.beta[g * 8 + k]; }
+  int64_t r = r0 + rl;
+  if (!a.res) {   // two rows in flight per thread
+    for (; r + RL < r1; r += 2 * RL) {
+      float v0[8], v1[8], o[8];
+      ld8(a.x + r * a.xcs + g * 8, v0);
+      ld8(a.x + (r + RL) * a.xcs + g * 8, v1);
+#pragma unroll
+      for (int k = 0; k < 8; k++) { const float z = (v0[k] - mu[k]) * sc[k] + be[k]; o[k] = a.relu ? fmaxf(z, 0.f) : z; }
+      st8(a.y + r * a.ycs + a.ycoff + g * 8, o);
+#pragma unroll
+      for (int k = 0; k < 8; k++) { const float z = (v1[k] - mu[k]) * sc[k] + be[k]; o[k] = a.relu ? fmaxf(z, 0.f) : z; }
+      st8(a.y + (r + RL) * a.ycs + a.ycoff + g * 8, o);
+    }
+  }
+  for (; r < r1; r += RL) {
+    float v[8], o[8], rv[8];
+    ld8(a.x + r * a.xcs + g * 8, v);
+    if (a.res) ld8(a.res + r * a.rcs + g * 8, rv);
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      float z = (v[k] - mu[k]) * sc[k] + be[k];
+      if (a.res) z += rv[k];
+      o[k] = a.relu ? fmaxf(z, 0.f) : z;
+    }
+    st8(a.y + r * a.ycs + a.ycoff + g * 8, o);
+  }
+}
+
+struct BwdArgs {
+  const bf16* dy; int dycs; const bf16* x; int xcs; const bf16* y; int ycs;
+  int64_t rows; int C;
+  const float* mean; const float* rstd; const float* gamma; const float* beta; int relu;
+  float* part; unsigned* bar; float* dgamma; float* dbeta;
+  bf16* dx; int dxcs; float* dx32; int accum32; bf16* dz_out;
+};
+
+__device__ __forceinline__ void bwd_load(const BwdArgs& a, int64_t r, int g, const float mu[8], const float rs[8],
+                                         const float ga[8], const float be[8], float d[8], float xh[8]) {
+  float xv[8], yv[8];
+  ld8(a.dy + r * a.dycs + g * 8, d);
+  ld8(a.x + r * a.xcs + g * 8, xv);
+  if (a.relu && a.y) ld8(a.y + r * a.ycs + g * 8, yv);
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    xh[k] = (xv[k] - mu[k]) * rs[k];
+    if (a.relu) {
+      const float z = a.y ? yv[k] : xh[k] * ga[k] + be[k];
+      if (!(z > 0.f)) d[k] = 0.f;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(THREADS) bn_bwd_fused(const BwdArgs a) {
+  extern __shared__ float sh[];
+  __shared__ double shd[2 * THREADS / 32];
+  const int C = a.C, G = C / 8, RL = THREADS / G;
+  const int g = threadIdx.x % G, rl = threadIdx.x / G;
+  const int64_t per = (a.rows + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(a.rows, r0 + per);
+  float mu[8], rs[8], ga[8], be[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const int c = g * 8 + k;
+    mu[k] = a.mean[c]; rs[k] = a.rstd[c]; ga[k] = a.gamma[c]; be[k] = a.beta[c];
+  }
+  // ---- pass 1: sum(dz), sum(dz * xhat) ----
+  float s[8] = {0}, q[8] = {0};
+  if (rl < RL) {
+    int64_t r = r0 + rl;
+    for (; r + RL < r1; r += 2 * RL) {
+      float d0[8], x0[8], d1[8], x1[8];
+      bwd_load(a, r, g, mu, rs, ga, be, d0, x0);
+      bwd_load(a, r + RL, g, mu, rs, ga, be, d1, x1);
+#pragma unroll
+      for (int k = 0; k < 8; k++) { s[k] += d0[k]; q[k] += d0[k] * x0[k]; }
+#pragma unroll
+      for (int k = 0; k < 8; k++) { s[k] += d1[k]; q[k] += d1[k] * x1[k]; }
+      if (a.dz_out) { st8(a.dz_out + r * C + g * 8, d0); st8(a.dz_out + (r + RL) * C + g * 8, d1); }
+    }
+    for (; r < r1; r += RL) {
+      float d[8], xh[8];
+      bwd_load(a, r, g, mu, rs, ga, be, d, xh);
+#pragma unroll
+      for (int k = 0; k < 8; k++) { s[k] += d[k]; q[k] += d[k] * xh[k]; }
+      if (a.dz_out) st8(a.dz_out + r * C + g * 8, d);
+    }
+  }
+  block_partials(s, q, G, RL, g, rl, C, a.part, sh);
+  grid_sync(a.bar);
+  for (int c = blockIdx.x; c < C; c += gridDim.x) {
+    double ts, tq;
+    channel_total(a.part, C, c, ts, tq, shd);
+    if (threadIdx.x == 0) { a.dbeta[c] = (float)ts; a.dgamma[c] = (float)tq; }
+  }
+  if (!a.dx && !a.dx32) return;
+  grid_sync(a.bar);
+  // ---- pass 2: dx over the same rows ----
+  if (rl >= RL) return;
+  const float invM = 1.0f / (float)a.rows;
+  float kb[8], kg[8], kk[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const int c = g * 8 + k;
+    kk[k] = ga[k] * rs[k];
+    kb[k] = __ldcg(a.dbeta + c) * invM;
+    kg[k] = __ldcg(a.dgamma + c) * invM;
+  }
+  int64_t r = r0 + rl;
+  if (!a.dx32) {   // bf16 dx: two rows in flight per thread
+    for (; r + RL < r1; r += 2 * RL) {
+      float d0[8], x0[8], d1[8], x1[8], o[8];
+      bwd_load(a, r, g, mu, rs, ga, be, d0, x0);
+      bwd_load(a, r + RL, g, mu, rs, ga, be, d1, x1);
+#pragma unroll
+      for (int k = 0; k < 8; k++) o[k] = kk[k] * (d0[k] - kb[k] - x0[k] * kg[k]);
+      st8(a.dx + r * a.dxcs + g * 8, o);
+#pragma unroll
+      for (int k = 0; k < 8; k++) o[k] = kk[k] * (d1[k] - kb[k] - x1[k] * kg[k]);
+      st8(a.dx + (r + RL) * a.dxcs + g * 8, o);
+    }
+  }
+  for (; r < r1; r += RL) {
+    float d[8], xh[8], o[8];
+    bwd_load(a, r, g, mu, rs, ga, be, d, xh);
+#pragma unroll
+    for (int k = 0; k < 8; k++) o[k] = kk[k] * (d[k] - kb[k] - xh[k] * kg[k]);
+    if (a.dx32) {
+      float* p = a.dx32 + r * a.dxcs + g * 8;
+      float4* p4 = reinterpret_cast<float4*>(p);
+      if (a.accum32) {
+        float4 u = p4[0], w = p4[1];
+        o[0] += u.x; o[1] += u.y; o[2] += u.z; o[3] += u.w;
+        o[4] += w.x; o[5] += w.y; o[6] += w.z; o[7] += w.w;
+      }
+      p4[0] = make_float4(o[0], o[1], o[2], o[3]);
+      p4[1] = make_float4(o[4], o[5], o[6], o[7]);
+    } else {
+      st8(a.dx + r * a.dxcs + g * 8, o);
+    }
+  }
+}
+
+unsigned* g_bar[64] = {nullptr};
+int g_grid[64] = {0};
+
+int fused_setup(int C, unsigned** bar, int* grid) {
+  int dev = 0;
+  CVB_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) { cvb_set_error("bn fused: device index"); return CVB_EINVAL; }
+  if (!g_bar[dev]) {
+    CVB_CUDA(cudaMalloc(&g_bar[dev], 2 * sizeof(unsigned)));
+    CVB_CUDA(cudaMemset(g_bar[dev], 0, 2 * sizeof(unsigned)));
+    CVB_CUDA(cudaDeviceSynchronize());
+    const size_t smem = (size_t)THREADS * 16 * sizeof(float);
+    CVB_CUDA(cudaFuncSetAttribute(bn_fwd_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CVB_CUDA(cudaFuncSetAttribute(bn_bwd_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ_f = 0, occ_b = 0;
+    CVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, bn_fwd_fused, THREADS, smem));
+    CVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, bn_bwd_fused, THREADS, smem));
+    int occ = occ_f < occ_b ? occ_f : occ_b;
+    if (occ > MAX_OCC) occ = MAX_OCC;
+    if (occ < 1) { cvb_set_error("bn fused: kernel does not fit on an SM"); return CVB_EINVAL; }
+    g_grid[dev] = occ * cvb_num_sms();
+  }
+  *bar = g_bar[dev];
+  *grid = g_grid[dev];
+  (void)C;
+  return CVB_OK;
+}
+
+template <class Args>
+int launch_coop(void (*kern)(Args), const Args& a, int grid, cudaStream_t stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = (size_t)THREADS * 16 * sizeof(float);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CVB_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  return CVB_OK;
+}
+
+}  // namespace
+
+// Floats of partials workspace the fused BN kernels need for C channels.
+CVB_API int64_t cvb_bn_fused_workspace_floats(int C) {
+  unsigned* bar;
+  int grid = 0;
+  if (fused_setup(C, &bar, &grid)) return -1;
+  return (int64_t)grid * 2 * C;
+}
+
+// Batch-norm forward in one launch: statistics of x ([rows][C], stride xcs) -> mean/rstd
+// (+ running stats), then y = act(gamma*(x-mean)*rstd + beta [+ res]) written at channel
+// offset ycoff of y (stride ycs).  y == NULL: statistics only.
+CVB_API int cvb_bn_forward(const void* x, int64_t rows, int C, int xcs, float* ws, float* mean, float* rstd, float eps,
+                           float* run_mean, float* run_var, float momentum, const float* gamma, const float* beta,
+                           const void* res, int rcs, int relu, void* y, int ycs, int ycoff, void* stream) {
+  if (C % 8 || C > 2048 || C / 8 > THREADS) { cvb_set_error("bn_forward: C must be a multiple of 8, <= 2048"); return CVB_EINVAL; }
+  unsigned* bar;
+  int grid;
+  int rc = fused_setup(C, &bar, &grid);
+  if (rc) return rc;
+  FwdArgs a{(const bf16*)x, rows, C, xcs, ws, bar, mean, rstd, eps, run_mean, run_var, momentum, gamma, beta,
+            (const bf16*)res, rcs, relu, (bf16*)y, ycs, ycoff};
+  return launch_coop(bn_fwd_fused, a, grid, (cudaStream_t)stream);
+}
+
+// Batch-norm (+ReLU) backward in one launch (same contract as cvb_bn_backward).
+CVB_API int cvb_bn_backward_fused(const void* dy, int dycs, const void* x, int xcs, const void* y, int ycs, int64_t rows,
+                                  int C, const float* mean, const float* rstd, const float* gamma, const float* beta,
+                                  int relu, float* ws, float* dgamma, float* dbeta, void* dx, int dxcs, float* dx32,
+                                  int accum32, void* dz_out, void* stream) {
+  if (C % 8 || C / 8 > THREADS) { cvb_set_error("bn_backward: bad C"); return CVB_EINVAL; }
+  unsigned* bar;
+  int grid;
+  int rc = fused_setup(C, &bar, &grid);
+  if (rc) return rc;
+  BwdArgs a{(const bf16*)dy, dycs, (const bf16*)x, xcs, (const bf16*)y, ycs, rows, C, mean, rstd, gamma, beta, relu,
+            ws, bar, dgamma, dbeta, (bf16*)dx, dxcs, dx32, accum32, (bf16*)dz_out};
+  return launch_coop(bn_bwd_fused, a, grid, (cudaStream_t)stream);
+}

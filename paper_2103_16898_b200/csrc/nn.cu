@@ -615,9 +615,11 @@ int stats_blocks(int64_t rows, int C, int64_t* rpb) {
 
 // Batch-norm forward statistics over rows of x ([rows][C], channel stride xcs).  ws must hold
 // cvb_bn_workspace_floats(rows, C) floats.  Writes mean/rstd; updates running stats if given.
+CVB_API int64_t cvb_bn_fused_workspace_floats(int C);
 CVB_API int64_t cvb_bn_workspace_floats(int64_t rows, int C) {
   int64_t rpb;
-  return (int64_t)stats_blocks(rows, C, &rpb) * 2 * C;
+  const int64_t a = (int64_t)stats_blocks(rows, C, &rpb) * 2 * C, b = cvb_bn_fused_workspace_floats(C);
+  return a > b ? a : b;
 }
 
 CVB_API int cvb_bn_stats(const void* x, int64_t rows, int C, int xcs, float* ws, float* mean, float* rstd, float eps,

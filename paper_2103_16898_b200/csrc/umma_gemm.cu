@@ -87,6 +87,9 @@ struct GemmParams {
   uint32_t st_swz;          // swizzle mask of the chunk rows (7: 128B, 3: 64B, 1: 32B)
   uint32_t stg_off;         // smem offset of the 4 x 2 staging buffers (4 KB each)
   int st_bw, st_bh, st_bn;  // the warp's box in pixel space (NHWC); dense/partial: 32,1,1
+  int st_rows;              // valid rows of an M tile (multiple of 32); warps past it store nothing
+  int out_par;              // NHWC output is the parity sub-grid (out_ph, out_pw) of an out_H x out_W image
+  int out_ph, out_pw, out_H, out_W;
   CUtensorMap mapC;
   int dbg;                  // profiling knobs: 1 = skip MMA, 2 = skip TMA (results invalid)
   long long* trace;         // debug: clock64 timeline of CTA 0 (5 x 4096 slots) or null
@@ -310,7 +313,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
   uint64_t* bres_full = tempty + 2;         // [1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // shfl: lets the compiler prove the role index warp-uniform (keeps the issue loops on the
+  // uniform datapath)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int tmem_cols = (2 * p.BN <= 32) ? 32 : (2 * p.BN <= 64) ? 64 : (2 * p.BN <= 128) ? 128 : (2 * p.BN <= 256) ? 256 : 512;
 
   if (warp == 0 && lane == 0) {
@@ -543,7 +548,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           c2 = p.out_mode == OUT_PARTIAL ? sp : 0;
         }
         const uint32_t stg = smem0 + p.stg_off + (uint32_t)(warp - 2) * 8192u;
-        for (int c = 0; c < p.BN; c += p.st_ch, ++stg_it) {
+        const int ncols = quarter * 32 < p.st_rows ? p.BN : 0;   // rows past a short tile: nothing to store
+        for (int c = 0; c < ncols; c += p.st_ch, ++stg_it) {
           const uint32_t buf = stg + (stg_it & 1) * 4096u;
           if (lane == 0) bulk_wait_read1();        // the store that last used this buffer has read it
           __syncwarp();
@@ -731,7 +737,8 @@ int plan_tma_store(GemmParams& p) {
   const uint64_t ld = (uint64_t)p.ldc * es;
   if (((uintptr_t)p.out & 15) || (ld & 15)) return CVB_OK;
   if (p.out_mode == OUT_NHWC) {
-    if (p.tw * p.th * p.tn != BM) return CVB_OK;
+    const int tile_rows = p.tw * p.th * p.tn;
+    if (tile_rows > BM || tile_rows % 32) return CVB_OK;
     if (p.tw >= 32) {
       if (p.tw % 32) return CVB_OK;
       bw = 32;
@@ -750,6 +757,9 @@ int plan_tma_store(GemmParams& p) {
     }
     dims[0] = (uint64_t)(p.col_off + p.N); dims[1] = p.OW; dims[2] = p.OH; dims[3] = p.NIMG;
     st[0] = ld; st[1] = ld * p.OW; st[2] = ld * p.OW * p.OH;
+    if (p.out_par) {   // rows out_ph::2, cols out_pw::2 of the full image
+      st[0] = 2 * ld; st[1] = 2 * ld * p.out_W; st[2] = ld * p.out_W * p.out_H;
+    }
   } else if (p.out_mode == OUT_ROWS) {
     dims[0] = (uint64_t)(p.col_off + p.N); dims[1] = (uint64_t)p.M; dims[2] = 1; dims[3] = 1;
     st[0] = ld; st[1] = ld * p.M; st[2] = ld * p.M;
@@ -760,11 +770,15 @@ int plan_tma_store(GemmParams& p) {
   uint32_t box[4] = {(uint32_t)ch, (uint32_t)bw, (uint32_t)bh, (uint32_t)bn};
   uint32_t ones[4] = {1, 1, 1, 1};
   const int rowbytes = ch * es;
+  void* base = p.out;
+  if (p.out_mode == OUT_NHWC && p.out_par)
+    base = (char*)p.out + ((int64_t)p.out_ph * p.out_W + p.out_pw) * (int64_t)ld;
   CUresult r = g_encode(&p.mapC, p.out_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
-                        p.out, dims, st, box, ones, CU_TENSOR_MAP_INTERLEAVE_NONE, swz_of(rowbytes),
+                        base, dims, st, box, ones, CU_TENSOR_MAP_INTERLEAVE_NONE, swz_of(rowbytes),
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return CVB_OK;   // geometry the encoder rejects: direct stores
   p.st_tma = 1;
+  p.st_rows = p.out_mode == OUT_NHWC ? p.tw * p.th * p.tn : BM;
   p.st_ch = ch;
   p.st_swz = rowbytes == 128 ? 7u : rowbytes == 64 ? 3u : 1u;
   p.st_bw = bw; p.st_bh = bh; p.st_bn = bn;
@@ -784,6 +798,7 @@ int launch(GemmParams& p, cudaStream_t stream) {
   plan_tma_store(p);
   const uint32_t stg_bytes = p.st_tma ? 4u * 8192u : 0u;
   if (p.st_tma && 2 * stage_bytes + p.b_res_bytes + stg_bytes > 224u * 1024u) p.st_tma = 0;   // keep 2 stages
+  if (p.out_par && !p.st_tma) { cvb_set_error("parity output needs the TMA-store epilogue"); return CVB_EINVAL; }
   const uint32_t stg = p.st_tma ? stg_bytes : 0u;
   p.stages = (int)((224u * 1024u - p.b_res_bytes - stg) / stage_bytes);
   if (p.stages > 8) p.stages = 8;
@@ -975,6 +990,136 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
   p.out_mode = OUT_NHWC; p.out_f32 = y_f32; p.out = y; p.ldc = ycs; p.col_off = yoff; p.bias = bias;
   p.accum = accumulate;
   return launch(p, (cudaStream_t)stream);
+}
+
+namespace {
+
+// ---- stride-2 dgrad by output-parity classes ------------------------------------------
+// dx[i] = sum_{o,k : 2o - pad + k = i} w[k] dy[o] (per spatial dim).  For output parity
+// rho = i mod 2 only taps k == rho + pad (mod 2) contribute, with o = i/2 + (rho + pad - k)/2.
+// So each of the 4 (rho_h, rho_w) classes is a stride-1 gather-conv of dY (no zero-upsampled
+// copy, no multiplications by inserted zeros: 4x fewer MMAs than the upsampled form) with its
+// own tap subset, written through a parity view of dx by the TMA-store epilogue.
+struct ClassW {
+  int ntaps[4];
+  int64_t off[5];
+  int kh[4][16], kw[4][16];
+};
+
+__global__ void dgrad_class_weights(const __nv_bfloat16* __restrict__ w, int cout, int KH, int KW, int cin, ClassW cw,
+                                    __nv_bfloat16* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cw.off[4]) return;
+  int c = 0;
+  while (i >= cw.off[c + 1]) c++;
+  const int64_t local = i - cw.off[c];
+  const int co = (int)(local % cout);
+  const int64_t r = local / cout;
+  const int nt = cw.ntaps[c];
+  const int t = (int)(r % nt), ci = (int)(r / nt);
+  out[i] = w[(((int64_t)co * KH + cw.kh[c][t]) * KW + cw.kw[c][t]) * cin + ci];
+}
+
+// One parity class: stride-1 gather conv of x (= dY) with explicit tap offsets (dh, dw),
+// output through the parity view (ph, pw) of y [n][H][W][ycs].
+int plan_gather_conv(GemmParams& p, const void* x, int n, int h, int w, int cin, int xcs, const void* wt, int cout,
+                     int ntaps, const int* dh, const int* dw, void* y, int H, int W, int ycs, int ph, int pw,
+                     int accumulate) {
+  const int acel = pick_cel(cin);
+  if (!acel || cout % 8) { cvb_set_error("dgrad: unsupported channels"); return CVB_EINVAL; }
+  memset(&p, 0, sizeof(p));
+  const int oh = (H - ph + 1) / 2, ow = (W - pw + 1) / 2;
+  p.mode = MODE_FWD;
+  p.a_cel = acel;
+  p.b_cel = 64;
+  p.ga = BK / acel;
+  p.gb = 1;
+  p.BN = pick_bn(cout);
+  p.M = n * oh * ow;
+  p.N = cout;
+  const int K = ntaps * cin;
+  int bw, bh, bnn;
+  pick_mbox(n, oh, ow, bw, bh, bnn);
+  p.tw = bw; p.th = bh; p.tn = bnn;
+  p.ptiles_w = (ow + bw - 1) / bw;
+  p.ptiles_h = (oh + bh - 1) / bh;
+  p.m_tiles = p.ptiles_w * p.ptiles_h * ((n + bnn - 1) / bnn);
+  p.n_tiles = (cout + p.BN - 1) / p.BN;
+  p.splits = 1;
+  p.num_kb = (K + BK - 1) / BK;
+  p.kb_per_split = p.num_kb;
+  p.OH = oh; p.OW = ow; p.NIMG = n;
+  p.nbox = p.num_kb * p.ga;
+  if (p.nbox > MAX_BOXES) { cvb_set_error("dgrad: K too large for the box table"); return CVB_EINVAL; }
+  for (int i = 0; i < p.nbox; i++) {
+    const int k = (i / p.ga) * BK + (i % p.ga) * acel;
+    const int tap = k / cin, ci = k - tap * cin;
+    p.boxtab[i] = tap >= ntaps ? pack_box(0, cin, 0, 0) : pack_box(0, ci, dw[tap], dh[tap]);
+  }
+  const uint32_t b_all = (uint32_t)p.num_kb * p.BN * BK * 2;
+  p.b_res = (p.n_tiles == 1 && b_all <= 96u * 1024u) ? 1 : 0;
+  p.b_res_bytes = p.b_res ? b_all : 0;
+  p.b_slabs = p.num_kb;
+  p.tx_bytes = p.ga * bw * bh * bnn * acel * 2 + (p.b_res ? 0 : p.gb * p.BN * p.b_cel * 2);
+  int rc;
+  if ((rc = encode_nhwc(&p.mapA[0], x, n, h, w, cin, xcs, acel, bw, bh, bnn))) return rc;
+  if ((rc = encode_2d(&p.mapB[0], wt, cout, K, K, p.b_cel, p.BN))) return rc;
+  p.out_mode = OUT_NHWC; p.out_f32 = 0; p.out = y; p.ldc = ycs; p.col_off = 0; p.bias = nullptr;
+  p.accum = accumulate;
+  p.out_par = 1; p.out_ph = ph; p.out_pw = pw; p.out_H = H; p.out_W = W;
+  plan_tma_store(p);
+  if (!p.st_tma) { cvb_set_error("dgrad: parity class geometry needs direct stores"); return CVB_EINVAL; }
+  return CVB_OK;
+}
+
+}  // namespace
+
+// dX of a stride-2 conv (w [cout][kh][kw][cin] bf16, pad) from dY [n][oh][ow][cout] (stride
+// dycs): dx [n][h][w][cin] bf16 (stride dxcs), added into dx when accumulate.  wscratch holds
+// cout*kh*kw*cin bf16 (the per-class weight matrices).  Returns CVB_EINVAL without launching
+// anything when a class geometry is unsupported (the caller then uses the upsampled form).
+// Classes without taps (e.g. odd positions of a 1x1 stride-2 conv) contribute nothing: the
+// caller must accumulate (or have zeroed dx).
+CVB_API int cvb_conv2d_dgrad_s2(const void* dy, int n, int oh, int ow, int cout, int dycs, const void* w, int cin,
+                                int kh, int kw, int pad, void* dx, int h, int wd, int dxcs, int accumulate,
+                                void* wscratch, void* stream) {
+  if (get_encoder()) return CVB_ECUDA;
+  static GemmParams plans[4];
+  static int dh[4][16], dw[4][16];
+  ClassW cw;
+  memset(&cw, 0, sizeof(cw));
+  int have = 0;
+  for (int c = 0; c < 4; c++) {
+    const int ph = c >> 1, pw = c & 1;
+    int nt = 0;
+    for (int y = 0; y < kh; y++)
+      for (int x = 0; x < kw; x++)
+        if (((y - ph - pad) & 1) == 0 && ((x - pw - pad) & 1) == 0) {
+          if (nt >= 16) { cvb_set_error("dgrad_s2: kernel too large"); return CVB_EINVAL; }
+          cw.kh[c][nt] = y; cw.kw[c][nt] = x;
+          dh[c][nt] = (ph + pad - y) / 2; dw[c][nt] = (pw + pad - x) / 2;
+          nt++;
+        }
+    cw.ntaps[c] = nt;
+    cw.off[c + 1] = cw.off[c] + (int64_t)cin * nt * cout;
+    if (!nt) continue;
+    const void* wc = (const char*)wscratch + cw.off[c] * 2;
+    int rc = plan_gather_conv(plans[c], dy, n, oh, ow, cout, dycs, wc, cin, nt, dh[c], dw[c], dx, h, wd, dxcs, ph, pw,
+                              accumulate);
+    if (rc) return rc;
+    have |= 1 << c;
+  }
+  if (!accumulate && have != 15) { cvb_set_error("dgrad_s2: a parity class has no taps; accumulate into zeroed dx"); return CVB_EINVAL; }
+  const int64_t total = cw.off[4];
+  dgrad_class_weights<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)w, cout, kh, kw, cin, cw, (__nv_bfloat16*)wscratch);
+  CVB_CHECK_LAUNCH();
+  for (int c = 0; c < 4; c++)
+    if (have & (1 << c)) {
+      int rc = launch(plans[c], (cudaStream_t)stream);
+      if (rc) return rc;
+    }
+  return CVB_OK;
 }
 
 // Weight gradient, fp32 partials: part[split][cout_rows][kh*kw*cin] (caller reduces with

@@ -7,6 +7,7 @@ gradients and optimiser state are fp32.  There is no fallback: a missing library
 from __future__ import annotations
 
 import ctypes
+import os
 import sys
 
 import torch
@@ -61,6 +62,7 @@ class Recorder:
 
 
 REC = Recorder()
+_UNFUSED_BN = bool(os.environ.get("CVB_BN_UNFUSED"))   # A/B switch: three-kernel BN
 
 
 def _ptr(t):
@@ -104,6 +106,26 @@ def conv2d_fwd(x, w, stride=1, pad=0, bias=None, out=None, out_f32=False, cin=No
     REC.end(tok)
     _lib.check(rc, "conv2d_fwd")
     return out
+
+
+def conv2d_dgrad_s2(dy, w, pad, dx, accumulate=False, wscratch=None, acct_flops=None):
+    """dX of a stride-2 conv by output-parity classes (csrc/umma_gemm.cu).  Returns False,
+    launching nothing, when the geometry is unsupported (caller uses the upsampled form)."""
+    n, oh, ow, cout = dy.shape
+    cout_w, kh, kw, cin = w.shape
+    _, h, wd, dcs = dx.shape
+    assert cout_w == cout and w.is_contiguous() and dx.dtype == BF16
+    if wscratch is None:
+        wscratch = torch.empty(w.numel(), dtype=BF16, device=w.device)
+    lib = _lib_bound()
+    tok = REC.begin(5, "umma_gemm", acct_flops if acct_flops is not None else 2 * n * oh * ow * cout * kh * kw * cin)
+    rc = lib.cvb_conv2d_dgrad_s2(dy.data_ptr(), n, oh, ow, cout, dy.stride(2), w.data_ptr(), cin, kh, kw, pad,
+                                 dx.data_ptr(), h, wd, dx.stride(2), int(accumulate), wscratch.data_ptr(), _stream())
+    REC.end(tok)
+    if rc == -1:
+        return False
+    _lib.check(rc, "conv2d_dgrad_s2")
+    return True
 
 
 def conv2d_wgrad_partials(dy, x, kh, kw, stride, pad, cin=None, max_splits=148, part=None, acct_flops=None):
@@ -158,11 +180,31 @@ def bn_workspace(rows, C, device="cuda"):
 
 
 def bn_stats(x, rows, C, xcs, ws, mean, rstd, eps=1e-5, run_mean=None, run_var=None, momentum=0.1):
-    tok = REC.begin(2, "bn", 0, rows * C * 2)
-    rc = _lib_bound().cvb_bn_stats(x.data_ptr(), rows, C, xcs, ws.data_ptr(), mean.data_ptr(), rstd.data_ptr(), eps,
-                                   _ptr(run_mean), _ptr(run_var), momentum, _stream())
+    tok = REC.begin(2 if _UNFUSED_BN else 1, "bn", 0, rows * C * 2)
+    if _UNFUSED_BN:
+        rc = _lib_bound().cvb_bn_stats(x.data_ptr(), rows, C, xcs, ws.data_ptr(), mean.data_ptr(), rstd.data_ptr(),
+                                       eps, _ptr(run_mean), _ptr(run_var), momentum, _stream())
+    else:   # single launch, statistics only
+        rc = _lib_bound().cvb_bn_forward(x.data_ptr(), rows, C, xcs, ws.data_ptr(), mean.data_ptr(), rstd.data_ptr(),
+                                         eps, _ptr(run_mean), _ptr(run_var), momentum, None, None, None, 0, 0, None,
+                                         0, 0, _stream())
     REC.end(tok)
     _lib.check(rc, "bn_stats")
+
+
+def bn_forward(x, rows, C, xcs, ws, mean, rstd, gamma, beta, y, ycs, ycoff=0, relu=True, res=None, rcs=0, eps=1e-5,
+               run_mean=None, run_var=None, momentum=0.1):
+    """Statistics + normalisation (+residual, +ReLU) of one BN layer in a single launch."""
+    if _UNFUSED_BN:
+        bn_stats(x, rows, C, xcs, ws, mean, rstd, eps, run_mean, run_var, momentum)
+        bn_apply(x, rows, C, xcs, mean, rstd, gamma, beta, y, ycs, ycoff, relu, res, rcs)
+        return
+    tok = REC.begin(1, "bn", 0, rows * C * 2 * (4 if res is not None else 3))
+    rc = _lib_bound().cvb_bn_forward(x.data_ptr(), rows, C, xcs, ws.data_ptr(), mean.data_ptr(), rstd.data_ptr(), eps,
+                                     _ptr(run_mean), _ptr(run_var), momentum, gamma.data_ptr(), beta.data_ptr(),
+                                     _ptr(res), rcs, int(relu), y.data_ptr(), ycs, ycoff, _stream())
+    REC.end(tok)
+    _lib.check(rc, "bn_forward")
 
 
 def bn_apply(x, rows, C, xcs, mean, rstd, gamma, beta, y, ycs, ycoff=0, relu=True, res=None, rcs=0):
@@ -177,8 +219,9 @@ def bn_backward(dy, dycs, x, xcs, rows, C, mean, rstd, gamma, beta, ws, dgamma, 
                 dx=None, dxcs=0, dx32=None, accum32=False, dz_out=None):
     # partial pass reads dy, x (, y) [+ writes dz]; apply pass re-reads them and writes dx
     nb = rows * C * 2 * ((3 if y is not None else 2) * 2 + (1 if dz_out is not None else 0) + 1)
-    tok = REC.begin(3 if (dx is not None or dx32 is not None) else 2, "bn", 0, nb)
-    rc = _lib_bound().cvb_bn_backward(dy.data_ptr(), dycs, x.data_ptr(), xcs, _ptr(y), ycs, rows, C, mean.data_ptr(),
+    fn = _lib_bound().cvb_bn_backward if _UNFUSED_BN else _lib_bound().cvb_bn_backward_fused
+    tok = REC.begin((3 if (dx is not None or dx32 is not None) else 2) if _UNFUSED_BN else 1, "bn", 0, nb)
+    rc = fn(dy.data_ptr(), dycs, x.data_ptr(), xcs, _ptr(y), ycs, rows, C, mean.data_ptr(),
                                       rstd.data_ptr(), gamma.data_ptr(), beta.data_ptr(), int(relu), ws.data_ptr(),
                                       dgamma.data_ptr(), dbeta.data_ptr(), _ptr(dx), dxcs, _ptr(dx32), int(accum32),
                                       _ptr(dz_out), _stream())

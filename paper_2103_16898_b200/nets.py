@@ -137,10 +137,9 @@ class ConvBN:
         """x: [n,h,w,cs] (channels [0,cin)); out: [n,oh,ow,ocs] written at channel out_coff."""
         K.conv2d_fwd(x, ps.b[self.W], self.s, self.pad, out=self.z, cin=cin if cin is not None else self.cin,
                      acct_flops=self.flops)
-        K.bn_stats(self.z, self.rows, self.cout, self.cout, self.scratch.bnws, self.mean, self.rstd,
-                   run_mean=self.run_mean, run_var=self.run_var)
-        K.bn_apply(self.z, self.rows, self.cout, self.cout, self.mean, self.rstd, ps.p[self.G], ps.p[self.B], out,
-                   out.shape[-1], out_coff, relu=self.relu, res=res, rcs=res.shape[-1] if res is not None else 0)
+        K.bn_forward(self.z, self.rows, self.cout, self.cout, self.scratch.bnws, self.mean, self.rstd, ps.p[self.G],
+                     ps.p[self.B], out, out.shape[-1], out_coff, relu=self.relu, res=res,
+                     rcs=res.shape[-1] if res is not None else 0, run_mean=self.run_mean, run_var=self.run_var)
 
     def backward(self, ps: ParamStore, dout, x, dx=None, y=None, dres=None, dx_accumulate=False, cin=None,
                  dout_coff=0):
@@ -161,6 +160,10 @@ class ConvBN:
         K.reduce_splits(part, used, count, ps.g[self.W])
         if dx is not None:
             wt = self.scratch.flip[:self.cout * self.k * self.k * cin].view(cin, self.k, self.k, self.cout)
+            if self.s == 2 and cin == self.cin and K.conv2d_dgrad_s2(self.dz, ps.b[self.W], self.pad, dx,
+                                                                     accumulate=dx_accumulate, wscratch=wt,
+                                                                     acct_flops=self.flops):
+                return
             K.weight_flip(ps.b[self.W], wt)
             src = self.dz
             if self.s == 2:
@@ -367,8 +370,9 @@ class BasicBlock:
         # out = relu(bn2(conv2(o1)) + sc): mask from `out`; the masked dout is the grad of sc
         if self.down is not None:
             self.c2.backward(ps, dout, self.o1, dx=self.do1, y=out, dres=self.dres)
-            self.down.backward(ps, self.dres, x, dx=dx)
-            self.c1.backward(ps, self.do1, x, dx=dx, dx_accumulate=True)
+            # 3x3 first (every output parity has taps), then the 1x1 shortcut accumulates
+            self.c1.backward(ps, self.do1, x, dx=dx)
+            self.down.backward(ps, self.dres, x, dx=dx, dx_accumulate=True)
         else:
             # identity shortcut: dx = masked dout (written by bn backward) + dgrad(conv1)
             self.c2.backward(ps, dout, self.o1, dx=self.do1, y=out, dres=dx)
@@ -453,8 +457,9 @@ class BNAct:
 
     def forward(self, ps, x, xcs, y, ycs, stats=True):
         if stats and not getattr(self, "shared", False):
-            K.bn_stats(x, self.rows, self.C, xcs, self.scratch.bnws, self.mean, self.rstd, run_mean=self.run_mean,
-                       run_var=self.run_var)
+            K.bn_forward(x, self.rows, self.C, xcs, self.scratch.bnws, self.mean, self.rstd, ps.p[self.G],
+                         ps.p[self.B], y, ycs, relu=self.relu, run_mean=self.run_mean, run_var=self.run_var)
+            return
         K.bn_apply(x, self.rows, self.C, xcs, self.mean, self.rstd, ps.p[self.G], ps.p[self.B], y, ycs,
                    relu=self.relu)
 

@@ -72,6 +72,53 @@ def test_bn_residual_and_dz_out():
     assert rel(dx, zr.grad) < 5e-3
 
 
+@pytest.mark.parametrize("rows,C,xcs,res", [(512 * 32 * 32, 64, 64, True), (3000, 96, 160, False),
+                                              (98 * 49, 1024, 1024, False), (77, 32, 32, True)])
+def test_bn_single_launch_forward_backward(rows, C, xcs, res):
+    """cvb_bn_forward / cvb_bn_backward_fused (one cooperative launch each) vs torch fp32:
+    strided input (DenseNet concat prefix), output at a channel offset, residual add, fp32
+    accumulated dx.  Same tolerances as the three-kernel path."""
+    g = torch.Generator(device=dev).manual_seed(rows + C + xcs)
+    zfull = (torch.randn(rows, xcs, device=dev, generator=g) * 1.5 + 0.3).bfloat16()
+    z = zfull[:, :C]
+    gamma = torch.rand(C, device=dev, generator=g) + 0.5
+    beta = torch.randn(C, device=dev, generator=g) * 0.1
+    r = torch.randn(rows, C, device=dev, generator=g).bfloat16() if res else None
+    mean, rstd = torch.empty(C, device=dev), torch.empty(C, device=dev)
+    rm, rv = torch.zeros(C, device=dev), torch.ones(C, device=dev)
+    ws = K.bn_workspace(rows, C)
+    yfull = torch.zeros(rows, C + 16, device=dev, dtype=torch.bfloat16)
+    K.bn_forward(zfull, rows, C, xcs, ws, mean, rstd, gamma, beta, yfull, C + 16, ycoff=8, relu=True, res=r,
+                 rcs=C, run_mean=rm, run_var=rv)
+    zf = z.float()
+    assert rel(mean, zf.mean(0)) < 1e-5
+    assert rel(rstd, 1 / torch.sqrt(zf.var(0, unbiased=False) + 1e-5)) < 1e-5
+    assert rel(rv, 0.9 + 0.1 * zf.var(0, unbiased=True)) < 1e-5
+    zr = zf.clone().requires_grad_(True)
+    gr, br = gamma.clone().requires_grad_(True), beta.clone().requires_grad_(True)
+    pre = F.batch_norm(zr, None, None, gr, br, training=True, eps=1e-5)
+    yr = F.relu(pre + r.float() if res else pre)
+    assert rel(yfull[:, 8:8 + C], yr) < 4e-3
+    assert yfull[:, :8].abs().max().item() == 0 and yfull[:, 8 + C:].abs().max().item() == 0
+    dy = torch.randn(rows, C, device=dev, generator=g).bfloat16()
+    dg, db = torch.empty(C, device=dev), torch.empty(C, device=dev)
+    base = torch.randn(rows, xcs, device=dev, generator=g)
+    dx32 = base.clone()
+    y = yfull[:, 8:8 + C].contiguous()
+    K.bn_backward(dy, C, zfull, xcs, rows, C, mean, rstd, gamma, beta, ws, dg, db, relu=True, y=y, ycs=C,
+                  dx32=dx32, dxcs=xcs, accum32=True)
+    # fp64 reference with the kernel's own ReLU mask (y > 0): near-zero pre-activations may
+    # round to the other side of zero between fp32 and torch's order of operations
+    d = dy.double() * (y.double() > 0)
+    xh = (zf.double() - zf.double().mean(0)) / torch.sqrt(zf.double().var(0, unbiased=False) + 1e-5)
+    rdb, rdg = d.sum(0), (d * xh).sum(0)
+    rdx = gamma.double() / torch.sqrt(zf.double().var(0, unbiased=False) + 1e-5) * (d - rdb / rows - xh * rdg / rows)
+    assert rel(db, rdb) < 1e-4
+    assert rel(dg, rdg) < 1e-4
+    assert rel(dx32[:, :C] - base[:, :C], rdx) < 1e-4
+    assert torch.equal(dx32[:, C:], base[:, C:])
+
+
 @pytest.mark.parametrize("k,s,p,h", [(2, 2, 0, 32), (3, 2, 1, 112), (2, 2, 0, 8)])
 def test_maxpool_exact(k, s, p, h):
     x = torch.randn(4, h, h, 64, device=dev).bfloat16()

@@ -141,3 +141,31 @@ def test_conv_accumulate_bf16_slice(n, h, w, cin, cout, k, s, p):
     want = before[..., 16:16 + cout].float() + _ref_conv(x, wt, s, p)
     _close(wide[..., 16:16 + cout], want, tol=1e-2)
     assert torch.equal(wide[..., :16], before[..., :16]) and torch.equal(wide[..., 16 + cout:], before[..., 16 + cout:])
+
+
+@pytest.mark.parametrize("n,h,w,cin,cout,k,p,acc", [(4, 8, 8, 64, 128, 3, 1, False), (4, 8, 8, 64, 128, 1, 0, True),
+                                                    (2, 32, 32, 64, 128, 3, 1, True), (8, 16, 16, 128, 256, 3, 1, False),
+                                                    (3, 16, 16, 32, 64, 1, 0, True)])
+def test_conv_dgrad_stride2_parity_classes(n, h, w, cin, cout, k, p, acc):
+    """Stride-2 dgrad as 4 output-parity gather convs of dY (no zero-upsampled copy) vs torch."""
+    g = torch.Generator(device="cuda").manual_seed(13 + n + h + cin + cout + k)
+    wt = (torch.randn(cout, k, k, cin, device="cuda", generator=g) / (k * k * cin) ** 0.5).to(torch.bfloat16)
+    oh, ow = K.conv_out_hw(h, w, k, 2, p)
+    dy = torch.randn(n, oh, ow, cout, device="cuda", generator=g).to(torch.bfloat16)
+    base = torch.randn(n, h, w, cin, device="cuda", generator=g).to(torch.bfloat16) if acc else \
+        torch.full((n, h, w, cin), 7.0, device="cuda", dtype=torch.bfloat16)
+    dx = base.clone()
+    assert K.conv2d_dgrad_s2(dy, wt, p, dx, accumulate=acc)
+    xr = torch.zeros(n, cin, h, w, device="cuda", requires_grad=True)
+    F.conv2d(xr, wt.permute(0, 3, 1, 2).float(), stride=2, padding=p).backward(dy.permute(0, 3, 1, 2).float())
+    want = xr.grad.permute(0, 2, 3, 1) + (base.float() if acc else 0)
+    _close(dx, want, tol=1e-2)
+
+
+def test_conv_dgrad_stride2_rejects_without_launch():
+    # 1x1 stride 2 without accumulate: odd positions have no taps -> refused, dx untouched
+    wt = torch.randn(64, 1, 1, 32, device="cuda").to(torch.bfloat16)
+    dy = torch.randn(2, 4, 4, 64, device="cuda").to(torch.bfloat16)
+    dx = torch.full((2, 8, 8, 32), 3.0, device="cuda", dtype=torch.bfloat16)
+    assert not K.conv2d_dgrad_s2(dy, wt, 0, dx, accumulate=False)
+    assert (dx == 3.0).all()
