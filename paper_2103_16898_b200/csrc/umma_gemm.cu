@@ -42,8 +42,26 @@ enum { OUT_NHWC = 0, OUT_ROWS = 1, OUT_PARTIAL = 2 };
 
 constexpr int BM = 128;          // UMMA M (cta_group::1)
 constexpr int BK = 64;           // K elements per pipeline stage
-constexpr int NUM_THREADS = 192; // 6 warps
+constexpr int NUM_THREADS = 320; // up to 10 warps: producer, MMA, 4 or 8 epilogue warps
 constexpr int MAX_BOXES = 512;   // box-table entries
+
+// n / d for 0 <= n < 2^31 by multiply-high (host-precomputed magic; no runtime divide in
+// the per-tile bookkeeping of the role loops).
+struct FastDiv {
+  uint32_t d, mul, shift;
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return (uint32_t)(((uint64_t)__umulhi(n, mul) + n) >> shift);
+  }
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  uint32_t s = 0;
+  while ((1ull << s) < d) s++;
+  f.shift = s;
+  f.mul = (uint32_t)((((1ull << 32) * ((1ull << s) - d)) / d) + 1);
+  return f;
+}
 
 struct GemmParams {
   CUtensorMap mapA[4];
@@ -87,6 +105,9 @@ struct GemmParams {
   uint32_t st_swz;          // swizzle mask of the chunk rows (7: 128B, 3: 64B, 1: 32B)
   uint32_t stg_off;         // smem offset of the 4 x 2 staging buffers (4 KB each)
   int st_bw, st_bh, st_bn;  // the warp's box in pixel space (NHWC); dense/partial: 32,1,1
+  FastDiv fd_m, fd_n, fd_mn, fd_pw, fd_ph;   // m_tiles, n_tiles, m_tiles*n_tiles, ptiles_w, ptiles_h
+  int n_epi;                // epilogue warps: 4, or 8 (two per TMEM lane quarter, column halves)
+  uint32_t stg_warp;        // staging bytes per epilogue warp (two buffers)
   int st_rows;              // valid rows of an M tile (multiple of 32); warps past it store nothing
   int out_par;              // NHWC output is the parity sub-grid (out_ph, out_pw) of an out_H x out_W image
   int out_ph, out_pw, out_H, out_W;
@@ -299,6 +320,52 @@ __device__ __forceinline__ void stage16(const GemmParams& p, uint32_t buf, int r
   }
 }
 
+// Halo-mode MMA issue for one K-block (channel group kb) with the tap geometry known at
+// compile time: every A/B descriptor offset folds to a constant or one uniform add per tap,
+// so the issue loop is a few uniform instructions per MMA (the generic loop needed ~18 and
+// starved the tensor core: 96 cycles per N=32 MMA against a 40-cycle floor).
+template <int KH, int KW, int NJ>
+__device__ __forceinline__ void halo_issue(uint32_t tmem_d, uint64_t a0, uint64_t b0, uint32_t idesc, uint32_t acc_flag,
+                                           uint32_t leader, int kb, uint32_t cin16, uint32_t slab16) {
+  constexpr uint32_t pitch = 8 + KW - 1;
+  constexpr uint32_t plane2 = 2u * ((((pitch * (16 + KH - 1) * 16) + 127) / 128 * 128) >> 4);
+  uint32_t qt = (uint32_t)kb * NJ;
+#pragma unroll
+  for (int kh = 0; kh < KH; kh++) {
+#pragma unroll
+    for (int kw = 0; kw < KW; kw++) {
+      // NJ consecutive 16-element K units starting at qt never cross a 64-wide slab when
+      // NJ divides 4 and qt is a multiple of NJ
+      const uint64_t bt = b0 + (uint64_t)((qt >> 2) * slab16 + ((qt & 3u) << 1));
+#pragma unroll
+      for (int j = 0; j < NJ; j++) {
+        umma_bf16_el(tmem_d, a0 + (uint32_t)(kh * pitch + kw) + (uint32_t)j * plane2, bt + 2u * j, idesc, acc_flag, leader);
+        acc_flag = 1u;
+      }
+      qt += cin16;
+    }
+  }
+}
+
+// Halo mode with 8 input channels (the padded RGB / grey stem): one 16-wide MMA K step
+// covers TWO taps.  The second K half of a no-swizzle K-major operand sits LBO bytes after
+// the first, so LBO = 16 B (the next pixel = the next kw tap, a0) or (pitch - KW + 1) * 16 B
+// (the next tap wraps to the next halo row, a1).  Flattened K = tap * 8 + ci matches the
+// natural [cout][kh][kw][8] weights; the odd last tap pairs with K >= KH*KW*8, which the
+// weight map zero-fills (its A half reads the extra halo column, finite data).
+template <int KH, int KW>
+__device__ __forceinline__ void halo8_issue(uint32_t tmem_d, uint64_t a0, uint64_t a1, uint64_t b0, uint32_t idesc,
+                                            uint32_t leader, uint32_t slab16) {
+  constexpr int T = KH * KW, PITCH = 8 + KW;
+#pragma unroll
+  for (int q = 0; q < (T + 1) / 2; q++) {
+    const int t0 = 2 * q, kh = t0 / KW, kw = t0 % KW;
+    const bool wraps = (t0 + 1 < T) && ((t0 + 1) / KW != kh);
+    umma_bf16_el(tmem_d, (wraps ? a1 : a0) + (uint32_t)(kh * PITCH + kw),
+                 b0 + (uint64_t)((q >> 2) * slab16 + ((q & 3) << 1)), idesc, q > 0 ? 1u : 0u, leader);
+  }
+}
+
 __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_constant__ GemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -306,7 +373,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
   const uint32_t b_stage = p.b_res ? 0u : p.BN * p.kr * 2;
   const uint32_t stage_bytes = a_stage + b_stage;
   const uint32_t b_kb_bytes = p.BN * BK * 2;        // resident B: one K-block slab
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes + p.b_res_bytes + (p.st_tma ? 32768u : 0u));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes + p.b_res_bytes +
+                                               (p.st_tma ? (uint32_t)p.n_epi * p.stg_warp : 0u));
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;       // [2]
   uint64_t* tempty = tfull + 2;             // [2]
@@ -322,7 +390,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
     for (int i = 0; i < 4; i++) { prefetch_map(&p.mapA[i]); prefetch_map(&p.mapB[i]); }
     if (p.st_tma) prefetch_map(&p.mapC);
     for (int i = 0; i < p.stages; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < 2; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    for (int i = 0; i < 2; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], p.n_epi); }
     mbar_init(bres_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -355,15 +423,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
     }
     __syncwarp();
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int mt = u % p.m_tiles, rest = u / p.m_tiles;
-      const int nt = rest % p.n_tiles, sp = rest / p.n_tiles;
+      const int rest = (int)p.fd_m.div((uint32_t)u), mt = u - rest * p.m_tiles;
+      const int sp = (int)p.fd_n.div((uint32_t)rest), nt = rest - sp * p.n_tiles;
       const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
       int tw0 = 0, th0 = 0, tn0 = 0;
       if (p.mode == MODE_FWD || p.mode == MODE_HALO) {
-        tw0 = (mt % p.ptiles_w) * p.tw;
-        const int r2 = mt / p.ptiles_w;
-        th0 = (r2 % p.ptiles_h) * p.th;
-        tn0 = (r2 / p.ptiles_h) * p.tn;
+        const int r2 = (int)p.fd_pw.div((uint32_t)mt), r3 = (int)p.fd_ph.div((uint32_t)r2);
+        tw0 = (mt - r2 * p.ptiles_w) * p.tw;
+        th0 = (r2 - r3 * p.ptiles_h) * p.th;
+        tn0 = r3 * p.tn;
       }
       // WGRAD: K-block kb is a pixel box; walk it incrementally
       int pw = 0, ph0 = 0, pn = 0;
@@ -444,7 +512,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
     uint32_t ph = 0;
     int it = 0, lt = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
-      const int sp = u / (p.m_tiles * p.n_tiles);
+      const int sp = (int)p.fd_mn.div((uint32_t)u);
       const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
       const int acc = lt & 1;
       if (lt == 0 && p.b_res) mbar_wait(bres_full, 0);
@@ -469,6 +537,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
             const uint32_t nj = (uint32_t)p.h_cg >> 4, cin16 = (uint32_t)p.h_cin >> 4;
             const uint32_t plane2 = 2u * (p.h_plane_stride >> 4), slab16 = (uint32_t)p.BN * (BK * 2 / 16);
             uint32_t acc_flag = kb > kb0 ? 1u : 0u;
+            const int geo = p.h_kh * 100 + p.h_kw * 10 + (int)nj;
+            if (p.h_cg == 8) halo8_issue<3, 3>(tmem_d, a0, p.adesc[1] + sa, b0, p.idesc, leader, slab16);
+            else if (geo == 334) halo_issue<3, 3, 4>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (geo == 332) halo_issue<3, 3, 2>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (geo == 331) halo_issue<3, 3, 1>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (geo == 114) halo_issue<1, 1, 4>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (geo == 112) halo_issue<1, 1, 2>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (geo == 111) halo_issue<1, 1, 1>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else {
             uint32_t qt = (uint32_t)kb * nj;
             for (int kh = 0; kh < p.h_kh; kh++) {
               const uint64_t arow = a0 + (uint32_t)(kh * p.h_pitch);
@@ -483,6 +560,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
                   }
                 }
               }
+            }
             }
           } else {
             const uint64_t sb = p.b_res ? (uint64_t)((bres + kb * b_kb_bytes) >> 4) : sa + (a_stage >> 4);
@@ -506,9 +584,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
     // row -> pixel offsets inside an NHWC M-tile (constant over tiles)
     const int wb = row % p.tw, r2 = row / p.tw, hb = r2 % p.th, nb = r2 / p.th;
     int lt = 0, stg_it = 0;
+    // this warp's first row inside an NHWC M tile (constant over tiles)
+    const int r0w = quarter * 32;
+    const int w_off = r0w % p.tw, h_off = (r0w / p.tw) % p.th, n_off = r0w / (p.tw * p.th);
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
-      const int mt = u % p.m_tiles, rest = u / p.m_tiles;
-      const int nt = rest % p.n_tiles, sp = rest / p.n_tiles;
+      const int rest = (int)p.fd_m.div((uint32_t)u), mt = u - rest * p.m_tiles;
+      const int sp = (int)p.fd_n.div((uint32_t)rest), nt = rest - sp * p.n_tiles;
       const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
       const int acc = lt & 1;
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
@@ -516,7 +597,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       tc_fence_after();
       bool valid = true;
       int64_t dst_row = 0;
-      if (p.out_mode == OUT_NHWC) {
+      if (p.st_tma) {
+      } else if (p.out_mode == OUT_NHWC) {
         const int ow = (mt % p.ptiles_w) * p.tw + wb;
         const int q = mt / p.ptiles_w;
         const int oh = (q % p.ptiles_h) * p.th + hb;
@@ -534,31 +616,51 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       }
       const bool has_k = kb1 > kb0;
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * p.BN;
+      if (p.dbg & 8) {   // profiling knob: no epilogue work (results invalid)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (warp == 2 && lane == 0) TRACE(4, lt);
+        continue;
+      }
       if (p.st_tma) {
         // box origin of this warp's 32 rows
         int c1 = 0, c2 = 0, c3 = 0;
         if (p.out_mode == OUT_NHWC) {
-          const int r0 = quarter * 32;
-          c1 = (mt % p.ptiles_w) * p.tw + r0 % p.tw;
-          const int q = mt / p.ptiles_w;
-          c2 = (q % p.ptiles_h) * p.th + (r0 / p.tw) % p.th;
-          c3 = (q / p.ptiles_h) * p.tn + r0 / (p.tw * p.th);
+          const int q = (int)p.fd_pw.div((uint32_t)mt), q2 = (int)p.fd_ph.div((uint32_t)q);
+          c1 = (mt - q * p.ptiles_w) * p.tw + w_off;
+          c2 = (q - q2 * p.ptiles_h) * p.th + h_off;
+          c3 = q2 * p.tn + n_off;
         } else {
           c1 = mt * BM + quarter * 32;
           c2 = p.out_mode == OUT_PARTIAL ? sp : 0;
         }
-        const uint32_t stg = smem0 + p.stg_off + (uint32_t)(warp - 2) * 8192u;
-        const int ncols = quarter * 32 < p.st_rows ? p.BN : 0;   // rows past a short tile: nothing to store
-        for (int c = 0; c < ncols; c += p.st_ch, ++stg_it) {
-          const uint32_t buf = stg + (stg_it & 1) * 4096u;
-          if (lane == 0) bulk_wait_read1();        // the store that last used this buffer has read it
-          __syncwarp();
+        const uint32_t stg = smem0 + p.stg_off + (uint32_t)(warp - 2) * p.stg_warp;
+        const int span = p.n_epi == 8 ? p.BN >> 1 : p.BN;          // columns this warp stores
+        const int cbeg = p.n_epi == 8 && warp >= 6 ? span : 0;
+        const int cend = quarter * 32 < p.st_rows ? cbeg + span : cbeg;   // short tile: nothing to store
+        const bool one_chunk = span <= p.st_ch;
+        bool released = false;
+        for (int c = cbeg; c < cend; c += p.st_ch, ++stg_it) {
+          const uint32_t buf = stg + (stg_it & 1) * (p.stg_warp >> 1);
+          // TMEM first: a single-chunk tile hands its accumulator back to the MMA warp before
+          // waiting for the staging buffer
           uint32_t r[64];
           if (p.st_ch == 64) { tmem_ld32(tbase + c, *reinterpret_cast<uint32_t(*)[32]>(r));
                                tmem_ld32(tbase + c + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32)); }
           else if (p.st_ch == 32) tmem_ld32(tbase + c, *reinterpret_cast<uint32_t(*)[32]>(r));
           else tmem_ld16(tbase + c, r);
           tmem_wait();
+          if (warp == 2 && lane == 0) TRACE(5, lt);
+          if (one_chunk) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            released = true;
+          }
+          if (lane == 0) bulk_wait_read1();        // the store that last used this buffer has read it
+          __syncwarp();
+          if (warp == 2 && lane == 0) TRACE(6, lt);
 #pragma unroll
           for (int cc = 0; cc < 64; cc += 16)
             if (cc < p.st_ch) stage16(p, buf, lane, cc, nt * p.BN + c + cc, r + cc, has_k);
@@ -570,10 +672,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
             else tma_store_4d(&p.mapC, buf, c0, c1, c2, c3);
             bulk_commit();
           }
+          if (warp == 2 && lane == 0) TRACE(7, lt);
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (!released) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
         if (warp == 2 && lane == 0) TRACE(4, lt);
         continue;
       }
@@ -729,9 +834,10 @@ int plan_tma_store(GemmParams& p) {
   if (off) return CVB_OK;
   const int es = p.out_f32 ? 4 : 2;
   const int maxch = 128 / es;
+  const int span = p.n_epi == 8 ? p.BN / 2 : p.BN;   // columns per epilogue warp
   int ch = maxch;
-  while (ch > 8 && p.BN % ch) ch >>= 1;
-  if (p.BN % ch || ch * es < 32) return CVB_OK;
+  while (ch > 8 && span % ch) ch >>= 1;
+  if (span % ch || ch * es < 32) return CVB_OK;
   int bw = 32, bh = 1, bn = 1;
   uint64_t dims[4], st[3];
   const uint64_t ld = (uint64_t)p.ldc * es;
@@ -795,8 +901,16 @@ int launch(GemmParams& p, cudaStream_t stream) {
   p.ksteps = p.kr / 16;
   if (!p.a_stage_bytes) p.a_stage_bytes = BM * p.kr * 2;
   const uint32_t stage_bytes = p.a_stage_bytes + (p.b_res ? 0u : (uint32_t)p.BN * p.kr * 2);
+  static int env_epi4 = -1;
+  if (env_epi4 < 0) env_epi4 = getenv("CVB_EPI4") ? 1 : 0;
+  // narrow tiles: two epilogue warps per TMEM lane quarter (each stores half the columns) so
+  // the per-tile epilogue latency (TMEM load, staging, store issue) overlaps across warps
+  p.n_epi = (!env_epi4 && p.BN <= 64 && p.BN % 32 == 0) ? 8 : 4;
   plan_tma_store(p);
-  const uint32_t stg_bytes = p.st_tma ? 4u * 8192u : 0u;
+  if (!p.st_tma && p.n_epi == 8) { p.n_epi = 4; plan_tma_store(p); }
+  if (!p.st_tma) p.n_epi = 4;
+  p.stg_warp = p.st_tma ? 2u * 32u * (uint32_t)p.st_ch * (p.out_f32 ? 4u : 2u) : 0u;
+  const uint32_t stg_bytes = p.st_tma ? (uint32_t)p.n_epi * p.stg_warp : 0u;
   if (p.st_tma && 2 * stage_bytes + p.b_res_bytes + stg_bytes > 224u * 1024u) p.st_tma = 0;   // keep 2 stages
   if (p.out_par && !p.st_tma) { cvb_set_error("parity output needs the TMA-store epilogue"); return CVB_EINVAL; }
   const uint32_t stg = p.st_tma ? stg_bytes : 0u;
@@ -814,8 +928,8 @@ int launch(GemmParams& p, cudaStream_t stream) {
   p.trace = nullptr;
   if (env_dbg & 4) {
     static long long* tr = nullptr;
-    if (!tr) cudaMalloc(&tr, 5 * 4096 * sizeof(long long));
-    cudaMemsetAsync(tr, 0, 5 * 4096 * sizeof(long long), stream);
+    if (!tr) cudaMalloc(&tr, 8 * 4096 * sizeof(long long));
+    cudaMemsetAsync(tr, 0, 8 * 4096 * sizeof(long long), stream);
     p.trace = tr;
     g_trace = tr;
   }
@@ -836,9 +950,18 @@ int launch(GemmParams& p, cudaStream_t stream) {
   }
   if (p.mode == MODE_HALO)   // no-swizzle K-major: LBO = next 8-channel plane, SBO = one halo row
     p.adesc[0] = desc_tmpl(0, p.h_plane_stride, (uint32_t)p.h_pitch * 16, 0);
+  if (p.mode == MODE_HALO && p.h_cg == 8) {   // tap pairs: second K half = next pixel / next row
+    p.adesc[0] = desc_tmpl(0, 16, (uint32_t)p.h_pitch * 16, 0);
+    p.adesc[1] = desc_tmpl(0, (uint32_t)(p.h_pitch - p.h_kw + 1) * 16, (uint32_t)p.h_pitch * 16, 0);
+  }
   const int units = p.m_tiles * p.n_tiles * p.splits;
   const int grid = units < g_num_sms ? units : g_num_sms;
-  umma_gemm_kernel<<<grid, NUM_THREADS, smem, stream>>>(p);
+  p.fd_m = make_fastdiv((uint32_t)p.m_tiles);
+  p.fd_n = make_fastdiv((uint32_t)p.n_tiles);
+  p.fd_mn = make_fastdiv((uint32_t)(p.m_tiles * p.n_tiles));
+  p.fd_pw = make_fastdiv((uint32_t)(p.ptiles_w > 0 ? p.ptiles_w : 1));
+  p.fd_ph = make_fastdiv((uint32_t)(p.ptiles_h > 0 ? p.ptiles_h : 1));
+  umma_gemm_kernel<<<grid, (2 + p.n_epi) * 32, smem, stream>>>(p);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
@@ -911,7 +1034,8 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
     const int K = kh * kw * cin;
     const int BN = pick_bn(cout);
     const uint32_t b_all = (uint32_t)((K + BK - 1) / BK) * BN * BK * 2;
-    const int cg = cin % 64 == 0 ? 64 : cin % 32 == 0 ? 32 : cin % 16 == 0 ? 16 : 0;
+    int cg = cin % 64 == 0 ? 64 : cin % 32 == 0 ? 32 : cin % 16 == 0 ? 16 : 0;
+    if (cin == 8 && kh == 3 && kw == 3) cg = 8;   // stem: tap-pair MMAs (halo8_issue)
     if (!no_halo && stride == 1 && cg && cout <= 256 && b_all <= 96u * 1024u && kh <= 7 && kw <= 7) {
       p.mode = MODE_HALO;
       p.a_major = 0; p.b_major = 0;
@@ -925,8 +1049,8 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
       p.m_tiles = p.ptiles_w * p.ptiles_h * n;
       p.n_tiles = 1;
       p.splits = 1;
-      p.h_cin = cin; p.h_cg = cg; p.h_planes = cg / 8; p.h_pad = pad; p.h_kh = kh; p.h_kw = kw;
-      p.h_pitch = 8 + kw - 1;
+      p.h_cin = cin; p.h_cg = cg; p.h_planes = cg >= 8 ? cg / 8 : 1; p.h_pad = pad; p.h_kh = kh; p.h_kw = kw;
+      p.h_pitch = 8 + kw - 1 + (cg == 8 ? 1 : 0);   // tap pairs read one pixel past the last tap
       const int hrows = 16 + kh - 1;
       p.h_box_bytes = (uint32_t)p.h_pitch * hrows * 16;
       p.h_plane_stride = (p.h_box_bytes + 127) / 128 * 128;
@@ -1252,7 +1376,7 @@ __global__ void __launch_bounds__(96, 1) mma_rate_kernel(int n_mma, int bn, int 
   __syncthreads();
   tc_fence_after();
   const int me = warp == 0 ? 0 : warp == 2 ? 1 : -1;
-  if (me >= 0 && me < issuers) {
+  if (me >= 0 && me < (issuers == 3 ? 1 : issuers)) {
     const uint32_t tmem = slot + (uint32_t)me * 256u;
     const bool leader = elect_one();
     const uint64_t sa = smem_u32(smem) >> 4, sb = sa + (16384 >> 4);
@@ -1263,7 +1387,16 @@ __global__ void __launch_bounds__(96, 1) mma_rate_kernel(int n_mma, int bn, int 
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(bn >> 3) << 17) | (8u << 24);
     long long t0 = clock64();
     if (leader) {
-      for (int i = 0; i < n_mma; i++) umma_bf16(tmem, da + sa + (i & 3) * (a_halo ? 1 : 2), d0 + sb + (i & 3) * 2, idesc, 1u);
+      if (a_halo == 2) {   // the halo conv's exact 3x3 x 2-plane offset sequence, 2 accumulators
+        for (int i = 0; i < n_mma; i++) {
+          const int t = (i >> 1) % 9, j = i & 1;
+          const uint32_t aoff = (uint32_t)((t / 3) * 10 + t % 3) + (uint32_t)j * 368u;
+          umma_bf16(tmem + ((i / 18) & 1) * 32u, dh + sa + aoff, d0 + sb + j * 2, idesc, (i % 18) ? 1u : 0u);
+          if (issuers == 3 && i % 18 == 17) umma_commit(&bar[1]);   // per-tile commit, never waited on
+        }
+      } else {
+        for (int i = 0; i < n_mma; i++) umma_bf16(tmem, da + sa + (i & 3) * (a_halo ? 1 : 2), d0 + sb + (i & 3) * 2, idesc, 1u);
+      }
       umma_commit(&bar[me]);
     }
     __syncwarp();
@@ -1341,7 +1474,7 @@ CVB_API long long cvb_debug_tma_cycles(int n_tma, int dims, int cel) {
 CVB_API int cvb_debug_trace(long long* host_out) {
   if (!g_trace) return -1;
   cudaDeviceSynchronize();
-  cudaMemcpy(host_out, g_trace, 5 * 4096 * sizeof(long long), cudaMemcpyDeviceToHost);
+  cudaMemcpy(host_out, g_trace, 8 * 4096 * sizeof(long long), cudaMemcpyDeviceToHost);
   return 0;
 }
 

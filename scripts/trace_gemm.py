@@ -4,7 +4,11 @@ sys.path.insert(0, '.')
 import numpy as np, torch
 from paper_2103_16898_b200 import kernels as K, _lib
 which = sys.argv[1] if len(sys.argv) > 1 else "conv"
-if which == "conv64":
+if which == "stem":
+    x = torch.randn(512, 32, 32, 8, device="cuda").bfloat16(); w = torch.randn(32, 3, 3, 8, device="cuda").bfloat16()
+    y = torch.empty(512, 32, 32, 32, device="cuda", dtype=torch.bfloat16)
+    f = lambda: K.conv2d_fwd(x, w, 1, 1, out=y)
+elif which == "conv64":
     x = torch.randn(512, 32, 32, 64, device="cuda").bfloat16(); w = torch.randn(64, 3, 3, 64, device="cuda").bfloat16()
     y = torch.empty(512, 32, 32, 64, device="cuda", dtype=torch.bfloat16)
     f = lambda: K.conv2d_fwd(x, w, 1, 1, out=y)
@@ -19,9 +23,9 @@ else:
 for _ in range(3): f()
 torch.cuda.synchronize()
 L = _lib.load(); L.cvb_debug_trace.argtypes = [ctypes.c_void_p]
-buf = np.zeros(5 * 4096, dtype=np.int64)
+buf = np.zeros(8 * 4096, dtype=np.int64)
 L.cvb_debug_trace(buf.ctypes.data)
-t = buf.reshape(5, 4096)
+t = buf.reshape(8, 4096)
 base = t[0][0]
 names = ["prod_empty_ok", "mma_full_ok", "mma_committed", "epi_tfull_ok", "epi_done"]
 n_it = int((t[1] > 0).sum()); n_t = int((t[3] > 0).sum())
@@ -36,3 +40,9 @@ print("median full-wait->commit", np.median(t[2][:n_it] - t[1][:n_it]))
 print("median producer empty_ok - prev mma commit of slot", )
 e = t[4][:n_t] - t[3][:n_t]
 print("median epilogue cycles (tfull_ok -> done)", np.median(e), "tile period", np.median(np.diff(t[3][:n_t])))
+if (t[5] > 0).sum():
+    print("epilogue phases (median cycles from tfull_ok): tmem loaded", np.median(t[5][:n_t] - t[3][:n_t]),
+          "buffer free", np.median(t[6][:n_t] - t[3][:n_t]), "store issued", np.median(t[7][:n_t] - t[3][:n_t]))
+print("per-tile timeline (cycles rel. to CTA start): prod_empty_ok mma_full_ok mma_commit | epi: tfull tmem_ld buf_free store_issued done")
+for i in range(10, 16):
+    print(i, [int(t[k][i] - base) for k in (0, 1, 2)], "|", [int(t[k][i] - base) for k in (3, 5, 6, 7, 4)])
