@@ -359,6 +359,14 @@ def main():
         run_reference(args, rank, world)
         return
     force = bool(os.environ.get("CVB_FORCE_DIST"))   # exercise the NCCL path even at world 1
+    if force and "RANK" not in os.environ:
+        import socket
+
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                          MASTER_PORT=str(sk.getsockname()[1]))
+        sk.close()
     if world > 1 or force:
         import torch.distributed as dist
 

@@ -38,6 +38,12 @@ class ParamStore:
     def __init__(self):
         self.specs = []      # (name, shape, init cpu tensor)
         self.logical = 0     # parameter count without layout padding
+        self.grad_hook = None   # data parallelism: called with parameter names whose grads are final
+
+    def grad_ready(self, *names):
+        """Backward marks parameters whose gradients are final (launches bucket all-reduces)."""
+        if self.grad_hook is not None:
+            self.grad_hook(names)
 
     def add(self, name, init: torch.Tensor, logical: int | None = None):
         self.specs.append((name, tuple(init.shape), init.float()))
@@ -158,6 +164,7 @@ class ConvBN:
                                                                                         self.k * self.k * cin),
                                              acct_flops=self.flops)
         K.reduce_splits(part, used, count, ps.g[self.W])
+        ps.grad_ready(self.W, self.G, self.B)
         if dx is not None:
             wt = self.scratch.flip[:self.cout * self.k * self.k * cin].view(cin, self.k, self.k, self.cout)
             if self.s == 2 and cin == self.cin and K.conv2d_dgrad_s2(self.dz, ps.b[self.W], self.pad, dx,
@@ -226,6 +233,7 @@ class Linear:
         else:
             K.gemm(dy, x, self.fpad, self.fin, B, 1, 1, out=ps.g[self.W], out_f32=True, acct_flops=fl)
         K.col_sum(dy, B, self.fpad, self.fpad, ps.g[self.Bn])
+        ps.grad_ready(self.W, self.Bn)
         if dx is not None:
             K.gemm(dy, ps.b[self.W], B, self.fin, self.fpad, 0, 1, out=dx, acct_flops=fl)
 
@@ -467,6 +475,7 @@ class BNAct:
         K.bn_backward(dy, dycs, x, xcs, self.rows, self.C, self.mean, self.rstd, ps.p[self.G], ps.p[self.B],
                       self.scratch.bnws, ps.g[self.G], ps.g[self.B], relu=self.relu, dx32=dx32, dxcs=dx32cs,
                       accum32=accumulate)
+        ps.grad_ready(self.G, self.B)
 
 
 class Conv:
@@ -500,6 +509,7 @@ class Conv:
                                                                                         self.k * self.k * self.cin),
                                              acct_flops=self.flops)
         K.reduce_splits(part, used, count, ps.g[self.W])
+        ps.grad_ready(self.W)
         if dx is not None:
             wt = self.scratch.flip[:count].view(self.cin, self.k, self.k, self.cout)
             K.weight_flip(ps.b[self.W], wt)
@@ -547,6 +557,7 @@ class DenseLayer:
         K.bn_backward(dy2, self.mid, self.z1, self.mid, rows, self.mid, self.bn2.mean, self.bn2.rstd,
                       ps.p[self.bn2.G], ps.p[self.bn2.B], self.bn2.scratch.bnws, ps.g[self.bn2.G], ps.g[self.bn2.B],
                       relu=True, dx=dz1, dxcs=self.mid)
+        ps.grad_ready(self.bn2.G, self.bn2.B)
         self.conv1.backward(ps, dz1, y1, dx=dy1)
         self.bn1.backward(ps, dy1, self.cin, blk, cs, dblk32, cs, accumulate=True)
 

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import json
 import struct
+import warnings
 
 import numpy as np
 import torch
@@ -46,6 +47,96 @@ class GradAllReduce:
             w.wait()
 
 
+class OverlappedGradAllReduce:
+    """Bucketed SUM all-reduce of the flat fp32 gradient buffer, overlapped with backward.
+
+    Buckets are contiguous ranges of the flat buffer, built back to front (the order backward
+    produces gradients), ~bucket_mb each.  Backward reports finished parameters through
+    ParamStore.grad_ready; as soon as every parameter of the next bucket is final the bucket's
+    all-reduce is launched on a side stream (after an event on the compute stream), so NCCL
+    traffic over NVLink overlaps the remaining dgrad/wgrad kernels.  Buckets launch strictly in
+    order (identical on every rank).  finish() launches the rest and joins the side stream.
+
+    CUDA graphs: a `segment` callback, when set, is invoked at each bucket boundary instead of
+    launching; EncryptedTrainer.capture uses it to split the captured backward into graph
+    segments, and replays them with the bucket all-reduces issued between segments (NCCL stays
+    outside the captured graphs).
+    """
+
+    def __init__(self, ps, bucket_mb: float | None = None, group=None):
+        import torch.distributed as dist
+
+        self.dist, self.group, self.ps = dist, group, ps
+        if bucket_mb is None:   # <= 25 MB, and at least ~4 buckets so small models overlap too
+            bucket_mb = min(25.0, ps.total * 4 / (1 << 20) / 4)
+        per = max(1, int(bucket_mb * (1 << 20) / 4))
+        self.buckets = []           # (lo, hi, names) flat ranges, back to front
+        names, lo, hi = [], None, None
+        order = sorted(ps.offsets.items(), key=lambda kv: -kv[1])
+        ends = {}
+        prev = ps.total
+        for name, off in order:      # each parameter owns [off, next parameter's offset)
+            ends[name] = prev
+            prev = off
+        for name, off in order:
+            if hi is None:
+                hi = ends[name]
+            names.append(name)
+            lo = off
+            if hi - lo >= per:
+                self.buckets.append((lo, hi, frozenset(names)))
+                names, hi = [], None
+        if names:
+            self.buckets.append((0, hi, frozenset(names)))
+        self.side = torch.cuda.Stream() if ps.g32.is_cuda else None
+        self.segment = None
+        self.reset()
+
+    def reset(self):
+        self.ready, self.next, self.works = set(), 0, []
+
+    def __call__(self, names):
+        self.ready.update(names)
+        done = []
+        while self.next < len(self.buckets) and self.buckets[self.next][2] <= self.ready:
+            done.append(self.next)
+            self.next += 1
+        if done:
+            self._launch(done)
+
+    def launch_bucket(self, i):
+        lo, hi, _ = self.buckets[i]
+        view = self.ps.g32[lo:hi]
+        if self.side is None:
+            self.works.append(self.dist.all_reduce(view, op=self.dist.ReduceOp.SUM, group=self.group, async_op=True))
+            return
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self.side.wait_event(ev)
+        with torch.cuda.stream(self.side):
+            self.dist.all_reduce(view, op=self.dist.ReduceOp.SUM, group=self.group)
+
+    def _launch(self, idx):
+        if self.segment is not None:
+            self.segment(idx)
+        else:
+            for i in idx:
+                self.launch_bucket(i)
+
+    def finish(self):
+        if self.next < len(self.buckets):
+            self._launch(list(range(self.next, len(self.buckets))))
+            self.next = len(self.buckets)
+        self.join()
+
+    def join(self):
+        for w in self.works:
+            w.wait()
+        self.works = []
+        if self.side is not None:
+            torch.cuda.current_stream().wait_stream(self.side)
+
+
 class EncryptedTrainer:
     def __init__(self, model="small_cnn", key: bytes = bytes(range(32)), batch=512, spec=CIFAR, seed=0,
                  world=1, rank=0, max_shard_bytes=None, lr=1e-3, force_allreduce=False):
@@ -55,7 +146,10 @@ class EncryptedTrainer:
         self.ctx = GcmContext(key)
         rec = record_bytes(spec["c"], spec["h"], spec["w"])
         self.loader = ShardLoader(self.ctx, max_shard_bytes or batch * rec, batch, spec)
-        self.allreduce = GradAllReduce(self.net.ps.g32) if (world > 1 or force_allreduce) else None
+        self.allreduce = None
+        if world > 1 or force_allreduce:
+            self.allreduce = OverlappedGradAllReduce(self.net.ps)
+            self.net.ps.grad_hook = self.allreduce
         self.graph = None
         self.status_host = torch.zeros(8, dtype=torch.int32).pin_memory()
         self.loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()
@@ -64,6 +158,8 @@ class EncryptedTrainer:
     def _train_body(self):
         x, lab = self.loader.x[:self.batch], self.loader.labels[:self.batch]
         net = self.net
+        if self.allreduce is not None:
+            self.allreduce.reset()
         net.forward(x)
         net.loss_and_grad(lab)
         net.backward(x)
@@ -72,32 +168,63 @@ class EncryptedTrainer:
         self.net.optimizer_step()
 
     def capture(self):
-        """Capture forward+backward and the optimiser into CUDA graphs (the NCCL all-reduce,
-        when distributed, runs between the two)."""
+        """Capture the step into CUDA graphs.  Single GPU: forward+backward and the optimiser.
+        Data parallel: the backward is split into segments at gradient-bucket boundaries; at
+        replay each bucket's NCCL all-reduce is issued (side stream) right after the segment
+        that finishes it, so communication overlaps the rest of the backward."""
+        ar = self.allreduce
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
             for _ in range(2):   # warm-up on a side stream, as torch requires before capture
                 self._train_body()
+                if ar is not None:
+                    ar.finish()
         torch.cuda.current_stream().wait_stream(s)
-        self.g_train, self.g_opt = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.g_train):
+        torch.cuda.synchronize()
+        pool = torch.cuda.graph_pool_handle()
+        self.segments = []
+        cur = [torch.cuda.CUDAGraph()]
+        if ar is not None:
+            def cut(idx):
+                cur[0].capture_end()
+                self.segments.append((cur[0], idx))
+                cur[0] = torch.cuda.CUDAGraph()
+                cur[0].capture_begin(pool=pool)
+            ar.segment = cut
+        with torch.cuda.stream(s), warnings.catch_warnings():
+            warnings.filterwarnings("ignore", message="The CUDA Graph is empty")   # tail after the last bucket
+            cur[0].capture_begin(pool=pool)
             self._train_body()
-        with torch.cuda.graph(self.g_opt):
+            cur[0].capture_end()
+        self.g_train = cur[0]
+        if ar is not None:
+            ar.segment = None
+            self.tail_from = ar.next
+        self.g_opt = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.g_opt, pool=pool):
             self._opt_body()
+        torch.cuda.current_stream().wait_stream(s)
         self.graph = True
         self.net.ps.step_dev.zero_()
 
     def _run_train(self):
+        ar = self.allreduce
         if self.graph:
+            for g, idx in self.segments:
+                g.replay()
+                for i in idx:
+                    ar.launch_bucket(i)
             self.g_train.replay()
-            if self.allreduce is not None:
-                self.allreduce()
+            if ar is not None:
+                for i in range(self.tail_from, len(ar.buckets)):
+                    ar.launch_bucket(i)
+                ar.join()
             self.g_opt.replay()
         else:
             self._train_body()
-            if self.allreduce is not None:
-                self.allreduce()
+            if ar is not None:
+                ar.finish()
             self._opt_body()
 
     def step_resident(self, ct_dev: torch.Tensor, nonce: bytes, aad_dev: torch.Tensor, nrec: int):

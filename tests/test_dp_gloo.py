@@ -59,6 +59,44 @@ def _worker_convention(rank, world, port, q):
     dist.destroy_process_group()
 
 
+class _FakeStore:
+    """The ParamStore fields the overlapped all-reduce uses (flat fp32 grads, offsets)."""
+
+    def __init__(self, sizes, rank):
+        self.offsets, off = {}, 0
+        for i, n in enumerate(sizes):
+            self.offsets[f"p{i}"] = off
+            off += (n + 63) // 64 * 64
+        self.total = off
+        self.g32 = torch.zeros(off)
+        for i, n in enumerate(sizes):
+            o = self.offsets[f"p{i}"]
+            self.g32[o:o + n] = (i + 1) * (rank + 1)
+
+
+def _worker_overlapped(rank, world, port, q):
+    from paper_2103_16898_b200.trainer import OverlappedGradAllReduce
+
+    _init(rank, world, port)
+    sizes = [3000, 64, 64, 5000, 10, 10, 20000, 256]
+    ps = _FakeStore(sizes, rank)
+    ar = OverlappedGradAllReduce(ps, bucket_mb=0.02)     # ~5k floats per bucket
+    launched = []
+    ar.segment = None
+    orig = ar.launch_bucket
+    ar.launch_bucket = lambda i: (launched.append(i), orig(i))   # noqa: E731
+    # backward reports parameters last-to-first, two at a time (like conv W then BN G/B)
+    names = [f"p{i}" for i in range(len(sizes))][::-1]
+    progress = []
+    for k in range(0, len(names), 2):
+        ar(names[k:k + 2])
+        progress.append(list(launched))
+    ar.finish()
+    ok = all(float(ps.g32[ps.offsets[f"p{i}"]]) == (i + 1) * 3 for i in range(len(sizes)))
+    q.put((rank, len(ar.buckets), launched, progress, ok))
+    dist.destroy_process_group()
+
+
 def _run(target, world=2):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -87,3 +125,14 @@ def test_bucketed_allreduce_sums_every_bucket():
 def test_weak_scaling_gradient_convention():
     for rank, err in _run(_worker_convention):
         assert err < 1e-6
+
+
+@pytest.mark.timeout(300)
+def test_overlapped_allreduce_launches_buckets_as_backward_finishes_them():
+    """Buckets are contiguous back-to-front ranges; each launches as soon as backward has
+    reported all of its parameters (before backward ends), in order, and every parameter is
+    summed over the ranks exactly once."""
+    for rank, nb, launched, progress, ok in _run(_worker_overlapped):
+        assert ok
+        assert launched == list(range(nb)) and nb >= 3
+        assert progress[0] != [] and len(progress[-2]) < nb    # launches overlap the "backward"

@@ -1,0 +1,61 @@
+"""Data-parallel step machinery on one B200: NCCL process group of world size 1 (the
+all-reduce is then the identity), so the overlapped-bucket path -- grad-ready hooks, side-stream
+NCCL launches, CUDA-graph segments split at bucket boundaries -- must reproduce the plain
+single-GPU step bit for bit."""
+import os
+import socket
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.fixture(scope="module")
+def nccl_group():
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield dist
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("model", ["small_cnn", "resnet18"])
+def test_overlapped_allreduce_step_matches_single_gpu(nccl_group, model):
+    from bench import make_shards
+    from paper_2103_16898_b200.loader import CIFAR
+    from paper_2103_16898_b200.trainer import EncryptedTrainer
+
+    key, B = bytes(range(32)), 32
+    shards = make_shards(3, B, 5, key, CIFAR)
+    cts = [torch.frombuffer(bytearray(s[3]), dtype=torch.uint8).cuda() for s in shards]
+    aads = [torch.frombuffer(bytearray(s[2]), dtype=torch.uint8).cuda() for s in shards]
+    runs = {}
+    for dp in (False, True):
+        tr = EncryptedTrainer(model, key, batch=B, spec=CIFAR, seed=3, force_allreduce=dp)
+        if dp:
+            assert len(tr.allreduce.buckets) >= 1
+            tr.allreduce.__init__(tr.net.ps, bucket_mb=0.25)     # several buckets -> several segments
+        losses = []
+        tr.step_resident(cts[0], shards[0][1], aads[0], B)       # eager step
+        losses.append(float(tr.net.loss.item()))
+        tr.capture()
+        if dp:
+            assert len(tr.segments) >= 2, "backward was not split at bucket boundaries"
+        for i in (1, 2):
+            tr.step_resident(cts[i], shards[i][1], aads[i], B)
+            losses.append(float(tr.net.loss.item()))
+        torch.cuda.synchronize()
+        runs[dp] = (losses, tr.net.ps.p32.clone())
+    assert runs[False][0] == runs[True][0]
+    assert torch.equal(runs[False][1], runs[True][1])
