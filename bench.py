@@ -308,7 +308,16 @@ def run_ours(args, rank, world, local_rank):
     else:
         ach = dby / (dms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm}
-    roof.update({"traffic": None, "kernel": kind, "launches_per_step": calls,
+    traffic = None
+    try:   # ncu-measured DRAM bytes of this kernel class in one step (profiles/, scripts/traffic_json.py)
+        tj = json.loads((ROOT / "profiles" / "traffic.json").read_text())[args.model]
+        kd = tj["kinds"][kind]
+        traffic = {"dram_bytes_per_launch": kd["dram_bytes"] / kd["launches"],
+                   "dram_bytes_per_step": kd["dram_bytes"],
+                   "algorithmic_bytes_per_step": dby if dfl == 0 else None, "source": tj["source"]}
+    except Exception:
+        pass
+    roof.update({"traffic": traffic, "kernel": kind, "launches_per_step": calls,
                  "share_of_step": dms / step_ms_instr, "peak_source": src,
                  "per_kind_ms": {k: round(v[1], 4) for k, v in summ.items()},
                  "algorithmic": "sum over the step's launches of 2*M*N*K (real channel counts)"

@@ -69,6 +69,12 @@ int cvb_maxpool_fwd(const void* x, int n, int h, int w, int C, int k, int s, int
                     void* stream);
 int cvb_maxpool_bwd(const void* x, const void* dy, int n, int h, int w, int C, int k, int s, int p, int oh, int ow,
                     void* dx, void* stream);
+/* arg-max variants: the forward stores each output element's window offset (uint8, same
+   [n][oh][ow][C] layout), the backward gathers from it without re-scanning windows */
+int cvb_maxpool_fwd_idx(const void* x, int n, int h, int w, int C, int k, int s, int p, void* y, int oh, int ow,
+                        int ycs, void* idx, void* stream);
+int cvb_maxpool_bwd_idx(const void* idx, const void* dy, int n, int h, int w, int C, int k, int s, int p, int oh,
+                        int ow, void* dx, void* stream);
 int cvb_avgpool_fwd(const void* x, int n, int h, int w, int C, int xcs, int k, void* y, int ycs, void* stream);
 int cvb_avgpool_bwd(const void* dy, int n, int h, int w, int C, int k, void* dx, int dxcs, void* stream);
 int cvb_gap_fwd(const void* x, int n, int hw, int C, int xcs, void* y, void* stream);

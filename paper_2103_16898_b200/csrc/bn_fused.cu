@@ -204,43 +204,65 @@ struct BwdArgs {
   bf16* dx; int dxcs; float* dx32; int accum32; bf16* dz_out;
 };
 
-__device__ __forceinline__ void bwd_load(const BwdArgs& a, int64_t r, int g, const float mu[8], const float rs[8],
-                                         const float ga[8], const float be[8], float d[8], float xh[8]) {
-  float xv[8], yv[8];
+// Per-channel constants live in shared memory (8 consecutive floats per channel group, two
+// 16-byte LDS each): keeps the kernel under 64 registers so two 512-thread CTAs fit per SM
+// (twice the loads in flight of the register-resident form, no spills).
+struct ChanSmem {
+  float mu[2048], rs[2048], ga[2048], be[2048];
+};
+
+__device__ __forceinline__ void lds8(const float* p, float v[8]) {
+  const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
+// dz = dy * relu-mask and xhat for one row (8 channels of group g)
+__device__ __forceinline__ void bwd_load(const BwdArgs& a, int64_t r, int g, const ChanSmem& cs, float d[8],
+                                         float xh[8]) {
+  float xv[8];
   ld8(a.dy + r * a.dycs + g * 8, d);
   ld8(a.x + r * a.xcs + g * 8, xv);
-  if (a.relu && a.y) ld8(a.y + r * a.ycs + g * 8, yv);
+  float mu[8], rs[8];
+  lds8(cs.mu + g * 8, mu);
+  lds8(cs.rs + g * 8, rs);
 #pragma unroll
-  for (int k = 0; k < 8; k++) {
-    xh[k] = (xv[k] - mu[k]) * rs[k];
-    if (a.relu) {
-      const float z = a.y ? yv[k] : xh[k] * ga[k] + be[k];
-      if (!(z > 0.f)) d[k] = 0.f;
+  for (int k = 0; k < 8; k++) xh[k] = (xv[k] - mu[k]) * rs[k];
+  if (a.relu) {
+    if (a.y) {
+      float yv[8];
+      ld8(a.y + r * a.ycs + g * 8, yv);
+#pragma unroll
+      for (int k = 0; k < 8; k++) if (!(yv[k] > 0.f)) d[k] = 0.f;
+    } else {
+      float ga[8], be[8];
+      lds8(cs.ga + g * 8, ga);
+      lds8(cs.be + g * 8, be);
+#pragma unroll
+      for (int k = 0; k < 8; k++) if (!(xh[k] * ga[k] + be[k] > 0.f)) d[k] = 0.f;
     }
   }
 }
 
-__global__ void __launch_bounds__(THREADS) bn_bwd_fused(const BwdArgs a) {
+__global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
   extern __shared__ float sh[];
   __shared__ double shd[2 * THREADS / 32];
+  __shared__ ChanSmem cs;
   const int C = a.C, G = C / 8, RL = THREADS / G;
   const int g = threadIdx.x % G, rl = threadIdx.x / G;
   const int64_t per = (a.rows + gridDim.x - 1) / gridDim.x;
   const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(a.rows, r0 + per);
-  float mu[8], rs[8], ga[8], be[8];
-#pragma unroll
-  for (int k = 0; k < 8; k++) {
-    const int c = g * 8 + k;
-    mu[k] = a.mean[c]; rs[k] = a.rstd[c]; ga[k] = a.gamma[c]; be[k] = a.beta[c];
+  for (int c = threadIdx.x; c < C; c += THREADS) {
+    cs.mu[c] = a.mean[c]; cs.rs[c] = a.rstd[c]; cs.ga[c] = a.gamma[c]; cs.be[c] = a.beta[c];
   }
+  __syncthreads();
   // ---- pass 1: sum(dz), sum(dz * xhat) ----
   float s[8] = {0}, q[8] = {0};
   if (rl < RL) {
     int64_t r = r0 + rl;
     for (; r + RL < r1; r += 2 * RL) {
       float d0[8], x0[8], d1[8], x1[8];
-      bwd_load(a, r, g, mu, rs, ga, be, d0, x0);
-      bwd_load(a, r + RL, g, mu, rs, ga, be, d1, x1);
+      bwd_load(a, r, g, cs, d0, x0);
+      bwd_load(a, r + RL, g, cs, d1, x1);
 #pragma unroll
       for (int k = 0; k < 8; k++) { s[k] += d0[k]; q[k] += d0[k] * x0[k]; }
 #pragma unroll
@@ -249,7 +271,7 @@ __global__ void __launch_bounds__(THREADS) bn_bwd_fused(const BwdArgs a) {
     }
     for (; r < r1; r += RL) {
       float d[8], xh[8];
-      bwd_load(a, r, g, mu, rs, ga, be, d, xh);
+      bwd_load(a, r, g, cs, d, xh);
 #pragma unroll
       for (int k = 0; k < 8; k++) { s[k] += d[k]; q[k] += d[k] * xh[k]; }
       if (a.dz_out) st8(a.dz_out + r * C + g * 8, d);
@@ -264,39 +286,26 @@ __global__ void __launch_bounds__(THREADS) bn_bwd_fused(const BwdArgs a) {
   }
   if (!a.dx && !a.dx32) return;
   grid_sync(a.bar);
-  // ---- pass 2: dx over the same rows ----
-  if (rl >= RL) return;
+  // ---- pass 2: dx over the same rows; its per-channel factors go to the (now free)
+  // partial-reduction smem: sh[0:C) = gamma*rstd, sh[C:2C) = mean(dz), sh[2C:3C) = mean(dz*xhat)
   const float invM = 1.0f / (float)a.rows;
-  float kb[8], kg[8], kk[8];
-#pragma unroll
-  for (int k = 0; k < 8; k++) {
-    const int c = g * 8 + k;
-    kk[k] = ga[k] * rs[k];
-    kb[k] = __ldcg(a.dbeta + c) * invM;
-    kg[k] = __ldcg(a.dgamma + c) * invM;
+  for (int c = threadIdx.x; c < C; c += THREADS) {
+    sh[c] = cs.ga[c] * cs.rs[c];
+    sh[C + c] = __ldcg(a.dbeta + c) * invM;
+    sh[2 * C + c] = __ldcg(a.dgamma + c) * invM;
   }
-  int64_t r = r0 + rl;
-  if (!a.dx32) {   // bf16 dx: two rows in flight per thread
-    for (; r + RL < r1; r += 2 * RL) {
-      float d0[8], x0[8], d1[8], x1[8], o[8];
-      bwd_load(a, r, g, mu, rs, ga, be, d0, x0);
-      bwd_load(a, r + RL, g, mu, rs, ga, be, d1, x1);
-#pragma unroll
-      for (int k = 0; k < 8; k++) o[k] = kk[k] * (d0[k] - kb[k] - x0[k] * kg[k]);
-      st8(a.dx + r * a.dxcs + g * 8, o);
-#pragma unroll
-      for (int k = 0; k < 8; k++) o[k] = kk[k] * (d1[k] - kb[k] - x1[k] * kg[k]);
-      st8(a.dx + (r + RL) * a.dxcs + g * 8, o);
-    }
-  }
-  for (; r < r1; r += RL) {
-    float d[8], xh[8], o[8];
-    bwd_load(a, r, g, mu, rs, ga, be, d, xh);
+  __syncthreads();
+  if (rl >= RL) return;
+  for (int64_t r = r0 + rl; r < r1; r += RL) {
+    float d[8], xh[8], o[8], kk[8], kb[8], kg[8];
+    bwd_load(a, r, g, cs, d, xh);
+    lds8(sh + g * 8, kk);
+    lds8(sh + C + g * 8, kb);
+    lds8(sh + 2 * C + g * 8, kg);
 #pragma unroll
     for (int k = 0; k < 8; k++) o[k] = kk[k] * (d[k] - kb[k] - xh[k] * kg[k]);
     if (a.dx32) {
-      float* p = a.dx32 + r * a.dxcs + g * 8;
-      float4* p4 = reinterpret_cast<float4*>(p);
+      float4* p4 = reinterpret_cast<float4*>(a.dx32 + r * a.dxcs + g * 8);
       if (a.accum32) {
         float4 u = p4[0], w = p4[1];
         o[0] += u.x; o[1] += u.y; o[2] += u.z; o[3] += u.w;
@@ -311,9 +320,11 @@ __global__ void __launch_bounds__(THREADS) bn_bwd_fused(const BwdArgs a) {
 }
 
 unsigned* g_bar[64] = {nullptr};
-int g_grid[64] = {0};
+int g_grid[64] = {0}, g_grid_f[64] = {0};
 
-int fused_setup(int C, unsigned** bar, int* grid) {
+// *grid: the backward kernel's co-resident grid; *grid_f: the forward kernel's (it needs
+// fewer registers, so more CTAs fit).  The partials workspace covers the larger.
+int fused_setup(int C, unsigned** bar, int* grid, int* grid_f = nullptr) {
   int dev = 0;
   CVB_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) { cvb_set_error("bn fused: device index"); return CVB_EINVAL; }
@@ -327,13 +338,15 @@ int fused_setup(int C, unsigned** bar, int* grid) {
     int occ_f = 0, occ_b = 0;
     CVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, bn_fwd_fused, THREADS, smem));
     CVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, bn_bwd_fused, THREADS, smem));
-    int occ = occ_f < occ_b ? occ_f : occ_b;
-    if (occ > MAX_OCC) occ = MAX_OCC;
-    if (occ < 1) { cvb_set_error("bn fused: kernel does not fit on an SM"); return CVB_EINVAL; }
-    g_grid[dev] = occ * cvb_num_sms();
+    if (occ_f > MAX_OCC) occ_f = MAX_OCC;
+    if (occ_b > MAX_OCC) occ_b = MAX_OCC;
+    if (occ_f < 1 || occ_b < 1) { cvb_set_error("bn fused: kernel does not fit on an SM"); return CVB_EINVAL; }
+    g_grid[dev] = occ_b * cvb_num_sms();
+    g_grid_f[dev] = occ_f * cvb_num_sms();
   }
   *bar = g_bar[dev];
   *grid = g_grid[dev];
+  if (grid_f) *grid_f = g_grid_f[dev];
   (void)C;
   return CVB_OK;
 }
@@ -359,9 +372,9 @@ int launch_coop(void (*kern)(Args), const Args& a, int grid, cudaStream_t stream
 // Floats of partials workspace the fused BN kernels need for C channels.
 CVB_API int64_t cvb_bn_fused_workspace_floats(int C) {
   unsigned* bar;
-  int grid = 0;
-  if (fused_setup(C, &bar, &grid)) return -1;
-  return (int64_t)grid * 2 * C;
+  int grid = 0, grid_f = 0;
+  if (fused_setup(C, &bar, &grid, &grid_f)) return -1;
+  return (int64_t)(grid > grid_f ? grid : grid_f) * 2 * C;
 }
 
 // Batch-norm forward in one launch: statistics of x ([rows][C], stride xcs) -> mean/rstd
@@ -372,8 +385,8 @@ CVB_API int cvb_bn_forward(const void* x, int64_t rows, int C, int xcs, float* w
                            const void* res, int rcs, int relu, void* y, int ycs, int ycoff, void* stream) {
   if (C % 8 || C > 2048 || C / 8 > THREADS) { cvb_set_error("bn_forward: C must be a multiple of 8, <= 2048"); return CVB_EINVAL; }
   unsigned* bar;
-  int grid;
-  int rc = fused_setup(C, &bar, &grid);
+  int grid_b, grid;
+  int rc = fused_setup(C, &bar, &grid_b, &grid);
   if (rc) return rc;
   FwdArgs a{(const bf16*)x, rows, C, xcs, ws, bar, mean, rstd, eps, run_mean, run_var, momentum, gamma, beta,
             (const bf16*)res, rcs, relu, (bf16*)y, ycs, ycoff};

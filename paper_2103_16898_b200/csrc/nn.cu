@@ -29,6 +29,11 @@ __device__ __forceinline__ void store8(bf16* p, const float v[8]) {
 
 constexpr int ST_THREADS = 256;
 
+__device__ __forceinline__ void ld8f(const float* p, float v[8]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
 // ---- per-channel sum / sum of squares (two-level) -------------------------------------
 // grid.x = blocks over rows; thread (rl, g) handles channel group g (8 channels) of rows
 // rl, rl + RL, ... inside the block's row range.  Partial layout: [blk][2][C].
@@ -117,11 +122,12 @@ __global__ void bn_apply(const bf16* __restrict__ x, int64_t rows, int C, int xc
   load8(x + r * xcs + g * 8, v);
   float rv[8];
   if (res) load8(res + r * rcs + g * 8, rv);
+  // per-channel parameters as 16-byte vectors (8 loads instead of 32 scalar ones)
+  float mu[8], rs[8], ga[8], be[8];
+  ld8f(mean + g * 8, mu); ld8f(rstd + g * 8, rs); ld8f(gamma + g * 8, ga); ld8f(beta + g * 8, be);
 #pragma unroll
   for (int k = 0; k < 8; k++) {
-    const int c = g * 8 + k;
-    const float sc = gamma[c] * rstd[c];
-    float z = (v[k] - mean[c]) * sc + beta[c];
+    float z = (v[k] - mu[k]) * (ga[k] * rs[k]) + be[k];
     if (res) z += rv[k];
     o[k] = relu ? fmaxf(z, 0.f) : z;
   }
@@ -287,6 +293,67 @@ __global__ void maxpool_bwd(const bf16* __restrict__ x, const bf16* __restrict__
       const int me = iy * w + ix;
 #pragma unroll
       for (int c = 0; c < 8; c++) if (am[c] == me) acc[c] += d[c];
+    }
+  }
+  store8(dx + pix * C + g * 8, acc);
+}
+
+// forward with the window's first arg-max (offset dy*k+dx, row-major scan, strict >) kept
+// per output element: the backward then needs no window re-scan
+__global__ void maxpool_fwd_idx(const bf16* __restrict__ x, int n, int h, int w, int C, int k, int s, int p, int oh,
+                                int ow, bf16* __restrict__ y, int ycs, uint8_t* __restrict__ idx) {
+  const int G = C / 8;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * oh * ow * G) return;
+  const int g = (int)(i % G);
+  int64_t pix = i / G;
+  const int ox = (int)(pix % ow), oy = (int)((pix / ow) % oh), b = (int)(pix / ((int64_t)ow * oh));
+  float m[8];
+  uint32_t am[8];
+#pragma unroll
+  for (int c = 0; c < 8; c++) { m[c] = -INFINITY; am[c] = 0; }
+  for (int dy = 0; dy < k; dy++) {
+    const int iy = oy * s - p + dy;
+    if (iy < 0 || iy >= h) continue;
+    for (int dx = 0; dx < k; dx++) {
+      const int ix = ox * s - p + dx;
+      if (ix < 0 || ix >= w) continue;
+      float v[8];
+      load8(x + (((int64_t)b * h + iy) * w + ix) * C + g * 8, v);
+#pragma unroll
+      for (int c = 0; c < 8; c++) if (v[c] > m[c]) { m[c] = v[c]; am[c] = (uint32_t)(dy * k + dx); }
+    }
+  }
+  store8(y + pix * ycs + g * 8, m);
+  uint2 packed = make_uint2(am[0] | (am[1] << 8) | (am[2] << 16) | (am[3] << 24),
+                            am[4] | (am[5] << 8) | (am[6] << 16) | (am[7] << 24));
+  *reinterpret_cast<uint2*>(idx + pix * C + g * 8) = packed;
+}
+
+// gather: input (iy, ix) takes dy of every window (oy, ox) whose stored arg-max is it
+__global__ void maxpool_bwd_idx(const uint8_t* __restrict__ idx, const bf16* __restrict__ dyp, int n, int h, int w,
+                                int C, int k, int s, int p, int oh, int ow, bf16* __restrict__ dx) {
+  const int G = C / 8;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * h * w * G) return;
+  const int g = (int)(i % G);
+  const int64_t pix = i / G;
+  const int ix = (int)(pix % w), iy = (int)((pix / w) % h), b = (int)(pix / ((int64_t)w * h));
+  float acc[8] = {0};
+  const int oy0 = max(0, (iy + p - k + s) / s), oy1 = min(oh - 1, (iy + p) / s);
+  const int ox0 = max(0, (ix + p - k + s) / s), ox1 = min(ow - 1, (ix + p) / s);
+  for (int oy = oy0; oy <= oy1; oy++) {
+    for (int ox = ox0; ox <= ox1; ox++) {
+      const uint32_t me = (uint32_t)((iy - (oy * s - p)) * k + (ix - (ox * s - p)));
+      const int64_t o = (((int64_t)b * oh + oy) * ow + ox) * C + g * 8;
+      const uint2 a = *reinterpret_cast<const uint2*>(idx + o);
+      float d[8];
+      load8(dyp + o, d);
+#pragma unroll
+      for (int c = 0; c < 8; c++) {
+        const uint32_t am = ((c < 4 ? a.x : a.y) >> (8 * (c & 3))) & 0xffu;
+        if (am == me) acc[c] += d[c];
+      }
     }
   }
   store8(dx + pix * C + g * 8, acc);
@@ -684,6 +751,23 @@ CVB_API int cvb_maxpool_bwd(const void* x, const void* dy, int n, int h, int w, 
   else
     maxpool_bwd<<<nblocks((int64_t)n * h * w * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, (const bf16*)dy, n, h, w, C,
                                                                            k, s, p, oh, ow, (bf16*)dx);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_maxpool_fwd_idx(const void* x, int n, int h, int w, int C, int k, int s, int p, void* y, int oh, int ow,
+                                int ycs, void* idx, void* stream) {
+  if (C % 8 || k * k > 256) { cvb_set_error("maxpool_fwd_idx: bad shape"); return CVB_EINVAL; }
+  maxpool_fwd_idx<<<nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, n, h, w, C, k, s, p, oh,
+                                                                              ow, (bf16*)y, ycs, (uint8_t*)idx);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_maxpool_bwd_idx(const void* idx, const void* dy, int n, int h, int w, int C, int k, int s, int p, int oh,
+                                int ow, void* dx, void* stream) {
+  maxpool_bwd_idx<<<nblocks((int64_t)n * h * w * (C / 8)), 256, 0, STREAM>>>((const uint8_t*)idx, (const bf16*)dy, n, h,
+                                                                            w, C, k, s, p, oh, ow, (bf16*)dx);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }

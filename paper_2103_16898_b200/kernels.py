@@ -229,21 +229,32 @@ def bn_backward(dy, dycs, x, xcs, rows, C, mean, rstd, gamma, beta, ws, dgamma, 
     _lib.check(rc, "bn_backward")
 
 
-def maxpool_fwd(x, k, s, p, y):
+def maxpool_fwd(x, k, s, p, y, idx=None):
+    """idx (uint8 [n][oh][ow][C], optional): keep the window arg-max for maxpool_bwd."""
     n, h, w, c = x.shape
     _, oh, ow, _ = y.shape
-    tok = REC.begin(1, "pool", 0, (x.numel() + y.numel()) * 2)
-    rc = _lib_bound().cvb_maxpool_fwd(x.data_ptr(), n, h, w, c, k, s, p, y.data_ptr(), oh, ow, y.stride(2), _stream())
+    tok = REC.begin(1, "pool", 0, (x.numel() + y.numel()) * 2 + (idx.numel() if idx is not None else 0))
+    if idx is not None:
+        rc = _lib_bound().cvb_maxpool_fwd_idx(x.data_ptr(), n, h, w, c, k, s, p, y.data_ptr(), oh, ow, y.stride(2),
+                                              idx.data_ptr(), _stream())
+    else:
+        rc = _lib_bound().cvb_maxpool_fwd(x.data_ptr(), n, h, w, c, k, s, p, y.data_ptr(), oh, ow, y.stride(2),
+                                          _stream())
     REC.end(tok)
     _lib.check(rc, "maxpool_fwd")
 
 
-def maxpool_bwd(x, dy, k, s, p, dx):
+def maxpool_bwd(x, dy, k, s, p, dx, idx=None):
     n, h, w, c = x.shape
     _, oh, ow, _ = dy.shape
-    tok = REC.begin(1, "pool", 0, (2 * x.numel() + dy.numel()) * 2)
-    rc = _lib_bound().cvb_maxpool_bwd(x.data_ptr(), dy.data_ptr(), n, h, w, c, k, s, p, oh, ow, dx.data_ptr(),
-                                      _stream())
+    if idx is not None:
+        tok = REC.begin(1, "pool", 0, dy.numel() * 2 + idx.numel() + dx.numel() * 2)
+        rc = _lib_bound().cvb_maxpool_bwd_idx(idx.data_ptr(), dy.data_ptr(), n, h, w, c, k, s, p, oh, ow,
+                                              dx.data_ptr(), _stream())
+    else:
+        tok = REC.begin(1, "pool", 0, (2 * x.numel() + dy.numel()) * 2)
+        rc = _lib_bound().cvb_maxpool_bwd(x.data_ptr(), dy.data_ptr(), n, h, w, c, k, s, p, oh, ow, dx.data_ptr(),
+                                          _stream())
     REC.end(tok)
     _lib.check(rc, "maxpool_bwd")
 

@@ -598,6 +598,7 @@ class DenseNet121(Net):
         self.a0 = e(n, oh, ow, self.stem.cout)
         self.da0 = e(n, oh, ow, self.stem.cout)
         h, w = (oh + 2 - 3) // 2 + 1, (ow + 2 - 3) // 2 + 1
+        self.pool_idx = torch.empty(n, h, w, self.stem.cout, dtype=torch.uint8, device=dev)   # stem max-pool arg-max
         self.geo, self.bufs, self.dbufs = [], [], []
         self.bmean, self.brstd, self.ty = [], [], []
         ymax = 0
@@ -648,7 +649,7 @@ class DenseNet121(Net):
         ps, n = self.ps, self.batch
         self.stem.forward(ps, x, self.a0)
         c0 = self.stem.cout
-        K.maxpool_fwd(self.a0, 3, 2, 1, self.bufs[0][..., :c0])
+        K.maxpool_fwd(self.a0, 3, 2, 1, self.bufs[0][..., :c0], idx=self.pool_idx)
         h, w = self.geo[0]
         K.bn_stats(self.bufs[0], n * h * w, c0, self.bufs[0].shape[-1], self.scratch.bnws, self.bmean[0][:c0],
                    self.brstd[0][:c0])
@@ -707,7 +708,7 @@ class DenseNet121(Net):
         h, w = self.geo[0]
         d0 = self._v(self.dcast, n, h, w, self.stem.cout)
         K.cast_rows(self.dbufs[0], self.dbufs[0].shape[-1], d0, self.stem.cout, n * h * w, self.stem.cout)
-        K.maxpool_bwd(self.a0, d0, 3, 2, 1, self.da0)
+        K.maxpool_bwd(self.a0, d0, 3, 2, 1, self.da0, idx=self.pool_idx)
         self.stem.backward(ps, self.da0, x, dx=None)
 
 

@@ -134,6 +134,14 @@ def test_maxpool_exact(k, s, p, h):
     K.maxpool_bwd(x, dy, k, s, p, dx)
     yr.backward(nchw(dy).cpu())
     assert rel(nchw(dx).cpu(), xr.grad) < 4e-3   # overlapping windows sum in fp32 -> bf16
+    # arg-max variant: identical forward, identical backward (same first-max rule, same order)
+    y2 = torch.empty_like(y)
+    idx = torch.empty(4, oh, oh, 64, device=dev, dtype=torch.uint8)
+    K.maxpool_fwd(x, k, s, p, y2, idx=idx)
+    assert torch.equal(y2, y)
+    dx2 = torch.empty_like(x)
+    K.maxpool_bwd(x, dy, k, s, p, dx2, idx=idx)
+    assert torch.equal(dx2, dx)
 
 
 def test_avgpool_and_gap():
