@@ -163,6 +163,28 @@ class Volume:
             os.close(fd)
             (self.root / LOCK_NAME).unlink(missing_ok=True)
 
+    def put_sealed(self, key, logical_path: str, nonce: bytes, blob: bytes, plaintext_length: int) -> None:
+        """Install a blob already sealed under this volume's key/AAD (the GPU gate copy
+        seals on the device); same lock / naming / manifest discipline as put()."""
+        _check_path(logical_path)
+        if key_id_hex(key) != self.key_id:
+            raise KeyMismatch("key commitment does not match the volume manifest")
+        try:
+            fd = os.open(self.root / LOCK_NAME, os.O_CREAT | os.O_EXCL | os.O_WRONLY)
+        except FileExistsError:
+            raise VolumeLocked(f"another writer holds {self.root}") from None
+        try:
+            h = hashlib.sha256(blob).hexdigest()
+            (self.root / h).write_bytes(blob)
+            old = self._entries.get(logical_path)
+            self._entries[logical_path] = ManifestEntry(logical_path, nonce, h, plaintext_length)
+            self._write_manifest()
+            if old is not None and old.ciphertext_hash != h:
+                (self.root / old.ciphertext_hash).unlink(missing_ok=True)
+        finally:
+            os.close(fd)
+            (self.root / LOCK_NAME).unlink(missing_ok=True)
+
     # -- readers ---------------------------------------------------------------------------
     def get(self, key, logical_path: str) -> bytes:
         """Exact original bytes or AuthenticationFailure; never partial (volume.py:185-197)."""
@@ -224,3 +246,68 @@ class Volume:
             if child.name not in referenced:
                 violations.append(("orphan_blob", child.name))
         return violations
+
+
+# -- tree helpers (volume.py:239-258) and the gate's re-encryption copy
+def seal_tree(volume: Volume, key, source) -> int:
+    """Seal every regular file under ``source`` by its relative path (volume.py:239-247);
+    the AES-GCM seal of each file runs on the GPU (Volume.put)."""
+    source = Path(source)
+    count = 0
+    for path in sorted(source.rglob("*")):
+        if path.is_file():
+            volume.put(key, path.relative_to(source).as_posix(), path.read_bytes())
+            count += 1
+    return count
+
+
+def unseal_tree(volume: Volume, key, dest) -> int:
+    """volume.py:250-258 with the GPU open."""
+    dest = Path(dest)
+    count = 0
+    for logical_path in volume.paths():
+        target = dest.joinpath(*logical_path.split("/"))
+        target.parent.mkdir(parents=True, exist_ok=True)
+        target.write_bytes(volume.get(key, logical_path))
+        count += 1
+    return count
+
+
+def gate_copy(source: Volume, source_key, dest: Volume, dest_key) -> list[tuple[str, str, int]]:
+    """The trusted-boot gate's copy loop (gate.py:186-190) with the crypto on the device:
+    each source blob is copied to HBM once, opened (tag verified on the device), re-sealed
+    under the destination key / AAD / a fresh nonce without the plaintext leaving HBM, and
+    the sealed blob comes back for the destination volume.  Returns the copy report's
+    (path, SHA-256(plaintext) hex, length) entries; the plaintext digest is computed on the
+    device-resident plaintext after a D2H into pinned memory of the gate's own address space
+    (the reference holds the same plaintext in host memory).  Raises AuthenticationFailure on
+    the first bad source blob -- the gate maps it to "volume_auth_failure" and discards the
+    staging volume, exactly as gate.py:191-192 does."""
+    import torch
+
+    src_ctx, dst_ctx = _crypto.GcmContext(source_key), _crypto.GcmContext(dest_key)
+    if key_id_hex(dest_key) != dest.key_id:
+        raise KeyMismatch("key commitment does not match the destination manifest")
+    report = []
+    work_o, work_s = src_ctx.new_workspace(), dst_ctx.new_workspace()
+    for logical_path in source.paths():
+        e = source.entry(logical_path)
+        blob = source.read_blob(logical_path)
+        if len(blob) < 16 or len(blob) - 16 != e.plaintext_length:
+            raise AuthenticationFailure("blob length disagrees with manifest")
+        n = e.plaintext_length
+        blob_dev = torch.frombuffer(bytearray(blob), dtype=torch.uint8).pin_memory().to("cuda", non_blocking=True)
+        aad_s = torch.frombuffer(bytearray(aad_for(source.volume_name, logical_path)), dtype=torch.uint8).cuda()
+        aad_d = torch.frombuffer(bytearray(aad_for(dest.volume_name, logical_path)), dtype=torch.uint8).cuda()
+        pt = torch.empty(max(1, n), dtype=torch.uint8, device="cuda")
+        src_ctx.open_device(e.nonce, aad_s, blob_dev, pt, work_o)
+        if not src_ctx.status_ok(work_o):          # tag verdict before anything is re-sealed
+            raise AuthenticationFailure("AEAD authentication failed")
+        nonce = _crypto.fresh_nonce()
+        sealed = torch.empty(n + 16, dtype=torch.uint8, device="cuda")
+        dst_ctx.seal_device(nonce, aad_d, pt[:n], sealed, work_s)
+        out = sealed.cpu().numpy().tobytes()
+        digest = hashlib.sha256(pt[:n].cpu().numpy().tobytes()).hexdigest()
+        dest.put_sealed(dest_key, logical_path, nonce, out, n)
+        report.append((logical_path, digest, n))
+    return report
