@@ -23,6 +23,7 @@ struct RecParams {
 
 template <typename T>
 __global__ void records_to_nhwc(const __grid_constant__ RecParams p) {
+  CVB_PDL_PROLOGUE();
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t total = p.nrec * p.hw;
   if (gid >= total) return;
@@ -65,8 +66,8 @@ CVB_API int cvb_records_to_nhwc(const uint8_t* pt_dev, int64_t nrec, int64_t rec
   p.out = out_dev; p.labels = labels_dev;
   int64_t total = nrec * p.hw;
   unsigned grid = (unsigned)((total + 255) / 256);
-  if (dtype == 0) records_to_nhwc<__nv_bfloat16><<<grid, 256, 0, (cudaStream_t)stream>>>(p);
-  else records_to_nhwc<float><<<grid, 256, 0, (cudaStream_t)stream>>>(p);
+  if (dtype == 0) cvb_launch(records_to_nhwc<__nv_bfloat16>, grid, 256, 0, (cudaStream_t)stream, p);
+  else cvb_launch(records_to_nhwc<float>, grid, 256, 0, (cudaStream_t)stream, p);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }

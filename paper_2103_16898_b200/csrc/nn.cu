@@ -39,6 +39,7 @@ __device__ __forceinline__ void ld8f(const float* p, float v[8]) {
 // rl, rl + RL, ... inside the block's row range.  Partial layout: [blk][2][C].
 __global__ void chan_stats_partial(const bf16* __restrict__ x, int64_t rows, int C, int cs, int64_t rows_per_blk,
                                    float* __restrict__ part) {
+  CVB_PDL_PROLOGUE();
   const int G = C / 8;
   const int RL = ST_THREADS / G;  // row lanes (G <= 256 guaranteed by host)
   const int t = threadIdx.x, g = t % G, rl = t / G;
@@ -93,6 +94,7 @@ __device__ __forceinline__ void sum_partials(const float* __restrict__ part, int
 __global__ void __launch_bounds__(FIN_WARPS * 32) bn_finalize(const float* __restrict__ part, int nblk, int C, double count, float eps,
                             float* __restrict__ mean, float* __restrict__ rstd, float* __restrict__ run_mean,
                             float* __restrict__ run_var, float momentum) {
+  CVB_PDL_PROLOGUE();
   const int c = blockIdx.x * 32 + (threadIdx.x & 31);
   double s, q;
   sum_partials(part, nblk, C, c, s, q);
@@ -113,6 +115,7 @@ __global__ void __launch_bounds__(FIN_WARPS * 32) bn_finalize(const float* __res
 __global__ void bn_apply(const bf16* __restrict__ x, int64_t rows, int C, int xcs, const float* __restrict__ mean,
                          const float* __restrict__ rstd, const float* __restrict__ gamma, const float* __restrict__ beta,
                          const bf16* __restrict__ res, int rcs, int relu, bf16* __restrict__ y, int ycs, int ycoff) {
+  CVB_PDL_PROLOGUE();
   const int G = C / 8;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= rows * G) return;
@@ -141,6 +144,7 @@ __global__ void bn_bwd_partial(const bf16* __restrict__ dy, int dycs, const bf16
                                const bf16* __restrict__ y, int ycs, int64_t rows, int C, const float* __restrict__ mean,
                                const float* __restrict__ rstd, const float* __restrict__ gamma, const float* __restrict__ beta,
                                int relu, int64_t rows_per_blk, float* __restrict__ part, bf16* __restrict__ dz_out) {
+  CVB_PDL_PROLOGUE();
   const int G = C / 8;
   const int RL = ST_THREADS / G;
   const int t = threadIdx.x, g = t % G, rl = t / G;
@@ -187,6 +191,7 @@ __global__ void bn_bwd_partial(const bf16* __restrict__ dy, int dycs, const bf16
 
 __global__ void __launch_bounds__(FIN_WARPS * 32) bn_bwd_finalize(const float* __restrict__ part, int nblk, int C, float* __restrict__ dbeta,
                                 float* __restrict__ dgamma) {
+  CVB_PDL_PROLOGUE();
   const int c = blockIdx.x * 32 + (threadIdx.x & 31);
   double s, q;
   sum_partials(part, nblk, C, c, s, q);
@@ -201,6 +206,7 @@ __global__ void bn_bwd_apply(const bf16* __restrict__ dy, int dycs, const bf16* 
                              const float* __restrict__ rstd, const float* __restrict__ gamma, const float* __restrict__ beta,
                              int relu, const float* __restrict__ dbeta, const float* __restrict__ dgamma,
                              bf16* __restrict__ dx, int dxcs, float* __restrict__ dx32, int accum32) {
+  CVB_PDL_PROLOGUE();
   const int G = C / 8;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= rows * G) return;
@@ -233,6 +239,7 @@ __global__ void bn_bwd_apply(const bf16* __restrict__ dy, int dycs, const bf16* 
 // ---- pooling --------------------------------------------------------------------------
 __global__ void maxpool_fwd(const bf16* __restrict__ x, int n, int h, int w, int C, int k, int s, int p, int oh, int ow,
                             bf16* __restrict__ y, int ycs) {
+  CVB_PDL_PROLOGUE();
   const int G = C / 8;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)n * oh * ow * G) return;
@@ -260,6 +267,7 @@ __global__ void maxpool_fwd(const bf16* __restrict__ x, int n, int h, int w, int
 // gather form: each input element collects dy of every window whose FIRST arg-max it is
 __global__ void maxpool_bwd(const bf16* __restrict__ x, const bf16* __restrict__ dyp, int n, int h, int w, int C, int k,
                             int s, int p, int oh, int ow, bf16* __restrict__ dx) {
+  CVB_PDL_PROLOGUE();
   const int G = C / 8;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)n * h * w * G) return;
@@ -302,6 +310,7 @@ __global__ void maxpool_bwd(const bf16* __restrict__ x, const bf16* __restrict__
 // per output element: the backward then needs no window re-scan
 __global__ void maxpool_fwd_idx(const bf16* __restrict__ x, int n, int h, int w, int C, int k, int s, int p, int oh,
                                 int ow, bf16* __restrict__ y, int ycs, uint8_t* __restrict__ idx) {
+  CVB_PDL_PROLOGUE();
   const int G = C / 8;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)n * oh * ow * G) return;
@@ -333,6 +342,7 @@ __global__ void maxpool_fwd_idx(const bf16* __restrict__ x, int n, int h, int w,
 // gather: input (iy, ix) takes dy of every window (oy, ox) whose stored arg-max is it
 __global__ void maxpool_bwd_idx(const uint8_t* __restrict__ idx, const bf16* __restrict__ dyp, int n, int h, int w,
                                 int C, int k, int s, int p, int oh, int ow, bf16* __restrict__ dx) {
+  CVB_PDL_PROLOGUE();
   const int G = C / 8;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)n * h * w * G) return;
@@ -363,6 +373,7 @@ __global__ void maxpool_bwd_idx(const uint8_t* __restrict__ idx, const bf16* __r
 // routes dy to the window's first arg-max and writes zeros to the other three inputs.
 __global__ void maxpool2_bwd(const bf16* __restrict__ x, const bf16* __restrict__ dyp, int n, int h, int w, int C,
                              int oh, int ow, bf16* __restrict__ dx) {
+  CVB_PDL_PROLOGUE();
   const int G = C / 8;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)n * oh * ow * G) return;
@@ -393,6 +404,7 @@ __global__ void maxpool2_bwd(const bf16* __restrict__ x, const bf16* __restrict_
 
 __global__ void avgpool_fwd(const bf16* __restrict__ x, int n, int h, int w, int C, int xcs, int k, int oh, int ow,
                             bf16* __restrict__ y, int ycs) {
+  CVB_PDL_PROLOGUE();
   const int G = C / 8;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)n * oh * ow * G) return;
@@ -415,6 +427,7 @@ __global__ void avgpool_fwd(const bf16* __restrict__ x, int n, int h, int w, int
 
 __global__ void avgpool_bwd(const bf16* __restrict__ dy, int n, int h, int w, int C, int k, int oh, int ow,
                             bf16* __restrict__ dx, int dxcs) {
+  CVB_PDL_PROLOGUE();
   const int G = C / 8;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)n * h * w * G) return;
@@ -437,6 +450,7 @@ __global__ void avgpool_bwd(const bf16* __restrict__ dy, int n, int h, int w, in
 
 // global average pool: x [n][hw][C] (stride xcs) -> y [n][C] bf16
 __global__ void gap_fwd(const bf16* __restrict__ x, int n, int hw, int C, int xcs, bf16* __restrict__ y) {
+  CVB_PDL_PROLOGUE();
   const int G = C / 8;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n * G) return;
@@ -455,6 +469,7 @@ __global__ void gap_fwd(const bf16* __restrict__ x, int n, int hw, int C, int xc
 }
 
 __global__ void gap_bwd(const bf16* __restrict__ dy, int n, int hw, int C, bf16* __restrict__ dx) {
+  CVB_PDL_PROLOGUE();
   const int G = C / 8;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)n * hw * G) return;
@@ -472,6 +487,7 @@ __global__ void gap_bwd(const bf16* __restrict__ dy, int n, int hw, int C, bf16*
 // ---- softmax cross-entropy: one warp per row, classes <= 32*4 ----------------------------
 __global__ void softmax_xent(const float* __restrict__ logits, int B, int C, const int32_t* __restrict__ labels,
                              float scale, float* __restrict__ row_loss, bf16* __restrict__ dlogits, int ldd) {
+  CVB_PDL_PROLOGUE();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (row >= B) return;
   const float* l = logits + (int64_t)row * ldd;   // logits and dlogits share the row stride
@@ -499,6 +515,7 @@ __global__ void softmax_xent(const float* __restrict__ logits, int B, int C, con
 
 // deterministic sum of n floats into out[0] (single block)
 __global__ void sum_small(const float* __restrict__ x, int n, float scale, float* __restrict__ out) {
+  CVB_PDL_PROLOGUE();
   __shared__ double sh[256];
   double a = 0;
   for (int i = threadIdx.x; i < n; i += 256) a += x[i];
@@ -514,6 +531,7 @@ __global__ void sum_small(const float* __restrict__ x, int n, float scale, float
 // ---- misc -------------------------------------------------------------------------------
 __global__ void reduce_splits(const float* __restrict__ part, int splits, int64_t count, float* __restrict__ out,
                               int accumulate, float scale) {
+  CVB_PDL_PROLOGUE();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
   float a = 0.f;
@@ -526,6 +544,7 @@ __global__ void reduce_splits(const float* __restrict__ part, int splits, int64_
 __global__ void reduce_splits_act(const float* __restrict__ part, int splits, int rows, int cols,
                                   const float* __restrict__ bias, int relu, void* __restrict__ out, int out_f32,
                                   int64_t ldo) {
+  CVB_PDL_PROLOGUE();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t count = (int64_t)rows * cols;
   if (i >= count) return;
@@ -540,6 +559,7 @@ __global__ void reduce_splits_act(const float* __restrict__ part, int splits, in
 
 // wt[ci][kh'][kw'][co] = w[co][KH-1-kh'][KW-1-kw'][ci]
 __global__ void weight_flip(const bf16* __restrict__ w, int cout, int kh, int kw, int cin, bf16* __restrict__ wt) {
+  CVB_PDL_PROLOGUE();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t total = (int64_t)cout * kh * kw * cin;
   if (i >= total) return;
@@ -553,6 +573,7 @@ __global__ void weight_flip(const bf16* __restrict__ w, int cout, int kh, int kw
 
 __global__ void zero_upsample(const bf16* __restrict__ dy, int n, int oh, int ow, int C, int dycs, bf16* __restrict__ out,
                               int uh, int uw) {
+  CVB_PDL_PROLOGUE();
   const int G = C / 8;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)n * uh * uw * G) return;
@@ -567,6 +588,7 @@ __global__ void zero_upsample(const bf16* __restrict__ dy, int n, int oh, int ow
 // column sums of a row-major [rows][cols] bf16/fp32 matrix -> fp32 (bias gradients)
 __global__ void col_sum(const void* __restrict__ x, int is_f32, int64_t rows, int cols, int64_t ld, float* __restrict__ out,
                         int accumulate) {
+  CVB_PDL_PROLOGUE();
   const int c = blockIdx.x * 32 + (threadIdx.x & 31);
   const int rl = threadIdx.x >> 5;  // 8 row lanes
   __shared__ float sh[8][32];
@@ -586,6 +608,7 @@ __global__ void col_sum(const void* __restrict__ x, int is_f32, int64_t rows, in
 
 // relu backward on a bf16 matrix in place: dx = dy * (y > 0)
 __global__ void relu_bwd(bf16* __restrict__ dy, const bf16* __restrict__ y, int64_t n8) {
+  CVB_PDL_PROLOGUE();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n8) return;
   float d[8], v[8];
@@ -597,6 +620,7 @@ __global__ void relu_bwd(bf16* __restrict__ dy, const bf16* __restrict__ y, int6
 }
 
 __global__ void relu_fwd(bf16* __restrict__ x, int64_t n8) {
+  CVB_PDL_PROLOGUE();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n8) return;
   float v[8];
@@ -611,6 +635,7 @@ __global__ void relu_fwd(bf16* __restrict__ x, int64_t n8) {
 // Device-side step counter so a captured CUDA graph can be replayed: step += 1 and the
 // bias-correction factors are recomputed on the device every replay.
 __global__ void adam_schedule(int32_t* step, float lr, float b1, float b2, float* sched) {
+  CVB_PDL_PROLOGUE();
   const int t = ++(*step);
   sched[0] = (float)((double)lr / (1.0 - pow((double)b1, (double)t)));
   sched[1] = (float)(1.0 / sqrt(1.0 - pow((double)b2, (double)t)));
@@ -619,6 +644,7 @@ __global__ void adam_schedule(int32_t* step, float lr, float b1, float b2, float
 __global__ void adam_step(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v,
                           bf16* __restrict__ pb, int64_t n, float b1, float b2, float eps, float step_size,
                           float inv_bc2_sqrt, float grad_scale, const float* __restrict__ sched) {
+  CVB_PDL_PROLOGUE();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (sched) { step_size = sched[0]; inv_bc2_sqrt = sched[1]; }
@@ -636,6 +662,7 @@ __global__ void adam_step(float* __restrict__ p, const float* __restrict__ g, fl
 // torch.optim.SGD with momentum (dampening 0, no nesterov) + optional weight decay
 __global__ void sgd_step(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ buf, bf16* __restrict__ pb,
                          int64_t n, float lr, float momentum, float wd, float grad_scale, int first) {
+  CVB_PDL_PROLOGUE();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   float d = g[i] * grad_scale + wd * p[i];
@@ -648,6 +675,7 @@ __global__ void sgd_step(float* __restrict__ p, const float* __restrict__ g, flo
 // strided 2-D cast: y[r][c] = bf16(x[r][c]) with row strides (DenseNet concat-gradient slices)
 __global__ void cast_rows(const float* __restrict__ x, int64_t ldx, bf16* __restrict__ y, int64_t ldy, int64_t rows,
                           int cols) {
+  CVB_PDL_PROLOGUE();
   const int G = cols / 8;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= rows * G) return;
@@ -660,6 +688,7 @@ __global__ void cast_rows(const float* __restrict__ x, int64_t ldx, bf16* __rest
 }
 
 __global__ void cast_f32_bf16(const float* __restrict__ x, bf16* __restrict__ y, int64_t n) {
+  CVB_PDL_PROLOGUE();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = __float2bfloat16_rn(x[i]);
 }
@@ -695,8 +724,8 @@ CVB_API int cvb_bn_stats(const void* x, int64_t rows, int C, int xcs, float* ws,
   int64_t rpb;
   int nb = stats_blocks(rows, C, &rpb);
   const int G = C / 8, RL = ST_THREADS / G;
-  chan_stats_partial<<<nb, ST_THREADS, RL * G * 16 * sizeof(float), STREAM>>>((const bf16*)x, rows, C, xcs, rpb, ws);
-  bn_finalize<<<(C + 31) / 32, FIN_WARPS * 32, 0, STREAM>>>(ws, nb, C, (double)rows, eps, mean, rstd, run_mean,
+  cvb_launch(chan_stats_partial, nb, ST_THREADS, RL * G * 16 * sizeof(float), STREAM, (const bf16*)x, rows, C, xcs, rpb, ws);
+  cvb_launch(bn_finalize, (C + 31) / 32, FIN_WARPS * 32, 0, STREAM, ws, nb, C, (double)rows, eps, mean, rstd, run_mean,
                                                              run_var, momentum);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
@@ -705,7 +734,7 @@ CVB_API int cvb_bn_stats(const void* x, int64_t rows, int C, int xcs, float* ws,
 CVB_API int cvb_bn_apply(const void* x, int64_t rows, int C, int xcs, const float* mean, const float* rstd,
                          const float* gamma, const float* beta, const void* res, int rcs, int relu, void* y, int ycs,
                          int ycoff, void* stream) {
-  bn_apply<<<nblocks(rows * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, rows, C, xcs, mean, rstd, gamma, beta,
+  cvb_launch(bn_apply, nblocks(rows * (C / 8)), 256, 0, STREAM, (const bf16*)x, rows, C, xcs, mean, rstd, gamma, beta,
                                                        (const bf16*)res, rcs, relu, (bf16*)y, ycs, ycoff);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
@@ -723,12 +752,12 @@ CVB_API int cvb_bn_backward(const void* dy, int dycs, const void* x, int xcs, co
   int64_t rpb;
   int nb = stats_blocks(rows, C, &rpb);
   const int G = C / 8, RL = ST_THREADS / G;
-  bn_bwd_partial<<<nb, ST_THREADS, RL * G * 16 * sizeof(float), STREAM>>>(
+  cvb_launch(bn_bwd_partial, nb, ST_THREADS, RL * G * 16 * sizeof(float), STREAM, 
       (const bf16*)dy, dycs, (const bf16*)x, xcs, (const bf16*)y, ycs, rows, C, mean, rstd, gamma, beta, relu, rpb, ws,
       (bf16*)dz_out);
-  bn_bwd_finalize<<<(C + 31) / 32, FIN_WARPS * 32, 0, STREAM>>>(ws, nb, C, dbeta, dgamma);
+  cvb_launch(bn_bwd_finalize, (C + 31) / 32, FIN_WARPS * 32, 0, STREAM, ws, nb, C, dbeta, dgamma);
   if (dx || dx32)
-    bn_bwd_apply<<<nblocks(rows * G), 256, 0, STREAM>>>((const bf16*)dy, dycs, (const bf16*)x, xcs, (const bf16*)y, ycs,
+    cvb_launch(bn_bwd_apply, nblocks(rows * G), 256, 0, STREAM, (const bf16*)dy, dycs, (const bf16*)x, xcs, (const bf16*)y, ycs,
                                                         rows, C, mean, rstd, gamma, beta, relu, dbeta, dgamma, (bf16*)dx,
                                                         dxcs, dx32, accum32);
   CVB_CHECK_LAUNCH();
@@ -737,7 +766,7 @@ CVB_API int cvb_bn_backward(const void* dy, int dycs, const void* x, int xcs, co
 
 CVB_API int cvb_maxpool_fwd(const void* x, int n, int h, int w, int C, int k, int s, int p, void* y, int oh, int ow,
                             int ycs, void* stream) {
-  maxpool_fwd<<<nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, n, h, w, C, k, s, p, oh, ow,
+  cvb_launch(maxpool_fwd, nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM, (const bf16*)x, n, h, w, C, k, s, p, oh, ow,
                                                                           (bf16*)y, ycs);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
@@ -746,10 +775,10 @@ CVB_API int cvb_maxpool_fwd(const void* x, int n, int h, int w, int C, int k, in
 CVB_API int cvb_maxpool_bwd(const void* x, const void* dy, int n, int h, int w, int C, int k, int s, int p, int oh,
                             int ow, void* dx, void* stream) {
   if (k == 2 && s == 2 && p == 0 && h == 2 * oh && w == 2 * ow)
-    maxpool2_bwd<<<nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, (const bf16*)dy, n, h, w,
+    cvb_launch(maxpool2_bwd, nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM, (const bf16*)x, (const bf16*)dy, n, h, w,
                                                                               C, oh, ow, (bf16*)dx);
   else
-    maxpool_bwd<<<nblocks((int64_t)n * h * w * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, (const bf16*)dy, n, h, w, C,
+    cvb_launch(maxpool_bwd, nblocks((int64_t)n * h * w * (C / 8)), 256, 0, STREAM, (const bf16*)x, (const bf16*)dy, n, h, w, C,
                                                                            k, s, p, oh, ow, (bf16*)dx);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
@@ -758,7 +787,7 @@ CVB_API int cvb_maxpool_bwd(const void* x, const void* dy, int n, int h, int w, 
 CVB_API int cvb_maxpool_fwd_idx(const void* x, int n, int h, int w, int C, int k, int s, int p, void* y, int oh, int ow,
                                 int ycs, void* idx, void* stream) {
   if (C % 8 || k * k > 256) { cvb_set_error("maxpool_fwd_idx: bad shape"); return CVB_EINVAL; }
-  maxpool_fwd_idx<<<nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, n, h, w, C, k, s, p, oh,
+  cvb_launch(maxpool_fwd_idx, nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM, (const bf16*)x, n, h, w, C, k, s, p, oh,
                                                                               ow, (bf16*)y, ycs, (uint8_t*)idx);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
@@ -766,7 +795,7 @@ CVB_API int cvb_maxpool_fwd_idx(const void* x, int n, int h, int w, int C, int k
 
 CVB_API int cvb_maxpool_bwd_idx(const void* idx, const void* dy, int n, int h, int w, int C, int k, int s, int p, int oh,
                                 int ow, void* dx, void* stream) {
-  maxpool_bwd_idx<<<nblocks((int64_t)n * h * w * (C / 8)), 256, 0, STREAM>>>((const uint8_t*)idx, (const bf16*)dy, n, h,
+  cvb_launch(maxpool_bwd_idx, nblocks((int64_t)n * h * w * (C / 8)), 256, 0, STREAM, (const uint8_t*)idx, (const bf16*)dy, n, h,
                                                                             w, C, k, s, p, oh, ow, (bf16*)dx);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
@@ -774,7 +803,7 @@ CVB_API int cvb_maxpool_bwd_idx(const void* idx, const void* dy, int n, int h, i
 
 CVB_API int cvb_avgpool_fwd(const void* x, int n, int h, int w, int C, int xcs, int k, void* y, int ycs, void* stream) {
   const int oh = h / k, ow = w / k;
-  avgpool_fwd<<<nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, n, h, w, C, xcs, k, oh, ow,
+  cvb_launch(avgpool_fwd, nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM, (const bf16*)x, n, h, w, C, xcs, k, oh, ow,
                                                                           (bf16*)y, ycs);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
@@ -782,19 +811,19 @@ CVB_API int cvb_avgpool_fwd(const void* x, int n, int h, int w, int C, int xcs, 
 
 CVB_API int cvb_avgpool_bwd(const void* dy, int n, int h, int w, int C, int k, void* dx, int dxcs, void* stream) {
   const int oh = h / k, ow = w / k;
-  avgpool_bwd<<<nblocks((int64_t)n * h * w * (C / 8)), 256, 0, STREAM>>>((const bf16*)dy, n, h, w, C, k, oh, ow, (bf16*)dx, dxcs);
+  cvb_launch(avgpool_bwd, nblocks((int64_t)n * h * w * (C / 8)), 256, 0, STREAM, (const bf16*)dy, n, h, w, C, k, oh, ow, (bf16*)dx, dxcs);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
 
 CVB_API int cvb_gap_fwd(const void* x, int n, int hw, int C, int xcs, void* y, void* stream) {
-  gap_fwd<<<nblocks((int64_t)n * (C / 8)), 256, 0, STREAM>>>((const bf16*)x, n, hw, C, xcs, (bf16*)y);
+  cvb_launch(gap_fwd, nblocks((int64_t)n * (C / 8)), 256, 0, STREAM, (const bf16*)x, n, hw, C, xcs, (bf16*)y);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
 
 CVB_API int cvb_gap_bwd(const void* dy, int n, int hw, int C, void* dx, void* stream) {
-  gap_bwd<<<nblocks((int64_t)n * hw * (C / 8)), 256, 0, STREAM>>>((const bf16*)dy, n, hw, C, (bf16*)dx);
+  cvb_launch(gap_bwd, nblocks((int64_t)n * hw * (C / 8)), 256, 0, STREAM, (const bf16*)dy, n, hw, C, (bf16*)dx);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
@@ -804,55 +833,55 @@ CVB_API int cvb_gap_bwd(const void* dy, int n, int hw, int C, void* dx, void* st
 CVB_API int cvb_softmax_xent(const float* logits, int B, int C, const int32_t* labels, float grad_scale, float* row_ws,
                              float* loss_out, void* dlogits, int ldd, void* stream) {
   if (C > 128) { cvb_set_error("softmax_xent: C > 128"); return CVB_EINVAL; }
-  softmax_xent<<<nblocks((int64_t)B * 32), 256, 0, STREAM>>>(logits, B, C, labels, grad_scale, row_ws, (bf16*)dlogits, ldd);
-  sum_small<<<1, 256, 0, STREAM>>>(row_ws, B, 1.0f / B, loss_out);
+  cvb_launch(softmax_xent, nblocks((int64_t)B * 32), 256, 0, STREAM, logits, B, C, labels, grad_scale, row_ws, (bf16*)dlogits, ldd);
+  cvb_launch(sum_small, 1, 256, 0, STREAM, row_ws, B, 1.0f / B, loss_out);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
 
 CVB_API int cvb_reduce_splits(const float* part, int splits, int64_t count, float* out, int accumulate, float scale,
                               void* stream) {
-  reduce_splits<<<nblocks(count), 256, 0, STREAM>>>(part, splits, count, out, accumulate, scale);
+  cvb_launch(reduce_splits, nblocks(count), 256, 0, STREAM, part, splits, count, out, accumulate, scale);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
 
 CVB_API int cvb_reduce_splits_act(const float* part, int splits, int rows, int cols, const float* bias, int relu,
                                   void* out, int out_f32, int64_t ldo, void* stream) {
-  reduce_splits_act<<<nblocks((int64_t)rows * cols), 256, 0, STREAM>>>(part, splits, rows, cols, bias, relu, out, out_f32,
+  cvb_launch(reduce_splits_act, nblocks((int64_t)rows * cols), 256, 0, STREAM, part, splits, rows, cols, bias, relu, out, out_f32,
                                                                       ldo);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
 
 CVB_API int cvb_weight_flip(const void* w, int cout, int kh, int kw, int cin, void* wt, void* stream) {
-  weight_flip<<<nblocks((int64_t)cout * kh * kw * cin), 256, 0, STREAM>>>((const bf16*)w, cout, kh, kw, cin, (bf16*)wt);
+  cvb_launch(weight_flip, nblocks((int64_t)cout * kh * kw * cin), 256, 0, STREAM, (const bf16*)w, cout, kh, kw, cin, (bf16*)wt);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
 
 CVB_API int cvb_zero_upsample(const void* dy, int n, int oh, int ow, int C, int dycs, void* out, void* stream) {
   const int uh = 2 * oh - 1, uw = 2 * ow - 1;
-  zero_upsample<<<nblocks((int64_t)n * uh * uw * (C / 8)), 256, 0, STREAM>>>((const bf16*)dy, n, oh, ow, C, dycs, (bf16*)out, uh, uw);
+  cvb_launch(zero_upsample, nblocks((int64_t)n * uh * uw * (C / 8)), 256, 0, STREAM, (const bf16*)dy, n, oh, ow, C, dycs, (bf16*)out, uh, uw);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
 
 CVB_API int cvb_col_sum(const void* x, int is_f32, int64_t rows, int cols, int64_t ld, float* out, int accumulate,
                         void* stream) {
-  col_sum<<<(cols + 31) / 32, 256, 0, STREAM>>>(x, is_f32, rows, cols, ld, out, accumulate);
+  cvb_launch(col_sum, (cols + 31) / 32, 256, 0, STREAM, x, is_f32, rows, cols, ld, out, accumulate);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
 
 CVB_API int cvb_relu_fwd(void* x, int64_t n, void* stream) {
-  relu_fwd<<<nblocks(n / 8), 256, 0, STREAM>>>((bf16*)x, n / 8);
+  cvb_launch(relu_fwd, nblocks(n / 8), 256, 0, STREAM, (bf16*)x, n / 8);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
 
 CVB_API int cvb_relu_bwd(void* dy, const void* y, int64_t n, void* stream) {
-  relu_bwd<<<nblocks(n / 8), 256, 0, STREAM>>>((bf16*)dy, (const bf16*)y, n / 8);
+  cvb_launch(relu_bwd, nblocks(n / 8), 256, 0, STREAM, (bf16*)dy, (const bf16*)y, n / 8);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
@@ -863,12 +892,12 @@ CVB_API int cvb_adam_step(float* p, const float* g, float* m, float* v, void* pb
                           float eps, int64_t step, float grad_scale, int32_t* step_dev, float* sched_dev, void* stream) {
   if (step > 0) {
     const double bc1 = 1.0 - pow((double)b1, (double)step), bc2 = 1.0 - pow((double)b2, (double)step);
-    adam_step<<<nblocks(n), 256, 0, STREAM>>>(p, g, m, v, (bf16*)pb, n, b1, b2, eps, (float)(lr / bc1),
+    cvb_launch(adam_step, nblocks(n), 256, 0, STREAM, p, g, m, v, (bf16*)pb, n, b1, b2, eps, (float)(lr / bc1),
                                               (float)(1.0 / sqrt(bc2)), grad_scale, nullptr);
   } else {
     if (!step_dev || !sched_dev) { cvb_set_error("adam_step: device counter mode needs step_dev/sched_dev"); return CVB_EINVAL; }
-    adam_schedule<<<1, 1, 0, STREAM>>>(step_dev, lr, b1, b2, sched_dev);
-    adam_step<<<nblocks(n), 256, 0, STREAM>>>(p, g, m, v, (bf16*)pb, n, b1, b2, eps, 0.f, 0.f, grad_scale, sched_dev);
+    cvb_launch(adam_schedule, 1, 1, 0, STREAM, step_dev, lr, b1, b2, sched_dev);
+    cvb_launch(adam_step, nblocks(n), 256, 0, STREAM, p, g, m, v, (bf16*)pb, n, b1, b2, eps, 0.f, 0.f, grad_scale, sched_dev);
   }
   CVB_CHECK_LAUNCH();
   return CVB_OK;
@@ -876,20 +905,20 @@ CVB_API int cvb_adam_step(float* p, const float* g, float* m, float* v, void* pb
 
 CVB_API int cvb_sgd_step(float* p, const float* g, float* buf, void* pb, int64_t n, float lr, float momentum, float wd,
                          float grad_scale, int first, void* stream) {
-  sgd_step<<<nblocks(n), 256, 0, STREAM>>>(p, g, buf, (bf16*)pb, n, lr, momentum, wd, grad_scale, first);
+  cvb_launch(sgd_step, nblocks(n), 256, 0, STREAM, p, g, buf, (bf16*)pb, n, lr, momentum, wd, grad_scale, first);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
 
 CVB_API int cvb_cast_rows(const float* x, int64_t ldx, void* y, int64_t ldy, int64_t rows, int cols, void* stream) {
   if (cols % 8) { cvb_set_error("cast_rows: cols must be a multiple of 8"); return CVB_EINVAL; }
-  cast_rows<<<nblocks(rows * (cols / 8)), 256, 0, STREAM>>>(x, ldx, (bf16*)y, ldy, rows, cols);
+  cvb_launch(cast_rows, nblocks(rows * (cols / 8)), 256, 0, STREAM, x, ldx, (bf16*)y, ldy, rows, cols);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
 
 CVB_API int cvb_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream) {
-  cast_f32_bf16<<<nblocks(n), 256, 0, STREAM>>>(x, (bf16*)y, n);
+  cvb_launch(cast_f32_bf16, nblocks(n), 256, 0, STREAM, x, (bf16*)y, n);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }

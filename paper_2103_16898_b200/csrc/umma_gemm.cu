@@ -403,6 +403,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const uint32_t smem0 = smem_u32(smem);
+  CVB_PDL_PROLOGUE();   // barrier init / TMEM alloc / descriptor prefetch overlap the previous kernel
 
   const int units = p.m_tiles * p.n_tiles * p.splits;
 
@@ -961,7 +962,7 @@ int launch(GemmParams& p, cudaStream_t stream) {
   p.fd_mn = make_fastdiv((uint32_t)(p.m_tiles * p.n_tiles));
   p.fd_pw = make_fastdiv((uint32_t)(p.ptiles_w > 0 ? p.ptiles_w : 1));
   p.fd_ph = make_fastdiv((uint32_t)(p.ptiles_h > 0 ? p.ptiles_h : 1));
-  umma_gemm_kernel<<<grid, (2 + p.n_epi) * 32, smem, stream>>>(p);
+  cvb_launch(umma_gemm_kernel, grid, (2 + p.n_epi) * 32, smem, stream, p);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
@@ -1132,6 +1133,7 @@ struct ClassW {
 
 __global__ void dgrad_class_weights(const __nv_bfloat16* __restrict__ w, int cout, int KH, int KW, int cin, ClassW cw,
                                     __nv_bfloat16* __restrict__ out) {
+  CVB_PDL_PROLOGUE();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= cw.off[4]) return;
   int c = 0;
@@ -1235,7 +1237,7 @@ CVB_API int cvb_conv2d_dgrad_s2(const void* dy, int n, int oh, int ow, int cout,
   }
   if (!accumulate && have != 15) { cvb_set_error("dgrad_s2: a parity class has no taps; accumulate into zeroed dx"); return CVB_EINVAL; }
   const int64_t total = cw.off[4];
-  dgrad_class_weights<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+  cvb_launch(dgrad_class_weights, (unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream, 
       (const __nv_bfloat16*)w, cout, kh, kw, cin, cw, (__nv_bfloat16*)wscratch);
   CVB_CHECK_LAUNCH();
   for (int c = 0; c < 4; c++)
