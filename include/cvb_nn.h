@@ -88,6 +88,10 @@ int cvb_reduce_splits(const float* part, int splits, int64_t count, float* out, 
 /* split-K epilogue of a dense layer: out[r][c] = act(sum_s part[s][r][c] + bias[c]) */
 int cvb_reduce_splits_act(const float* part, int splits, int rows, int cols, const float* bias, int relu, void* out,
                           int out_f32, int64_t ldo, void* stream);
+/* all stride-1 dgrad weight flips in one launch: desc_dev = nlayers x {src, dst, cout, kh, kw, cin}
+   (int64 element offsets into pb / fb) */
+int cvb_weight_flip_batched(const void* pb, void* fb, const int64_t* desc_dev, int nlayers, int64_t max_elems,
+                            void* stream);
 int cvb_weight_flip(const void* w, int cout, int kh, int kw, int cin, void* wt, void* stream);
 int cvb_zero_upsample(const void* dy, int n, int oh, int ow, int C, int dycs, void* out, void* stream);
 int cvb_col_sum(const void* x, int is_f32, int64_t rows, int cols, int64_t ld, float* out, int accumulate, void* stream);

@@ -65,6 +65,7 @@ SIGNATURES = {
                               _P, _INT, _INT, _P]),
     "cvb_bn_backward_fused": (_INT, [_P, _INT, _P, _INT, _P, _INT, _I64, _INT, _P, _P, _P, _P, _INT, _P, _P, _P, _P,
                                      _INT, _P, _INT, _P, _P]),
+    "cvb_weight_flip_batched": (_INT, [_P, _P, _P, _INT, _I64, _P]),
     "cvb_maxpool_fwd_idx": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT, _INT, _P, _P]),
     "cvb_maxpool_bwd_idx": (_INT, [_P, _P, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _P, _P]),
     "cvb_maxpool_fwd": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT, _INT, _P]),

@@ -571,6 +571,25 @@ __global__ void weight_flip(const bf16* __restrict__ w, int cout, int kh, int kw
   wt[i] = w[(((int64_t)co * kh + (kh - 1 - y)) * kw + (kw - 1 - x)) * cin + ci];
 }
 
+// All stride-1 dgrad weight flips of the model in one launch (run after the optimiser):
+// desc[l] = {src offset, dst offset, cout, kh, kw, cin} into the flat bf16 weight / flipped
+// buffers; blockIdx.y = layer.
+__global__ void weight_flip_batched(const bf16* __restrict__ pb, bf16* __restrict__ fb, const int64_t* __restrict__ desc) {
+  CVB_PDL_PROLOGUE();
+  const int64_t* d = desc + 6 * blockIdx.y;
+  const int64_t src = d[0], dst = d[1];
+  const int cout = (int)d[2], kh = (int)d[3], kw = (int)d[4], cin = (int)d[5];
+  const int64_t total = (int64_t)cout * kh * kw * cin;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int co = (int)(i % cout);
+    int64_t r = i / cout;
+    const int x = (int)(r % kw); r /= kw;
+    const int y = (int)(r % kh);
+    const int ci = (int)(r / kh);
+    fb[dst + i] = pb[src + (((int64_t)co * kh + (kh - 1 - y)) * kw + (kw - 1 - x)) * cin + ci];
+  }
+}
+
 __global__ void zero_upsample(const bf16* __restrict__ dy, int n, int oh, int ow, int C, int dycs, bf16* __restrict__ out,
                               int uh, int uw) {
   CVB_PDL_PROLOGUE();
@@ -856,6 +875,16 @@ CVB_API int cvb_reduce_splits_act(const float* part, int splits, int rows, int c
 
 CVB_API int cvb_weight_flip(const void* w, int cout, int kh, int kw, int cin, void* wt, void* stream) {
   cvb_launch(weight_flip, nblocks((int64_t)cout * kh * kw * cin), 256, 0, STREAM, (const bf16*)w, cout, kh, kw, cin, (bf16*)wt);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_weight_flip_batched(const void* pb, void* fb, const int64_t* desc_dev, int nlayers, int64_t max_elems,
+                                    void* stream) {
+  if (nlayers <= 0) return CVB_OK;
+  unsigned gx = (unsigned)((max_elems + 255) / 256);
+  if (gx > 512) gx = 512;
+  cvb_launch(weight_flip_batched, dim3(gx, nlayers), 256, 0, STREAM, (const bf16*)pb, (bf16*)fb, desc_dev);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }

@@ -321,6 +321,14 @@ def weight_flip(w, wt):
     _lib.check(rc, "weight_flip")
 
 
+def weight_flip_batched(pb, fb, desc_dev, nlayers, max_elems, nbytes):
+    tok = REC.begin(1, "layout", 0, nbytes)
+    rc = _lib_bound().cvb_weight_flip_batched(pb.data_ptr(), fb.data_ptr(), desc_dev.data_ptr(), nlayers, max_elems,
+                                              _stream())
+    REC.end(tok)
+    _lib.check(rc, "weight_flip_batched")
+
+
 def zero_upsample(dy, out):
     n, oh, ow, c = dy.shape
     tok = REC.begin(1, "layout", 0, (dy.numel() + out.numel()) * 2)

@@ -50,6 +50,16 @@ class ParamStore:
         self.logical += init.numel() if logical is None else logical
         return name
 
+    def want_flip(self, name):
+        """Keep a flipped/transposed bf16 copy [cin][kh][kw][cout] of conv weight `name` for
+        stride-1 dgrad, refreshed for all layers in one launch after every optimiser step."""
+        if name not in getattr(self, "flip_names", []):
+            self.flip_names = getattr(self, "flip_names", []) + [name]
+
+    def flip_all(self):
+        if self.flip_n:
+            K.weight_flip_batched(self.pb, self.fb, self.flip_desc, self.flip_n, self.flip_max, self.flip_bytes)
+
     def finalize(self, device):
         offs, off = {}, 0
         for name, shape, _ in self.specs:
@@ -70,6 +80,24 @@ class ParamStore:
             self.b[name] = self.pb[o:o + n].view(shape)
             self.p[name].copy_(init.to(device))
         K.cast_f32_bf16(self.p32, self.pb)
+        # flipped dgrad weights: one flat bf16 buffer, one launch for all layers
+        shapes = {name: shape for name, shape, _ in self.specs}
+        names = getattr(self, "flip_names", [])
+        desc, self.f, foff, self.flip_max = [], {}, 0, 1
+        for name in names:
+            cout, kh, kw, cin = shapes[name]
+            n = cout * kh * kw * cin
+            desc += [offs[name], foff, cout, kh, kw, cin]
+            self.f[name] = (foff, (cin, kh, kw, cout))
+            foff += (n + ALIGN - 1) // ALIGN * ALIGN
+            self.flip_max = max(self.flip_max, n)
+        self.fb = torch.zeros(max(1, foff), dtype=BF16, device=device)
+        for name, (o, shp) in list(self.f.items()):
+            self.f[name] = self.fb[o:o + math.prod(shp)].view(shp)
+        self.flip_n = len(names)
+        self.flip_bytes = 4 * foff
+        self.flip_desc = torch.tensor(desc if desc else [0], dtype=torch.int64, device=device)
+        self.flip_all()
         self.step_dev = torch.zeros(1, dtype=torch.int32, device=device)
         self.sched = torch.zeros(2, dtype=F32, device=device)
 
@@ -115,6 +143,8 @@ class ConvBN:
         if cin_real != cin:
             w = torch.cat([w, torch.zeros(cout, k, k, cin - cin_real)], dim=3)
         self.W = ps.add(f"{name}.w", w, logical=cout * k * k * cin_real)
+        if need_dgrad and stride == 1:
+            ps.want_flip(self.W)
         self.G = ps.add(f"{name}.gamma", torch.ones(cout))
         self.B = ps.add(f"{name}.beta", torch.zeros(cout))
 
@@ -171,7 +201,10 @@ class ConvBN:
                                                                      accumulate=dx_accumulate, wscratch=wt,
                                                                      acct_flops=self.flops):
                 return
-            K.weight_flip(ps.b[self.W], wt)
+            if self.s == 1 and cin == self.cin and self.W in ps.f:
+                wt = ps.f[self.W]          # refreshed for every layer by ParamStore.flip_all
+            else:
+                K.weight_flip(ps.b[self.W], wt)
             src = self.dz
             if self.s == 2:
                 uh, uw = 2 * self.oh - 1, 2 * self.ow - 1
@@ -283,6 +316,7 @@ class Net:
     def optimizer_step(self):
         K.adam_step(self.ps.p32, self.ps.g32, self.ps.m, self.ps.v, self.ps.pb, self.lr, self.b1, self.b2, self.eps,
                     step=0, grad_scale=self.grad_scale, step_dev=self.ps.step_dev, sched_dev=self.ps.sched)
+        self.ps.flip_all()   # next step's dgrad weights
 
     @property
     def num_params(self):
@@ -486,6 +520,8 @@ class Conv:
         self.cin, self.cout, self.k, self.s, self.pad = cin, cout, k, stride, pad
         bound = 1.0 / math.sqrt(cin * k * k)
         self.W = ps.add(f"{name}.w", _uniform(gen, (cout, k, k, cin), bound))
+        if stride == 1:
+            ps.want_flip(self.W)
 
     def build(self, n, h, w, scratch):
         self.n, self.h, self.w = n, h, w
@@ -511,8 +547,11 @@ class Conv:
         K.reduce_splits(part, used, count, ps.g[self.W])
         ps.grad_ready(self.W)
         if dx is not None:
-            wt = self.scratch.flip[:count].view(self.cin, self.k, self.k, self.cout)
-            K.weight_flip(ps.b[self.W], wt)
+            if self.W in ps.f:
+                wt = ps.f[self.W]
+            else:
+                wt = self.scratch.flip[:count].view(self.cin, self.k, self.k, self.cout)
+                K.weight_flip(ps.b[self.W], wt)
             K.conv2d_fwd(dz, wt, 1, self.k - 1 - self.pad, out=dx, out_hw=(self.h, self.w), acct_flops=self.flops)
 
 
