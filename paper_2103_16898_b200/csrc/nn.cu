@@ -513,6 +513,55 @@ __global__ void softmax_xent(const float* __restrict__ logits, int B, int C, con
   }
 }
 
+// softmax-CE + mean loss in one launch: every block writes its rows' losses, the last block
+// to finish (device-scope counter) sums all rows in index order -> deterministic.
+__global__ void softmax_xent_mean(const float* __restrict__ logits, int B, int C, const int32_t* __restrict__ labels,
+                                  float scale, float* __restrict__ row_loss, bf16* __restrict__ dlogits, int ldd,
+                                  float* __restrict__ loss_out, unsigned* __restrict__ counter) {
+  CVB_PDL_PROLOGUE();
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row < B) {
+    const float* l = logits + (int64_t)row * ldd;
+    float v[4];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 4; j++) { const int c = lane + 32 * j; v[j] = c < C ? l[c] : -INFINITY; mx = fmaxf(mx, v[j]); }
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float se = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; j++) { const int c = lane + 32 * j; if (c < C) se += expf(v[j] - mx); }
+    for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+    const int lab = labels[row];
+    const float lse = logf(se) + mx;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int c = lane + 32 * j;
+      if (c < C) {
+        const float pr = expf(v[j] - lse);
+        dlogits[(int64_t)row * ldd + c] = __float2bfloat16_rn((pr - (c == lab ? 1.f : 0.f)) * scale);
+        if (c == lab) row_loss[row] = lse - v[j];
+      }
+    }
+  }
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ double sh[256];
+  double a = 0;
+  for (int i = threadIdx.x; i < B; i += blockDim.x) a += __ldcg(row_loss + i);
+  sh[threadIdx.x] = a;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { loss_out[0] = (float)(sh[0] / B); *counter = 0u; }
+}
+
 // deterministic sum of n floats into out[0] (single block)
 __global__ void sum_small(const float* __restrict__ x, int n, float scale, float* __restrict__ out) {
   CVB_PDL_PROLOGUE();
@@ -608,19 +657,25 @@ __global__ void zero_upsample(const bf16* __restrict__ dy, int n, int oh, int ow
 __global__ void col_sum(const void* __restrict__ x, int is_f32, int64_t rows, int cols, int64_t ld, float* __restrict__ out,
                         int accumulate) {
   CVB_PDL_PROLOGUE();
+  // 32 columns x 32 row lanes per block; fixed-order two-level sum (deterministic)
   const int c = blockIdx.x * 32 + (threadIdx.x & 31);
-  const int rl = threadIdx.x >> 5;  // 8 row lanes
-  __shared__ float sh[8][32];
-  float a = 0.f;
+  const int rl = threadIdx.x >> 5;
+  __shared__ float sh[32][33];
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
   if (c < cols) {
-    for (int64_t r = rl; r < rows; r += 8)
-      a += is_f32 ? reinterpret_cast<const float*>(x)[r * ld + c] : __bfloat162float(reinterpret_cast<const bf16*>(x)[r * ld + c]);
+    auto at = [&](int64_t r) -> float {
+      return is_f32 ? __ldg(reinterpret_cast<const float*>(x) + r * ld + c)
+                    : __bfloat162float(reinterpret_cast<const bf16*>(x)[r * ld + c]);
+    };
+    int64_t r = rl;
+    for (; r + 96 < rows; r += 128) { a0 += at(r); a1 += at(r + 32); a2 += at(r + 64); a3 += at(r + 96); }
+    for (; r < rows; r += 32) a0 += at(r);
   }
-  sh[rl][threadIdx.x & 31] = a;
+  sh[rl][threadIdx.x & 31] = (a0 + a1) + (a2 + a3);
   __syncthreads();
   if (rl == 0 && c < cols) {
     float s = 0.f;
-    for (int l = 0; l < 8; l++) s += sh[l][threadIdx.x];
+    for (int l = 0; l < 32; l++) s += sh[l][threadIdx.x];
     out[c] = accumulate ? out[c] + s : s;
   }
 }
@@ -852,8 +907,16 @@ CVB_API int cvb_gap_bwd(const void* dy, int n, int hw, int C, void* dx, void* st
 CVB_API int cvb_softmax_xent(const float* logits, int B, int C, const int32_t* labels, float grad_scale, float* row_ws,
                              float* loss_out, void* dlogits, int ldd, void* stream) {
   if (C > 128) { cvb_set_error("softmax_xent: C > 128"); return CVB_EINVAL; }
-  cvb_launch(softmax_xent, nblocks((int64_t)B * 32), 256, 0, STREAM, logits, B, C, labels, grad_scale, row_ws, (bf16*)dlogits, ldd);
-  cvb_launch(sum_small, 1, 256, 0, STREAM, row_ws, B, 1.0f / B, loss_out);
+  static unsigned* counters[64] = {nullptr};
+  int dev = 0;
+  CVB_CUDA(cudaGetDevice(&dev));
+  if (!counters[dev]) {
+    CVB_CUDA(cudaMalloc(&counters[dev], sizeof(unsigned)));
+    CVB_CUDA(cudaMemset(counters[dev], 0, sizeof(unsigned)));
+    CVB_CUDA(cudaDeviceSynchronize());
+  }
+  cvb_launch(softmax_xent_mean, nblocks((int64_t)B * 32), 256, 0, STREAM, logits, B, C, labels, grad_scale, row_ws,
+             (bf16*)dlogits, ldd, loss_out, counters[dev]);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
@@ -898,7 +961,7 @@ CVB_API int cvb_zero_upsample(const void* dy, int n, int oh, int ow, int C, int 
 
 CVB_API int cvb_col_sum(const void* x, int is_f32, int64_t rows, int cols, int64_t ld, float* out, int accumulate,
                         void* stream) {
-  cvb_launch(col_sum, (cols + 31) / 32, 256, 0, STREAM, x, is_f32, rows, cols, ld, out, accumulate);
+  cvb_launch(col_sum, (cols + 31) / 32, 1024, 0, STREAM, x, is_f32, rows, cols, ld, out, accumulate);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }

@@ -291,7 +291,7 @@ def gap_bwd(dy, n, hw, c, dx):
 def softmax_xent(logits, B, C, labels, grad_scale, row_ws, loss_out, dlogits):
     ld = logits.shape[-1]
     assert dlogits.shape[-1] == ld
-    tok = REC.begin(2, "head", 0, B * ld * 6)
+    tok = REC.begin(1, "head", 0, B * ld * 6)
     rc = _lib_bound().cvb_softmax_xent(logits.data_ptr(), B, C, labels.data_ptr(), grad_scale, row_ws.data_ptr(),
                                        loss_out.data_ptr(), dlogits.data_ptr(), ld, _stream())
     REC.end(tok)
