@@ -84,6 +84,41 @@ class ShardLoader:
         self.aad[:len(aad)].copy_(torch.frombuffer(bytearray(aad), dtype=torch.uint8), non_blocking=True)
         self.n, self.aad_len = n, len(aad)
 
+    # -- double-buffered host->device staging (the e2e path overlaps the next shard's H2D
+    #    with this step's decrypt + training) ------------------------------------------------
+    def prefetch(self, blob_host: torch.Tensor, aad: bytes):
+        """Start the H2D copy of the NEXT shard on a copy stream into the spare buffer."""
+        if not hasattr(self, "ct_next"):
+            self.ct_next = torch.empty_like(self.ct)
+            self.aad_next = torch.zeros_like(self.aad)
+            self.copy_stream = torch.cuda.Stream()
+            self.copy_done = torch.cuda.Event()
+            self.buf_free = torch.cuda.Event()
+            self.buf_free.record()
+        n = blob_host.numel()
+        self.copy_stream.wait_event(self.buf_free)       # the spare buffer's last reader is done
+        with torch.cuda.stream(self.copy_stream):
+            self.ct_next[:n].copy_(blob_host, non_blocking=True)
+            self.aad_next[:len(aad)].copy_(torch.frombuffer(bytearray(aad), dtype=torch.uint8), non_blocking=True)
+        self.copy_done.record(self.copy_stream)
+        self.next_n, self.next_aad_len = n, len(aad)
+        self.next_src = blob_host.data_ptr()
+
+    def take_prefetched(self):
+        """Swap the prefetched shard in (the compute stream waits for its copy); returns
+        (ciphertext view, aad view)."""
+        torch.cuda.current_stream().wait_event(self.copy_done)
+        self.ct, self.ct_next = self.ct_next, self.ct
+        self.aad, self.aad_next = self.aad_next, self.aad
+        self.n, self.aad_len = self.next_n, self.next_aad_len
+        self.next_n, self.next_src = None, None
+        return self.ct[:self.n], self.aad[:self.aad_len]
+
+    def release_spare(self):
+        """Record that the compute stream is done with the (now spare) previous buffer."""
+        if hasattr(self, "buf_free"):
+            self.buf_free.record()
+
     def decrypt_decode(self, nonce: bytes, nrec: int):
         """GCM open + record decode, stream-ordered, no host sync."""
         s = self.spec

@@ -236,12 +236,25 @@ class EncryptedTrainer:
         self._run_train()
         return self.net.loss
 
-    def step_host(self, blob_host: torch.Tensor, nonce: bytes, aad: bytes, nrec: int):
-        """End-to-end step from pinned host ciphertext: H2D, decrypt, train, D2H of loss+status."""
-        self.loader.stage(blob_host, aad)
-        self.step_resident(self.loader.ct[:self.loader.n], nonce, self.loader.aad[:self.loader.aad_len], nrec)
+    def step_host(self, blob_host: torch.Tensor, nonce: bytes, aad: bytes, nrec: int, next_blob=None,
+                  next_aad: bytes | None = None):
+        """End-to-end step from pinned host ciphertext: H2D, decrypt, train, D2H of loss+status.
+
+        With ``next_blob``/``next_aad`` (the following shard) the next H2D copy is issued on a
+        copy stream while this step computes, and the next call consumes it (double buffering);
+        the result of each step is identical either way."""
+        ld = self.loader
+        if getattr(ld, "next_src", None) == blob_host.data_ptr() and ld.next_n == blob_host.numel():
+            ct, aad_dev = ld.take_prefetched()     # copied during the previous step
+        else:
+            ld.stage(blob_host, aad)
+            ct, aad_dev = ld.ct[:ld.n], ld.aad[:ld.aad_len]
+        if next_blob is not None:
+            ld.prefetch(next_blob, next_aad)
+        self.step_resident(ct, nonce, aad_dev, nrec)
+        ld.release_spare()
         self.loss_host.copy_(self.net.loss, non_blocking=True)
-        self.status_host[:1].copy_(self.loader.work[4:5], non_blocking=True)
+        self.status_host[:1].copy_(ld.work[4:5], non_blocking=True)
         return self.loss_host
 
     def check_status(self):

@@ -59,3 +59,31 @@ def test_overlapped_allreduce_step_matches_single_gpu(nccl_group, model):
         runs[dp] = (losses, tr.net.ps.p32.clone())
     assert runs[False][0] == runs[True][0]
     assert torch.equal(runs[False][1], runs[True][1])
+
+
+def test_double_buffered_host_steps_match_plain_host_steps():
+    """step_host with the next shard prefetched on a copy stream == step_host staging each
+    shard on the compute stream (same losses, same weights, bit for bit)."""
+    from bench import make_shards
+    from paper_2103_16898_b200.loader import CIFAR
+    from paper_2103_16898_b200.trainer import EncryptedTrainer
+
+    key, B = bytes(range(32)), 64
+    shards = make_shards(4, B, 9, key, CIFAR)
+    host = [torch.frombuffer(bytearray(s[3]), dtype=torch.uint8).pin_memory() for s in shards]
+    runs = []
+    for pipelined in (False, True):
+        tr = EncryptedTrainer("small_cnn", key, batch=B, spec=CIFAR, seed=2)
+        tr.capture()
+        losses = []
+        for i in range(6):
+            j, k = i % 4, (i + 1) % 4
+            if pipelined:
+                tr.step_host(host[j], shards[j][1], shards[j][2], B, next_blob=host[k], next_aad=shards[k][2])
+            else:
+                tr.step_host(host[j], shards[j][1], shards[j][2], B)
+            tr.check_status()
+            losses.append(float(tr.loss_host[0]))
+        runs.append((losses, tr.net.ps.p32.clone()))
+    assert runs[0][0] == runs[1][0]
+    assert torch.equal(runs[0][1], runs[1][1])
