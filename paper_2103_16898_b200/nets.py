@@ -229,7 +229,11 @@ class Linear:
 
     @staticmethod
     def _splits(M, N, Kd, bn_cap=256):
-        """split-K factor so that the (m, n, split) work units cover the 148 SMs."""
+        """split-K factor so that the (m, n, split) work units cover the 148 SMs; short K
+        (<= 8 K-blocks) and tiny outputs skip split-K -- the partial-sum reduction launch
+        would cost more than the GEMM."""
+        if Kd <= 512 or M * N <= 64 * 1024:
+            return 1
         tiles = -(-M // 128) * -(-N // min(bn_cap, _pad16(N)))
         return max(1, min(-(-Kd // 64), 148 // max(1, tiles)))
 
