@@ -248,11 +248,16 @@ def run_ours(args, rank, world, local_rank):
     cts = [torch.frombuffer(bytearray(s[3]), dtype=torch.uint8).to(dev) for s in shards]
     aads = [torch.frombuffer(bytearray(s[2]), dtype=torch.uint8).to(dev) for s in shards]
     host = [torch.frombuffer(bytearray(s[3]), dtype=torch.uint8).pin_memory() for s in shards]
-    # parity gate before timing: shard 0 decrypts bit-exactly on the device
-    tr.step_resident(cts[0], shards[0][1], aads[0], B)
+    # parity gate before timing: shard 0 decrypts bit-exactly on the device, and the fused
+    # decrypt-and-normalise step sees the same labels
+    tr.ctx.open_device(shards[0][1], aads[0], cts[0], tr.loader.pt, tr.loader.work)
     torch.cuda.synchronize()
     assert int(tr.loader.work[4].item()) == 0, "tag check failed"
     assert bytes(tr.loader.pt[:len(shards[0][4])].cpu().numpy()) == shards[0][4], "decrypt mismatch"
+    tr.step_resident(cts[0], shards[0][1], aads[0], B)
+    torch.cuda.synchronize()
+    want_labels = np.frombuffer(shards[0][4], dtype=np.uint8).reshape(B, rb)[:, 0]
+    assert np.array_equal(tr.loader.labels[:B].cpu().numpy(), want_labels), "fused loader labels mismatch"
     tr.capture()
 
     def barrier():

@@ -70,6 +70,15 @@ int cvb_gcm_seal_dev(cvb_gcm_ctx* ctx, const uint8_t nonce[12], const uint8_t* a
  * the binary record payload (1 label byte + C*H*W CHW bytes per record).  Output NHWC with
  * channels padded to 8, value (x/255 - mean_c)/std_c; dtype 0 = bf16, 1 = fp32; labels
  * int32.  Asynchronous. */
+/* Fused decrypt-and-normalise loader (K1b): open a sealed shard of binary records (1 label byte +
+   C*H*W CHW bytes, C <= 8) straight into the bf16 NHWC-8 training tile (allocate it zeroed; pad
+   channels are never written) and int32 labels.  Status in work_dev[4]; on a tag mismatch the
+   tile and labels are zeroed on-stream.  Replaces Volume.get + parse_dataset for the CNN
+   datasets (volume.py:185-197, workload.py:24-41). */
+int cvb_gcm_open_records_dev(cvb_gcm_ctx* ctx, const uint8_t nonce[12], const uint8_t* aad_dev, size_t aad_len,
+                             const uint8_t* blob_dev, size_t blob_len, int64_t rec_bytes, int nch, int64_t hw,
+                             const float* mean, const float* std, void* tile_dev, int32_t* labels_dev,
+                             uint32_t* work_dev, void* stream);
 int cvb_records_to_nhwc(const uint8_t* pt_dev, int64_t nrec, int64_t rec_bytes, int64_t c, int64_t h,
                         int64_t w, const float* mean, const float* std, int dtype, void* out_dev,
                         int32_t* labels_dev, void* stream);

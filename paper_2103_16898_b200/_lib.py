@@ -44,6 +44,7 @@ SIGNATURES = {
     "cvb_gcm_ctx_destroy": (None, [_P]),
     "cvb_gcm_open_dev": (_INT, [_P, _P, _P, _SZ, _P, _SZ, _P, _P, _P]),
     "cvb_gcm_seal_dev": (_INT, [_P, _P, _P, _SZ, _P, _SZ, _P, _P, _P]),
+    "cvb_gcm_open_records_dev": (_INT, [_P, _P, _P, _SZ, _P, _SZ, _I64, _INT, _I64, _P, _P, _P, _P, _P, _P]),
     "cvb_records_to_nhwc": (_INT, [_P, _I64, _I64, _I64, _I64, _I64, _P, _P, _INT, _P, _P, _P]),
     "cvb_logistic_train": (_INT, [_P, _P, _I64, _I64, _c.c_double, _I64, _INT, _P, _P]),
     # tcgen05 implicit-GEMM engine (include/cvb_nn.h)

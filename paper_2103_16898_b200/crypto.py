@@ -158,6 +158,22 @@ class GcmContext:
                                         n, out_dev.data_ptr(), work.data_ptr(), _lib.stream_ptr(stream))
         _lib.check(rc, "gcm_seal_dev")
 
+    def open_records_device(self, nonce: bytes, aad_dev, blob_dev, tile, labels, work, spec, stream=None):
+        """Fused decrypt-and-normalise (K1b): sealed binary records -> bf16 NHWC-8 training
+        tile + int32 labels in one kernel (no plaintext buffer).  ``tile`` must have been
+        allocated zeroed (its pad channels are never written).  Verdict as open_device."""
+        if len(nonce) != AEAD_NONCE_SIZE:
+            raise DecodeError(f"nonce must be {AEAD_NONCE_SIZE} bytes")
+        c, h, w = spec["c"], spec["h"], spec["w"]
+        m = (ctypes.c_float * 8)(*spec["mean"])
+        sd = (ctypes.c_float * 8)(*spec["std"])
+        aad_ptr = aad_dev.data_ptr() if aad_dev is not None and aad_dev.numel() else None
+        aad_len = aad_dev.numel() if aad_dev is not None else 0
+        rc = self._lib.cvb_gcm_open_records_dev(self._ptr, bytes(nonce), aad_ptr, aad_len, blob_dev.data_ptr(),
+                                                blob_dev.numel(), 1 + c * h * w, c, h * w, m, sd, tile.data_ptr(),
+                                                labels.data_ptr(), work.data_ptr(), _lib.stream_ptr(stream))
+        _lib.check(rc, "gcm_open_records_dev")
+
     @staticmethod
     def status_ok(work) -> bool:
         """Host check of the tag verdict (synchronises on the work tensor)."""

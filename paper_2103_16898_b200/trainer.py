@@ -229,10 +229,9 @@ class EncryptedTrainer:
 
     def step_resident(self, ct_dev: torch.Tensor, nonce: bytes, aad_dev: torch.Tensor, nrec: int):
         """Ciphertext already in HBM: GCM open + decode + train.  Returns the device loss."""
-        self.ctx.open_device(nonce, aad_dev, ct_dev, self.loader.pt, self.loader.work)
-        s = self.spec
-        decode_records(self.loader.pt, nrec, s["c"], s["h"], s["w"], s["mean"], s["std"], out=self.loader.x,
-                       labels=self.loader.labels)
+        # fused decrypt-and-normalise: ciphertext -> bf16 tile + labels, tag checked on the device
+        self.ctx.open_records_device(nonce, aad_dev, ct_dev, self.loader.x, self.loader.labels, self.loader.work,
+                                     self.spec)
         self._run_train()
         return self.net.loss
 

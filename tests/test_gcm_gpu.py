@@ -126,3 +126,37 @@ def test_volume_round_trip_and_reference_interop(tmp_path):
     assert rvol.verify() == []
     rvol.put(rkey, "ref.bin", b"written by the reference")
     assert Volume.open(tmp_path / "v").get(key, "ref.bin") == b"written by the reference"
+
+
+@pytest.mark.parametrize("c,h,w,nrec", [(3, 32, 32, 37), (1, 224, 224, 3), (3, 32, 32, 1)])
+def test_fused_decrypt_normalise_matches_two_kernel_path(c, h, w, nrec):
+    """K1b: cvb_gcm_open_records_dev (one kernel) == GCM open + records_to_nhwc, bit for bit,
+    and a tampered shard leaves an all-zero tile and labels."""
+    import numpy as np
+    import torch
+
+    from paper_2103_16898_b200.loader import decode_records, record_bytes
+
+    spec = dict(c=c, h=h, w=w, mean=(0.5,) * c, std=(0.25,) * c)
+    rb = record_bytes(c, h, w)
+    rng = np.random.default_rng(nrec + c)
+    pt = rng.integers(0, 256, size=nrec * rb, dtype=np.uint8).tobytes()
+    key, iv, aad = bytes(range(32)), bytes(range(12)), b"training-data\x00shard-x.bin"
+    blob = ref.gcm_seal(key, iv, aad, pt)
+    ctx = crypto.GcmContext(key)
+    dev = torch.frombuffer(bytearray(blob), dtype=torch.uint8).cuda()
+    aad_dev = torch.frombuffer(bytearray(aad), dtype=torch.uint8).cuda()
+    out = torch.empty(len(pt), dtype=torch.uint8, device="cuda")
+    work = ctx.new_workspace()
+    ctx.open_device(iv, aad_dev, dev, out, work)
+    x_ref, lab_ref = decode_records(out, nrec, c, h, w, spec["mean"], spec["std"])
+    tile = torch.zeros(nrec, h, w, 8, dtype=torch.bfloat16, device="cuda")
+    labels = torch.empty(nrec, dtype=torch.int32, device="cuda")
+    work2 = ctx.new_workspace()
+    ctx.open_records_device(iv, aad_dev, dev, tile, labels, work2, spec)
+    assert crypto.GcmContext.status_ok(work2)
+    assert torch.equal(tile, x_ref) and torch.equal(labels, lab_ref)
+    dev[len(pt) // 2] ^= 0x40
+    ctx.open_records_device(iv, aad_dev, dev, tile, labels, work2, spec)
+    assert not crypto.GcmContext.status_ok(work2)
+    assert int(tile.count_nonzero()) == 0 and int(labels.count_nonzero()) == 0
