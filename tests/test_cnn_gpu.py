@@ -27,3 +27,14 @@ def test_loss_decreases():
     x, lab = P.gpu_inputs(rec, P.loader.CIFAR)
     losses = [float(net.step(x, lab).item()) for _ in range(30)]
     assert losses[-1] < 0.5 * losses[0], losses
+
+
+def test_configs1_full_batch_loss_curve():
+    """BASELINE configs[1] at its own size: small CNN, batch 512, fp32 accumulate -- the GPU
+    loss curve over 4 steps tracks the CPU restatement (bf16-emulating oracle: tolerances of
+    tests/cnn_parity.py; plain fp32 oracle: 2e-2 relative per step)."""
+    report, wrel = P.run_parity("small_cnn", batch=512, steps=4)
+    P.check(report, wrel, "small_cnn")
+    report32, _ = P.run_parity("small_cnn", batch=512, steps=4, emulate=False)
+    for r in report32:
+        assert abs(r["loss_gpu"] - r["loss_ref"]) <= P.FP32_LOSS_TOL * max(1.0, abs(r["loss_ref"])), r
