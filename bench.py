@@ -373,6 +373,8 @@ def main():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if os.environ.get("CVB_ONE_GPU"):   # test aid: run every rank on cuda:0 (use with CVB_DIST_BACKEND=gloo)
+        local_rank = 0
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -389,7 +391,11 @@ def main():
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("CVB_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     run_ours(args, rank, world, local_rank)
     if world > 1 or force:
         import torch.distributed as dist

@@ -87,3 +87,52 @@ def test_double_buffered_host_steps_match_plain_host_steps():
         runs.append((losses, tr.net.ps.p32.clone()))
     assert runs[0][0] == runs[1][0]
     assert torch.equal(runs[0][1], runs[1][1])
+
+
+def _dp_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from bench import make_shards
+    from paper_2103_16898_b200.loader import CIFAR
+    from paper_2103_16898_b200.trainer import EncryptedTrainer
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)   # both ranks share cuda:0
+    key, B = bytes(range(32)), 32
+    shards = make_shards(3, B, 40 + rank, key, CIFAR)                 # different data per rank
+    cts = [torch.frombuffer(bytearray(s[3]), dtype=torch.uint8).cuda() for s in shards]
+    aads = [torch.frombuffer(bytearray(s[2]), dtype=torch.uint8).cuda() for s in shards]
+    tr = EncryptedTrainer("resnet18", key, batch=B, spec=CIFAR, seed=3, world=world, rank=rank)
+    tr.allreduce.__init__(tr.net.ps, bucket_mb=4.0)
+    tr.step_resident(cts[0], shards[0][1], aads[0], B)           # eager, overlapped buckets
+    tr.capture()                                                  # graph segments between buckets
+    for i in (1, 2):
+        tr.step_resident(cts[i], shards[i][1], aads[i], B)
+    torch.cuda.synchronize()
+    p = tr.net.ps.p32.detach().cpu()
+    ref = p.clone()
+    dist.broadcast(ref, src=0)
+    q.put((rank, len(tr.segments), float((p - ref).abs().max()), float(p.abs().sum())))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_two_rank_data_parallel_weights_stay_identical():
+    """Two ranks (gloo, sharing the one GPU), different shards, overlapped bucket all-reduce
+    with the backward split into CUDA-graph segments: after 3 steps every rank holds the
+    same weights bit for bit."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=500) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, nseg, diff, norm in out:
+        assert nseg >= 2 and diff == 0.0 and norm > 0
