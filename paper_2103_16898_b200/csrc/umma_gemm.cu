@@ -81,6 +81,8 @@ struct GemmParams {
   uint32_t tx_bytes;
   uint32_t a_box_bytes;     // bytes TMA writes per A box (WGRAD: per-tile A box count varies)
   uint32_t a_stage_bytes;   // smem bytes of the A part of one pipeline stage
+  uint32_t b_stage_bytes;   // smem bytes of the B part of one stage (0: BN * kr * 2)
+  int w_halo;               // WGRAD halo: one (bw+KW-1)-wide box per K-block carries every kw tap
   int b_res;                // 1: the whole B operand (one N tile, all K) is loaded once per CTA
   uint32_t b_res_bytes;     // size of the resident B region
   int b_slabs;              // 64-wide K slabs of the resident B
@@ -370,7 +372,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t a_stage = p.a_stage_bytes;         // 16 KB (halo mode: planes * plane stride)
-  const uint32_t b_stage = p.b_res ? 0u : p.BN * p.kr * 2;
+  const uint32_t b_stage = p.b_res ? 0u : (p.b_stage_bytes ? p.b_stage_bytes : p.BN * p.kr * 2);
   const uint32_t stage_bytes = a_stage + b_stage;
   const uint32_t b_kb_bytes = p.BN * BK * 2;        // resident B: one K-block slab
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes + p.b_res_bytes +
@@ -901,7 +903,8 @@ int launch(GemmParams& p, cudaStream_t stream) {
   if (!p.kr) p.kr = BK;
   p.ksteps = p.kr / 16;
   if (!p.a_stage_bytes) p.a_stage_bytes = BM * p.kr * 2;
-  const uint32_t stage_bytes = p.a_stage_bytes + (p.b_res ? 0u : (uint32_t)p.BN * p.kr * 2);
+  const uint32_t stage_bytes = p.a_stage_bytes + (p.b_res ? 0u : (p.b_stage_bytes ? p.b_stage_bytes
+                                                                                   : (uint32_t)p.BN * p.kr * 2));
   static int env_epi4 = -1;
   if (env_epi4 < 0) env_epi4 = getenv("CVB_EPI4") ? 1 : 0;
   // narrow tiles: two epilogue warps per TMEM lane quarter (each stores half the columns) so
@@ -951,6 +954,16 @@ int launch(GemmParams& p, cudaStream_t stream) {
   }
   if (p.mode == MODE_HALO)   // no-swizzle K-major: LBO = next 8-channel plane, SBO = one halo row
     p.adesc[0] = desc_tmpl(0, p.h_plane_stride, (uint32_t)p.h_pitch * 16, 0);
+  if (p.mode == MODE_WGRAD && p.w_halo) {
+    // B = the (tw+KW-1)-wide halo box, MN-major, rows of R = cin*2 bytes (one pixel each).
+    // k-step s = pixels [16s, 16s+16) of the tw x th box -> halo row (16s/tw)*(tw+KW-1) + 16s%tw;
+    // the kw taps are the MN atoms of one MMA: LBO = one row (the next kw shift), SBO = 8 rows.
+    const uint32_t R = (uint32_t)p.b_cel * 2, pitch = (uint32_t)(p.tw + p.h_kw - 1);
+    for (int k = 0; k < p.ksteps; k++) {
+      const uint32_t row = (uint32_t)(16 * k / p.tw) * pitch + (uint32_t)(16 * k % p.tw);
+      p.bdesc[k] = desc_tmpl(row * R, R, 8 * R, layout_of((int)R));
+    }
+  }
   if (p.mode == MODE_HALO && p.h_cg == 8) {   // tap pairs: second K half = next pixel / next row
     p.adesc[0] = desc_tmpl(0, 16, (uint32_t)p.h_pitch * 16, 0);
     p.adesc[1] = desc_tmpl(0, (uint32_t)(p.h_pitch - p.h_kw + 1) * 16, (uint32_t)p.h_pitch * 16, 0);
@@ -1302,6 +1315,36 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
   p.a_box_bytes = p.kr * acel * 2;
   int rc;
   if ((rc = encode_nhwc(&p.mapA[0], dy, n, oh, ow, cout, dycs, acel, bw, bh, bnn))) return rc;
+  static int no_whalo = -1;
+  if (no_whalo < 0) no_whalo = getenv("CVB_NO_WGRAD_HALO") ? 1 : 0;
+  // WGRAD halo: stride 1, one 64-channel group (one 128-byte SW128 row per pixel; the 32-channel
+  // SW64 variant computes correctly but measured 2x slower), one image
+  // row box whose width is a multiple of 16 pixels, whole kw rows per N tile (N = KW*cin <= 256).
+  if (!no_whalo && stride == 1 && cin == 64 && bcel == cin && bnn == 1 && bw % 16 == 0 &&
+      kw * cin <= 256 && oh == h && ow == w) {
+    p.w_halo = 1;
+    p.h_kw = kw;
+    p.BN = kw * cin;
+    p.gb = 1;
+    p.n_tiles = kh;
+    const int hw_ = bw + kw - 1;
+    p.b_stage_bytes = ((uint32_t)hw_ * bh * bcel * 2 + 1023) / 1024 * 1024;
+    p.tx_bytes = p.ga * p.kr * acel * 2 + (uint32_t)hw_ * bh * bcel * 2;
+    tiles = p.m_tiles * p.n_tiles;
+    splits = (g_num_sms + tiles - 1) / tiles;
+    if (splits > max_splits) splits = max_splits;
+    if (splits > p.num_kb) splits = p.num_kb;
+    if (splits < 1) splits = 1;
+    p.kb_per_split = (p.num_kb + splits - 1) / splits;
+    splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
+    p.splits = splits;
+    p.nbox = p.n_tiles;
+    for (int t = 0; t < kh; t++) p.boxtab[t] = pack_box(0, 0, -pad, t - pad);   // row kh = t, all kw
+    if ((rc = encode_nhwc(&p.mapB[0], x, n, h, w, cin, xcs, bcel, hw_, bh, bnn))) return rc;
+    p.out_mode = OUT_PARTIAL; p.out_f32 = 1; p.out = part; p.ldc = Ncols; p.col_off = 0; p.part_rows = cout;
+    *splits_out = splits;
+    return launch(p, (cudaStream_t)stream);
+  }
   if (stride == 1) {
     if ((rc = encode_nhwc(&p.mapB[0], x, n, h, w, cin, xcs, bcel, bw, bh, bnn))) return rc;
   } else {

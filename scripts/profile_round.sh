@@ -21,6 +21,6 @@ timeout 900 ncu --profile-from-start off -k regex:bn_bwd_fused -s 2 -c 1 --set f
 timeout 900 ncu --profile-from-start off -k regex:umma_gemm -s 8 -c 1 --set full --import-source on \
   --clock-control none -o gpurun_out/prof/umma_r18_stage3 python scripts/profile_step.py resnet18 512 \
   > gpurun_out/prof/umma_r18.log 2>&1
-timeout 900 ncu -k regex:gcm_kernel -s 3 -c 1 --set full --import-source on --clock-control none \
-  -o gpurun_out/prof/gcm_open_256m python scripts/gcm_bench.py > gpurun_out/prof/gcm.log 2>&1
+timeout 900 ncu -k regex:gcm_kernel -s 1 -c 1 --set full --import-source on --clock-control none \
+  -o gpurun_out/prof/gcm_open_256m python scripts/gcm_one.py 256 > gpurun_out/prof/gcm.log 2>&1
 ls -la gpurun_out/prof
