@@ -42,7 +42,7 @@ UNIT = "images/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--model", default="small_cnn")
@@ -100,52 +100,63 @@ def make_shards(n_shards, batch, seed, key, spec):
 
 
 class ClockSampler:
-    """NVML clock + throttle-reason sampling in a background thread (every ~5 ms) while the
-    timed region runs (nvidia-smi's 200 ms floor is longer than a small-CNN timed region)."""
+    """NVML clock + throttle-reason sampling every ~5 ms while the timed region runs, in a
+    separate process (a thread would compete for the GIL with the launch loop and starve)."""
 
+    CODE = r"""
+import sys, time, pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+print("max", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=True)
+while True:
+    try:
+        print(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+              pynvml.nvmlDeviceGetCurrentClocksEventReasons(h), flush=True)
+    except Exception:
+        pass
+    time.sleep(0.005)
+"""
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
                "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
-    def __init__(self, dev_index, period=0.005):
-        import threading
+    def __init__(self, dev_index):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen([sys.executable, "-c", self.CODE, str(dev_index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.proc.stdout.readline()   # started (max clock line)
+        except Exception:
+            self.proc = None
 
-        self.sm, self.reasons, self.mx, self.ok = [], set(), 0.0, False
+    def summary(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            return None
+        sm, reasons, mx = [], set(), 0.0
+        for line in out.strip().splitlines():
+            f = line.split()
+            if len(f) != 2 or f[0] == "max":
+                continue
+            sm.append(float(f[0]))
+            for nm, bit in self.REASONS.items():
+                if int(f[1]) & bit:
+                    reasons.add(nm)
         try:
             import pynvml
 
             pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
-            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
-            self.ok = True
+            mx = float(pynvml.nvmlDeviceGetMaxClockInfo(pynvml.nvmlDeviceGetHandleByIndex(0), pynvml.NVML_CLOCK_SM))
         except Exception:
-            return
-        self.period, self.stop_ev = period, threading.Event()
-        self.th = threading.Thread(target=self._run, daemon=True)
-        self.th.start()
-
-    def _run(self):
-        nv = self.nv
-        while not self.stop_ev.is_set():
-            try:
-                self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for nm, bit in self.REASONS.items():
-                    if r & bit:
-                        self.reasons.add(nm)
-            except Exception:
-                pass
-            self.stop_ev.wait(self.period)
-
-    def summary(self):
-        if not self.ok:
+            pass
+        if not sm:
             return None
-        self.stop_ev.set()
-        self.th.join(timeout=2)
-        if not self.sm:
-            return None
-        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": self.mx, "reasons": sorted(self.reasons),
-                "samples": len(self.sm), "source": "nvml, sampled during the timed region"}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml (separate process, 5 ms period) during the timed region"}
 
 
 def peaks():
