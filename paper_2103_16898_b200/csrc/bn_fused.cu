@@ -351,6 +351,16 @@ int fused_setup(int C, unsigned** bar, int* grid, int* grid_f = nullptr) {
   return CVB_OK;
 }
 
+// Experiment knob (CVB_BN_MIN_ELEMS): fewer CTAs for small tensors.  Measured on B200: no gain
+// (the fixed cost is per phase, not per CTA) -- off by default.
+int size_grid(int grid, int64_t rows, int C) {
+  static int env = -1;
+  if (env < 0) { const char* e = getenv("CVB_BN_MIN_ELEMS"); env = e ? atoi(e) : 0; }   // measured: no gain, off
+  if (env <= 0) return grid;
+  const int64_t want = (rows * C + env - 1) / env;
+  return (int)(want < grid ? (want < 8 ? 8 : want) : grid);
+}
+
 template <class Args>
 int launch_coop(void (*kern)(Args), const Args& a, int grid, cudaStream_t stream) {
   cudaLaunchConfig_t cfg = {};
@@ -390,7 +400,7 @@ CVB_API int cvb_bn_forward(const void* x, int64_t rows, int C, int xcs, float* w
   if (rc) return rc;
   FwdArgs a{(const bf16*)x, rows, C, xcs, ws, bar, mean, rstd, eps, run_mean, run_var, momentum, gamma, beta,
             (const bf16*)res, rcs, relu, (bf16*)y, ycs, ycoff};
-  return launch_coop(bn_fwd_fused, a, grid, (cudaStream_t)stream);
+  return launch_coop(bn_fwd_fused, a, size_grid(grid, rows, C), (cudaStream_t)stream);
 }
 
 // Batch-norm (+ReLU) backward in one launch (same contract as cvb_bn_backward).
@@ -405,5 +415,5 @@ CVB_API int cvb_bn_backward_fused(const void* dy, int dycs, const void* x, int x
   if (rc) return rc;
   BwdArgs a{(const bf16*)dy, dycs, (const bf16*)x, xcs, (const bf16*)y, ycs, rows, C, mean, rstd, gamma, beta, relu,
             ws, bar, dgamma, dbeta, (bf16*)dx, dxcs, dx32, accum32, (bf16*)dz_out};
-  return launch_coop(bn_bwd_fused, a, grid, (cudaStream_t)stream);
+  return launch_coop(bn_bwd_fused, a, size_grid(grid, rows, C), (cudaStream_t)stream);
 }
