@@ -37,6 +37,9 @@ int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, int dycs, 
 /* C[M][N] (+bias) = sum_k A(m,k) B(n,k); A [M][K] (a_major 0) or [K][M] (1); B [N][K] or [K][N] */
 int cvb_gemm(const void* a, int a_major, int64_t lda, const void* b, int b_major, int64_t ldb, int M, int N, int K,
              void* c, int64_t ldc, int c_f32, const float* bias, int splits, int accumulate, void* stream);
+int cvb_gemm_ex(const void* a, int a_major, int64_t lda, const void* b, int b_major, int64_t ldb, int M, int N, int K,
+                void* c, int64_t ldc, int c_f32, const float* bias, int splits, int accumulate, int max_bn,
+                void* stream);   /* cvb_gemm with N tiles of at most max_bn columns */
 int cvb_gemm_splits_used(int K, int splits);
 /* profiling aids (not on the hot path): raw tcgen05.mma issue rate; CTA-0 pipeline timeline
  * of the last GEMM launched with CVB_GEMM_DBG=4 (5 x 4096 clock64 stamps) */

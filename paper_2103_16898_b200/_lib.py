@@ -53,6 +53,7 @@ SIGNATURES = {
     "cvb_conv2d_wgrad": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT, _INT, _INT, _INT, _INT, _INT,
                                 _INT, _P, _INT, _c.POINTER(_INT), _P]),
     "cvb_gemm": (_INT, [_P, _INT, _I64, _P, _INT, _I64, _INT, _INT, _INT, _P, _I64, _INT, _P, _INT, _INT, _P]),
+    "cvb_gemm_ex": (_INT, [_P, _INT, _I64, _P, _INT, _I64, _INT, _INT, _INT, _P, _I64, _INT, _P, _INT, _INT, _INT, _P]),
     "cvb_gemm_splits_used": (_INT, [_INT, _INT]),
     "cvb_bn_workspace_floats": (_I64, [_I64, _INT]),
     "cvb_bn_stats": (_INT, [_P, _I64, _INT, _INT, _P, _P, _P, _c.c_float, _P, _P, _c.c_float, _P]),

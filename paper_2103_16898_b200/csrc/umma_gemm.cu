@@ -1399,9 +1399,20 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
 //   A: a_major 0 -> row-major [M][K] (lda), 1 -> row-major [K][M] (lda)
 //   B: b_major 0 -> row-major [N][K] (ldb), 1 -> row-major [K][N] (ldb)
 // C row-major [M][ldc] bf16 or fp32; split-K > 1 writes fp32 partials [split][M][ldc].
+CVB_API int cvb_gemm_ex(const void* a, int a_major, int64_t lda, const void* b, int b_major, int64_t ldb, int M, int N,
+                        int K, void* c, int64_t ldc, int c_f32, const float* bias, int splits, int accumulate,
+                        int max_bn, void* stream);
 CVB_API int cvb_gemm(const void* a, int a_major, int64_t lda, const void* b, int b_major, int64_t ldb, int M, int N,
                      int K, void* c, int64_t ldc, int c_f32, const float* bias, int splits, int accumulate,
                      void* stream) {
+  return cvb_gemm_ex(a, a_major, lda, b, b_major, ldb, M, N, K, c, ldc, c_f32, bias, splits, accumulate, 256, stream);
+}
+
+// max_bn (16..256, multiple of 16): narrower N tiles -> more (m, n) tiles and fewer split-K
+// partial bytes for small-M FC layers.
+CVB_API int cvb_gemm_ex(const void* a, int a_major, int64_t lda, const void* b, int b_major, int64_t ldb, int M, int N,
+                        int K, void* c, int64_t ldc, int c_f32, const float* bias, int splits, int accumulate,
+                        int max_bn, void* stream) {
   if (get_encoder()) return CVB_ECUDA;
   static GemmParams p;
   memset(&p, 0, sizeof(p));
@@ -1412,6 +1423,7 @@ CVB_API int cvb_gemm(const void* a, int a_major, int64_t lda, const void* b, int
   if (a_major == 0) p.a_cel = pick_cel(K) ? (pick_cel(K) < 64 ? pick_cel(K) : 64) : 8;
   if (b_major == 0) p.b_cel = pick_cel(K) ? (pick_cel(K) < 64 ? pick_cel(K) : 64) : 8;
   p.BN = pick_bn(N);
+  if (max_bn >= 16 && max_bn < p.BN) p.BN = max_bn / 16 * 16;
   if (b_major == 1) { p.BN = (p.BN + 63) / 64 * 64; if (p.BN > 256) p.BN = 256; }
   p.ga = a_major == 0 ? BK / p.a_cel : BM / p.a_cel;
   p.gb = b_major == 0 ? BK / p.b_cel : p.BN / p.b_cel;

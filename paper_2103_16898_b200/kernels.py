@@ -153,7 +153,7 @@ def splits_used(K, splits):
 
 
 def gemm(a, b, M, N, K, a_major=0, b_major=0, out=None, out_f32=False, bias=None, splits=1, accumulate=False,
-         acct_flops=None):
+         acct_flops=None, max_bn=256):
     """C[M,N] = sum_k A(m,k) B(n,k) with A [M,K] (a_major 0) or [K,M] (1), B [N,K] (0) or [K,N] (1)."""
     lib = _lib_bound()
     used = lib.cvb_gemm_splits_used(K, splits)
@@ -163,9 +163,9 @@ def gemm(a, b, M, N, K, a_major=0, b_major=0, out=None, out_f32=False, bias=None
         else:
             out = torch.empty((M, N), dtype=F32 if out_f32 else BF16, device=a.device)
     tok = REC.begin(1, "umma_gemm", acct_flops if acct_flops is not None else 2 * M * N * K)
-    rc = lib.cvb_gemm(a.data_ptr(), a_major, a.stride(0), b.data_ptr(), b_major, b.stride(0), M, N, K,
-                      out.data_ptr(), out.stride(-2), int(out_f32 or used > 1), _ptr(bias), splits, int(accumulate),
-                      _stream())
+    rc = lib.cvb_gemm_ex(a.data_ptr(), a_major, a.stride(0), b.data_ptr(), b_major, b.stride(0), M, N, K,
+                         out.data_ptr(), out.stride(-2), int(out_f32 or used > 1), _ptr(bias), splits, int(accumulate),
+                         max_bn, _stream())
     REC.end(tok)
     _lib.check(rc, "gemm")
     return out

@@ -239,7 +239,9 @@ class Linear:
 
     def build(self, batch, scratch):
         B = batch
-        self.s_fwd = self._splits(B, self.fpad, self.fin)
+        # forward: narrow (64-column) N tiles -> 4x more output tiles, 4x fewer split-K partials
+        self.bn_fwd = 64 if self.fpad > 64 else 256
+        self.s_fwd = self._splits(B, self.fpad, self.fin, bn_cap=self.bn_fwd)
         self.s_wg = self._splits(self.fpad, self.fin, B)
         need = max(self.s_fwd * B * self.fpad, self.s_wg * self.fpad * self.fin if self.s_wg > 1 else 0)
         scratch.part_floats = max(scratch.part_floats, need)
@@ -250,7 +252,8 @@ class Linear:
         fl = 2 * B * self.fout * self.fin
         if self.s_fwd > 1:
             part = self.scratch.part[:self.s_fwd * B * self.fpad].view(self.s_fwd, B, self.fpad)
-            K.gemm(x, ps.b[self.W], B, self.fpad, self.fin, 0, 0, out=part, splits=self.s_fwd, acct_flops=fl)
+            K.gemm(x, ps.b[self.W], B, self.fpad, self.fin, 0, 0, out=part, splits=self.s_fwd, acct_flops=fl,
+                   max_bn=self.bn_fwd)
             used = K.splits_used(self.fin, self.s_fwd)
             K.reduce_splits_act(part, used, B, self.fpad, out, bias=ps.p[self.Bn], relu=relu)
         else:

@@ -169,3 +169,12 @@ def test_conv_dgrad_stride2_rejects_without_launch():
     dx = torch.full((2, 8, 8, 32), 3.0, device="cuda", dtype=torch.bfloat16)
     assert not K.conv2d_dgrad_s2(dy, wt, 0, dx, accumulate=False)
     assert (dx == 3.0).all()
+
+
+def test_dense_narrow_n_tiles_split_k():
+    """cvb_gemm_ex with 64-column N tiles + split-K (the FC forward configuration)."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = torch.randn(512, 4096, device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randn(256, 4096, device="cuda", generator=g).to(torch.bfloat16)
+    out = K.gemm(A, B, 512, 256, 4096, 0, 0, splits=9, max_bn=64)
+    _close(out.sum(0), A.float() @ B.float().t())
