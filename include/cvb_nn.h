@@ -95,6 +95,12 @@ int cvb_reduce_splits_act(const float* part, int splits, int rows, int cols, con
    (int64 element offsets into pb / fb) */
 int cvb_weight_flip_batched(const void* pb, void* fb, const int64_t* desc_dev, int nlayers, int64_t max_elems,
                             void* stream);
+/* space-to-depth stem: the 7x7 stride-2 pad-3 conv on x [n][h][w][C] equals a 4x4 stride-1 pad-2
+   conv on xs = s2d(x) [n][h/2][w/2][4C] with weights s2d_weights(w) [cout][4][4][4C]; the weight
+   gradient maps back with s2d_weights_grad (fp32) */
+int cvb_space_to_depth2(const void* x, int n, int h, int w, int C, void* xs, void* stream);
+int cvb_s2d_weights(const void* w7, int cout, int C, void* ws, void* stream);
+int cvb_s2d_weights_grad(const float* dws, int cout, int C, float* dw7, void* stream);
 int cvb_weight_flip(const void* w, int cout, int kh, int kw, int cin, void* wt, void* stream);
 int cvb_zero_upsample(const void* dy, int n, int oh, int ow, int C, int dycs, void* out, void* stream);
 int cvb_col_sum(const void* x, int is_f32, int64_t rows, int cols, int64_t ld, float* out, int accumulate, void* stream);

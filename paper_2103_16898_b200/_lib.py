@@ -68,6 +68,9 @@ SIGNATURES = {
     "cvb_bn_backward_fused": (_INT, [_P, _INT, _P, _INT, _P, _INT, _I64, _INT, _P, _P, _P, _P, _INT, _P, _P, _P, _P,
                                      _INT, _P, _INT, _P, _P]),
     "cvb_weight_flip_batched": (_INT, [_P, _P, _P, _INT, _I64, _P]),
+    "cvb_space_to_depth2": (_INT, [_P, _INT, _INT, _INT, _INT, _P, _P]),
+    "cvb_s2d_weights": (_INT, [_P, _INT, _INT, _P, _P]),
+    "cvb_s2d_weights_grad": (_INT, [_P, _INT, _INT, _P, _P]),
     "cvb_maxpool_fwd_idx": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT, _INT, _P, _P]),
     "cvb_maxpool_bwd_idx": (_INT, [_P, _P, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _P, _P]),
     "cvb_maxpool_fwd": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT, _INT, _P]),

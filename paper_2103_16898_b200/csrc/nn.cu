@@ -639,6 +639,50 @@ __global__ void weight_flip_batched(const bf16* __restrict__ pb, bf16* __restric
   }
 }
 
+// ---- space-to-depth stem (7x7 stride-2 pad-3 conv == 4x4 stride-1 conv on 2x2 s2d input) ----
+// xs[n][i][j][(2a+b)*C + c] = x[n][2i+a][2j+b][c]
+__global__ void space_to_depth2(const bf16* __restrict__ x, int n, int h, int w, int C, bf16* __restrict__ xs) {
+  CVB_PDL_PROLOGUE();
+  const int G = C / 8, oh = h / 2, ow = w / 2;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // one 16-byte group of the output
+  if (i >= (int64_t)n * oh * ow * 4 * G) return;
+  const int g = (int)(i % (4 * G));
+  const int64_t pix = i / (4 * G);
+  const int ph = g / G, cg = g % G, a = ph >> 1, b = ph & 1;
+  const int j = (int)(pix % ow), ii = (int)((pix / ow) % oh), nn = (int)(pix / ((int64_t)ow * oh));
+  *reinterpret_cast<uint4*>(xs + pix * 4 * C + g * 8) =
+      *reinterpret_cast<const uint4*>(x + (((int64_t)nn * h + 2 * ii + a) * w + 2 * j + b) * C + cg * 8);
+}
+
+// ws[co][u][v][(2a+b)*C + c] = w[co][2u+a-1][2v+b-1][c] (zero where the 7x7 tap does not exist)
+__global__ void s2d_weights(const bf16* __restrict__ w, int cout, int C, bf16* __restrict__ ws) {
+  CVB_PDL_PROLOGUE();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)cout * 16 * 4 * C) return;
+  const int c = (int)(i % C);
+  int64_t r = i / C;
+  const int ph = (int)(r % 4); r /= 4;
+  const int v = (int)(r % 4); r /= 4;
+  const int u = (int)(r % 4);
+  const int co = (int)(r / 4);
+  const int kh = 2 * u + (ph >> 1) - 1, kw = 2 * v + (ph & 1) - 1;
+  ws[i] = (kh >= 0 && kw >= 0) ? w[(((int64_t)co * 7 + kh) * 7 + kw) * C + c] : __float2bfloat16_rn(0.f);
+}
+
+// dw[co][kh][kw][c] (+)= dws[co][u][v][(2a+b)*C + c] with kh = 2u+a-1, kw = 2v+b-1 (fp32)
+__global__ void s2d_weights_grad(const float* __restrict__ dws, int cout, int C, float* __restrict__ dw) {
+  CVB_PDL_PROLOGUE();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)cout * 49 * C) return;
+  const int c = (int)(i % C);
+  int64_t r = i / C;
+  const int kw = (int)(r % 7); r /= 7;
+  const int kh = (int)(r % 7);
+  const int co = (int)(r / 7);
+  const int u = (kh + 1) >> 1, a = (kh + 1) & 1, v = (kw + 1) >> 1, b = (kw + 1) & 1;
+  dw[i] = dws[((((int64_t)co * 4 + u) * 4 + v) * 4 + (2 * a + b)) * C + c];
+}
+
 __global__ void zero_upsample(const bf16* __restrict__ dy, int n, int oh, int ow, int C, int dycs, bf16* __restrict__ out,
                               int uh, int uw) {
   CVB_PDL_PROLOGUE();
@@ -948,6 +992,27 @@ CVB_API int cvb_weight_flip_batched(const void* pb, void* fb, const int64_t* des
   unsigned gx = (unsigned)((max_elems + 255) / 256);
   if (gx > 512) gx = 512;
   cvb_launch(weight_flip_batched, dim3(gx, nlayers), 256, 0, STREAM, (const bf16*)pb, (bf16*)fb, desc_dev);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+// Space-to-depth stem helpers (DenseNet's 7x7 stride-2 stem as a 4x4 stride-1 halo conv).
+CVB_API int cvb_space_to_depth2(const void* x, int n, int h, int w, int C, void* xs, void* stream) {
+  if (C % 8 || h % 2 || w % 2) { cvb_set_error("space_to_depth2: bad shape"); return CVB_EINVAL; }
+  cvb_launch(space_to_depth2, nblocks((int64_t)n * (h / 2) * (w / 2) * (C / 2)), 256, 0, STREAM, (const bf16*)x, n, h,
+             w, C, (bf16*)xs);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_s2d_weights(const void* w7, int cout, int C, void* ws, void* stream) {
+  cvb_launch(s2d_weights, nblocks((int64_t)cout * 64 * C), 256, 0, STREAM, (const bf16*)w7, cout, C, (bf16*)ws);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_s2d_weights_grad(const float* dws, int cout, int C, float* dw7, void* stream) {
+  cvb_launch(s2d_weights_grad, nblocks((int64_t)cout * 49 * C), 256, 0, STREAM, dws, cout, C, dw7);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }

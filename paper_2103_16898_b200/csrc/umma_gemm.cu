@@ -572,6 +572,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
             else if (p.h_rows && geo == 114) halo_rows_issue<1, 1, 4>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
             else if (p.h_rows && geo == 332) halo_rows_issue<3, 3, 2>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
             else if (p.h_rows && geo == 112) halo_rows_issue<1, 1, 2>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (p.h_rows && geo == 442) halo_rows_issue<4, 4, 2>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
             else if (geo == 334) halo_issue<3, 3, 4>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
             else if (geo == 332) halo_issue<3, 3, 2>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
             else if (geo == 331) halo_issue<3, 3, 1>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
@@ -1102,7 +1103,8 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
       if (no_rows < 0) no_rows = getenv("CVB_NO_HALO_ROWS") ? 1 : 0;
       static int rows32 = -1;
       if (rows32 < 0) rows32 = getenv("CVB_NO_HALO_ROWS32") ? 0 : 1;   // SW64 rows for 32-channel groups
-      p.h_rows = (!no_rows && (cg == 64 || (cg == 32 && rows32)) && ((kh == 3 && kw == 3) || (kh == 1 && kw == 1))) ? 1 : 0;
+      p.h_rows = (!no_rows && (cg == 64 || (cg == 32 && rows32)) &&
+                  ((kh == 3 && kw == 3) || (kh == 1 && kw == 1) || (kh == 4 && kw == 4))) ? 1 : 0;
       if (p.h_rows) p.h_planes = 1;
       p.h_box_bytes = (uint32_t)p.h_pitch * hrows * (p.h_rows ? cg * 2 : 16);
       p.h_plane_stride = (p.h_box_bytes + 127) / 128 * 128;

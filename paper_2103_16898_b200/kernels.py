@@ -329,6 +329,30 @@ def weight_flip_batched(pb, fb, desc_dev, nlayers, max_elems, nbytes):
     _lib.check(rc, "weight_flip_batched")
 
 
+def space_to_depth2(x, xs):
+    n, h, w, c = x.shape
+    tok = REC.begin(1, "layout", 0, x.numel() * 4)
+    rc = _lib_bound().cvb_space_to_depth2(x.data_ptr(), n, h, w, c, xs.data_ptr(), _stream())
+    REC.end(tok)
+    _lib.check(rc, "space_to_depth2")
+
+
+def s2d_weights(w7, ws):
+    cout, _, _, c = w7.shape
+    tok = REC.begin(1, "layout", 0, ws.numel() * 4)
+    rc = _lib_bound().cvb_s2d_weights(w7.data_ptr(), cout, c, ws.data_ptr(), _stream())
+    REC.end(tok)
+    _lib.check(rc, "s2d_weights")
+
+
+def s2d_weights_grad(dws, dw7):
+    cout, _, _, c = dw7.shape
+    tok = REC.begin(1, "layout", 0, dw7.numel() * 8)
+    rc = _lib_bound().cvb_s2d_weights_grad(dws.data_ptr(), cout, c, dw7.data_ptr(), _stream())
+    REC.end(tok)
+    _lib.check(rc, "s2d_weights_grad")
+
+
 def zero_upsample(dy, out):
     n, oh, ow, c = dy.shape
     tok = REC.begin(1, "layout", 0, (dy.numel() + out.numel()) * 2)

@@ -19,6 +19,7 @@ of parameters fp32, activation gradients stored bf16, master weights fp32.
 from __future__ import annotations
 
 import math
+import os
 
 import torch
 
@@ -138,6 +139,11 @@ class ConvBN:
         self.relu, self.need_dgrad = relu, need_dgrad
         cin_real = cin if cin_real is None else cin_real
         self.cin_real = cin_real
+        # DenseNet's 7x7 stride-2 stem on 8-channel (1 real) input: computed as a 4x4 stride-1
+        # conv on the 2x2 space-to-depth input (32 channels) -> the halo conv path instead of
+        # 49 gathered 16-byte-row boxes per K-block (same result, exact same products)
+        self.s2d = (k == 7 and stride == 2 and pad == 3 and cin == 8 and not need_dgrad
+                    and not os.environ.get("CVB_NO_S2D"))
         bound = 1.0 / math.sqrt(cin_real * k * k)  # torch default (kaiming_uniform a=sqrt(5))
         w = _uniform(gen, (cout, k, k, cin_real), bound)
         if cin_real != cin:
@@ -152,6 +158,10 @@ class ConvBN:
         self.n, self.h, self.w = n, h, w
         self.oh, self.ow = K.conv_out_hw(h, w, self.k, self.s, self.pad)
         self.rows = n * self.oh * self.ow
+        if self.s2d:
+            self.xs = torch.empty(n, h // 2, w // 2, 4 * self.cin, dtype=BF16, device=device)
+            self.ws = torch.empty(self.cout, 4, 4, 4 * self.cin, dtype=BF16, device=device)
+            self.dws = torch.empty(self.cout, 16 * 4 * self.cin, dtype=F32, device=device)
         self.flops = 2 * self.rows * self.cout * self.k * self.k * self.cin_real   # algorithmic, per pass
         self.z = torch.empty(n, self.oh, self.ow, self.cout, dtype=BF16, device=device)
         self.dz = torch.empty_like(self.z)
@@ -171,8 +181,13 @@ class ConvBN:
 
     def forward(self, ps: ParamStore, x, out, res=None, out_coff=0, cin=None):
         """x: [n,h,w,cs] (channels [0,cin)); out: [n,oh,ow,ocs] written at channel out_coff."""
-        K.conv2d_fwd(x, ps.b[self.W], self.s, self.pad, out=self.z, cin=cin if cin is not None else self.cin,
-                     acct_flops=self.flops)
+        if self.s2d:
+            K.space_to_depth2(x, self.xs)
+            K.s2d_weights(ps.b[self.W], self.ws)
+            K.conv2d_fwd(self.xs, self.ws, 1, 2, out=self.z, out_hw=(self.oh, self.ow), acct_flops=self.flops)
+        else:
+            K.conv2d_fwd(x, ps.b[self.W], self.s, self.pad, out=self.z, cin=cin if cin is not None else self.cin,
+                         acct_flops=self.flops)
         K.bn_forward(self.z, self.rows, self.cout, self.cout, self.scratch.bnws, self.mean, self.rstd, ps.p[self.G],
                      ps.p[self.B], out, out.shape[-1], out_coff, relu=self.relu, res=res,
                      rcs=res.shape[-1] if res is not None else 0, run_mean=self.run_mean, run_var=self.run_var)
@@ -187,6 +202,17 @@ class ConvBN:
         K.bn_backward(dsrc, dcs, self.z, self.cout, self.rows, self.cout, self.mean, self.rstd, ps.p[self.G],
                       ps.p[self.B], self.scratch.bnws, ps.g[self.G], ps.g[self.B], relu=self.relu,
                       y=y, ycs=y.shape[-1] if y is not None else 0, dx=self.dz, dxcs=self.cout, dz_out=dres)
+        if self.s2d:   # wgrad of the 4x4 s2d conv, mapped back onto the 7x7 weights
+            count = self.cout * 16 * 4 * self.cin
+            maxs = max(1, min(MAX_SPLITS, self.scratch.part.numel() // count))
+            part, used = K.conv2d_wgrad_partials(self.dz, self.xs, 4, 4, 1, 2,
+                                                 part=self.scratch.part[:maxs * count].view(maxs, self.cout,
+                                                                                            16 * 4 * self.cin),
+                                                 acct_flops=self.flops)
+            K.reduce_splits(part, used, count, self.dws)
+            K.s2d_weights_grad(self.dws, ps.g[self.W])
+            ps.grad_ready(self.W, self.G, self.B)
+            return
         count = self.cout * self.k * self.k * cin
         maxs = max(1, min(MAX_SPLITS, self.scratch.part.numel() // count))
         part, used = K.conv2d_wgrad_partials(self.dz, x, self.k, self.k, self.s, self.pad, cin=cin,
