@@ -31,12 +31,6 @@ int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs, const v
 int cvb_conv2d_dgrad_s2(const void* dy, int n, int oh, int ow, int cout, int dycs, const void* w, int cin, int kh,
                         int kw, int pad, void* dx, int h, int wd, int dxcs, int accumulate, void* wscratch,
                         void* stream);
-/* cvb_conv2d_fwd (bf16 out, no accumulate) that also writes per-(tile, warp) BN partial sums of its
-   outputs [rows][2][cout] (sum, sum of squares) into st_part; *st_rows = rows written or 0 (geometry
-   without the TMA-store epilogue / capacity st_cap floats exceeded). */
-int cvb_conv2d_fwd_stats(const void* x, int n, int h, int w, int cin, int xcs, const void* wt, int cout, int kh,
-                         int kw, int stride, int pad, void* y, int oh, int ow, int ycs, int yoff, const float* bias,
-                         float* st_part, int64_t st_cap, int* st_rows, void* stream);
 int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, int dycs, const void* x, int h, int w, int cin,
                      int xcs, int kh, int kw, int stride, int pad, float* part, int max_splits, int* splits_out,
                      void* stream);
@@ -56,8 +50,6 @@ int cvb_debug_trace(long long* host_out);
 int64_t cvb_bn_workspace_floats(int64_t rows, int C);
 int cvb_bn_stats(const void* x, int64_t rows, int C, int xcs, float* ws, float* mean, float* rstd, float eps,
                  float* run_mean, float* run_var, float momentum, void* stream);
-int cvb_bn_finalize_partials(const float* part, int nrows, int C, int64_t count, float eps, float* mean, float* rstd,
-                             float* run_mean, float* run_var, float momentum, void* stream);
 int cvb_bn_apply(const void* x, int64_t rows, int C, int xcs, const float* mean, const float* rstd, const float* gamma,
                  const float* beta, const void* res, int rcs, int relu, void* y, int ycs, int ycoff, void* stream);
 int cvb_bn_backward(const void* dy, int dycs, const void* x, int xcs, const void* y, int ycs, int64_t rows, int C,

@@ -61,9 +61,6 @@ SIGNATURES = {
     "cvb_bn_backward": (_INT, [_P, _INT, _P, _INT, _P, _INT, _I64, _INT, _P, _P, _P, _P, _INT, _P, _P, _P, _P, _INT,
                                _P, _INT, _P, _P]),
     "cvb_bn_fused_workspace_floats": (_I64, [_INT]),
-    "cvb_conv2d_fwd_stats": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT,
-                                    _INT, _INT, _P, _P, _I64, _P, _P]),
-    "cvb_bn_finalize_partials": (_INT, [_P, _INT, _INT, _I64, _c.c_float, _P, _P, _P, _P, _c.c_float, _P]),
     "cvb_conv2d_dgrad_s2": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT, _INT, _INT, _P, _INT, _INT, _INT,
                                    _INT, _P, _P]),
     "cvb_bn_forward": (_INT, [_P, _I64, _INT, _INT, _P, _P, _P, _c.c_float, _P, _P, _c.c_float, _P, _P, _P, _INT, _INT,

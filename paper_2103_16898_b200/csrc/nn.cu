@@ -849,16 +849,6 @@ CVB_API int cvb_bn_stats(const void* x, int64_t rows, int C, int xcs, float* ws,
   return CVB_OK;
 }
 
-// Finalise BN statistics from partial sums [nrows][2][C] (e.g. written by the conv epilogue,
-// cvb_conv2d_fwd_stats): mean / rstd (+ running stats), fixed-order double sums.
-CVB_API int cvb_bn_finalize_partials(const float* part, int nrows, int C, int64_t count, float eps, float* mean,
-                                     float* rstd, float* run_mean, float* run_var, float momentum, void* stream) {
-  cvb_launch(bn_finalize, (C + 31) / 32, FIN_WARPS * 32, 0, STREAM, part, nrows, C, (double)count, eps, mean, rstd,
-             run_mean, run_var, momentum);
-  CVB_CHECK_LAUNCH();
-  return CVB_OK;
-}
-
 CVB_API int cvb_bn_apply(const void* x, int64_t rows, int C, int xcs, const float* mean, const float* rstd,
                          const float* gamma, const float* beta, const void* res, int rcs, int relu, void* y, int ycs,
                          int ycoff, void* stream) {

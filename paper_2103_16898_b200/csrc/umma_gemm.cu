@@ -108,7 +108,6 @@ struct GemmParams {
   uint32_t stg_off;         // smem offset of the 4 x 2 staging buffers (4 KB each)
   int st_bw, st_bh, st_bn;  // the warp's box in pixel space (NHWC); dense/partial: 32,1,1
   FastDiv fd_m, fd_n, fd_mn, fd_pw, fd_ph;   // m_tiles, n_tiles, m_tiles*n_tiles, ptiles_w, ptiles_h
-  float* st_part;           // BN statistics of the stored bf16 outputs: [m_tiles*4][2][N] (sum, sumsq)
   int n_epi;                // epilogue warps: 4, or 8 (two per TMEM lane quarter, column halves)
   uint32_t stg_warp;        // staging bytes per epilogue warp (two buffers)
   int st_rows;              // valid rows of an M tile (multiple of 32); warps past it store nothing
@@ -661,17 +660,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       if (p.st_tma) {
         // box origin of this warp's 32 rows
         int c1 = 0, c2 = 0, c3 = 0;
-        float rvalid = 1.f;   // this thread's row is a real output pixel (BN statistics mask)
         if (p.out_mode == OUT_NHWC) {
           const int q = (int)p.fd_pw.div((uint32_t)mt), q2 = (int)p.fd_ph.div((uint32_t)q);
           c1 = (mt - q * p.ptiles_w) * p.tw + w_off;
           c2 = (q - q2 * p.ptiles_h) * p.th + h_off;
           c3 = q2 * p.tn + n_off;
-          if (p.st_part) {
-            const int pw_ = (mt - q * p.ptiles_w) * p.tw + wb, ph_ = (q - q2 * p.ptiles_h) * p.th + hb,
-                      pn_ = q2 * p.tn + nb;
-            rvalid = (row < p.st_rows && pw_ < p.OW && ph_ < p.OH && pn_ < p.NIMG) ? 1.f : 0.f;
-          }
         } else {
           c1 = mt * BM + quarter * 32;
           c2 = p.out_mode == OUT_PARTIAL ? sp : 0;
@@ -705,37 +698,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
 #pragma unroll
           for (int cc = 0; cc < 64; cc += 16)
             if (cc < p.st_ch) stage16(p, buf, lane, cc, nt * p.BN + c + cc, r + cc, has_k);
-          if (p.st_part) {
-            // per-column sum / sum of squares of the bf16-rounded outputs over this warp's 32
-            // rows: reduce-scatter over the lanes (31 shuffles per 16 columns) leaves lane l
-            // with value l (l < 16: sum of column l, else sumsq of column l-16)
-#pragma unroll
-            for (int cc = 0; cc < 64; cc += 16) {
-              if (cc >= p.st_ch) break;
-              float a[32];
-#pragma unroll
-              for (int jj = 0; jj < 16; jj++) {
-                float v = __uint_as_float(r[cc + jj]);
-                if (p.bias) v += __ldg(p.bias + min(nt * p.BN + c + cc + jj, p.N - 1));
-                v = __bfloat162float(__float2bfloat16_rn(v)) * rvalid;
-                a[jj] = v;
-                a[16 + jj] = v * v;
-              }
-#pragma unroll
-              for (int wdt = 16; wdt >= 1; wdt >>= 1) {
-                const bool upper = (lane & wdt) != 0;
-#pragma unroll
-                for (int i = 0; i < wdt; i++) {
-                  const float send = upper ? a[i] : a[i + wdt];
-                  const float keep = upper ? a[i + wdt] : a[i];
-                  a[i] = keep + __shfl_xor_sync(0xffffffffu, send, wdt);
-                }
-              }
-              const int col = nt * p.BN + c + cc + (lane & 15);
-              if (col < p.N)
-                p.st_part[((int64_t)(mt * 4 + quarter) * 2 + (lane >> 4)) * p.N + col] = a[0];
-            }
-          }
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
@@ -965,7 +927,6 @@ int plan_tma_store(GemmParams& p) {
 
 int g_num_sms = 0;
 bool g_attr_done = false;
-int g_last_stats_rows = 0;   // partial rows the last launch wrote to st_part (0: none)
 long long* g_trace = nullptr;
 
 int launch(GemmParams& p, cudaStream_t stream) {
@@ -987,8 +948,6 @@ int launch(GemmParams& p, cudaStream_t stream) {
   const uint32_t stg_bytes = p.st_tma ? (uint32_t)p.n_epi * p.stg_warp : 0u;
   if (p.st_tma && 2 * stage_bytes + p.b_res_bytes + stg_bytes > 224u * 1024u) p.st_tma = 0;   // keep 2 stages
   if (p.out_par && !p.st_tma) { cvb_set_error("parity output needs the TMA-store epilogue"); return CVB_EINVAL; }
-  if (!p.st_tma || p.out_mode != OUT_NHWC || p.out_f32 || p.accum) p.st_part = nullptr;
-  g_last_stats_rows = p.st_part ? p.m_tiles * 4 : 0;
   const uint32_t stg = p.st_tma ? stg_bytes : 0u;
   p.stages = (int)((224u * 1024u - p.b_res_bytes - stg) / stage_bytes);
   if (p.stages > 8) p.stages = 8;
@@ -1107,29 +1066,6 @@ uint32_t gather_entry(int k_elem, int cin, int ntaps, int KW, int pad, int strid
 //   y[n,oh,ow, yoff+co] = bias[co] + sum_{kh,kw,ci} x[n, oh*s-pad+kh, ow*s-pad+kw, ci] * w[co][kh][kw][ci]
 // x: NHWC bf16 (channel stride xcs, channels [0,cin)), cin multiple of 8.
 // w: bf16 [cout][kh*kw*cin] (K-major).  y: NHWC (bf16, or fp32 if y_f32) with channel stride ycs.
-static float* g_req_stats = nullptr;   // set by cvb_conv2d_fwd_stats around one cvb_conv2d_fwd call
-static int64_t g_req_stats_cap = 0;
-
-CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs, const void* wt, int cout, int kh,
-                           int kw, int stride, int pad, void* y, int oh, int ow, int ycs, int yoff, const float* bias,
-                           int y_f32, int accumulate, void* stream);
-
-// Convolution forward that also writes per-(tile, warp) BN statistics of its bf16 outputs
-// (sum, sum of squares per channel) to st_part [rows][2][cout]; *st_rows = rows written, or
-// 0 when this geometry cannot produce them (or they would exceed st_cap floats) -- the caller
-// then computes statistics separately.  Finalise with cvb_bn_finalize_partials.
-CVB_API int cvb_conv2d_fwd_stats(const void* x, int n, int h, int w, int cin, int xcs, const void* wt, int cout,
-                                 int kh, int kw, int stride, int pad, void* y, int oh, int ow, int ycs, int yoff,
-                                 const float* bias, float* st_part, int64_t st_cap, int* st_rows, void* stream) {
-  g_req_stats = st_part;
-  g_req_stats_cap = st_cap;
-  g_last_stats_rows = 0;
-  int rc = cvb_conv2d_fwd(x, n, h, w, cin, xcs, wt, cout, kh, kw, stride, pad, y, oh, ow, ycs, yoff, bias, 0, 0, stream);
-  g_req_stats = nullptr;
-  *st_rows = rc == CVB_OK ? g_last_stats_rows : 0;
-  return rc;
-}
-
 CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs, const void* wt, int cout, int kh,
                            int kw, int stride, int pad, void* y, int oh, int ow, int ycs, int yoff, const float* bias,
                            int y_f32, int accumulate, void* stream) {
@@ -1186,7 +1122,6 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
       if ((rc = encode_2d(&p.mapB[0], wt, cout, K, K, p.b_cel, p.BN))) return rc;
       p.out_mode = OUT_NHWC; p.out_f32 = y_f32; p.out = y; p.ldc = ycs; p.col_off = yoff; p.bias = bias;
       p.accum = accumulate;
-      if (g_req_stats && (int64_t)p.m_tiles * 8 * cout <= g_req_stats_cap) p.st_part = g_req_stats;
       return launch(p, (cudaStream_t)stream);
     }
   }
@@ -1232,7 +1167,6 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
   if ((rc = encode_2d(&p.mapB[0], wt, cout, K, K, p.b_cel, p.BN))) return rc;
   p.out_mode = OUT_NHWC; p.out_f32 = y_f32; p.out = y; p.ldc = ycs; p.col_off = yoff; p.bias = bias;
   p.accum = accumulate;
-  if (g_req_stats && (int64_t)p.m_tiles * 8 * cout <= g_req_stats_cap) p.st_part = g_req_stats;
   return launch(p, (cudaStream_t)stream);
 }
 

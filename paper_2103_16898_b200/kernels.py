@@ -108,32 +108,6 @@ def conv2d_fwd(x, w, stride=1, pad=0, bias=None, out=None, out_f32=False, cin=No
     return out
 
 
-def conv2d_fwd_stats(x, w, stride, pad, out, st_part, acct_flops=None, cin=None):
-    """conv2d_fwd (bf16 out) + per-(tile, warp) BN partial sums of the outputs in st_part.
-    Returns the number of partial rows written (0: not available for this geometry)."""
-    lib = _lib_bound()
-    n, h, wd, cs = x.shape
-    cin = cs if cin is None else cin
-    cout, kh, kw, _ = w.shape
-    _, oh, ow, ycs = out.shape
-    rows = ctypes.c_int(0)
-    tok = REC.begin(1, "umma_gemm", acct_flops if acct_flops is not None else 2 * n * oh * ow * cout * kh * kw * cin)
-    rc = lib.cvb_conv2d_fwd_stats(x.data_ptr(), n, h, wd, cin, x.stride(2), w.data_ptr(), cout, kh, kw, stride, pad,
-                                  out.data_ptr(), oh, ow, ycs, 0, None, st_part.data_ptr(), st_part.numel(),
-                                  ctypes.byref(rows), _stream())
-    REC.end(tok)
-    _lib.check(rc, "conv2d_fwd_stats")
-    return rows.value
-
-
-def bn_finalize_partials(part, nrows, C, count, mean, rstd, eps=1e-5, run_mean=None, run_var=None, momentum=0.1):
-    tok = REC.begin(1, "bn", 0, nrows * 2 * C * 4)
-    rc = _lib_bound().cvb_bn_finalize_partials(part.data_ptr(), nrows, C, count, eps, mean.data_ptr(), rstd.data_ptr(),
-                                               _ptr(run_mean), _ptr(run_var), momentum, _stream())
-    REC.end(tok)
-    _lib.check(rc, "bn_finalize_partials")
-
-
 def conv2d_dgrad_s2(dy, w, pad, dx, accumulate=False, wscratch=None, acct_flops=None):
     """dX of a stride-2 conv by output-parity classes (csrc/umma_gemm.cu).  Returns False,
     launching nothing, when the geometry is unsupported (caller uses the upsampled form)."""

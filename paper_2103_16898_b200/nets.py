@@ -26,11 +26,6 @@ import torch
 from . import kernels as K
 
 BF16, F32 = torch.bfloat16, torch.float32
-# BN statistics from the conv epilogue (cvb_conv2d_fwd_stats): correct, but measured SLOWER on
-# B200 (small CNN 0.667 -> 0.875 ms/step: the lane reductions lengthen the epilogue, which bounds
-# the narrow convs, and the partial-row finalisation costs more than the fused statistics
-# pass it replaces) -- opt-in only.
-EPI_STATS = bool(os.environ.get("CVB_EPI_STATS"))
 ALIGN = 64  # elements; keeps every parameter view 128-byte aligned (TMA needs 16 B)
 
 
@@ -177,8 +172,6 @@ class ConvBN:
         self.wcount = self.cout * self.k * self.k * self.cin
         scratch.part_floats = max(scratch.part_floats, min(MAX_SPLITS * self.wcount, max(PART_CAP, 8 * self.wcount)))
         scratch.bn_floats = max(scratch.bn_floats, K._lib_bound().cvb_bn_workspace_floats(self.rows, self.cout))
-        if EPI_STATS:   # conv-epilogue statistics: <= 4 warps x (one tile per 8x8 pixels) x 2 x cout
-            scratch.bn_floats = max(scratch.bn_floats, 8 * self.cout * n * -(-self.oh // 8) * -(-self.ow // 8))
         if self.need_dgrad:
             scratch.flip_elems = max(scratch.flip_elems, self.cout * self.k * self.k * self.cin)
             if self.s == 2:
@@ -188,24 +181,13 @@ class ConvBN:
 
     def forward(self, ps: ParamStore, x, out, res=None, out_coff=0, cin=None):
         """x: [n,h,w,cs] (channels [0,cin)); out: [n,oh,ow,ocs] written at channel out_coff."""
-        st_rows = 0
         if self.s2d:
             K.space_to_depth2(x, self.xs)
             K.s2d_weights(ps.b[self.W], self.ws)
             K.conv2d_fwd(self.xs, self.ws, 1, 2, out=self.z, out_hw=(self.oh, self.ow), acct_flops=self.flops)
-        elif EPI_STATS:
-            # BN statistics come out of the conv epilogue: no statistics pass over z
-            st_rows = K.conv2d_fwd_stats(x, ps.b[self.W], self.s, self.pad, self.z, self.scratch.bnws,
-                                         acct_flops=self.flops, cin=cin if cin is not None else self.cin)
         else:
             K.conv2d_fwd(x, ps.b[self.W], self.s, self.pad, out=self.z, cin=cin if cin is not None else self.cin,
                          acct_flops=self.flops)
-        if st_rows:
-            K.bn_finalize_partials(self.scratch.bnws, st_rows, self.cout, self.rows, self.mean, self.rstd,
-                                   run_mean=self.run_mean, run_var=self.run_var)
-            K.bn_apply(self.z, self.rows, self.cout, self.cout, self.mean, self.rstd, ps.p[self.G], ps.p[self.B], out,
-                       out.shape[-1], out_coff, relu=self.relu, res=res, rcs=res.shape[-1] if res is not None else 0)
-            return
         K.bn_forward(self.z, self.rows, self.cout, self.cout, self.scratch.bnws, self.mean, self.rstd, ps.p[self.G],
                      ps.p[self.B], out, out.shape[-1], out_coff, relu=self.relu, res=res,
                      rcs=res.shape[-1] if res is not None else 0, run_mean=self.run_mean, run_var=self.run_var)
