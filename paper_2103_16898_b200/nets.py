@@ -297,11 +297,12 @@ class Linear:
             used = K.splits_used(B, self.s_wg)
             K.reduce_splits(part, used, self.fpad * self.fin, ps.g[self.W])
         else:
-            K.gemm(dy, x, self.fpad, self.fin, B, 1, 1, out=ps.g[self.W], out_f32=True, acct_flops=fl)
+            # unsplit wgrad: 64-column N tiles so the (m, n) tiles fill the SMs
+            K.gemm(dy, x, self.fpad, self.fin, B, 1, 1, out=ps.g[self.W], out_f32=True, acct_flops=fl, max_bn=64)
         K.col_sum(dy, B, self.fpad, self.fpad, ps.g[self.Bn])
         ps.grad_ready(self.W, self.Bn)
         if dx is not None:
-            K.gemm(dy, ps.b[self.W], B, self.fin, self.fpad, 0, 1, out=dx, acct_flops=fl)
+            K.gemm(dy, ps.b[self.W], B, self.fin, self.fpad, 0, 1, out=dx, acct_flops=fl, max_bn=128)
 
 
 class Net:
