@@ -341,7 +341,7 @@ def run_ours(args, rank, world, local_rank):
                  "share_of_step": dms / step_ms_instr, "peak_source": src,
                  "per_kind_ms": {k: round(v[1], 4) for k, v in summ.items()},
                  "algorithmic": "sum over the step's launches of 2*M*N*K (real channel counts)"
-                 if dfl > 0 else "sum of read+write bytes"})
+                 if dfl > 0 else "sum over the step's launches of each input read once + each output written once"})
     prof = ROOT / "profiles" / "roofline_live.json"
     if rank == 0:
         try:
@@ -357,7 +357,7 @@ def run_ours(args, rank, world, local_rank):
         v, cores, sample, _ = cpu_reference(args.model, B, key, spec, args.cpu_seconds, warmup=1)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
     if rank == 0:
-        decrypt_launches = 2   # gcm_kernel (finalises in its last CTA) + records_to_nhwc
+        decrypt_launches = 1   # fused gcm_kernel<decode>: open + tag finalisation (last CTA) + NHWC-8 decode
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",

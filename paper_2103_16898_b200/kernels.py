@@ -199,7 +199,8 @@ def bn_forward(x, rows, C, xcs, ws, mean, rstd, gamma, beta, y, ycs, ycoff=0, re
         bn_stats(x, rows, C, xcs, ws, mean, rstd, eps, run_mean, run_var, momentum)
         bn_apply(x, rows, C, xcs, mean, rstd, gamma, beta, y, ycs, ycoff, relu, res, rcs)
         return
-    tok = REC.begin(1, "bn", 0, rows * C * 2 * (4 if res is not None else 3))
+    # algorithmic bytes: x (+res) read once, y written once (the statistics pass's read of x is traffic)
+    tok = REC.begin(1, "bn", 0, rows * C * 2 * (3 if res is not None else 2))
     rc = _lib_bound().cvb_bn_forward(x.data_ptr(), rows, C, xcs, ws.data_ptr(), mean.data_ptr(), rstd.data_ptr(), eps,
                                      _ptr(run_mean), _ptr(run_var), momentum, gamma.data_ptr(), beta.data_ptr(),
                                      _ptr(res), rcs, int(relu), y.data_ptr(), ycs, ycoff, _stream())
@@ -217,8 +218,11 @@ def bn_apply(x, rows, C, xcs, mean, rstd, gamma, beta, y, ycs, ycoff=0, relu=Tru
 
 def bn_backward(dy, dycs, x, xcs, rows, C, mean, rstd, gamma, beta, ws, dgamma, dbeta, relu=True, y=None, ycs=0,
                 dx=None, dxcs=0, dx32=None, accum32=False, dz_out=None):
-    # partial pass reads dy, x (, y) [+ writes dz]; apply pass re-reads them and writes dx
-    nb = rows * C * 2 * ((3 if y is not None else 2) * 2 + (1 if dz_out is not None else 0) + 1)
+    # algorithmic bytes: dy, x (, y) read once, dz (bf16) and dx written once -- dx as bf16, fp32, or fp32
+    # read-modify-write when accumulating. The kernel's second pass re-reads its inputs (mostly from L2);
+    # those re-reads are traffic, not algorithmic bytes.
+    dx_b = 8 if (dx32 is not None and accum32) else 4 if dx32 is not None else 2 if dx is not None else 0
+    nb = rows * C * (2 * (3 if y is not None else 2) + (2 if dz_out is not None else 0) + dx_b)
     fn = _lib_bound().cvb_bn_backward if _UNFUSED_BN else _lib_bound().cvb_bn_backward_fused
     tok = REC.begin((3 if (dx is not None or dx32 is not None) else 2) if _UNFUSED_BN else 1, "bn", 0, nb)
     rc = fn(dy.data_ptr(), dycs, x.data_ptr(), xcs, _ptr(y), ycs, rows, C, mean.data_ptr(),
