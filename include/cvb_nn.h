@@ -86,6 +86,17 @@ int cvb_gap_bwd(const void* dy, int n, int hw, int C, void* dx, void* stream);
 /* ---- loss, reductions, layout helpers ---------------------------------------------------------- */
 int cvb_softmax_xent(const float* logits, int B, int C, const int32_t* labels, float grad_scale, float* row_ws,
                      float* loss_out, void* dlogits, int ldd, void* stream);
+/* Fused classifier head (csrc/head.cu): Linear(fin -> C <= 16, weights padded to 16 rows) forward,
+ * softmax cross-entropy (row_loss, mean loss, dlogits scaled by `scale`) and the layer's backward
+ * (dw [16][fin], db [16], dx = dlogits W optionally masked by x > 0, dprev_b = column sums of dx)
+ * in one cooperative launch.  fin a multiple of 256, <= 1024; part holds
+ * cvb_head_workspace_floats(B, fin) floats.  Replaces gemm + softmax_xent + gemm + col_sum + gemm
+ * (+ relu_bwd + col_sum) of the unfused head. */
+int cvb_head_train(const void* x, int64_t ldx, const void* w, const float* bias, const int32_t* labels, int B,
+                   int fin, int C, float scale, int relu_mask, float* logits, void* dlogits, float* row_loss,
+                   float* loss, void* dx, int64_t lddx, float* dw, float* db, float* dprev_b, float* part,
+                   void* stream);
+int64_t cvb_head_workspace_floats(int B, int fin);
 int cvb_reduce_splits(const float* part, int splits, int64_t count, float* out, int accumulate, float scale,
                       void* stream);
 /* split-K epilogue of a dense layer: out[r][c] = act(sum_s part[s][r][c] + bias[c]) */

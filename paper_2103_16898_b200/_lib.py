@@ -80,6 +80,9 @@ SIGNATURES = {
     "cvb_gap_fwd": (_INT, [_P, _INT, _INT, _INT, _INT, _P, _P]),
     "cvb_gap_bwd": (_INT, [_P, _INT, _INT, _INT, _P, _P]),
     "cvb_softmax_xent": (_INT, [_P, _INT, _INT, _P, _c.c_float, _P, _P, _P, _INT, _P]),
+    "cvb_head_train": (_INT, [_P, _I64, _P, _P, _P, _INT, _INT, _INT, _c.c_float, _INT, _P, _P, _P, _P, _P, _I64,
+                              _P, _P, _P, _P, _P]),
+    "cvb_head_workspace_floats": (_I64, [_INT, _INT]),
     "cvb_reduce_splits": (_INT, [_P, _INT, _I64, _P, _INT, _c.c_float, _P]),
     "cvb_reduce_splits_act": (_INT, [_P, _INT, _INT, _INT, _P, _INT, _P, _INT, _I64, _P]),
     "cvb_weight_flip": (_INT, [_P, _INT, _INT, _INT, _INT, _P, _P]),

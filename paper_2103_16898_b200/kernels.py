@@ -302,6 +302,26 @@ def softmax_xent(logits, B, C, labels, grad_scale, row_ws, loss_out, dlogits):
     _lib.check(rc, "softmax_xent")
 
 
+def head_workspace_floats(B, fin):
+    return int(_lib_bound().cvb_head_workspace_floats(B, fin))
+
+
+def head_train(x, w, bias, labels, B, C, scale, logits, dlogits, row_loss, loss, dw, db, part, dx=None,
+               relu_mask=False, dprev_b=None):
+    """Fused classifier head (csrc/head.cu): forward + softmax-CE + backward of Linear(fin -> C <= 16)."""
+    fin = w.shape[-1]
+    nb = (B * x.stride(0) * 2 + w.numel() * 2 + B * 16 * 6 + dw.numel() * 4
+          + (B * fin * 2 if dx is not None else 0))
+    tok = REC.begin(1, "head", 0, nb)   # CUDA-core kernel: accounted by bytes
+    rc = _lib_bound().cvb_head_train(x.data_ptr(), x.stride(0), w.data_ptr(), bias.data_ptr(), labels.data_ptr(), B,
+                                     fin, C, scale, int(relu_mask), logits.data_ptr(), dlogits.data_ptr(),
+                                     row_loss.data_ptr(), loss.data_ptr(), _ptr(dx),
+                                     dx.stride(0) if dx is not None else 0, dw.data_ptr(), db.data_ptr(),
+                                     _ptr(dprev_b), part.data_ptr(), _stream())
+    REC.end(tok)
+    _lib.check(rc, "head_train")
+
+
 def reduce_splits(part, splits, count, out, accumulate=False, scale=1.0):
     tok = REC.begin(1, "reduce", 0, (splits + 1) * count * 4)
     rc = _lib_bound().cvb_reduce_splits(part.data_ptr(), splits, count, out.data_ptr(), int(accumulate), scale, _stream())

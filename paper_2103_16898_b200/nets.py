@@ -26,6 +26,7 @@ import torch
 from . import kernels as K
 
 BF16, F32 = torch.bfloat16, torch.float32
+_UNFUSED_HEAD = os.environ.get("CVB_UNFUSED_HEAD", "0") not in ("", "0")
 ALIGN = 64  # elements; keeps every parameter view 128-byte aligned (TMA needs 16 B)
 
 
@@ -288,7 +289,7 @@ class Linear:
             if relu:
                 K.relu_fwd(out)
 
-    def backward(self, ps, dy, x, dx=None):
+    def backward(self, ps, dy, x, dx=None, bias_grad=True):
         B = x.shape[0]
         fl = 2 * B * self.fout * self.fin
         if self.s_wg > 1:
@@ -299,7 +300,8 @@ class Linear:
         else:
             # unsplit wgrad: 64-column N tiles so the (m, n) tiles fill the SMs
             K.gemm(dy, x, self.fpad, self.fin, B, 1, 1, out=ps.g[self.W], out_f32=True, acct_flops=fl, max_bn=64)
-        K.col_sum(dy, B, self.fpad, self.fpad, ps.g[self.Bn])
+        if bias_grad:
+            K.col_sum(dy, B, self.fpad, self.fpad, ps.g[self.Bn])
         ps.grad_ready(self.W, self.Bn)
         if dx is not None:
             K.gemm(dy, ps.b[self.W], B, self.fin, self.fpad, 0, 1, out=dx, acct_flops=fl, max_bn=128)
@@ -324,6 +326,13 @@ class Net:
         self.global_batch = global_batch or batch
         self.device = device
         self._build(batch, device)
+        # fused classifier head (csrc/head.cu): one launch for the last Linear's forward, the loss
+        # and its backward; CVB_UNFUSED_HEAD=1 keeps the gemm/softmax/col_sum launches
+        h = self.head
+        self.fused_head = (not _UNFUSED_HEAD and h.fpad == 16 and h.fin % 256 == 0 and h.fin <= 1024
+                           and self.num_classes <= 16)
+        if self.fused_head:
+            self.scratch.part_floats = max(self.scratch.part_floats, K.head_workspace_floats(batch, h.fin))
         self.scratch.finalize(device)
         self.ps.finalize(device)
         fpad = self.head.fpad
@@ -333,15 +342,45 @@ class Net:
         self.loss = torch.zeros(1, dtype=F32, device=device)
         return self
 
+    # models provide features(x) (everything before the head, writing head_in), features_backward(x,
+    # fused) (everything after the head's dx), and the attributes head_in / head_dx / head_relu
+    # (head_in is a ReLU output: mask dx) / prev_bias (Linear whose bias gradient = colsum(head_dx))
+    prev_bias = None
+
+    def forward(self, x):
+        self.features(x)
+        self.head.forward(self.ps, self.head_in, self.logits, out_f32=True)
+
+    def backward(self, x):
+        self.head.backward(self.ps, self.dlogits, self.head_in, self.head_dx)
+        if self.head_relu:
+            K.relu_bwd(self.head_dx, self.head_in)
+        self.features_backward(x, False)
+
+    def fwd_bwd(self, x, labels):
+        """Forward, loss and backward of one step (gradients in ps.g32, loss in self.loss)."""
+        if not self.fused_head:
+            self.forward(x)
+            self.loss_and_grad(labels)
+            self.backward(x)
+            return
+        self.features(x)
+        ps, h = self.ps, self.head
+        pb = self.prev_bias
+        K.head_train(self.head_in, ps.b[h.W], ps.p[h.Bn], labels, self.batch, self.num_classes,
+                     1.0 / self.global_batch, self.logits, self.dlogits, self.row_loss, self.loss, ps.g[h.W],
+                     ps.g[h.Bn], self.scratch.part, dx=self.head_dx, relu_mask=self.head_relu,
+                     dprev_b=ps.g[pb.Bn] if pb is not None else None)
+        ps.grad_ready(h.W, h.Bn)
+        self.features_backward(x, True)
+
     def loss_and_grad(self, labels):
         K.softmax_xent(self.logits, self.batch, self.num_classes, labels, 1.0 / self.global_batch, self.row_loss,
                        self.loss, self.dlogits)
 
     def step(self, x, labels, allreduce=None):
         """One training step on a resident input tile (NHWC8 bf16) and int32 labels."""
-        self.forward(x)
-        self.loss_and_grad(labels)
-        self.backward(x)
+        self.fwd_bwd(x, labels)
         if allreduce is not None:
             allreduce(self.ps.g32)
         self.optimizer_step()
@@ -387,8 +426,9 @@ class SmallCNN(Net):
         self.dh, self.dp2 = e(n, 256), e(n, 8, 8, 64)
         self.da4, self.da3, self.dp1 = e(n, 16, 16, 64), e(n, 16, 16, 64), e(n, 16, 16, 32)
         self.da2, self.da1 = e(n, 32, 32, 32), e(n, 32, 32, 32)
+        self.head_in, self.head_dx, self.head_relu, self.prev_bias = self.h, self.dh, True, self.fc1
 
-    def forward(self, x):
+    def features(self, x):
         ps = self.ps
         self.c1.forward(ps, x, self.a1)
         self.c2.forward(ps, self.a1, self.a2)
@@ -398,14 +438,12 @@ class SmallCNN(Net):
         K.maxpool_fwd(self.a4, 2, 2, 0, self.p2)
         flat = self.p2.view(self.batch, -1)
         self.fc1.forward(ps, flat, self.h, relu=True)
-        self.head.forward(ps, self.h, self.logits, out_f32=True)
 
-    def backward(self, x):
+    def features_backward(self, x, fused):
         ps = self.ps
         flat = self.p2.view(self.batch, -1)
-        self.head.backward(ps, self.dlogits, self.h, self.dh)
-        K.relu_bwd(self.dh, self.h)
-        self.fc1.backward(ps, self.dh, flat, self.dp2.view(self.batch, -1))
+        # fused head: dh is already ReLU-masked and fc1's bias gradient already written
+        self.fc1.backward(ps, self.dh, flat, self.dp2.view(self.batch, -1), bias_grad=not fused)
         K.maxpool_bwd(self.a4, self.dp2, 2, 2, 0, self.da4)
         self.c4.backward(ps, self.da4, self.a3, dx=self.da3)
         self.c3.backward(ps, self.da3, self.p1, dx=self.dp1)
@@ -483,8 +521,9 @@ class ResNet18(Net):
         self.final_hw = h * w
         self.pooled, self.dpooled = e(n, 512), e(n, 512)
         self.head.build(n, S)
+        self.head_in, self.head_dx, self.head_relu = self.pooled, self.dpooled, False
 
-    def forward(self, x):
+    def features(self, x):
         ps = self.ps
         self.stem.forward(ps, x, self.x0)
         cur = self.x0
@@ -492,11 +531,9 @@ class ResNet18(Net):
             b.forward(ps, cur, o)
             cur = o
         K.gap_fwd(cur, self.batch, self.final_hw, 512, 512, self.pooled)
-        self.head.forward(ps, self.pooled, self.logits, out_f32=True)
 
-    def backward(self, x):
+    def features_backward(self, x, fused):
         ps = self.ps
-        self.head.backward(ps, self.dlogits, self.pooled, self.dpooled)
         K.gap_bwd(self.dpooled, self.batch, self.final_hw, 512, self.douts[-1])
         for i in range(len(self.blocks) - 1, -1, -1):
             b = self.blocks[i]
@@ -713,12 +750,13 @@ class DenseNet121(Net):
         self.dy5 = e(n * h * w * self.final_c)
         self.final_hw = h * w
         self.pooled, self.dpooled = e(n, self.final_c), e(n, self.final_c)
+        self.head_in, self.head_dx, self.head_relu = self.pooled, self.dpooled, False
         self.dcast = e(ymax)
 
     def _v(self, buf, *shape):
         return buf[:math.prod(shape)].view(*shape)
 
-    def forward(self, x):
+    def features(self, x):
         ps, n = self.ps, self.batch
         self.stem.forward(ps, x, self.a0)
         c0 = self.stem.cout
@@ -745,12 +783,10 @@ class DenseNet121(Net):
         c = self.final_c
         self.norm5.forward(ps, self.bufs[-1], c, self._v(self.y5, n, h, w, c), c)
         K.gap_fwd(self._v(self.y5, n, h, w, c), n, h * w, c, c, self.pooled)
-        self.head.forward(ps, self.pooled, self.logits, out_f32=True)
 
-    def backward(self, x):
+    def features_backward(self, x, fused):
         ps, n = self.ps, self.batch
         c = self.final_c
-        self.head.backward(ps, self.dlogits, self.pooled, self.dpooled)
         h, w = self.geo[-1]
         dy5 = self._v(self.dy5, n, h, w, c)
         K.gap_bwd(self.dpooled, n, h * w, c, dy5)

@@ -160,9 +160,7 @@ class EncryptedTrainer:
         net = self.net
         if self.allreduce is not None:
             self.allreduce.reset()
-        net.forward(x)
-        net.loss_and_grad(lab)
-        net.backward(x)
+        net.fwd_bwd(x, lab)
 
     def _opt_body(self):
         self.net.optimizer_step()
