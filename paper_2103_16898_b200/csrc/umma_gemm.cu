@@ -109,6 +109,8 @@ struct GemmParams {
   int st_bw, st_bh, st_bn;  // the warp's box in pixel space (NHWC); dense/partial: 32,1,1
   FastDiv fd_m, fd_n, fd_mn, fd_pw, fd_ph;   // m_tiles, n_tiles, m_tiles*n_tiles, ptiles_w, ptiles_h
   int n_epi;                // epilogue warps: 4, or 8 (two per TMEM lane quarter, column halves)
+  int epi_alt;              // n_epi == 8: the two warp groups take alternate tiles (all columns)
+  int nacc_log2;            // TMEM accumulator buffers: 1 << nacc_log2 (2 or 4)
   uint32_t stg_warp;        // staging bytes per epilogue warp (two buffers)
   int st_rows;              // valid rows of an M tile (multiple of 32); warps past it store nothing
   int out_par;              // NHWC output is the parity sub-grid (out_ph, out_pw) of an out_H x out_W image
@@ -404,21 +406,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes + p.b_res_bytes +
                                                (p.st_tma ? (uint32_t)p.n_epi * p.stg_warp : 0u));
   uint64_t* empty = full + p.stages;
-  uint64_t* tfull = empty + p.stages;       // [2]
-  uint64_t* tempty = tfull + 2;             // [2]
-  uint64_t* bres_full = tempty + 2;         // [1]
+  uint64_t* tfull = empty + p.stages;       // [nacc <= 4]
+  uint64_t* tempty = tfull + 4;             // [nacc <= 4]
+  uint64_t* bres_full = tempty + 4;         // [1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
 
   // shfl: lets the compiler prove the role index warp-uniform (keeps the issue loops on the
   // uniform datapath)
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  const int tmem_cols = (2 * p.BN <= 32) ? 32 : (2 * p.BN <= 64) ? 64 : (2 * p.BN <= 128) ? 128 : (2 * p.BN <= 256) ? 256 : 512;
+  const int nacc = 1 << p.nacc_log2, acc_cols = nacc * p.BN;
+  const int tmem_cols = acc_cols <= 32 ? 32 : acc_cols <= 64 ? 64 : acc_cols <= 128 ? 128 : acc_cols <= 256 ? 256 : 512;
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < 4; i++) { prefetch_map(&p.mapA[i]); prefetch_map(&p.mapB[i]); }
     if (p.st_tma) prefetch_map(&p.mapC);
     for (int i = 0; i < p.stages; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < 2; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], p.n_epi); }
+    for (int i = 0; i < nacc; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], p.epi_alt ? 4 : p.n_epi); }
     mbar_init(bres_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -543,9 +546,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
       const int sp = (int)p.fd_mn.div((uint32_t)u);
       const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
-      const int acc = lt & 1;
+      const int acc = lt & (nacc - 1);
       if (lt == 0 && p.b_res) mbar_wait(bres_full, 0);
-      mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+      mbar_wait(&tempty[acc], ((lt >> p.nacc_log2) & 1) ^ 1);
       tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * p.BN;
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -625,8 +628,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       const int rest = (int)p.fd_m.div((uint32_t)u), mt = u - rest * p.m_tiles;
       const int sp = (int)p.fd_n.div((uint32_t)rest), nt = rest - sp * p.n_tiles;
       const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
-      const int acc = lt & 1;
-      mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      if (p.epi_alt && (lt & 1) != ((warp - 2) >> 2)) continue;   // the other warp group's tile
+      const int acc = lt & (nacc - 1);
+      mbar_wait(&tfull[acc], (lt >> p.nacc_log2) & 1);
       if (warp == 2 && lane == 0) TRACE(3, lt);
       tc_fence_after();
       bool valid = true;
@@ -670,8 +674,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           c2 = p.out_mode == OUT_PARTIAL ? sp : 0;
         }
         const uint32_t stg = smem0 + p.stg_off + (uint32_t)(warp - 2) * p.stg_warp;
-        const int span = p.n_epi == 8 ? p.BN >> 1 : p.BN;          // columns this warp stores
-        const int cbeg = p.n_epi == 8 && warp >= 6 ? span : 0;
+        const int span = p.n_epi == 8 && !p.epi_alt ? p.BN >> 1 : p.BN;   // columns this warp stores
+        const int cbeg = p.n_epi == 8 && !p.epi_alt && warp >= 6 ? span : 0;
         const int cend = quarter * 32 < p.st_rows ? cbeg + span : cbeg;   // short tile: nothing to store
         const bool one_chunk = span <= p.st_ch;
         bool released = false;
@@ -868,7 +872,7 @@ int plan_tma_store(GemmParams& p) {
   if (off) return CVB_OK;
   const int es = p.out_f32 ? 4 : 2;
   const int maxch = 128 / es;
-  const int span = p.n_epi == 8 ? p.BN / 2 : p.BN;   // columns per epilogue warp
+  const int span = p.n_epi == 8 && !p.epi_alt ? p.BN / 2 : p.BN;   // columns per epilogue warp
   int ch = maxch;
   while (ch > 8 && span % ch) ch >>= 1;
   if (span % ch || ch * es < 32) return CVB_OK;
@@ -940,10 +944,21 @@ int launch(GemmParams& p, cudaStream_t stream) {
   if (env_epi4 < 0) env_epi4 = getenv("CVB_EPI4") ? 1 : 0;
   // narrow tiles: two epilogue warps per TMEM lane quarter (each stores half the columns) so
   // the per-tile epilogue latency (TMEM load, staging, store issue) overlaps across warps
+  static int env_alt = -1, env_nacc = -1;
+  if (env_alt < 0) {
+    const char* e = getenv("CVB_EPI_ALT");
+    env_alt = e ? atoi(e) : 1;
+    e = getenv("CVB_NACC");
+    env_nacc = e ? atoi(e) : 4;
+  }
   p.n_epi = (!env_epi4 && p.BN <= 64 && p.BN % 32 == 0) ? 8 : 4;
+  // narrow tiles: more TMEM accumulators (the epilogue of tile i no longer gates the MMAs of
+  // tile i+2) and alternate-tile epilogue warp groups (two tiles drain concurrently)
+  p.nacc_log2 = (env_nacc >= 4 && 4 * p.BN <= 512) ? 2 : 1;
+  p.epi_alt = (p.n_epi == 8 && env_alt && p.nacc_log2 == 2) ? 1 : 0;
   plan_tma_store(p);
-  if (!p.st_tma && p.n_epi == 8) { p.n_epi = 4; plan_tma_store(p); }
-  if (!p.st_tma) p.n_epi = 4;
+  if (!p.st_tma && p.n_epi == 8) { p.n_epi = 4; p.epi_alt = 0; plan_tma_store(p); }
+  if (!p.st_tma) { p.n_epi = 4; p.epi_alt = 0; }
   p.stg_warp = p.st_tma ? 2u * 32u * (uint32_t)p.st_ch * (p.out_f32 ? 4u : 2u) : 0u;
   const uint32_t stg_bytes = p.st_tma ? (uint32_t)p.n_epi * p.stg_warp : 0u;
   if (p.st_tma && 2 * stage_bytes + p.b_res_bytes + stg_bytes > 224u * 1024u) p.st_tma = 0;   // keep 2 stages
