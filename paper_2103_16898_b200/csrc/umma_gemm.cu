@@ -122,6 +122,8 @@ struct GemmParams {
   // MODE_HALO geometry
   int h_cin, h_cg, h_planes, h_pitch, h_pad, h_kh, h_kw;
   int h_rows;                   // 1: the halo is ONE SW128 box of 64-channel (128-byte) pixel rows
+  int h_rowpad;                 // 1: 32-channel input (cin == 32) loaded as 128-byte SW128 rows whose
+                                //    upper half is TMA zero fill (SW64 operand reads run at half rate)
   int h_mps;                    // MMAs per stage (taps * cg/16)
   uint32_t h_plane_stride;      // bytes between 8-channel planes (>= halo pixels * 16, 128-aligned)
   uint32_t h_box_bytes;         // bytes TMA writes per plane
@@ -356,11 +358,11 @@ __device__ __forceinline__ void halo_issue(uint32_t tmem_d, uint64_t a0, uint64_
 // instead of eight 16-byte plane rows): tap (kh, kw) = start row kh*pitch + kw (8 x 16-byte
 // units per row), 16-channel step j = +32 bytes inside the swizzled row.  UMMA derives the
 // swizzle from absolute smem address bits, so row-shifted starts read the TMA layout exactly.
-template <int KH, int KW, int NJ>
-__device__ __forceinline__ void halo_rows_issue(uint32_t tmem_d, uint64_t a0, uint64_t b0, uint32_t idesc,
+template <int KH, int KW, int NJ, int RU>
+__device__ __forceinline__ void halo_rows_issue_t(uint32_t tmem_d, uint64_t a0, uint64_t b0, uint32_t idesc,
                                                 uint32_t acc_flag, uint32_t leader, int kb, uint32_t cin16,
                                                 uint32_t slab16) {
-  constexpr uint32_t pitch = 8 + KW - 1, RU = 2 * NJ;   // row = NJ 16-channel steps = 2*NJ 16-byte units
+  constexpr uint32_t pitch = 8 + KW - 1;   // RU: 16-byte units per smem pixel row (>= 2*NJ)
   uint32_t qt = (uint32_t)kb * NJ;
 #pragma unroll
   for (int kh = 0; kh < KH; kh++) {
@@ -571,11 +573,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
             uint32_t acc_flag = kb > kb0 ? 1u : 0u;
             const int geo = p.h_kh * 100 + p.h_kw * 10 + (int)nj;
             if (p.h_cg == 8) halo8_issue<3, 3>(tmem_d, a0, p.adesc[1] + sa, b0, p.idesc, leader, slab16);
-            else if (p.h_rows && geo == 334) halo_rows_issue<3, 3, 4>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
-            else if (p.h_rows && geo == 114) halo_rows_issue<1, 1, 4>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
-            else if (p.h_rows && geo == 332) halo_rows_issue<3, 3, 2>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
-            else if (p.h_rows && geo == 112) halo_rows_issue<1, 1, 2>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
-            else if (p.h_rows && geo == 442) halo_rows_issue<4, 4, 2>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (p.h_rowpad && geo == 332) halo_rows_issue_t<3, 3, 2, 8>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (p.h_rowpad && geo == 442) halo_rows_issue_t<4, 4, 2, 8>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (p.h_rows && geo == 334) halo_rows_issue_t<3, 3, 4, 8>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (p.h_rows && geo == 114) halo_rows_issue_t<1, 1, 4, 8>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (p.h_rows && geo == 332) halo_rows_issue_t<3, 3, 2, 4>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (p.h_rows && geo == 112) halo_rows_issue_t<1, 1, 2, 4>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (p.h_rows && geo == 442) halo_rows_issue_t<4, 4, 2, 4>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
             else if (geo == 334) halo_issue<3, 3, 4>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
             else if (geo == 332) halo_issue<3, 3, 2>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
             else if (geo == 331) halo_issue<3, 3, 1>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
@@ -1011,7 +1015,8 @@ int launch(GemmParams& p, cudaStream_t stream) {
     }
   }
   if (p.mode == MODE_HALO && p.h_rows)   // SW128/SW64 K-major rows: SBO = one halo row of 8-pixel groups
-    p.adesc[0] = desc_tmpl(0, 16, (uint32_t)p.h_pitch * p.h_cg * 2, layout_of(p.h_cg * 2));
+    p.adesc[0] = desc_tmpl(0, 16, (uint32_t)p.h_pitch * (p.h_rowpad ? 128 : p.h_cg * 2),
+                           layout_of(p.h_rowpad ? 128 : p.h_cg * 2));
   if (p.mode == MODE_HALO && p.h_cg == 8) {   // tap pairs: second K half = next pixel / next row
     p.adesc[0] = desc_tmpl(0, 16, (uint32_t)p.h_pitch * 16, 0);
     p.adesc[1] = desc_tmpl(0, (uint32_t)(p.h_pitch - p.h_kw + 1) * 16, (uint32_t)p.h_pitch * 16, 0);
@@ -1120,8 +1125,13 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
       if (rows32 < 0) rows32 = getenv("CVB_NO_HALO_ROWS32") ? 0 : 1;   // SW64 rows for 32-channel groups
       p.h_rows = (!no_rows && (cg == 64 || (cg == 32 && rows32)) &&
                   ((kh == 3 && kw == 3) || (kh == 1 && kw == 1) || (kh == 4 && kw == 4))) ? 1 : 0;
+      static int rowpad = -1;
+      if (rowpad < 0) rowpad = getenv("CVB_NO_ROWPAD") ? 0 : 1;
+      p.h_rowpad = (p.h_rows && rowpad && cg == 32 && cin == 32 &&
+                    ((kh == 3 && kw == 3) || (kh == 4 && kw == 4))) ? 1 : 0;
       if (p.h_rows) p.h_planes = 1;
-      p.h_box_bytes = (uint32_t)p.h_pitch * hrows * (p.h_rows ? cg * 2 : 16);
+      const int rowb = p.h_rowpad ? 128 : cg * 2;   // smem bytes per halo pixel row
+      p.h_box_bytes = (uint32_t)p.h_pitch * hrows * (p.h_rows ? rowb : 16);
       p.h_plane_stride = (p.h_box_bytes + 127) / 128 * 128;
       p.a_stage_bytes = (p.h_planes * p.h_plane_stride + 1023) / 1024 * 1024;
       p.num_kb = cin / cg;
@@ -1133,7 +1143,7 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
       p.h_mps = kh * kw * (cg / 16);   // MMAs per K-block (offsets computed in the issue loop)
       p.tx_bytes = p.h_planes * p.h_box_bytes;
       int rc;
-      if ((rc = encode_nhwc(&p.mapA[0], x, n, h, w, cin, xcs, p.h_rows ? cg : 8, p.h_pitch, hrows, 1))) return rc;
+      if ((rc = encode_nhwc(&p.mapA[0], x, n, h, w, cin, xcs, p.h_rows ? rowb / 2 : 8, p.h_pitch, hrows, 1))) return rc;
       if ((rc = encode_2d(&p.mapB[0], wt, cout, K, K, p.b_cel, p.BN))) return rc;
       p.out_mode = OUT_NHWC; p.out_f32 = y_f32; p.out = y; p.ldc = ycs; p.col_off = yoff; p.bias = bias;
       p.accum = accumulate;

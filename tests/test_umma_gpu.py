@@ -62,6 +62,17 @@ def test_conv_fwd_channel_slices():
     assert out[..., :64].abs().max().item() == 0 and out[..., 96:].abs().max().item() == 0
 
 
+@pytest.mark.parametrize("k,p", [(3, 1), (4, 2)])
+def test_conv_fwd_cin32_of_wider_buffer(k, p):
+    # 32 input channels read as zero-padded 128-byte rows (h_rowpad): the pad half must be TMA
+    # zero fill even when the buffer holds more channels past cin
+    g = torch.Generator(device="cuda").manual_seed(31 + k)
+    x_full = torch.randn(2, 16, 16, 64, device="cuda", generator=g).to(torch.bfloat16)
+    wt = (torch.randn(48, k, k, 32, device="cuda", generator=g) * 0.1).to(torch.bfloat16)
+    y = K.conv2d_fwd(x_full, wt, 1, p, out_f32=True, cin=32)
+    _close(y, _ref_conv(x_full[..., :32].contiguous(), wt, 1, p))
+
+
 @pytest.mark.parametrize("n,h,w,cin,cout,k,s,p", CONV_CASES)
 def test_conv_wgrad(n, h, w, cin, cout, k, s, p):
     g = torch.Generator(device="cuda").manual_seed(7 + n + h + cin + cout)
