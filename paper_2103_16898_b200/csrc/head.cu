@@ -223,14 +223,37 @@ __global__ void __launch_bounds__(HT) head_train_kernel(const __grid_constant__ 
 
   head_grid_sync(a.bar);
 
-  // phase 2: sum the CTA partials in CTA order
+  // phase 2: sum the CTA partials -- 32 consecutive outputs per pass of a CTA (lanes,
+  // coalesced) x 8 groups of CTAs (warps, 8 loads in flight each), groups added in fixed order
+  __shared__ float red[HT / 32][32];
   const int64_t n_out = (int64_t)HO * fin + fin + HO;
-  for (int64_t e = (int64_t)blockIdx.x * HT + threadIdx.x; e < n_out; e += (int64_t)gridDim.x * HT) {
+  const int G = (int)gridDim.x, per = (G + HT / 32 - 1) / (HT / 32);
+  const int c0 = warp * per, c1 = min(G, c0 + per);
+  for (int64_t e0 = (int64_t)blockIdx.x * 32; e0 < n_out; e0 += (int64_t)gridDim.x * 32) {
+    const int64_t e = e0 + lane;
     float s = 0.f;
-    for (int c = 0; c < (int)gridDim.x; c++) s += __ldcg(a.part + (int64_t)c * a.E + e);
-    if (e < (int64_t)HO * fin) a.dw[e] = s;
-    else if (e < (int64_t)HO * fin + fin) { if (a.dprev_b) a.dprev_b[e - (int64_t)HO * fin] = s; }
-    else a.db[e - (int64_t)HO * fin - fin] = s;
+    if (e < n_out) {
+      int c = c0;
+      for (; c + 8 <= c1; c += 8) {
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) v[j] = __ldcg(a.part + (int64_t)(c + j) * a.E + e);
+#pragma unroll
+        for (int j = 0; j < 8; j++) s += v[j];
+      }
+      for (; c < c1; c++) s += __ldcg(a.part + (int64_t)c * a.E + e);
+    }
+    red[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && e < n_out) {
+      float t = red[0][lane];
+#pragma unroll
+      for (int w = 1; w < HT / 32; w++) t += red[w][lane];
+      if (e < (int64_t)HO * fin) a.dw[e] = t;
+      else if (e < (int64_t)HO * fin + fin) { if (a.dprev_b) a.dprev_b[e - (int64_t)HO * fin] = t; }
+      else a.db[e - (int64_t)HO * fin - fin] = t;
+    }
+    __syncthreads();
   }
   if (blockIdx.x == 0) {
     __shared__ double sh[HT];

@@ -578,8 +578,13 @@ __global__ void sum_small(const float* __restrict__ x, int n, float scale, float
 }
 
 // ---- misc -------------------------------------------------------------------------------
-__global__ void reduce_splits(const float* __restrict__ part, int splits, int64_t count, float* __restrict__ out,
-                              int accumulate, float scale) {
+// Split-K reduction out[i] (+)= scale * sum_s part[s][i].  The split count of a conv wgrad is
+// large (up to 148) and its element count small, so one thread per element would be a chain
+// of `splits` dependent L2 round trips: instead a 256-thread block covers 32 consecutive
+// elements (lanes, coalesced) x 8 split groups (warps); each thread sums a contiguous range of
+// splits with 8 loads in flight, and the 8 group sums are added in fixed order (deterministic).
+__global__ void reduce_splits_flat(const float* __restrict__ part, int splits, int64_t count, float* __restrict__ out,
+                                   int accumulate, float scale) {
   CVB_PDL_PROLOGUE();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
@@ -587,6 +592,38 @@ __global__ void reduce_splits(const float* __restrict__ part, int splits, int64_
   for (int s = 0; s < splits; s++) a += part[s * count + i];
   a *= scale;
   out[i] = accumulate ? out[i] + a : a;
+}
+
+constexpr int RS_GROUPS = 8;
+__global__ void __launch_bounds__(256) reduce_splits(const float* __restrict__ part, int splits, int64_t count,
+                                                     float* __restrict__ out, int accumulate, float scale) {
+  CVB_PDL_PROLOGUE();
+  __shared__ float sh[RS_GROUPS][32];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * 32 + lane;
+  const int per = (splits + RS_GROUPS - 1) / RS_GROUPS;
+  const int s0 = grp * per, s1 = min(splits, s0 + per);
+  float a = 0.f;
+  if (i < count) {
+    int s = s0;
+    for (; s + 8 <= s1; s += 8) {
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++) v[j] = __ldcg(part + (int64_t)(s + j) * count + i);
+#pragma unroll
+      for (int j = 0; j < 8; j++) a += v[j];
+    }
+    for (; s < s1; s++) a += __ldcg(part + (int64_t)s * count + i);
+  }
+  sh[grp][lane] = a;
+  __syncthreads();
+  if (grp == 0 && i < count) {
+    float t = sh[0][lane];
+#pragma unroll
+    for (int g = 1; g < RS_GROUPS; g++) t += sh[g][lane];
+    t *= scale;
+    out[i] = accumulate ? out[i] + t : t;
+  }
 }
 
 // split-K epilogue of a dense layer: out[r][c] = act(sum_s part[s][r][c] + bias[c])
@@ -967,7 +1004,10 @@ CVB_API int cvb_softmax_xent(const float* logits, int B, int C, const int32_t* l
 
 CVB_API int cvb_reduce_splits(const float* part, int splits, int64_t count, float* out, int accumulate, float scale,
                               void* stream) {
-  cvb_launch(reduce_splits, nblocks(count), 256, 0, STREAM, part, splits, count, out, accumulate, scale);
+  if (splits >= 16)   // deep split-K (conv wgrad): split groups per element
+    cvb_launch(reduce_splits, (int)((count + 31) / 32), 256, 0, STREAM, part, splits, count, out, accumulate, scale);
+  else
+    cvb_launch(reduce_splits_flat, nblocks(count), 256, 0, STREAM, part, splits, count, out, accumulate, scale);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }

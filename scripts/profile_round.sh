@@ -23,4 +23,9 @@ timeout 900 ncu --profile-from-start off -k regex:umma_gemm -s 8 -c 1 --set full
   > gpurun_out/prof/umma_r18.log 2>&1
 timeout 900 ncu -k regex:gcm_kernel -s 1 -c 1 --set full --import-source on --clock-control none \
   -o gpurun_out/prof/gcm_open_256m python scripts/gcm_one.py 256 > gpurun_out/prof/gcm.log 2>&1
+timeout 900 ncu -k regex:gcm_kernel -s 3 -c 1 --set full --import-source on --clock-control none \
+  -o gpurun_out/prof/gcm_shard_512 python scripts/gcm_shard.py > gpurun_out/prof/gcm_shard.log 2>&1
+timeout 900 ncu --profile-from-start off -k regex:head_train -c 1 --set full --import-source on \
+  --clock-control none -o gpurun_out/prof/head_small python scripts/profile_step.py small_cnn 512 \
+  > gpurun_out/prof/head.log 2>&1
 ls -la gpurun_out/prof

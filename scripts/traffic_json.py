@@ -7,7 +7,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 KIND = {"umma_gemm_kernel": "umma_gemm", "bn_bwd_fused": "bn", "bn_fwd_fused": "bn", "bn_apply": "bn",
-        "chan_stats_partial": "bn", "bn_finalize": "bn"}
+        "chan_stats_partial": "bn", "bn_finalize": "bn", "head_train_kernel": "head", "softmax_xent_mean": "head"}
 
 
 def summarize(path):
