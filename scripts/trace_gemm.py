@@ -8,6 +8,12 @@ if which == "stem":
     x = torch.randn(512, 32, 32, 8, device="cuda").bfloat16(); w = torch.randn(32, 3, 3, 8, device="cuda").bfloat16()
     y = torch.empty(512, 32, 32, 32, device="cuda", dtype=torch.bfloat16)
     f = lambda: K.conv2d_fwd(x, w, 1, 1, out=y)
+elif which == "stemwg":
+    x = torch.randn(512, 32, 32, 8, device="cuda").bfloat16(); dy = torch.randn(512, 32, 32, 32, device="cuda").bfloat16()
+    f = lambda: K.conv2d_wgrad_partials(dy, x, 3, 3, 1, 1)
+elif which == "wg32":
+    x = torch.randn(512, 32, 32, 32, device="cuda").bfloat16(); dy = torch.randn(512, 32, 32, 32, device="cuda").bfloat16()
+    f = lambda: K.conv2d_wgrad_partials(dy, x, 3, 3, 1, 1)
 elif which == "conv64":
     x = torch.randn(512, 32, 32, 64, device="cuda").bfloat16(); w = torch.randn(64, 3, 3, 64, device="cuda").bfloat16()
     y = torch.empty(512, 32, 32, 64, device="cuda", dtype=torch.bfloat16)
