@@ -122,6 +122,10 @@ struct GemmParams {
   // MODE_HALO geometry
   int h_cin, h_cg, h_planes, h_pitch, h_pad, h_kh, h_kw;
   int h_rows;                   // 1: the halo is ONE SW128 box of 64-channel (128-byte) pixel rows
+  int h_kwbox;                  // 1: one 8-pixel-wide SW128 box per kw tap (planes = KW): every tap's
+                                //    A start is 1024-byte aligned (row-shifted SW128 starts issue at
+                                //    ~99 cycles per MMA, aligned ones at 44-64: scripts/mma_rate.py)
+  int no_epi_alt;               // planning: keep the column-split epilogue (smaller staging)
   int h_rowpad;                 // 1: 32-channel input (cin == 32) loaded as 128-byte SW128 rows whose
                                 //    upper half is TMA zero fill (SW64 operand reads run at half rate)
   int h_mps;                    // MMAs per stage (taps * cg/16)
@@ -379,6 +383,29 @@ __device__ __forceinline__ void halo_rows_issue_t(uint32_t tmem_d, uint64_t a0, 
   }
 }
 
+// kw-box halo: box kw holds the 8 x (16+KH-1) pixels the kw taps read, so tap (kh, kw) starts
+// kh*8 rows (kh KB) into box kw -- an aligned SW128 start (SBO = 1024 B)
+template <int KH, int KW, int NJ>
+__device__ __forceinline__ void halo_kw_issue(uint32_t tmem_d, uint64_t a0, uint64_t b0, uint32_t idesc,
+                                              uint32_t acc_flag, uint32_t leader, int kb, uint32_t cin16,
+                                              uint32_t slab16, uint32_t box16) {
+  uint32_t qt = (uint32_t)kb * NJ;
+#pragma unroll
+  for (int kh = 0; kh < KH; kh++) {
+#pragma unroll
+    for (int kw = 0; kw < KW; kw++) {
+      const uint64_t bt = b0 + (uint64_t)((qt >> 2) * slab16 + ((qt & 3u) << 1));
+#pragma unroll
+      for (int j = 0; j < NJ; j++) {
+        umma_bf16_el(tmem_d, a0 + (uint32_t)kw * box16 + (uint32_t)(kh * 64 + 2 * j), bt + 2u * j, idesc, acc_flag,
+                     leader);
+        acc_flag = 1u;
+      }
+      qt += cin16;
+    }
+  }
+}
+
 // Halo mode with 8 input channels (the padded RGB / grey stem): one 16-wide MMA K step
 // covers TWO taps.  The second K half of a no-swizzle K-major operand sits LBO bytes after
 // the first, so LBO = 16 B (the next pixel = the next kw tap, a0) or (pitch - KW + 1) * 16 B
@@ -487,16 +514,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
         mbar_wait(&empty[s], ph ^ 1);
         if (leader) {
-          TRACE(0, it);
+          if (!(p.dbg & 32)) TRACE(0, it);
           const uint32_t sa = smem0 + s * stage_bytes, sb = sa + a_stage;
           if (p.dbg & 2) {
             mbar_arrive(&full[s]);
           } else {
             mbar_expect_tx(&full[s], tx);
             if (p.mode == MODE_HALO) {
-              for (int j = 0; j < p.h_planes; j++)
-                tma_load_4d(&p.mapA[0], sa + j * p.h_plane_stride, &full[s], kb * p.h_cg + 8 * j, tw0 - p.h_pad,
-                            th0 - p.h_pad, tn0);
+              if (p.h_kwbox) {
+                for (int j = 0; j < p.h_planes; j++)
+                  tma_load_4d(&p.mapA[0], sa + j * p.h_plane_stride, &full[s], kb * p.h_cg, tw0 - p.h_pad + j,
+                              th0 - p.h_pad, tn0);
+              } else {
+                for (int j = 0; j < p.h_planes; j++)
+                  tma_load_4d(&p.mapA[0], sa + j * p.h_plane_stride, &full[s], kb * p.h_cg + 8 * j, tw0 - p.h_pad,
+                              th0 - p.h_pad, tn0);
+              }
             } else if (p.mode == MODE_FWD) {
               const uint32_t* tab = p.boxtab + kb * p.ga;
               for (int g = 0; g < p.ga; g++) {
@@ -551,6 +584,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       const int acc = lt & (nacc - 1);
       if (lt == 0 && p.b_res) mbar_wait(bres_full, 0);
       mbar_wait(&tempty[acc], ((lt >> p.nacc_log2) & 1) ^ 1);
+      if ((p.dbg & 32) && leader) TRACE(0, it);   // debug: slot 0 = MMA warp passed the accumulator wait
       tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * p.BN;
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -572,7 +606,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
             const uint32_t plane2 = 2u * (p.h_plane_stride >> 4), slab16 = (uint32_t)p.BN * (BK * 2 / 16);
             uint32_t acc_flag = kb > kb0 ? 1u : 0u;
             const int geo = p.h_kh * 100 + p.h_kw * 10 + (int)nj;
-            if (p.h_cg == 8) halo8_issue<3, 3>(tmem_d, a0, p.adesc[1] + sa, b0, p.idesc, leader, slab16);
+            const uint32_t box16 = p.h_plane_stride >> 4;
+            if (p.h_kwbox && geo == 334) halo_kw_issue<3, 3, 4>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16, box16);
+            else if (p.h_kwbox && geo == 332) halo_kw_issue<3, 3, 2>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16, box16);
+            else if (p.h_cg == 8) halo8_issue<3, 3>(tmem_d, a0, p.adesc[1] + sa, b0, p.idesc, leader, slab16);
             else if (p.h_rowpad && geo == 332) halo_rows_issue_t<3, 3, 2, 8>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
             else if (p.h_rowpad && geo == 442) halo_rows_issue_t<4, 4, 2, 8>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
             else if (p.h_rows && geo == 334) halo_rows_issue_t<3, 3, 4, 8>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
@@ -959,13 +996,18 @@ int launch(GemmParams& p, cudaStream_t stream) {
   // narrow tiles: more TMEM accumulators (the epilogue of tile i no longer gates the MMAs of
   // tile i+2) and alternate-tile epilogue warp groups (two tiles drain concurrently)
   p.nacc_log2 = (env_nacc >= 4 && 4 * p.BN <= 512) ? 2 : 1;
-  p.epi_alt = (p.n_epi == 8 && env_alt && p.nacc_log2 == 2) ? 1 : 0;
+  p.epi_alt = (p.n_epi == 8 && env_alt && p.nacc_log2 == 2 && !p.no_epi_alt) ? 1 : 0;
   plan_tma_store(p);
   if (!p.st_tma && p.n_epi == 8) { p.n_epi = 4; p.epi_alt = 0; plan_tma_store(p); }
   if (!p.st_tma) { p.n_epi = 4; p.epi_alt = 0; }
   p.stg_warp = p.st_tma ? 2u * 32u * (uint32_t)p.st_ch * (p.out_f32 ? 4u : 2u) : 0u;
   const uint32_t stg_bytes = p.st_tma ? (uint32_t)p.n_epi * p.stg_warp : 0u;
-  if (p.st_tma && 2 * stage_bytes + p.b_res_bytes + stg_bytes > 224u * 1024u) p.st_tma = 0;   // keep 2 stages
+  if (p.st_tma && 2 * stage_bytes + p.b_res_bytes + stg_bytes > 224u * 1024u) {   // keep 2 stages: direct stores
+    p.st_tma = 0;
+    p.n_epi = 4;      // the direct-store epilogue is one warp per TMEM lane quarter, all columns
+    p.epi_alt = 0;
+    p.stg_warp = 0;
+  }
   if (p.out_par && !p.st_tma) { cvb_set_error("parity output needs the TMA-store epilogue"); return CVB_EINVAL; }
   const uint32_t stg = p.st_tma ? stg_bytes : 0u;
   p.stages = (int)((224u * 1024u - p.b_res_bytes - stg) / stage_bytes);
@@ -1014,7 +1056,9 @@ int launch(GemmParams& p, cudaStream_t stream) {
       p.bdesc[k] = desc_tmpl(row * R, R, 8 * R, layout_of((int)R));
     }
   }
-  if (p.mode == MODE_HALO && p.h_rows)   // SW128/SW64 K-major rows: SBO = one halo row of 8-pixel groups
+  if (p.mode == MODE_HALO && p.h_rows && p.h_kwbox)   // kw boxes: plain SW128 K-major, 8-row groups 1 KB apart
+    p.adesc[0] = desc_tmpl(0, 16, 1024, 2u);
+  else if (p.mode == MODE_HALO && p.h_rows)   // SW128/SW64 K-major rows: SBO = one halo row of 8-pixel groups
     p.adesc[0] = desc_tmpl(0, 16, (uint32_t)p.h_pitch * (p.h_rowpad ? 128 : p.h_cg * 2),
                            layout_of(p.h_rowpad ? 128 : p.h_cg * 2));
   if (p.mode == MODE_HALO && p.h_cg == 8) {   // tap pairs: second K half = next pixel / next row
@@ -1118,7 +1162,9 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
       p.splits = 1;
       p.h_cin = cin; p.h_cg = cg; p.h_planes = cg >= 8 ? cg / 8 : 1; p.h_pad = pad; p.h_kh = kh; p.h_kw = kw;
       p.h_pitch = 8 + kw - 1 + (cg == 8 ? 1 : 0);   // tap pairs read one pixel past the last tap
-      const int hrows = 16 + kh - 1;
+      static int dbg_rows = -1;   // profiling knob CVB_HALO_DBG_ROWS: load only this many halo rows (results invalid)
+      if (dbg_rows < 0) { const char* e = getenv("CVB_HALO_DBG_ROWS"); dbg_rows = e ? atoi(e) : 0; }
+      const int hrows = dbg_rows > 0 ? dbg_rows : 16 + kh - 1;
       static int no_rows = -1;
       if (no_rows < 0) no_rows = getenv("CVB_NO_HALO_ROWS") ? 1 : 0;
       static int rows32 = -1;
@@ -1134,6 +1180,23 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
       p.h_box_bytes = (uint32_t)p.h_pitch * hrows * (p.h_rows ? rowb : 16);
       p.h_plane_stride = (p.h_box_bytes + 127) / 128 * 128;
       p.a_stage_bytes = (p.h_planes * p.h_plane_stride + 1023) / 1024 * 1024;
+      static int kwbox = -1;
+      if (kwbox < 0) kwbox = getenv("CVB_NO_KWBOX") ? 0 : 1;
+      // (64-channel groups only: for the zero-padded 32-channel rows the 3x box writes cost more
+      // than the aligned starts save -- measured conv 32->32 28.8 -> 29.3 us)
+      if (kwbox && p.h_rows && !p.h_rowpad && rowb == 128 && kh == 3 && kw == 3) {
+        const uint32_t box = 8u * (uint32_t)hrows * 128u, stride = (box + 1023) / 1024 * 1024;
+        const uint32_t a_stage = (uint32_t)kw * stride;
+        if (2 * a_stage + b_all + 32u * 1024u <= 224u * 1024u) {
+          p.h_kwbox = 1;
+          p.h_pitch = 8;
+          p.h_planes = kw;
+          p.h_box_bytes = box;
+          p.h_plane_stride = stride;
+          p.a_stage_bytes = a_stage;
+          p.no_epi_alt = 2 * a_stage + b_all + 64u * 1024u > 224u * 1024u;
+        }
+      }
       p.num_kb = cin / cg;
       p.kb_per_split = p.num_kb;
       p.OH = oh; p.OW = ow; p.NIMG = n;
@@ -1509,7 +1572,27 @@ __global__ void __launch_bounds__(96, 1) mma_rate_kernel(int n_mma, int bn, int 
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(bn >> 3) << 17) | (8u << 24);
     long long t0 = clock64();
     if (leader) {
-      if (a_halo == 2) {   // the halo conv's exact 3x3 x 2-plane offset sequence, 2 accumulators
+      if (a_halo >= 5) {
+        // one issuer alternating between two accumulators (two independent chains);
+        // 5 = SW128 aligned A, 6 = row-shifted SW128 halo A, 7 = four accumulators aligned
+        const uint64_t dr = ((uint64_t)1 << 16) | ((uint64_t)(1280 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+        const int nch = a_halo == 7 ? 4 : 2;
+        for (int i = 0; i < n_mma; i++) {
+          const int t = (i >> 1) % 9, j = i & 1;
+          const uint32_t aoff = (a_halo == 6 ? (uint32_t)((t / 3) * 10 + t % 3) * 8u : 0u) + (uint32_t)j * 2u;
+          umma_bf16(tmem + (uint32_t)(i % nch) * (uint32_t)bn, (a_halo == 6 ? dr : d0) + sa + aoff, d0 + sb + j * 2,
+                    idesc, i >= nch ? 1u : 0u);
+        }
+      } else if (a_halo == 3 || a_halo == 4) {
+        // SW128 halo rows (pitch 10 pixels of 128 B, SBO = 1280 B): 3 = the rowpad conv's
+        // row-shifted 3x3 start sequence, 4 = the same descriptors without the row shift
+        const uint64_t dr = ((uint64_t)1 << 16) | ((uint64_t)(1280 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+        for (int i = 0; i < n_mma; i++) {
+          const int t = (i >> 1) % 9, j = i & 1;
+          const uint32_t aoff = (a_halo == 3 ? (uint32_t)((t / 3) * 10 + t % 3) * 8u : 0u) + (uint32_t)j * 2u;
+          umma_bf16(tmem + ((i / 18) & 1) * 32u, dr + sa + aoff, d0 + sb + j * 2, idesc, (i % 18) ? 1u : 0u);
+        }
+      } else if (a_halo == 2) {   // the halo conv's exact 3x3 x 2-plane offset sequence, 2 accumulators
         for (int i = 0; i < n_mma; i++) {
           const int t = (i >> 1) % 9, j = i & 1;
           const uint32_t aoff = (uint32_t)((t / 3) * 10 + t % 3) + (uint32_t)j * 368u;
