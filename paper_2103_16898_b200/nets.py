@@ -27,6 +27,15 @@ from . import kernels as K
 
 BF16, F32 = torch.bfloat16, torch.float32
 _UNFUSED_HEAD = os.environ.get("CVB_UNFUSED_HEAD", "0") not in ("", "0")
+_NO_OVERLAP = os.environ.get("CVB_NO_OVERLAP", "0") not in ("", "0")
+
+
+class _nullctx:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *a):
+        return False
 ALIGN = 64  # elements; keeps every parameter view 128-byte aligned (TMA needs 16 B)
 
 
@@ -41,6 +50,8 @@ class ParamStore:
         self.specs = []      # (name, shape, init cpu tensor)
         self.logical = 0     # parameter count without layout padding
         self.grad_hook = None   # data parallelism: called with parameter names whose grads are final
+        self.side = None        # single GPU: stream the conv weight gradients run on, beside the dgrads
+        self.side_used = False
 
     def grad_ready(self, *names):
         """Backward marks parameters whose gradients are final (launches bucket all-reduces)."""
@@ -216,12 +227,20 @@ class ConvBN:
             return
         count = self.cout * self.k * self.k * cin
         maxs = max(1, min(MAX_SPLITS, self.scratch.part.numel() // count))
-        part, used = K.conv2d_wgrad_partials(self.dz, x, self.k, self.k, self.s, self.pad, cin=cin,
-                                             part=self.scratch.part[:maxs * count].view(maxs, self.cout,
-                                                                                        self.k * self.k * cin),
-                                             acct_flops=self.flops)
-        K.reduce_splits(part, used, count, ps.g[self.W])
-        ps.grad_ready(self.W, self.G, self.B)
+        # single GPU: the weight gradient (split-K wgrad + reduction) runs on the side stream while
+        # the dgrad and the next layer's BN backward proceed (both only need dz); the side stream
+        # serialises the wgrads, so the shared split-K scratch is never used by two at once
+        side = ps.side if dx is not None else None
+        if side is not None:
+            side.wait_stream(torch.cuda.current_stream())
+            ps.side_used = True
+        with torch.cuda.stream(side) if side is not None else _nullctx():
+            part, used = K.conv2d_wgrad_partials(self.dz, x, self.k, self.k, self.s, self.pad, cin=cin,
+                                                 part=self.scratch.part[:maxs * count].view(maxs, self.cout,
+                                                                                            self.k * self.k * cin),
+                                                 acct_flops=self.flops)
+            K.reduce_splits(part, used, count, ps.g[self.W])
+            ps.grad_ready(self.W, self.G, self.B)
         if dx is not None:
             wt = self.scratch.flip[:self.cout * self.k * self.k * cin].view(cin, self.k, self.k, self.cout)
             if self.s == 2 and cin == self.cin and K.conv2d_dgrad_s2(self.dz, ps.b[self.W], self.pad, dx,
@@ -292,17 +311,23 @@ class Linear:
     def backward(self, ps, dy, x, dx=None, bias_grad=True):
         B = x.shape[0]
         fl = 2 * B * self.fout * self.fin
-        if self.s_wg > 1:
-            part = self.scratch.part[:self.s_wg * self.fpad * self.fin].view(self.s_wg, self.fpad, self.fin)
-            K.gemm(dy, x, self.fpad, self.fin, B, 1, 1, out=part, splits=self.s_wg, acct_flops=fl)
-            used = K.splits_used(B, self.s_wg)
-            K.reduce_splits(part, used, self.fpad * self.fin, ps.g[self.W])
-        else:
-            # unsplit wgrad: 64-column N tiles so the (m, n) tiles fill the SMs
-            K.gemm(dy, x, self.fpad, self.fin, B, 1, 1, out=ps.g[self.W], out_f32=True, acct_flops=fl, max_bn=64)
-        if bias_grad:
-            K.col_sum(dy, B, self.fpad, self.fpad, ps.g[self.Bn])
-        ps.grad_ready(self.W, self.Bn)
+        side = ps.side if dx is not None else None   # weight gradient beside the dgrad (ConvBN.backward)
+        if side is not None:
+            side.wait_stream(torch.cuda.current_stream())
+            ps.side_used = True
+        with torch.cuda.stream(side) if side is not None else _nullctx():
+            if self.s_wg > 1:
+                part = self.scratch.part[:self.s_wg * self.fpad * self.fin].view(self.s_wg, self.fpad, self.fin)
+                K.gemm(dy, x, self.fpad, self.fin, B, 1, 1, out=part, splits=self.s_wg, acct_flops=fl)
+                used = K.splits_used(B, self.s_wg)
+                K.reduce_splits(part, used, self.fpad * self.fin, ps.g[self.W])
+            else:
+                # unsplit wgrad: 64-column N tiles so the (m, n) tiles fill the SMs
+                K.gemm(dy, x, self.fpad, self.fin, B, 1, 1, out=ps.g[self.W], out_f32=True, acct_flops=fl,
+                       max_bn=64)
+            if bias_grad:
+                K.col_sum(dy, B, self.fpad, self.fpad, ps.g[self.Bn])
+            ps.grad_ready(self.W, self.Bn)
         if dx is not None:
             K.gemm(dy, ps.b[self.W], B, self.fin, self.fpad, 0, 1, out=dx, acct_flops=fl, max_bn=128)
 
@@ -359,6 +384,22 @@ class Net:
 
     def fwd_bwd(self, x, labels):
         """Forward, loss and backward of one step (gradients in ps.g32, loss in self.loss)."""
+        ps = self.ps
+        # wgrad/dgrad overlap on a side stream: single GPU only (the data-parallel capture is cut
+        # into per-bucket graph segments, which must not end with side-stream work outstanding)
+        ps.side, ps.side_used = None, False
+        if not _NO_OVERLAP and ps.grad_hook is None and torch.cuda.is_available():
+            if getattr(self, "_side", None) is None:
+                self._side = torch.cuda.Stream()
+            ps.side = self._side
+        try:
+            self._fwd_bwd(x, labels)
+        finally:
+            if ps.side_used:   # join only a stream that was forked from this one (graph capture)
+                torch.cuda.current_stream().wait_stream(ps.side)
+            ps.side, ps.side_used = None, False
+
+    def _fwd_bwd(self, x, labels):
         if not self.fused_head:
             self.forward(x)
             self.loss_and_grad(labels)

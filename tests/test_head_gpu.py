@@ -116,3 +116,22 @@ def test_fused_head_matches_unfused_step(model, batch):
         b.step(x, lab)
     torch.cuda.synchronize()
     assert abs(a.loss.item() - b.loss.item()) < 1e-2 * max(1.0, abs(b.loss.item()))
+
+
+@pytest.mark.parametrize("model,batch", [("small_cnn", 128), ("resnet18", 32)])
+def test_wgrad_side_stream_overlap_is_bit_exact(model, batch, monkeypatch):
+    """Weight gradients on the side stream (single GPU) == the serial order, bit for bit."""
+    from tests.cnn_parity import gpu_inputs, make_records
+    from paper_2103_16898_b200 import loader
+    a = nets.make_model(model, seed=5).build(batch)
+    b = nets.make_model(model, seed=5).build(batch)
+    rec = make_records(batch, 9, c=3, h=32, w=32, classes=a.num_classes)
+    x, lab = gpu_inputs(rec, loader.CIFAR)
+    monkeypatch.setattr(nets, "_NO_OVERLAP", False)
+    a.fwd_bwd(x, lab)
+    assert a.ps.side is None and a._side is not None   # the side stream was used and joined
+    monkeypatch.setattr(nets, "_NO_OVERLAP", True)
+    b.fwd_bwd(x, lab)
+    torch.cuda.synchronize()
+    assert torch.equal(a.ps.g32, b.ps.g32)
+    assert torch.equal(a.loss, b.loss)
