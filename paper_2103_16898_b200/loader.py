@@ -46,6 +46,17 @@ def decode_records(pt_dev: torch.Tensor, nrec: int, c: int, h: int, w: int, mean
     return out, labels
 
 
+
+def _pinned(b: bytes) -> torch.Tensor:
+    """bytes -> page-locked uint8 tensor.  An H2D copy from pageable memory is staged
+    synchronously by the driver (and can wait on the copy stream's pending work); from
+    page-locked memory it is a true async DMA.  torch's caching host allocator keeps the
+    block alive until the copy that reads it has completed."""
+    t = torch.empty(len(b), dtype=torch.uint8, pin_memory=True)
+    if len(b):
+        t.numpy()[:] = memoryview(b)
+    return t
+
 class ShardSet:
     """Sealed shards of one volume, held as pinned host ciphertext (the e2e input)."""
 
@@ -82,7 +93,7 @@ class ShardLoader:
         """H2D copy of one sealed shard (async on the current stream)."""
         n = blob_host.numel()
         self.ct[:n].copy_(blob_host, non_blocking=True)
-        self.aad[:len(aad)].copy_(torch.frombuffer(bytearray(aad), dtype=torch.uint8), non_blocking=True)
+        self.aad[:len(aad)].copy_(_pinned(aad), non_blocking=True)
         self.n, self.aad_len = n, len(aad)
 
     # -- double-buffered host->device staging (the e2e path overlaps the next shard's H2D
@@ -100,7 +111,7 @@ class ShardLoader:
         self.copy_stream.wait_event(self.buf_free)       # the spare buffer's last reader is done
         with torch.cuda.stream(self.copy_stream):
             self.ct_next[:n].copy_(blob_host, non_blocking=True)
-            self.aad_next[:len(aad)].copy_(torch.frombuffer(bytearray(aad), dtype=torch.uint8), non_blocking=True)
+            self.aad_next[:len(aad)].copy_(_pinned(aad), non_blocking=True)
         self.copy_done.record(self.copy_stream)
         self.next_n, self.next_aad_len = n, len(aad)
         self.next_src = blob_host.data_ptr()

@@ -206,7 +206,9 @@ class EncryptedTrainer:
         self.graph = True
         self.net.ps.step_dev.zero_()
 
-    def _run_train(self):
+    def _run_train(self, after_train=None):
+        """after_train: host callback issued between the forward/backward and the optimiser
+        (the e2e path's D2H of loss + verdict, whose latency then hides behind the optimiser)."""
         ar = self.allreduce
         if self.graph:
             for g, idx in self.segments:
@@ -218,20 +220,39 @@ class EncryptedTrainer:
                 for i in range(self.tail_from, len(ar.buckets)):
                     ar.launch_bucket(i)
                 ar.join()
+            if after_train is not None:
+                after_train()
             self.g_opt.replay()
         else:
             self._train_body()
             if ar is not None:
                 ar.finish()
+            if after_train is not None:
+                after_train()
             self._opt_body()
 
-    def step_resident(self, ct_dev: torch.Tensor, nonce: bytes, aad_dev: torch.Tensor, nrec: int):
+    def step_resident(self, ct_dev: torch.Tensor, nonce: bytes, aad_dev: torch.Tensor, nrec: int,
+                      after_train=None):
         """Ciphertext already in HBM: GCM open + decode + train.  Returns the device loss."""
+        d2h = getattr(self, "d2h_done", None)
+        if d2h is not None:   # the previous step's D2H has read the loss and the verdict
+            torch.cuda.current_stream().wait_event(d2h)
         # fused decrypt-and-normalise: ciphertext -> bf16 tile + labels, tag checked on the device
         self.ctx.open_records_device(nonce, aad_dev, ct_dev, self.loader.x, self.loader.labels, self.loader.work,
                                      self.spec)
-        self._run_train()
+        self._run_train(after_train)
         return self.net.loss
+
+    def _issue_d2h(self):
+        """D2H of the step's loss and tag verdict on a side stream (after forward/backward)."""
+        if getattr(self, "d2h_stream", None) is None:
+            self.d2h_stream = torch.cuda.Stream()
+            self.d2h_done = torch.cuda.Event()
+        self.d2h_stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.d2h_stream):
+            self.loss_host.copy_(self.net.loss, non_blocking=True)
+            self.status_host[:1].copy_(self.loader.work[4:5], non_blocking=True)
+        self.d2h_done.record(self.d2h_stream)
 
     def step_host(self, blob_host: torch.Tensor, nonce: bytes, aad: bytes, nrec: int, next_blob=None,
                   next_aad: bytes | None = None):
@@ -248,15 +269,15 @@ class EncryptedTrainer:
             ct, aad_dev = ld.ct[:ld.n], ld.aad[:ld.aad_len]
         if next_blob is not None:
             ld.prefetch(next_blob, next_aad)
-        self.step_resident(ct, nonce, aad_dev, nrec)
+        self.step_resident(ct, nonce, aad_dev, nrec, after_train=self._issue_d2h)
         ld.release_spare()
-        self.loss_host.copy_(self.net.loss, non_blocking=True)
-        self.status_host[:1].copy_(ld.work[4:5], non_blocking=True)
         return self.loss_host
 
     def check_status(self):
         """Raise if the last shard's tag failed (its plaintext was zeroed on the device)."""
         torch.cuda.current_stream().synchronize()
+        if getattr(self, "d2h_done", None) is not None:
+            self.d2h_done.synchronize()
         if int(self.status_host[0]) != 0:
             raise AuthenticationFailure("training shard failed authentication")
 
