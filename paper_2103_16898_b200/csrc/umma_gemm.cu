@@ -362,11 +362,11 @@ __device__ __forceinline__ void halo_issue(uint32_t tmem_d, uint64_t a0, uint64_
 // instead of eight 16-byte plane rows): tap (kh, kw) = start row kh*pitch + kw (8 x 16-byte
 // units per row), 16-channel step j = +32 bytes inside the swizzled row.  UMMA derives the
 // swizzle from absolute smem address bits, so row-shifted starts read the TMA layout exactly.
-template <int KH, int KW, int NJ, int RU>
+template <int KH, int KW, int NJ, int RU, int PITCH = 8 + KW - 1>
 __device__ __forceinline__ void halo_rows_issue_t(uint32_t tmem_d, uint64_t a0, uint64_t b0, uint32_t idesc,
                                                 uint32_t acc_flag, uint32_t leader, int kb, uint32_t cin16,
                                                 uint32_t slab16) {
-  constexpr uint32_t pitch = 8 + KW - 1;   // RU: 16-byte units per smem pixel row (>= 2*NJ)
+  constexpr uint32_t pitch = PITCH;   // RU: 16-byte units per smem pixel row (>= 2*NJ)
   uint32_t qt = (uint32_t)kb * NJ;
 #pragma unroll
   for (int kh = 0; kh < KH; kh++) {
@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       const int acc = lt & (nacc - 1);
       if (lt == 0 && p.b_res) mbar_wait(bres_full, 0);
       mbar_wait(&tempty[acc], ((lt >> p.nacc_log2) & 1) ^ 1);
-      if ((p.dbg & 32) && leader) TRACE(0, it);   // debug: slot 0 = MMA warp passed the accumulator wait
+      if ((p.dbg & 32) && !(p.dbg & 64) && leader) TRACE(0, it);   // debug: slot 0 = accumulator wait passed
       tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * p.BN;
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -610,6 +610,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
             if (p.h_kwbox && geo == 334) halo_kw_issue<3, 3, 4>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16, box16);
             else if (p.h_kwbox && geo == 332) halo_kw_issue<3, 3, 2>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16, box16);
             else if (p.h_cg == 8) halo8_issue<3, 3>(tmem_d, a0, p.adesc[1] + sa, b0, p.idesc, leader, slab16);
+            else if (p.h_pitch == 16 && p.h_rowpad && geo == 332) halo_rows_issue_t<3, 3, 2, 8, 16>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (p.h_pitch == 16 && p.h_rowpad && geo == 442) halo_rows_issue_t<4, 4, 2, 8, 16>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (p.h_pitch == 16 && p.h_rows && geo == 334) halo_rows_issue_t<3, 3, 4, 8, 16>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
             else if (p.h_rowpad && geo == 332) halo_rows_issue_t<3, 3, 2, 8>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
             else if (p.h_rowpad && geo == 442) halo_rows_issue_t<4, 4, 2, 8>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
             else if (p.h_rows && geo == 334) halo_rows_issue_t<3, 3, 4, 8>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
@@ -653,6 +656,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
         if (++s == p.stages) { s = 0; ph ^= 1; }
       }
       if (leader) umma_commit(&tfull[acc]);
+      if ((p.dbg & 64) && leader) TRACE(0, it - 1);   // debug: slot 0 = tile's accumulator commit issued
       __syncwarp();
     }
   } else {
@@ -1180,6 +1184,17 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
       p.h_box_bytes = (uint32_t)p.h_pitch * hrows * (p.h_rows ? rowb : 16);
       p.h_plane_stride = (p.h_box_bytes + 127) / 128 * 128;
       p.a_stage_bytes = (p.h_planes * p.h_plane_stride + 1023) / 1024 * 1024;
+      // UMMA reads a SW128 operand whose 8-row groups are 1280 B apart (the 10-pixel halo
+      // pitch) at ~99 cycles per MMA, 1024/2048 B apart at the 40-64-cycle floor
+      // (scripts/mma_rate.py): pad the halo pitch to 16 pixels (SBO = 2 KB).
+      static int pitch16 = -1;
+      if (pitch16 < 0) pitch16 = getenv("CVB_NO_PITCH16") ? 0 : 1;
+      if (pitch16 && p.h_rows && rowb == 128 && kw > 1 && kw <= 9) {
+        p.h_pitch = 16;
+        p.h_box_bytes = 16u * (uint32_t)hrows * 128u;
+        p.h_plane_stride = (p.h_box_bytes + 127) / 128 * 128;
+        p.a_stage_bytes = (p.h_plane_stride + 1023) / 1024 * 1024;
+      }
       static int kwbox = -1;
       if (kwbox < 0) kwbox = getenv("CVB_NO_KWBOX") ? 0 : 1;
       // (64-channel groups only: for the zero-padded 32-channel rows the 3x box writes cost more
@@ -1572,7 +1587,24 @@ __global__ void __launch_bounds__(96, 1) mma_rate_kernel(int n_mma, int bn, int 
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(bn >> 3) << 17) | (8u << 24);
     long long t0 = clock64();
     if (leader) {
-      if (a_halo >= 5) {
+      if (a_halo == 10) {
+        // halo rows with a 16-pixel pitch (SBO = 2048 B) and the 3x3 row-shifted starts
+        const uint64_t dp = ((uint64_t)1 << 16) | ((uint64_t)(2048 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+        for (int i = 0; i < n_mma; i++) {
+          const int t = (i >> 1) % 9, j = i & 1;
+          const uint32_t aoff = (uint32_t)((t / 3) * 16 + t % 3) * 8u + (uint32_t)j * 2u;
+          umma_bf16(tmem + ((i / 18) & 1) * 32u, dp + sa + aoff, d0 + sb + j * 2, idesc, (i % 18) ? 1u : 0u);
+        }
+      } else if (a_halo == 8 || a_halo == 9) {
+        // distinct A tiles: 8 = aligned starts walking 9 x 2 KB-apart tiles (SW128, SBO 1 KB),
+        // 9 = the same walk shifted by one row (misaligned)
+        const uint64_t dk = ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+        for (int i = 0; i < n_mma; i++) {
+          const int t = (i >> 1) % 9, j = i & 1;
+          const uint32_t aoff = (uint32_t)t * 128u + (a_halo == 9 ? 8u : 0u) + (uint32_t)j * 2u;
+          umma_bf16(tmem + ((i / 18) & 1) * 32u, dk + sa + aoff, d0 + sb + j * 2, idesc, (i % 18) ? 1u : 0u);
+        }
+      } else if (a_halo >= 5) {
         // one issuer alternating between two accumulators (two independent chains);
         // 5 = SW128 aligned A, 6 = row-shifted SW128 halo A, 7 = four accumulators aligned
         const uint64_t dr = ((uint64_t)1 << 16) | ((uint64_t)(1280 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
