@@ -313,8 +313,12 @@ def run_ours(args, rank, world, local_rank):
     K.REC.timing, K.REC.records = True, []
     l0 = K.REC.launches
     tr.graph = None
+    from paper_2103_16898_b200 import nets as _nets
+    overlap = _nets._NO_OVERLAP
+    _nets._NO_OVERLAP = True   # per-launch events need the launches serial (no side-stream wgrads)
     resident(0)
     torch.cuda.synchronize()
+    _nets._NO_OVERLAP = overlap
     per_step_eager = K.REC.launches - l0
     K.REC.timing = False
     summ = K.REC.summary()
