@@ -14,10 +14,12 @@ are per rank (DDP default).
 from __future__ import annotations
 
 import json
+import os
 import struct
 import warnings
 
 import numpy as np
+
 import torch
 
 from . import kernels as K
@@ -27,6 +29,9 @@ from .nets import make_model
 
 CNN_MAGIC = b"CVC1"
 
+
+
+_NO_PREFETCH = os.environ.get("CVB_NO_DECRYPT_PREFETCH", "0") not in ("", "0")
 
 class GradAllReduce:
     """Bucketed NCCL all-reduce of the flat fp32 gradient buffer (~bucket_mb per bucket,
@@ -232,16 +237,63 @@ class EncryptedTrainer:
             self._opt_body()
 
     def step_resident(self, ct_dev: torch.Tensor, nonce: bytes, aad_dev: torch.Tensor, nrec: int,
-                      after_train=None):
-        """Ciphertext already in HBM: GCM open + decode + train.  Returns the device loss."""
+                      after_train=None, next_shard=None):
+        """Ciphertext already in HBM: GCM open + decode + train.  Returns the device loss.
+
+        ``next_shard = (ct_dev, nonce, aad_dev)`` of the following step: with a captured step its
+        decrypt is issued on a side stream as soon as this step's forward/backward no longer
+        needs the input tile, so it runs beside the optimiser; the next call with that shard
+        then skips its decrypt.  Each shard's tag verdict lands in its own work buffer."""
+        main = torch.cuda.current_stream()
         d2h = getattr(self, "d2h_done", None)
         if d2h is not None:   # the previous step's D2H has read the loss and the verdict
-            torch.cuda.current_stream().wait_event(d2h)
-        # fused decrypt-and-normalise: ciphertext -> bf16 tile + labels, tag checked on the device
-        self.ctx.open_records_device(nonce, aad_dev, ct_dev, self.loader.x, self.loader.labels, self.loader.work,
-                                     self.spec)
-        self._run_train(after_train)
+            main.wait_event(d2h)
+        key = (ct_dev.data_ptr(), ct_dev.numel(), bytes(nonce))
+        pend = getattr(self, "_pend", None)
+        if pend is not None:
+            main.wait_event(self._pend_ev)   # the prefetched decrypt has written the tile
+            self._pend = None
+        if pend is not None and pend[0] == key:
+            self._wcur = pend[1]
+        else:
+            # fused decrypt-and-normalise: ciphertext -> bf16 tile + labels, tag checked on the device
+            self._wcur = self._wnext()
+            self.ctx.open_records_device(nonce, aad_dev, ct_dev, self.loader.x, self.loader.labels,
+                                         self._works[self._wcur], self.spec)
+
+        def after():
+            if after_train is not None:
+                after_train()
+            if next_shard is not None and self.graph and not _NO_PREFETCH:
+                self._prefetch_decrypt(*next_shard)
+
+        self._run_train(after)
         return self.net.loss
+
+    @property
+    def _works(self):
+        if getattr(self, "_work_pair", None) is None:
+            self._work_pair = [self.loader.work, self.ctx.new_workspace(self.loader.work.device)]
+        return self._work_pair
+
+    def _wnext(self):
+        return (getattr(self, "_wcur", 1) + 1) % 2
+
+    def _prefetch_decrypt(self, ct_dev, nonce, aad_dev, wait_event=None):
+        """Decrypt the next shard into the input tile on the decrypt stream (after this step's
+        backward: the tile's last readers are done)."""
+        if getattr(self, "dstream", None) is None:
+            self.dstream = torch.cuda.Stream()
+            self._pend_ev = torch.cuda.Event()
+        self.dstream.wait_stream(torch.cuda.current_stream())
+        if wait_event is not None:
+            self.dstream.wait_event(wait_event)
+        w = self._wnext()
+        with torch.cuda.stream(self.dstream):
+            self.ctx.open_records_device(nonce, aad_dev, ct_dev, self.loader.x, self.loader.labels, self._works[w],
+                                         self.spec)
+        self._pend_ev.record(self.dstream)
+        self._pend = ((ct_dev.data_ptr(), ct_dev.numel(), bytes(nonce)), w)
 
     def _issue_d2h(self):
         """D2H of the step's loss and tag verdict on a side stream (after forward/backward)."""
@@ -251,11 +303,11 @@ class EncryptedTrainer:
         self.d2h_stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(self.d2h_stream):
             self.loss_host.copy_(self.net.loss, non_blocking=True)
-            self.status_host[:1].copy_(self.loader.work[4:5], non_blocking=True)
+            self.status_host[:1].copy_(self._works[self._wcur][4:5], non_blocking=True)
         self.d2h_done.record(self.d2h_stream)
 
     def step_host(self, blob_host: torch.Tensor, nonce: bytes, aad: bytes, nrec: int, next_blob=None,
-                  next_aad: bytes | None = None):
+                  next_aad: bytes | None = None, next_nonce: bytes | None = None):
         """End-to-end step from pinned host ciphertext: H2D, decrypt, train, D2H of loss+status.
 
         With ``next_blob``/``next_aad`` (the following shard) the next H2D copy is issued on a
@@ -269,7 +321,14 @@ class EncryptedTrainer:
             ct, aad_dev = ld.ct[:ld.n], ld.aad[:ld.aad_len]
         if next_blob is not None:
             ld.prefetch(next_blob, next_aad)
-        self.step_resident(ct, nonce, aad_dev, nrec, after_train=self._issue_d2h)
+        after = self._issue_d2h
+        if next_blob is not None and next_nonce is not None and self.graph and not _NO_PREFETCH:
+            # also decrypt the next shard beside this step's optimiser, once its H2D copy is in
+            def after():
+                self._issue_d2h()
+                self._prefetch_decrypt(ld.ct_next[:ld.next_n], next_nonce, ld.aad_next[:ld.next_aad_len],
+                                       wait_event=ld.copy_done)
+        self.step_resident(ct, nonce, aad_dev, nrec, after_train=after)
         ld.release_spare()
         return self.loss_host
 
