@@ -202,6 +202,7 @@ struct BwdArgs {
   const float* mean; const float* rstd; const float* gamma; const float* beta; int relu;
   float* part; unsigned* bar; float* dgamma; float* dbeta;
   bf16* dx; int dxcs; float* dx32; int accum32; bf16* dz_out;
+  int two_rows;              // pass 2: two rows' raw loads in flight (CVB_BN_BWD_ONE_ROW=1: off)
 };
 
 // Per-channel constants live in shared memory (8 consecutive floats per channel group, two
@@ -241,6 +242,39 @@ __device__ __forceinline__ void bwd_load(const BwdArgs& a, int64_t r, int g, con
       for (int k = 0; k < 8; k++) if (!(xh[k] * ga[k] + be[k] > 0.f)) d[k] = 0.f;
     }
   }
+}
+
+// pass-2 body for one row from raw loads: dz = dy * relu-mask(x), dx = gamma*rstd*(dz - mean(dz)
+// - xhat*mean(dz*xhat)) (same arithmetic as bwd_load + the generic loop)
+__device__ __forceinline__ void bwd_apply_raw(const BwdArgs& a, const ChanSmem& cs, const float* sh, int C, int g,
+                                              const uint4& ud, const uint4& ux, bf16* dst) {
+  float d[8], xv[8], mu[8], rs[8];
+  const __nv_bfloat162* hd = reinterpret_cast<const __nv_bfloat162*>(&ud);
+  const __nv_bfloat162* hx = reinterpret_cast<const __nv_bfloat162*>(&ux);
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const float2 fd = __bfloat1622float2(hd[i]), fx = __bfloat1622float2(hx[i]);
+    d[2 * i] = fd.x; d[2 * i + 1] = fd.y; xv[2 * i] = fx.x; xv[2 * i + 1] = fx.y;
+  }
+  lds8(cs.mu + g * 8, mu);
+  lds8(cs.rs + g * 8, rs);
+  float xh[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) xh[k] = (xv[k] - mu[k]) * rs[k];
+  if (a.relu) {
+    float ga[8], be[8];
+    lds8(cs.ga + g * 8, ga);
+    lds8(cs.be + g * 8, be);
+#pragma unroll
+    for (int k = 0; k < 8; k++) if (!(xh[k] * ga[k] + be[k] > 0.f)) d[k] = 0.f;
+  }
+  float kk[8], kb[8], kg[8], o[8];
+  lds8(sh + g * 8, kk);
+  lds8(sh + C + g * 8, kb);
+  lds8(sh + 2 * C + g * 8, kg);
+#pragma unroll
+  for (int k = 0; k < 8; k++) o[k] = kk[k] * (d[k] - kb[k] - xh[k] * kg[k]);
+  st8(dst, o);
 }
 
 __global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
@@ -296,7 +330,20 @@ __global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
   }
   __syncthreads();
   if (rl >= RL) return;
-  for (int64_t r = r0 + rl; r < r1; r += RL) {
+  int64_t r = r0 + rl;
+  if (a.two_rows && !a.dx32 && !a.y) {
+    // bf16 dx, mask recomputed from x: two rows' raw 16-byte loads in flight per thread (the
+    // pass is load-latency bound), converted one row at a time (stays within 64 registers)
+    for (; r + RL < r1; r += 2 * RL) {
+      const uint4 ud0 = __ldcg(reinterpret_cast<const uint4*>(a.dy + r * a.dycs + g * 8));
+      const uint4 ux0 = __ldcg(reinterpret_cast<const uint4*>(a.x + r * a.xcs + g * 8));
+      const uint4 ud1 = __ldcg(reinterpret_cast<const uint4*>(a.dy + (r + RL) * a.dycs + g * 8));
+      const uint4 ux1 = __ldcg(reinterpret_cast<const uint4*>(a.x + (r + RL) * a.xcs + g * 8));
+      bwd_apply_raw(a, cs, sh, C, g, ud0, ux0, a.dx + r * a.dxcs + g * 8);
+      bwd_apply_raw(a, cs, sh, C, g, ud1, ux1, a.dx + (r + RL) * a.dxcs + g * 8);
+    }
+  }
+  for (; r < r1; r += RL) {
     float d[8], xh[8], o[8], kk[8], kb[8], kg[8];
     bwd_load(a, r, g, cs, d, xh);
     lds8(sh + g * 8, kk);
@@ -361,6 +408,12 @@ int size_grid(int grid, int64_t rows, int C) {
   return (int)(want < grid ? (want < 8 ? 8 : want) : grid);
 }
 
+int two_rows_knob() {
+  static int v = -1;
+  if (v < 0) v = getenv("CVB_BN_BWD_ONE_ROW") ? 0 : 1;
+  return v;
+}
+
 template <class Args>
 int launch_coop(void (*kern)(Args), const Args& a, int grid, cudaStream_t stream) {
   cudaLaunchConfig_t cfg = {};
@@ -414,6 +467,6 @@ CVB_API int cvb_bn_backward_fused(const void* dy, int dycs, const void* x, int x
   int rc = fused_setup(C, &bar, &grid);
   if (rc) return rc;
   BwdArgs a{(const bf16*)dy, dycs, (const bf16*)x, xcs, (const bf16*)y, ycs, rows, C, mean, rstd, gamma, beta, relu,
-            ws, bar, dgamma, dbeta, (bf16*)dx, dxcs, dx32, accum32, (bf16*)dz_out};
+            ws, bar, dgamma, dbeta, (bf16*)dx, dxcs, dx32, accum32, (bf16*)dz_out, two_rows_knob()};
   return launch_coop(bn_bwd_fused, a, size_grid(grid, rows, C), (cudaStream_t)stream);
 }
