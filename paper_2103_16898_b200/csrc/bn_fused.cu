@@ -106,6 +106,7 @@ struct FwdArgs {
   float* mean; float* rstd; float eps; float* run_mean; float* run_var; float momentum;
   const float* gamma; const float* beta; const bf16* res; int rcs; int relu;
   bf16* y; int ycs, ycoff;   // y == nullptr: statistics only
+  int four_rows;             // pass 2 without residual: 4 rows in flight (CVB_BN_FWD_TWO_ROWS=1: off)
 };
 
 __global__ void __launch_bounds__(THREADS) bn_fwd_fused(const FwdArgs a) {
@@ -169,6 +170,27 @@ __global__ void __launch_bounds__(THREADS) bn_fwd_fused(const FwdArgs a) {
 #pragma unroll
   for (int k = 0; k < 8; k++) { sc[k] = s_scale[g * 8 + k]; mu[k] = s_shift[g * 8 + k]; be[k] = a.beta[g * 8 + k]; }
   int64_t r = r0 + rl;
+  if (!a.res && a.four_rows) {   // four rows' raw 16-byte loads in flight per thread
+    for (; r + 3 * RL < r1; r += 4 * RL) {
+      uint4 u[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) u[j] = __ldcg(reinterpret_cast<const uint4*>(a.x + (r + j * RL) * a.xcs + g * 8));
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u[j]);
+        float o[8];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          const float2 f = __bfloat1622float2(h[i]);
+          const float z0 = (f.x - mu[2 * i]) * sc[2 * i] + be[2 * i];
+          const float z1 = (f.y - mu[2 * i + 1]) * sc[2 * i + 1] + be[2 * i + 1];
+          o[2 * i] = a.relu ? fmaxf(z0, 0.f) : z0;
+          o[2 * i + 1] = a.relu ? fmaxf(z1, 0.f) : z1;
+        }
+        st8(a.y + (r + j * RL) * a.ycs + a.ycoff + g * 8, o);
+      }
+    }
+  }
   if (!a.res) {   // two rows in flight per thread
     for (; r + RL < r1; r += 2 * RL) {
       float v0[8], v1[8], o[8];
@@ -452,7 +474,7 @@ CVB_API int cvb_bn_forward(const void* x, int64_t rows, int C, int xcs, float* w
   int rc = fused_setup(C, &bar, &grid_b, &grid);
   if (rc) return rc;
   FwdArgs a{(const bf16*)x, rows, C, xcs, ws, bar, mean, rstd, eps, run_mean, run_var, momentum, gamma, beta,
-            (const bf16*)res, rcs, relu, (bf16*)y, ycs, ycoff};
+            (const bf16*)res, rcs, relu, (bf16*)y, ycs, ycoff, getenv("CVB_BN_FWD_TWO_ROWS") ? 0 : 1};
   return launch_coop(bn_fwd_fused, a, size_grid(grid, rows, C), (cudaStream_t)stream);
 }
 
