@@ -111,6 +111,7 @@ struct GemmParams {
   int n_epi;                // epilogue warps: 4, or 8 (two per TMEM lane quarter, column halves)
   int epi_alt;              // n_epi == 8: the two warp groups take alternate tiles (all columns)
   int nacc_log2;            // TMEM accumulator buffers: 1 << nacc_log2 (2 or 4)
+  int two_cta;              // launched with two CTAs per SM (half the shared memory each)
   uint32_t stg_warp;        // staging bytes per epilogue warp (two buffers)
   int st_rows;              // valid rows of an M tile (multiple of 32); warps past it store nothing
   int out_par;              // NHWC output is the parity sub-grid (out_ph, out_pw) of an out_H x out_W image
@@ -996,7 +997,14 @@ int launch(GemmParams& p, cudaStream_t stream) {
     e = getenv("CVB_NACC");
     env_nacc = e ? atoi(e) : 4;
   }
-  p.n_epi = (!env_epi4 && p.BN <= 64 && p.BN % 32 == 0) ? 8 : 4;
+  // two CTAs per SM for narrow HALO convs whose resident weights + 2 stages fit in half the
+  // shared memory: two independent MMA issue streams share the SM's tensor core
+  static int env_2cta = -1;
+  if (env_2cta < 0) { const char* e = getenv("CVB_GEMM_2CTA"); env_2cta = e ? atoi(e) : 1; }   // measured +3% step
+  const uint32_t half = 112u * 1024u;
+  const bool two = env_2cta && p.mode == MODE_HALO && p.BN <= 32 &&
+                   2 * stage_bytes + p.b_res_bytes + 16u * 1024u + 1280u <= half;
+  p.n_epi = (!env_epi4 && !two && p.BN <= 64 && p.BN % 32 == 0) ? 8 : 4;
   // narrow tiles: more TMEM accumulators (the epilogue of tile i no longer gates the MMAs of
   // tile i+2) and alternate-tile epilogue warp groups (two tiles drain concurrently)
   p.nacc_log2 = (env_nacc >= 4 && 4 * p.BN <= 512) ? 2 : 1;
@@ -1014,8 +1022,10 @@ int launch(GemmParams& p, cudaStream_t stream) {
   }
   if (p.out_par && !p.st_tma) { cvb_set_error("parity output needs the TMA-store epilogue"); return CVB_EINVAL; }
   const uint32_t stg = p.st_tma ? stg_bytes : 0u;
-  p.stages = (int)((224u * 1024u - p.b_res_bytes - stg) / stage_bytes);
+  p.stages = (int)(((two ? half - 1280u : 224u * 1024u) - p.b_res_bytes - stg) / stage_bytes);
   if (p.stages > 8) p.stages = 8;
+  p.two_cta = two && p.stages >= 2 ? 1 : 0;
+  if (two && !p.two_cta) p.stages = (int)((224u * 1024u - p.b_res_bytes - stg) / stage_bytes);
   static int env_stages = -1, env_dbg = -1;
   if (env_stages < 0) {
     const char* e = getenv("CVB_STAGES");
@@ -1070,7 +1080,8 @@ int launch(GemmParams& p, cudaStream_t stream) {
     p.adesc[1] = desc_tmpl(0, (uint32_t)(p.h_pitch - p.h_kw + 1) * 16, (uint32_t)p.h_pitch * 16, 0);
   }
   const int units = p.m_tiles * p.n_tiles * p.splits;
-  const int grid = units < g_num_sms ? units : g_num_sms;
+  const int slots = g_num_sms * (p.two_cta ? 2 : 1);
+  const int grid = units < slots ? units : slots;
   p.fd_m = make_fastdiv((uint32_t)p.m_tiles);
   p.fd_n = make_fastdiv((uint32_t)p.n_tiles);
   p.fd_mn = make_fastdiv((uint32_t)(p.m_tiles * p.n_tiles));
