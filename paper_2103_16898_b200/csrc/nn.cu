@@ -789,13 +789,6 @@ __global__ void relu_fwd(bf16* __restrict__ x, int64_t n8) {
 // bf16 compute copy.  step_size = lr / (1 - b1^t), inv_bc2_sqrt = 1 / sqrt(1 - b2^t).
 // Device-side step counter so a captured CUDA graph can be replayed: step += 1 and the
 // bias-correction factors are recomputed on the device every replay.
-__global__ void adam_schedule(int32_t* step, float lr, float b1, float b2, float* sched) {
-  CVB_PDL_PROLOGUE();
-  const int t = ++(*step);
-  sched[0] = (float)((double)lr / (1.0 - pow((double)b1, (double)t)));
-  sched[1] = (float)(1.0 / sqrt(1.0 - pow((double)b2, (double)t)));
-}
-
 __global__ void adam_step(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v,
                           bf16* __restrict__ pb, int64_t n, float b1, float b2, float eps, float step_size,
                           float inv_bc2_sqrt, float grad_scale, const float* __restrict__ sched) {
@@ -812,6 +805,47 @@ __global__ void adam_step(float* __restrict__ p, const float* __restrict__ g, fl
   const float pi = p[i] - step_size * (mi / denom);
   p[i] = pi;
   if (pb) pb[i] = __float2bfloat16_rn(pi);
+}
+
+// Device-counter Adam in one launch: every CTA derives this step's bias corrections from
+// step+1 (thread 0, double precision: lr / (1 - b1^t), 1 / sqrt(1 - b2^t)) and the last CTA to
+// finish advances the counter -- all CTAs have read it by then.
+__global__ void adam_step_dev(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                              float* __restrict__ v, bf16* __restrict__ pb, int64_t n, float lr, float b1, float b2,
+                              float eps, float grad_scale, int32_t* step, float* sched, unsigned* counter) {
+  CVB_PDL_PROLOGUE();
+  __shared__ float ss[2];
+  __shared__ bool last;
+  __shared__ int t_s;
+  if (threadIdx.x == 0) {
+    const int t = *(volatile int32_t*)step + 1;
+    t_s = t;
+    ss[0] = (float)((double)lr / (1.0 - pow((double)b1, (double)t)));
+    ss[1] = (float)(1.0 / sqrt(1.0 - pow((double)b2, (double)t)));
+  }
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const float step_size = ss[0], inv_bc2_sqrt = ss[1];
+    const float gi = g[i] * grad_scale;
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    const float denom = sqrtf(vi) * inv_bc2_sqrt + eps;
+    const float pi = p[i] - step_size * (mi / denom);
+    p[i] = pi;
+    if (pb) pb[i] = __float2bfloat16_rn(pi);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    *step = t_s;
+    sched[0] = ss[0];
+    sched[1] = ss[1];
+    *counter = 0u;
+  }
 }
 
 // torch.optim.SGD with momentum (dampening 0, no nesterov) + optional weight decay
@@ -1093,8 +1127,9 @@ CVB_API int cvb_adam_step(float* p, const float* g, float* m, float* v, void* pb
                                               (float)(1.0 / sqrt(bc2)), grad_scale, nullptr);
   } else {
     if (!step_dev || !sched_dev) { cvb_set_error("adam_step: device counter mode needs step_dev/sched_dev"); return CVB_EINVAL; }
-    cvb_launch(adam_schedule, 1, 1, 0, STREAM, step_dev, lr, b1, b2, sched_dev);
-    cvb_launch(adam_step, nblocks(n), 256, 0, STREAM, p, g, m, v, (bf16*)pb, n, b1, b2, eps, 0.f, 0.f, grad_scale, sched_dev);
+    // sched_dev[2] (as an unsigned, zero-initialised by the caller) is the CTA completion counter
+    cvb_launch(adam_step_dev, nblocks(n), 256, 0, STREAM, p, g, m, v, (bf16*)pb, n, lr, b1, b2, eps, grad_scale, step_dev,
+               sched_dev, reinterpret_cast<unsigned*>(sched_dev + 2));
   }
   CVB_CHECK_LAUNCH();
   return CVB_OK;

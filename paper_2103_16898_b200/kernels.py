@@ -408,7 +408,9 @@ def relu_bwd(dy, y):
 
 
 def adam_step(p, g, m, v, pb, lr, b1, b2, eps, step=0, grad_scale=1.0, step_dev=None, sched_dev=None):
-    tok = REC.begin(1 if step > 0 else 2, "optimizer", 0, p.numel() * (4 * 7 + 2))
+    if step <= 0 and (sched_dev is None or sched_dev.numel() < 4):
+        raise ValueError("adam_step: device-counter mode needs sched_dev with 4 floats (factors + CTA counter)")
+    tok = REC.begin(1, "optimizer", 0, p.numel() * (4 * 7 + 2))   # one launch in either mode
     rc = _lib_bound().cvb_adam_step(p.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(), _ptr(pb), p.numel(), lr, b1,
                                     b2, eps, step, grad_scale, _ptr(step_dev), _ptr(sched_dev), _stream())
     REC.end(tok)

@@ -112,7 +112,7 @@ class ParamStore:
         self.flip_desc = torch.tensor(desc if desc else [0], dtype=torch.int64, device=device)
         self.flip_all()
         self.step_dev = torch.zeros(1, dtype=torch.int32, device=device)
-        self.sched = torch.zeros(2, dtype=F32, device=device)
+        self.sched = torch.zeros(4, dtype=F32, device=device)   # bias-correction factors + Adam's CTA counter
 
     def state_cpu(self):
         return {name: self.p[name].detach().cpu().clone() for name, _, _ in self.specs}

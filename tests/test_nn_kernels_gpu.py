@@ -184,7 +184,7 @@ def test_adam_matches_torch():
     p, g = p0.clone(), torch.randn(n, device=dev)
     m, v = torch.zeros(n, device=dev), torch.zeros(n, device=dev)
     pb = torch.empty(n, device=dev, dtype=torch.bfloat16)
-    step_dev, sched = torch.zeros(1, dtype=torch.int32, device=dev), torch.zeros(2, device=dev)
+    step_dev, sched = torch.zeros(1, dtype=torch.int32, device=dev), torch.zeros(4, device=dev)
     pr = p0.clone().requires_grad_(True)
     opt = torch.optim.Adam([pr], lr=1e-3, foreach=False)
     for _ in range(3):
@@ -193,6 +193,7 @@ def test_adam_matches_torch():
         opt.step()
     assert rel(p, pr.detach()) < 1e-6
     assert torch.equal(pb, p.bfloat16())
+    assert int(step_dev.item()) == 3 and sched[2].view(torch.int32).item() == 0   # counter advanced, CTA count reset
     assert int(step_dev.item()) == 3
 
 
