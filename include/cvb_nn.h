@@ -119,8 +119,9 @@ int cvb_relu_fwd(void* x, int64_t n, void* stream);
 int cvb_relu_bwd(void* dy, const void* y, int64_t n, void* stream);
 
 /* ---- fused optimisers over flat fp32 buffers (refresh the bf16 compute copy pb) ---------------- */
-/* step > 0: host bias correction; step <= 0: device counter in one launch (step_dev += 1, the
- * factors land in sched_dev[0..1]; sched_dev holds 4 floats, [2] zero-initialised: CTA counter),
+/* step > 0: host bias correction; step <= 0: device counter in one launch (step_dev += 1;
+ * sched_dev holds 4 floats, zero-initialised: [0..1] the next step's bias corrections
+ * 1/(1-b1^t), 1/sqrt(1-b2^t) (cached for fixed b1, b2), [2] the CTA counter),
  * so a captured CUDA graph replays correctly. */
 int cvb_adam_step(float* p, const float* g, float* m, float* v, void* pb, int64_t n, float lr, float b1, float b2,
                   float eps, int64_t step, float grad_scale, int32_t* step_dev, float* sched_dev, void* stream);

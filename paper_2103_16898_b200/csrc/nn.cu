@@ -807,9 +807,15 @@ __global__ void adam_step(float* __restrict__ p, const float* __restrict__ g, fl
   if (pb) pb[i] = __float2bfloat16_rn(pi);
 }
 
-// Device-counter Adam in one launch: every CTA derives this step's bias corrections from
-// step+1 (thread 0, double precision: lr / (1 - b1^t), 1 / sqrt(1 - b2^t)) and the last CTA to
-// finish advances the counter -- all CTAs have read it by then.
+// Device-counter Adam in one launch.  sched holds the bias corrections of the UPCOMING step
+// (1/(1-b1^t), 1/sqrt(1-b2^t)), written by the last CTA of the previous launch (all CTAs
+// have read them by then), so CTAs only read two floats; the very first step (counter 0)
+// derives them in place.  The last CTA also advances the step counter.
+__device__ __forceinline__ void adam_bias_corr(int t, float b1, float b2, float* c1, float* c2) {
+  *c1 = (float)(1.0 / (1.0 - pow((double)b1, (double)t)));
+  *c2 = (float)(1.0 / sqrt(1.0 - pow((double)b2, (double)t)));
+}
+
 __global__ void adam_step_dev(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                               float* __restrict__ v, bf16* __restrict__ pb, int64_t n, float lr, float b1, float b2,
                               float eps, float grad_scale, int32_t* step, float* sched, unsigned* counter) {
@@ -820,13 +826,39 @@ __global__ void adam_step_dev(float* __restrict__ p, const float* __restrict__ g
   if (threadIdx.x == 0) {
     const int t = *(volatile int32_t*)step + 1;
     t_s = t;
-    ss[0] = (float)((double)lr / (1.0 - pow((double)b1, (double)t)));
-    ss[1] = (float)(1.0 / sqrt(1.0 - pow((double)b2, (double)t)));
+    if (t == 1) adam_bias_corr(1, b1, b2, &ss[0], &ss[1]);
+    else { ss[0] = *(volatile float*)&sched[0]; ss[1] = *(volatile float*)&sched[1]; }
   }
   __syncthreads();
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
-    const float step_size = ss[0], inv_bc2_sqrt = ss[1];
+  // grid-stride (a few CTAs per SM): the completion counter below is one same-address atomic
+  // per CTA, which serialises in L2 -- thousands of CTAs would cost ~10 us
+  const float step_size = lr * ss[0], inv_bc2_sqrt = ss[1];
+  const int64_t n4 = (n & 3) == 0 && !(((uintptr_t)p | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v) & 15) &&
+                             !((uintptr_t)pb & 7) ? n / 4 : 0;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n4; k += (int64_t)gridDim.x * blockDim.x) {
+    float4 pv = reinterpret_cast<float4*>(p)[k], mv = reinterpret_cast<float4*>(m)[k], vv = reinterpret_cast<float4*>(v)[k];
+    const float4 gv = __ldg(reinterpret_cast<const float4*>(g) + k);
+    float* pp = &pv.x; float* mp = &mv.x; float* vp = &vv.x; const float* gp = &gv.x;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const float gi = gp[j] * grad_scale;
+      mp[j] = b1 * mp[j] + (1.f - b1) * gi;
+      vp[j] = b2 * vp[j] + (1.f - b2) * gi * gi;
+      const float denom = sqrtf(vp[j]) * inv_bc2_sqrt + eps;
+      pp[j] = pp[j] - step_size * (mp[j] / denom);
+    }
+    reinterpret_cast<float4*>(p)[k] = pv;
+    reinterpret_cast<float4*>(m)[k] = mv;
+    reinterpret_cast<float4*>(v)[k] = vv;
+    if (pb) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(pv.x, pv.y), hi = __floats2bfloat162_rn(pv.z, pv.w);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&lo);
+      u.y = *reinterpret_cast<uint32_t*>(&hi);
+      reinterpret_cast<uint2*>(pb)[k] = u;
+    }
+  }
+  for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float gi = g[i] * grad_scale;
     const float mi = b1 * m[i] + (1.f - b1) * gi;
     const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
@@ -842,8 +874,7 @@ __global__ void adam_step_dev(float* __restrict__ p, const float* __restrict__ g
   __syncthreads();
   if (last && threadIdx.x == 0) {
     *step = t_s;
-    sched[0] = ss[0];
-    sched[1] = ss[1];
+    adam_bias_corr(t_s + 1, b1, b2, &sched[0], &sched[1]);   // the next step's corrections
     *counter = 0u;
   }
 }
@@ -1128,7 +1159,8 @@ CVB_API int cvb_adam_step(float* p, const float* g, float* m, float* v, void* pb
   } else {
     if (!step_dev || !sched_dev) { cvb_set_error("adam_step: device counter mode needs step_dev/sched_dev"); return CVB_EINVAL; }
     // sched_dev[2] (as an unsigned, zero-initialised by the caller) is the CTA completion counter
-    cvb_launch(adam_step_dev, nblocks(n), 256, 0, STREAM, p, g, m, v, (bf16*)pb, n, lr, b1, b2, eps, grad_scale, step_dev,
+    const int64_t nb = nblocks(n), cap = 4 * (int64_t)cvb_num_sms();
+    cvb_launch(adam_step_dev, (int)(nb < cap ? nb : cap), 256, 0, STREAM, p, g, m, v, (bf16*)pb, n, lr, b1, b2, eps, grad_scale, step_dev,
                sched_dev, reinterpret_cast<unsigned*>(sched_dev + 2));
   }
   CVB_CHECK_LAUNCH();
