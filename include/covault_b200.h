@@ -51,6 +51,13 @@ int cvb_aes256_encrypt_block_host(const uint8_t key[32], const uint8_t in[16], u
 typedef struct cvb_gcm_ctx cvb_gcm_ctx;
 int cvb_gcm_ctx_create(const uint8_t key[32], cvb_gcm_ctx** out);
 void cvb_gcm_ctx_destroy(cvb_gcm_ctx* ctx);
+/* Attach a caller-owned zeroed device word that every later open / decode through `ctx` ORs
+ * its tag verdict into (1 = some message failed): a sticky per-run verdict that training
+ * gates its optimiser on and the host checks once (Volume.get's "never partial" contract,
+ * volume.py:185-197, applied to a whole multi-shard run).  nullptr detaches. */
+int cvb_gcm_ctx_set_verdict(cvb_gcm_ctx* ctx, uint32_t* verdict_dev);
+/* Destroy the host-path context cache of cvb_aead_open/seal and zero its key bytes. */
+void cvb_aead_cache_clear(void);
 
 /* Asynchronous, stream-ordered open of a blob already in HBM.  work: >= 8 zeroed uint32
  * device words private to this call; status (0 ok / 1 tag mismatch) lands in work[4].
@@ -83,6 +90,18 @@ int cvb_records_to_nhwc(const uint8_t* pt_dev, int64_t nrec, int64_t rec_bytes, 
                         int64_t w, const float* mean, const float* std, int dtype, void* out_dev,
                         int32_t* labels_dev, void* stream);
 
+/* ---- SHA-256 (FIPS 180-4) over message batches --------------------------------------- */
+
+/* Replaces hashlib SHA-256 as used by covault.crypto.hash_bytes (pkg/src/covault/crypto.py:91-93)
+ * for blob names (Volume.put, volume.py:170-171), key-free Volume.verify (volume.py:199-222) and
+ * the gate's plaintext digests (gate.py:188).  One thread per message (a message's blocks are a
+ * sequential chain); digests_dev gets 32 bytes per message.  offsets_dev: n+1 int64 byte offsets
+ * into data_dev (device memory).  Asynchronous. */
+int cvb_sha256_batch_dev(const uint8_t* data_dev, const int64_t* offsets_dev, int64_t n, uint8_t* digests_dev,
+                         void* stream);
+/* Host-buffer form: n messages (pointer + length each) -> n x 32 digest bytes.  Synchronous. */
+int cvb_sha256_batch(const uint8_t* const* msgs, const size_t* lens, int64_t n, uint8_t* digests);
+
 /* ---- reference trainer ---------------------------------------------------------------- */
 
 /* Numeric core of covault.workload.run_training (pkg/src/covault/workload.py:48-71).
@@ -90,6 +109,20 @@ int cvb_records_to_nhwc(const uint8_t* pt_dev, int64_t nrec, int64_t rec_bytes, 
  * order (reproduces the golden model digest), 1 = parallel reductions.  Synchronous. */
 int cvb_logistic_train(const double* X, const double* y, int64_t n, int64_t f, double lr, int64_t epochs,
                        int mode, double* w_out, double* b_out);
+
+/* Device-resident epoch pieces of the same trainer (stream-ordered, all pointers in HBM), so a
+ * data-parallel trainer can all-reduce the F+1 gradient sums between them (
+ * the reference's epoch body is workload.py:57-70):
+ *   grad:  g[0..f) = sum_r delta_r x_r, g[f] = sum_r delta_r over the n rows given (rows in
+ *          order in mode 0; mode 0 reads Xt = the feature-major copy, mode 1 ignores it);
+ *          scratch: cvb_logistic_scratch_doubles(n, f, mode) doubles.
+ *   apply: w_i -= (lr * g_i) / nrows ; b -= (lr * g_b) / nrows  (nrows = the global count). */
+int64_t cvb_logistic_scratch_doubles(int64_t n, int64_t f, int mode);
+int cvb_logistic_transpose_dev(const double* X, int64_t n, int64_t f, double* Xt, void* stream);
+int cvb_logistic_grad_dev(const double* X, const double* Xt, const double* y, int64_t n, int64_t f,
+                          const double* w, const double* b, int mode, double* g, double* scratch, void* stream);
+int cvb_logistic_apply_dev(const double* g, int64_t f, double lr, double nrows, double* w, double* b,
+                           void* stream);
 
 #ifdef __cplusplus
 }

@@ -123,8 +123,13 @@ int cvb_relu_bwd(void* dy, const void* y, int64_t n, void* stream);
  * sched_dev holds 4 floats, zero-initialised: [0..1] the next step's bias corrections
  * 1/(1-b1^t), 1/sqrt(1-b2^t) (cached for fixed b1, b2), [2] the CTA counter),
  * so a captured CUDA graph replays correctly. */
+/* skip_dev (nullable): when *skip_dev != 0 the update is skipped entirely (parameters, moments,
+ * step counter) -- the decrypt-verdict gate of an encrypted training step. */
 int cvb_adam_step(float* p, const float* g, float* m, float* v, void* pb, int64_t n, float lr, float b1, float b2,
-                  float eps, int64_t step, float grad_scale, int32_t* step_dev, float* sched_dev, void* stream);
+                  float eps, int64_t step, float grad_scale, int32_t* step_dev, float* sched_dev,
+                  const float* skip_dev, void* stream);
+/* *slot = (*word != 0) ? 1.0f : 0.0f  (one thread; the per-step verdict snapshot) */
+int cvb_verdict_snapshot(const uint32_t* word, float* slot, void* stream);
 int cvb_sgd_step(float* p, const float* g, float* buf, void* pb, int64_t n, float lr, float momentum, float wd,
                  float grad_scale, int first, void* stream);
 int cvb_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream);

@@ -42,11 +42,19 @@ SIGNATURES = {
     "cvb_aead_seal": (_INT, [_P, _P, _P, _SZ, _P, _SZ, _P]),
     "cvb_gcm_ctx_create": (_INT, [_P, _c.POINTER(_P)]),
     "cvb_gcm_ctx_destroy": (None, [_P]),
+    "cvb_gcm_ctx_set_verdict": (_INT, [_P, _P]),
+    "cvb_aead_cache_clear": (None, []),
     "cvb_gcm_open_dev": (_INT, [_P, _P, _P, _SZ, _P, _SZ, _P, _P, _P]),
     "cvb_gcm_seal_dev": (_INT, [_P, _P, _P, _SZ, _P, _SZ, _P, _P, _P]),
     "cvb_gcm_open_records_dev": (_INT, [_P, _P, _P, _SZ, _P, _SZ, _I64, _INT, _I64, _P, _P, _P, _P, _P, _P]),
     "cvb_records_to_nhwc": (_INT, [_P, _I64, _I64, _I64, _I64, _I64, _P, _P, _INT, _P, _P, _P]),
+    "cvb_sha256_batch_dev": (_INT, [_P, _P, _I64, _P, _P]),
+    "cvb_sha256_batch": (_INT, [_P, _P, _I64, _P]),
     "cvb_logistic_train": (_INT, [_P, _P, _I64, _I64, _c.c_double, _I64, _INT, _P, _P]),
+    "cvb_logistic_scratch_doubles": (_I64, [_I64, _I64, _INT]),
+    "cvb_logistic_transpose_dev": (_INT, [_P, _I64, _I64, _P, _P]),
+    "cvb_logistic_grad_dev": (_INT, [_P, _P, _P, _I64, _I64, _P, _P, _INT, _P, _P, _P]),
+    "cvb_logistic_apply_dev": (_INT, [_P, _I64, _c.c_double, _c.c_double, _P, _P, _P]),
     # tcgen05 implicit-GEMM engine (include/cvb_nn.h)
     "cvb_conv2d_fwd": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT,
                               _INT, _INT, _P, _INT, _INT, _P]),
@@ -93,7 +101,8 @@ SIGNATURES = {
     "cvb_relu_fwd": (_INT, [_P, _I64, _P]),
     "cvb_relu_bwd": (_INT, [_P, _P, _I64, _P]),
     "cvb_adam_step": (_INT, [_P, _P, _P, _P, _P, _I64, _c.c_float, _c.c_float, _c.c_float, _c.c_float, _I64,
-                             _c.c_float, _P, _P, _P]),
+                             _c.c_float, _P, _P, _P, _P]),
+    "cvb_verdict_snapshot": (_INT, [_P, _P, _P]),
     "cvb_sgd_step": (_INT, [_P, _P, _P, _P, _I64, _c.c_float, _c.c_float, _c.c_float, _c.c_float, _INT, _P]),
     "cvb_cast_f32_bf16": (_INT, [_P, _P, _I64, _P]),
     "cvb_cast_rows": (_INT, [_P, _I64, _P, _I64, _I64, _INT, _P]),
@@ -135,18 +144,26 @@ def check(rc: int, what: str) -> int:
     return rc
 
 
-_device_bound = set()
+_tls = threading.local()
 
 
 def bind_device(dev: int | None = None) -> None:
-    """Point the library's CUDA runtime at torch's current device (once per device)."""
-    import torch
+    """Point the library's CUDA runtime at torch's current device.
 
+    The library links cudart statically, so its current device is its own and per thread:
+    re-bind whenever the calling thread's torch device differs from what this thread last
+    bound (torch cuda:0 -> cuda:1 -> cuda:0 and new threads are all handled).  Without
+    torch imported (the host AEAD path) the device is left at the thread's default."""
     if dev is None:
+        import sys
+
+        torch = sys.modules.get("torch")
+        if torch is None or not torch.cuda.is_available() or not torch.cuda.is_initialized():
+            return
         dev = torch.cuda.current_device()
-    if dev not in _device_bound:
+    if getattr(_tls, "dev", None) != dev:
         check(load().cvb_set_device(int(dev)), "cvb_set_device")
-        _device_bound.add(dev)
+        _tls.dev = dev
 
 
 def stream_ptr(stream=None) -> int:

@@ -75,6 +75,7 @@ def aead_seal(key, nonce: bytes, aad: bytes, plaintext: bytes) -> bytes:
     if len(nonce) != AEAD_NONCE_SIZE:
         raise DecodeError(f"nonce must be {AEAD_NONCE_SIZE} bytes")
     lib = _lib.load()
+    _lib.bind_device()
     kb = _key_bytes(key)
     out = ctypes.create_string_buffer(len(plaintext) + 16)
     rc = lib.cvb_aead_seal(kb, bytes(nonce), bytes(aad), len(aad), bytes(plaintext), len(plaintext), out)
@@ -87,6 +88,7 @@ def aead_open(key, nonce: bytes, aad: bytes, ciphertext: bytes) -> bytes:
     if len(nonce) != AEAD_NONCE_SIZE:
         raise DecodeError(f"nonce must be {AEAD_NONCE_SIZE} bytes")
     lib = _lib.load()
+    _lib.bind_device()
     kb = _key_bytes(key)
     n = len(ciphertext)
     out = ctypes.create_string_buffer(max(1, n - 16))
@@ -95,6 +97,39 @@ def aead_open(key, nonce: bytes, aad: bytes, ciphertext: bytes) -> bytes:
     if rc == _lib.CVB_AUTH_FAIL:
         raise AuthenticationFailure("AEAD authentication failed")
     return out.raw[: n - 16]
+
+
+def sha256_many(messages) -> list[bytes]:
+    """SHA-256 of each message (bytes-like) on the GPU, one launch for the whole batch --
+    the batched form of covault.crypto.hash_bytes (crypto.py:91-93)."""
+    msgs = [bytes(m) for m in messages]
+    n = len(msgs)
+    if n == 0:
+        return []
+    lib = _lib.load()
+    _lib.bind_device()
+    ptrs = (ctypes.c_char_p * n)(*msgs)
+    lens = (ctypes.c_size_t * n)(*[len(m) for m in msgs])
+    out = ctypes.create_string_buffer(32 * n)
+    _lib.check(lib.cvb_sha256_batch(ctypes.cast(ptrs, ctypes.c_void_p), lens, n, out), "sha256_batch")
+    raw = out.raw
+    return [raw[32 * i:32 * i + 32] for i in range(n)]
+
+
+def sha256_device(data_dev, offsets_dev, stream=None):
+    """Digests (uint8 CUDA tensor [n, 32]) of the n messages data_dev[offsets[i]:offsets[i+1]]
+    of a uint8 CUDA arena; stream-ordered, the messages never leave HBM."""
+    import torch
+
+    _lib.bind_device()
+    n = offsets_dev.numel() - 1
+    out = torch.empty((max(0, n), 32), dtype=torch.uint8, device=data_dev.device)
+    if n > 0:
+        if offsets_dev.dtype != torch.int64 or not offsets_dev.is_cuda:
+            raise ValueError("offsets must be an int64 CUDA tensor")
+        _lib.check(_lib.load().cvb_sha256_batch_dev(data_dev.data_ptr(), offsets_dev.data_ptr(), n, out.data_ptr(),
+                                                    _lib.stream_ptr(stream)), "sha256_batch_dev")
+    return out
 
 
 def fresh_nonce() -> bytes:
@@ -117,6 +152,14 @@ class GcmContext:
         self._ptr = ctypes.c_void_p()
         _lib.check(self._lib.cvb_gcm_ctx_create(_key_bytes(key), ctypes.byref(self._ptr)), "gcm_ctx_create")
         self._torch = torch
+
+    def set_verdict(self, word) -> None:
+        """Attach a zeroed int32 CUDA word that every later open / decode through this context
+        ORs its tag verdict into (sticky over a whole run; ``None`` detaches).  The caller
+        keeps ``word`` alive while launches that may write it are in flight."""
+        self._verdict = word
+        _lib.check(self._lib.cvb_gcm_ctx_set_verdict(self._ptr, word.data_ptr() if word is not None else None),
+                   "gcm_ctx_set_verdict")
 
     def close(self):
         if self._ptr:

@@ -42,6 +42,17 @@ static inline int cvb_num_sms() {
   return n;
 }
 
+// True the first time it is called for the current device with this flag word (one bit per
+// device): per-device one-time setup such as cudaFuncSetAttribute, which is per device.
+static inline bool cvb_first_on_device(unsigned long long* mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (__atomic_load_n(mask, __ATOMIC_ACQUIRE) & bit) return false;
+  __atomic_fetch_or(mask, bit, __ATOMIC_ACQ_REL);
+  return true;
+}
+
 #define CVB_API extern "C" __attribute__((visibility("default")))
 
 // ---- programmatic dependent launch (PDL) -----------------------------------------------

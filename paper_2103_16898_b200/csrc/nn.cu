@@ -791,10 +791,11 @@ __global__ void relu_fwd(bf16* __restrict__ x, int64_t n8) {
 // bias-correction factors are recomputed on the device every replay.
 __global__ void adam_step(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v,
                           bf16* __restrict__ pb, int64_t n, float b1, float b2, float eps, float step_size,
-                          float inv_bc2_sqrt, float grad_scale, const float* __restrict__ sched) {
+                          float inv_bc2_sqrt, float grad_scale, const float* __restrict__ sched,
+                          const float* __restrict__ skip) {
   CVB_PDL_PROLOGUE();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i >= n || (skip && *skip != 0.f)) return;
   if (sched) { step_size = sched[0]; inv_bc2_sqrt = sched[1]; }
   const float gi = g[i] * grad_scale;
   const float mi = b1 * m[i] + (1.f - b1) * gi;
@@ -818,8 +819,13 @@ __device__ __forceinline__ void adam_bias_corr(int t, float b1, float b2, float*
 
 __global__ void adam_step_dev(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                               float* __restrict__ v, bf16* __restrict__ pb, int64_t n, float lr, float b1, float b2,
-                              float eps, float grad_scale, int32_t* step, float* sched, unsigned* counter) {
+                              float eps, float grad_scale, int32_t* step, float* sched, unsigned* counter,
+                              const float* __restrict__ skip) {
   CVB_PDL_PROLOGUE();
+  // verdict gate: a non-zero skip word (a failed shard tag on any rank, summed into the
+  // gradient exchange) leaves parameters, moments and the step counter untouched.  The word
+  // is written only by stream-ordered predecessors, so every CTA reads the same value.
+  if (skip && *skip != 0.f) return;
   __shared__ float ss[2];
   __shared__ bool last;
   __shared__ int t_s;
@@ -1151,18 +1157,33 @@ CVB_API int cvb_relu_bwd(void* dy, const void* y, int64_t n, void* stream) {
 // step > 0: host-side bias correction for that step.  step <= 0: device counter mode --
 // step_dev is incremented on the device and the factors land in sched_dev (2 floats).
 CVB_API int cvb_adam_step(float* p, const float* g, float* m, float* v, void* pb, int64_t n, float lr, float b1, float b2,
-                          float eps, int64_t step, float grad_scale, int32_t* step_dev, float* sched_dev, void* stream) {
+                          float eps, int64_t step, float grad_scale, int32_t* step_dev, float* sched_dev,
+                          const float* skip_dev, void* stream) {
   if (step > 0) {
     const double bc1 = 1.0 - pow((double)b1, (double)step), bc2 = 1.0 - pow((double)b2, (double)step);
     cvb_launch(adam_step, nblocks(n), 256, 0, STREAM, p, g, m, v, (bf16*)pb, n, b1, b2, eps, (float)(lr / bc1),
-                                              (float)(1.0 / sqrt(bc2)), grad_scale, nullptr);
+                                              (float)(1.0 / sqrt(bc2)), grad_scale, nullptr, skip_dev);
   } else {
     if (!step_dev || !sched_dev) { cvb_set_error("adam_step: device counter mode needs step_dev/sched_dev"); return CVB_EINVAL; }
     // sched_dev[2] (as an unsigned, zero-initialised by the caller) is the CTA completion counter
     const int64_t nb = nblocks(n), cap = 4 * (int64_t)cvb_num_sms();
     cvb_launch(adam_step_dev, (int)(nb < cap ? nb : cap), 256, 0, STREAM, p, g, m, v, (bf16*)pb, n, lr, b1, b2, eps, grad_scale, step_dev,
-               sched_dev, reinterpret_cast<unsigned*>(sched_dev + 2));
+               sched_dev, reinterpret_cast<unsigned*>(sched_dev + 2), skip_dev);
   }
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+// slot = (verdict word != 0) ? 1 : 0 -- the step's snapshot of the sticky decrypt verdict,
+// taken while no decrypt is in flight; it travels in the gradient exchange and gates Adam.
+__global__ void verdict_snapshot(const uint32_t* __restrict__ word, float* __restrict__ slot) {
+  CVB_PDL_PROLOGUE();
+  if (threadIdx.x == 0) *slot = *word ? 1.f : 0.f;
+}
+
+CVB_API int cvb_verdict_snapshot(const uint32_t* word, float* slot, void* stream) {
+  if (!word || !slot) { cvb_set_error("verdict_snapshot: null argument"); return CVB_EINVAL; }
+  cvb_launch(verdict_snapshot, 1, 32, 0, STREAM, word, slot);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }

@@ -976,11 +976,11 @@ int plan_tma_store(GemmParams& p) {
 }
 
 int g_num_sms = 0;
-bool g_attr_done = false;
+unsigned long long g_attr_done = 0;   // one bit per device
 long long* g_trace = nullptr;
 
 int launch(GemmParams& p, cudaStream_t stream) {
-  if (!g_num_sms) g_num_sms = cvb_num_sms();
+  g_num_sms = cvb_num_sms();   // cached per device
   if (!p.kr) p.kr = BK;
   p.ksteps = p.kr / 16;
   if (!p.a_stage_bytes) p.a_stage_bytes = BM * p.kr * 2;
@@ -1046,10 +1046,8 @@ int launch(GemmParams& p, cudaStream_t stream) {
   if (p.stages < 2) { cvb_set_error("BN too large"); return CVB_EINVAL; }
   p.stg_off = (uint32_t)p.stages * stage_bytes + p.b_res_bytes;   // 1024-aligned (stages, slabs are)
   size_t smem = (size_t)p.stages * stage_bytes + p.b_res_bytes + stg + 1024 + 256;
-  if (!g_attr_done) {
+  if (cvb_first_on_device(&g_attr_done))
     CVB_CUDA(cudaFuncSetAttribute(umma_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    g_attr_done = true;
-  }
   p.idesc = make_idesc(p.a_major, p.b_major, p.BN);
   // smem box strides and descriptor templates
   p.a_box_stride = p.a_major == 0 ? BM * p.a_cel * 2 : p.kr * p.a_cel * 2;
@@ -1452,7 +1450,7 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
   p.num_kb = p.ptiles_w * p.ptiles_h * ptiles_n;
   p.m_tiles = (cout + BM - 1) / BM;
   p.n_tiles = (Ncols + p.BN - 1) / p.BN;
-  if (!g_num_sms) g_num_sms = cvb_num_sms();
+  g_num_sms = cvb_num_sms();   // cached per device
   int tiles = p.m_tiles * p.n_tiles;
   int splits = (g_num_sms + tiles - 1) / tiles;
   if (splits > max_splits) splits = max_splits;

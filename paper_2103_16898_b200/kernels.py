@@ -407,14 +407,21 @@ def relu_bwd(dy, y):
     _lib.check(rc, "relu_bwd")
 
 
-def adam_step(p, g, m, v, pb, lr, b1, b2, eps, step=0, grad_scale=1.0, step_dev=None, sched_dev=None):
+def adam_step(p, g, m, v, pb, lr, b1, b2, eps, step=0, grad_scale=1.0, step_dev=None, sched_dev=None, skip_dev=None):
     if step <= 0 and (sched_dev is None or sched_dev.numel() < 4):
         raise ValueError("adam_step: device-counter mode needs sched_dev with 4 floats (factors + CTA counter)")
     tok = REC.begin(1, "optimizer", 0, p.numel() * (4 * 7 + 2))   # one launch in either mode
     rc = _lib_bound().cvb_adam_step(p.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(), _ptr(pb), p.numel(), lr, b1,
-                                    b2, eps, step, grad_scale, _ptr(step_dev), _ptr(sched_dev), _stream())
+                                    b2, eps, step, grad_scale, _ptr(step_dev), _ptr(sched_dev), _ptr(skip_dev),
+                                    _stream())
     REC.end(tok)
     _lib.check(rc, "adam_step")
+
+
+def verdict_snapshot(word, slot):
+    """slot[0] = 1.0 if the sticky decrypt verdict word is set else 0.0 (one tiny launch)."""
+    rc = _lib_bound().cvb_verdict_snapshot(word.data_ptr(), slot.data_ptr(), _stream())
+    _lib.check(rc, "verdict_snapshot")
 
 
 def sgd_step(p, g, buf, pb, lr, momentum=0.0, wd=0.0, grad_scale=1.0, first=False):

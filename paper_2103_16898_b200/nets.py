@@ -81,7 +81,10 @@ class ParamStore:
             off += (n + ALIGN - 1) // ALIGN * ALIGN
         self.total = off
         self.p32 = torch.zeros(off, dtype=F32, device=device)
-        self.g32 = torch.zeros(off, dtype=F32, device=device)
+        # one extra aligned slot after the parameters: the step's decrypt verdict (0/1 per rank,
+        # summed by the gradient all-reduce like any gradient) that gates the optimiser
+        self.g32 = torch.zeros(off + ALIGN, dtype=F32, device=device)
+        self.verdict_slot = self.g32[off:off + 1]
         self.m = torch.zeros(off, dtype=F32, device=device)
         self.v = torch.zeros(off, dtype=F32, device=device)
         self.pb = torch.zeros(off, dtype=BF16, device=device)
@@ -429,7 +432,8 @@ class Net:
 
     def optimizer_step(self):
         K.adam_step(self.ps.p32, self.ps.g32, self.ps.m, self.ps.v, self.ps.pb, self.lr, self.b1, self.b2, self.eps,
-                    step=0, grad_scale=self.grad_scale, step_dev=self.ps.step_dev, sched_dev=self.ps.sched)
+                    step=0, grad_scale=self.grad_scale, step_dev=self.ps.step_dev, sched_dev=self.ps.sched,
+                    skip_dev=self.ps.verdict_slot)
         self.ps.flip_all()   # next step's dgrad weights
 
     @property

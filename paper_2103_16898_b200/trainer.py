@@ -79,7 +79,7 @@ class OverlappedGradAllReduce:
         names, lo, hi = [], None, None
         order = sorted(ps.offsets.items(), key=lambda kv: -kv[1])
         ends = {}
-        prev = ps.total
+        prev = ps.g32.numel()        # the first bucket also carries the verdict slot past ps.total
         for name, off in order:      # each parameter owns [off, next parameter's offset)
             ends[name] = prev
             prev = off
@@ -156,7 +156,13 @@ class EncryptedTrainer:
             self.allreduce = OverlappedGradAllReduce(self.net.ps)
             self.net.ps.grad_hook = self.allreduce
         self.graph = None
+        # sticky run verdict: every shard opened through self.ctx ORs its tag verdict into this
+        # word; each step snapshots it into the gradient buffer's verdict slot (summed over
+        # ranks by the gradient all-reduce), and Adam skips the update when the slot is non-zero
+        self.verdict = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.ctx.set_verdict(self.verdict)
         self.status_host = torch.zeros(8, dtype=torch.int32).pin_memory()
+        self.verdict_host = torch.zeros(1, dtype=torch.float32).pin_memory()
         self.loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()
 
     # -- the step ------------------------------------------------------------------------
@@ -165,6 +171,7 @@ class EncryptedTrainer:
         net = self.net
         if self.allreduce is not None:
             self.allreduce.reset()
+        K.verdict_snapshot(self.verdict, net.ps.verdict_slot)   # no decrypt is in flight here
         net.fwd_bwd(x, lab)
 
     def _opt_body(self):
@@ -296,14 +303,15 @@ class EncryptedTrainer:
         self._pend = ((ct_dev.data_ptr(), ct_dev.numel(), bytes(nonce)), w)
 
     def _issue_d2h(self):
-        """D2H of the step's loss and tag verdict on a side stream (after forward/backward)."""
+        """D2H of the step's loss and run verdict on a side stream (after forward/backward and
+        the gradient exchange: with data parallelism the verdict slot is the sum over ranks)."""
         if getattr(self, "d2h_stream", None) is None:
             self.d2h_stream = torch.cuda.Stream()
             self.d2h_done = torch.cuda.Event()
         self.d2h_stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(self.d2h_stream):
             self.loss_host.copy_(self.net.loss, non_blocking=True)
-            self.status_host[:1].copy_(self._works[self._wcur][4:5], non_blocking=True)
+            self.verdict_host.copy_(self.net.ps.verdict_slot, non_blocking=True)
         self.d2h_done.record(self.d2h_stream)
 
     def step_host(self, blob_host: torch.Tensor, nonce: bytes, aad: bytes, nrec: int, next_blob=None,
@@ -332,12 +340,22 @@ class EncryptedTrainer:
         ld.release_spare()
         return self.loss_host
 
-    def check_status(self):
-        """Raise if the last shard's tag failed (its plaintext was zeroed on the device)."""
+    def check_status(self, include_pending: bool = False):
+        """Raise if any shard trained so far -- on any rank -- failed authentication.
+
+        The device already kept every failed shard out of training (its tile was zeroed and
+        the optimiser skipped that step and every later one); this surfaces the verdict on
+        the host.  It reads the verdict slot of the last step, which the gradient all-reduce
+        summed over ranks, so every rank raises at the same step.  ``include_pending`` also
+        reads this rank's sticky word, which additionally covers a shard already decrypted
+        ahead but not trained on yet (the final check before a model is sealed)."""
         torch.cuda.current_stream().synchronize()
         if getattr(self, "d2h_done", None) is not None:
             self.d2h_done.synchronize()
-        if int(self.status_host[0]) != 0:
+        bad = float(self.net.ps.verdict_slot.item()) != 0.0
+        if include_pending:
+            bad = bad or int(self.verdict.item()) != 0
+        if bad:
             raise AuthenticationFailure("training shard failed authentication")
 
 

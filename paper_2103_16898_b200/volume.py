@@ -216,8 +216,16 @@ class Volume:
         aad = torch.tensor(list(aad_for(self.volume_name, logical_path)), dtype=torch.uint8, device="cuda")
         out = torch.empty(max(1, e.plaintext_length), dtype=torch.uint8, device="cuda")
         work = ctx.new_workspace()
+        if stream is not None:
+            # the H2D copy, AAD upload and workspace zeroing above ran on the current stream
+            stream.wait_stream(torch.cuda.current_stream())
         ctx.open_device(e.nonce, aad, dev, out, work, stream)
+        if stream is not None:
+            for t in (dev, aad, out, work):   # keep the allocator from recycling them early
+                t.record_stream(stream)
         if sync:
+            if stream is not None:
+                stream.synchronize()   # the verdict is written on `stream`
             if not ctx.status_ok(work):
                 del out
                 raise AuthenticationFailure("AEAD authentication failed")

@@ -67,11 +67,78 @@ def train_arrays(X: np.ndarray, y: np.ndarray, learning_rate: float, epochs: int
     return w, float(b[0])
 
 
+def shard_rows(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous row block [lo, hi) of rank `rank` (blocks in rank order, sizes differ by <= 1),
+    so each rank's in-order partial sums concatenate to the reference's file order."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank / world size")
+    base, extra = divmod(int(n), int(world))
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+class LogisticTrainer:
+    """Device-resident form of the reference trainer (workload.py:48-71) for one rank.
+
+    ``X``/``y`` are this rank's rows (float64 CUDA tensors, row-major); with a process group
+    every epoch's F+1 gradient sums are all-reduced (SUM) between the gradient and update
+    kernels and the update divides by the GLOBAL row count -- data-parallel full-batch
+    gradient descent.  Ranks must hold contiguous row blocks in rank
+    order; the result then differs from the single-rank schedule only by the order of the
+    cross-rank sum (tolerance gate), and at world size 1 (or without a group) mode 0 is the
+    bit-exact reference schedule."""
+
+    def __init__(self, X, y, exact: bool = True, group=None, n_total: int | None = None):
+        import torch
+
+        if X.dtype != torch.float64 or y.dtype != torch.float64 or not X.is_cuda or X.dim() != 2:
+            raise ValueError("X, y must be float64 CUDA tensors, X of shape (n, f)")
+        _lib.bind_device()
+        self.torch, self.group = torch, group
+        self.X, self.y = X.contiguous(), y.contiguous()
+        self.n, self.f = X.shape
+        self.mode = 0 if exact else 1
+        self.n_total = int(n_total if n_total is not None else self.n)
+        self._lib = _lib.load()
+        dev = X.device
+        self.wb = torch.zeros(self.f + 1, dtype=torch.float64, device=dev)   # weights, then the bias
+        self.g = torch.zeros(self.f + 1, dtype=torch.float64, device=dev)
+        self.scratch = torch.empty(max(1, self._lib.cvb_logistic_scratch_doubles(self.n, self.f, self.mode)),
+                                   dtype=torch.float64, device=dev)
+        self.Xt = None
+        if self.mode == 0:
+            self.Xt = torch.empty_like(self.X)
+            _lib.check(self._lib.cvb_logistic_transpose_dev(self.X.data_ptr(), self.n, self.f, self.Xt.data_ptr(),
+                                                            _lib.stream_ptr()), "logistic_transpose")
+
+    def epoch(self, learning_rate: float) -> None:
+        lib, s = self._lib, _lib.stream_ptr()
+        wp = self.wb.data_ptr()
+        _lib.check(lib.cvb_logistic_grad_dev(self.X.data_ptr(), self.Xt.data_ptr() if self.Xt is not None else None,
+                                             self.y.data_ptr(), self.n, self.f, wp, wp + 8 * self.f, self.mode,
+                                             self.g.data_ptr(), self.scratch.data_ptr(), s), "logistic_grad")
+        if self.group is not None:
+            import torch.distributed as dist
+
+            dist.all_reduce(self.g, op=dist.ReduceOp.SUM, group=self.group)
+        _lib.check(lib.cvb_logistic_apply_dev(self.g.data_ptr(), self.f, float(learning_rate), float(self.n_total),
+                                              wp, wp + 8 * self.f, _lib.stream_ptr()), "logistic_apply")
+
+    def train(self, learning_rate: float, epochs: int):
+        for _ in range(max(0, int(epochs))):
+            self.epoch(learning_rate)
+        return self.weights()
+
+    def weights(self):
+        wb = self.wb.cpu().numpy()
+        return wb[:-1].copy(), float(wb[-1])
+
+
 def run_training(params: dict, csv_text: str) -> bytes:
     """Deterministic model bytes for fixed params and dataset (workload.py:48-71)."""
     X, y = parse_dataset_arrays(csv_text)
     lr = float(params.get("learning_rate", 0.1))
-    epochs = int(params.get("epochs", 50))
+    epochs = max(0, int(params.get("epochs", 50)))   # range(epochs) runs none for epochs < 0
     exact = bool(params.get("exact", True))
     w, b = train_arrays(X, y, lr, epochs, exact)
     return serialize_model(list(w), b)

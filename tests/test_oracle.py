@@ -97,3 +97,14 @@ def test_parse_dataset_mirrors_reference():
 def test_model_serialization_round_trip():
     w, b = [0.25, -1.5, 3.0], 0.125
     assert workload.deserialize_model(workload.serialize_model(w, b)) == (w, b)
+
+
+def test_shard_rows_partitions_in_order():
+    from paper_2103_16898_b200.workload import shard_rows
+
+    for n in (0, 1, 5, 60, 2001):
+        for world in (1, 2, 3, 8):
+            blocks = [shard_rows(n, world, r) for r in range(world)]
+            assert blocks[0][0] == 0 and blocks[-1][1] == n
+            assert all(blocks[i][1] == blocks[i + 1][0] for i in range(world - 1))
+            assert max(h - l for l, h in blocks) - min(h - l for l, h in blocks) <= 1
