@@ -43,6 +43,11 @@ int cvb_aead_open(const uint8_t key[32], const uint8_t nonce[12], const uint8_t*
 int cvb_aead_seal(const uint8_t key[32], const uint8_t nonce[12], const uint8_t* aad, size_t aad_len,
                   const uint8_t* pt, size_t len, uint8_t* out);
 
+/* Volume.put's seal and blob name (pkg/src/covault/volume.py:168-171) in one round trip: out gets
+ * C || T, digest = SHA-256(C || T) computed on the device.  Synchronous; host buffers. */
+int cvb_aead_seal_named(const uint8_t key[32], const uint8_t nonce[12], const uint8_t* aad, size_t aad_len,
+                        const uint8_t* pt, size_t len, uint8_t* out, uint8_t digest[32]);
+
 /* FIPS-197 single block (host) -- self test of the key schedule the kernels use. */
 int cvb_aes256_encrypt_block_host(const uint8_t key[32], const uint8_t in[16], uint8_t out[16]);
 
@@ -98,6 +103,10 @@ int cvb_records_to_nhwc(const uint8_t* pt_dev, int64_t nrec, int64_t rec_bytes, 
  * sequential chain); digests_dev gets 32 bytes per message.  offsets_dev: n+1 int64 byte offsets
  * into data_dev (device memory).  Asynchronous. */
 int cvb_sha256_batch_dev(const uint8_t* data_dev, const int64_t* offsets_dev, int64_t n, uint8_t* digests_dev,
+                         void* stream);
+/* Span form: message i = ptrs_dev[i][0 .. lens_dev[i]) (pointer / length arrays in device memory,
+ * messages in separate allocations).  Asynchronous. */
+int cvb_sha256_spans_dev(const uint8_t* const* ptrs_dev, const int64_t* lens_dev, int64_t n, uint8_t* digests_dev,
                          void* stream);
 /* Host-buffer form: n messages (pointer + length each) -> n x 32 digest bytes.  Synchronous. */
 int cvb_sha256_batch(const uint8_t* const* msgs, const size_t* lens, int64_t n, uint8_t* digests);

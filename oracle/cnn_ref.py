@@ -76,6 +76,27 @@ class RefModel(torch.nn.Module):
         self.params = torch.nn.ParameterDict({k.replace(".", "__"): torch.nn.Parameter(v.clone().float())
                                               for k, v in state.items()})
         self.running = {}
+        # mask matching (tests/cnn_parity.py): ReLU masks and 2x2 max-pool arg-max positions
+        # taken from the GPU's own forward pass, so fp32-summation-order noise cannot toggle a
+        # near-zero pre-activation or a near-tie window between the two runs; the oracle still
+        # computes every value itself
+        self.forced_relu, self.forced_pool = {}, {}
+
+    def force(self, relu_masks=None, pool_argmax=None):
+        self.forced_relu = dict(relu_masks or {})
+        self.forced_pool = dict(pool_argmax or {})
+
+    def relu(self, y, site):
+        m = self.forced_relu.get(site)
+        return F.relu(y) if m is None else y * m
+
+    def maxpool2(self, x, site):
+        idx = self.forced_pool.get(site)
+        if idx is None:
+            return F.max_pool2d(x, 2)
+        n, c, h, w = x.shape
+        win = x.reshape(n, c, h // 2, 2, w // 2, 2).permute(0, 1, 2, 4, 3, 5).reshape(n, c, h // 2, w // 2, 4)
+        return win.gather(-1, idx.unsqueeze(-1)).squeeze(-1)
 
     def P(self, name):
         return self.params[name.replace(".", "__")]
@@ -92,7 +113,7 @@ class RefModel(torch.nn.Module):
         if res is not None:
             y = y + res
         if relu:
-            y = F.relu(y)
+            y = self.relu(y, name)
         return R.rb(y)
 
     def linear(self, x, name, fout, out_f32=False, relu=False):
@@ -102,7 +123,7 @@ class RefModel(torch.nn.Module):
         wb = _bf16_param(w) if R.on else w
         y = x @ wb.t() + b
         if relu:
-            y = F.relu(y)
+            y = self.relu(y, name)
         return y if out_f32 else R.rb(y)
 
 
@@ -117,10 +138,10 @@ class SmallCNNRef(RefModel):
         R = self.R
         a = self.conv_bn(x, "conv1", 1, 1, cin_real=3)
         a = self.conv_bn(a, "conv2", 1, 1)
-        a = F.max_pool2d(a, 2)
+        a = self.maxpool2(a, "pool1")
         a = self.conv_bn(a, "conv3", 1, 1)
         a = self.conv_bn(a, "conv4", 1, 1)
-        a = F.max_pool2d(a, 2)
+        a = self.maxpool2(a, "pool2")
         flat = R.rb(a.permute(0, 2, 3, 1).reshape(a.shape[0], -1))   # NHWC flatten order
         h = self.linear(flat, "fc1", 256, relu=True)
         return self.linear(h, "fc2", self.num_classes, out_f32=True)
@@ -211,6 +232,21 @@ class RefTrainer:
     def __init__(self, name, state, emulate_bf16=True, lr=1e-3):
         self.model = REF_MODELS[name](state, emulate_bf16)
         self.opt = torch.optim.Adam(self.model.parameters(), lr=lr, betas=(0.9, 0.999), eps=1e-8, foreach=False)
+
+    def load(self, state, exp_avg=None, exp_avg_sq=None, step=0):
+        """Teacher forcing: start the next step from the given weights and Adam state (the GPU's
+        pre-step state), so one step is compared on identical parameters."""
+        with torch.no_grad():
+            for k, p in self.model.params.items():
+                name = k.replace("__", ".")
+                p.copy_(state[name])
+                if step > 0:
+                    st = self.opt.state[p]
+                    st["step"] = torch.tensor(float(step))
+                    st["exp_avg"] = exp_avg[name].clone().float()
+                    st["exp_avg_sq"] = exp_avg_sq[name].clone().float()
+                else:
+                    self.opt.state.pop(p, None)
 
     def step(self, x, labels):
         self.opt.zero_grad(set_to_none=False)

@@ -40,6 +40,7 @@ SIGNATURES = {
     "cvb_aes256_encrypt_block_host": (_INT, [_P, _P, _P]),
     "cvb_aead_open": (_INT, [_P, _P, _P, _SZ, _P, _SZ, _P]),
     "cvb_aead_seal": (_INT, [_P, _P, _P, _SZ, _P, _SZ, _P]),
+    "cvb_aead_seal_named": (_INT, [_P, _P, _P, _SZ, _P, _SZ, _P, _P]),
     "cvb_gcm_ctx_create": (_INT, [_P, _c.POINTER(_P)]),
     "cvb_gcm_ctx_destroy": (None, [_P]),
     "cvb_gcm_ctx_set_verdict": (_INT, [_P, _P]),
@@ -50,6 +51,7 @@ SIGNATURES = {
     "cvb_records_to_nhwc": (_INT, [_P, _I64, _I64, _I64, _I64, _I64, _P, _P, _INT, _P, _P, _P]),
     "cvb_sha256_batch_dev": (_INT, [_P, _P, _I64, _P, _P]),
     "cvb_sha256_batch": (_INT, [_P, _P, _I64, _P]),
+    "cvb_sha256_spans_dev": (_INT, [_P, _P, _I64, _P, _P]),
     "cvb_logistic_train": (_INT, [_P, _P, _I64, _I64, _c.c_double, _I64, _INT, _P, _P]),
     "cvb_logistic_scratch_doubles": (_I64, [_I64, _I64, _INT]),
     "cvb_logistic_transpose_dev": (_INT, [_P, _I64, _I64, _P, _P]),

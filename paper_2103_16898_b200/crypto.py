@@ -11,6 +11,7 @@ ciphertext and plaintext in HBM for the training loader.
 """
 from __future__ import annotations
 
+import collections
 import ctypes
 import hashlib
 import secrets
@@ -20,6 +21,10 @@ from . import _lib
 AEAD_NONCE_SIZE = 12
 SYMMETRIC_KEY_SIZE = 32
 KEY_COMMITMENT_TAG = b"covault.key-commitment.v1"   # crypto.py:38
+
+# host-API calls that ran on the GPU, by entry point (evidence that a patched reference
+# test suite really exercised this path; see tests/test_reference_suites_gpu.py)
+CALLS = collections.Counter()
 
 try:  # share exception identity with the reference when it is installed
     from covault.crypto import AuthenticationFailure, CryptoError, DecodeError  # type: ignore
@@ -72,6 +77,7 @@ def _key_bytes(key) -> bytes:
 
 def aead_seal(key, nonce: bytes, aad: bytes, plaintext: bytes) -> bytes:
     """AES-256-GCM seal on the GPU -> C || T (crypto.py:258-262)."""
+    CALLS["aead_seal"] += 1
     if len(nonce) != AEAD_NONCE_SIZE:
         raise DecodeError(f"nonce must be {AEAD_NONCE_SIZE} bytes")
     lib = _lib.load()
@@ -83,8 +89,25 @@ def aead_seal(key, nonce: bytes, aad: bytes, plaintext: bytes) -> bytes:
     return out.raw
 
 
+def aead_seal_named(key, nonce: bytes, aad: bytes, plaintext: bytes) -> tuple[bytes, bytes]:
+    """aead_seal plus SHA-256 of the sealed blob computed on the device in the same round trip:
+    (blob, digest) -- Volume.put's seal + blob name (volume.py:168-171)."""
+    CALLS["aead_seal"] += 1
+    if len(nonce) != AEAD_NONCE_SIZE:
+        raise DecodeError(f"nonce must be {AEAD_NONCE_SIZE} bytes")
+    lib = _lib.load()
+    _lib.bind_device()
+    kb = _key_bytes(key)
+    out = ctypes.create_string_buffer(len(plaintext) + 16)
+    dig = ctypes.create_string_buffer(32)
+    rc = lib.cvb_aead_seal_named(kb, bytes(nonce), bytes(aad), len(aad), bytes(plaintext), len(plaintext), out, dig)
+    _lib.check(rc, "aead_seal_named")
+    return out.raw, dig.raw
+
+
 def aead_open(key, nonce: bytes, aad: bytes, ciphertext: bytes) -> bytes:
     """AES-256-GCM open on the GPU; raises AuthenticationFailure on any mismatch."""
+    CALLS["aead_open"] += 1
     if len(nonce) != AEAD_NONCE_SIZE:
         raise DecodeError(f"nonce must be {AEAD_NONCE_SIZE} bytes")
     lib = _lib.load()
@@ -104,6 +127,7 @@ def sha256_many(messages) -> list[bytes]:
     the batched form of covault.crypto.hash_bytes (crypto.py:91-93)."""
     msgs = [bytes(m) for m in messages]
     n = len(msgs)
+    CALLS["sha256"] += n
     if n == 0:
         return []
     lib = _lib.load()
@@ -129,6 +153,25 @@ def sha256_device(data_dev, offsets_dev, stream=None):
             raise ValueError("offsets must be an int64 CUDA tensor")
         _lib.check(_lib.load().cvb_sha256_batch_dev(data_dev.data_ptr(), offsets_dev.data_ptr(), n, out.data_ptr(),
                                                     _lib.stream_ptr(stream)), "sha256_batch_dev")
+    return out
+
+
+def sha256_tensors(tensors, stream=None):
+    """Digests (uint8 CUDA tensor [n, 32]) of n uint8 CUDA tensors in separate allocations, one
+    launch; stream-ordered, nothing leaves HBM but the pointer/length table going in."""
+    import torch
+
+    _lib.bind_device()
+    n = len(tensors)
+    dev = tensors[0].device if n else torch.device("cuda")
+    out = torch.empty((n, 32), dtype=torch.uint8, device=dev)
+    if n:
+        meta = torch.tensor([t.data_ptr() for t in tensors] + [t.numel() for t in tensors], dtype=torch.int64)
+        meta = meta.pin_memory().to(dev, non_blocking=True)
+        if stream is not None:
+            meta.record_stream(stream)
+        _lib.check(_lib.load().cvb_sha256_spans_dev(meta.data_ptr(), meta.data_ptr() + 8 * n, n, out.data_ptr(),
+                                                    _lib.stream_ptr(stream)), "sha256_spans_dev")
     return out
 
 

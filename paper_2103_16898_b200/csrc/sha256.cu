@@ -60,13 +60,15 @@ __device__ __forceinline__ uint32_t ld_be32(const uint8_t* p, bool aligned) {
   return __byte_perm(v, 0, 0x0123);
 }
 
-__global__ void sha256_batch(const uint8_t* __restrict__ data, const int64_t* __restrict__ off, int64_t n,
-                             uint8_t* __restrict__ out) {
+// message m is data[off[m] .. off[m+1]) (arena form) or ptrs[m][0 .. off[m]) (span form)
+template <bool SPANS>
+__global__ void sha256_batch(const uint8_t* __restrict__ data, const uint8_t* const* __restrict__ ptrs,
+                             const int64_t* __restrict__ off, int64_t n, uint8_t* __restrict__ out) {
   CVB_PDL_PROLOGUE();
   const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= n) return;
-  const uint8_t* msg = data + off[m];
-  const uint64_t len = (uint64_t)(off[m + 1] - off[m]);
+  const uint8_t* msg = SPANS ? ptrs[m] : data + off[m];
+  const uint64_t len = SPANS ? (uint64_t)off[m] : (uint64_t)(off[m + 1] - off[m]);
   const bool aligned = ((uintptr_t)msg & 3) == 0;
   uint32_t st[8] = {0x6a09e667u, 0xbb67ae85u, 0x3c6ef372u, 0xa54ff53au,
                     0x510e527fu, 0x9b05688cu, 0x1f83d9abu, 0x5be0cd19u};
@@ -129,8 +131,22 @@ CVB_API int cvb_sha256_batch_dev(const uint8_t* data_dev, const int64_t* offsets
   if (n < 0 || (n && (!offsets_dev || !digests_dev))) { cvb_set_error("sha256_batch: bad arguments"); return CVB_EINVAL; }
   if (n == 0) return CVB_OK;
   const int threads = 64;   // many small CTAs: one message per thread, spread over all SMs
-  cvb_launch(sha256_batch, (unsigned)((n + threads - 1) / threads), threads, 0, (cudaStream_t)stream, data_dev,
-             offsets_dev, n, digests_dev);
+  cvb_launch(sha256_batch<false>, (unsigned)((n + threads - 1) / threads), threads, 0, (cudaStream_t)stream, data_dev,
+             (const uint8_t* const*)nullptr, offsets_dev, n, digests_dev);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+// Asynchronous span form: message i is ptrs_dev[i][0 .. lens_dev[i]) -- messages in separate
+// device allocations (e.g. a gate copy's plaintext and its re-sealed blob), pointer and length
+// arrays in device memory.
+CVB_API int cvb_sha256_spans_dev(const uint8_t* const* ptrs_dev, const int64_t* lens_dev, int64_t n,
+                                 uint8_t* digests_dev, void* stream) {
+  if (n < 0 || (n && (!ptrs_dev || !lens_dev || !digests_dev))) { cvb_set_error("sha256_spans: bad arguments"); return CVB_EINVAL; }
+  if (n == 0) return CVB_OK;
+  const int threads = 64;
+  cvb_launch(sha256_batch<true>, (unsigned)((n + threads - 1) / threads), threads, 0, (cudaStream_t)stream,
+             (const uint8_t*)nullptr, ptrs_dev, lens_dev, n, digests_dev);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }

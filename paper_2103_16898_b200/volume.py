@@ -151,8 +151,9 @@ class Volume:
             raise VolumeLocked(f"another writer holds {self.root}") from None
         try:
             nonce = _crypto.fresh_nonce()
-            blob = _crypto.aead_seal(key, nonce, aad_for(self.volume_name, logical_path), plaintext)
-            h = hashlib.sha256(blob).hexdigest()
+            # seal and blob name (SHA-256 of the sealed blob) in one device round trip
+            blob, digest = _crypto.aead_seal_named(key, nonce, aad_for(self.volume_name, logical_path), plaintext)
+            h = digest.hex()
             (self.root / h).write_bytes(blob)
             old = self._entries.get(logical_path)
             self._entries[logical_path] = ManifestEntry(logical_path, nonce, h, len(plaintext))
@@ -163,9 +164,11 @@ class Volume:
             os.close(fd)
             (self.root / LOCK_NAME).unlink(missing_ok=True)
 
-    def put_sealed(self, key, logical_path: str, nonce: bytes, blob: bytes, plaintext_length: int) -> None:
+    def put_sealed(self, key, logical_path: str, nonce: bytes, blob: bytes, plaintext_length: int,
+                   blob_digest: bytes | None = None) -> None:
         """Install a blob already sealed under this volume's key/AAD (the GPU gate copy
-        seals on the device); same lock / naming / manifest discipline as put()."""
+        seals on the device and hashes the blob there: ``blob_digest``); same lock / naming /
+        manifest discipline as put()."""
         _check_path(logical_path)
         if key_id_hex(key) != self.key_id:
             raise KeyMismatch("key commitment does not match the volume manifest")
@@ -174,7 +177,7 @@ class Volume:
         except FileExistsError:
             raise VolumeLocked(f"another writer holds {self.root}") from None
         try:
-            h = hashlib.sha256(blob).hexdigest()
+            h = (blob_digest if blob_digest is not None else _crypto.sha256_many([blob])[0]).hex()
             (self.root / h).write_bytes(blob)
             old = self._entries.get(logical_path)
             self._entries[logical_path] = ManifestEntry(logical_path, nonce, h, plaintext_length)
@@ -231,22 +234,45 @@ class Volume:
                 raise AuthenticationFailure("AEAD authentication failed")
         return out[: e.plaintext_length], work
 
-    def verify(self) -> list[tuple[str, str]]:
-        """Key-free integrity scan (volume.py:199-222): (kind, path) pairs."""
+    def verify(self, batch_bytes: int = 1 << 30) -> list[tuple[str, str]]:
+        """Key-free integrity scan (volume.py:199-222): (kind, path) pairs.  Blob digests are
+        computed on the GPU, one launch per ~``batch_bytes`` of blobs (one thread per blob)."""
         violations = []
         referenced = set()
+        pending = []          # (path, expected hex, blob bytes) awaiting a hash batch
+        results = {}
+
+        def flush():
+            if pending:
+                for (p, _, _), d in zip(pending, _crypto.sha256_many([b for _, _, b in pending])):
+                    results[p] = d.hex()
+                pending.clear()
+
+        checks = []
+        size = 0
         for path, e in sorted(self._entries.items()):
             try:
                 _check_path(path)
             except VolumeError:
-                violations.append(("bad_path", path))
+                checks.append(("bad_path", path, None))
                 continue
             bp = self.root / e.ciphertext_hash
             referenced.add(e.ciphertext_hash)
             if not bp.exists():
-                violations.append(("missing_blob", path))
+                checks.append(("missing_blob", path, None))
                 continue
-            if hashlib.sha256(bp.read_bytes()).hexdigest() != e.ciphertext_hash:
+            blob = bp.read_bytes()
+            pending.append((path, e.ciphertext_hash, blob))
+            checks.append(("hash", path, e.ciphertext_hash))
+            size += len(blob)
+            if size >= batch_bytes:
+                flush()
+                size = 0
+        flush()
+        for kind, path, want in checks:
+            if kind != "hash":
+                violations.append((kind, path))
+            elif results[path] != want:
                 violations.append(("hash_mismatch", path))
         for child in self.root.iterdir():
             if child.name in (MANIFEST_NAME, LOCK_NAME) or child.name.endswith(".tmp"):
@@ -282,40 +308,45 @@ def unseal_tree(volume: Volume, key, dest) -> int:
 
 
 def gate_copy(source: Volume, source_key, dest: Volume, dest_key) -> list[tuple[str, str, int]]:
-    """The trusted-boot gate's copy loop (gate.py:186-190) with the crypto on the device:
-    each source blob is copied to HBM once, opened (tag verified on the device), re-sealed
-    under the destination key / AAD / a fresh nonce without the plaintext leaving HBM, and
-    the sealed blob comes back for the destination volume.  Returns the copy report's
-    (path, SHA-256(plaintext) hex, length) entries; the plaintext digest is computed on the
-    device-resident plaintext after a D2H into pinned memory of the gate's own address space
-    (the reference holds the same plaintext in host memory).  Raises AuthenticationFailure on
-    the first bad source blob -- the gate maps it to "volume_auth_failure" and discards the
-    staging volume, exactly as gate.py:191-192 does."""
+    """The trusted-boot gate's copy loop (gate.py:186-190) with every byte of plaintext kept in
+    HBM: each source blob is copied to the device once, opened (tag verified on the device),
+    re-sealed under the destination key / AAD / a fresh nonce, and both the plaintext digest
+    for the copy report and the sealed blob's name are computed by the device SHA-256 -- only
+    the sealed blob and two digests come back to the host.  Raises AuthenticationFailure on
+    the first bad source blob (the gate maps it to "volume_auth_failure" and discards the
+    staging volume, gate.py:191-192)."""
     import torch
 
-    src_ctx, dst_ctx = _crypto.GcmContext(source_key), _crypto.GcmContext(dest_key)
     if key_id_hex(dest_key) != dest.key_id:
         raise KeyMismatch("key commitment does not match the destination manifest")
+    src_ctx, dst_ctx = _crypto.GcmContext(source_key), _crypto.GcmContext(dest_key)
     report = []
     work_o, work_s = src_ctx.new_workspace(), dst_ctx.new_workspace()
-    for logical_path in source.paths():
-        e = source.entry(logical_path)
-        blob = source.read_blob(logical_path)
-        if len(blob) < 16 or len(blob) - 16 != e.plaintext_length:
-            raise AuthenticationFailure("blob length disagrees with manifest")
-        n = e.plaintext_length
-        blob_dev = torch.frombuffer(bytearray(blob), dtype=torch.uint8).pin_memory().to("cuda", non_blocking=True)
-        aad_s = torch.frombuffer(bytearray(aad_for(source.volume_name, logical_path)), dtype=torch.uint8).cuda()
-        aad_d = torch.frombuffer(bytearray(aad_for(dest.volume_name, logical_path)), dtype=torch.uint8).cuda()
-        pt = torch.empty(max(1, n), dtype=torch.uint8, device="cuda")
-        src_ctx.open_device(e.nonce, aad_s, blob_dev, pt, work_o)
-        if not src_ctx.status_ok(work_o):          # tag verdict before anything is re-sealed
-            raise AuthenticationFailure("AEAD authentication failed")
-        nonce = _crypto.fresh_nonce()
-        sealed = torch.empty(n + 16, dtype=torch.uint8, device="cuda")
-        dst_ctx.seal_device(nonce, aad_d, pt[:n], sealed, work_s)
-        out = sealed.cpu().numpy().tobytes()
-        digest = hashlib.sha256(pt[:n].cpu().numpy().tobytes()).hexdigest()
-        dest.put_sealed(dest_key, logical_path, nonce, out, n)
-        report.append((logical_path, digest, n))
+    try:
+        for logical_path in source.paths():
+            e = source.entry(logical_path)
+            blob = source.read_blob(logical_path)
+            if len(blob) < 16 or len(blob) - 16 != e.plaintext_length:
+                raise AuthenticationFailure("blob length disagrees with manifest")
+            n = e.plaintext_length
+            blob_dev = torch.frombuffer(bytearray(blob), dtype=torch.uint8).pin_memory().to("cuda", non_blocking=True)
+            aad_s = torch.frombuffer(bytearray(aad_for(source.volume_name, logical_path)), dtype=torch.uint8).cuda()
+            aad_d = torch.frombuffer(bytearray(aad_for(dest.volume_name, logical_path)), dtype=torch.uint8).cuda()
+            pt = torch.empty(max(1, n), dtype=torch.uint8, device="cuda")
+            work_o.zero_()
+            src_ctx.open_device(e.nonce, aad_s, blob_dev, pt, work_o)
+            if not src_ctx.status_ok(work_o):          # tag verdict before anything is re-sealed
+                raise AuthenticationFailure("AEAD authentication failed")
+            nonce = _crypto.fresh_nonce()
+            sealed = torch.empty(n + 16, dtype=torch.uint8, device="cuda")
+            work_s.zero_()
+            dst_ctx.seal_device(nonce, aad_d, pt[:n], sealed, work_s)
+            digests = _crypto.sha256_tensors([pt[:n], sealed]).cpu().numpy()   # plaintext, blob name
+            pt.zero_()
+            dest.put_sealed(dest_key, logical_path, nonce, sealed.cpu().numpy().tobytes(), n,
+                            blob_digest=bytes(digests[1]))
+            report.append((logical_path, bytes(digests[0]).hex(), n))
+    finally:
+        src_ctx.close()
+        dst_ctx.close()
     return report

@@ -136,6 +136,9 @@ class LogisticTrainer:
 
 def run_training(params: dict, csv_text: str) -> bytes:
     """Deterministic model bytes for fixed params and dataset (workload.py:48-71)."""
+    from .crypto import CALLS
+
+    CALLS["run_training"] += 1
     X, y = parse_dataset_arrays(csv_text)
     lr = float(params.get("learning_rate", 0.1))
     epochs = max(0, int(params.get("epochs", 50)))   # range(epochs) runs none for epochs < 0

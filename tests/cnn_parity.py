@@ -101,6 +101,88 @@ def check(report, wrel, model):
     assert wrel <= W_TOL, wrel
 
 
+# ---- mask-matched, teacher-forced per-step parity ------------------------------------------
+# Every step starts the oracle from the GPU's pre-step weights and Adam moments, and the
+# oracle's ReLU masks and max-pool arg-max positions are the GPU's own (read back from the
+# GPU's stored activations after its step).  What remains is pure arithmetic noise (fp32
+# summation order, bf16 rounding of a different fp32 sum), so each step's loss, EVERY
+# per-tensor gradient and every updated weight tensor are held to tight relative bounds:
+FORCED_LOSS_TOL = 1e-3      # |dL| <= 1e-3 * max(1, |L|)
+FORCED_GRAD_TOL = 1e-2      # ||g_gpu - g_ref|| <= 1e-2 * ||g_ref||, every parameter tensor
+FORCED_W_TOL = 1e-3         # ||w_gpu - w_ref|| <= 1e-3 * ||w_ref||, every parameter tensor
+
+
+def _nchw(t):
+    return t.detach().float().cpu().permute(0, 3, 1, 2).contiguous()
+
+
+def pool2_argmax(x_nchw):
+    """First arg-max (window order (0,0),(0,1),(1,0),(1,1)) of every 2x2/stride-2 window, the
+    tie rule of csrc/nn.cu maxpool2_bwd."""
+    n, c, h, w = x_nchw.shape
+    win = x_nchw.reshape(n, c, h // 2, 2, w // 2, 2).permute(0, 1, 2, 4, 3, 5).reshape(n, c, h // 2, w // 2, 4)
+    return win.argmax(dim=-1)
+
+
+def gpu_forcing(net, model):
+    """(ReLU masks, pool arg-max) of the GPU's last forward, keyed by oracle site names."""
+    if model == "small_cnn":
+        acts = {"conv1": net.a1, "conv2": net.a2, "conv3": net.a3, "conv4": net.a4}
+        masks = {k: (_nchw(v) > 0).float() for k, v in acts.items()}
+        masks["fc1"] = (net.h.detach().float().cpu() > 0).float()
+        return masks, {"pool1": pool2_argmax(_nchw(net.a2)), "pool2": pool2_argmax(_nchw(net.a4))}
+    if model == "resnet18":
+        masks = {"stem": (_nchw(net.x0) > 0).float()}
+        for i, (b, o) in enumerate(zip(net.blocks, net.outs)):
+            nm = f"layer{i // 2 + 1}.{i % 2}"
+            masks[f"{nm}.conv1"] = (_nchw(b.o1) > 0).float()
+            masks[f"{nm}.conv2"] = (_nchw(o) > 0).float()
+        return masks, {}
+    raise ValueError(f"no mask matching for {model}")
+
+
+def _moment_views(ps, buf):
+    return {name: buf[ps.offsets[name]:ps.offsets[name] + int(np.prod(shape))].view(shape).detach().cpu().clone()
+            for name, shape, _ in ps.specs}
+
+
+def run_forced(model="small_cnn", batch=64, steps=3, seed=0, lr=1e-3):
+    """Per step: (loss_gpu, loss_ref, {param: grad rel err}, {param: weight rel err})."""
+    spec = loader.CIFAR
+    net = nets.make_model(model, seed=seed).build(batch)
+    net.lr = lr
+    ref = RefTrainer(model, net.ps.state_cpu(), emulate_bf16=True, lr=lr)
+    out = []
+    for s in range(steps):
+        rec = make_records(batch, seed * 100 + s, c=spec["c"], h=spec["h"], w=spec["w"])
+        x, lab = gpu_inputs(rec, spec)
+        xr, labr = normalise_records(torch.from_numpy(rec), spec["c"], spec["h"], spec["w"], spec["mean"],
+                                     spec["std"], emulate_bf16=True)
+        k = int(net.ps.step_dev.item())
+        ref.load(net.ps.state_cpu(), _moment_views(net.ps, net.ps.m), _moment_views(net.ps, net.ps.v), step=k)
+        loss_gpu = float(net.step(x, lab).item())
+        torch.cuda.synchronize()
+        ref.model.force(*gpu_forcing(net, model))
+        loss_ref, g_ref = ref.step(xr, labr)
+        w_gpu, w_ref = net.ps.state_cpu(), ref.state()
+        grads, wts = {}, {}
+        for key, gr in g_ref.items():
+            name = key.replace("__", ".")
+            grads[name] = rel(net.ps.g[name].detach().float().cpu(), gr.float())
+            wts[name] = rel(w_gpu[name].float(), w_ref[name].float())
+        out.append((loss_gpu, loss_ref, grads, wts))
+    return out
+
+
+def check_forced(out):
+    for s, (lg, lr_, grads, wts) in enumerate(out):
+        assert abs(lg - lr_) <= FORCED_LOSS_TOL * max(1.0, abs(lr_)), (s, lg, lr_)
+        bad = {k: v for k, v in grads.items() if v > FORCED_GRAD_TOL}
+        assert not bad, (s, bad)
+        bad = {k: v for k, v in wts.items() if v > FORCED_W_TOL}
+        assert not bad, (s, bad)
+
+
 def one_step_check(batch=16, model="small_cnn"):
     report, wrel = run_parity(model, batch=batch, steps=2)
     check(report, wrel, model)

@@ -115,3 +115,42 @@ def test_missing_data_key_exits_3(tmp_path, golden):
     run = _run(tee, manager, artifact, vols2, roles2, policy="bob/solo")
     assert run.provisioned and run.exit_code == 3
     assert not (tmp_path / "v/solo-model").exists()
+
+
+def _tamper(vols, refs, index):
+    d = vols[refs["data"]]
+    entry = json.loads((d / "manifest.json").read_text())["entries"][index]
+    blob = d / entry["ciphertext_hash"]
+    raw = bytearray(blob.read_bytes())
+    raw[1000] ^= 1
+    blob.write_bytes(bytes(raw))
+
+
+def test_two_rank_cnn_training_through_attested_run(tmp_path, golden):
+    """world_size 2 (two spawned ranks sharing the one B200 over gloo): the artifact trains
+    data-parallel and seals one model."""
+    params = json.dumps({"model": "small_cnn", "epochs": 1, "batch_size": 16, "world_size": 2,
+                         "backend": "gloo"}).encode()
+    tee, manager, artifact, vols, roles, bob, refs = _lab(tmp_path, golden, _shards(4, 16), params)
+    run = _run(tee, manager, artifact, vols, roles)
+    assert run.provisioned and run.exit_code == 0, run.handle.diagnostics() if run.handle else run.reject_reason
+    _, bk = owner_fetch_keys(manager, "bob/trainer", bob)
+    from paper_2103_16898_b200.trainer import deserialize_cnn_model
+
+    header, _ = deserialize_cnn_model(Volume.open(vols[refs["model"]]).get(bk[refs["model"]], "model.bin"))
+    assert header["model"] == "SmallCNN"
+
+
+def test_two_rank_tampered_shard_on_rank1_exits_4_without_output(tmp_path, golden):
+    """A shard of rank 1 fails its tag: the verdict travels with the gradient all-reduce, both
+    ranks stop, the workload exits 4 and no model.bin is sealed (train.py:44-46)."""
+    params = json.dumps({"model": "small_cnn", "epochs": 1, "batch_size": 16, "world_size": 2,
+                         "backend": "gloo"}).encode()
+    tee, manager, artifact, vols, roles, bob, refs = _lab(tmp_path, golden, _shards(4, 16), params)
+    names = sorted(json.loads((vols[refs["data"]] / "manifest.json").read_text())["entries"],
+                   key=lambda e: e["path"])
+    idx = [e["path"] for e in names].index("shard-00003.bin")        # rank 1 owns shards 1 and 3
+    _tamper(vols, refs, idx)
+    run = _run(tee, manager, artifact, vols, roles)
+    assert run.provisioned and run.exit_code == 4
+    assert not (vols[refs["model"]] / "manifest.json").exists()
