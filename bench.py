@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--model", default="small_cnn")
+    ap.add_argument("--model", default="resnet18", choices=["resnet18", "small_cnn", "densenet121", "logistic"])
+    ap.add_argument("--rows", type=int, default=20000, help="logistic: CSV rows (x 3,072 features)")
     ap.add_argument("--batch", type=int, default=None, help="per-GPU batch (default: 512, DenseNet 128)")
     ap.add_argument("--shards", type=int, default=None, help="resident shards per rank (default: > 150 MB)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -329,23 +330,67 @@ def run_ours(args, rank, world, local_rank):
     ms_e2e = timed(e2e_loop(args.steps), args.steps)
     tr.check_status(include_pending=True)
 
-    # instrumented eager step (per-launch CUDA events) for the roofline and launch count
+    # ---- roofline ---------------------------------------------------------------------
+    # (1) one eager step through the kernel wrappers: launch count and, per kernel class, the
+    #     algorithmic FLOPs (2*M*N*K, real channel counts) and bytes of the step's launches.
     K.REC.timing, K.REC.records = True, []
     l0 = K.REC.launches
     tr.graph = None
-    from paper_2103_16898_b200 import nets as _nets
-    overlap = _nets._NO_OVERLAP
-    _nets._NO_OVERLAP = True   # per-launch events need the launches serial (no side-stream wgrads)
     resident(0)
     torch.cuda.synchronize()
-    _nets._NO_OVERLAP = overlap
     per_step_eager = K.REC.launches - l0
     K.REC.timing = False
-    summ = K.REC.summary()
-    step_ms_instr = sum(v[1] for v in summ.values())
-    dom = max(summ.items(), key=lambda kv: kv[1][1])
+    summ = K.REC.summary()            # {kind: [calls, ms (eager, not used), flops, bytes]}
+    tr.graph = True
+    # (2) per class, the in-graph time: a CUDA graph of the step captured with every other
+    #     class's launches filtered out (kernels.ONLY_CLASSES) replays exactly that class's
+    #     kernels back to back -- their time inside a graph, without launch gaps of an eager
+    #     replay and without the rest of the step in between.  The decrypt (outside the step
+    #     graphs) is timed the same way on its own stream.
+    def graph_ms(body, reps=20):
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                body()
+        torch.cuda.current_stream().wait_stream(s)
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    ar = tr.allreduce
+    if ar is not None:
+        ar.segment = lambda idx: None     # no collectives inside the measurement graphs
+    class_ms = {}
+    import warnings
+    with warnings.catch_warnings():
+        warnings.filterwarnings("ignore", message="The CUDA Graph is empty")
+        for kind in summ:
+            K.ONLY_CLASSES = {kind}
+            try:
+                class_ms[kind] = graph_ms(lambda: (tr._train_body(), tr._opt_body()))
+            finally:
+                K.ONLY_CLASSES = None
+        class_ms["decrypt"] = graph_ms(lambda: tr.ctx.open_records_device(shards[1][1], aads[1], cts[1], tr.loader.x,
+                                                                           tr.loader.labels, tr._works[0], spec))
+    if ar is not None:
+        ar.segment = None
+    tr.check_status(include_pending=True)
+    dec_bytes = len(shards[0][3]) + B * spec["h"] * spec["w"] * spec["c"] * 2 + B * 4   # C||T in, tile + labels out
+    summ["decrypt"] = [1, 0.0, 0, dec_bytes]
+    step_ms = ms / args.steps
+    kind = max(class_ms, key=class_ms.get)
+    calls, _, dfl, dby = summ[kind]
+    dms = class_ms[kind]
     hbm, tflops, src = peaks()
-    kind, (calls, dms, dfl, dby) = dom
     if dfl > 0:
         ach = dfl / (dms * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": ach, "peak": tflops, "unit": "TFLOP/s", "frac": ach / tflops}
@@ -357,19 +402,25 @@ def run_ours(args, rank, world, local_rank):
         tj = json.loads((ROOT / "profiles" / "traffic.json").read_text())[args.model]
         kd = tj["kinds"][kind]
         traffic = {"dram_bytes_per_launch": kd["dram_bytes"] / kd["launches"],
-                   "dram_bytes_per_step": kd["dram_bytes"],
-                   "algorithmic_bytes_per_step": dby if dfl == 0 else None, "source": tj["source"]}
+                   "dram_bytes_per_step": kd["dram_bytes"], "algorithmic_bytes_per_step": dby,
+                   "source": tj["source"]}
     except Exception:
         pass
     roof.update({"traffic": traffic, "kernel": kind, "launches_per_step": calls,
-                 "share_of_step": dms / step_ms_instr, "peak_source": src,
-                 "per_kind_ms": {k: round(v[1], 4) for k, v in summ.items()},
+                 "algorithmic_per_step": dfl if dfl > 0 else dby,
+                 "class_ms_in_graph": round(dms, 5), "share_of_step": dms / step_ms, "peak_source": src,
+                 "per_class_ms_in_graph": {k: round(v, 5) for k, v in sorted(class_ms.items(), key=lambda kv: -kv[1])},
+                 "method": "per-class CUDA graph of the step (other classes filtered out), 20 replays, CUDA events",
                  "algorithmic": "sum over the step's launches of 2*M*N*K (real channel counts)"
                  if dfl > 0 else "sum over the step's launches of each input read once + each output written once"})
+    if dfl > 0:   # the same class against HBM: its algorithmic bytes over the same time
+        roof["hbm_gbs_at_algorithmic_bytes"] = dby / (dms * 1e-3) / 1e9
     prof = ROOT / "profiles" / "roofline_live.json"
     if rank == 0:
         try:
-            prof.write_text(json.dumps({"summary": {k: v for k, v in summ.items()}, "roofline": roof}, indent=1))
+            prof.write_text(json.dumps({"model": args.model, "ms_per_step": step_ms,
+                                        "summary": {k: v for k, v in summ.items()}, "class_ms": class_ms,
+                                        "roofline": roof}, indent=1))
         except Exception:
             pass
 
@@ -410,6 +461,16 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     if os.environ.get("CVB_ONE_GPU"):   # test aid: run every rank on cuda:0 (use with CVB_DIST_BACKEND=gloo)
         local_rank = 0
+    if args.model == "logistic":   # the reference's own trainer (bench_logistic.py), one GPU
+        import bench_logistic as BL
+
+        if rank != 0:
+            return
+        if args.impl == "reference":
+            BL.run_reference(args, METRIC, UNIT)
+        else:
+            BL.run(args, METRIC, UNIT, peaks, ClockSampler)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

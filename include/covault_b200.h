@@ -111,6 +111,20 @@ int cvb_sha256_spans_dev(const uint8_t* const* ptrs_dev, const int64_t* lens_dev
 /* Host-buffer form: n messages (pointer + length each) -> n x 32 digest bytes.  Synchronous. */
 int cvb_sha256_batch(const uint8_t* const* msgs, const size_t* lens, int64_t n, uint8_t* digests);
 
+/* ---- bit-exact CSV parse (covault.workload.parse_dataset, pkg/src/covault/workload.py:24-41) ---- */
+
+/* ASCII dataset text in HBM (ending with a line break) -> rows of binary64 features + label, every
+ * field converted exactly like Python float() (correctly rounded).  Two passes:
+ *   index: line / field structure; info = {rows, F, min fields, max fields, lines, fields}
+ *   fill:  X (rows x F, row-major) and y (rows) when every data row has F+1 fields;
+ *          err = {line, column, line start, line end} of the first too-short row or invalid
+ *          number in file order, or -1s.
+ * Both synchronise `stream`.  cvb_csv_free releases the index. */
+typedef struct cvb_csv cvb_csv;
+int cvb_csv_index(const uint8_t* text_dev, size_t len, int64_t info[6], cvb_csv** out, void* stream);
+int cvb_csv_fill(cvb_csv* csv, double* X_dev, double* y_dev, int64_t err[4]);
+void cvb_csv_free(cvb_csv* csv);
+
 /* ---- reference trainer ---------------------------------------------------------------- */
 
 /* Numeric core of covault.workload.run_training (pkg/src/covault/workload.py:48-71).

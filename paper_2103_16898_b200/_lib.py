@@ -52,6 +52,9 @@ SIGNATURES = {
     "cvb_sha256_batch_dev": (_INT, [_P, _P, _I64, _P, _P]),
     "cvb_sha256_batch": (_INT, [_P, _P, _I64, _P]),
     "cvb_sha256_spans_dev": (_INT, [_P, _P, _I64, _P, _P]),
+    "cvb_csv_index": (_INT, [_P, _SZ, _P, _c.POINTER(_P), _P]),
+    "cvb_csv_fill": (_INT, [_P, _P, _P, _P]),
+    "cvb_csv_free": (None, [_P]),
     "cvb_logistic_train": (_INT, [_P, _P, _I64, _I64, _c.c_double, _I64, _INT, _P, _P]),
     "cvb_logistic_scratch_doubles": (_I64, [_I64, _I64, _INT]),
     "cvb_logistic_transpose_dev": (_INT, [_P, _I64, _I64, _P, _P]),

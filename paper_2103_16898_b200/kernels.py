@@ -73,8 +73,43 @@ def _stream():
     return torch.cuda.current_stream().cuda_stream
 
 
+# launch entry point -> kernel class (the roofline / per-class timing vocabulary of bench.py)
+LAUNCH_CLASS = {
+    **{n: "umma_gemm" for n in ("cvb_conv2d_fwd", "cvb_conv2d_wgrad", "cvb_gemm", "cvb_gemm_ex",
+                                "cvb_conv2d_dgrad_s2")},
+    **{n: "bn" for n in ("cvb_bn_stats", "cvb_bn_forward", "cvb_bn_apply", "cvb_bn_backward",
+                         "cvb_bn_backward_fused")},
+    **{n: "pool" for n in ("cvb_maxpool_fwd", "cvb_maxpool_fwd_idx", "cvb_maxpool_bwd", "cvb_maxpool_bwd_idx",
+                           "cvb_avgpool_fwd", "cvb_avgpool_bwd", "cvb_gap_fwd", "cvb_gap_bwd")},
+    **{n: "head" for n in ("cvb_softmax_xent", "cvb_head_train")},
+    **{n: "reduce" for n in ("cvb_reduce_splits", "cvb_reduce_splits_act", "cvb_col_sum")},
+    **{n: "layout" for n in ("cvb_weight_flip", "cvb_weight_flip_batched", "cvb_space_to_depth2", "cvb_s2d_weights",
+                             "cvb_s2d_weights_grad", "cvb_zero_upsample", "cvb_cast_rows", "cvb_cast_f32_bf16")},
+    **{n: "eltwise" for n in ("cvb_relu_fwd", "cvb_relu_bwd")},
+    **{n: "optimizer" for n in ("cvb_adam_step", "cvb_sgd_step")},
+    "cvb_verdict_snapshot": "verdict",
+}
+# Measurement only (bench.py): when set to a set of class names, launches of every other class
+# become no-ops, so a CUDA graph captured under the filter replays exactly that class's
+# kernels of a step -- their in-graph time without the rest of the step in between.
+ONLY_CLASSES = None
+
+
+class _ClassFilter:
+    def __init__(self, lib, keep):
+        self._lib, self._keep = lib, keep
+
+    def __getattr__(self, name):
+        cls = LAUNCH_CLASS.get(name)
+        if cls is None or cls in self._keep:
+            return getattr(self._lib, name)
+        return lambda *args: 0
+
+
 def _lib_bound():
     _lib.bind_device()
+    if ONLY_CLASSES is not None:
+        return _ClassFilter(_lib.load(), ONLY_CLASSES)
     return _lib.load()
 
 
@@ -99,7 +134,9 @@ def conv2d_fwd(x, w, stride=1, pad=0, bias=None, out=None, out_f32=False, cin=No
     ycs = out.shape[-1]
     assert out.shape[:3] == (n, oh, ow) and (out.dtype == F32) == bool(out_f32)
     flops = acct_flops if acct_flops is not None else 2 * n * oh * ow * cout * kh * kw * cin
-    tok = REC.begin(1, kind, flops)
+    # algorithmic bytes: input and weights read once, output written once (+ read when accumulating)
+    nbytes = 2 * (n * h * wd * cin + w.numel()) + n * oh * ow * cout * out.element_size() * (2 if accumulate else 1)
+    tok = REC.begin(1, kind, flops, nbytes)
     rc = lib.cvb_conv2d_fwd(x.data_ptr(), n, h, wd, cin, x.stride(2), w.data_ptr(), cout, kh, kw, stride, pad,
                             out.data_ptr(), oh, ow, ycs, out_coff, _ptr(bias), int(out_f32), int(accumulate),
                             _stream())
@@ -118,7 +155,9 @@ def conv2d_dgrad_s2(dy, w, pad, dx, accumulate=False, wscratch=None, acct_flops=
     if wscratch is None:
         wscratch = torch.empty(w.numel(), dtype=BF16, device=w.device)
     lib = _lib_bound()
-    tok = REC.begin(5, "umma_gemm", acct_flops if acct_flops is not None else 2 * n * oh * ow * cout * kh * kw * cin)
+    nbytes = 2 * (dy.numel() + w.numel() + n * h * wd * cin * (2 if accumulate else 1))
+    tok = REC.begin(5, "umma_gemm", acct_flops if acct_flops is not None else 2 * n * oh * ow * cout * kh * kw * cin,
+                    nbytes)
     rc = lib.cvb_conv2d_dgrad_s2(dy.data_ptr(), n, oh, ow, cout, dy.stride(2), w.data_ptr(), cin, kh, kw, pad,
                                  dx.data_ptr(), h, wd, dx.stride(2), int(accumulate), wscratch.data_ptr(), _stream())
     REC.end(tok)
@@ -139,7 +178,8 @@ def conv2d_wgrad_partials(dy, x, kh, kw, stride, pad, cin=None, max_splits=148, 
         part = torch.empty((max_splits, cout, ncols), dtype=F32, device=dy.device)
     used = ctypes.c_int(0)
     flops = acct_flops if acct_flops is not None else 2 * n * oh * ow * cout * ncols
-    tok = REC.begin(1, "umma_gemm", flops)
+    nbytes = 2 * (dy.numel() + n * h * wd * cin) + 4 * cout * ncols   # dY, X read once; dW (fp32) written once
+    tok = REC.begin(1, "umma_gemm", flops, nbytes)
     rc = lib.cvb_conv2d_wgrad(dy.data_ptr(), n, oh, ow, cout, dy.stride(2), x.data_ptr(), h, wd, cin, x.stride(2),
                               kh, kw, stride, pad, part.data_ptr(), min(max_splits, part.shape[0]),
                               ctypes.byref(used), _stream())
@@ -162,7 +202,8 @@ def gemm(a, b, M, N, K, a_major=0, b_major=0, out=None, out_f32=False, bias=None
             out = torch.empty((used, M, N), dtype=F32, device=a.device)
         else:
             out = torch.empty((M, N), dtype=F32 if out_f32 else BF16, device=a.device)
-    tok = REC.begin(1, "umma_gemm", acct_flops if acct_flops is not None else 2 * M * N * K)
+    nbytes = 2 * (M * K + N * K) + M * N * (4 if (out_f32 or used > 1) else 2)   # A, B once; C once
+    tok = REC.begin(1, "umma_gemm", acct_flops if acct_flops is not None else 2 * M * N * K, nbytes)
     rc = lib.cvb_gemm_ex(a.data_ptr(), a_major, a.stride(0), b.data_ptr(), b_major, b.stride(0), M, N, K,
                          out.data_ptr(), out.stride(-2), int(out_f32 or used > 1), _ptr(bias), splits, int(accumulate),
                          max_bn, _stream())

@@ -388,10 +388,12 @@ class Net:
     def fwd_bwd(self, x, labels):
         """Forward, loss and backward of one step (gradients in ps.g32, loss in self.loss)."""
         ps = self.ps
-        # wgrad/dgrad overlap on a side stream: single GPU only (the data-parallel capture is cut
-        # into per-bucket graph segments, which must not end with side-stream work outstanding)
+        # wgrad/dgrad overlap on a side stream: single GPU, or data parallel with the collectives
+        # captured inside the step graph (a segmented capture must not end a segment with
+        # side-stream work outstanding)
         ps.side, ps.side_used = None, False
-        if not _NO_OVERLAP and ps.grad_hook is None and torch.cuda.is_available():
+        if not _NO_OVERLAP and (ps.grad_hook is None or getattr(ps, "overlap_with_hook", False)) \
+                and torch.cuda.is_available():
             if getattr(self, "_side", None) is None:
                 self._side = torch.cuda.Stream()
             ps.side = self._side

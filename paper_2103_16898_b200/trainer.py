@@ -115,9 +115,13 @@ class OverlappedGradAllReduce:
         if self.side is None:
             self.works.append(self.dist.all_reduce(view, op=self.dist.ReduceOp.SUM, group=self.group, async_op=True))
             return
-        ev = torch.cuda.Event()
-        ev.record(torch.cuda.current_stream())
-        self.side.wait_event(ev)
+        # the bucket's gradients come from the compute stream and, with the wgrad overlap on,
+        # from the wgrad side stream: the collective waits for both
+        cur = torch.cuda.current_stream()
+        self.side.wait_stream(cur)
+        wg = self.ps.side
+        if wg is not None and wg != cur:
+            self.side.wait_stream(wg)
         with torch.cuda.stream(self.side):
             self.dist.all_reduce(view, op=self.dist.ReduceOp.SUM, group=self.group)
 
@@ -144,7 +148,7 @@ class OverlappedGradAllReduce:
 
 class EncryptedTrainer:
     def __init__(self, model="small_cnn", key: bytes = bytes(range(32)), batch=512, spec=CIFAR, seed=0,
-                 world=1, rank=0, max_shard_bytes=None, lr=1e-3, force_allreduce=False):
+                 world=1, rank=0, max_shard_bytes=None, lr=1e-3, force_allreduce=False, graph_collectives=None):
         self.spec, self.batch, self.world, self.rank = spec, batch, world, rank
         self.net = make_model(model, seed=seed).build(batch, global_batch=batch * world)
         self.net.lr = lr
@@ -155,6 +159,18 @@ class EncryptedTrainer:
         if world > 1 or force_allreduce:
             self.allreduce = OverlappedGradAllReduce(self.net.ps)
             self.net.ps.grad_hook = self.allreduce
+        # NCCL collectives are capturable: the whole step (backward + bucket all-reduces on the
+        # side stream + optimiser) is then ONE graph replay with no host issue between buckets,
+        # and the wgrad side-stream overlap stays on.  gloo is not: its steps are captured as
+        # segments cut at bucket boundaries, the all-reduces issued between segment replays.
+        if graph_collectives is None:
+            graph_collectives = False
+            if self.allreduce is not None:
+                import torch.distributed as dist
+
+                graph_collectives = dist.is_initialized() and dist.get_backend() == "nccl"
+        self.graph_collectives = bool(graph_collectives) and self.allreduce is not None
+        self.net.ps.overlap_with_hook = self.graph_collectives
         self.graph = None
         # sticky run verdict: every shard opened through self.ctx ORs its tag verdict into this
         # word; each step snapshots it into the gradient buffer's verdict slot (summed over
@@ -193,6 +209,23 @@ class EncryptedTrainer:
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
         pool = torch.cuda.graph_pool_handle()
+        if self.graph_collectives:
+            # one graph: forward, backward with the bucket all-reduces issued from the grad-ready
+            # hooks on the collective side stream as buckets complete, the join, the optimiser
+            self.segments, self.tail_from = [], len(ar.buckets)
+            self.g_train = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s):
+                self.g_train.capture_begin(pool=pool)
+                self._train_body()
+                ar.finish()
+                self.g_train.capture_end()
+            self.g_opt = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.g_opt, pool=pool):
+                self._opt_body()
+            torch.cuda.current_stream().wait_stream(s)
+            self.graph = True
+            self.net.ps.step_dev.zero_()
+            return
         self.segments = []
         cur = [torch.cuda.CUDAGraph()]
         if ar is not None:
@@ -228,7 +261,7 @@ class EncryptedTrainer:
                 for i in idx:
                     ar.launch_bucket(i)
             self.g_train.replay()
-            if ar is not None:
+            if ar is not None and not self.graph_collectives:
                 for i in range(self.tail_from, len(ar.buckets)):
                     ar.launch_bucket(i)
                 ar.join()

@@ -46,6 +46,55 @@ def parse_dataset(csv_text: str) -> list[tuple[list[float], float]]:
     return rows
 
 
+_LINE_BREAKS = ("\n", "\r", "\x0b", "\x0c", "\x1c", "\x1d", "\x1e")
+
+
+def parse_dataset_device(csv_text: str, device=None):
+    """parse_dataset on the GPU: (X float64 CUDA tensor [rows, F], y float64 CUDA tensor [rows]),
+    bit-identical to the reference's Python float() values, same exceptions in the same
+    precedence (WorkloadError for a short row / empty / ragged dataset, ValueError for a field
+    float() rejects).  ASCII text only -- the reference's Unicode line-break / whitespace /
+    digit handling is not restated on the device; callers check ``csv_text.isascii()``."""
+    import ctypes
+
+    import torch
+
+    if not csv_text.isascii():
+        raise ValueError("parse_dataset_device: ASCII text only")
+    _lib.bind_device()
+    lib = _lib.load()
+    raw = csv_text.encode("ascii")
+    if not raw.endswith(tuple(c.encode() for c in _LINE_BREAKS)):
+        raw += b"\n"      # every line ends with a break (splitlines drops a final empty line)
+    host = torch.frombuffer(bytearray(raw), dtype=torch.uint8)
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    text = host.pin_memory().to(dev, non_blocking=True)
+    info = (ctypes.c_int64 * 6)()
+    h = ctypes.c_void_p()
+    _lib.check(lib.cvb_csv_index(text.data_ptr(), len(raw), info, ctypes.byref(h), _lib.stream_ptr()), "csv_index")
+    try:
+        rows, F, nf_min, nf_max = info[0], info[1], info[2], info[3]
+        X = torch.empty((rows, max(F, 0)), dtype=torch.float64, device=dev)
+        y = torch.empty(rows, dtype=torch.float64, device=dev)
+        err = (ctypes.c_int64 * 4)()
+        _lib.check(lib.cvb_csv_fill(h, X.data_ptr() if X.numel() else None, y.data_ptr() if rows else None, err),
+                   "csv_fill")
+    finally:
+        lib.cvb_csv_free(h)
+    if err[0] >= 0:   # the first failing row, in file order -- the reference raises there
+        line = raw[err[2]:err[3]].decode("ascii").strip()
+        fields = line.split(",")
+        if len(fields) < 2:
+            raise WorkloadError(f"bad dataset row {line!r}")
+        float(fields[err[1]])       # raises Python's own ValueError (message) for this field
+        raise RuntimeError(f"device CSV parser rejected {fields[err[1]]!r}, which float() accepts")
+    if rows == 0:
+        raise WorkloadError("empty dataset")
+    if nf_min != nf_max:
+        raise WorkloadError("inconsistent feature count")
+    return X, y
+
+
 def parse_dataset_arrays(csv_text: str) -> tuple[np.ndarray, np.ndarray]:
     rows = parse_dataset(csv_text)
     X = np.array([f for f, _ in rows], dtype=np.float64)
@@ -139,11 +188,17 @@ def run_training(params: dict, csv_text: str) -> bytes:
     from .crypto import CALLS
 
     CALLS["run_training"] += 1
-    X, y = parse_dataset_arrays(csv_text)
     lr = float(params.get("learning_rate", 0.1))
     epochs = max(0, int(params.get("epochs", 50)))   # range(epochs) runs none for epochs < 0
     exact = bool(params.get("exact", True))
-    w, b = train_arrays(X, y, lr, epochs, exact)
+    if csv_text.isascii():
+        # text -> HBM once; parse, train and keep everything on the device (bit-exact in mode 0)
+        X, y = parse_dataset_device(csv_text)
+        w, b = LogisticTrainer(X, y, exact=exact).train(lr, epochs)
+    else:
+        # the reference's Unicode splitlines/strip/float semantics are only restated on the host
+        X, y = parse_dataset_arrays(csv_text)
+        w, b = train_arrays(X, y, lr, epochs, exact)
     return serialize_model(list(w), b)
 
 

@@ -30,8 +30,9 @@ def nccl_group():
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("model", ["small_cnn", "resnet18"])
-def test_overlapped_allreduce_step_matches_single_gpu(nccl_group, model):
+@pytest.mark.parametrize("model,graph_collectives", [("small_cnn", False), ("resnet18", False),
+                                                      ("small_cnn", True), ("resnet18", True)])
+def test_overlapped_allreduce_step_matches_single_gpu(nccl_group, model, graph_collectives):
     from bench import make_shards
     from paper_2103_16898_b200.loader import CIFAR
     from paper_2103_16898_b200.trainer import EncryptedTrainer
@@ -42,7 +43,8 @@ def test_overlapped_allreduce_step_matches_single_gpu(nccl_group, model):
     aads = [torch.frombuffer(bytearray(s[2]), dtype=torch.uint8).cuda() for s in shards]
     runs = {}
     for dp in (False, True):
-        tr = EncryptedTrainer(model, key, batch=B, spec=CIFAR, seed=3, force_allreduce=dp)
+        tr = EncryptedTrainer(model, key, batch=B, spec=CIFAR, seed=3, force_allreduce=dp,
+                              graph_collectives=graph_collectives)
         if dp:
             assert len(tr.allreduce.buckets) >= 1
             tr.allreduce.__init__(tr.net.ps, bucket_mb=0.25)     # several buckets -> several segments
@@ -50,8 +52,10 @@ def test_overlapped_allreduce_step_matches_single_gpu(nccl_group, model):
         tr.step_resident(cts[0], shards[0][1], aads[0], B)       # eager step
         losses.append(float(tr.net.loss.item()))
         tr.capture()
-        if dp:
+        if dp and not graph_collectives:
             assert len(tr.segments) >= 2, "backward was not split at bucket boundaries"
+        if dp and graph_collectives:   # one graph: NCCL captured, wgrad side stream kept on
+            assert tr.segments == [] and tr.net.ps.overlap_with_hook
         for i in (1, 2):
             tr.step_resident(cts[i], shards[i][1], aads[i], B)
             losses.append(float(tr.net.loss.item()))
