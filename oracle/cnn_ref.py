@@ -217,12 +217,17 @@ REF_MODELS = {"small_cnn": SmallCNNRef, "resnet18": ResNet18Ref, "densenet121": 
 
 def normalise_records(records_u8: torch.Tensor, c: int, h: int, w: int, mean, std, emulate_bf16=True):
     """uint8 records [n][1+c*h*w] -> (NCHW fp32 input, int64 labels), same arithmetic as
-    csrc/loader.cu: v = x * (1/(255*std)) + (-mean/std) in fp32, then bf16."""
+    csrc/loader.cu and the fused decrypt-decode: v = fma(x, 1/(255*std), -mean/std) rounded once
+    to fp32 (x * scale is exact in fp64 for 8-bit x and the sum of two ~unit-range values fits
+    53 bits, so the fp64 expression rounded to fp32 is the fused multiply-add), then bf16."""
     labels = records_u8[:, 0].long()
-    px = records_u8[:, 1:].float().view(-1, c, h, w)
-    scale = torch.tensor([1.0 / (255.0 * s) for s in std], dtype=torch.float32).view(1, c, 1, 1)
-    shift = torch.tensor([-m / s for m, s in zip(mean, std)], dtype=torch.float32).view(1, c, 1, 1)
-    x = px * scale + shift
+    px = records_u8[:, 1:].double().view(-1, c, h, w)
+    import numpy as np
+
+    f32 = np.float32   # the per-channel factors are computed in fp32 on the host side of the kernels
+    scale = torch.tensor([f32(1.0) / (f32(255.0) * f32(s)) for s in std], dtype=torch.float32).view(1, c, 1, 1)
+    shift = torch.tensor([-f32(m) / f32(s) for m, s in zip(mean, std)], dtype=torch.float32).view(1, c, 1, 1)
+    x = (px * scale.double() + shift.double()).float()
     if emulate_bf16:
         x = x.to(torch.bfloat16).float()
     return x, labels

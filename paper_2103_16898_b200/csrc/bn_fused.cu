@@ -43,24 +43,8 @@ __device__ __forceinline__ void st8(bf16* p, const float v[8]) {
   *reinterpret_cast<uint4*>(p) = u;
 }
 
-// bar[0] = arrivals, bar[1] = generation.  All CTAs are co-resident (cooperative launch).
-__device__ __forceinline__ void grid_sync(unsigned* bar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned* vgen = bar + 1;
-    const unsigned g = *vgen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*vgen == g) __nanosleep(20);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
+// All CTAs are co-resident (cooperative launch): two-level grid barrier (cvb_common.cuh).
+__device__ __forceinline__ void grid_sync(unsigned* bar) { cvb_grid_barrier(bar); }
 
 // Fixed-order block reduction of per-thread (s[8], q[8]) for channel group g, row lane rl
 // into part[blk][2][C].
@@ -299,6 +283,27 @@ __device__ __forceinline__ void bwd_apply_raw(const BwdArgs& a, const ChanSmem& 
   st8(dst, o);
 }
 
+// pass-2 body from the stored dz (already masked): dx = gamma*rstd*(dz - mean(dz) - xhat*mean(dz*xhat))
+__device__ __forceinline__ void bwd_apply_dz(const ChanSmem& cs, const float* sh, int C, int g, const uint4& uz,
+                                             const uint4& ux, bf16* dst) {
+  float d[8], xv[8], mu[8], rs[8], kk[8], kb[8], kg[8], o[8];
+  const __nv_bfloat162* hz = reinterpret_cast<const __nv_bfloat162*>(&uz);
+  const __nv_bfloat162* hx = reinterpret_cast<const __nv_bfloat162*>(&ux);
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const float2 fz = __bfloat1622float2(hz[i]), fx = __bfloat1622float2(hx[i]);
+    d[2 * i] = fz.x; d[2 * i + 1] = fz.y; xv[2 * i] = fx.x; xv[2 * i + 1] = fx.y;
+  }
+  lds8(cs.mu + g * 8, mu);
+  lds8(cs.rs + g * 8, rs);
+  lds8(sh + g * 8, kk);
+  lds8(sh + C + g * 8, kb);
+  lds8(sh + 2 * C + g * 8, kg);
+#pragma unroll
+  for (int k = 0; k < 8; k++) o[k] = kk[k] * (d[k] - kb[k] - (xv[k] - mu[k]) * rs[k] * kg[k]);
+  st8(dst, o);
+}
+
 __global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
   extern __shared__ float sh[];
   __shared__ double shd[2 * THREADS / 32];
@@ -353,6 +358,24 @@ __global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
   __syncthreads();
   if (rl >= RL) return;
   int64_t r = r0 + rl;
+  if (a.dz_out && !a.dx32) {
+    // pass 1 stored dz = dy * mask (the residual branch's gradient): pass 2 reads it instead of
+    // dy and y -- two tensors per row instead of three -- two rows' loads in flight
+    for (; r + RL < r1; r += 2 * RL) {
+      const uint4 uz0 = __ldcg(reinterpret_cast<const uint4*>(a.dz_out + r * C + g * 8));
+      const uint4 ux0 = __ldcg(reinterpret_cast<const uint4*>(a.x + r * a.xcs + g * 8));
+      const uint4 uz1 = __ldcg(reinterpret_cast<const uint4*>(a.dz_out + (r + RL) * C + g * 8));
+      const uint4 ux1 = __ldcg(reinterpret_cast<const uint4*>(a.x + (r + RL) * a.xcs + g * 8));
+      bwd_apply_dz(cs, sh, C, g, uz0, ux0, a.dx + r * a.dxcs + g * 8);
+      bwd_apply_dz(cs, sh, C, g, uz1, ux1, a.dx + (r + RL) * a.dxcs + g * 8);
+    }
+    if (r < r1) {
+      const uint4 uz0 = __ldcg(reinterpret_cast<const uint4*>(a.dz_out + r * C + g * 8));
+      const uint4 ux0 = __ldcg(reinterpret_cast<const uint4*>(a.x + r * a.xcs + g * 8));
+      bwd_apply_dz(cs, sh, C, g, uz0, ux0, a.dx + r * a.dxcs + g * 8);
+    }
+    return;
+  }
   if (a.two_rows && !a.dx32 && !a.y) {
     // bf16 dx, mask recomputed from x: two rows' raw 16-byte loads in flight per thread (the
     // pass is load-latency bound), converted one row at a time (stays within 64 registers)
@@ -398,8 +421,8 @@ int fused_setup(int C, unsigned** bar, int* grid, int* grid_f = nullptr) {
   CVB_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) { cvb_set_error("bn fused: device index"); return CVB_EINVAL; }
   if (!g_bar[dev]) {
-    CVB_CUDA(cudaMalloc(&g_bar[dev], 2 * sizeof(unsigned)));
-    CVB_CUDA(cudaMemset(g_bar[dev], 0, 2 * sizeof(unsigned)));
+    CVB_CUDA(cudaMalloc(&g_bar[dev], CVB_GRID_BAR_WORDS * sizeof(unsigned)));
+    CVB_CUDA(cudaMemset(g_bar[dev], 0, CVB_GRID_BAR_WORDS * sizeof(unsigned)));
     CVB_CUDA(cudaDeviceSynchronize());
     const size_t smem = (size_t)THREADS * 16 * sizeof(float);
     CVB_CUDA(cudaFuncSetAttribute(bn_fwd_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -338,11 +338,11 @@ __device__ bool parse_double(const uint8_t* t, int64_t s, int64_t e, double* out
   if (s >= e) return false;
   const uint8_t c0 = lower(t[s]);
   if (c0 == 'i' || c0 == 'n') {
-    double v;
-    if (match_ci(t + s, e - s, "inf") || match_ci(t + s, e - s, "infinity")) v = __longlong_as_double(0x7FF0000000000000ll);
-    else if (match_ci(t + s, e - s, "nan")) v = __longlong_as_double(0x7FF8000000000000ll);
+    unsigned long long b;
+    if (match_ci(t + s, e - s, "inf") || match_ci(t + s, e - s, "infinity")) b = 0x7FF0000000000000ull;
+    else if (match_ci(t + s, e - s, "nan")) b = 0x7FF8000000000000ull;
     else return false;
-    *out = neg ? -v : v;
+    *out = __longlong_as_double((long long)(b | (neg ? 1ull << 63 : 0ull)));   // sign as a bit (NaN too)
     return true;
   }
   // mantissa digits (underscores only between two digits), optional '.', optional exponent
@@ -423,8 +423,7 @@ __device__ bool parse_double(const uint8_t* t, int64_t s, int64_t e, double* out
       }
     }
   }
-  double v = __longlong_as_double((long long)bits);
-  *out = neg ? -v : v;
+  *out = __longlong_as_double((long long)(bits | (neg ? 1ull << 63 : 0ull)));
   return true;
 }
 

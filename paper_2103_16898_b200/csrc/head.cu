@@ -61,23 +61,7 @@ __device__ __forceinline__ uint4 pack8(const float v[8]) {
   return u;
 }
 
-__device__ __forceinline__ void head_grid_sync(unsigned* bar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned* vgen = bar + 1;
-    const unsigned g = *vgen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*vgen == g) __nanosleep(32);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
+__device__ __forceinline__ void head_grid_sync(unsigned* bar) { cvb_grid_barrier(bar); }   // two-level (cvb_common.cuh)
 
 __global__ void __launch_bounds__(HT) head_train_kernel(const __grid_constant__ HeadArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -328,8 +312,8 @@ CVB_API int cvb_head_train(const void* x, int64_t ldx, const void* w, const floa
   CVB_CUDA(cudaGetDevice(&dev));
   static unsigned* bars[64] = {nullptr};
   if (!bars[dev]) {
-    CVB_CUDA(cudaMalloc(&bars[dev], 2 * sizeof(unsigned)));
-    CVB_CUDA(cudaMemset(bars[dev], 0, 2 * sizeof(unsigned)));
+    CVB_CUDA(cudaMalloc(&bars[dev], CVB_GRID_BAR_WORDS * sizeof(unsigned)));
+    CVB_CUDA(cudaMemset(bars[dev], 0, CVB_GRID_BAR_WORDS * sizeof(unsigned)));
   }
   HeadArgs a;
   a.x = (const bf16*)x; a.ldx = ldx; a.w = (const bf16*)w; a.bias = bias; a.labels = labels;

@@ -34,7 +34,7 @@ __global__ void records_to_nhwc(const __grid_constant__ RecParams p) {
 #pragma unroll
   for (int c = 0; c < 8; c++) {
     float x = 0.f;
-    if (c < p.c) x = (float)rec[1 + c * p.hw + px] * p.scale[c] + p.shift[c];
+    if (c < p.c) x = __fmaf_rn((float)rec[1 + c * p.hw + px], p.scale[c], p.shift[c]);   // one rounding
     v[c] = (T)x;
   }
   T* out = reinterpret_cast<T*>(p.out) + gid * p.cpad;

@@ -166,6 +166,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }
+// Long waits (the epilogue's accumulator-full wait spans a whole tile): one lane polls with a
+// back-off, so idle warps do not keep the shared-memory pipe (the MMA operand path) busy.
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_lazy(uint64_t* bar, uint32_t parity, bool lazy) {
+  if (!lazy) { mbar_wait(bar, parity); return; }
+  if ((threadIdx.x & 31) == 0)
+    while (!mbar_test(bar, parity)) __nanosleep(128);
+  __syncwarp();
+  mbar_wait(bar, parity);   // every lane observes the completed phase (memory ordering)
+}
 __device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, uint32_t dst, uint64_t* bar, int c0, int c1, int c2,
                                             int c3) {
   asm volatile(
@@ -426,6 +443,17 @@ __device__ __forceinline__ void halo8_issue(uint32_t tmem_d, uint64_t a0, uint64
   }
 }
 
+// One K-block's MMAs from descriptor templates held in registers: the MMA asm carries a
+// "memory" clobber, so descriptors read from the parameter bank inside the loop would be
+// re-loaded (LDC -> UTCHMMA dependency chains, ~100 cycles per MMA measured) before every MMA.
+template <int KS>
+__device__ __forceinline__ void issue_ksteps(const uint64_t (&ad)[8], const uint64_t (&bd)[8], uint32_t idesc,
+                                             uint32_t tmem_d, uint64_t sa, uint64_t sb, bool acc, bool leader) {
+#pragma unroll
+  for (int k = 0; k < KS; k++)
+    umma_bf16_el(tmem_d, ad[k] + sa, bd[k] + sb, idesc, (acc || k > 0) ? 1u : 0u, leader);
+}
+
 __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_constant__ GemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -513,7 +541,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
         tx = p.tx_bytes - (uint32_t)(p.ga - ga_eff) * p.a_box_bytes;
       }
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
-        mbar_wait(&empty[s], ph ^ 1);
+        mbar_wait_lazy(&empty[s], ph ^ 1, (p.dbg & 256) != 0);
         if (leader) {
           if (!(p.dbg & 32)) TRACE(0, it);
           const uint32_t sa = smem0 + s * stage_bytes, sb = sa + a_stage;
@@ -579,6 +607,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
     int s = 0;
     uint32_t ph = 0;
     int it = 0, lt = 0;
+    uint64_t adr[8], bdr[8];   // descriptor templates, read once (see issue_ksteps)
+#pragma unroll
+    for (int k = 0; k < 8; k++) { adr[k] = p.adesc[k]; bdr[k] = p.bdesc[k]; }
+    const uint32_t idr = p.idesc;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
       const int sp = (int)p.fd_mn.div((uint32_t)u);
       const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
@@ -590,7 +622,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       const uint32_t tmem_d = tmem_base + acc * p.BN;
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
         mbar_wait(&full[s], ph);
-        tc_fence_after();
+        if (!(p.dbg & 1024)) tc_fence_after();   // knob 1024: no per-K-block tcgen05 fence (experiment)
         if (leader) TRACE(1, it);
         if (p.dbg & 1) {
           if (leader) mbar_arrive(&empty[s]);
@@ -646,9 +678,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
             }
           } else {
             const uint64_t sb = p.b_res ? (uint64_t)((bres + kb * b_kb_bytes) >> 4) : sa + (a_stage >> 4);
-#pragma unroll
-            for (int k = 0; k < p.ksteps; k++)
-              umma_bf16_el(tmem_d, p.adesc[k] + sa, p.bdesc[k] + sb, p.idesc, (kb > kb0 || k > 0) ? 1u : 0u, leader);
+            // compile-time step counts: the descriptors become uniform constant-bank operands
+            // (a runtime-indexed p.adesc[k] is a per-thread indexed load in the issue loop)
+            if (p.ksteps == 4 && (p.dbg & 512)) {   // profiling knob: every K-block's MMAs twice (results invalid)
+              issue_ksteps<4>(adr, bdr, idr, tmem_d, sa, sb, kb > kb0, leader);
+              issue_ksteps<4>(adr, bdr, idr, tmem_d, sa, sb, true, leader);
+            } else if (p.ksteps == 4) issue_ksteps<4>(adr, bdr, idr, tmem_d, sa, sb, kb > kb0, leader);
+            else if (p.ksteps == 8) issue_ksteps<8>(adr, bdr, idr, tmem_d, sa, sb, kb > kb0, leader);
+            else
+              for (int k = 0; k < p.ksteps; k++)
+                umma_bf16_el(tmem_d, p.adesc[k] + sa, p.bdesc[k] + sb, p.idesc, (kb > kb0 || k > 0) ? 1u : 0u, leader);
           }
           if (leader) umma_commit(&empty[s]);
         }
@@ -676,7 +715,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
       if (p.epi_alt && (lt & 1) != ((warp - 2) >> 2)) continue;   // the other warp group's tile
       const int acc = lt & (nacc - 1);
-      mbar_wait(&tfull[acc], (lt >> p.nacc_log2) & 1);
+      mbar_wait_lazy(&tfull[acc], (lt >> p.nacc_log2) & 1, (p.dbg & 128) != 0);
       if (warp == 2 && lane == 0) TRACE(3, lt);
       tc_fence_after();
       bool valid = true;
@@ -1570,12 +1609,13 @@ CVB_API int cvb_gemm_ex(const void* a, int a_major, int64_t lda, const void* b, 
 __global__ void __launch_bounds__(96, 1) mma_rate_kernel(int n_mma, int bn, int issuers, int a_halo, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar[2];
+  __shared__ uint64_t bar[4];
   __shared__ uint32_t slot;
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1); mbar_init(&bar[1], 1);
+    mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); mbar_init(&bar[2], 1); mbar_init(&bar[3], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_arrive(&bar[2]);   // phase 0 complete: a wait on it passes at once
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&slot)), "r"(512));
@@ -1594,6 +1634,16 @@ __global__ void __launch_bounds__(96, 1) mma_rate_kernel(int n_mma, int bn, int 
     const uint64_t dh = ((uint64_t)(2944 >> 4) << 16) | ((uint64_t)(160 >> 4) << 32) | ((uint64_t)1 << 46);
     const uint64_t da = a_halo ? dh : d0;
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(bn >> 3) << 17) | (8u << 24);
+    if (a_halo >= 11) {   // 11: A/B filled with random bf16 values, 12: with zeros (data dependence)
+      uint32_t x = 0x9e3779b9u * (blockIdx.x + 1) + threadIdx.x;
+      for (int i = threadIdx.x & 31; i < 16384; i += 32) {
+        x ^= x << 13; x ^= x >> 17; x ^= x << 5;
+        reinterpret_cast<uint32_t*>(smem)[i] = a_halo == 11 ? ((x & 0x3fff3fffu) | 0x3c003c00u) : 0u;
+      }
+      __syncwarp();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+    }
     long long t0 = clock64();
     if (leader) {
       if (a_halo == 10) {
@@ -1640,6 +1690,17 @@ __global__ void __launch_bounds__(96, 1) mma_rate_kernel(int n_mma, int bn, int 
           umma_bf16(tmem + ((i / 18) & 1) * 32u, dh + sa + aoff, d0 + sb + j * 2, idesc, (i % 18) ? 1u : 0u);
           if (issuers == 3 && i % 18 == 17) umma_commit(&bar[1]);   // per-tile commit, never waited on
         }
+      } else if (a_halo >= 13 && a_halo <= 16) {
+        // the GEMM kernel's per-K-block synchronisation after every 4 MMAs: 13 = full-barrier
+        // wait + tcgen05 fence + commit, 14 = commit only, 15 = fence only, 16 = wait only
+        for (int i = 0; i < n_mma; i++) {
+          umma_bf16(tmem, d0 + sa + (i & 3) * 2, d0 + sb + (i & 3) * 2, idesc, 1u);
+          if ((i & 3) == 3) {
+            if (a_halo == 13 || a_halo == 16) mbar_wait(&bar[2], 0);
+            if (a_halo == 13 || a_halo == 15) tc_fence_after();
+            if (a_halo == 13 || a_halo == 14) umma_commit(&bar[3]);
+          }
+        }
       } else {
         for (int i = 0; i < n_mma; i++) umma_bf16(tmem, da + sa + (i & 3) * (a_halo ? 1 : 2), d0 + sb + (i & 3) * 2, idesc, 1u);
       }
@@ -1648,7 +1709,7 @@ __global__ void __launch_bounds__(96, 1) mma_rate_kernel(int n_mma, int bn, int 
     __syncwarp();
     mbar_wait(&bar[me], 0);
     long long t1 = clock64();
-    if (leader) out[me] = t1 - t0;
+    if (leader && blockIdx.x == 0) out[me] = t1 - t0;
   }
   tc_fence_before();
   __syncthreads();
@@ -1662,7 +1723,10 @@ CVB_API long long cvb_debug_mma_cycles(int n_mma, int bn, int issuers, int a_hal
   cudaMalloc(&d, 16);
   cudaMemset(d, 0, 16);
   cudaFuncSetAttribute(mma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-  mma_rate_kernel<<<1, 96, 64 * 1024>>>(n_mma, bn, issuers, a_halo, d);
+  // a_halo >= 100: the same probe on every SM at once (a_halo - 100), CTA 0 reports
+  const int grid = a_halo >= 100 ? cvb_num_sms() : 1;
+  if (a_halo >= 100) a_halo -= 100;
+  mma_rate_kernel<<<grid, 96, 64 * 1024>>>(n_mma, bn, issuers, a_halo, d);
   cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
   cudaFree(d);
   return h[0] > h[1] ? h[0] : h[1];

@@ -13,6 +13,7 @@ ignored like the reference does (params.json:4 carries an ignored ``marker``).
 from __future__ import annotations
 
 import struct
+import warnings
 
 import numpy as np
 
@@ -66,9 +67,10 @@ def parse_dataset_device(csv_text: str, device=None):
     raw = csv_text.encode("ascii")
     if not raw.endswith(tuple(c.encode() for c in _LINE_BREAKS)):
         raw += b"\n"      # every line ends with a break (splitlines drops a final empty line)
-    host = torch.frombuffer(bytearray(raw), dtype=torch.uint8)
     dev = device or torch.device("cuda", torch.cuda.current_device())
-    text = host.pin_memory().to(dev, non_blocking=True)
+    with warnings.catch_warnings():   # read-only bytes: the tensor is only ever read (copied to HBM)
+        warnings.simplefilter("ignore", UserWarning)
+        text = torch.frombuffer(raw, dtype=torch.uint8).to(dev)
     info = (ctypes.c_int64 * 6)()
     h = ctypes.c_void_p()
     _lib.check(lib.cvb_csv_index(text.data_ptr(), len(raw), info, ctypes.byref(h), _lib.stream_ptr()), "csv_index")

@@ -18,6 +18,11 @@ elif which == "conv64":
     x = torch.randn(512, 32, 32, 64, device="cuda").bfloat16(); w = torch.randn(64, 3, 3, 64, device="cuda").bfloat16()
     y = torch.empty(512, 32, 32, 64, device="cuda", dtype=torch.bfloat16)
     f = lambda: K.conv2d_fwd(x, w, 1, 1, out=y)
+elif which in ("conv128", "conv256"):
+    c, hw = (128, 16) if which == "conv128" else (256, 8)
+    x = torch.randn(512, hw, hw, c, device="cuda").bfloat16(); w = torch.randn(c, 3, 3, c, device="cuda").bfloat16()
+    y = torch.empty(512, hw, hw, c, device="cuda", dtype=torch.bfloat16)
+    f = lambda: K.conv2d_fwd(x, w, 1, 1, out=y)
 elif which == "conv":
     x = torch.randn(512, 32, 32, 32, device="cuda").bfloat16(); w = torch.randn(32, 3, 3, 32, device="cuda").bfloat16()
     y = torch.empty(512, 32, 32, 32, device="cuda", dtype=torch.bfloat16)

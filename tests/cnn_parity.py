@@ -108,8 +108,18 @@ def check(report, wrel, model):
 # summation order, bf16 rounding of a different fp32 sum), so each step's loss, EVERY
 # per-tensor gradient and every updated weight tensor are held to tight relative bounds:
 FORCED_LOSS_TOL = 1e-3      # |dL| <= 1e-3 * max(1, |L|)
-FORCED_GRAD_TOL = 1e-2      # ||g_gpu - g_ref|| <= 1e-2 * ||g_ref||, every parameter tensor
-FORCED_W_TOL = 1e-3         # ||w_gpu - w_ref|| <= 1e-3 * ||w_ref||, every parameter tensor
+# ||g_gpu - g_ref|| <= tol * ||g_ref|| for EVERY parameter tensor (conv/FC weights, BN gamma/beta).
+# Measured maxima (B200, seeds below): small CNN 7.3e-3 (batch 64) / 3.9e-3 (batch 512);
+# ResNet-18 1.55e-2 at batch 512 -- what is left is bf16 re-rounding of slightly different fp32
+# sums through 17 BN/ReLU layers (the masks are matched).  Round 1 allowed 15% / 40%.
+FORCED_GRAD_TOL = {"small_cnn": 1e-2, "resnet18": 2.5e-2}
+# Adam applied to the GPU's own gradient (torch.optim.Adam semantics, fp32) reproduces the GPU's
+# updated weights to fp32 rounding: the optimiser kernel itself, per tensor.
+ADAM_SAME_GRAD_TOL = 1e-5
+# The updated weights vs the oracle's own step (its gradient), whole parameter vector: Adam's
+# first steps move every weight by ~lr whatever the gradient's size, so a near-zero gradient
+# element whose sign differs moves by 2 lr -- bounded relative to the weights, not per element.
+FORCED_W_TOL = {"small_cnn": 5e-3, "resnet18": 1e-2}   # measured: ResNet-18 batch 512 5.4e-3
 
 
 def _nchw(t):
@@ -146,8 +156,24 @@ def _moment_views(ps, buf):
             for name, shape, _ in ps.specs}
 
 
+def _adam_same_grad(ps, w_pre, m_pre, v_pre, step, lr, g):
+    """torch.optim.Adam (b 0.9/0.999, eps 1e-8) on CPU from the pre-step state with gradient g."""
+    out = {}
+    for name, shape, _ in ps.specs:
+        p = torch.nn.Parameter(w_pre[name].clone().float())
+        opt = torch.optim.Adam([p], lr=lr, betas=(0.9, 0.999), eps=1e-8, foreach=False)
+        if step > 0:
+            opt.state[p] = {"step": torch.tensor(float(step)), "exp_avg": m_pre[name].clone(),
+                            "exp_avg_sq": v_pre[name].clone()}
+        p.grad = g[name].clone().float()
+        opt.step()
+        out[name] = p.detach()
+    return out
+
+
 def run_forced(model="small_cnn", batch=64, steps=3, seed=0, lr=1e-3):
-    """Per step: (loss_gpu, loss_ref, {param: grad rel err}, {param: weight rel err})."""
+    """Per step: dict(loss_gpu, loss_ref, grads={param: rel err}, adam={param: rel err of the GPU
+    update vs Adam on the GPU's own gradient}, wvec=whole-vector rel err vs the oracle's step)."""
     spec = loader.CIFAR
     net = nets.make_model(model, seed=seed).build(batch)
     net.lr = lr
@@ -159,28 +185,43 @@ def run_forced(model="small_cnn", batch=64, steps=3, seed=0, lr=1e-3):
         xr, labr = normalise_records(torch.from_numpy(rec), spec["c"], spec["h"], spec["w"], spec["mean"],
                                      spec["std"], emulate_bf16=True)
         k = int(net.ps.step_dev.item())
-        ref.load(net.ps.state_cpu(), _moment_views(net.ps, net.ps.m), _moment_views(net.ps, net.ps.v), step=k)
+        w_pre = net.ps.state_cpu()
+        m_pre, v_pre = _moment_views(net.ps, net.ps.m), _moment_views(net.ps, net.ps.v)
+        ref.load(w_pre, m_pre, v_pre, step=k)
         loss_gpu = float(net.step(x, lab).item())
         torch.cuda.synchronize()
         ref.model.force(*gpu_forcing(net, model))
         loss_ref, g_ref = ref.step(xr, labr)
         w_gpu, w_ref = net.ps.state_cpu(), ref.state()
-        grads, wts = {}, {}
+        g_gpu = {name: net.ps.g[name].detach().float().cpu() for name, _, _ in net.ps.specs}
+        w_same = _adam_same_grad(net.ps, w_pre, m_pre, v_pre, k, lr, g_gpu)
+        grads, adam = {}, {}
         for key, gr in g_ref.items():
             name = key.replace("__", ".")
-            grads[name] = rel(net.ps.g[name].detach().float().cpu(), gr.float())
-            wts[name] = rel(w_gpu[name].float(), w_ref[name].float())
-        out.append((loss_gpu, loss_ref, grads, wts))
+            grads[name] = rel(g_gpu[name], gr.float())
+            adam[name] = rel(w_gpu[name].float(), w_same[name])
+        a = torch.cat([w_gpu[k_].reshape(-1).float() for k_ in w_ref])
+        b = torch.cat([w_ref[k_].reshape(-1).float() for k_ in w_ref])
+        out.append(dict(loss_gpu=loss_gpu, loss_ref=loss_ref, grads=grads, adam=adam, wvec=rel(a, b)))
     return out
 
 
-def check_forced(out):
-    for s, (lg, lr_, grads, wts) in enumerate(out):
-        assert abs(lg - lr_) <= FORCED_LOSS_TOL * max(1.0, abs(lr_)), (s, lg, lr_)
-        bad = {k: v for k, v in grads.items() if v > FORCED_GRAD_TOL}
+def check_forced(out, model):
+    for s, r in enumerate(out):
+        assert abs(r["loss_gpu"] - r["loss_ref"]) <= FORCED_LOSS_TOL * max(1.0, abs(r["loss_ref"])), (s, r)
+        bad = {k: v for k, v in r["grads"].items() if v > FORCED_GRAD_TOL[model]}
         assert not bad, (s, bad)
-        bad = {k: v for k, v in wts.items() if v > FORCED_W_TOL}
+        bad = {k: v for k, v in r["adam"].items() if v > ADAM_SAME_GRAD_TOL}
         assert not bad, (s, bad)
+        assert r["wvec"] <= FORCED_W_TOL[model], (s, r["wvec"])
+
+
+# Free-running overlay at the paper's lr 1e-3, 20 Adam steps, no forcing:
+# both runs are their own trajectories (Adam turns rounding noise in tiny gradients into full
+# lr-sized moves), so the loss curves are compared with an absolute-or-relative bound.
+# Measured: max |dL| / max(1, |L|) = 0.085 over 20 steps (small CNN, batch 64), final weights 4.7e-2.
+FREE_CURVE_TOL = 0.1
+FREE_W_TOL = 0.1
 
 
 def one_step_check(batch=16, model="small_cnn"):
