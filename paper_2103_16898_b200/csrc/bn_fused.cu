@@ -46,42 +46,49 @@ __device__ __forceinline__ void st8(bf16* p, const float v[8]) {
 // All CTAs are co-resident (cooperative launch): two-level grid barrier (cvb_common.cuh).
 __device__ __forceinline__ void grid_sync(unsigned* bar) { cvb_grid_barrier(bar); }
 
-// Fixed-order block reduction of per-thread (s[8], q[8]) for channel group g, row lane rl
-// into part[blk][2][C].
-__device__ __forceinline__ void block_partials(const float s[8], const float q[8], int G, int RL, int g, int rl,
-                                               int C, float* __restrict__ part, float* sh) {
-  if (rl < RL) {
-#pragma unroll
-    for (int i = 0; i < 8; i++) { sh[(rl * G + g) * 16 + i] = s[i]; sh[(rl * G + g) * 16 + 8 + i] = q[i]; }
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < G * 16; idx += THREADS) {
-    const int gg = idx >> 4, k = idx & 15;
-    float acc = 0.f;
-    for (int l = 0; l < RL; l++) acc += sh[(l * G + gg) * 16 + k];
-    part[((int64_t)blockIdx.x * 2 + (k >> 3)) * C + gg * 8 + (k & 7)] = acc;
+__device__ __forceinline__ void bn_trace(long long* tr, int k) {
+  if (tr && threadIdx.x == 0) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[blockIdx.x * 8 + k] = t;
   }
 }
 
-// Channel c's totals over all CTAs' partials, fixed order (warp-strided, then smem in warp
-// order).  Called by a whole CTA for one channel; result valid in thread 0.
-__device__ __forceinline__ void channel_total(const float* __restrict__ part, int C, int c, double& s, double& q,
-                                              double* shd) {
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = THREADS / 32;
-  double a = 0, b = 0;
-  for (int k = threadIdx.x; k < (int)gridDim.x; k += THREADS) {
-    a += __ldcg(part + (int64_t)(2 * k) * C + c);
-    b += __ldcg(part + (int64_t)(2 * k + 1) * C + c);
+// Fixed-order block reduction of per-thread (s[8], q[8]) for channel group g, row lane rl
+// into the channel-major partials part[2][C][grid] (this CTA's column).  The staging layout
+// sh[k][rl][g] is conflict-free for both the writes (consecutive threads = consecutive g) and
+// the column sums (consecutive threads = consecutive g of one k); the row-major [rl][g][16]
+// layout it replaces was 16-way bank-conflicted (1.8 us per launch, traced).
+__device__ __forceinline__ void block_partials(const float s[8], const float q[8], int G, int RL, int g, int rl,
+                                               int C, float* __restrict__ part, float* sh) {
+  const int RG = RL * G;
+  if (rl < RL) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) { sh[i * RG + rl * G + g] = s[i]; sh[(8 + i) * RG + rl * G + g] = q[i]; }
   }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < G * 16; idx += THREADS) {
+    const int k = idx / G, gg = idx - k * G;
+    float acc = 0.f;
+    for (int l = 0; l < RL; l++) acc += sh[k * RG + l * G + gg];
+    part[((int64_t)(k >> 3) * C + gg * 8 + (k & 7)) * gridDim.x + blockIdx.x] = acc;
+  }
+}
+
+// Channel c's totals over all CTAs' partials, fixed order (lane-strided, then a warp tree),
+// computed by ONE warp reading the channel's contiguous partial row (coalesced); no block
+// barrier, so a CTA finalises up to 16 channels at once.  Result valid in lane 0.
+__device__ __forceinline__ void channel_total_warp(const float* __restrict__ part, int C, int c, double& s,
+                                                   double& q) {
+  const int l = threadIdx.x & 31, P = (int)gridDim.x;
+  const float* ps = part + (int64_t)c * P;
+  const float* pq = part + ((int64_t)C + c) * P;
+  double a = 0, b = 0;
+  for (int k = l; k < P; k += 32) { a += __ldcg(ps + k); b += __ldcg(pq + k); }
 #pragma unroll
   for (int o = 16; o; o >>= 1) { a += __shfl_down_sync(0xffffffffu, a, o); b += __shfl_down_sync(0xffffffffu, b, o); }
-  if (l == 0) { shd[w] = a; shd[nw + w] = b; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    s = 0; q = 0;
-    for (int k = 0; k < nw; k++) { s += shd[k]; q += shd[nw + k]; }
-  }
-  __syncthreads();
+  s = a;
+  q = b;
 }
 
 struct FwdArgs {
@@ -91,16 +98,17 @@ struct FwdArgs {
   const float* gamma; const float* beta; const bf16* res; int rcs; int relu;
   bf16* y; int ycs, ycoff;   // y == nullptr: statistics only
   int four_rows;             // pass 2 without residual: 4 rows in flight (CVB_BN_FWD_TWO_ROWS=1: off)
+  long long* trace;          // CVB_BN_TRACE: per-CTA phase timestamps (globaltimer ns), debug only
 };
 
 __global__ void __launch_bounds__(THREADS) bn_fwd_fused(const FwdArgs a) {
   extern __shared__ float sh[];
-  __shared__ double shd[2 * THREADS / 32];
   __shared__ float s_scale[2048], s_shift[2048];
   const int C = a.C, G = C / 8, RL = THREADS / G;
   const int g = threadIdx.x % G, rl = threadIdx.x / G;
   const int64_t per = (a.rows + gridDim.x - 1) / gridDim.x;
   const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(a.rows, r0 + per);
+  bn_trace(a.trace, 0);
   // ---- pass 1: partial statistics ----
   float s[8] = {0}, q[8] = {0};
   if (rl < RL) {
@@ -121,28 +129,36 @@ __global__ void __launch_bounds__(THREADS) bn_fwd_fused(const FwdArgs a) {
       for (int i = 0; i < 8; i++) { s[i] += v[i]; q[i] += v[i] * v[i]; }
     }
   }
+  bn_trace(a.trace, 1);
   block_partials(s, q, G, RL, g, rl, C, a.part, sh);
+  bn_trace(a.trace, 2);
   grid_sync(a.bar);
-  // ---- finalisation: CTA b owns channels b, b + grid, ... ----
-  for (int c = blockIdx.x; c < C; c += gridDim.x) {
-    double ts, tq;
-    channel_total(a.part, C, c, ts, tq, shd);
-    if (threadIdx.x == 0) {
-      const double cnt = (double)a.rows;
-      const double m = ts / cnt;
-      double var = tq / cnt - m * m;
-      if (var < 0) var = 0;
-      a.mean[c] = (float)m;
-      a.rstd[c] = (float)(1.0 / sqrt(var + (double)a.eps));
-      if (a.run_mean) {
-        const double unb = cnt > 1 ? var * cnt / (cnt - 1) : var;
-        a.run_mean[c] = (float)((1.0 - a.momentum) * a.run_mean[c] + a.momentum * m);
-        a.run_var[c] = (float)((1.0 - a.momentum) * a.run_var[c] + a.momentum * unb);
+  bn_trace(a.trace, 3);
+  // ---- finalisation: warp w of CTA b owns channel b + w * grid ----
+  {
+    const int c = blockIdx.x + (threadIdx.x >> 5) * gridDim.x;
+    if (c < C) {
+      double ts, tq;
+      channel_total_warp(a.part, C, c, ts, tq);
+      if ((threadIdx.x & 31) == 0) {
+        const double cnt = (double)a.rows;
+        const double m = ts / cnt;
+        double var = tq / cnt - m * m;
+        if (var < 0) var = 0;
+        a.mean[c] = (float)m;
+        a.rstd[c] = (float)(1.0 / sqrt(var + (double)a.eps));
+        if (a.run_mean) {
+          const double unb = cnt > 1 ? var * cnt / (cnt - 1) : var;
+          a.run_mean[c] = (float)((1.0 - a.momentum) * a.run_mean[c] + a.momentum * m);
+          a.run_var[c] = (float)((1.0 - a.momentum) * a.run_var[c] + a.momentum * unb);
+        }
       }
     }
   }
+  bn_trace(a.trace, 4);
   if (!a.y) return;
   grid_sync(a.bar);
+  bn_trace(a.trace, 5);
   // ---- pass 2: normalise the same rows ----
   for (int c = threadIdx.x; c < C; c += THREADS) {
     s_scale[c] = a.gamma[c] * __ldcg(a.rstd + c);
@@ -200,6 +216,7 @@ __global__ void __launch_bounds__(THREADS) bn_fwd_fused(const FwdArgs a) {
     }
     st8(a.y + r * a.ycs + a.ycoff + g * 8, o);
   }
+  bn_trace(a.trace, 6);
 }
 
 struct BwdArgs {
@@ -209,6 +226,7 @@ struct BwdArgs {
   float* part; unsigned* bar; float* dgamma; float* dbeta;
   bf16* dx; int dxcs; float* dx32; int accum32; bf16* dz_out;
   int two_rows;              // pass 2: two rows' raw loads in flight (CVB_BN_BWD_ONE_ROW=1: off)
+  long long* trace;          // CVB_BN_TRACE: per-CTA phase timestamps (globaltimer ns), debug only
 };
 
 // Per-channel constants live in shared memory (8 consecutive floats per channel group, two
@@ -306,7 +324,6 @@ __device__ __forceinline__ void bwd_apply_dz(const ChanSmem& cs, const float* sh
 
 __global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
   extern __shared__ float sh[];
-  __shared__ double shd[2 * THREADS / 32];
   __shared__ ChanSmem cs;
   const int C = a.C, G = C / 8, RL = THREADS / G;
   const int g = threadIdx.x % G, rl = threadIdx.x / G;
@@ -340,10 +357,13 @@ __global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
   }
   block_partials(s, q, G, RL, g, rl, C, a.part, sh);
   grid_sync(a.bar);
-  for (int c = blockIdx.x; c < C; c += gridDim.x) {
-    double ts, tq;
-    channel_total(a.part, C, c, ts, tq, shd);
-    if (threadIdx.x == 0) { a.dbeta[c] = (float)ts; a.dgamma[c] = (float)tq; }
+  {
+    const int c = blockIdx.x + (threadIdx.x >> 5) * gridDim.x;   // warp w of CTA b: channel b + w * grid
+    if (c < C) {
+      double ts, tq;
+      channel_total_warp(a.part, C, c, ts, tq);
+      if ((threadIdx.x & 31) == 0) { a.dbeta[c] = (float)ts; a.dgamma[c] = (float)tq; }
+    }
   }
   if (!a.dx && !a.dx32) return;
   grid_sync(a.bar);
@@ -412,6 +432,15 @@ __global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
 }
 
 unsigned* g_bar[64] = {nullptr};
+long long* g_trace = nullptr;   // CVB_BN_TRACE: [grid][8] phase timestamps of the last launch
+
+long long* trace_buf() {
+  static int on = -1;
+  if (on < 0) on = getenv("CVB_BN_TRACE") ? 1 : 0;
+  if (!on) return nullptr;
+  if (!g_trace) cudaMalloc(&g_trace, sizeof(long long) * 8 * 4096);
+  return g_trace;
+}
 int g_grid[64] = {0}, g_grid_f[64] = {0};
 
 // *grid: the backward kernel's co-resident grid; *grid_f: the forward kernel's (it needs
@@ -497,8 +526,10 @@ CVB_API int cvb_bn_forward(const void* x, int64_t rows, int C, int xcs, float* w
   int rc = fused_setup(C, &bar, &grid_b, &grid);
   if (rc) return rc;
   FwdArgs a{(const bf16*)x, rows, C, xcs, ws, bar, mean, rstd, eps, run_mean, run_var, momentum, gamma, beta,
-            (const bf16*)res, rcs, relu, (bf16*)y, ycs, ycoff, getenv("CVB_BN_FWD_TWO_ROWS") ? 0 : 1};
-  return launch_coop(bn_fwd_fused, a, size_grid(grid, rows, C), (cudaStream_t)stream);
+            (const bf16*)res, rcs, relu, (bf16*)y, ycs, ycoff, getenv("CVB_BN_FWD_TWO_ROWS") ? 0 : 1, trace_buf()};
+  const int gf = size_grid(grid, rows, C);
+  if (C > 16 * gf) { cvb_set_error("bn_forward: more channels than finalising warps"); return CVB_EINVAL; }
+  return launch_coop(bn_fwd_fused, a, gf, (cudaStream_t)stream);
 }
 
 // Batch-norm (+ReLU) backward in one launch (same contract as cvb_bn_backward).
@@ -512,6 +543,16 @@ CVB_API int cvb_bn_backward_fused(const void* dy, int dycs, const void* x, int x
   int rc = fused_setup(C, &bar, &grid);
   if (rc) return rc;
   BwdArgs a{(const bf16*)dy, dycs, (const bf16*)x, xcs, (const bf16*)y, ycs, rows, C, mean, rstd, gamma, beta, relu,
-            ws, bar, dgamma, dbeta, (bf16*)dx, dxcs, dx32, accum32, (bf16*)dz_out, two_rows_knob()};
-  return launch_coop(bn_bwd_fused, a, size_grid(grid, rows, C), (cudaStream_t)stream);
+            ws, bar, dgamma, dbeta, (bf16*)dx, dxcs, dx32, accum32, (bf16*)dz_out, two_rows_knob(), trace_buf()};
+  const int gb = size_grid(grid, rows, C);
+  if (C > 16 * gb) { cvb_set_error("bn_backward: more channels than finalising warps"); return CVB_EINVAL; }
+  return launch_coop(bn_bwd_fused, a, gb, (cudaStream_t)stream);
+}
+
+// Debug: copy the last traced BN launch's per-CTA phase timestamps ([n][8] globaltimer ns).
+CVB_API int cvb_bn_debug_trace(long long* out, int n) {
+  if (!g_trace) { cvb_set_error("bn trace: run with CVB_BN_TRACE=1"); return CVB_EINVAL; }
+  CVB_CUDA(cudaDeviceSynchronize());
+  CVB_CUDA(cudaMemcpy(out, g_trace, sizeof(long long) * 8 * (size_t)n, cudaMemcpyDeviceToHost));
+  return CVB_OK;
 }

@@ -118,6 +118,7 @@ struct GemmParams {
   int out_ph, out_pw, out_H, out_W;
   CUtensorMap mapC;
   int dbg;                  // profiling knobs: 1 = skip MMA, 2 = skip TMA (results invalid)
+  int kb_pair;              // MMA warp issues two 4-MMA K-blocks per batch (FWD / DENSE / WGRAD, ksteps 4)
   long long* trace;         // debug: clock64 timeline of CTA 0 (5 x 4096 slots) or null
   int nbox;
   // MODE_HALO geometry
@@ -620,6 +621,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       if ((p.dbg & 32) && !(p.dbg & 64) && leader) TRACE(0, it);   // debug: slot 0 = accumulator wait passed
       tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * p.BN;
+      if (p.kb_pair) {
+        // gathered / dense K-blocks are only 4 MMAs each: the MMA warp's fixed cost per issue
+        // batch (~450 cycles measured, independent of N) left the tensor pipe idle half the
+        // time.  Two stages are waited for and issued as one batch of 8 MMAs.
+        for (int kb = kb0; kb < kb1;) {
+          const bool two = kb + 1 < kb1;
+          const int s2 = s + 1 == p.stages ? 0 : s + 1;
+          const uint32_t ph2 = s + 1 == p.stages ? ph ^ 1u : ph;
+          mbar_wait(&full[s], ph);
+          if (two) mbar_wait(&full[s2], ph2);
+          tc_fence_after();
+          if (leader) TRACE(1, it);
+          const uint64_t sa = (smem0 + s * stage_bytes) >> 4;
+          issue_ksteps<4>(adr, bdr, idr, tmem_d, sa, sa + (a_stage >> 4), kb > kb0, leader);
+          if (two) {
+            const uint64_t sa2 = (smem0 + s2 * stage_bytes) >> 4;
+            issue_ksteps<4>(adr, bdr, idr, tmem_d, sa2, sa2 + (a_stage >> 4), true, leader);
+          }
+          if (leader) {
+            umma_commit(&empty[s]);
+            if (two) umma_commit(&empty[s2]);
+            TRACE(2, it);
+          }
+          __syncwarp();
+          const int n = two ? 2 : 1;
+          kb += n;
+          it += n;
+          for (int i = 0; i < n; i++)
+            if (++s == p.stages) { s = 0; ph ^= 1; }
+        }
+      } else
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
         mbar_wait(&full[s], ph);
         if (!(p.dbg & 1024)) tc_fence_after();   // knob 1024: no per-K-block tcgen05 fence (experiment)
@@ -1074,6 +1106,14 @@ int launch(GemmParams& p, cudaStream_t stream) {
   }
   if (env_stages > 0 && env_stages < p.stages) p.stages = env_stages;
   p.dbg = env_dbg;
+  // Paired K-blocks halve the MMA warp's per-batch cost (conv 128->128 with the TMA loads
+  // skipped: 57.6 -> 40.1 us), but with the loads on these convs sit at the L2 throughput cap
+  // (~42 B/clk/SM: 576 KB of operands per 128x128 tile) and the pairing delays stage release:
+  // measured +2.7% on the ResNet-18 GEMM class.  Opt-in (CVB_KB_PAIR=1) until operand reuse
+  // lowers the L2 demand.
+  static int pair_on = -1;
+  if (pair_on < 0) pair_on = getenv("CVB_KB_PAIR") ? 1 : 0;
+  p.kb_pair = (pair_on && p.mode != MODE_HALO && p.ksteps == 4 && !p.b_res && p.stages >= 4 && !(env_dbg & 1)) ? 1 : 0;
   p.trace = nullptr;
   if (env_dbg & 4) {
     static long long* tr = nullptr;
