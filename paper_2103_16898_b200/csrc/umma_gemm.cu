@@ -83,6 +83,8 @@ struct GemmParams {
   uint32_t a_stage_bytes;   // smem bytes of the A part of one pipeline stage
   uint32_t b_stage_bytes;   // smem bytes of the B part of one stage (0: BN * kr * 2)
   int w_halo;               // WGRAD halo: one (bw+KW-1)-wide box per K-block carries every kw tap
+  int w_pair;               // WGRAD halo, Cout = 64: an N tile holds TWO kh rows (M rows 0-63: kh 2t+1, 64-127: kh 2t)
+  int w_kh;                 // kernel height (w_pair: which M halves are real)
   int b_res;                // 1: the whole B operand (one N tile, all K) is loaded once per CTA
   uint32_t b_res_bytes;     // size of the resident B region
   int b_slabs;              // 64-wide K slabs of the resident B
@@ -540,6 +542,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       if (p.mode == MODE_WGRAD) {
         ga_eff = min(p.ga, (p.M - m0 + p.a_cel - 1) / p.a_cel);
         tx = p.tx_bytes - (uint32_t)(p.ga - ga_eff) * p.a_box_bytes;
+        if (p.w_pair) { ga_eff = p.w_pair == 1 ? 1 : 2; tx = p.tx_bytes; }   // kh-paired dY boxes
       }
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
         mbar_wait_lazy(&empty[s], ph ^ 1, (p.dbg & 256) != 0);
@@ -571,8 +574,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
                 for (int g = 0; g < p.gb; g++)
                   tma_load_2d(&p.mapB[0], sb + g * p.b_box_stride, &full[s], kb * BK + g * p.b_cel, n0);
             } else if (p.mode == MODE_WGRAD) {
-              for (int b = 0; b < ga_eff; b++)
-                tma_load_4d(&p.mapA[0], sa + b * p.a_box_stride, &full[s], m0 + b * p.a_cel, pw, ph0, pn);
+              if (p.w_pair == 2) {   // M atom 0 = dY rows one up (kh 2t+1), atom 1 = dY rows (kh 2t)
+                for (int b = 0; b < 2; b++)
+                  tma_load_4d(&p.mapA[0], sa + b * p.a_box_stride, &full[s], 0, pw, ph0 - 1 + b, pn);
+              } else {
+                for (int b = 0; b < ga_eff; b++)
+                  tma_load_4d(&p.mapA[0], sa + b * p.a_box_stride, &full[s], m0 + b * p.a_cel, pw,
+                              p.w_pair ? ph0 - 1 : ph0, pn);
+              }
               const uint32_t* tab = p.boxtab + nt * p.gb;
               for (int j = 0; j < p.gb; j++) {
                 const uint32_t e = tab[j];
@@ -764,6 +773,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
         const int m = mt * BM + row;
         valid = m < p.M;
         dst_row = m;
+      } else if (p.w_pair) {
+        valid = 2 * nt + (quarter < 2 ? 1 : 0) < p.w_kh;
+        dst_row = (int64_t)sp * p.part_rows + (row & 63);
       } else {
         const int m = mt * BM + row;
         valid = m < p.part_rows;
@@ -790,10 +802,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           c1 = mt * BM + quarter * 32;
           c2 = p.out_mode == OUT_PARTIAL ? sp : 0;
         }
+        // kh-paired wgrad: lane quarters 0-1 hold kh 2nt+1, quarters 2-3 kh 2nt, both for Cout 0..63
+        const int pair_kh = 2 * nt + (quarter < 2 ? 1 : 0);
+        const int colbase = p.w_pair ? pair_kh * p.BN : nt * p.BN;
+        if (p.w_pair) c1 = (quarter & 1) * 32;
         const uint32_t stg = smem0 + p.stg_off + (uint32_t)(warp - 2) * p.stg_warp;
         const int span = p.n_epi == 8 && !p.epi_alt ? p.BN >> 1 : p.BN;   // columns this warp stores
         const int cbeg = p.n_epi == 8 && !p.epi_alt && warp >= 6 ? span : 0;
-        const int cend = quarter * 32 < p.st_rows ? cbeg + span : cbeg;   // short tile: nothing to store
+        const bool rows_real = p.w_pair ? pair_kh < p.w_kh : quarter * 32 < p.st_rows;
+        const int cend = rows_real ? cbeg + span : cbeg;   // short tile: nothing to store
         const bool one_chunk = span <= p.st_ch;
         bool released = false;
         for (int c = cbeg; c < cend; c += p.st_ch, ++stg_it) {
@@ -822,7 +839,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
-            const int c0 = p.col_off + nt * p.BN + c;
+            const int c0 = p.col_off + colbase + c;
             if (p.accum) tma_red_add_4d(&p.mapC, buf, c0, c1, c2, c3);
             else tma_store_4d(&p.mapC, buf, c0, c1, c2, c3);
             bulk_commit();
@@ -837,7 +854,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
         if (warp == 2 && lane == 0) TRACE(4, lt);
         continue;
       }
-      const int64_t rowoff = dst_row * p.ldc + p.col_off + nt * p.BN;
+      const int64_t rowoff = dst_row * p.ldc + p.col_off +
+                             (p.w_pair ? (2 * nt + (quarter < 2 ? 1 : 0)) * p.BN : nt * p.BN);
       int c = 0;
       for (; c + 32 <= p.BN; c += 32) {
         uint32_t r[32];
@@ -1145,6 +1163,9 @@ int launch(GemmParams& p, cudaStream_t stream) {
     for (int k = 0; k < p.ksteps; k++) {
       const uint32_t row = (uint32_t)(16 * k / p.tw) * pitch + (uint32_t)(16 * k % p.tw);
       p.bdesc[k] = desc_tmpl(row * R, R, 8 * R, layout_of((int)R));
+      // kh pairs: A = one (bh+1)-row dY box; M atom 0 (kh 2t+1) starts at box row 0, atom 1
+      // (kh 2t) one dY row later: LBO = one box row of pixels
+      if (p.w_pair == 1) p.adesc[k] = desc_tmpl((uint32_t)(16 * k) * 128u, (uint32_t)p.tw * 128u, 8u * 128u, 2u);
     }
   }
   if (p.mode == MODE_HALO && p.h_rows && p.h_kwbox)   // kw boxes: plain SW128 K-major, 8-row groups 1 KB apart
@@ -1569,8 +1590,41 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
     p.kb_per_split = (p.num_kb + splits - 1) / splits;
     splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
     p.splits = splits;
+    static int no_pair = -1;
+    if (no_pair < 0) no_pair = getenv("CVB_NO_WGRAD_PAIR") ? 1 : 0;
+    // Cout = 64 fills only half of the 128-row MMA: pair the kh rows instead.  With the input
+    // box fixed at X rows (2t - pad + r), kh = 2t reads dY row r and kh = 2t+1 dY row r - 1, so
+    // ONE dY box of bh+1 rows (starting a row early) carries both as the two M atoms.
+    static int one_box = -1;   // default: one (bh+1)-row box (measured 47.0 vs 48.6 us, stage-1 ResNet wgrad)
+    if (one_box < 0) one_box = getenv("CVB_WGRAD_PAIR_TWOBOX") ? 0 : 1;
+    if (!no_pair && cout == 64 && kh >= 2) {
+      p.w_pair = one_box ? 1 : 2;
+      p.w_kh = kh;
+      p.n_tiles = (kh + 1) / 2;
+      // kh = 2t+1 pairs dY row r-1 with the input rows of kh = 2t at row r: its last dY row
+      // (oh-1) is reached only from K row oh -> the pixel range runs one row past the image
+      // (that row is TMA zero fill for kh = 2t)
+      p.ptiles_h = (oh + 1 + bh - 1) / bh;
+      p.num_kb = p.ptiles_w * p.ptiles_h * ((n + bnn - 1) / bnn);
+      if (p.w_pair == 1) {   // one (bh+1)-row box, M atoms one box row apart (LBO = a row of pixels)
+        p.a_stage_bytes = ((uint32_t)bw * (bh + 1) * 128u + 1023u) / 1024u * 1024u;
+        p.tx_bytes = (uint32_t)bw * (bh + 1) * 128u + (uint32_t)hw_ * bh * bcel * 2;
+        if ((rc = encode_nhwc(&p.mapA[0], dy, n, oh, ow, cout, dycs, acel, bw, bh + 1, bnn))) return rc;
+      } else {               // two boxes of the same dY channels, one row apart (standard MN atoms)
+        p.tx_bytes = 2u * (uint32_t)bw * bh * 128u + (uint32_t)hw_ * bh * bcel * 2;
+      }
+      tiles = p.m_tiles * p.n_tiles;
+      splits = (g_num_sms + tiles - 1) / tiles;
+      if (splits > max_splits) splits = max_splits;
+      if (splits > p.num_kb) splits = p.num_kb;
+      if (splits < 1) splits = 1;
+      p.kb_per_split = (p.num_kb + splits - 1) / splits;
+      splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
+      p.splits = splits;
+    }
     p.nbox = p.n_tiles;
-    for (int t = 0; t < kh; t++) p.boxtab[t] = pack_box(0, 0, -pad, t - pad);   // row kh = t, all kw
+    for (int t = 0; t < p.n_tiles; t++)   // row kh = t (paired: kh = 2t and 2t+1), all kw
+      p.boxtab[t] = pack_box(0, 0, -pad, (p.w_pair ? 2 * t : t) - pad);
     if ((rc = encode_nhwc(&p.mapB[0], x, n, h, w, cin, xcs, bcel, hw_, bh, bnn))) return rc;
     p.out_mode = OUT_PARTIAL; p.out_f32 = 1; p.out = part; p.ldc = Ncols; p.col_off = 0; p.part_rows = cout;
     *splits_out = splits;

