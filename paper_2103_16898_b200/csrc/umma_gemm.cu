@@ -121,6 +121,9 @@ struct GemmParams {
   CUtensorMap mapC;
   int dbg;                  // profiling knobs: 1 = skip MMA, 2 = skip TMA (results invalid)
   int kb_pair;              // MMA warp issues two 4-MMA K-blocks per batch (FWD / DENSE / WGRAD, ksteps 4)
+  int pair;                 // CTA pair (cta_group::2, M = 256): FWD with streamed weights; B split by rank
+  const void* b_ptr;        // FWD weights [b_rows][b_ld] (host-side: the pair plan re-encodes mapB)
+  int64_t b_rows, b_cols, b_ld;
   long long* trace;         // debug: clock64 timeline of CTA 0 (5 x 4096 slots) or null
   int nbox;
   // MODE_HALO geometry
@@ -233,6 +236,65 @@ __device__ __forceinline__ void umma_bf16_el(uint32_t tmem_d, uint64_t adesc, ui
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// ---- CTA pair (cta_group::2): one 256 x N MMA over the two SMs of a TPC ------------------
+// The leader (cluster rank 0) issues every MMA; each CTA holds its own 128 rows of A and N/2
+// rows of B at the same smem offsets, and its 128 accumulator rows in its own TMEM.  Both
+// CTAs' TMA loads complete on the LEADER's full barrier; the MMA commits arrive on the same
+// barrier offset in both CTAs (multicast); both epilogues release the leader's accumulator.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same smem offset in cluster rank 0
+__device__ __forceinline__ uint32_t mapa_rank0(uint32_t saddr) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(saddr));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_pair(const CUtensorMap* map, uint32_t dst, uint32_t bar_c, int c0, int c1,
+                                                 int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_c), "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t dst, uint32_t bar_c, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_c), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair_el(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                  uint32_t acc, uint32_t leader) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "@q tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc), "r"(leader) : "memory");
+}
+// commit to the same barrier offset in both CTAs of the pair
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(smem_u32(bar)), "h"((uint16_t)3) : "memory");
+}
+template <int PAIR>
+__device__ __forceinline__ void umma_t(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc,
+                                       uint32_t leader) {
+  if (PAIR) umma_bf16_pair_el(tmem_d, adesc, bdesc, idesc, acc, leader);
+  else umma_bf16_el(tmem_d, adesc, bdesc, idesc, acc, leader);
+}
+template <int PAIR>
+__device__ __forceinline__ void commit_t(uint64_t* bar) {
+  if (PAIR) umma_commit_pair(bar);
+  else umma_commit(bar);
 }
 // 32 consecutive fp32 columns of this thread's TMEM lane; caller waits with tmem_wait()
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
@@ -449,14 +511,25 @@ __device__ __forceinline__ void halo8_issue(uint32_t tmem_d, uint64_t a0, uint64
 // One K-block's MMAs from descriptor templates held in registers: the MMA asm carries a
 // "memory" clobber, so descriptors read from the parameter bank inside the loop would be
 // re-loaded (LDC -> UTCHMMA dependency chains, ~100 cycles per MMA measured) before every MMA.
-template <int KS>
+template <int KS, int PAIR = 0>
 __device__ __forceinline__ void issue_ksteps(const uint64_t (&ad)[8], const uint64_t (&bd)[8], uint32_t idesc,
                                              uint32_t tmem_d, uint64_t sa, uint64_t sb, bool acc, bool leader) {
 #pragma unroll
   for (int k = 0; k < KS; k++)
-    umma_bf16_el(tmem_d, ad[k] + sa, bd[k] + sb, idesc, (acc || k > 0) ? 1u : 0u, leader);
+    umma_t<PAIR>(tmem_d, ad[k] + sa, bd[k] + sb, idesc, (acc || k > 0) ? 1u : 0u, leader);
 }
 
+template <int PAIR>
+__device__ __forceinline__ void release_acc_t(uint32_t tempty0, int acc) {
+  if (PAIR) mbar_arrive_remote(tempty0 + 8u * (uint32_t)acc);
+  else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty0 + 8u * (uint32_t)acc) : "memory");
+}
+#define release_acc(t0, a) release_acc_t<PAIR>(t0, a)
+
+// PAIR = 1: CTA-pair instantiation (MODE_FWD with streamed weights only; see the cta_group::2
+// helpers above).  Every tcgen05 instruction of a kernel must use one cta_group, hence the
+// separate instantiation.
+template <int PAIR>
 __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_constant__ GemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -478,26 +551,40 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
   const int nacc = 1 << p.nacc_log2, acc_cols = nacc * p.BN;
   const int tmem_cols = acc_cols <= 32 ? 32 : acc_cols <= 64 ? 64 : acc_cols <= 128 ? 128 : acc_cols <= 256 ? 256 : 512;
 
+  // CTA pair: rank 1's tiles are the odd M tiles of each unit; only rank 0 issues MMAs
+  const int rank = PAIR ? (int)cluster_rank() : 0;
+  const int cl = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;      // scheduling slot
+  const int ncl = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int mtu = PAIR ? p.m_tiles >> 1 : p.m_tiles;                   // M units (tile pairs)
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < 4; i++) { prefetch_map(&p.mapA[i]); prefetch_map(&p.mapB[i]); }
     if (p.st_tma) prefetch_map(&p.mapC);
     for (int i = 0; i < p.stages; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < nacc; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], p.epi_alt ? 4 : p.n_epi); }
+    for (int i = 0; i < nacc; i++) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], (p.epi_alt ? 4 : p.n_epi) * (PAIR ? 2 : 1));
+    }
     mbar_init(bres_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(tmem_cols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(tmem_cols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(tmem_cols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all();   // the peer's barriers exist before any multicast commit / TMA
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const uint32_t smem0 = smem_u32(smem);
   CVB_PDL_PROLOGUE();   // barrier init / TMEM alloc / descriptor prefetch overlap the previous kernel
 
-  const int units = p.m_tiles * p.n_tiles * p.splits;
+  const int units = mtu * p.n_tiles * p.splits;
 
   // Role loops run on whole, converged warps; only the issuing instructions are predicated on
   // one elected lane.  Stage / phase counters are incremental (no divisions in the loops).
@@ -507,7 +594,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
     int s = 0;
     uint32_t ph = 0;
     int it = 0;
-    if (p.b_res && leader && blockIdx.x < units) {
+    if (!PAIR && p.b_res && leader && cl < units) {
       // whole B operand (single N tile): b_slabs slabs of BN x 64, loaded once per CTA
       mbar_expect_tx(bres_full, p.b_slabs * p.gb * p.BN * p.b_cel * 2);
       for (int kb = 0; kb < p.b_slabs; kb++)
@@ -515,8 +602,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           tma_load_2d(&p.mapB[0], bres + kb * b_kb_bytes + g * p.b_box_stride, bres_full, kb * BK + g * p.b_cel, 0);
     }
     __syncwarp();
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int rest = (int)p.fd_m.div((uint32_t)u), mt = u - rest * p.m_tiles;
+    for (int u = cl; u < units; u += ncl) {
+      const int rest = (int)p.fd_m.div((uint32_t)u), mt = (u - rest * mtu) * (PAIR ? 2 : 1) + rank;
       const int sp = (int)p.fd_n.div((uint32_t)rest), nt = rest - sp * p.n_tiles;
       const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
       int tw0 = 0, th0 = 0, tn0 = 0;
@@ -549,7 +636,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
         if (leader) {
           if (!(p.dbg & 32)) TRACE(0, it);
           const uint32_t sa = smem0 + s * stage_bytes, sb = sa + a_stage;
-          if (p.dbg & 2) {
+          if constexpr (PAIR) {
+            // both CTAs' boxes complete on the leader's barrier; the leader expects both halves
+            const uint32_t bar_c = mapa_rank0(smem_u32(&full[s]));
+            if (rank == 0) mbar_expect_tx(&full[s], 2u * tx);
+            const uint32_t* tab = p.boxtab + kb * p.ga;
+            for (int g = 0; g < p.ga; g++) {
+              const uint32_t e = tab[g];
+              tma_load_4d_pair(&p.mapA[e & 3], sa + g * p.a_box_stride, bar_c, (int)((e >> 2) & 0xFFFF),
+                               tw0 + (int)((e >> 18) & 127) - 64, th0 + (int)(e >> 25) - 64, tn0);
+            }
+            for (int g = 0; g < p.gb; g++)
+              tma_load_2d_pair(&p.mapB[0], sb + g * p.b_box_stride, bar_c, kb * BK + g * p.b_cel,
+                               n0 + rank * (p.BN >> 1));
+          } else if (p.dbg & 2) {
             mbar_arrive(&full[s]);
           } else {
             mbar_expect_tx(&full[s], tx);
@@ -612,7 +712,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
         if (++s == p.stages) { s = 0; ph ^= 1; }
       }
     }
+    if (PAIR) {
+      // producer tail: every stage's last multicast release has landed in this CTA before it
+      // may exit (the leader's commits write our barriers)
+      for (int i = 0; i < p.stages; i++) {
+        mbar_wait(&empty[s], ph ^ 1);
+        if (++s == p.stages) { s = 0; ph ^= 1; }
+      }
+    }
   } else if (warp == 1) {
+    if (PAIR && rank != 0) {
+      // the peer CTA's MMA warp has no work: the leader issues for both SMs
+    } else {
     const bool leader = elect_one();
     int s = 0;
     uint32_t ph = 0;
@@ -621,7 +732,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
 #pragma unroll
     for (int k = 0; k < 8; k++) { adr[k] = p.adesc[k]; bdr[k] = p.bdesc[k]; }
     const uint32_t idr = p.idesc;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
+    for (int u = cl; u < units; u += ncl, ++lt) {
       const int sp = (int)p.fd_mn.div((uint32_t)u);
       const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
       const int acc = lt & (nacc - 1);
@@ -643,14 +754,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           tc_fence_after();
           if (leader) TRACE(1, it);
           const uint64_t sa = (smem0 + s * stage_bytes) >> 4;
-          issue_ksteps<4>(adr, bdr, idr, tmem_d, sa, sa + (a_stage >> 4), kb > kb0, leader);
+          issue_ksteps<4, PAIR>(adr, bdr, idr, tmem_d, sa, sa + (a_stage >> 4), kb > kb0, leader);
           if (two) {
             const uint64_t sa2 = (smem0 + s2 * stage_bytes) >> 4;
-            issue_ksteps<4>(adr, bdr, idr, tmem_d, sa2, sa2 + (a_stage >> 4), true, leader);
+            issue_ksteps<4, PAIR>(adr, bdr, idr, tmem_d, sa2, sa2 + (a_stage >> 4), true, leader);
           }
           if (leader) {
-            umma_commit(&empty[s]);
-            if (two) umma_commit(&empty[s2]);
+            commit_t<PAIR>(&empty[s]);
+            if (two) commit_t<PAIR>(&empty[s2]);
             TRACE(2, it);
           }
           __syncwarp();
@@ -669,7 +780,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           if (leader) mbar_arrive(&empty[s]);
         } else {
           const uint64_t sa = (smem0 + s * stage_bytes) >> 4;
-          if (p.mode == MODE_HALO) {
+          if (!PAIR && p.mode == MODE_HALO) {
+            if constexpr (!PAIR) {
             // every tap of this channel group reads the same halo planes at a row offset.
             // Offsets are plain uniform arithmetic (no table loads: with N = 64 an MMA is
             // only 48 smem-read cycles, so the issue loop must stay below that):
@@ -717,28 +829,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
               }
             }
             }
+            }
           } else {
             const uint64_t sb = p.b_res ? (uint64_t)((bres + kb * b_kb_bytes) >> 4) : sa + (a_stage >> 4);
             // compile-time step counts: the descriptors become uniform constant-bank operands
             // (a runtime-indexed p.adesc[k] is a per-thread indexed load in the issue loop)
             if (p.ksteps == 4 && (p.dbg & 512)) {   // profiling knob: every K-block's MMAs twice (results invalid)
-              issue_ksteps<4>(adr, bdr, idr, tmem_d, sa, sb, kb > kb0, leader);
-              issue_ksteps<4>(adr, bdr, idr, tmem_d, sa, sb, true, leader);
-            } else if (p.ksteps == 4) issue_ksteps<4>(adr, bdr, idr, tmem_d, sa, sb, kb > kb0, leader);
-            else if (p.ksteps == 8) issue_ksteps<8>(adr, bdr, idr, tmem_d, sa, sb, kb > kb0, leader);
+              issue_ksteps<4, PAIR>(adr, bdr, idr, tmem_d, sa, sb, kb > kb0, leader);
+              issue_ksteps<4, PAIR>(adr, bdr, idr, tmem_d, sa, sb, true, leader);
+            } else if (p.ksteps == 4) issue_ksteps<4, PAIR>(adr, bdr, idr, tmem_d, sa, sb, kb > kb0, leader);
+            else if (p.ksteps == 8) issue_ksteps<8, PAIR>(adr, bdr, idr, tmem_d, sa, sb, kb > kb0, leader);
             else
               for (int k = 0; k < p.ksteps; k++)
-                umma_bf16_el(tmem_d, p.adesc[k] + sa, p.bdesc[k] + sb, p.idesc, (kb > kb0 || k > 0) ? 1u : 0u, leader);
+                umma_t<PAIR>(tmem_d, p.adesc[k] + sa, p.bdesc[k] + sb, p.idesc, (kb > kb0 || k > 0) ? 1u : 0u, leader);
           }
-          if (leader) umma_commit(&empty[s]);
+          if (leader) commit_t<PAIR>(&empty[s]);
         }
         if (leader) TRACE(2, it);
         __syncwarp();
         if (++s == p.stages) { s = 0; ph ^= 1; }
       }
-      if (leader) umma_commit(&tfull[acc]);
+      if (leader) commit_t<PAIR>(&tfull[acc]);
       if ((p.dbg & 64) && leader) TRACE(0, it - 1);   // debug: slot 0 = tile's accumulator commit issued
       __syncwarp();
+    }
     }
   } else {
     // ===================== epilogue (warps 2..5) =====================
@@ -750,8 +864,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
     // this warp's first row inside an NHWC M tile (constant over tiles)
     const int r0w = quarter * 32;
     const int w_off = r0w % p.tw, h_off = (r0w / p.tw) % p.th, n_off = r0w / (p.tw * p.th);
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
-      const int rest = (int)p.fd_m.div((uint32_t)u), mt = u - rest * p.m_tiles;
+    // the accumulator buffers are released on the leader's barriers (pair) or our own
+    const uint32_t tempty0 = PAIR ? mapa_rank0(smem_u32(&tempty[0])) : smem_u32(&tempty[0]);
+    for (int u = cl; u < units; u += ncl, ++lt) {
+      const int rest = (int)p.fd_m.div((uint32_t)u), mt = (u - rest * mtu) * (PAIR ? 2 : 1) + rank;
       const int sp = (int)p.fd_n.div((uint32_t)rest), nt = rest - sp * p.n_tiles;
       const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
       if (p.epi_alt && (lt & 1) != ((warp - 2) >> 2)) continue;   // the other warp group's tile
@@ -786,7 +902,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       if (p.dbg & 8) {   // profiling knob: no epilogue work (results invalid)
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) release_acc(tempty0, acc);
         if (warp == 2 && lane == 0) TRACE(4, lt);
         continue;
       }
@@ -827,7 +943,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           if (one_chunk) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) release_acc(tempty0, acc);
             released = true;
           }
           if (lane == 0) bulk_wait_read1();        // the store that last used this buffer has read it
@@ -849,7 +965,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
         if (!released) {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (lane == 0) release_acc(tempty0, acc);
         }
         if (warp == 2 && lane == 0) TRACE(4, lt);
         continue;
@@ -874,16 +990,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) release_acc(tempty0, acc);
       if (warp == 2 && lane == 0) TRACE(4, lt);
     }
     if (p.st_tma && lane == 0) bulk_wait_all();
   }
   __syncwarp();
-  __syncthreads();
+  tc_fence_before();
+  if (PAIR) cluster_sync_all();   // the leader's MMAs into the peer's TMEM / smem are done
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
+    if (PAIR) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
+    else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
   }
 }
 
@@ -960,7 +1079,7 @@ int pick_cel(int c) {
   return 0;
 }
 
-uint32_t make_idesc(int a_major, int b_major, int bn) {
+uint32_t make_idesc(int a_major, int b_major, int bn, int m = BM) {
   uint32_t d = 0;
   d |= 1u << 4;                    // D = f32
   d |= 1u << 7;                    // A = bf16
@@ -968,7 +1087,7 @@ uint32_t make_idesc(int a_major, int b_major, int bn) {
   d |= (uint32_t)a_major << 15;
   d |= (uint32_t)b_major << 16;
   d |= (uint32_t)(bn >> 3) << 17;
-  d |= (uint32_t)(BM >> 4) << 24;
+  d |= (uint32_t)(m >> 4) << 24;
   return d;
 }
 
@@ -1073,6 +1192,20 @@ int launch(GemmParams& p, cudaStream_t stream) {
   if (!p.kr) p.kr = BK;
   p.ksteps = p.kr / 16;
   if (!p.a_stage_bytes) p.a_stage_bytes = BM * p.kr * 2;
+  // CTA pair for gathered convs / dgrads with streamed weights: the two SMs of a TPC share
+  // one 256 x BN MMA, each loading its own 128-row A tile and HALF of the weight tile (the L2
+  // traffic per tile drops from A + B to A + B/2 and the B smem reads halve)
+  static int env_pair = -1;
+  if (env_pair < 0) { const char* e = getenv("CVB_GEMM_PAIR"); env_pair = e ? atoi(e) : 1; }
+  p.pair = (env_pair && p.mode == MODE_FWD && !p.b_res && p.b_ptr && p.m_tiles % 2 == 0 && p.BN % 32 == 0 &&
+            p.splits == 1 && g_num_sms % 2 == 0 && p.b_cel == 64 && p.gb == 1 && p.b_major == 0 && p.kr == BK &&
+            !(p.dbg & 3)) ? 1 : 0;
+  if (p.pair) {
+    int rc = encode_2d(&p.mapB[0], p.b_ptr, p.b_rows, p.b_cols, p.b_ld, p.b_cel, p.BN / 2);
+    if (rc) return rc;
+    p.b_stage_bytes = (uint32_t)(p.BN / 2) * p.kr * 2;
+    p.tx_bytes -= (uint32_t)(p.BN / 2) * p.b_cel * 2;   // this CTA's half of the weight box
+  }
   const uint32_t stage_bytes = p.a_stage_bytes + (p.b_res ? 0u : (p.b_stage_bytes ? p.b_stage_bytes
                                                                                    : (uint32_t)p.BN * p.kr * 2));
   static int env_epi4 = -1;
@@ -1129,9 +1262,11 @@ int launch(GemmParams& p, cudaStream_t stream) {
   // (~42 B/clk/SM: 576 KB of operands per 128x128 tile) and the pairing delays stage release:
   // measured +2.7% on the ResNet-18 GEMM class.  Opt-in (CVB_KB_PAIR=1) until operand reuse
   // lowers the L2 demand.
+  // With the CTA pair (half the L2 demand) pairing is the default; CVB_KB_PAIR=0/1 forces it.
   static int pair_on = -1;
-  if (pair_on < 0) pair_on = getenv("CVB_KB_PAIR") ? 1 : 0;
-  p.kb_pair = (pair_on && p.mode != MODE_HALO && p.ksteps == 4 && !p.b_res && p.stages >= 4 && !(env_dbg & 1)) ? 1 : 0;
+  if (pair_on < 0) { const char* e = getenv("CVB_KB_PAIR"); pair_on = e ? atoi(e) : 2; }
+  const bool want_kb_pair = pair_on == 1 || (pair_on == 2 && p.pair);
+  p.kb_pair = (want_kb_pair && p.mode != MODE_HALO && p.ksteps == 4 && !p.b_res && p.stages >= 4 && !(env_dbg & 1)) ? 1 : 0;
   p.trace = nullptr;
   if (env_dbg & 4) {
     static long long* tr = nullptr;
@@ -1143,9 +1278,11 @@ int launch(GemmParams& p, cudaStream_t stream) {
   if (p.stages < 2) { cvb_set_error("BN too large"); return CVB_EINVAL; }
   p.stg_off = (uint32_t)p.stages * stage_bytes + p.b_res_bytes;   // 1024-aligned (stages, slabs are)
   size_t smem = (size_t)p.stages * stage_bytes + p.b_res_bytes + stg + 1024 + 256;
-  if (cvb_first_on_device(&g_attr_done))
-    CVB_CUDA(cudaFuncSetAttribute(umma_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-  p.idesc = make_idesc(p.a_major, p.b_major, p.BN);
+  if (cvb_first_on_device(&g_attr_done)) {
+    CVB_CUDA(cudaFuncSetAttribute(umma_gemm_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    CVB_CUDA(cudaFuncSetAttribute(umma_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  }
+  p.idesc = make_idesc(p.a_major, p.b_major, p.BN, p.pair ? 2 * BM : BM);
   // smem box strides and descriptor templates
   p.a_box_stride = p.a_major == 0 ? BM * p.a_cel * 2 : p.kr * p.a_cel * 2;
   p.b_box_stride = p.b_major == 0 ? p.BN * p.b_cel * 2 : p.kr * p.b_cel * 2;
@@ -1177,15 +1314,32 @@ int launch(GemmParams& p, cudaStream_t stream) {
     p.adesc[0] = desc_tmpl(0, 16, (uint32_t)p.h_pitch * 16, 0);
     p.adesc[1] = desc_tmpl(0, (uint32_t)(p.h_pitch - p.h_kw + 1) * 16, (uint32_t)p.h_pitch * 16, 0);
   }
-  const int units = p.m_tiles * p.n_tiles * p.splits;
-  const int slots = g_num_sms * (p.two_cta ? 2 : 1);
-  const int grid = units < slots ? units : slots;
-  p.fd_m = make_fastdiv((uint32_t)p.m_tiles);
+  const int mtu = p.pair ? p.m_tiles / 2 : p.m_tiles;   // M scheduling units (tile pairs)
+  const int units = mtu * p.n_tiles * p.splits;
+  const int slots = p.pair ? g_num_sms / 2 : g_num_sms * (p.two_cta ? 2 : 1);
+  const int grid = (units < slots ? units : slots) * (p.pair ? 2 : 1);
+  p.fd_m = make_fastdiv((uint32_t)mtu);
   p.fd_n = make_fastdiv((uint32_t)p.n_tiles);
-  p.fd_mn = make_fastdiv((uint32_t)(p.m_tiles * p.n_tiles));
+  p.fd_mn = make_fastdiv((uint32_t)(mtu * p.n_tiles));
   p.fd_pw = make_fastdiv((uint32_t)(p.ptiles_w > 0 ? p.ptiles_w : 1));
   p.fd_ph = make_fastdiv((uint32_t)(p.ptiles_h > 0 ? p.ptiles_h : 1));
-  cvb_launch(umma_gemm_kernel, grid, (2 + p.n_epi) * 32, smem, stream, p);
+  if (p.pair) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3((2 + p.n_epi) * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = cvb_pdl_enabled() ? 2 : 1;
+    cudaLaunchKernelEx(&cfg, umma_gemm_kernel<1>, p);
+  } else {
+    cvb_launch(umma_gemm_kernel<0>, grid, (2 + p.n_epi) * 32, smem, stream, p);
+  }
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
@@ -1377,6 +1531,7 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
         if ((rc = encode_nhwc(&p.mapA[rh * 2 + rw], x, n, h, w, cin, xcs, acel, bw, bh, bnn, rh, rw))) return rc;
   }
   if ((rc = encode_2d(&p.mapB[0], wt, cout, K, K, p.b_cel, p.BN))) return rc;
+  p.b_ptr = wt; p.b_rows = cout; p.b_cols = K; p.b_ld = K;
   p.out_mode = OUT_NHWC; p.out_f32 = y_f32; p.out = y; p.ldc = ycs; p.col_off = yoff; p.bias = bias;
   p.accum = accumulate;
   return launch(p, (cudaStream_t)stream);
@@ -1455,6 +1610,7 @@ int plan_gather_conv(GemmParams& p, const void* x, int n, int h, int w, int cin,
   int rc;
   if ((rc = encode_nhwc(&p.mapA[0], x, n, h, w, cin, xcs, acel, bw, bh, bnn))) return rc;
   if ((rc = encode_2d(&p.mapB[0], wt, cout, K, K, p.b_cel, p.BN))) return rc;
+  p.b_ptr = wt; p.b_rows = cout; p.b_cols = K; p.b_ld = K;
   p.out_mode = OUT_NHWC; p.out_f32 = 0; p.out = y; p.ldc = ycs; p.col_off = 0; p.bias = nullptr;
   p.accum = accumulate;
   p.out_par = 1; p.out_ph = ph; p.out_pw = pw; p.out_H = H; p.out_W = W;

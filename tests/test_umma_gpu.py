@@ -39,6 +39,13 @@ CONV_CASES = [
     (2, 32, 32, 64, 256, 3, 1, 1),
     (4, 32, 32, 64, 64, 3, 1, 1),      # kh-paired wgrad (Cout 64): ResNet-18 stage-1 geometry
     (2, 24, 48, 64, 64, 3, 1, 1),
+    # CTA-pair (cta_group::2) gathered convs: ResNet-18 stage 2-4 geometries, the stride-2
+    # downsample, and an odd number of M tiles (single-CTA fallback)
+    (4, 16, 16, 128, 128, 3, 1, 1),
+    (4, 8, 8, 256, 256, 3, 1, 1),
+    (16, 4, 4, 512, 512, 3, 1, 1),
+    (8, 16, 16, 64, 128, 3, 2, 1),
+    (5, 8, 8, 128, 128, 3, 1, 1),
 ]
 
 
