@@ -60,19 +60,22 @@ static inline bool cvb_first_on_device(unsigned long long* mask) {
 #define CVB_GRID_BAR_WORDS 32
 #ifdef __CUDACC__
 __device__ __forceinline__ void cvb_grid_barrier(unsigned* bar) {
+  // release/acquire form: one acq_rel arrival (releases this CTA's writes, ordered before it
+  // by the __syncthreads), acquire polling of the generation word -- no full (sc) fences
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned* vgen = bar + 1;
-    const unsigned g = *vgen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
+    unsigned g, old;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+    if (old == gridDim.x - 1) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
     } else {
-      while (*vgen == g) __nanosleep(20);
+      unsigned cur;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
+      } while (cur == g);
     }
-    __threadfence();
   }
   __syncthreads();
 }
