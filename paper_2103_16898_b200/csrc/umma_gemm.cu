@@ -418,7 +418,7 @@ __device__ __forceinline__ void stage16(const GemmParams& p, uint32_t buf, int r
 // compile time: every A/B descriptor offset folds to a constant or one uniform add per tap,
 // so the issue loop is a few uniform instructions per MMA (the generic loop needed ~18 and
 // starved the tensor core: 96 cycles per N=32 MMA against a 40-cycle floor).
-template <int KH, int KW, int NJ>
+template <int KH, int KW, int NJ, int PAIR = 0>
 __device__ __forceinline__ void halo_issue(uint32_t tmem_d, uint64_t a0, uint64_t b0, uint32_t idesc, uint32_t acc_flag,
                                            uint32_t leader, int kb, uint32_t cin16, uint32_t slab16) {
   constexpr uint32_t pitch = 8 + KW - 1;
@@ -433,7 +433,7 @@ __device__ __forceinline__ void halo_issue(uint32_t tmem_d, uint64_t a0, uint64_
       const uint64_t bt = b0 + (uint64_t)((qt >> 2) * slab16 + ((qt & 3u) << 1));
 #pragma unroll
       for (int j = 0; j < NJ; j++) {
-        umma_bf16_el(tmem_d, a0 + (uint32_t)(kh * pitch + kw) + (uint32_t)j * plane2, bt + 2u * j, idesc, acc_flag, leader);
+        umma_t<PAIR>(tmem_d, a0 + (uint32_t)(kh * pitch + kw) + (uint32_t)j * plane2, bt + 2u * j, idesc, acc_flag, leader);
         acc_flag = 1u;
       }
       qt += cin16;
@@ -445,7 +445,7 @@ __device__ __forceinline__ void halo_issue(uint32_t tmem_d, uint64_t a0, uint64_
 // instead of eight 16-byte plane rows): tap (kh, kw) = start row kh*pitch + kw (8 x 16-byte
 // units per row), 16-channel step j = +32 bytes inside the swizzled row.  UMMA derives the
 // swizzle from absolute smem address bits, so row-shifted starts read the TMA layout exactly.
-template <int KH, int KW, int NJ, int RU, int PITCH = 8 + KW - 1>
+template <int KH, int KW, int NJ, int RU, int PITCH = 8 + KW - 1, int PAIR = 0>
 __device__ __forceinline__ void halo_rows_issue_t(uint32_t tmem_d, uint64_t a0, uint64_t b0, uint32_t idesc,
                                                 uint32_t acc_flag, uint32_t leader, int kb, uint32_t cin16,
                                                 uint32_t slab16) {
@@ -458,7 +458,7 @@ __device__ __forceinline__ void halo_rows_issue_t(uint32_t tmem_d, uint64_t a0, 
       const uint64_t bt = b0 + (uint64_t)((qt >> 2) * slab16 + ((qt & 3u) << 1));
 #pragma unroll
       for (int j = 0; j < NJ; j++) {
-        umma_bf16_el(tmem_d, a0 + (uint32_t)((kh * pitch + kw) * RU + 2 * j), bt + 2u * j, idesc, acc_flag, leader);
+        umma_t<PAIR>(tmem_d, a0 + (uint32_t)((kh * pitch + kw) * RU + 2 * j), bt + 2u * j, idesc, acc_flag, leader);
         acc_flag = 1u;
       }
       qt += cin16;
@@ -468,7 +468,7 @@ __device__ __forceinline__ void halo_rows_issue_t(uint32_t tmem_d, uint64_t a0, 
 
 // kw-box halo: box kw holds the 8 x (16+KH-1) pixels the kw taps read, so tap (kh, kw) starts
 // kh*8 rows (kh KB) into box kw -- an aligned SW128 start (SBO = 1024 B)
-template <int KH, int KW, int NJ>
+template <int KH, int KW, int NJ, int PAIR = 0>
 __device__ __forceinline__ void halo_kw_issue(uint32_t tmem_d, uint64_t a0, uint64_t b0, uint32_t idesc,
                                               uint32_t acc_flag, uint32_t leader, int kb, uint32_t cin16,
                                               uint32_t slab16, uint32_t box16) {
@@ -480,7 +480,7 @@ __device__ __forceinline__ void halo_kw_issue(uint32_t tmem_d, uint64_t a0, uint
       const uint64_t bt = b0 + (uint64_t)((qt >> 2) * slab16 + ((qt & 3u) << 1));
 #pragma unroll
       for (int j = 0; j < NJ; j++) {
-        umma_bf16_el(tmem_d, a0 + (uint32_t)kw * box16 + (uint32_t)(kh * 64 + 2 * j), bt + 2u * j, idesc, acc_flag,
+        umma_t<PAIR>(tmem_d, a0 + (uint32_t)kw * box16 + (uint32_t)(kh * 64 + 2 * j), bt + 2u * j, idesc, acc_flag,
                      leader);
         acc_flag = 1u;
       }
@@ -495,7 +495,7 @@ __device__ __forceinline__ void halo_kw_issue(uint32_t tmem_d, uint64_t a0, uint
 // (the next tap wraps to the next halo row, a1).  Flattened K = tap * 8 + ci matches the
 // natural [cout][kh][kw][8] weights; the odd last tap pairs with K >= KH*KW*8, which the
 // weight map zero-fills (its A half reads the extra halo column, finite data).
-template <int KH, int KW>
+template <int KH, int KW, int PAIR = 0>
 __device__ __forceinline__ void halo8_issue(uint32_t tmem_d, uint64_t a0, uint64_t a1, uint64_t b0, uint32_t idesc,
                                             uint32_t leader, uint32_t slab16) {
   constexpr int T = KH * KW, PITCH = 8 + KW;
@@ -503,7 +503,7 @@ __device__ __forceinline__ void halo8_issue(uint32_t tmem_d, uint64_t a0, uint64
   for (int q = 0; q < (T + 1) / 2; q++) {
     const int t0 = 2 * q, kh = t0 / KW, kw = t0 % KW;
     const bool wraps = (t0 + 1 < T) && ((t0 + 1) / KW != kh);
-    umma_bf16_el(tmem_d, (wraps ? a1 : a0) + (uint32_t)(kh * PITCH + kw),
+    umma_t<PAIR>(tmem_d, (wraps ? a1 : a0) + (uint32_t)(kh * PITCH + kw),
                  b0 + (uint64_t)((q >> 2) * slab16 + ((q & 3) << 1)), idesc, q > 0 ? 1u : 0u, leader);
   }
 }
@@ -594,12 +594,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
     int s = 0;
     uint32_t ph = 0;
     int it = 0;
-    if (!PAIR && p.b_res && leader && cl < units) {
-      // whole B operand (single N tile): b_slabs slabs of BN x 64, loaded once per CTA
-      mbar_expect_tx(bres_full, p.b_slabs * p.gb * p.BN * p.b_cel * 2);
-      for (int kb = 0; kb < p.b_slabs; kb++)
-        for (int g = 0; g < p.gb; g++)
-          tma_load_2d(&p.mapB[0], bres + kb * b_kb_bytes + g * p.b_box_stride, bres_full, kb * BK + g * p.b_cel, 0);
+    if (p.b_res && leader && cl < units) {
+      // whole B operand (single N tile): b_slabs slabs of BN x 64, loaded once per CTA (pair:
+      // this CTA's BN/2 rows, completing on the leader's barrier)
+      if constexpr (PAIR) {
+        const uint32_t bar_c = mapa_rank0(smem_u32(bres_full));
+        const int half = p.BN >> 1;
+        if (rank == 0) mbar_expect_tx(bres_full, 2u * p.b_slabs * p.gb * half * p.b_cel * 2);
+        for (int kb = 0; kb < p.b_slabs; kb++)
+          for (int g = 0; g < p.gb; g++)
+            tma_load_2d_pair(&p.mapB[0], bres + kb * (half * BK * 2) + g * p.b_box_stride, bar_c, kb * BK + g * p.b_cel,
+                             rank * half);
+      } else {
+        mbar_expect_tx(bres_full, p.b_slabs * p.gb * p.BN * p.b_cel * 2);
+        for (int kb = 0; kb < p.b_slabs; kb++)
+          for (int g = 0; g < p.gb; g++)
+            tma_load_2d(&p.mapB[0], bres + kb * b_kb_bytes + g * p.b_box_stride, bres_full, kb * BK + g * p.b_cel, 0);
+      }
     }
     __syncwarp();
     for (int u = cl; u < units; u += ncl) {
@@ -640,6 +651,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
             // both CTAs' boxes complete on the leader's barrier; the leader expects both halves
             const uint32_t bar_c = mapa_rank0(smem_u32(&full[s]));
             if (rank == 0) mbar_expect_tx(&full[s], 2u * tx);
+            if (p.mode == MODE_HALO) {   // this CTA's halo tile (weights are resident)
+              for (int j = 0; j < p.h_planes; j++) {
+                if (p.h_kwbox)
+                  tma_load_4d_pair(&p.mapA[0], sa + j * p.h_plane_stride, bar_c, kb * p.h_cg, tw0 - p.h_pad + j,
+                                   th0 - p.h_pad, tn0);
+                else
+                  tma_load_4d_pair(&p.mapA[0], sa + j * p.h_plane_stride, bar_c, kb * p.h_cg + 8 * j, tw0 - p.h_pad,
+                                   th0 - p.h_pad, tn0);
+              }
+            } else {
             const uint32_t* tab = p.boxtab + kb * p.ga;
             for (int g = 0; g < p.ga; g++) {
               const uint32_t e = tab[g];
@@ -649,6 +670,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
             for (int g = 0; g < p.gb; g++)
               tma_load_2d_pair(&p.mapB[0], sb + g * p.b_box_stride, bar_c, kb * BK + g * p.b_cel,
                                n0 + rank * (p.BN >> 1));
+            }
           } else if (p.dbg & 2) {
             mbar_arrive(&full[s]);
           } else {
@@ -780,8 +802,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           if (leader) mbar_arrive(&empty[s]);
         } else {
           const uint64_t sa = (smem0 + s * stage_bytes) >> 4;
-          if (!PAIR && p.mode == MODE_HALO) {
-            if constexpr (!PAIR) {
+          if (p.mode == MODE_HALO) {
+            {
             // every tap of this channel group reads the same halo planes at a row offset.
             // Offsets are plain uniform arithmetic (no table loads: with N = 64 an MMA is
             // only 48 smem-read cycles, so the issue loop must stay below that):
@@ -789,29 +811,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
             //   B: 16-element K unit q = tap*cin/16 + kb*cg/16 + j -> slab q/4, step q%4
             const uint64_t a0 = p.adesc[0] + sa, b0 = p.bdesc[0] + (bres >> 4);
             const uint32_t nj = (uint32_t)p.h_cg >> 4, cin16 = (uint32_t)p.h_cin >> 4;
-            const uint32_t plane2 = 2u * (p.h_plane_stride >> 4), slab16 = (uint32_t)p.BN * (BK * 2 / 16);
+            const uint32_t plane2 = 2u * (p.h_plane_stride >> 4), slab16 = (uint32_t)(PAIR ? p.BN >> 1 : p.BN) * (BK * 2 / 16);
             uint32_t acc_flag = kb > kb0 ? 1u : 0u;
             const int geo = p.h_kh * 100 + p.h_kw * 10 + (int)nj;
             const uint32_t box16 = p.h_plane_stride >> 4;
-            if (p.h_kwbox && geo == 334) halo_kw_issue<3, 3, 4>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16, box16);
-            else if (p.h_kwbox && geo == 332) halo_kw_issue<3, 3, 2>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16, box16);
-            else if (p.h_cg == 8) halo8_issue<3, 3>(tmem_d, a0, p.adesc[1] + sa, b0, p.idesc, leader, slab16);
-            else if (p.h_pitch == 16 && p.h_rowpad && geo == 332) halo_rows_issue_t<3, 3, 2, 8, 16>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
-            else if (p.h_pitch == 16 && p.h_rowpad && geo == 442) halo_rows_issue_t<4, 4, 2, 8, 16>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
-            else if (p.h_pitch == 16 && p.h_rows && geo == 334) halo_rows_issue_t<3, 3, 4, 8, 16>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
-            else if (p.h_rowpad && geo == 332) halo_rows_issue_t<3, 3, 2, 8>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
-            else if (p.h_rowpad && geo == 442) halo_rows_issue_t<4, 4, 2, 8>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
-            else if (p.h_rows && geo == 334) halo_rows_issue_t<3, 3, 4, 8>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
-            else if (p.h_rows && geo == 114) halo_rows_issue_t<1, 1, 4, 8>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
-            else if (p.h_rows && geo == 332) halo_rows_issue_t<3, 3, 2, 4>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
-            else if (p.h_rows && geo == 112) halo_rows_issue_t<1, 1, 2, 4>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
-            else if (p.h_rows && geo == 442) halo_rows_issue_t<4, 4, 2, 4>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
-            else if (geo == 334) halo_issue<3, 3, 4>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
-            else if (geo == 332) halo_issue<3, 3, 2>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
-            else if (geo == 331) halo_issue<3, 3, 1>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
-            else if (geo == 114) halo_issue<1, 1, 4>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
-            else if (geo == 112) halo_issue<1, 1, 2>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
-            else if (geo == 111) halo_issue<1, 1, 1>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            if (p.h_kwbox && geo == 334) halo_kw_issue<3, 3, 4, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16, box16);
+            else if (p.h_kwbox && geo == 332) halo_kw_issue<3, 3, 2, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16, box16);
+            else if (p.h_cg == 8) halo8_issue<3, 3, PAIR>(tmem_d, a0, p.adesc[1] + sa, b0, p.idesc, leader, slab16);
+            else if (p.h_pitch == 16 && p.h_rowpad && geo == 332) halo_rows_issue_t<3, 3, 2, 8, 16, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (p.h_pitch == 16 && p.h_rowpad && geo == 442) halo_rows_issue_t<4, 4, 2, 8, 16, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (p.h_pitch == 16 && p.h_rows && geo == 334) halo_rows_issue_t<3, 3, 4, 8, 16, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (p.h_rowpad && geo == 332) halo_rows_issue_t<3, 3, 2, 8, 8 + 3 - 1, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (p.h_rowpad && geo == 442) halo_rows_issue_t<4, 4, 2, 8, 8 + 4 - 1, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (p.h_rows && geo == 334) halo_rows_issue_t<3, 3, 4, 8, 8 + 3 - 1, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (p.h_rows && geo == 114) halo_rows_issue_t<1, 1, 4, 8, 8 + 1 - 1, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (p.h_rows && geo == 332) halo_rows_issue_t<3, 3, 2, 4, 8 + 3 - 1, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (p.h_rows && geo == 112) halo_rows_issue_t<1, 1, 2, 4, 8 + 1 - 1, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (p.h_rows && geo == 442) halo_rows_issue_t<4, 4, 2, 4, 8 + 4 - 1, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (geo == 334) halo_issue<3, 3, 4, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (geo == 332) halo_issue<3, 3, 2, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (geo == 331) halo_issue<3, 3, 1, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (geo == 114) halo_issue<1, 1, 4, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (geo == 112) halo_issue<1, 1, 2, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
+            else if (geo == 111) halo_issue<1, 1, 1, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
             else {
             uint32_t qt = (uint32_t)kb * nj;
             for (int kh = 0; kh < p.h_kh; kh++) {
@@ -821,7 +843,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
                 for (uint32_t j = 0; j < 4; j++) {
                   if (j < nj) {
                     const uint32_t q = qt + j;
-                    umma_bf16_el(tmem_d, arow + (uint32_t)kw + j * plane2, b0 + (q >> 2) * slab16 + ((q & 3u) << 1),
+                    umma_t<PAIR>(tmem_d, arow + (uint32_t)kw + j * plane2, b0 + (q >> 2) * slab16 + ((q & 3u) << 1),
                                  p.idesc, acc_flag, leader);
                     acc_flag = 1u;
                   }
@@ -1197,14 +1219,24 @@ int launch(GemmParams& p, cudaStream_t stream) {
   // traffic per tile drops from A + B to A + B/2 and the B smem reads halve)
   static int env_pair = -1;
   if (env_pair < 0) { const char* e = getenv("CVB_GEMM_PAIR"); env_pair = e ? atoi(e) : 1; }
-  p.pair = (env_pair && p.mode == MODE_FWD && !p.b_res && p.b_ptr && p.m_tiles % 2 == 0 && p.BN % 32 == 0 &&
-            p.splits == 1 && g_num_sms % 2 == 0 && p.b_cel == 64 && p.gb == 1 && p.b_major == 0 && p.kr == BK &&
-            !(p.dbg & 3)) ? 1 : 0;
+  // HALO convs (resident weights, each CTA keeps half the weight rows): correct but measured
+  // slower (conv 64->64 @32x32, batch 512: 49.9 -> 69.3 us; 32->32: 25.8 -> 38.7 us, it also
+  // displaces the two-CTA-per-SM plan) -- opt-in only (CVB_GEMM_PAIR_HALO=1)
+  static int env_pair_halo = -1;
+  if (env_pair_halo < 0) { const char* e = getenv("CVB_GEMM_PAIR_HALO"); env_pair_halo = e ? atoi(e) : 0; }
+  const bool pair_fwd = p.mode == MODE_FWD && !p.b_res && p.b_cel == 64 && p.gb == 1 && p.b_major == 0 && p.kr == BK;
+  const bool pair_halo = env_pair_halo && p.mode == MODE_HALO && p.b_res && p.b_cel == 64 && p.gb == 1;
+  p.pair = (env_pair && (pair_fwd || pair_halo) && p.b_ptr && p.m_tiles % 2 == 0 && p.BN % 32 == 0 &&
+            p.splits == 1 && g_num_sms % 2 == 0) ? 1 : 0;
   if (p.pair) {
     int rc = encode_2d(&p.mapB[0], p.b_ptr, p.b_rows, p.b_cols, p.b_ld, p.b_cel, p.BN / 2);
     if (rc) return rc;
-    p.b_stage_bytes = (uint32_t)(p.BN / 2) * p.kr * 2;
-    p.tx_bytes -= (uint32_t)(p.BN / 2) * p.b_cel * 2;   // this CTA's half of the weight box
+    if (p.b_res) {
+      p.b_res_bytes /= 2;   // this CTA's half of every weight slab
+    } else {
+      p.b_stage_bytes = (uint32_t)(p.BN / 2) * p.kr * 2;
+      p.tx_bytes -= (uint32_t)(p.BN / 2) * p.b_cel * 2;   // this CTA's half of the weight box
+    }
   }
   const uint32_t stage_bytes = p.a_stage_bytes + (p.b_res ? 0u : (p.b_stage_bytes ? p.b_stage_bytes
                                                                                    : (uint32_t)p.BN * p.kr * 2));
@@ -1224,7 +1256,7 @@ int launch(GemmParams& p, cudaStream_t stream) {
   static int env_2cta = -1;
   if (env_2cta < 0) { const char* e = getenv("CVB_GEMM_2CTA"); env_2cta = e ? atoi(e) : 1; }   // measured +3% step
   const uint32_t half = 112u * 1024u;
-  const bool two = env_2cta && p.mode == MODE_HALO && p.BN <= 32 &&
+  const bool two = env_2cta && !p.pair && p.mode == MODE_HALO && p.BN <= 32 &&
                    2 * stage_bytes + p.b_res_bytes + 16u * 1024u + 1280u <= half;
   p.n_epi = (!env_epi4 && !two && p.BN <= 64 && p.BN % 32 == 0) ? 8 : 4;
   // narrow tiles: more TMEM accumulators (the epilogue of tile i no longer gates the MMAs of
@@ -1486,6 +1518,7 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
       int rc;
       if ((rc = encode_nhwc(&p.mapA[0], x, n, h, w, cin, xcs, p.h_rows ? rowb / 2 : 8, p.h_pitch, hrows, 1))) return rc;
       if ((rc = encode_2d(&p.mapB[0], wt, cout, K, K, p.b_cel, p.BN))) return rc;
+      p.b_ptr = wt; p.b_rows = cout; p.b_cols = K; p.b_ld = K;
       p.out_mode = OUT_NHWC; p.out_f32 = y_f32; p.out = y; p.ldc = ycs; p.col_off = yoff; p.bias = bias;
       p.accum = accumulate;
       return launch(p, (cudaStream_t)stream);

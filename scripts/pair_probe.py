@@ -11,11 +11,14 @@ import torch  # noqa: E402
 from paper_2103_16898_b200 import kernels as K  # noqa: E402
 
 SHAPES = [  # n, h, w, cin, cout, k, s, p
+    (512, 32, 32, 8, 64, 3, 1, 1), (512, 32, 32, 64, 64, 3, 1, 1),                                   # ResNet-18 stem, stage 1 (halo)
+    (512, 32, 32, 8, 32, 3, 1, 1), (512, 32, 32, 32, 32, 3, 1, 1), (512, 16, 16, 32, 64, 3, 1, 1),   # small CNN (halo)
+    (512, 16, 16, 64, 64, 3, 1, 1),
     (512, 16, 16, 128, 128, 3, 1, 1), (512, 32, 32, 64, 128, 3, 2, 1), (512, 32, 32, 64, 128, 1, 2, 0),
     (512, 8, 8, 256, 256, 3, 1, 1), (512, 16, 16, 128, 256, 3, 2, 1),
     (512, 4, 4, 512, 512, 3, 1, 1), (512, 8, 8, 256, 512, 3, 2, 1),
 ]
-tag = f"pair={os.environ.get('CVB_GEMM_PAIR', '1')} kbpair={os.environ.get('CVB_KB_PAIR', 'auto')}"
+tag = f"pair={os.environ.get('CVB_GEMM_PAIR', '1')}/{os.environ.get('CVB_GEMM_PAIR_HALO', '1')} kbpair={os.environ.get('CVB_KB_PAIR', 'auto')}"
 for (n, h, w, cin, cout, k, s, p) in SHAPES:
     x = torch.randn(n, h, w, cin, device="cuda").to(torch.bfloat16)
     wt = (torch.randn(cout, k, k, cin, device="cuda") / (k * k * cin) ** 0.5).to(torch.bfloat16)
