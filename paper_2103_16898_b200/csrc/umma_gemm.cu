@@ -651,7 +651,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
             // both CTAs' boxes complete on the leader's barrier; the leader expects both halves
             const uint32_t bar_c = mapa_rank0(smem_u32(&full[s]));
             if (rank == 0) mbar_expect_tx(&full[s], 2u * tx);
-            if (p.mode == MODE_HALO) {   // this CTA's halo tile (weights are resident)
+            if (p.mode == MODE_WGRAD) {   // own 128 Cout rows of dY, this CTA's half of the input boxes
+              for (int b = 0; b < p.ga; b++)
+                tma_load_4d_pair(&p.mapA[0], sa + b * p.a_box_stride, bar_c, m0 + b * p.a_cel, pw, ph0, pn);
+              const int gh = p.gb >> 1;
+              const uint32_t* tab = p.boxtab + nt * p.gb + rank * gh;
+              for (int j = 0; j < gh; j++) {
+                const uint32_t e = tab[j];
+                tma_load_4d_pair(&p.mapB[e & 3], sb + j * p.b_box_stride, bar_c, (int)((e >> 2) & 0xFFFF),
+                                 pw + (int)((e >> 18) & 127) - 64, ph0 + (int)(e >> 25) - 64, pn);
+              }
+            } else if (p.mode == MODE_HALO) {   // this CTA's halo tile (weights are resident)
               for (int j = 0; j < p.h_planes; j++) {
                 if (p.h_kwbox)
                   tma_load_4d_pair(&p.mapA[0], sa + j * p.h_plane_stride, bar_c, kb * p.h_cg, tw0 - p.h_pad + j,
@@ -1226,9 +1236,19 @@ int launch(GemmParams& p, cudaStream_t stream) {
   if (env_pair_halo < 0) { const char* e = getenv("CVB_GEMM_PAIR_HALO"); env_pair_halo = e ? atoi(e) : 0; }
   const bool pair_fwd = p.mode == MODE_FWD && !p.b_res && p.b_cel == 64 && p.gb == 1 && p.b_major == 0 && p.kr == BK;
   const bool pair_halo = env_pair_halo && p.mode == MODE_HALO && p.b_res && p.b_cel == 64 && p.gb == 1;
+  // weight gradients with Cout a multiple of 256: the pair shares the input (B) boxes
+  static int env_pair_wg = -1;
+  if (env_pair_wg < 0) { const char* e = getenv("CVB_GEMM_PAIR_WGRAD"); env_pair_wg = e ? atoi(e) : 1; }
+  const bool pair_wgrad = env_pair_wg && p.mode == MODE_WGRAD && !p.w_halo && !p.w_pair && p.M % 256 == 0 &&
+                          p.gb % 2 == 0 && p.a_major == 1 && p.b_major == 1;
+  if (env_pair && pair_wgrad && p.m_tiles % 2 == 0 && g_num_sms % 2 == 0 && p.BN % 32 == 0) {
+    p.pair = 1;
+    p.b_stage_bytes = (uint32_t)(p.BN / 2) * p.kr * 2;
+    p.tx_bytes -= (uint32_t)(p.gb / 2) * p.kr * p.b_cel * 2;   // this CTA's half of the input boxes
+  } else
   p.pair = (env_pair && (pair_fwd || pair_halo) && p.b_ptr && p.m_tiles % 2 == 0 && p.BN % 32 == 0 &&
             p.splits == 1 && g_num_sms % 2 == 0) ? 1 : 0;
-  if (p.pair) {
+  if (p.pair && p.mode != MODE_WGRAD) {
     int rc = encode_2d(&p.mapB[0], p.b_ptr, p.b_rows, p.b_cols, p.b_ld, p.b_cel, p.BN / 2);
     if (rc) return rc;
     if (p.b_res) {
