@@ -74,6 +74,7 @@ __device__ __forceinline__ void cvb_grid_barrier(unsigned* bar) {
       unsigned cur;
       do {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
+        if (cur == g) __nanosleep(32);
       } while (cur == g);
     }
   }
