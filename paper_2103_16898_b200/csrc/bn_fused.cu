@@ -35,6 +35,35 @@ __device__ __forceinline__ void ld8(const bf16* p, float v[8]) {
 #pragma unroll
   for (int i = 0; i < 4; i++) { float2 f = __bfloat1622float2(h[i]); v[2 * i] = f.x; v[2 * i + 1] = f.y; }
 }
+// L2 residency between the two passes: pass-1 loads mark lines evict_last, pass-2 loads
+// evict_first, and pass 2 walks each CTA's rows last-to-first (the lines pass 1 touched last
+// are the ones still in L2).  hint == 0: plain __ldcg, forward order (A/B knob CVB_BN_L2HINT=0).
+__device__ __forceinline__ uint4 ldv_pol(const void* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint64_t pol_keep() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t pol_drop() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint4 ldv(const void* p, bool hint, uint64_t pol) {
+  return hint ? ldv_pol(p, pol) : __ldcg(reinterpret_cast<const uint4*>(p));
+}
+__device__ __forceinline__ void unpack8(const uint4& u, float v[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; i++) { float2 f = __bfloat1622float2(h[i]); v[2 * i] = f.x; v[2 * i + 1] = f.y; }
+}
+__device__ __forceinline__ void ld8h(const bf16* p, float v[8], bool hint, uint64_t pol) { unpack8(ldv(p, hint, pol), v); }
+
 __device__ __forceinline__ void st8(bf16* p, const float v[8]) {
   uint4 u;
   __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
@@ -99,6 +128,7 @@ struct FwdArgs {
   bf16* y; int ycs, ycoff;   // y == nullptr: statistics only
   int four_rows;             // pass 2 without residual: 4 rows in flight (CVB_BN_FWD_TWO_ROWS=1: off)
   long long* trace;          // CVB_BN_TRACE: per-CTA phase timestamps (globaltimer ns), debug only
+  int hint;                  // L2 residency hints + reversed pass 2 (see ldv)
 };
 
 __global__ void __launch_bounds__(THREADS) bn_fwd_fused(const FwdArgs a) {
@@ -110,13 +140,15 @@ __global__ void __launch_bounds__(THREADS) bn_fwd_fused(const FwdArgs a) {
   const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(a.rows, r0 + per);
   bn_trace(a.trace, 0);
   // ---- pass 1: partial statistics ----
+  const bool hint = a.hint != 0;
+  const uint64_t pk = hint ? pol_keep() : 0, pd = hint ? pol_drop() : 0;
   float s[8] = {0}, q[8] = {0};
   if (rl < RL) {
     int64_t r = r0 + rl;
     for (; r + (UNROLL - 1) * RL < r1; r += UNROLL * RL) {
       float v[UNROLL][8];
 #pragma unroll
-      for (int u = 0; u < UNROLL; u++) ld8(a.x + (r + u * RL) * a.xcs + g * 8, v[u]);
+      for (int u = 0; u < UNROLL; u++) ld8h(a.x + (r + u * RL) * a.xcs + g * 8, v[u], hint, pk);
 #pragma unroll
       for (int u = 0; u < UNROLL; u++)
 #pragma unroll
@@ -124,7 +156,7 @@ __global__ void __launch_bounds__(THREADS) bn_fwd_fused(const FwdArgs a) {
     }
     for (; r < r1; r += RL) {
       float v[8];
-      ld8(a.x + r * a.xcs + g * 8, v);
+      ld8h(a.x + r * a.xcs + g * 8, v, hint, pk);
 #pragma unroll
       for (int i = 0; i < 8; i++) { s[i] += v[i]; q[i] += v[i] * v[i]; }
     }
@@ -170,11 +202,13 @@ __global__ void __launch_bounds__(THREADS) bn_fwd_fused(const FwdArgs a) {
 #pragma unroll
   for (int k = 0; k < 8; k++) { sc[k] = s_scale[g * 8 + k]; mu[k] = s_shift[g * 8 + k]; be[k] = a.beta[g * 8 + k]; }
   int64_t r = r0 + rl;
+  // pass 2 row order: reversed with the hints (R maps a forward row index to the row visited)
+#define R(x) (hint ? r0 + r1 - 1 - (x) : (x))
   if (!a.res && a.four_rows) {   // four rows' raw 16-byte loads in flight per thread
     for (; r + 3 * RL < r1; r += 4 * RL) {
       uint4 u[4];
 #pragma unroll
-      for (int j = 0; j < 4; j++) u[j] = __ldcg(reinterpret_cast<const uint4*>(a.x + (r + j * RL) * a.xcs + g * 8));
+      for (int j = 0; j < 4; j++) u[j] = ldv(a.x + R(r + j * RL) * a.xcs + g * 8, hint, pd);
 #pragma unroll
       for (int j = 0; j < 4; j++) {
         const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u[j]);
@@ -187,35 +221,36 @@ __global__ void __launch_bounds__(THREADS) bn_fwd_fused(const FwdArgs a) {
           o[2 * i] = a.relu ? fmaxf(z0, 0.f) : z0;
           o[2 * i + 1] = a.relu ? fmaxf(z1, 0.f) : z1;
         }
-        st8(a.y + (r + j * RL) * a.ycs + a.ycoff + g * 8, o);
+        st8(a.y + R(r + j * RL) * a.ycs + a.ycoff + g * 8, o);
       }
     }
   }
   if (!a.res) {   // two rows in flight per thread
     for (; r + RL < r1; r += 2 * RL) {
       float v0[8], v1[8], o[8];
-      ld8(a.x + r * a.xcs + g * 8, v0);
-      ld8(a.x + (r + RL) * a.xcs + g * 8, v1);
+      ld8h(a.x + R(r) * a.xcs + g * 8, v0, hint, pd);
+      ld8h(a.x + R(r + RL) * a.xcs + g * 8, v1, hint, pd);
 #pragma unroll
       for (int k = 0; k < 8; k++) { const float z = (v0[k] - mu[k]) * sc[k] + be[k]; o[k] = a.relu ? fmaxf(z, 0.f) : z; }
-      st8(a.y + r * a.ycs + a.ycoff + g * 8, o);
+      st8(a.y + R(r) * a.ycs + a.ycoff + g * 8, o);
 #pragma unroll
       for (int k = 0; k < 8; k++) { const float z = (v1[k] - mu[k]) * sc[k] + be[k]; o[k] = a.relu ? fmaxf(z, 0.f) : z; }
-      st8(a.y + (r + RL) * a.ycs + a.ycoff + g * 8, o);
+      st8(a.y + R(r + RL) * a.ycs + a.ycoff + g * 8, o);
     }
   }
   for (; r < r1; r += RL) {
     float v[8], o[8], rv[8];
-    ld8(a.x + r * a.xcs + g * 8, v);
-    if (a.res) ld8(a.res + r * a.rcs + g * 8, rv);
+    ld8h(a.x + R(r) * a.xcs + g * 8, v, hint, pd);
+    if (a.res) ld8(a.res + R(r) * a.rcs + g * 8, rv);
 #pragma unroll
     for (int k = 0; k < 8; k++) {
       float z = (v[k] - mu[k]) * sc[k] + be[k];
       if (a.res) z += rv[k];
       o[k] = a.relu ? fmaxf(z, 0.f) : z;
     }
-    st8(a.y + r * a.ycs + a.ycoff + g * 8, o);
+    st8(a.y + R(r) * a.ycs + a.ycoff + g * 8, o);
   }
+#undef R
   bn_trace(a.trace, 6);
 }
 
@@ -227,6 +262,7 @@ struct BwdArgs {
   bf16* dx; int dxcs; float* dx32; int accum32; bf16* dz_out;
   int two_rows;              // pass 2: two rows' raw loads in flight (CVB_BN_BWD_ONE_ROW=1: off)
   long long* trace;          // CVB_BN_TRACE: per-CTA phase timestamps (globaltimer ns), debug only
+  int hint;                  // L2 residency hints + reversed pass 2 (see ldv)
 };
 
 // Per-channel constants live in shared memory (8 consecutive floats per channel group, two
@@ -243,10 +279,10 @@ __device__ __forceinline__ void lds8(const float* p, float v[8]) {
 
 // dz = dy * relu-mask and xhat for one row (8 channels of group g)
 __device__ __forceinline__ void bwd_load(const BwdArgs& a, int64_t r, int g, const ChanSmem& cs, float d[8],
-                                         float xh[8]) {
+                                         float xh[8], bool hint = false, uint64_t pol = 0) {
   float xv[8];
-  ld8(a.dy + r * a.dycs + g * 8, d);
-  ld8(a.x + r * a.xcs + g * 8, xv);
+  ld8h(a.dy + r * a.dycs + g * 8, d, hint, pol);
+  ld8h(a.x + r * a.xcs + g * 8, xv, hint, pol);
   float mu[8], rs[8];
   lds8(cs.mu + g * 8, mu);
   lds8(cs.rs + g * 8, rs);
@@ -255,7 +291,7 @@ __device__ __forceinline__ void bwd_load(const BwdArgs& a, int64_t r, int g, con
   if (a.relu) {
     if (a.y) {
       float yv[8];
-      ld8(a.y + r * a.ycs + g * 8, yv);
+      ld8h(a.y + r * a.ycs + g * 8, yv, hint, pol);
 #pragma unroll
       for (int k = 0; k < 8; k++) if (!(yv[k] > 0.f)) d[k] = 0.f;
     } else {
@@ -334,13 +370,15 @@ __global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
   }
   __syncthreads();
   // ---- pass 1: sum(dz), sum(dz * xhat) ----
+  const bool hint = a.hint != 0;
+  const uint64_t pk = hint ? pol_keep() : 0, pd = hint ? pol_drop() : 0;
   float s[8] = {0}, q[8] = {0};
   if (rl < RL) {
     int64_t r = r0 + rl;
     for (; r + RL < r1; r += 2 * RL) {
       float d0[8], x0[8], d1[8], x1[8];
-      bwd_load(a, r, g, cs, d0, x0);
-      bwd_load(a, r + RL, g, cs, d1, x1);
+      bwd_load(a, r, g, cs, d0, x0, hint, pk);
+      bwd_load(a, r + RL, g, cs, d1, x1, hint, pk);
 #pragma unroll
       for (int k = 0; k < 8; k++) { s[k] += d0[k]; q[k] += d0[k] * x0[k]; }
 #pragma unroll
@@ -349,7 +387,7 @@ __global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
     }
     for (; r < r1; r += RL) {
       float d[8], xh[8];
-      bwd_load(a, r, g, cs, d, xh);
+      bwd_load(a, r, g, cs, d, xh, hint, pk);
 #pragma unroll
       for (int k = 0; k < 8; k++) { s[k] += d[k]; q[k] += d[k] * xh[k]; }
       if (a.dz_out) st8(a.dz_out + r * C + g * 8, d);
@@ -378,21 +416,22 @@ __global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
   __syncthreads();
   if (rl >= RL) return;
   int64_t r = r0 + rl;
+#define R(x) (hint ? r0 + r1 - 1 - (x) : (x))
   if (a.dz_out && !a.dx32) {
     // pass 1 stored dz = dy * mask (the residual branch's gradient): pass 2 reads it instead of
     // dy and y -- two tensors per row instead of three -- two rows' loads in flight
     for (; r + RL < r1; r += 2 * RL) {
-      const uint4 uz0 = __ldcg(reinterpret_cast<const uint4*>(a.dz_out + r * C + g * 8));
-      const uint4 ux0 = __ldcg(reinterpret_cast<const uint4*>(a.x + r * a.xcs + g * 8));
-      const uint4 uz1 = __ldcg(reinterpret_cast<const uint4*>(a.dz_out + (r + RL) * C + g * 8));
-      const uint4 ux1 = __ldcg(reinterpret_cast<const uint4*>(a.x + (r + RL) * a.xcs + g * 8));
-      bwd_apply_dz(cs, sh, C, g, uz0, ux0, a.dx + r * a.dxcs + g * 8);
-      bwd_apply_dz(cs, sh, C, g, uz1, ux1, a.dx + (r + RL) * a.dxcs + g * 8);
+      const uint4 uz0 = ldv(a.dz_out + R(r) * C + g * 8, hint, pd);
+      const uint4 ux0 = ldv(a.x + R(r) * a.xcs + g * 8, hint, pd);
+      const uint4 uz1 = ldv(a.dz_out + R(r + RL) * C + g * 8, hint, pd);
+      const uint4 ux1 = ldv(a.x + R(r + RL) * a.xcs + g * 8, hint, pd);
+      bwd_apply_dz(cs, sh, C, g, uz0, ux0, a.dx + R(r) * a.dxcs + g * 8);
+      bwd_apply_dz(cs, sh, C, g, uz1, ux1, a.dx + R(r + RL) * a.dxcs + g * 8);
     }
     if (r < r1) {
-      const uint4 uz0 = __ldcg(reinterpret_cast<const uint4*>(a.dz_out + r * C + g * 8));
-      const uint4 ux0 = __ldcg(reinterpret_cast<const uint4*>(a.x + r * a.xcs + g * 8));
-      bwd_apply_dz(cs, sh, C, g, uz0, ux0, a.dx + r * a.dxcs + g * 8);
+      const uint4 uz0 = ldv(a.dz_out + R(r) * C + g * 8, hint, pd);
+      const uint4 ux0 = ldv(a.x + R(r) * a.xcs + g * 8, hint, pd);
+      bwd_apply_dz(cs, sh, C, g, uz0, ux0, a.dx + R(r) * a.dxcs + g * 8);
     }
     return;
   }
@@ -400,24 +439,24 @@ __global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
     // bf16 dx, mask recomputed from x: two rows' raw 16-byte loads in flight per thread (the
     // pass is load-latency bound), converted one row at a time (stays within 64 registers)
     for (; r + RL < r1; r += 2 * RL) {
-      const uint4 ud0 = __ldcg(reinterpret_cast<const uint4*>(a.dy + r * a.dycs + g * 8));
-      const uint4 ux0 = __ldcg(reinterpret_cast<const uint4*>(a.x + r * a.xcs + g * 8));
-      const uint4 ud1 = __ldcg(reinterpret_cast<const uint4*>(a.dy + (r + RL) * a.dycs + g * 8));
-      const uint4 ux1 = __ldcg(reinterpret_cast<const uint4*>(a.x + (r + RL) * a.xcs + g * 8));
-      bwd_apply_raw(a, cs, sh, C, g, ud0, ux0, a.dx + r * a.dxcs + g * 8);
-      bwd_apply_raw(a, cs, sh, C, g, ud1, ux1, a.dx + (r + RL) * a.dxcs + g * 8);
+      const uint4 ud0 = ldv(a.dy + R(r) * a.dycs + g * 8, hint, pd);
+      const uint4 ux0 = ldv(a.x + R(r) * a.xcs + g * 8, hint, pd);
+      const uint4 ud1 = ldv(a.dy + R(r + RL) * a.dycs + g * 8, hint, pd);
+      const uint4 ux1 = ldv(a.x + R(r + RL) * a.xcs + g * 8, hint, pd);
+      bwd_apply_raw(a, cs, sh, C, g, ud0, ux0, a.dx + R(r) * a.dxcs + g * 8);
+      bwd_apply_raw(a, cs, sh, C, g, ud1, ux1, a.dx + R(r + RL) * a.dxcs + g * 8);
     }
   }
   for (; r < r1; r += RL) {
     float d[8], xh[8], o[8], kk[8], kb[8], kg[8];
-    bwd_load(a, r, g, cs, d, xh);
+    bwd_load(a, R(r), g, cs, d, xh, hint, pd);
     lds8(sh + g * 8, kk);
     lds8(sh + C + g * 8, kb);
     lds8(sh + 2 * C + g * 8, kg);
 #pragma unroll
     for (int k = 0; k < 8; k++) o[k] = kk[k] * (d[k] - kb[k] - xh[k] * kg[k]);
     if (a.dx32) {
-      float4* p4 = reinterpret_cast<float4*>(a.dx32 + r * a.dxcs + g * 8);
+      float4* p4 = reinterpret_cast<float4*>(a.dx32 + R(r) * a.dxcs + g * 8);
       if (a.accum32) {
         float4 u = p4[0], w = p4[1];
         o[0] += u.x; o[1] += u.y; o[2] += u.z; o[3] += u.w;
@@ -426,9 +465,10 @@ __global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
       p4[0] = make_float4(o[0], o[1], o[2], o[3]);
       p4[1] = make_float4(o[4], o[5], o[6], o[7]);
     } else {
-      st8(a.dx + r * a.dxcs + g * 8, o);
+      st8(a.dx + R(r) * a.dxcs + g * 8, o);
     }
   }
+#undef R
 }
 
 unsigned* g_bar[64] = {nullptr};
@@ -482,6 +522,12 @@ int size_grid(int grid, int64_t rows, int C) {
   return (int)(want < grid ? (want < 8 ? 8 : want) : grid);
 }
 
+int l2hint_knob() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("CVB_BN_L2HINT"); v = e ? atoi(e) : 1; }
+  return v;
+}
+
 int two_rows_knob() {
   static int v = -1;
   if (v < 0) v = getenv("CVB_BN_BWD_ONE_ROW") ? 0 : 1;
@@ -526,7 +572,8 @@ CVB_API int cvb_bn_forward(const void* x, int64_t rows, int C, int xcs, float* w
   int rc = fused_setup(C, &bar, &grid_b, &grid);
   if (rc) return rc;
   FwdArgs a{(const bf16*)x, rows, C, xcs, ws, bar, mean, rstd, eps, run_mean, run_var, momentum, gamma, beta,
-            (const bf16*)res, rcs, relu, (bf16*)y, ycs, ycoff, getenv("CVB_BN_FWD_TWO_ROWS") ? 0 : 1, trace_buf()};
+            (const bf16*)res, rcs, relu, (bf16*)y, ycs, ycoff, getenv("CVB_BN_FWD_TWO_ROWS") ? 0 : 1, trace_buf(),
+            l2hint_knob()};
   const int gf = size_grid(grid, rows, C);
   if (C > 16 * gf) { cvb_set_error("bn_forward: more channels than finalising warps"); return CVB_EINVAL; }
   return launch_coop(bn_fwd_fused, a, gf, (cudaStream_t)stream);
@@ -543,7 +590,8 @@ CVB_API int cvb_bn_backward_fused(const void* dy, int dycs, const void* x, int x
   int rc = fused_setup(C, &bar, &grid);
   if (rc) return rc;
   BwdArgs a{(const bf16*)dy, dycs, (const bf16*)x, xcs, (const bf16*)y, ycs, rows, C, mean, rstd, gamma, beta, relu,
-            ws, bar, dgamma, dbeta, (bf16*)dx, dxcs, dx32, accum32, (bf16*)dz_out, two_rows_knob(), trace_buf()};
+            ws, bar, dgamma, dbeta, (bf16*)dx, dxcs, dx32, accum32, (bf16*)dz_out, two_rows_knob(), trace_buf(),
+            l2hint_knob()};
   const int gb = size_grid(grid, rows, C);
   if (C > 16 * gb) { cvb_set_error("bn_backward: more channels than finalising warps"); return CVB_EINVAL; }
   return launch_coop(bn_bwd_fused, a, gb, (cudaStream_t)stream);
