@@ -62,6 +62,16 @@ int64_t cvb_bn_fused_workspace_floats(int C);
 int cvb_bn_forward(const void* x, int64_t rows, int C, int xcs, float* ws, float* mean, float* rstd, float eps,
                    float* run_mean, float* run_var, float momentum, const float* gamma, const float* beta,
                    const void* res, int rcs, int relu, void* y, int ycs, int ycoff, void* stream);
+/* DenseNet: input gradient of the BNs over a concat range, formed once from every later layer's
+   dY slice after those layers ran the statistics pass only (cvb_bn_backward_fused with dx = dx32 =
+   NULL): out[r][c] = base[r][c] + sum_l gamma_l*rstd*(dz_l - dbeta_l/M - xhat*dgamma_l/M) for c in
+   [0, nc), dz_l = dy_l * [gamma_l*xhat + beta_l > 0]; layers summed in array order.  The pointer
+   arrays (host, nl <= 32) are offset to the range's first channel; out (bf16, or fp32 if out_f32)
+   may alias base. */
+int cvb_bn_gather_dx(const void* x, int xcs, int64_t rows, int nc, const float* mean, const float* rstd,
+                     const float* base, int bcs, int nl, const void* const* dy, const int* dycs,
+                     const float* const* gamma, const float* const* beta, const float* const* dgamma,
+                     const float* const* dbeta, void* out, int ocs, int out_f32, void* stream);
 int cvb_bn_backward_fused(const void* dy, int dycs, const void* x, int xcs, const void* y, int ycs, int64_t rows,
                           int C, const float* mean, const float* rstd, const float* gamma, const float* beta, int relu,
                           float* ws, float* dgamma, float* dbeta, void* dx, int dxcs, float* dx32, int accum32,

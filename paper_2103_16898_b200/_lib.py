@@ -63,6 +63,8 @@ SIGNATURES = {
     # tcgen05 implicit-GEMM engine (include/cvb_nn.h)
     "cvb_conv2d_fwd": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT,
                               _INT, _INT, _P, _INT, _INT, _P]),
+    "cvb_bn_gather_dx": (_INT, [_P, _INT, _I64, _INT, _P, _P, _P, _INT, _INT, _P, _P, _P, _P, _P, _P, _P, _INT,
+                                _INT, _P]),
     "cvb_conv2d_wgrad": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT, _INT, _INT, _INT, _INT, _INT,
                                 _INT, _P, _INT, _c.POINTER(_INT), _P]),
     "cvb_gemm": (_INT, [_P, _INT, _I64, _P, _INT, _I64, _INT, _INT, _INT, _P, _I64, _INT, _P, _INT, _INT, _P]),

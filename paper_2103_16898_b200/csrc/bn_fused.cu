@@ -286,8 +286,10 @@ __device__ __forceinline__ void bwd_load(const BwdArgs& a, int64_t r, int g, con
   float mu[8], rs[8];
   lds8(cs.mu + g * 8, mu);
   lds8(cs.rs + g * 8, rs);
+  // explicit roundings (no FMA contraction): DenseNet's deferred gather (bn_gather_dx) repeats
+  // this arithmetic and must reproduce it bit for bit
 #pragma unroll
-  for (int k = 0; k < 8; k++) xh[k] = (xv[k] - mu[k]) * rs[k];
+  for (int k = 0; k < 8; k++) xh[k] = __fmul_rn(__fsub_rn(xv[k], mu[k]), rs[k]);
   if (a.relu) {
     if (a.y) {
       float yv[8];
@@ -299,7 +301,7 @@ __device__ __forceinline__ void bwd_load(const BwdArgs& a, int64_t r, int g, con
       lds8(cs.ga + g * 8, ga);
       lds8(cs.be + g * 8, be);
 #pragma unroll
-      for (int k = 0; k < 8; k++) if (!(xh[k] * ga[k] + be[k] > 0.f)) d[k] = 0.f;
+      for (int k = 0; k < 8; k++) if (!(__fadd_rn(__fmul_rn(xh[k], ga[k]), be[k]) > 0.f)) d[k] = 0.f;
     }
   }
 }
@@ -454,13 +456,14 @@ __global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
     lds8(sh + C + g * 8, kb);
     lds8(sh + 2 * C + g * 8, kg);
 #pragma unroll
-    for (int k = 0; k < 8; k++) o[k] = kk[k] * (d[k] - kb[k] - xh[k] * kg[k]);
+    for (int k = 0; k < 8; k++) o[k] = __fmul_rn(kk[k], __fsub_rn(__fsub_rn(d[k], kb[k]), __fmul_rn(xh[k], kg[k])));
     if (a.dx32) {
       float4* p4 = reinterpret_cast<float4*>(a.dx32 + R(r) * a.dxcs + g * 8);
       if (a.accum32) {
         float4 u = p4[0], w = p4[1];
-        o[0] += u.x; o[1] += u.y; o[2] += u.z; o[3] += u.w;
-        o[4] += w.x; o[5] += w.y; o[6] += w.z; o[7] += w.w;
+        o[0] = __fadd_rn(u.x, o[0]); o[1] = __fadd_rn(u.y, o[1]); o[2] = __fadd_rn(u.z, o[2]);
+        o[3] = __fadd_rn(u.w, o[3]); o[4] = __fadd_rn(w.x, o[4]); o[5] = __fadd_rn(w.y, o[5]);
+        o[6] = __fadd_rn(w.z, o[6]); o[7] = __fadd_rn(w.w, o[7]);
       }
       p4[0] = make_float4(o[0], o[1], o[2], o[3]);
       p4[1] = make_float4(o[4], o[5], o[6], o[7]);
@@ -596,6 +599,143 @@ CVB_API int cvb_bn_backward_fused(const void* dy, int dycs, const void* x, int x
   if (C > 16 * gb) { cvb_set_error("bn_backward: more channels than finalising warps"); return CVB_EINVAL; }
   return launch_coop(bn_bwd_fused, a, gb, (cudaStream_t)stream);
 }
+
+// ---- DenseNet: deferred input gradient of the BNs over a concat prefix ------------------
+// Every BN over the concat buffer of a dense block normalises the same channels with the same
+// batch statistics (mean, rstd shared); only gamma/beta differ per layer.  Instead of each
+// layer's backward adding its dx into an fp32 concat gradient (pass 2 re-reading dy and x and
+// read-modify-writing 4 bytes per element per layer), the layers run the statistics pass only
+// (dbeta = sum dz, dgamma = sum dz*xhat) and keep their dY.  The gradient of a channel range is
+// then formed ONCE, when it is needed, from every later layer's dY slice:
+//   out = base + sum_l  k_l * (dz_l - dbeta_l/M - xhat * dgamma_l/M),
+//   dz_l = dy_l * [gamma_l * xhat + beta_l > 0],  k_l = gamma_l * rstd,  xhat = (x - mean) * rstd
+// with the layers summed in the order given (the backward order) -- the same fp32 arithmetic,
+// in the same order, as the accumulating per-layer form (bit-identical).
+namespace {
+constexpr int GATHER_MAX_LAYERS = 32;
+struct GatherArgs {
+  const bf16* x; int xcs; int64_t rows; int nc;
+  const float* mean; const float* rstd;
+  const float* base; int bcs;            // fp32 base gradient (channel 0 of the range), may be null
+  int nl;
+  const bf16* dy[GATHER_MAX_LAYERS];     // layer l's dY at channel 0 of the range (stride dycs[l])
+  int dycs[GATHER_MAX_LAYERS];
+  const float* gamma[GATHER_MAX_LAYERS];
+  const float* beta[GATHER_MAX_LAYERS];
+  const float* dgamma[GATHER_MAX_LAYERS];   // raw sums from the statistics pass
+  const float* dbeta[GATHER_MAX_LAYERS];
+  void* out; int ocs; int out_f32;
+};
+
+constexpr int GATHER_THREADS = 256, GATHER_CH = 64;   // a CTA: 64 channels (8 groups) x 32 row lanes
+
+__global__ void __launch_bounds__(GATHER_THREADS) bn_gather_dx(const __grid_constant__ GatherArgs a) {
+  __shared__ __align__(16) float cf[GATHER_MAX_LAYERS][5][GATHER_CH];   // kk, kb, kg, gamma, beta
+  __shared__ __align__(16) float cm[2][GATHER_CH];                      // mean, rstd
+  CVB_PDL_PROLOGUE();
+  const int cbase = blockIdx.y * GATHER_CH, nch = min(GATHER_CH, a.nc - cbase);
+  const float invM = 1.0f / (float)a.rows;
+  for (int i = threadIdx.x; i < a.nl * GATHER_CH; i += GATHER_THREADS) {
+    const int l = i / GATHER_CH, c = i % GATHER_CH;
+    if (c < nch) {
+      const float ga = a.gamma[l][cbase + c], rs = a.rstd[cbase + c];
+      cf[l][0][c] = ga * rs;
+      cf[l][1][c] = a.dbeta[l][cbase + c] * invM;
+      cf[l][2][c] = a.dgamma[l][cbase + c] * invM;
+      cf[l][3][c] = ga;
+      cf[l][4][c] = a.beta[l][cbase + c];
+    }
+  }
+  for (int c = threadIdx.x; c < nch; c += GATHER_THREADS) { cm[0][c] = a.mean[cbase + c]; cm[1][c] = a.rstd[cbase + c]; }
+  __syncthreads();
+  // G channel groups of 8 x (256 / G) row lanes: every thread busy for 32-channel slices too
+  const int G = nch / 8, g = threadIdx.x % G, rl = threadIdx.x / G, RL = GATHER_THREADS / G;
+  if (rl >= RL) return;
+  const int cg = cbase + g * 8;
+  float mu[8], rs[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) { mu[k] = cm[0][g * 8 + k]; rs[k] = cm[1][g * 8 + k]; }
+  for (int64_t r = (int64_t)blockIdx.x * RL + rl; r < a.rows; r += (int64_t)gridDim.x * RL) {
+    float xh[8], acc[8];
+    {
+      float xv[8];
+      ld8(a.x + r * a.xcs + cg, xv);
+#pragma unroll
+      for (int k = 0; k < 8; k++) xh[k] = __fmul_rn(__fsub_rn(xv[k], mu[k]), rs[k]);
+    }
+    if (a.base) {
+      const float4* b4 = reinterpret_cast<const float4*>(a.base + r * a.bcs + cg);
+      const float4 u = __ldcg(b4), w = __ldcg(b4 + 1);
+      acc[0] = u.x; acc[1] = u.y; acc[2] = u.z; acc[3] = u.w; acc[4] = w.x; acc[5] = w.y; acc[6] = w.z; acc[7] = w.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; k++) acc[k] = 0.f;
+    }
+    for (int l0 = 0; l0 < a.nl; l0 += 8) {   // eight layers' 16-byte dY loads in flight
+      uint4 u[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++)
+        if (l0 + j < a.nl) u[j] = __ldcg(reinterpret_cast<const uint4*>(a.dy[l0 + j] + r * a.dycs[l0 + j] + cg));
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        if (l0 + j >= a.nl) break;
+        const int l = l0 + j;
+        float d[8];
+        unpack8(u[j], d);
+        float kk[8], kb[8], kg[8], ga[8], be[8];
+        lds8(&cf[l][0][g * 8], kk);
+        lds8(&cf[l][1][g * 8], kb);
+        lds8(&cf[l][2][g * 8], kg);
+        lds8(&cf[l][3][g * 8], ga);
+        lds8(&cf[l][4][g * 8], be);
+#pragma unroll
+        for (int k = 0; k < 8; k++) {   // bwd_load + the accumulating pass-2 loop, same roundings
+          if (!(__fadd_rn(__fmul_rn(xh[k], ga[k]), be[k]) > 0.f)) d[k] = 0.f;
+          const float o = __fmul_rn(kk[k], __fsub_rn(__fsub_rn(d[k], kb[k]), __fmul_rn(xh[k], kg[k])));
+          acc[k] = __fadd_rn(acc[k], o);
+        }
+      }
+    }
+    if (a.out_f32) {
+      float4* o4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + r * a.ocs + cg);
+      o4[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      o4[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    } else {
+      st8(reinterpret_cast<bf16*>(a.out) + r * a.ocs + cg, acc);
+    }
+  }
+}
+
+}  // namespace
+
+// DenseNet deferred BN input gradient over channels [0, nc) of a concat range (see
+// bn_gather_dx).  Pointer arrays are host arrays of nl (<= 32) entries, each already offset to
+// the range's first channel; layers are summed in array order.  out may alias base (fp32).
+CVB_API int cvb_bn_gather_dx(const void* x, int xcs, int64_t rows, int nc, const float* mean, const float* rstd,
+                             const float* base, int bcs, int nl, const void* const* dy, const int* dycs,
+                             const float* const* gamma, const float* const* beta, const float* const* dgamma,
+                             const float* const* dbeta, void* out, int ocs, int out_f32, void* stream) {
+  if (nc % 8 || nl < 0 || nl > GATHER_MAX_LAYERS || !out) { cvb_set_error("bn_gather_dx: bad arguments"); return CVB_EINVAL; }
+  GatherArgs a;
+  memset(&a, 0, sizeof(a));
+  a.x = (const bf16*)x; a.xcs = xcs; a.rows = rows; a.nc = nc; a.mean = mean; a.rstd = rstd;
+  a.base = base; a.bcs = bcs; a.nl = nl;
+  for (int l = 0; l < nl; l++) {
+    a.dy[l] = (const bf16*)dy[l]; a.dycs[l] = dycs[l];
+    a.gamma[l] = gamma[l]; a.beta[l] = beta[l]; a.dgamma[l] = dgamma[l]; a.dbeta[l] = dbeta[l];
+  }
+  a.out = out; a.ocs = ocs; a.out_f32 = out_f32;
+  const int chunks = (nc + GATHER_CH - 1) / GATHER_CH;
+  const int rl_per_cta = GATHER_THREADS / ((nc < GATHER_CH ? nc : GATHER_CH) / 8);
+  const int64_t rblocks = (rows + rl_per_cta - 1) / rl_per_cta;
+  int64_t bx = (int64_t)cvb_num_sms() * 8 / chunks;
+  if (bx < 1) bx = 1;
+  if (bx > rblocks) bx = rblocks;
+  cvb_launch(bn_gather_dx, dim3((unsigned)bx, (unsigned)chunks), dim3(GATHER_THREADS), 0, (cudaStream_t)stream, a);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
 
 // Debug: copy the last traced BN launch's per-CTA phase timestamps ([n][8] globaltimer ns).
 CVB_API int cvb_bn_debug_trace(long long* out, int n) {

@@ -78,7 +78,7 @@ LAUNCH_CLASS = {
     **{n: "umma_gemm" for n in ("cvb_conv2d_fwd", "cvb_conv2d_wgrad", "cvb_gemm", "cvb_gemm_ex",
                                 "cvb_conv2d_dgrad_s2")},
     **{n: "bn" for n in ("cvb_bn_stats", "cvb_bn_forward", "cvb_bn_apply", "cvb_bn_backward",
-                         "cvb_bn_backward_fused")},
+                         "cvb_bn_backward_fused", "cvb_bn_gather_dx")},
     **{n: "pool" for n in ("cvb_maxpool_fwd", "cvb_maxpool_fwd_idx", "cvb_maxpool_bwd", "cvb_maxpool_bwd_idx",
                            "cvb_avgpool_fwd", "cvb_avgpool_bwd", "cvb_gap_fwd", "cvb_gap_bwd")},
     **{n: "head" for n in ("cvb_softmax_xent", "cvb_head_train")},
@@ -272,6 +272,26 @@ def bn_backward(dy, dycs, x, xcs, rows, C, mean, rstd, gamma, beta, ws, dgamma, 
                                       _ptr(dz_out), _stream())
     REC.end(tok)
     _lib.check(rc, "bn_backward")
+
+
+def bn_gather_dx(x, xcs, rows, nc, mean, rstd, layers, out, ocs, base=None, bcs=0):
+    """DenseNet deferred BN input gradient over nc channels (csrc/bn_fused.cu bn_gather_dx).
+
+    layers: [(dy, dycs, gamma, beta, dgamma, dbeta)] in summation order, every tensor already
+    sliced to the range's first channel; out bf16 or fp32 (may alias base)."""
+    nl = len(layers)
+    P = ctypes.c_void_p * max(1, nl)
+    I = ctypes.c_int * max(1, nl)
+    dy = P(*[t[0].data_ptr() for t in layers])
+    dycs = I(*[t[1] for t in layers])
+    ga, be, dg, db = (P(*[t[i].data_ptr() for t in layers]) for i in (2, 3, 4, 5))
+    out_f32 = out.dtype == F32
+    nb = rows * nc * (2 + (4 if base is not None else 0) + (4 if out_f32 else 2) + 2 * nl)
+    tok = REC.begin(1, "bn", 0, nb)
+    rc = _lib_bound().cvb_bn_gather_dx(x.data_ptr(), xcs, rows, nc, mean.data_ptr(), rstd.data_ptr(), _ptr(base), bcs,
+                                       nl, dy, dycs, ga, be, dg, db, out.data_ptr(), ocs, int(out_f32), _stream())
+    REC.end(tok)
+    _lib.check(rc, "bn_gather_dx")
 
 
 def maxpool_fwd(x, k, s, p, y, idx=None):

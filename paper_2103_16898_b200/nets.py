@@ -689,6 +689,10 @@ class DenseLayer:
         self.conv1.build(n, h, w, S)
         self.bn2.build(rows, S, dev)
         self.conv2.build(n, h, w, S)
+        # deferred BN1 input gradient (DEFERRED_DX): the statistics pass's raw sums, kept apart
+        # from the parameter gradients (those may be all-reduced in place before the gather)
+        self.cg = torch.zeros(self.cin, dtype=F32, device=dev)
+        self.cb = torch.zeros(self.cin, dtype=F32, device=dev)
         # kept for backward (no recompute): BN1/BN2 outputs and the 1x1 conv output
         self.z1 = torch.empty(n, h, w, self.mid, dtype=BF16, device=dev)
         self.y1 = torch.empty(n, h, w, self.cin, dtype=BF16, device=dev)
@@ -704,19 +708,39 @@ class DenseLayer:
         m, r = self.slice_stats
         K.bn_stats(blk[..., self.cin:], self.bn1.rows, self.growth, cs, self.bn1.scratch.bnws, m, r)
 
-    def backward(self, ps, blk, dblk32, y1, y2, dz2, dy2, dz1, dy1):
+    def gather_terms(self, ps, c0):
+        """This layer's term of the deferred BN1 input gradient for channels from c0 on."""
+        return (self.dy1_slot[..., c0:], self.cin, ps.p[self.bn1.G][c0:], ps.p[self.bn1.B][c0:], self.cg[c0:],
+                self.cb[c0:])
+
+    def backward(self, ps, blk, dblk32, y1, y2, dz2, dy2, dz1, dy1, later=None):
         cs = blk.shape[-1]
         rows = self.bn1.rows
         y1, y2 = self.y1, self.y2
-        # gradient of this layer's output slice is complete (later layers already added)
-        K.cast_rows(dblk32[..., self.cin:], cs, dz2, self.growth, rows, self.growth)
+        if later is None:
+            # gradient of this layer's output slice is complete (later layers already added)
+            K.cast_rows(dblk32[..., self.cin:], cs, dz2, self.growth, rows, self.growth)
+        else:
+            # deferred: the transition's gradient + every later layer's BN1 term, formed once
+            m, r = self.slice_stats
+            K.bn_gather_dx(blk[..., self.cin:], cs, rows, self.growth, m, r, [L.gather_terms(ps, self.cin) for L in later],
+                           dz2, self.growth, base=dblk32[..., self.cin:], bcs=cs)
+            dy1 = self.dy1_slot
         self.conv2.backward(ps, dz2, y2, dx=dy2)
         K.bn_backward(dy2, self.mid, self.z1, self.mid, rows, self.mid, self.bn2.mean, self.bn2.rstd,
                       ps.p[self.bn2.G], ps.p[self.bn2.B], self.bn2.scratch.bnws, ps.g[self.bn2.G], ps.g[self.bn2.B],
                       relu=True, dx=dz1, dxcs=self.mid)
         ps.grad_ready(self.bn2.G, self.bn2.B)
         self.conv1.backward(ps, dz1, y1, dx=dy1)
-        self.bn1.backward(ps, dy1, self.cin, blk, cs, dblk32, cs, accumulate=True)
+        if later is None:
+            self.bn1.backward(ps, dy1, self.cin, blk, cs, dblk32, cs, accumulate=True)
+        else:   # statistics pass only; the input gradient is gathered later
+            b = self.bn1
+            K.bn_backward(dy1, self.cin, blk, cs, b.rows, b.C, b.mean, b.rstd, ps.p[b.G], ps.p[b.B],
+                          b.scratch.bnws, self.cg, self.cb, relu=b.relu)
+            ps.g[b.G].copy_(self.cg)
+            ps.g[b.B].copy_(self.cb)
+            ps.grad_ready(b.G, b.B)
 
 
 class DenseNet121(Net):
@@ -757,6 +781,7 @@ class DenseNet121(Net):
         h, w = (oh + 2 - 3) // 2 + 1, (ow + 2 - 3) // 2 + 1
         self.pool_idx = torch.empty(n, h, w, self.stem.cout, dtype=torch.uint8, device=dev)   # stem max-pool arg-max
         self.geo, self.bufs, self.dbufs = [], [], []
+        self.deferred = not os.environ.get("CVB_DENSE_ACCUM")   # A/B: per-layer fp32 accumulation
         self.bmean, self.brstd, self.ty = [], [], []
         ymax = 0
         for bi, (c0, c1, layers) in enumerate(self.blocks):
@@ -799,6 +824,19 @@ class DenseNet121(Net):
         self.pooled, self.dpooled = e(n, self.final_c), e(n, self.final_c)
         self.head_in, self.head_dx, self.head_relu = self.pooled, self.dpooled, False
         self.dcast = e(ymax)
+        if self.deferred:   # every layer's dY1 stays alive until its block's gradients are gathered
+            need = 0
+            for bi, (c0, c1, layers) in enumerate(self.blocks):
+                gh, gw = self.geo[bi]
+                need = max(need, sum(n * gh * gw * L.cin for L in layers))
+            self.dy1_store = e(need)
+            for bi, (c0, c1, layers) in enumerate(self.blocks):
+                gh, gw = self.geo[bi]
+                off = 0
+                for L in layers:
+                    cnt = n * gh * gw * L.cin
+                    L.dy1_slot = self.dy1_store[off:off + cnt].view(n, gh, gw, L.cin)
+                    off += cnt
 
     def _v(self, buf, *shape):
         return buf[:math.prod(shape)].view(*shape)
@@ -855,11 +893,16 @@ class DenseNet121(Net):
                 dy = self._v(self.dy1, n, h, w, c1)
                 conv.backward(ps, dt, y, dx=dy)
                 bn.backward(ps, dy, c1, blk, c1, dblk, c1, accumulate=False)
-            for L in reversed(layers):
-                rows = n * h * w
+            for li in range(len(layers) - 1, -1, -1):
+                L = layers[li]
+                later = [layers[j] for j in range(len(layers) - 1, li, -1)] if self.deferred else None
                 L.backward(ps, blk, dblk, self._v(self.y1, n, h, w, L.cin), self._v(self.y2, n, h, w, L.mid),
                            self._v(self.dz2, n, h, w, L.growth), self._v(self.dy2, n, h, w, L.mid),
-                           self._v(self.dz1, n, h, w, L.mid), self._v(self.dy1, n, h, w, L.cin))
+                           self._v(self.dz1, n, h, w, L.mid), self._v(self.dy1, n, h, w, L.cin), later=later)
+            if self.deferred:   # the block input's gradient: the transition's term + every layer's
+                K.bn_gather_dx(blk, blk.shape[-1], n * h * w, c0, self.bmean[bi][:c0], self.brstd[bi][:c0],
+                               [layers[j].gather_terms(ps, 0) for j in range(len(layers) - 1, -1, -1)],
+                               dblk, dblk.shape[-1], base=dblk, bcs=dblk.shape[-1])
         # stem: max-pool backward from the first 64 channels of block 1's gradient
         h, w = self.geo[0]
         d0 = self._v(self.dcast, n, h, w, self.stem.cout)

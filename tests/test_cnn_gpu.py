@@ -106,3 +106,25 @@ def test_fused_decrypt_decode_bit_exact_vs_oracle():
     assert torch.equal(got.view(torch.int32), xr.contiguous().view(torch.int32))
     assert torch.equal(lab.long().cpu(), labr)
     assert torch.count_nonzero(tile[..., 3:]) == 0
+
+
+def test_densenet_deferred_bn_gradient_matches_accumulating_form(monkeypatch):
+    """DenseNet's deferred BN input gradient (statistics pass per layer + one gather per channel
+    range, csrc/bn_fused.cu bn_gather_dx) reproduces the per-layer fp32-accumulating form: same
+    terms, same order, same (uncontracted) roundings -> bit-identical gradients."""
+    from paper_2103_16898_b200 import nets
+
+    rec = P.make_records(8, 11, c=1, h=224, w=224, classes=2)
+    x, lab = P.gpu_inputs(rec, P.loader.MEDICAL)
+    grads = []
+    for accum in (False, True):
+        if accum:
+            monkeypatch.setenv("CVB_DENSE_ACCUM", "1")
+        net = nets.make_model("densenet121", seed=3).build(8)
+        assert net.deferred == (not accum)
+        net.fwd_bwd(x, lab)
+        torch.cuda.synchronize()
+        grads.append(net.ps.g32.clone())
+    a, b = grads
+    assert torch.isfinite(a).all()
+    assert torch.equal(a, b), ((a - b).norm() / b.norm()).item()
