@@ -72,6 +72,13 @@ int cvb_bn_gather_dx(const void* x, int xcs, int64_t rows, int nc, const float* 
                      const float* base, int bcs, int nl, const void* const* dy, const int* dycs,
                      const float* const* gamma, const float* const* beta, const float* const* dgamma,
                      const float* const* dbeta, void* out, int ocs, int out_f32, void* stream);
+/* cvb_bn_forward with the batch statistics computed only for channels [st_off, st_off + st_C)
+   (the other channels' mean/rstd are inputs; no running statistics): DenseNet's newest concat
+   slice and the normalisation of the whole prefix in one launch. */
+int cvb_bn_forward_range(const void* x, int64_t rows, int C, int xcs, float* ws, float* mean, float* rstd, float eps,
+                         float* run_mean, float* run_var, float momentum, const float* gamma, const float* beta,
+                         const void* res, int rcs, int relu, void* y, int ycs, int ycoff, int st_off, int st_C,
+                         void* stream);
 int cvb_bn_backward_fused(const void* dy, int dycs, const void* x, int xcs, const void* y, int ycs, int64_t rows,
                           int C, const float* mean, const float* rstd, const float* gamma, const float* beta, int relu,
                           float* ws, float* dgamma, float* dbeta, void* dx, int dxcs, float* dx32, int accum32,

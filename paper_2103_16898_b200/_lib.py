@@ -80,6 +80,8 @@ SIGNATURES = {
                                    _INT, _P, _P]),
     "cvb_bn_forward": (_INT, [_P, _I64, _INT, _INT, _P, _P, _P, _c.c_float, _P, _P, _c.c_float, _P, _P, _P, _INT, _INT,
                               _P, _INT, _INT, _P]),
+    "cvb_bn_forward_range": (_INT, [_P, _I64, _INT, _INT, _P, _P, _P, _c.c_float, _P, _P, _c.c_float, _P, _P, _P,
+                                    _INT, _INT, _P, _INT, _INT, _INT, _INT, _P]),
     "cvb_bn_backward_fused": (_INT, [_P, _INT, _P, _INT, _P, _INT, _I64, _INT, _P, _P, _P, _P, _INT, _P, _P, _P, _P,
                                      _INT, _P, _INT, _P, _P]),
     "cvb_weight_flip_batched": (_INT, [_P, _P, _P, _INT, _I64, _P]),

@@ -129,6 +129,8 @@ struct FwdArgs {
   int four_rows;             // pass 2 without residual: 4 rows in flight (CVB_BN_FWD_TWO_ROWS=1: off)
   long long* trace;          // CVB_BN_TRACE: per-CTA phase timestamps (globaltimer ns), debug only
   int hint;                  // L2 residency hints + reversed pass 2 (see ldv)
+  int st_off, st_C;          // st_C > 0: statistics of channels [st_off, st_off + st_C) only (the
+                             // others' mean/rstd are given); pass 2 normalises all C channels
 };
 
 __global__ void __launch_bounds__(THREADS) bn_fwd_fused(const FwdArgs a) {
@@ -139,46 +141,50 @@ __global__ void __launch_bounds__(THREADS) bn_fwd_fused(const FwdArgs a) {
   const int64_t per = (a.rows + gridDim.x - 1) / gridDim.x;
   const int64_t r0 = (int64_t)blockIdx.x * per, r1 = min(a.rows, r0 + per);
   bn_trace(a.trace, 0);
-  // ---- pass 1: partial statistics ----
+  // ---- pass 1: partial statistics (of the statistics channel range) ----
+  const int C1 = a.st_C ? a.st_C : C, G1 = C1 / 8, RL1 = THREADS / G1;
+  const int g1 = threadIdx.x % G1, rl1 = threadIdx.x / G1;
+  const bf16* x1 = a.x + (a.st_C ? a.st_off : 0);
   const bool hint = a.hint != 0;
   const uint64_t pk = hint ? pol_keep() : 0, pd = hint ? pol_drop() : 0;
   float s[8] = {0}, q[8] = {0};
-  if (rl < RL) {
-    int64_t r = r0 + rl;
-    for (; r + (UNROLL - 1) * RL < r1; r += UNROLL * RL) {
+  if (rl1 < RL1) {
+    int64_t r = r0 + rl1;
+    for (; r + (UNROLL - 1) * RL1 < r1; r += UNROLL * RL1) {
       float v[UNROLL][8];
 #pragma unroll
-      for (int u = 0; u < UNROLL; u++) ld8h(a.x + (r + u * RL) * a.xcs + g * 8, v[u], hint, pk);
+      for (int u = 0; u < UNROLL; u++) ld8h(x1 + (r + u * RL1) * a.xcs + g1 * 8, v[u], hint, pk);
 #pragma unroll
       for (int u = 0; u < UNROLL; u++)
 #pragma unroll
         for (int i = 0; i < 8; i++) { s[i] += v[u][i]; q[i] += v[u][i] * v[u][i]; }
     }
-    for (; r < r1; r += RL) {
+    for (; r < r1; r += RL1) {
       float v[8];
-      ld8h(a.x + r * a.xcs + g * 8, v, hint, pk);
+      ld8h(x1 + r * a.xcs + g1 * 8, v, hint, pk);
 #pragma unroll
       for (int i = 0; i < 8; i++) { s[i] += v[i]; q[i] += v[i] * v[i]; }
     }
   }
   bn_trace(a.trace, 1);
-  block_partials(s, q, G, RL, g, rl, C, a.part, sh);
+  block_partials(s, q, G1, RL1, g1, rl1, C1, a.part, sh);
   bn_trace(a.trace, 2);
   grid_sync(a.bar);
   bn_trace(a.trace, 3);
   // ---- finalisation: warp w of CTA b owns channel b + w * grid ----
   {
     const int c = blockIdx.x + (threadIdx.x >> 5) * gridDim.x;
-    if (c < C) {
+    if (c < C1) {
       double ts, tq;
-      channel_total_warp(a.part, C, c, ts, tq);
+      channel_total_warp(a.part, C1, c, ts, tq);
       if ((threadIdx.x & 31) == 0) {
         const double cnt = (double)a.rows;
         const double m = ts / cnt;
         double var = tq / cnt - m * m;
         if (var < 0) var = 0;
-        a.mean[c] = (float)m;
-        a.rstd[c] = (float)(1.0 / sqrt(var + (double)a.eps));
+        const int co = c + (a.st_C ? a.st_off : 0);
+        a.mean[co] = (float)m;
+        a.rstd[co] = (float)(1.0 / sqrt(var + (double)a.eps));
         if (a.run_mean) {
           const double unb = cnt > 1 ? var * cnt / (cnt - 1) : var;
           a.run_mean[c] = (float)((1.0 - a.momentum) * a.run_mean[c] + a.momentum * m);
@@ -566,9 +572,29 @@ CVB_API int64_t cvb_bn_fused_workspace_floats(int C) {
 // Batch-norm forward in one launch: statistics of x ([rows][C], stride xcs) -> mean/rstd
 // (+ running stats), then y = act(gamma*(x-mean)*rstd + beta [+ res]) written at channel
 // offset ycoff of y (stride ycs).  y == NULL: statistics only.
+CVB_API int cvb_bn_forward_range(const void* x, int64_t rows, int C, int xcs, float* ws, float* mean, float* rstd,
+                                 float eps, float* run_mean, float* run_var, float momentum, const float* gamma,
+                                 const float* beta, const void* res, int rcs, int relu, void* y, int ycs, int ycoff,
+                                 int st_off, int st_C, void* stream);
 CVB_API int cvb_bn_forward(const void* x, int64_t rows, int C, int xcs, float* ws, float* mean, float* rstd, float eps,
                            float* run_mean, float* run_var, float momentum, const float* gamma, const float* beta,
                            const void* res, int rcs, int relu, void* y, int ycs, int ycoff, void* stream) {
+  return cvb_bn_forward_range(x, rows, C, xcs, ws, mean, rstd, eps, run_mean, run_var, momentum, gamma, beta, res, rcs,
+                              relu, y, ycs, ycoff, 0, 0, stream);
+}
+
+// As cvb_bn_forward, but the batch statistics are computed only for channels [st_off,
+// st_off + st_C) (st_C > 0; multiple of 8); mean/rstd of the other channels are inputs.  DenseNet:
+// the statistics of the newest concat slice and the normalisation of the whole prefix in one
+// launch (no running statistics are updated for a partial range).
+CVB_API int cvb_bn_forward_range(const void* x, int64_t rows, int C, int xcs, float* ws, float* mean, float* rstd,
+                                 float eps, float* run_mean, float* run_var, float momentum, const float* gamma,
+                                 const float* beta, const void* res, int rcs, int relu, void* y, int ycs, int ycoff,
+                                 int st_off, int st_C, void* stream) {
+  if (st_C && (st_C % 8 || st_off % 8 || st_off < 0 || st_off + st_C > C || run_mean)) {
+    cvb_set_error("bn_forward_range: bad statistics range");
+    return CVB_EINVAL;
+  }
   if (C % 8 || C > 2048 || C / 8 > THREADS) { cvb_set_error("bn_forward: C must be a multiple of 8, <= 2048"); return CVB_EINVAL; }
   unsigned* bar;
   int grid_b, grid;
@@ -576,7 +602,7 @@ CVB_API int cvb_bn_forward(const void* x, int64_t rows, int C, int xcs, float* w
   if (rc) return rc;
   FwdArgs a{(const bf16*)x, rows, C, xcs, ws, bar, mean, rstd, eps, run_mean, run_var, momentum, gamma, beta,
             (const bf16*)res, rcs, relu, (bf16*)y, ycs, ycoff, getenv("CVB_BN_FWD_TWO_ROWS") ? 0 : 1, trace_buf(),
-            l2hint_knob()};
+            l2hint_knob(), st_off, st_C};
   const int gf = size_grid(grid, rows, C);
   if (C > 16 * gf) { cvb_set_error("bn_forward: more channels than finalising warps"); return CVB_EINVAL; }
   return launch_coop(bn_fwd_fused, a, gf, (cudaStream_t)stream);

@@ -77,7 +77,7 @@ def _stream():
 LAUNCH_CLASS = {
     **{n: "umma_gemm" for n in ("cvb_conv2d_fwd", "cvb_conv2d_wgrad", "cvb_gemm", "cvb_gemm_ex",
                                 "cvb_conv2d_dgrad_s2")},
-    **{n: "bn" for n in ("cvb_bn_stats", "cvb_bn_forward", "cvb_bn_apply", "cvb_bn_backward",
+    **{n: "bn" for n in ("cvb_bn_stats", "cvb_bn_forward", "cvb_bn_forward_range", "cvb_bn_apply", "cvb_bn_backward",
                          "cvb_bn_backward_fused", "cvb_bn_gather_dx")},
     **{n: "pool" for n in ("cvb_maxpool_fwd", "cvb_maxpool_fwd_idx", "cvb_maxpool_bwd", "cvb_maxpool_bwd_idx",
                            "cvb_avgpool_fwd", "cvb_avgpool_bwd", "cvb_gap_fwd", "cvb_gap_bwd")},
@@ -247,6 +247,17 @@ def bn_forward(x, rows, C, xcs, ws, mean, rstd, gamma, beta, y, ycs, ycoff=0, re
                                      _ptr(res), rcs, int(relu), y.data_ptr(), ycs, ycoff, _stream())
     REC.end(tok)
     _lib.check(rc, "bn_forward")
+
+
+def bn_forward_range(x, rows, C, xcs, ws, mean, rstd, gamma, beta, y, ycs, st_off, st_C, ycoff=0, relu=True, eps=1e-5):
+    """Batch norm (+ReLU) of all C channels whose statistics are computed here only for channels
+    [st_off, st_off + st_C) (the others' mean/rstd are given): one launch."""
+    tok = REC.begin(1, "bn", 0, rows * (C * 4 + st_C * 2))
+    rc = _lib_bound().cvb_bn_forward_range(x.data_ptr(), rows, C, xcs, ws.data_ptr(), mean.data_ptr(), rstd.data_ptr(),
+                                           eps, None, None, 0.0, gamma.data_ptr(), beta.data_ptr(), None, 0, int(relu),
+                                           y.data_ptr(), ycs, ycoff, st_off, st_C, _stream())
+    REC.end(tok)
+    _lib.check(rc, "bn_forward_range")
 
 
 def bn_apply(x, rows, C, xcs, mean, rstd, gamma, beta, y, ycs, ycoff=0, relu=True, res=None, rcs=0):

@@ -615,7 +615,13 @@ class BNAct:
         self.mean, self.rstd = mean, rstd
         self.shared = True
 
-    def forward(self, ps, x, xcs, y, ycs, stats=True):
+    def forward(self, ps, x, xcs, y, ycs, stats=True, pending=None):
+        """pending = (off, n): the shared statistics of channels [off, off + n) are not computed
+        yet -- they are computed in the same launch as the normalisation (DenseNet)."""
+        if pending is not None:
+            K.bn_forward_range(x, self.rows, self.C, xcs, self.scratch.bnws, self.mean, self.rstd, ps.p[self.G],
+                               ps.p[self.B], y, ycs, pending[0], pending[1], relu=self.relu)
+            return
         if stats and not getattr(self, "shared", False):
             K.bn_forward(x, self.rows, self.C, xcs, self.scratch.bnws, self.mean, self.rstd, ps.p[self.G],
                          ps.p[self.B], y, ycs, relu=self.relu, run_mean=self.run_mean, run_var=self.run_var)
@@ -698,15 +704,18 @@ class DenseLayer:
         self.y1 = torch.empty(n, h, w, self.cin, dtype=BF16, device=dev)
         self.y2 = torch.empty(n, h, w, self.mid, dtype=BF16, device=dev)
 
-    def forward(self, ps, blk, y1=None, y2=None):
+    def forward(self, ps, blk, y1=None, y2=None, pending=None, defer_stats=False):
+        """pending: the previous layer's slice whose statistics this layer's BN1 computes in the
+        same launch; defer_stats: leave this layer's slice statistics to the next BN over the block."""
         cs = blk.shape[-1]
-        self.bn1.forward(ps, blk, cs, self.y1, self.cin)
+        self.bn1.forward(ps, blk, cs, self.y1, self.cin, pending=pending)
         self.conv1.forward(ps, self.y1, self.z1)
         self.bn2.forward(ps, self.z1, self.mid, self.y2, self.mid)
         self.conv2.forward(ps, self.y2, blk, out_coff=self.cin)
-        # batch statistics of the 32 new channels, shared by every later BN over this block
-        m, r = self.slice_stats
-        K.bn_stats(blk[..., self.cin:], self.bn1.rows, self.growth, cs, self.bn1.scratch.bnws, m, r)
+        if not defer_stats:
+            # batch statistics of the 32 new channels, shared by every later BN over this block
+            m, r = self.slice_stats
+            K.bn_stats(blk[..., self.cin:], self.bn1.rows, self.growth, cs, self.bn1.scratch.bnws, m, r)
 
     def gather_terms(self, ps, c0):
         """This layer's term of the deferred BN1 input gradient for channels from c0 on."""
@@ -782,6 +791,7 @@ class DenseNet121(Net):
         self.pool_idx = torch.empty(n, h, w, self.stem.cout, dtype=torch.uint8, device=dev)   # stem max-pool arg-max
         self.geo, self.bufs, self.dbufs = [], [], []
         self.deferred = not os.environ.get("CVB_DENSE_ACCUM")   # A/B: per-layer fp32 accumulation
+        self.merge_stats = not os.environ.get("CVB_DENSE_SLICE_STATS")   # A/B: separate slice-statistics launch
         self.bmean, self.brstd, self.ty = [], [], []
         ymax = 0
         for bi, (c0, c1, layers) in enumerate(self.blocks):
@@ -852,12 +862,16 @@ class DenseNet121(Net):
         for bi, (c0, c1, layers) in enumerate(self.blocks):
             h, w = self.geo[bi]
             blk = self.bufs[bi]
+            pend = None
             for L in layers:
-                L.forward(ps, blk)
+                # the newest slice's statistics are computed by the next BN over the block, in
+                # the same launch as its normalisation (no separate statistics launch)
+                L.forward(ps, blk, pending=pend, defer_stats=self.merge_stats)
+                pend = (L.cin, L.growth) if self.merge_stats else None
             if bi < len(self.trans):
                 bn, conv = self.trans[bi]
                 y = self.ty[bi]
-                bn.forward(ps, blk, c1, y, c1)
+                bn.forward(ps, blk, c1, y, c1, pending=pend)
                 t = self._v(self.t, n, h, w, c1 // 2)
                 conv.forward(ps, y, t)
                 nxt = self.bufs[bi + 1]
@@ -866,7 +880,7 @@ class DenseNet121(Net):
                            self.bmean[bi + 1][:c1 // 2], self.brstd[bi + 1][:c1 // 2])
         h, w = self.geo[-1]
         c = self.final_c
-        self.norm5.forward(ps, self.bufs[-1], c, self._v(self.y5, n, h, w, c), c)
+        self.norm5.forward(ps, self.bufs[-1], c, self._v(self.y5, n, h, w, c), c, pending=pend)
         K.gap_fwd(self._v(self.y5, n, h, w, c), n, h * w, c, c, self.pooled)
 
     def features_backward(self, x, fused):

@@ -117,14 +117,17 @@ def test_densenet_deferred_bn_gradient_matches_accumulating_form(monkeypatch):
     rec = P.make_records(8, 11, c=1, h=224, w=224, classes=2)
     x, lab = P.gpu_inputs(rec, P.loader.MEDICAL)
     grads = []
-    for accum in (False, True):
-        if accum:
-            monkeypatch.setenv("CVB_DENSE_ACCUM", "1")
+    # default (deferred gradient, slice statistics merged into the next BN's launch), then the
+    # per-layer accumulating backward, then a separate slice-statistics launch as well
+    for env in (None, "CVB_DENSE_ACCUM", "CVB_DENSE_SLICE_STATS"):
+        if env:
+            monkeypatch.setenv(env, "1")
         net = nets.make_model("densenet121", seed=3).build(8)
-        assert net.deferred == (not accum)
+        assert net.deferred == (env is None) and net.merge_stats == (env != "CVB_DENSE_SLICE_STATS")
         net.fwd_bwd(x, lab)
         torch.cuda.synchronize()
         grads.append(net.ps.g32.clone())
-    a, b = grads
+    a = grads[0]
     assert torch.isfinite(a).all()
-    assert torch.equal(a, b), ((a - b).norm() / b.norm()).item()
+    for b in grads[1:]:
+        assert torch.equal(a, b), ((a - b).norm() / b.norm()).item()
