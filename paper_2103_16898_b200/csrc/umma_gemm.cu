@@ -83,6 +83,8 @@ struct GemmParams {
   uint32_t a_stage_bytes;   // smem bytes of the A part of one pipeline stage
   uint32_t b_stage_bytes;   // smem bytes of the B part of one stage (0: BN * kr * 2)
   int w_halo;               // WGRAD halo: one (bw+KW-1)-wide box per K-block carries every kw tap
+  int w_groups;             // WGRAD halo over cin = 64 * w_groups: N tile t = (kh t / G, channel group t % G)
+  int w_cin;                // ... its input channels (output column = kh*KW*cin + kw*cin + g*64 + ci)
   int w_pair;               // WGRAD halo, Cout = 64: an N tile holds TWO kh rows (M rows 0-63: kh 2t+1, 64-127: kh 2t)
   int w_kh;                 // kernel height (w_pair: which M halves are real)
   int b_res;                // 1: the whole B operand (one N tile, all K) is loaded once per CTA
@@ -987,7 +989,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
-            const int c0 = p.col_off + colbase + c;
+            int c0 = p.col_off + colbase + c;
+            if (p.w_groups > 1) {   // tile (kh, g): 64-column kw segments of the [kh][kw][cin] row
+              const int khh = nt / p.w_groups, gg = nt - khh * p.w_groups;
+              c0 = (khh * p.h_kw + (c >> 6)) * p.w_cin + gg * 64 + (c & 63);
+            }
             if (p.accum) tma_red_add_4d(&p.mapC, buf, c0, c1, c2, c3);
             else tma_store_4d(&p.mapC, buf, c0, c1, c2, c3);
             bulk_commit();
@@ -1295,6 +1301,7 @@ int launch(GemmParams& p, cudaStream_t stream) {
     p.stg_warp = 0;
   }
   if (p.out_par && !p.st_tma) { cvb_set_error("parity output needs the TMA-store epilogue"); return CVB_EINVAL; }
+  if (p.w_groups > 1 && !p.st_tma) { cvb_set_error("grouped halo wgrad needs the TMA-store epilogue"); return CVB_EINVAL; }
   const uint32_t stg = p.st_tma ? stg_bytes : 0u;
   p.stages = (int)(((two ? half - 1280u : 224u * 1024u) - p.b_res_bytes - stg) / stage_bytes);
   if (p.stages > 8) p.stages = 8;
@@ -1781,13 +1788,22 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
   // WGRAD halo: stride 1, one 64-channel group (one 128-byte SW128 row per pixel; the 32-channel
   // SW64 variant computes correctly but measured 2x slower), one image
   // row box whose width is a multiple of 16 pixels, whole kw rows per N tile (N = KW*cin <= 256).
-  if (!no_whalo && stride == 1 && cin == 64 && bcel == cin && bnn == 1 && bw % 16 == 0 &&
-      kw * cin <= 256 && oh == h && ow == w) {
+  // cin = 64 * G (G > 1): N tile (kh, channel group g) = KW x 64 columns, one box of group g
+  static int no_whalo_g = -1;
+  if (no_whalo_g < 0) no_whalo_g = getenv("CVB_NO_WGRAD_HALO_GROUPS") ? 1 : 0;
+  // (only for narrow Cout: with Cout = 128 the dY operand is re-read per (kh, g) tile and the
+  // gathered plan measured faster -- stage-2 ResNet wgrad 57.5 vs 63.2 us)
+  const int wg = cin % 64 == 0 ? cin / 64 : 0;
+  if (!no_whalo && stride == 1 && wg >= 1 && (wg == 1 || (!no_whalo_g && cout <= 64)) && bcel == 64 && bnn == 1 &&
+      bw % 16 == 0 &&
+      kw * 64 <= 256 && oh == h && ow == w) {
     p.w_halo = 1;
+    p.w_groups = wg;
+    p.w_cin = cin;
     p.h_kw = kw;
-    p.BN = kw * cin;
+    p.BN = kw * 64;
     p.gb = 1;
-    p.n_tiles = kh;
+    p.n_tiles = kh * wg;
     const int hw_ = bw + kw - 1;
     p.b_stage_bytes = ((uint32_t)hw_ * bh * bcel * 2 + 1023) / 1024 * 1024;
     p.tx_bytes = p.ga * p.kr * acel * 2 + (uint32_t)hw_ * bh * bcel * 2;
@@ -1806,7 +1822,7 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
     // ONE dY box of bh+1 rows (starting a row early) carries both as the two M atoms.
     static int one_box = -1;   // default: one (bh+1)-row box (measured 47.0 vs 48.6 us, stage-1 ResNet wgrad)
     if (one_box < 0) one_box = getenv("CVB_WGRAD_PAIR_TWOBOX") ? 0 : 1;
-    if (!no_pair && cout == 64 && kh >= 2) {
+    if (!no_pair && cout == 64 && kh >= 2 && wg == 1) {
       p.w_pair = one_box ? 1 : 2;
       p.w_kh = kh;
       p.n_tiles = (kh + 1) / 2;
@@ -1832,8 +1848,9 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
       p.splits = splits;
     }
     p.nbox = p.n_tiles;
-    for (int t = 0; t < p.n_tiles; t++)   // row kh = t (paired: kh = 2t and 2t+1), all kw
-      p.boxtab[t] = pack_box(0, 0, -pad, (p.w_pair ? 2 * t : t) - pad);
+    if (p.nbox > MAX_BOXES) { cvb_set_error("conv2d_wgrad: too many halo tiles"); return CVB_EINVAL; }
+    for (int t = 0; t < p.n_tiles; t++)   // row kh = t (paired: kh = 2t and 2t+1; groups: t / G), all kw
+      p.boxtab[t] = p.w_pair ? pack_box(0, 0, -pad, 2 * t - pad) : pack_box(0, (t % wg) * 64, -pad, t / wg - pad);
     if ((rc = encode_nhwc(&p.mapB[0], x, n, h, w, cin, xcs, bcel, hw_, bh, bnn))) return rc;
     p.out_mode = OUT_PARTIAL; p.out_f32 = 1; p.out = part; p.ldc = Ncols; p.col_off = 0; p.part_rows = cout;
     *splits_out = splits;

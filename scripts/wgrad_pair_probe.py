@@ -12,8 +12,9 @@ from paper_2103_16898_b200 import kernels as K  # noqa: E402
 SHAPES = [  # n, h, w, cin, cout, k, s, p
     (512, 16, 16, 128, 128, 3, 1, 1), (512, 8, 8, 256, 256, 3, 1, 1), (512, 16, 16, 128, 256, 3, 2, 1),
     (512, 4, 4, 512, 512, 3, 1, 1), (512, 8, 8, 256, 512, 3, 2, 1), (512, 16, 16, 128, 256, 1, 2, 0),
+    (128, 56, 56, 128, 32, 3, 1, 1), (128, 28, 28, 128, 32, 3, 1, 1),   # DenseNet conv2
 ]
-tag = f"wgrad pair={os.environ.get('CVB_GEMM_PAIR_WGRAD', '1')}"
+tag = f"wgrad pair={os.environ.get('CVB_GEMM_PAIR_WGRAD', '1')} grp={0 if os.environ.get('CVB_NO_WGRAD_HALO_GROUPS') else 1}"
 for (n, h, w, cin, cout, k, s, p) in SHAPES:
     oh, ow = K.conv_out_hw(h, w, k, s, p)
     x = torch.randn(n, h, w, cin, device="cuda").to(torch.bfloat16)

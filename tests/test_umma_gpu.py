@@ -46,6 +46,10 @@ CONV_CASES = [
     (16, 4, 4, 512, 512, 3, 1, 1),
     (8, 16, 16, 64, 128, 3, 2, 1),
     (5, 8, 8, 128, 128, 3, 1, 1),
+    # halo weight gradients over several 64-channel groups (N tile = (kh, group)): DenseNet's
+    # 128 -> 32 conv2, a 192-channel input with Cout 64 (no kh pairing)
+    (2, 28, 28, 128, 32, 3, 1, 1),
+    (2, 16, 16, 192, 64, 3, 1, 1),
 ]
 
 
