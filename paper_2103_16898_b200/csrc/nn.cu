@@ -661,18 +661,31 @@ __global__ void weight_flip(const bf16* __restrict__ w, int cout, int kh, int kw
 // desc[l] = {src offset, dst offset, cout, kh, kw, cin} into the flat bf16 weight / flipped
 // buffers; blockIdx.y = layer.
 __global__ void weight_flip_batched(const bf16* __restrict__ pb, bf16* __restrict__ fb, const int64_t* __restrict__ desc) {
+  // 32 x 32 (cout x cin) tiles of one tap through shared memory: coalesced 64-byte rows in and
+  // out (the element-wise form with 64-bit index divisions ran at 0.9 TB/s); the flipped tap
+  // of source tap t is taps-1-t (both spatial axes reversed)
+  __shared__ bf16 tile[32][34];
   CVB_PDL_PROLOGUE();
   const int64_t* d = desc + 6 * blockIdx.y;
   const int64_t src = d[0], dst = d[1];
   const int cout = (int)d[2], kh = (int)d[3], kw = (int)d[4], cin = (int)d[5];
-  const int64_t total = (int64_t)cout * kh * kw * cin;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int co = (int)(i % cout);
-    int64_t r = i / cout;
-    const int x = (int)(r % kw); r /= kw;
-    const int y = (int)(r % kh);
-    const int ci = (int)(r / kh);
-    fb[dst + i] = pb[src + (((int64_t)co * kh + (kh - 1 - y)) * kw + (kw - 1 - x)) * cin + ci];
+  const int taps = kh * kw, tco = (cout + 31) / 32, tci = (cin + 31) / 32, per_tap = tco * tci;
+  const int ntiles = taps * per_tap;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 256 threads: 32 x 8
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int tap = t / per_tap, rem = t - tap * per_tap, co0 = (rem / tci) * 32, ci0 = (rem % tci) * 32;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int co = co0 + ty + 8 * k, ci = ci0 + tx;
+      if (co < cout && ci < cin) tile[ty + 8 * k][tx] = pb[src + ((int64_t)co * taps + tap) * cin + ci];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int ci = ci0 + ty + 8 * k, co = co0 + tx;
+      if (co < cout && ci < cin) fb[dst + ((int64_t)ci * taps + (taps - 1 - tap)) * cout + co] = tile[tx][ty + 8 * k];
+    }
+    __syncthreads();
   }
 }
 
@@ -1100,8 +1113,9 @@ CVB_API int cvb_weight_flip(const void* w, int cout, int kh, int kw, int cin, vo
 CVB_API int cvb_weight_flip_batched(const void* pb, void* fb, const int64_t* desc_dev, int nlayers, int64_t max_elems,
                                     void* stream) {
   if (nlayers <= 0) return CVB_OK;
-  unsigned gx = (unsigned)((max_elems + 255) / 256);
+  unsigned gx = (unsigned)((max_elems + 1023) / 1024);   // one 32 x 32 tile per CTA iteration
   if (gx > 512) gx = 512;
+  if (gx < 1) gx = 1;
   cvb_launch(weight_flip_batched, dim3(gx, nlayers), 256, 0, STREAM, (const bf16*)pb, (bf16*)fb, desc_dev);
   CVB_CHECK_LAUNCH();
   return CVB_OK;

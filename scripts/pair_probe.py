@@ -11,6 +11,7 @@ import torch  # noqa: E402
 from paper_2103_16898_b200 import kernels as K  # noqa: E402
 
 SHAPES = [  # n, h, w, cin, cout, k, s, p
+    (512, 32, 32, 64, 128, 1, 2, 0), (512, 16, 16, 128, 256, 1, 2, 0), (512, 8, 8, 256, 512, 1, 2, 0),   # downsample
     (512, 32, 32, 8, 64, 3, 1, 1), (512, 32, 32, 64, 64, 3, 1, 1),                                   # ResNet-18 stem, stage 1 (halo)
     (512, 32, 32, 8, 32, 3, 1, 1), (512, 32, 32, 32, 32, 3, 1, 1), (512, 16, 16, 32, 64, 3, 1, 1),   # small CNN (halo)
     (512, 16, 16, 64, 64, 3, 1, 1),
