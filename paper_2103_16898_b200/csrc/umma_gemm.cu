@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       if (p.mode == MODE_WGRAD) {
         ga_eff = min(p.ga, (p.M - m0 + p.a_cel - 1) / p.a_cel);
         tx = p.tx_bytes - (uint32_t)(p.ga - ga_eff) * p.a_box_bytes;
-        if (p.w_pair) { ga_eff = p.w_pair == 1 ? 1 : 2; tx = p.tx_bytes; }   // kh-paired dY boxes
+        if (p.w_pair) { ga_eff = p.w_pair == 2 ? 2 : 1; tx = p.tx_bytes; }   // kh-paired / kh-quad dY boxes
       }
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
         mbar_wait_lazy(&empty[s], ph ^ 1, (p.dbg & 256) != 0);
@@ -714,7 +714,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
               } else {
                 for (int b = 0; b < ga_eff; b++)
                   tma_load_4d(&p.mapA[0], sa + b * p.a_box_stride, &full[s], m0 + b * p.a_cel, pw,
-                              p.w_pair ? ph0 - 1 : ph0, pn);
+                              p.w_pair == 3 ? ph0 - (p.w_kh - 1) : p.w_pair ? ph0 - 1 : ph0, pn);
               }
               const uint32_t* tab = p.boxtab + nt * p.gb;
               for (int j = 0; j < p.gb; j++) {
@@ -952,14 +952,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           c1 = mt * BM + quarter * 32;
           c2 = p.out_mode == OUT_PARTIAL ? sp : 0;
         }
-        // kh-paired wgrad: lane quarters 0-1 hold kh 2nt+1, quarters 2-3 kh 2nt, both for Cout 0..63
-        const int pair_kh = 2 * nt + (quarter < 2 ? 1 : 0);
+        // kh-paired wgrad: lane quarters 0-1 hold kh 2nt+1, quarters 2-3 kh 2nt, both for Cout 0..63;
+        // kh-quad (Cout 32): lane quarter q holds kh = KH-1-q (q = KH.. unused), channel group nt
+        const int pair_kh = p.w_pair == 3 ? p.w_kh - 1 - quarter : 2 * nt + (quarter < 2 ? 1 : 0);
         const int colbase = p.w_pair ? pair_kh * p.BN : nt * p.BN;
-        if (p.w_pair) c1 = (quarter & 1) * 32;
+        if (p.w_pair) c1 = p.w_pair == 3 ? 0 : (quarter & 1) * 32;
         const uint32_t stg = smem0 + p.stg_off + (uint32_t)(warp - 2) * p.stg_warp;
         const int span = p.n_epi == 8 && !p.epi_alt ? p.BN >> 1 : p.BN;   // columns this warp stores
         const int cbeg = p.n_epi == 8 && !p.epi_alt && warp >= 6 ? span : 0;
-        const bool rows_real = p.w_pair ? pair_kh < p.w_kh : quarter * 32 < p.st_rows;
+        const bool rows_real = p.w_pair ? (pair_kh >= 0 && pair_kh < p.w_kh) : quarter * 32 < p.st_rows;
         const int cend = rows_real ? cbeg + span : cbeg;   // short tile: nothing to store
         const bool one_chunk = span <= p.st_ch;
         bool released = false;
@@ -990,7 +991,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           __syncwarp();
           if (lane == 0) {
             int c0 = p.col_off + colbase + c;
-            if (p.w_groups > 1) {   // tile (kh, g): 64-column kw segments of the [kh][kw][cin] row
+            if (p.w_pair == 3) {    // kh-quad: tile = channel group nt, kh from the lane quarter
+              c0 = (pair_kh * p.h_kw + (c >> 6)) * p.w_cin + nt * 64 + (c & 63);
+            } else if (p.w_groups > 1) {   // tile (kh, g): 64-column kw segments of the [kh][kw][cin] row
               const int khh = nt / p.w_groups, gg = nt - khh * p.w_groups;
               c0 = (khh * p.h_kw + (c >> 6)) * p.w_cin + gg * 64 + (c & 63);
             }
@@ -1301,7 +1304,7 @@ int launch(GemmParams& p, cudaStream_t stream) {
     p.stg_warp = 0;
   }
   if (p.out_par && !p.st_tma) { cvb_set_error("parity output needs the TMA-store epilogue"); return CVB_EINVAL; }
-  if (p.w_groups > 1 && !p.st_tma) { cvb_set_error("grouped halo wgrad needs the TMA-store epilogue"); return CVB_EINVAL; }
+  if ((p.w_groups > 1 || p.w_pair == 3) && !p.st_tma) { cvb_set_error("grouped halo wgrad needs the TMA-store epilogue"); return CVB_EINVAL; }
   const uint32_t stg = p.st_tma ? stg_bytes : 0u;
   p.stages = (int)(((two ? half - 1280u : 224u * 1024u) - p.b_res_bytes - stg) / stage_bytes);
   if (p.stages > 8) p.stages = 8;
@@ -1362,6 +1365,8 @@ int launch(GemmParams& p, cudaStream_t stream) {
       // kh pairs: A = one (bh+1)-row dY box; M atom 0 (kh 2t+1) starts at box row 0, atom 1
       // (kh 2t) one dY row later: LBO = one box row of pixels
       if (p.w_pair == 1) p.adesc[k] = desc_tmpl((uint32_t)(16 * k) * 128u, (uint32_t)p.tw * 128u, 8u * 128u, 2u);
+      // kh-quad: 32-channel (64-byte, SW64) dY rows; M atom q = the box one pixel row further down
+      if (p.w_pair == 3) p.adesc[k] = desc_tmpl((uint32_t)(16 * k) * 64u, (uint32_t)p.tw * 64u, 8u * 64u, 4u);
     }
   }
   if (p.mode == MODE_HALO && p.h_rows && p.h_kwbox)   // kw boxes: plain SW128 K-major, 8-row groups 1 KB apart
@@ -1822,7 +1827,29 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
     // ONE dY box of bh+1 rows (starting a row early) carries both as the two M atoms.
     static int one_box = -1;   // default: one (bh+1)-row box (measured 47.0 vs 48.6 us, stage-1 ResNet wgrad)
     if (one_box < 0) one_box = getenv("CVB_WGRAD_PAIR_TWOBOX") ? 0 : 1;
-    if (!no_pair && cout == 64 && kh >= 2 && wg == 1) {
+    // Cout = 32: a quarter of the MMA rows -- pack up to four kh rows as the M atoms of ONE
+    // (bh + KH - 1)-row dY box (atom q = kh KH-1-q, one box row = one pixel row further down);
+    // an N tile is then one 64-channel input group with every kh and kw (CVB_NO_WGRAD_QUAD=1: off)
+    static int no_quad = -1;
+    if (no_quad < 0) no_quad = getenv("CVB_NO_WGRAD_QUAD") ? 1 : 0;
+    if (!no_quad && cout == 32 && acel == 32 && kh >= 2 && kh <= 4 && (bw * 64) % 1024 == 0 && p.w_groups >= 1) {
+      p.w_pair = 3;
+      p.w_kh = kh;
+      p.n_tiles = wg;
+      p.ptiles_h = (oh + kh - 1 + bh - 1) / bh;   // the pixel range runs KH-1 rows past the image
+      p.num_kb = p.ptiles_w * p.ptiles_h * ((n + bnn - 1) / bnn);
+      p.a_stage_bytes = ((uint32_t)bw * (bh + kh - 1) * 64u + 1023u) / 1024u * 1024u;
+      p.tx_bytes = (uint32_t)bw * (bh + kh - 1) * 64u + (uint32_t)hw_ * bh * bcel * 2;
+      if ((rc = encode_nhwc(&p.mapA[0], dy, n, oh, ow, cout, dycs, acel, bw, bh + kh - 1, bnn))) return rc;
+      tiles = p.m_tiles * p.n_tiles;
+      splits = (g_num_sms + tiles - 1) / tiles;
+      if (splits > max_splits) splits = max_splits;
+      if (splits > p.num_kb) splits = p.num_kb;
+      if (splits < 1) splits = 1;
+      p.kb_per_split = (p.num_kb + splits - 1) / splits;
+      splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
+      p.splits = splits;
+    } else if (!no_pair && cout == 64 && kh >= 2 && wg == 1) {
       p.w_pair = one_box ? 1 : 2;
       p.w_kh = kh;
       p.n_tiles = (kh + 1) / 2;
@@ -1850,7 +1877,8 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
     p.nbox = p.n_tiles;
     if (p.nbox > MAX_BOXES) { cvb_set_error("conv2d_wgrad: too many halo tiles"); return CVB_EINVAL; }
     for (int t = 0; t < p.n_tiles; t++)   // row kh = t (paired: kh = 2t and 2t+1; groups: t / G), all kw
-      p.boxtab[t] = p.w_pair ? pack_box(0, 0, -pad, 2 * t - pad) : pack_box(0, (t % wg) * 64, -pad, t / wg - pad);
+      p.boxtab[t] = p.w_pair == 3 ? pack_box(0, t * 64, -pad, -pad)
+                  : p.w_pair ? pack_box(0, 0, -pad, 2 * t - pad) : pack_box(0, (t % wg) * 64, -pad, t / wg - pad);
     if ((rc = encode_nhwc(&p.mapB[0], x, n, h, w, cin, xcs, bcel, hw_, bh, bnn))) return rc;
     p.out_mode = OUT_PARTIAL; p.out_f32 = 1; p.out = part; p.ldc = Ncols; p.col_off = 0; p.part_rows = cout;
     *splits_out = splits;

@@ -23,6 +23,9 @@ elif which in ("conv128", "conv256"):
     x = torch.randn(512, hw, hw, c, device="cuda").bfloat16(); w = torch.randn(c, 3, 3, c, device="cuda").bfloat16()
     y = torch.empty(512, hw, hw, c, device="cuda", dtype=torch.bfloat16)
     f = lambda: K.conv2d_fwd(x, w, 1, 1, out=y)
+elif which == "dwg":   # DenseNet conv2 weight gradient (128 -> 32, 56x56, batch 128)
+    x = torch.randn(128, 56, 56, 128, device="cuda").bfloat16(); dy = torch.randn(128, 56, 56, 32, device="cuda").bfloat16()
+    f = lambda: K.conv2d_wgrad_partials(dy, x, 3, 3, 1, 1)
 elif which in ("ds64", "ds256"):   # 1x1 stride-2 downsample convs of ResNet-18
     c, hw = (64, 32) if which == "ds64" else (256, 8)
     x = torch.randn(512, hw, hw, c, device="cuda").bfloat16(); w = torch.randn(2 * c, 1, 1, c, device="cuda").bfloat16()

@@ -50,6 +50,7 @@ CONV_CASES = [
     # 128 -> 32 conv2, a 192-channel input with Cout 64 (no kh pairing)
     (2, 28, 28, 128, 32, 3, 1, 1),
     (2, 16, 16, 192, 64, 3, 1, 1),
+    (3, 32, 32, 64, 32, 3, 1, 1),      # kh-quad packing with one input group
 ]
 
 
