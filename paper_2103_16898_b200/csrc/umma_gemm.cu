@@ -965,6 +965,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
         const bool one_chunk = span <= p.st_ch;
         bool released = false;
         for (int c = cbeg; c < cend; c += p.st_ch, ++stg_it) {
+          if (p.w_halo && (c & 63) >= p.w_cin) { --stg_it; continue; }   // zero-fill channels: nothing to store
           const uint32_t buf = stg + (stg_it & 1) * (p.stg_warp >> 1);
           // TMEM first: a single-chunk tile hands its accumulator back to the MMA warp before
           // waiting for the staging buffer
@@ -991,10 +992,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           __syncwarp();
           if (lane == 0) {
             int c0 = p.col_off + colbase + c;
-            if (p.w_pair == 3) {    // kh-quad: tile = channel group nt, kh from the lane quarter
-              c0 = (pair_kh * p.h_kw + (c >> 6)) * p.w_cin + nt * 64 + (c & 63);
-            } else if (p.w_groups > 1) {   // tile (kh, g): 64-column kw segments of the [kh][kw][cin] row
-              const int khh = nt / p.w_groups, gg = nt - khh * p.w_groups;
+            if (p.w_halo) {   // halo wgrad tile: 64-column kw segments of the [kh][kw][cin] output row
+              const int khh = p.w_pair ? pair_kh : nt / p.w_groups;
+              const int gg = p.w_pair == 3 ? nt : p.w_pair ? 0 : nt - (nt / p.w_groups) * p.w_groups;
               c0 = (khh * p.h_kw + (c >> 6)) * p.w_cin + gg * 64 + (c & 63);
             }
             if (p.accum) tma_red_add_4d(&p.mapC, buf, c0, c1, c2, c3);
@@ -1304,7 +1304,7 @@ int launch(GemmParams& p, cudaStream_t stream) {
     p.stg_warp = 0;
   }
   if (p.out_par && !p.st_tma) { cvb_set_error("parity output needs the TMA-store epilogue"); return CVB_EINVAL; }
-  if ((p.w_groups > 1 || p.w_pair == 3) && !p.st_tma) { cvb_set_error("grouped halo wgrad needs the TMA-store epilogue"); return CVB_EINVAL; }
+  if ((p.w_groups > 1 || p.w_pair == 3 || (p.w_halo && p.w_cin < 64)) && !p.st_tma) { cvb_set_error("grouped halo wgrad needs the TMA-store epilogue"); return CVB_EINVAL; }
   const uint32_t stg = p.st_tma ? stg_bytes : 0u;
   p.stages = (int)(((two ? half - 1280u : 224u * 1024u) - p.b_res_bytes - stg) / stage_bytes);
   if (p.stages > 8) p.stages = 8;
@@ -1798,11 +1798,17 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
   if (no_whalo_g < 0) no_whalo_g = getenv("CVB_NO_WGRAD_HALO_GROUPS") ? 1 : 0;
   // (only for narrow Cout: with Cout = 128 the dY operand is re-read per (kh, g) tile and the
   // gathered plan measured faster -- stage-2 ResNet wgrad 57.5 vs 63.2 us)
-  const int wg = cin % 64 == 0 ? cin / 64 : 0;
-  if (!no_whalo && stride == 1 && wg >= 1 && (wg == 1 || (!no_whalo_g && cout <= 64)) && bcel == 64 && bnn == 1 &&
-      bw % 16 == 0 &&
+  // cin = 32: loaded as 64-channel SW128 rows whose upper half is TMA zero fill (the SW64 form
+  // read at half rate); the padded half's output columns are not stored (CVB_NO_WGRAD_ROWPAD)
+  static int no_wpad = -1;
+  if (no_wpad < 0) no_wpad = getenv("CVB_NO_WGRAD_ROWPAD") ? 1 : 0;
+  const bool wpad = cin == 32 && !no_wpad;
+  const int wg = cin % 64 == 0 ? cin / 64 : wpad ? 1 : 0;
+  if (!no_whalo && stride == 1 && wg >= 1 && (wg == 1 || (!no_whalo_g && cout <= 64)) && (bcel == 64 || wpad) &&
+      bnn == 1 && bw % 16 == 0 &&
       kw * 64 <= 256 && oh == h && ow == w) {
     p.w_halo = 1;
+    p.b_cel = 64;   // 64-channel SW128 rows (cin = 32: upper half zero fill)
     p.w_groups = wg;
     p.w_cin = cin;
     p.h_kw = kw;
@@ -1810,8 +1816,8 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
     p.gb = 1;
     p.n_tiles = kh * wg;
     const int hw_ = bw + kw - 1;
-    p.b_stage_bytes = ((uint32_t)hw_ * bh * bcel * 2 + 1023) / 1024 * 1024;
-    p.tx_bytes = p.ga * p.kr * acel * 2 + (uint32_t)hw_ * bh * bcel * 2;
+    p.b_stage_bytes = ((uint32_t)hw_ * bh * 64 * 2 + 1023) / 1024 * 1024;
+    p.tx_bytes = p.ga * p.kr * acel * 2 + (uint32_t)hw_ * bh * 64 * 2;
     tiles = p.m_tiles * p.n_tiles;
     splits = (g_num_sms + tiles - 1) / tiles;
     if (splits > max_splits) splits = max_splits;
@@ -1839,7 +1845,7 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
       p.ptiles_h = (oh + kh - 1 + bh - 1) / bh;   // the pixel range runs KH-1 rows past the image
       p.num_kb = p.ptiles_w * p.ptiles_h * ((n + bnn - 1) / bnn);
       p.a_stage_bytes = ((uint32_t)bw * (bh + kh - 1) * 64u + 1023u) / 1024u * 1024u;
-      p.tx_bytes = (uint32_t)bw * (bh + kh - 1) * 64u + (uint32_t)hw_ * bh * bcel * 2;
+      p.tx_bytes = (uint32_t)bw * (bh + kh - 1) * 64u + (uint32_t)hw_ * bh * 64 * 2;
       if ((rc = encode_nhwc(&p.mapA[0], dy, n, oh, ow, cout, dycs, acel, bw, bh + kh - 1, bnn))) return rc;
       tiles = p.m_tiles * p.n_tiles;
       splits = (g_num_sms + tiles - 1) / tiles;
@@ -1860,10 +1866,10 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
       p.num_kb = p.ptiles_w * p.ptiles_h * ((n + bnn - 1) / bnn);
       if (p.w_pair == 1) {   // one (bh+1)-row box, M atoms one box row apart (LBO = a row of pixels)
         p.a_stage_bytes = ((uint32_t)bw * (bh + 1) * 128u + 1023u) / 1024u * 1024u;
-        p.tx_bytes = (uint32_t)bw * (bh + 1) * 128u + (uint32_t)hw_ * bh * bcel * 2;
+        p.tx_bytes = (uint32_t)bw * (bh + 1) * 128u + (uint32_t)hw_ * bh * 64 * 2;
         if ((rc = encode_nhwc(&p.mapA[0], dy, n, oh, ow, cout, dycs, acel, bw, bh + 1, bnn))) return rc;
       } else {               // two boxes of the same dY channels, one row apart (standard MN atoms)
-        p.tx_bytes = 2u * (uint32_t)bw * bh * 128u + (uint32_t)hw_ * bh * bcel * 2;
+        p.tx_bytes = 2u * (uint32_t)bw * bh * 128u + (uint32_t)hw_ * bh * 64 * 2;
       }
       tiles = p.m_tiles * p.n_tiles;
       splits = (g_num_sms + tiles - 1) / tiles;
@@ -1879,7 +1885,7 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
     for (int t = 0; t < p.n_tiles; t++)   // row kh = t (paired: kh = 2t and 2t+1; groups: t / G), all kw
       p.boxtab[t] = p.w_pair == 3 ? pack_box(0, t * 64, -pad, -pad)
                   : p.w_pair ? pack_box(0, 0, -pad, 2 * t - pad) : pack_box(0, (t % wg) * 64, -pad, t / wg - pad);
-    if ((rc = encode_nhwc(&p.mapB[0], x, n, h, w, cin, xcs, bcel, hw_, bh, bnn))) return rc;
+    if ((rc = encode_nhwc(&p.mapB[0], x, n, h, w, cin, xcs, 64, hw_, bh, bnn))) return rc;
     p.out_mode = OUT_PARTIAL; p.out_f32 = 1; p.out = part; p.ldc = Ncols; p.col_off = 0; p.part_rows = cout;
     *splits_out = splits;
     return launch(p, (cudaStream_t)stream);
