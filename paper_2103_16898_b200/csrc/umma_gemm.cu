@@ -1170,6 +1170,7 @@ int plan_tma_store(GemmParams& p) {
   const int span = p.n_epi == 8 && !p.epi_alt ? p.BN / 2 : p.BN;   // columns per epilogue warp
   int ch = maxch;
   while (ch > 8 && span % ch) ch >>= 1;
+  if (p.mode == MODE_WGRAD && p.w_halo && p.w_cin < ch) ch = p.w_cin;   // padded rows: store the real channels only
   if (span % ch || ch * es < 32) return CVB_OK;
   int bw = 32, bh = 1, bn = 1;
   uint64_t dims[4], st[3];
@@ -1802,7 +1803,9 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
   // read at half rate); the padded half's output columns are not stored (CVB_NO_WGRAD_ROWPAD)
   static int no_wpad = -1;
   if (no_wpad < 0) no_wpad = getenv("CVB_NO_WGRAD_ROWPAD") ? 1 : 0;
-  const bool wpad = cin == 32 && !no_wpad;
+  // (cin = 16 too; not 8: the staging epilogue writes 16-column units, an 8-column store chunk
+  // would overrun its 32-byte staging rows)
+  const bool wpad = (cin == 32 || cin == 16) && !no_wpad;
   const int wg = cin % 64 == 0 ? cin / 64 : wpad ? 1 : 0;
   if (!no_whalo && stride == 1 && wg >= 1 && (wg == 1 || (!no_whalo_g && cout <= 64)) && (bcel == 64 || wpad) &&
       bnn == 1 && bw % 16 == 0 &&

@@ -14,6 +14,7 @@ SHAPES = [  # n, h, w, cin, cout, k, s, p
     (512, 4, 4, 512, 512, 3, 1, 1), (512, 8, 8, 256, 512, 3, 2, 1), (512, 16, 16, 128, 256, 1, 2, 0),
     (128, 56, 56, 128, 32, 3, 1, 1), (128, 28, 28, 128, 32, 3, 1, 1),   # DenseNet conv2
     (512, 32, 32, 32, 32, 3, 1, 1), (512, 16, 16, 32, 64, 3, 1, 1), (512, 16, 16, 64, 64, 3, 1, 1),   # small CNN
+    (512, 32, 32, 8, 32, 3, 1, 1), (512, 32, 32, 8, 64, 3, 1, 1),   # stems (8 = 3 padded channels)
 ]
 tag = f"wgrad pair={os.environ.get('CVB_GEMM_PAIR_WGRAD', '1')} grp={0 if os.environ.get('CVB_NO_WGRAD_HALO_GROUPS') else 1}"
 for (n, h, w, cin, cout, k, s, p) in SHAPES:

@@ -51,6 +51,7 @@ CONV_CASES = [
     (2, 28, 28, 128, 32, 3, 1, 1),
     (2, 16, 16, 192, 64, 3, 1, 1),
     (3, 32, 32, 64, 32, 3, 1, 1),      # kh-quad packing with one input group
+    (2, 16, 16, 16, 32, 3, 1, 1),      # 16-channel input as zero-padded 64-channel rows
 ]
 
 
