@@ -985,9 +985,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           if (lane == 0) bulk_wait_read1();        // the store that last used this buffer has read it
           __syncwarp();
           if (warp == 2 && lane == 0) TRACE(6, lt);
+          if (p.st_ch == 8) {   // 8 fp32 columns (32-byte rows): zero-padded 8-channel halo wgrad
+            const uint32_t off0 = (uint32_t)lane * 32u, off1 = off0 + 16u;
+            st_shared_v4(buf + (off0 ^ (((off0 >> 7) & p.st_swz) << 4)), has_k ? r[0] : 0u, has_k ? r[1] : 0u,
+                         has_k ? r[2] : 0u, has_k ? r[3] : 0u);
+            st_shared_v4(buf + (off1 ^ (((off1 >> 7) & p.st_swz) << 4)), has_k ? r[4] : 0u, has_k ? r[5] : 0u,
+                         has_k ? r[6] : 0u, has_k ? r[7] : 0u);
+          } else {
 #pragma unroll
           for (int cc = 0; cc < 64; cc += 16)
             if (cc < p.st_ch) stage16(p, buf, lane, cc, nt * p.BN + c + cc, r + cc, has_k);
+          }
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
@@ -1803,9 +1811,10 @@ CVB_API int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, in
   // read at half rate); the padded half's output columns are not stored (CVB_NO_WGRAD_ROWPAD)
   static int no_wpad = -1;
   if (no_wpad < 0) no_wpad = getenv("CVB_NO_WGRAD_ROWPAD") ? 1 : 0;
-  // (cin = 16 too; not 8: the staging epilogue writes 16-column units, an 8-column store chunk
-  // would overrun its 32-byte staging rows)
-  const bool wpad = (cin == 32 || cin == 16) && !no_wpad;
+  // (cin = 16 and 8 too: 16 / 8-column store chunks of the real channels only)
+  // (8 channels only with the kh-quad plan, Cout 32: kh-paired at Cout 64 it measured slower,
+  // the ResNet-18 stem wgrad 37.6 -> 46.9 us)
+  const bool wpad = (cin == 32 || cin == 16 || (cin == 8 && cout == 32)) && !no_wpad;
   const int wg = cin % 64 == 0 ? cin / 64 : wpad ? 1 : 0;
   if (!no_whalo && stride == 1 && wg >= 1 && (wg == 1 || (!no_whalo_g && cout <= 64)) && (bcel == 64 || wpad) &&
       bnn == 1 && bw % 16 == 0 &&

@@ -52,6 +52,7 @@ CONV_CASES = [
     (2, 16, 16, 192, 64, 3, 1, 1),
     (3, 32, 32, 64, 32, 3, 1, 1),      # kh-quad packing with one input group
     (2, 16, 16, 16, 32, 3, 1, 1),      # 16-channel input as zero-padded 64-channel rows
+    (3, 16, 16, 8, 32, 3, 1, 1),       # ... and an 8-channel (padded RGB) input, kh-quad
 ]
 
 
