@@ -377,6 +377,7 @@ __global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
     cs.mu[c] = a.mean[c]; cs.rs[c] = a.rstd[c]; cs.ga[c] = a.gamma[c]; cs.be[c] = a.beta[c];
   }
   __syncthreads();
+  bn_trace(a.trace, 0);
   // ---- pass 1: sum(dz), sum(dz * xhat) ----
   const bool hint = a.hint != 0;
   const uint64_t pk = hint ? pol_keep() : 0, pd = hint ? pol_drop() : 0;
@@ -401,8 +402,11 @@ __global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
       if (a.dz_out) st8(a.dz_out + r * C + g * 8, d);
     }
   }
+  bn_trace(a.trace, 1);
   block_partials(s, q, G, RL, g, rl, C, a.part, sh);
+  bn_trace(a.trace, 2);
   grid_sync(a.bar);
+  bn_trace(a.trace, 3);
   {
     const int c = blockIdx.x + (threadIdx.x >> 5) * gridDim.x;   // warp w of CTA b: channel b + w * grid
     if (c < C) {
@@ -411,8 +415,10 @@ __global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
       if ((threadIdx.x & 31) == 0) { a.dbeta[c] = (float)ts; a.dgamma[c] = (float)tq; }
     }
   }
+  bn_trace(a.trace, 4);
   if (!a.dx && !a.dx32) return;
   grid_sync(a.bar);
+  bn_trace(a.trace, 5);
   // ---- pass 2: dx over the same rows; its per-channel factors go to the (now free)
   // partial-reduction smem: sh[0:C) = gamma*rstd, sh[C:2C) = mean(dz), sh[2C:3C) = mean(dz*xhat)
   const float invM = 1.0f / (float)a.rows;
@@ -441,6 +447,7 @@ __global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
       const uint4 ux0 = ldv(a.x + R(r) * a.xcs + g * 8, hint, pd);
       bwd_apply_dz(cs, sh, C, g, uz0, ux0, a.dx + R(r) * a.dxcs + g * 8);
     }
+    bn_trace(a.trace, 6);
     return;
   }
   if (a.two_rows && !a.dx32 && !a.y) {
@@ -477,6 +484,7 @@ __global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
       st8(a.dx + R(r) * a.dxcs + g * 8, o);
     }
   }
+  bn_trace(a.trace, 6);
 #undef R
 }
 

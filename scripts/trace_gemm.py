@@ -23,6 +23,10 @@ elif which in ("conv128", "conv256"):
     x = torch.randn(512, hw, hw, c, device="cuda").bfloat16(); w = torch.randn(c, 3, 3, c, device="cuda").bfloat16()
     y = torch.empty(512, hw, hw, c, device="cuda", dtype=torch.bfloat16)
     f = lambda: K.conv2d_fwd(x, w, 1, 1, out=y)
+elif which == "c1x1":   # DenseNet conv1 dgrad shape: 1x1 conv 128 -> 256 at 56x56, batch 128
+    x = torch.randn(128, 56, 56, 128, device="cuda").bfloat16(); w = torch.randn(256, 1, 1, 128, device="cuda").bfloat16()
+    y = torch.empty(128, 56, 56, 256, device="cuda", dtype=torch.bfloat16)
+    f = lambda: K.conv2d_fwd(x, w, 1, 0, out=y)
 elif which == "dwg":   # DenseNet conv2 weight gradient (128 -> 32, 56x56, batch 128)
     x = torch.randn(128, 56, 56, 128, device="cuda").bfloat16(); dy = torch.randn(128, 56, 56, 32, device="cuda").bfloat16()
     f = lambda: K.conv2d_wgrad_partials(dy, x, 3, 3, 1, 1)
