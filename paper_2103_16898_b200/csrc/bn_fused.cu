@@ -292,8 +292,8 @@ __device__ __forceinline__ void bwd_load(const BwdArgs& a, int64_t r, int g, con
   float mu[8], rs[8];
   lds8(cs.mu + g * 8, mu);
   lds8(cs.rs + g * 8, rs);
-  // explicit roundings (no FMA contraction): DenseNet's deferred gather (bn_gather_dx) repeats
-  // this arithmetic and must reproduce it bit for bit
+  // explicit rounding / FMA steps (no compiler-chosen contraction): DenseNet's deferred gather
+  // (bn_gather_dx) repeats this arithmetic and must reproduce it bit for bit
 #pragma unroll
   for (int k = 0; k < 8; k++) xh[k] = __fmul_rn(__fsub_rn(xv[k], mu[k]), rs[k]);
   if (a.relu) {
@@ -307,7 +307,7 @@ __device__ __forceinline__ void bwd_load(const BwdArgs& a, int64_t r, int g, con
       lds8(cs.ga + g * 8, ga);
       lds8(cs.be + g * 8, be);
 #pragma unroll
-      for (int k = 0; k < 8; k++) if (!(__fadd_rn(__fmul_rn(xh[k], ga[k]), be[k]) > 0.f)) d[k] = 0.f;
+      for (int k = 0; k < 8; k++) if (!(__fmaf_rn(xh[k], ga[k], be[k]) > 0.f)) d[k] = 0.f;
     }
   }
 }
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
     lds8(sh + C + g * 8, kb);
     lds8(sh + 2 * C + g * 8, kg);
 #pragma unroll
-    for (int k = 0; k < 8; k++) o[k] = __fmul_rn(kk[k], __fsub_rn(__fsub_rn(d[k], kb[k]), __fmul_rn(xh[k], kg[k])));
+    for (int k = 0; k < 8; k++) o[k] = __fmul_rn(kk[k], __fmaf_rn(-xh[k], kg[k], __fsub_rn(d[k], kb[k])));
     if (a.dx32) {
       float4* p4 = reinterpret_cast<float4*>(a.dx32 + R(r) * a.dxcs + g * 8);
       if (a.accum32) {
@@ -724,8 +724,8 @@ __global__ void __launch_bounds__(GATHER_THREADS) bn_gather_dx(const __grid_cons
         lds8(&cf[l][4][g * 8], be);
 #pragma unroll
         for (int k = 0; k < 8; k++) {   // bwd_load + the accumulating pass-2 loop, same roundings
-          if (!(__fadd_rn(__fmul_rn(xh[k], ga[k]), be[k]) > 0.f)) d[k] = 0.f;
-          const float o = __fmul_rn(kk[k], __fsub_rn(__fsub_rn(d[k], kb[k]), __fmul_rn(xh[k], kg[k])));
+          if (!(__fmaf_rn(xh[k], ga[k], be[k]) > 0.f)) d[k] = 0.f;
+          const float o = __fmul_rn(kk[k], __fmaf_rn(-xh[k], kg[k], __fsub_rn(d[k], kb[k])));
           acc[k] = __fadd_rn(acc[k], o);
         }
       }
