@@ -124,6 +124,10 @@ struct GemmParams {
   int dbg;                  // profiling knobs: 1 = skip MMA, 2 = skip TMA (results invalid)
   int kb_pair;              // MMA warp issues two 4-MMA K-blocks per batch (FWD / DENSE / WGRAD, ksteps 4)
   int pair;                 // CTA pair (cta_group::2, M = 256): FWD with streamed weights; B split by rank
+  int hs;                   // HALO with streamed weights (wide stride-1 3x3 convs): A = kw-box halo per
+                            // 64-channel group (ring `stages`), B = one tap's weight box (ring `stages_b`)
+  int stages_b;
+  uint32_t b_tap_bytes;     // bytes of one tap's weight box in this CTA
   const void* b_ptr;        // FWD weights [b_rows][b_ld] (host-side: the pair plan re-encodes mapB)
   int64_t b_rows, b_cols, b_ld;
   long long* trace;         // debug: clock64 timeline of CTA 0 (5 x 4096 slots) or null
@@ -536,7 +540,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t a_stage = p.a_stage_bytes;         // 16 KB (halo mode: planes * plane stride)
-  const uint32_t b_stage = p.b_res ? 0u : (p.b_stage_bytes ? p.b_stage_bytes : p.BN * p.kr * 2);
+  const uint32_t b_stage = (p.b_res || p.hs) ? 0u : (p.b_stage_bytes ? p.b_stage_bytes : p.BN * p.kr * 2);
   const uint32_t stage_bytes = a_stage + b_stage;
   const uint32_t b_kb_bytes = p.BN * BK * 2;        // resident B: one K-block slab
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes + p.b_res_bytes +
@@ -546,6 +550,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
   uint64_t* tempty = tfull + 4;             // [nacc <= 4]
   uint64_t* bres_full = tempty + 4;         // [1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
+  uint64_t* full_b = bres_full + 2;           // HS: weight-tap ring [stages_b]
+  uint64_t* empty_b = full_b + 16;            // [stages_b <= 16]
 
   // shfl: lets the compiler prove the role index warp-uniform (keeps the issue loops on the
   // uniform datapath)
@@ -567,6 +573,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       mbar_init(&tempty[i], (p.epi_alt ? 4 : p.n_epi) * (PAIR ? 2 : 1));
     }
     mbar_init(bres_full, 1);
+    for (int i = 0; i < p.stages_b; i++) { mbar_init(&full_b[i], 1); mbar_init(&empty_b[i], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -596,6 +603,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
     int s = 0;
     uint32_t ph = 0;
     int it = 0;
+    int sb_i = 0;        // HS weight-tap ring
+    uint32_t phb = 0;
     if (p.b_res && leader && cl < units) {
       // whole B operand (single N tile): b_slabs slabs of BN x 64, loaded once per CTA (pair:
       // this CTA's BN/2 rows, completing on the leader's barrier)
@@ -635,6 +644,46 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
         pn = (r2 / p.ptiles_h) * p.tn;
       }
       const int m0 = mt * BM, n0 = nt * p.BN;
+      if (p.hs) {   // per channel group: the halo (3 kw boxes), then the 9 taps' weight boxes
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait_lazy(&empty[s], ph ^ 1, false);
+          if (leader) {
+            const uint32_t sa = smem0 + s * stage_bytes;
+            if constexpr (PAIR) {
+              const uint32_t bar_c = mapa_rank0(smem_u32(&full[s]));
+              if (rank == 0) mbar_expect_tx(&full[s], 2u * p.tx_bytes);
+              for (int j = 0; j < p.h_planes; j++)
+                tma_load_4d_pair(&p.mapA[0], sa + j * p.h_plane_stride, bar_c, kb * 64, tw0 - p.h_pad + j,
+                                 th0 - p.h_pad, tn0);
+            } else {
+              mbar_expect_tx(&full[s], p.tx_bytes);
+              for (int j = 0; j < p.h_planes; j++)
+                tma_load_4d(&p.mapA[0], sa + j * p.h_plane_stride, &full[s], kb * 64, tw0 - p.h_pad + j,
+                            th0 - p.h_pad, tn0);
+            }
+          }
+          __syncwarp();
+          if (++s == p.stages) { s = 0; ph ^= 1; }
+          for (int t = 0; t < p.h_kh * p.h_kw; t++) {
+            mbar_wait_lazy(&empty_b[sb_i], phb ^ 1, false);
+            if (leader) {
+              const uint32_t dst = bres + sb_i * p.b_tap_bytes;
+              const int col = t * p.h_cin + kb * 64;
+              if constexpr (PAIR) {
+                const uint32_t bar_c = mapa_rank0(smem_u32(&full_b[sb_i]));
+                if (rank == 0) mbar_expect_tx(&full_b[sb_i], 2u * p.b_tap_bytes);
+                tma_load_2d_pair(&p.mapB[0], dst, bar_c, col, n0 + rank * (p.BN >> 1));
+              } else {
+                mbar_expect_tx(&full_b[sb_i], p.b_tap_bytes);
+                tma_load_2d(&p.mapB[0], dst, &full_b[sb_i], col, n0);
+              }
+            }
+            __syncwarp();
+            if (++sb_i == p.stages_b) { sb_i = 0; phb ^= 1; }
+          }
+        }
+        continue;
+      }
       // WGRAD: A boxes past M (Cout) would be all zero fill -- skip them; their accumulator
       // rows are never stored.
       int ga_eff = p.ga;
@@ -753,6 +802,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
         mbar_wait(&empty[s], ph ^ 1);
         if (++s == p.stages) { s = 0; ph ^= 1; }
       }
+      for (int i = 0; i < p.stages_b; i++) {
+        mbar_wait(&empty_b[sb_i], phb ^ 1);
+        if (++sb_i == p.stages_b) { sb_i = 0; phb ^= 1; }
+      }
     }
   } else if (warp == 1) {
     if (PAIR && rank != 0) {
@@ -762,6 +815,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
     int s = 0;
     uint32_t ph = 0;
     int it = 0, lt = 0;
+    int sbm = 0;         // HS weight-tap ring
+    uint32_t phbm = 0;
     uint64_t adr[8], bdr[8];   // descriptor templates, read once (see issue_ksteps)
 #pragma unroll
     for (int k = 0; k < 8; k++) { adr[k] = p.adesc[k]; bdr[k] = p.bdesc[k]; }
@@ -775,7 +830,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       if ((p.dbg & 32) && !(p.dbg & 64) && leader) TRACE(0, it);   // debug: slot 0 = accumulator wait passed
       tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * p.BN;
-      if (p.kb_pair) {
+      if (p.hs) {
+        // per channel group: wait the halo, then per tap the weight box -> 4 MMAs (64 channels),
+        // the tap's A start = kw box + kh KB (aligned SW128 starts, as in halo_kw_issue)
+        uint32_t acc_flag = 0u;
+        const uint32_t box16 = p.h_plane_stride >> 4;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint64_t a0 = adr[0] + ((smem0 + s * stage_bytes) >> 4);
+          for (int t = 0; t < p.h_kh * p.h_kw; t++) {
+            const int kh = t / 3, kw = t - kh * 3;   // host plans 3x3 only
+            mbar_wait(&full_b[sbm], phbm);
+            tc_fence_after();
+            const uint64_t b0 = bdr[0] + ((bres + sbm * p.b_tap_bytes) >> 4);
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+              umma_t<PAIR>(tmem_d, a0 + (uint32_t)kw * box16 + (uint32_t)(kh * 64 + 2 * j), b0 + 2u * j, idr, acc_flag,
+                           leader);
+              acc_flag = 1u;
+            }
+            if (leader) commit_t<PAIR>(&empty_b[sbm]);
+            __syncwarp();
+            if (++sbm == p.stages_b) { sbm = 0; phbm ^= 1; }
+          }
+          if (leader) commit_t<PAIR>(&empty[s]);
+          __syncwarp();
+          if (++s == p.stages) { s = 0; ph ^= 1; }
+        }
+      } else if (p.kb_pair) {
         // gathered / dense K-blocks are only 4 MMAs each: the MMA warp's fixed cost per issue
         // batch (~450 cycles measured, independent of N) left the tensor pipe idle half the
         // time.  Two stages are waited for and issued as one batch of 8 MMAs.
@@ -1253,7 +1336,8 @@ int launch(GemmParams& p, cudaStream_t stream) {
   static int env_pair_halo = -1;
   if (env_pair_halo < 0) { const char* e = getenv("CVB_GEMM_PAIR_HALO"); env_pair_halo = e ? atoi(e) : 0; }
   const bool pair_fwd = p.mode == MODE_FWD && !p.b_res && p.b_cel == 64 && p.gb == 1 && p.b_major == 0 && p.kr == BK;
-  const bool pair_halo = env_pair_halo && p.mode == MODE_HALO && p.b_res && p.b_cel == 64 && p.gb == 1;
+  const bool pair_halo = (env_pair_halo && p.mode == MODE_HALO && p.b_res && p.b_cel == 64 && p.gb == 1) ||
+                         (p.hs && p.BN % 32 == 0);
   // weight gradients with Cout a multiple of 256: the pair shares the input (B) boxes
   static int env_pair_wg = -1;
   if (env_pair_wg < 0) { const char* e = getenv("CVB_GEMM_PAIR_WGRAD"); env_pair_wg = e ? atoi(e) : 1; }
@@ -1269,14 +1353,16 @@ int launch(GemmParams& p, cudaStream_t stream) {
   if (p.pair && p.mode != MODE_WGRAD) {
     int rc = encode_2d(&p.mapB[0], p.b_ptr, p.b_rows, p.b_cols, p.b_ld, p.b_cel, p.BN / 2);
     if (rc) return rc;
-    if (p.b_res) {
+    if (p.hs) {
+      p.b_tap_bytes /= 2;   // this CTA's half of every tap's weight box
+    } else if (p.b_res) {
       p.b_res_bytes /= 2;   // this CTA's half of every weight slab
     } else {
       p.b_stage_bytes = (uint32_t)(p.BN / 2) * p.kr * 2;
       p.tx_bytes -= (uint32_t)(p.BN / 2) * p.b_cel * 2;   // this CTA's half of the weight box
     }
   }
-  const uint32_t stage_bytes = p.a_stage_bytes + (p.b_res ? 0u : (p.b_stage_bytes ? p.b_stage_bytes
+  const uint32_t stage_bytes = p.a_stage_bytes + ((p.b_res || p.hs) ? 0u : (p.b_stage_bytes ? p.b_stage_bytes
                                                                                    : (uint32_t)p.BN * p.kr * 2));
   static int env_epi4 = -1;
   if (env_epi4 < 0) env_epi4 = getenv("CVB_EPI4") ? 1 : 0;
@@ -1315,8 +1401,15 @@ int launch(GemmParams& p, cudaStream_t stream) {
   if (p.out_par && !p.st_tma) { cvb_set_error("parity output needs the TMA-store epilogue"); return CVB_EINVAL; }
   if ((p.w_groups > 1 || p.w_pair == 3 || (p.w_halo && p.w_cin < 64)) && !p.st_tma) { cvb_set_error("grouped halo wgrad needs the TMA-store epilogue"); return CVB_EINVAL; }
   const uint32_t stg = p.st_tma ? stg_bytes : 0u;
+  if (p.hs) {   // two halo stages; the weight-tap ring takes the rest (<= 16 slots)
+    p.stages_b = (int)((224u * 1024u - 2u * stage_bytes - stg) / p.b_tap_bytes);
+    if (p.stages_b > 16) p.stages_b = 16;
+    if (p.stages_b < 2) { cvb_set_error("halo stream: no room for the weight ring"); return CVB_EINVAL; }
+    p.b_res_bytes = (uint32_t)p.stages_b * p.b_tap_bytes;
+  }
   p.stages = (int)(((two ? half - 1280u : 224u * 1024u) - p.b_res_bytes - stg) / stage_bytes);
   if (p.stages > 8) p.stages = 8;
+  if (p.hs) p.stages = 2;
   p.two_cta = two && p.stages >= 2 ? 1 : 0;
   if (two && !p.two_cta) p.stages = (int)((224u * 1024u - p.b_res_bytes - stg) / stage_bytes);
   static int env_stages = -1, env_dbg = -1;
@@ -1348,7 +1441,7 @@ int launch(GemmParams& p, cudaStream_t stream) {
   }
   if (p.stages < 2) { cvb_set_error("BN too large"); return CVB_EINVAL; }
   p.stg_off = (uint32_t)p.stages * stage_bytes + p.b_res_bytes;   // 1024-aligned (stages, slabs are)
-  size_t smem = (size_t)p.stages * stage_bytes + p.b_res_bytes + stg + 1024 + 256;
+  size_t smem = (size_t)p.stages * stage_bytes + p.b_res_bytes + stg + 1024 + 512;   // barriers: 64 words
   if (cvb_first_on_device(&g_attr_done)) {
     CVB_CUDA(cudaFuncSetAttribute(umma_gemm_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     CVB_CUDA(cudaFuncSetAttribute(umma_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -1560,6 +1653,48 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
       if ((rc = encode_nhwc(&p.mapA[0], x, n, h, w, cin, xcs, p.h_rows ? rowb / 2 : 8, p.h_pitch, hrows, 1))) return rc;
       if ((rc = encode_2d(&p.mapB[0], wt, cout, K, K, p.b_cel, p.BN))) return rc;
       p.b_ptr = wt; p.b_rows = cout; p.b_cols = K; p.b_ld = K;
+      p.out_mode = OUT_NHWC; p.out_f32 = y_f32; p.out = y; p.ldc = ycs; p.col_off = yoff; p.bias = bias;
+      p.accum = accumulate;
+      return launch(p, (cudaStream_t)stream);
+    }
+  }
+  {
+    // ---- halo with streamed weights: wide stride-1 3x3 convs whose weights do not stay
+    // resident (128+ channels).  The gathered plan reads the 128-pixel A box once per TAP from
+    // L2 (9x per channel group) and is bounded by the L2 -> SM rate (~34 B/clk/SM measured,
+    // ResNet-18 stage 2); here the kw-box halo is read once per channel group and only the
+    // weights stream per tap (A + B per tap 24 -> ~14 KB with the CTA pair).
+    static int no_hs = -1;
+    if (no_hs < 0) no_hs = getenv("CVB_NO_HALO_STREAM") ? 1 : 0;
+    const int Kh = kh * kw * cin, BNh = pick_bn(cout);
+    const uint32_t b_all_h = (uint32_t)((Kh + BK - 1) / BK) * BNh * BK * 2;
+    if (!no_hs && stride == 1 && kh == 3 && kw == 3 && pad == 1 && cin % 64 == 0 && cin >= 128 && cout % 32 == 0 &&
+        cout <= 256 && b_all_h > 96u * 1024u && ow % 8 == 0 && oh % 16 == 0 && xcs % 8 == 0) {
+      p.mode = MODE_HALO;
+      p.hs = 1;
+      p.a_major = 0; p.b_major = 0;
+      p.a_cel = 8; p.b_cel = 64;
+      p.gb = 1;
+      p.BN = BNh;
+      p.M = n * oh * ow; p.N = cout;
+      p.tw = 8; p.th = 16; p.tn = 1;
+      p.ptiles_w = ow / 8; p.ptiles_h = oh / 16;
+      p.m_tiles = p.ptiles_w * p.ptiles_h * n;
+      p.n_tiles = 1; p.splits = 1;
+      p.h_cin = cin; p.h_cg = 64; p.h_pad = pad; p.h_kh = kh; p.h_kw = kw;
+      p.h_rows = 1; p.h_kwbox = 1; p.h_planes = kw; p.h_pitch = 8;
+      p.h_box_bytes = 8u * 18u * 128u;
+      p.h_plane_stride = (p.h_box_bytes + 1023) / 1024 * 1024;
+      p.a_stage_bytes = (uint32_t)kw * p.h_plane_stride;
+      p.num_kb = cin / 64; p.kb_per_split = p.num_kb;
+      p.OH = oh; p.OW = ow; p.NIMG = n;
+      p.b_res = 0; p.b_res_bytes = 0;
+      p.tx_bytes = (uint32_t)kw * p.h_box_bytes;
+      p.b_tap_bytes = (uint32_t)BNh * 128u;   // launch(): halved for the CTA pair
+      int rc;
+      if ((rc = encode_nhwc(&p.mapA[0], x, n, h, w, cin, xcs, 64, 8, 18, 1))) return rc;
+      if ((rc = encode_2d(&p.mapB[0], wt, cout, Kh, Kh, 64, BNh))) return rc;
+      p.b_ptr = wt; p.b_rows = cout; p.b_cols = Kh; p.b_ld = Kh;
       p.out_mode = OUT_NHWC; p.out_f32 = y_f32; p.out = y; p.ldc = ycs; p.col_off = yoff; p.bias = bias;
       p.accum = accumulate;
       return launch(p, (cudaStream_t)stream);

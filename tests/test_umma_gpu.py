@@ -53,6 +53,11 @@ CONV_CASES = [
     (3, 32, 32, 64, 32, 3, 1, 1),      # kh-quad packing with one input group
     (2, 16, 16, 16, 32, 3, 1, 1),      # 16-channel input as zero-padded 64-channel rows
     (3, 16, 16, 8, 32, 3, 1, 1),       # ... and an 8-channel (padded RGB) input, kh-quad
+    # halo conv with streamed weights (wide stride-1 3x3): CTA pair, single-CTA (odd tile
+    # count), 256 output channels, 192-channel input
+    (3, 16, 8, 128, 128, 3, 1, 1),
+    (2, 32, 16, 128, 256, 3, 1, 1),
+    (2, 16, 16, 192, 64, 3, 1, 1),
 ]
 
 
