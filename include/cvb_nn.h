@@ -26,8 +26,10 @@ int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs, const v
                    int accumulate, void* stream);
 /* fp32 partial weight gradients part[split][cout][kh*kw*cin]; *splits_out receives the count */
 /* dX of a stride-2 conv by output-parity classes (no zero-upsampled dY): 4 gather convs of dY
-   through parity views of dx; wscratch = cout*kh*kw*cin bf16.  Returns CVB_EINVAL (nothing
-   launched) for unsupported geometry; classes without taps need accumulate=1. */
+   through parity views of dx; wscratch = cout*kh*kw*cin bf16 (the per-class weight matrices,
+   written here from w -- or, with w == NULL, already written, e.g. by cvb_transpose_batched).
+   Returns CVB_EINVAL (nothing launched) for unsupported geometry; classes without taps need
+   accumulate=1. */
 int cvb_conv2d_dgrad_s2(const void* dy, int n, int oh, int ow, int cout, int dycs, const void* w, int cin, int kh,
                         int kw, int pad, void* dx, int h, int wd, int dxcs, int accumulate, void* wscratch,
                         void* stream);
@@ -121,6 +123,12 @@ int cvb_reduce_splits_act(const float* part, int splits, int rows, int cols, con
                           int out_f32, int64_t ldo, void* stream);
 /* all stride-1 dgrad weight flips in one launch: desc_dev = nlayers x {src, dst, cout, kh, kw, cin}
    (int64 element offsets into pb / fb) */
+/* Batched bf16 matrix transposes, one launch: desc_dev = njobs x {src off, dst off, rows, cols,
+   src row stride, dst row stride} (elements); dst[c*dst_ld + r] = src[r*src_ld + c].  Used for
+   the flipped stride-1 dgrad weights (a job per tap) and the stride-2 dgrad parity-class
+   weights (a job per class and tap) after every optimiser step. */
+int cvb_transpose_batched(const void* src, void* dst, const int64_t* desc_dev, int njobs, int64_t max_elems,
+                          void* stream);
 int cvb_weight_flip_batched(const void* pb, void* fb, const int64_t* desc_dev, int nlayers, int64_t max_elems,
                             void* stream);
 /* space-to-depth stem: the 7x7 stride-2 pad-3 conv on x [n][h][w][C] equals a 4x4 stride-1 pad-2

@@ -85,6 +85,7 @@ SIGNATURES = {
     "cvb_bn_backward_fused": (_INT, [_P, _INT, _P, _INT, _P, _INT, _I64, _INT, _P, _P, _P, _P, _INT, _P, _P, _P, _P,
                                      _INT, _P, _INT, _P, _P]),
     "cvb_weight_flip_batched": (_INT, [_P, _P, _P, _INT, _I64, _P]),
+    "cvb_transpose_batched": (_INT, [_P, _P, _P, _INT, _I64, _P]),
     "cvb_space_to_depth2": (_INT, [_P, _INT, _INT, _INT, _INT, _P, _P]),
     "cvb_s2d_weights": (_INT, [_P, _INT, _INT, _P, _P]),
     "cvb_s2d_weights_grad": (_INT, [_P, _INT, _INT, _P, _P]),

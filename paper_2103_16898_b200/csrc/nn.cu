@@ -714,6 +714,36 @@ __global__ void weight_flip_batched(const bf16* __restrict__ pb, bf16* __restric
   }
 }
 
+// Batched transposes of bf16 matrices: job j = {src offset, dst offset, rows, cols, src row
+// stride, dst row stride}: dst[c * dst_ld + r] = src[r * src_ld + c] (elements).  One launch
+// refreshes every derived weight layout of a step after the optimiser: the flipped stride-1
+// dgrad weights (one job per tap) and the per-output-parity class weights of the stride-2
+// dgrads (one job per (class, tap)).  32 x 32 tiles through shared memory, 64-byte rows in/out.
+__global__ void transpose_batched(const bf16* __restrict__ src, bf16* __restrict__ dst, const int64_t* __restrict__ desc) {
+  __shared__ bf16 tile[32][34];
+  CVB_PDL_PROLOGUE();
+  const int64_t* d = desc + 6 * blockIdx.y;
+  const int64_t so = d[0], dof = d[1], sld = d[4], dld = d[5];
+  const int rows = (int)d[2], cols = (int)d[3];
+  const int tr = (rows + 31) / 32, tc = (cols + 31) / 32, ntiles = tr * tc;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int r0 = (t / tc) * 32, c0 = (t % tc) * 32;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int r = r0 + ty + 8 * k, c = c0 + tx;
+      if (r < rows && c < cols) tile[ty + 8 * k][tx] = src[so + (int64_t)r * sld + c];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int c = c0 + ty + 8 * k, r = r0 + tx;
+      if (r < rows && c < cols) dst[dof + (int64_t)c * dld + r] = tile[tx][ty + 8 * k];
+    }
+    __syncthreads();
+  }
+}
+
 // ---- space-to-depth stem (7x7 stride-2 pad-3 conv == 4x4 stride-1 conv on 2x2 s2d input) ----
 // xs[n][i][j][(2a+b)*C + c] = x[n][2i+a][2j+b][c]
 __global__ void space_to_depth2(const bf16* __restrict__ x, int n, int h, int w, int C, bf16* __restrict__ xs) {
@@ -1145,6 +1175,18 @@ CVB_API int cvb_weight_flip_batched(const void* pb, void* fb, const int64_t* des
   if (gx > 512) gx = 512;
   if (gx < 1) gx = 1;
   cvb_launch(weight_flip_batched, dim3(gx, nlayers), 256, 0, STREAM, (const bf16*)pb, (bf16*)fb, desc_dev);
+  CVB_CHECK_LAUNCH();
+  return CVB_OK;
+}
+
+CVB_API int cvb_transpose_batched(const void* src, void* dst, const int64_t* desc_dev, int njobs, int64_t max_elems,
+                                  void* stream) {
+  if (njobs <= 0) return CVB_OK;
+  if (njobs > 65535) { cvb_set_error("transpose_batched: too many jobs"); return CVB_EINVAL; }
+  unsigned gx = (unsigned)((max_elems + 1023) / 1024);
+  if (gx > 256) gx = 256;
+  if (gx < 1) gx = 1;
+  cvb_launch(transpose_batched, dim3(gx, njobs), 256, 0, STREAM, (const bf16*)src, (bf16*)dst, desc_dev);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }

@@ -1867,9 +1867,11 @@ CVB_API int cvb_conv2d_dgrad_s2(const void* dy, int n, int oh, int ow, int cout,
   }
   if (!accumulate && have != 15) { cvb_set_error("dgrad_s2: a parity class has no taps; accumulate into zeroed dx"); return CVB_EINVAL; }
   const int64_t total = cw.off[4];
-  cvb_launch(dgrad_class_weights, (unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream, 
-      (const __nv_bfloat16*)w, cout, kh, kw, cin, cw, (__nv_bfloat16*)wscratch);
-  CVB_CHECK_LAUNCH();
+  if (w) {   // w == NULL: wscratch already holds the class weights (cvb_transpose_batched jobs)
+    cvb_launch(dgrad_class_weights, (unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream,
+        (const __nv_bfloat16*)w, cout, kh, kw, cin, cw, (__nv_bfloat16*)wscratch);
+    CVB_CHECK_LAUNCH();
+  }
   for (int c = 0; c < 4; c++)
     if (have & (1 << c)) {
       int rc = launch(plans[c], (cudaStream_t)stream);

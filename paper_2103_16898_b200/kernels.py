@@ -83,7 +83,8 @@ LAUNCH_CLASS = {
                            "cvb_avgpool_fwd", "cvb_avgpool_bwd", "cvb_gap_fwd", "cvb_gap_bwd")},
     **{n: "head" for n in ("cvb_softmax_xent", "cvb_head_train")},
     **{n: "reduce" for n in ("cvb_reduce_splits", "cvb_reduce_splits_act", "cvb_col_sum")},
-    **{n: "layout" for n in ("cvb_weight_flip", "cvb_weight_flip_batched", "cvb_space_to_depth2", "cvb_s2d_weights",
+    **{n: "layout" for n in ("cvb_weight_flip", "cvb_weight_flip_batched", "cvb_transpose_batched",
+                             "cvb_space_to_depth2", "cvb_s2d_weights",
                              "cvb_s2d_weights_grad", "cvb_zero_upsample", "cvb_cast_rows", "cvb_cast_f32_bf16")},
     **{n: "eltwise" for n in ("cvb_relu_fwd", "cvb_relu_bwd")},
     **{n: "optimizer" for n in ("cvb_adam_step", "cvb_sgd_step")},
@@ -145,20 +146,24 @@ def conv2d_fwd(x, w, stride=1, pad=0, bias=None, out=None, out_f32=False, cin=No
     return out
 
 
-def conv2d_dgrad_s2(dy, w, pad, dx, accumulate=False, wscratch=None, acct_flops=None):
+def conv2d_dgrad_s2(dy, w, pad, dx, accumulate=False, wscratch=None, acct_flops=None, class_weights_ready=False):
     """dX of a stride-2 conv by output-parity classes (csrc/umma_gemm.cu).  Returns False,
-    launching nothing, when the geometry is unsupported (caller uses the upsampled form)."""
+    launching nothing, when the geometry is unsupported (caller uses the upsampled form).
+    class_weights_ready: wscratch already holds the parity-class weight matrices (written by
+    ParamStore.flip_all's batched transposes), so no permutation launch runs here."""
     n, oh, ow, cout = dy.shape
     cout_w, kh, kw, cin = w.shape
     _, h, wd, dcs = dx.shape
     assert cout_w == cout and w.is_contiguous() and dx.dtype == BF16
     if wscratch is None:
+        assert not class_weights_ready
         wscratch = torch.empty(w.numel(), dtype=BF16, device=w.device)
+    w_src = None if class_weights_ready else w
     lib = _lib_bound()
     nbytes = 2 * (dy.numel() + w.numel() + n * h * wd * cin * (2 if accumulate else 1))
     tok = REC.begin(5, "umma_gemm", acct_flops if acct_flops is not None else 2 * n * oh * ow * cout * kh * kw * cin,
                     nbytes)
-    rc = lib.cvb_conv2d_dgrad_s2(dy.data_ptr(), n, oh, ow, cout, dy.stride(2), w.data_ptr(), cin, kh, kw, pad,
+    rc = lib.cvb_conv2d_dgrad_s2(dy.data_ptr(), n, oh, ow, cout, dy.stride(2), _ptr(w_src), cin, kh, kw, pad,
                                  dx.data_ptr(), h, wd, dx.stride(2), int(accumulate), wscratch.data_ptr(), _stream())
     REC.end(tok)
     if rc == -1:
@@ -423,6 +428,27 @@ def weight_flip_batched(pb, fb, desc_dev, nlayers, max_elems, nbytes):
                                               _stream())
     REC.end(tok)
     _lib.check(rc, "weight_flip_batched")
+
+
+def transpose_batched(src, dst, desc_dev, njobs, max_elems, nbytes):
+    """Batched bf16 transposes (csrc/nn.cu transpose_batched): desc rows {src off, dst off, rows,
+    cols, src ld, dst ld}."""
+    tok = REC.begin(1, "layout", 0, nbytes)
+    rc = _lib_bound().cvb_transpose_batched(src.data_ptr(), dst.data_ptr(), desc_dev.data_ptr(), njobs, max_elems,
+                                            _stream())
+    REC.end(tok)
+    _lib.check(rc, "transpose_batched")
+
+
+def dgrad_s2_classes(kh, kw, pad):
+    """Output-parity classes of a stride-2 dgrad: [(class, [(ky, kx) taps])] in the order the
+    C-ABI lays out their weight matrices (csrc/umma_gemm.cu cvb_conv2d_dgrad_s2)."""
+    out = []
+    for c in range(4):
+        ph, pw = c >> 1, c & 1
+        out.append((c, [(y, x) for y in range(kh) for x in range(kw)
+                        if ((y - ph - pad) & 1) == 0 and ((x - pw - pad) & 1) == 0]))
+    return out
 
 
 def space_to_depth2(x, xs):

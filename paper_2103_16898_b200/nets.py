@@ -69,9 +69,15 @@ class ParamStore:
         if name not in getattr(self, "flip_names", []):
             self.flip_names = getattr(self, "flip_names", []) + [name]
 
+    def want_class_weights(self, name, pad):
+        """Keep the stride-2 dgrad's per-output-parity class weight matrices of conv weight `name`
+        (csrc/umma_gemm.cu cvb_conv2d_dgrad_s2 layout), refreshed by the same batched launch."""
+        if name not in dict(getattr(self, "class_names", [])):
+            self.class_names = getattr(self, "class_names", []) + [(name, pad)]
+
     def flip_all(self):
         if self.flip_n:
-            K.weight_flip_batched(self.pb, self.fb, self.flip_desc, self.flip_n, self.flip_max, self.flip_bytes)
+            K.transpose_batched(self.pb, self.fb, self.flip_desc, self.flip_n, self.flip_max, self.flip_bytes)
 
     def finalize(self, device):
         offs, off = {}, 0
@@ -98,19 +104,36 @@ class ParamStore:
         K.cast_f32_bf16(self.p32, self.pb)
         # flipped dgrad weights: one flat bf16 buffer, one launch for all layers
         shapes = {name: shape for name, shape, _ in self.specs}
+        # batched transpose jobs {src, dst, rows, cols, src ld, dst ld}: flipped stride-1 dgrad
+        # weights [cin][kh][kw][cout] (one job per tap, tap t -> taps-1-t) and stride-2 parity-class
+        # weights [ci][t][co] per class (one job per class tap)
         names = getattr(self, "flip_names", [])
-        desc, self.f, foff, self.flip_max = [], {}, 0, 1
+        desc, self.f, self.cw, foff, self.flip_max = [], {}, {}, 0, 1
         for name in names:
             cout, kh, kw, cin = shapes[name]
-            n = cout * kh * kw * cin
-            desc += [offs[name], foff, cout, kh, kw, cin]
+            n, taps = cout * kh * kw * cin, kh * kw
+            for t in range(taps):
+                desc += [offs[name] + t * cin, foff + (taps - 1 - t) * cout, cout, cin, taps * cin, taps * cout]
             self.f[name] = (foff, (cin, kh, kw, cout))
             foff += (n + ALIGN - 1) // ALIGN * ALIGN
-            self.flip_max = max(self.flip_max, n)
+            self.flip_max = max(self.flip_max, cout * cin)
+        for name, pad in getattr(self, "class_names", []):
+            cout, kh, kw, cin = shapes[name]
+            n, taps, coff = cout * kh * kw * cin, kh * kw, foff
+            for _, taplist in K.dgrad_s2_classes(kh, kw, pad):
+                nt = len(taplist)
+                for t, (y, x) in enumerate(taplist):
+                    desc += [offs[name] + (y * kw + x) * cin, coff + t * cout, cout, cin, taps * cin, nt * cout]
+                coff += cin * nt * cout
+            self.cw[name] = (foff, (n,))
+            foff += (n + ALIGN - 1) // ALIGN * ALIGN
+            self.flip_max = max(self.flip_max, cout * cin)
         self.fb = torch.zeros(max(1, foff), dtype=BF16, device=device)
         for name, (o, shp) in list(self.f.items()):
             self.f[name] = self.fb[o:o + math.prod(shp)].view(shp)
-        self.flip_n = len(names)
+        for name, (o, shp) in list(self.cw.items()):
+            self.cw[name] = self.fb[o:o + shp[0]]
+        self.flip_n = len(desc) // 6
         self.flip_bytes = 4 * foff
         self.flip_desc = torch.tensor(desc if desc else [0], dtype=torch.int64, device=device)
         self.flip_all()
@@ -166,6 +189,8 @@ class ConvBN:
         self.W = ps.add(f"{name}.w", w, logical=cout * k * k * cin_real)
         if need_dgrad and stride == 1:
             ps.want_flip(self.W)
+        elif need_dgrad and stride == 2:
+            ps.want_class_weights(self.W, pad)
         self.G = ps.add(f"{name}.gamma", torch.ones(cout))
         self.B = ps.add(f"{name}.beta", torch.zeros(cout))
 
@@ -246,10 +271,12 @@ class ConvBN:
             ps.grad_ready(self.W, self.G, self.B)
         if dx is not None:
             wt = self.scratch.flip[:self.cout * self.k * self.k * cin].view(cin, self.k, self.k, self.cout)
-            if self.s == 2 and cin == self.cin and K.conv2d_dgrad_s2(self.dz, ps.b[self.W], self.pad, dx,
-                                                                     accumulate=dx_accumulate, wscratch=wt,
-                                                                     acct_flops=self.flops):
-                return
+            if self.s == 2 and cin == self.cin:
+                ready = self.W in ps.cw   # class weights refreshed by ParamStore.flip_all
+                if K.conv2d_dgrad_s2(self.dz, ps.b[self.W], self.pad, dx, accumulate=dx_accumulate,
+                                     wscratch=ps.cw[self.W] if ready else wt, acct_flops=self.flops,
+                                     class_weights_ready=ready):
+                    return
             if self.s == 1 and cin == self.cin and self.W in ps.f:
                 wt = ps.f[self.W]          # refreshed for every layer by ParamStore.flip_all
             else:

@@ -210,3 +210,28 @@ def test_dense_narrow_n_tiles_split_k():
     B = torch.randn(256, 4096, device="cuda", generator=g).to(torch.bfloat16)
     out = K.gemm(A, B, 512, 256, 4096, 0, 0, splits=9, max_bn=64)
     _close(out.sum(0), A.float() @ B.float().t())
+
+
+@pytest.mark.parametrize("cin,cout,k,p", [(64, 128, 3, 1), (128, 256, 1, 0)])
+def test_dgrad_s2_with_batched_class_weights(cin, cout, k, p):
+    """Stride-2 dgrad with the parity-class weight matrices produced by the batched transpose
+    jobs (ParamStore.flip_all's layout) == the dgrad that permutes them itself, bit for bit."""
+    g = torch.Generator(device="cuda").manual_seed(cin + cout + k)
+    n, h, w = 4, 16, 16
+    wt = (torch.randn(cout, k, k, cin, device="cuda", generator=g) / (k * k * cin) ** 0.5).to(torch.bfloat16)
+    oh, ow = K.conv_out_hw(h, w, k, 2, p)
+    dy = torch.randn(n, oh, ow, cout, device="cuda", generator=g).to(torch.bfloat16)
+    acc = k == 1
+    dx_ref = torch.zeros(n, h, w, cin, device="cuda", dtype=torch.bfloat16)
+    assert K.conv2d_dgrad_s2(dy, wt, p, dx_ref, accumulate=acc)
+    desc, coff, taps = [], 0, k * k
+    for _, taplist in K.dgrad_s2_classes(k, k, p):
+        for t, (y, x) in enumerate(taplist):
+            desc += [(y * k + x) * cin, coff + t * cout, cout, cin, taps * cin, len(taplist) * cout]
+        coff += cin * len(taplist) * cout
+    cw = torch.zeros(wt.numel(), device="cuda", dtype=torch.bfloat16)
+    K.transpose_batched(wt.reshape(-1), cw, torch.tensor(desc, dtype=torch.int64, device="cuda"), len(desc) // 6,
+                        cout * cin, 0)
+    dx = torch.zeros_like(dx_ref)
+    assert K.conv2d_dgrad_s2(dy, wt, p, dx, accumulate=acc, wscratch=cw, class_weights_ready=True)
+    assert torch.equal(dx, dx_ref)
