@@ -133,7 +133,10 @@ struct FwdArgs {
                              // others' mean/rstd are given); pass 2 normalises all C channels
 };
 
-__global__ void __launch_bounds__(THREADS) bn_fwd_fused(const FwdArgs a) {
+// OCC = 2: two 512-thread CTAs per SM (<= 64 registers) -- more loads in flight for the
+// latency-bound wide-channel layers; OCC = 1 keeps 86 registers (measured better at C <= 64)
+template <int OCC>
+__global__ void __launch_bounds__(THREADS, OCC) bn_fwd_fused(const FwdArgs a) {
   extern __shared__ float sh[];
   __shared__ float s_scale[2048], s_shift[2048];
   const int C = a.C, G = C / 8, RL = THREADS / G;
@@ -498,7 +501,7 @@ long long* trace_buf() {
   if (!g_trace) cudaMalloc(&g_trace, sizeof(long long) * 8 * 4096);
   return g_trace;
 }
-int g_grid[64] = {0}, g_grid_f[64] = {0};
+int g_grid[64] = {0}, g_grid_f[64] = {0}, g_grid_f2[64] = {0};
 
 // *grid: the backward kernel's co-resident grid; *grid_f: the forward kernel's (it needs
 // fewer registers, so more CTAs fit).  The partials workspace covers the larger.
@@ -511,10 +514,14 @@ int fused_setup(int C, unsigned** bar, int* grid, int* grid_f = nullptr) {
     CVB_CUDA(cudaMemset(g_bar[dev], 0, CVB_GRID_BAR_WORDS * sizeof(unsigned)));
     CVB_CUDA(cudaDeviceSynchronize());
     const size_t smem = (size_t)THREADS * 16 * sizeof(float);
-    CVB_CUDA(cudaFuncSetAttribute(bn_fwd_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CVB_CUDA(cudaFuncSetAttribute(bn_fwd_fused<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CVB_CUDA(cudaFuncSetAttribute(bn_fwd_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CVB_CUDA(cudaFuncSetAttribute(bn_bwd_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int occ_f = 0, occ_b = 0;
-    CVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, bn_fwd_fused, THREADS, smem));
+    int occ_f = 0, occ_b = 0, occ_f2 = 0;
+    CVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, bn_fwd_fused<1>, THREADS, smem));
+    CVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f2, bn_fwd_fused<2>, THREADS, smem));
+    if (occ_f2 > MAX_OCC) occ_f2 = MAX_OCC;
+    g_grid_f2[dev] = (occ_f2 < 1 ? 1 : occ_f2) * cvb_num_sms();
     CVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, bn_bwd_fused, THREADS, smem));
     if (occ_f > MAX_OCC) occ_f = MAX_OCC;
     if (occ_b > MAX_OCC) occ_b = MAX_OCC;
@@ -574,7 +581,11 @@ CVB_API int64_t cvb_bn_fused_workspace_floats(int C) {
   unsigned* bar;
   int grid = 0, grid_f = 0;
   if (fused_setup(C, &bar, &grid, &grid_f)) return -1;
-  return (int64_t)(grid > grid_f ? grid : grid_f) * 2 * C;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int P = grid > grid_f ? grid : grid_f;
+  if (g_grid_f2[dev] > P) P = g_grid_f2[dev];   // the two-CTA forward's grid
+  return (int64_t)P * 2 * C;
 }
 
 // Batch-norm forward in one launch: statistics of x ([rows][C], stride xcs) -> mean/rstd
@@ -611,9 +622,20 @@ CVB_API int cvb_bn_forward_range(const void* x, int64_t rows, int C, int xcs, fl
   FwdArgs a{(const bf16*)x, rows, C, xcs, ws, bar, mean, rstd, eps, run_mean, run_var, momentum, gamma, beta,
             (const bf16*)res, rcs, relu, (bf16*)y, ycs, ycoff, getenv("CVB_BN_FWD_TWO_ROWS") ? 0 : 1, trace_buf(),
             l2hint_knob(), st_off, st_C};
-  const int gf = size_grid(grid, rows, C);
+  // two CTAs per SM for large statistics passes (>= 24M elements: ResNet-18's 33.5M-element
+  // stage-1 layers, +1.1% per step); smaller ones measured better at one CTA (fewer CTAs in the
+  // grid barriers).  Decided by the STATISTICS extent: the grid fixes the row partition of the
+  // fixed-order reduction, so a slice's statistics come out bit-identical whether computed alone
+  // or inside cvb_bn_forward_range.
+  static long long occ2_min = -1;
+  if (occ2_min < 0) { const char* e = getenv("CVB_BN_FWD_OCC2_MIN_ELEMS"); occ2_min = e ? atoll(e) : 24ll << 20; }
+  int dev = 0;
+  CVB_CUDA(cudaGetDevice(&dev));
+  const bool two = rows * (int64_t)(st_C ? st_C : C) >= occ2_min && g_grid_f2[dev] > 0;
+  const int gf = size_grid(two ? g_grid_f2[dev] : grid, rows, C);
   if (C > 16 * gf) { cvb_set_error("bn_forward: more channels than finalising warps"); return CVB_EINVAL; }
-  return launch_coop(bn_fwd_fused, a, gf, (cudaStream_t)stream);
+  return two ? launch_coop(bn_fwd_fused<2>, a, gf, (cudaStream_t)stream)
+             : launch_coop(bn_fwd_fused<1>, a, gf, (cudaStream_t)stream);
 }
 
 // Batch-norm (+ReLU) backward in one launch (same contract as cvb_bn_backward).
