@@ -369,7 +369,11 @@ __device__ __forceinline__ void bwd_apply_dz(const ChanSmem& cs, const float* sh
   st8(dst, o);
 }
 
-__global__ void __launch_bounds__(THREADS, 2) bn_bwd_fused(const BwdArgs a) {
+// OCC = 2: two 512-thread CTAs per SM at <= 64 registers (the large layers); OCC = 1: one CTA per
+// SM with room for every per-row value in registers (no spills; fewer CTAs in the grid
+// barriers) for the small, latency-bound layers
+template <int OCC>
+__global__ void __launch_bounds__(THREADS, OCC) bn_bwd_fused(const BwdArgs a) {
   extern __shared__ float sh[];
   __shared__ ChanSmem cs;
   const int C = a.C, G = C / 8, RL = THREADS / G;
@@ -516,13 +520,14 @@ int fused_setup(int C, unsigned** bar, int* grid, int* grid_f = nullptr) {
     const size_t smem = (size_t)THREADS * 16 * sizeof(float);
     CVB_CUDA(cudaFuncSetAttribute(bn_fwd_fused<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CVB_CUDA(cudaFuncSetAttribute(bn_fwd_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CVB_CUDA(cudaFuncSetAttribute(bn_bwd_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CVB_CUDA(cudaFuncSetAttribute(bn_bwd_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CVB_CUDA(cudaFuncSetAttribute(bn_bwd_fused<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ_f = 0, occ_b = 0, occ_f2 = 0;
     CVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, bn_fwd_fused<1>, THREADS, smem));
     CVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f2, bn_fwd_fused<2>, THREADS, smem));
     if (occ_f2 > MAX_OCC) occ_f2 = MAX_OCC;
     g_grid_f2[dev] = (occ_f2 < 1 ? 1 : occ_f2) * cvb_num_sms();
-    CVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, bn_bwd_fused, THREADS, smem));
+    CVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, bn_bwd_fused<2>, THREADS, smem));
     if (occ_f > MAX_OCC) occ_f = MAX_OCC;
     if (occ_b > MAX_OCC) occ_b = MAX_OCC;
     if (occ_f < 1 || occ_b < 1) { cvb_set_error("bn fused: kernel does not fit on an SM"); return CVB_EINVAL; }
@@ -651,9 +656,15 @@ CVB_API int cvb_bn_backward_fused(const void* dy, int dycs, const void* x, int x
   BwdArgs a{(const bf16*)dy, dycs, (const bf16*)x, xcs, (const bf16*)y, ycs, rows, C, mean, rstd, gamma, beta, relu,
             ws, bar, dgamma, dbeta, (bf16*)dx, dxcs, dx32, accum32, (bf16*)dz_out, two_rows_knob(), trace_buf(),
             l2hint_knob()};
-  const int gb = size_grid(grid, rows, C);
+  // one CTA per SM below 24M elements (same rule and reason as the forward; the grid is fixed
+  // by (rows, C), so DenseNet's statistics-only and full passes of a layer partition alike)
+  static long long one_max = -1;
+  if (one_max < 0) { const char* e = getenv("CVB_BN_BWD_OCC1_MAX_ELEMS"); one_max = e ? atoll(e) : 24ll << 20; }
+  const bool one = rows * (int64_t)C < one_max;
+  const int gb = size_grid(one ? cvb_num_sms() : grid, rows, C);
   if (C > 16 * gb) { cvb_set_error("bn_backward: more channels than finalising warps"); return CVB_EINVAL; }
-  return launch_coop(bn_bwd_fused, a, gb, (cudaStream_t)stream);
+  return one ? launch_coop(bn_bwd_fused<1>, a, gb, (cudaStream_t)stream)
+             : launch_coop(bn_bwd_fused<2>, a, gb, (cudaStream_t)stream);
 }
 
 // ---- DenseNet: deferred input gradient of the BNs over a concat prefix ------------------
