@@ -627,13 +627,13 @@ CVB_API int cvb_bn_forward_range(const void* x, int64_t rows, int C, int xcs, fl
   FwdArgs a{(const bf16*)x, rows, C, xcs, ws, bar, mean, rstd, eps, run_mean, run_var, momentum, gamma, beta,
             (const bf16*)res, rcs, relu, (bf16*)y, ycs, ycoff, getenv("CVB_BN_FWD_TWO_ROWS") ? 0 : 1, trace_buf(),
             l2hint_knob(), st_off, st_C};
-  // two CTAs per SM for large statistics passes (>= 24M elements: ResNet-18's 33.5M-element
-  // stage-1 layers, +1.1% per step); smaller ones measured better at one CTA (fewer CTAs in the
-  // grid barriers).  Decided by the STATISTICS extent: the grid fixes the row partition of the
+  // two CTAs per SM for large statistics passes (>= 12M elements: ResNet-18's stage-1..3
+  // layers, +1.1% per step at 24M, +0.2% more at 12M); smaller ones measured better at one CTA
+  // (fewer CTAs in the grid barriers).  Decided by the STATISTICS extent: the grid fixes the row partition of the
   // fixed-order reduction, so a slice's statistics come out bit-identical whether computed alone
   // or inside cvb_bn_forward_range.
   static long long occ2_min = -1;
-  if (occ2_min < 0) { const char* e = getenv("CVB_BN_FWD_OCC2_MIN_ELEMS"); occ2_min = e ? atoll(e) : 24ll << 20; }
+  if (occ2_min < 0) { const char* e = getenv("CVB_BN_FWD_OCC2_MIN_ELEMS"); occ2_min = e ? atoll(e) : 12000000ll; }
   int dev = 0;
   CVB_CUDA(cudaGetDevice(&dev));
   const bool two = rows * (int64_t)(st_C ? st_C : C) >= occ2_min && g_grid_f2[dev] > 0;
@@ -656,10 +656,11 @@ CVB_API int cvb_bn_backward_fused(const void* dy, int dycs, const void* x, int x
   BwdArgs a{(const bf16*)dy, dycs, (const bf16*)x, xcs, (const bf16*)y, ycs, rows, C, mean, rstd, gamma, beta, relu,
             ws, bar, dgamma, dbeta, (bf16*)dx, dxcs, dx32, accum32, (bf16*)dz_out, two_rows_knob(), trace_buf(),
             l2hint_knob()};
-  // one CTA per SM below 24M elements (same rule and reason as the forward; the grid is fixed
+  // one CTA per SM below 12M elements (same rule and reason as the forward; 24M measured 0.3%
+  // slower on both CNNs, 48M 2% slower on ResNet-18; the grid is fixed
   // by (rows, C), so DenseNet's statistics-only and full passes of a layer partition alike)
   static long long one_max = -1;
-  if (one_max < 0) { const char* e = getenv("CVB_BN_BWD_OCC1_MAX_ELEMS"); one_max = e ? atoll(e) : 24ll << 20; }
+  if (one_max < 0) { const char* e = getenv("CVB_BN_BWD_OCC1_MAX_ELEMS"); one_max = e ? atoll(e) : 12000000ll; }
   const bool one = rows * (int64_t)C < one_max;
   const int gb = size_grid(one ? cvb_num_sms() : grid, rows, C);
   if (C > 16 * gb) { cvb_set_error("bn_backward: more channels than finalising warps"); return CVB_EINVAL; }
