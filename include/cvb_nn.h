@@ -123,7 +123,7 @@ int cvb_reduce_splits_act(const float* part, int splits, int rows, int cols, con
                           int out_f32, int64_t ldo, void* stream);
 /* all stride-1 dgrad weight flips in one launch: desc_dev = nlayers x {src, dst, cout, kh, kw, cin}
    (int64 element offsets into pb / fb) */
-/* Batched bf16 matrix transposes, one launch: desc_dev = njobs x {src off, dst off, rows, cols,
+/* Batched bf16 matrix transposes (one launch per 8192 jobs): desc_dev = njobs x {src off, dst off, rows, cols,
    src row stride, dst row stride} (elements); dst[c*dst_ld + r] = src[r*src_ld + c].  Used for
    the flipped stride-1 dgrad weights (a job per tap) and the stride-2 dgrad parity-class
    weights (a job per class and tap) after every optimiser step. */

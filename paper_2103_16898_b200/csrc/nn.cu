@@ -719,28 +719,82 @@ __global__ void weight_flip_batched(const bf16* __restrict__ pb, bf16* __restric
 // refreshes every derived weight layout of a step after the optimiser: the flipped stride-1
 // dgrad weights (one job per tap) and the per-output-parity class weights of the stride-2
 // dgrads (one job per (class, tap)).  32 x 32 tiles through shared memory, 64-byte rows in/out.
-__global__ void transpose_batched(const bf16* __restrict__ src, bf16* __restrict__ dst, const int64_t* __restrict__ desc) {
-  __shared__ bf16 tile[32][34];
+// 64x64 tiles of every job in one flat tile index (a per-block prefix over the jobs' tile counts,
+// then a binary search per tile): the grid is sized by the total work, not by the largest job
+// times the job count (the 32x32 form launched ~50k mostly idle blocks per ResNet-18 step).  Jobs
+// whose offsets, strides and extents are multiples of 8 move 16-byte vectors through a swizzled
+// tile (conflict-free scatter, 128-byte coalesced rows both ways); others take an element path.
+constexpr int TP_T = 64;
+constexpr int TP_MAX_JOBS = 8192;
+
+__device__ __forceinline__ int tp_tiles(int64_t rows, int64_t cols) {
+  return (int)(((rows + TP_T - 1) / TP_T) * ((cols + TP_T - 1) / TP_T));
+}
+
+__global__ void __launch_bounds__(256) transpose_batched(const bf16* __restrict__ src, bf16* __restrict__ dst,
+                                                         const int64_t* __restrict__ desc, int njobs) {
+  extern __shared__ int s_pref[];                 // njobs + 1 tile prefix
+  __shared__ __align__(16) bf16 tile[TP_T][TP_T];   // [col][row], 16-byte chunks XOR-swizzled by col
+  __shared__ int s_warp[8];
   CVB_PDL_PROLOGUE();
-  const int64_t* d = desc + 6 * blockIdx.y;
-  const int64_t so = d[0], dof = d[1], sld = d[4], dld = d[5];
-  const int rows = (int)d[2], cols = (int)d[3];
-  const int tr = (rows + 31) / 32, tc = (cols + 31) / 32, ntiles = tr * tc;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int r0 = (t / tc) * 32, c0 = (t % tc) * 32;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // ---- exclusive prefix of the jobs' tile counts (each thread a contiguous segment) ----
+  const int seg = (njobs + 255) / 256, j0 = min(njobs, tid * seg), j1 = min(njobs, j0 + seg);
+  int mine = 0;
+  for (int j = j0; j < j1; j++) mine += tp_tiles(desc[6 * j + 2], desc[6 * j + 3]);
+  int incl = mine;
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
-      const int r = r0 + ty + 8 * k, c = c0 + tx;
-      if (r < rows && c < cols) tile[ty + 8 * k][tx] = src[so + (int64_t)r * sld + c];
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_warp[wid] = incl;
+  __syncthreads();
+  int base = 0;
+  for (int w = 0; w < wid; w++) base += s_warp[w];
+  int run = base + incl - mine;
+  for (int j = j0; j < j1; j++) { s_pref[j] = run; run += tp_tiles(desc[6 * j + 2], desc[6 * j + 3]); }
+  if (tid == 255) s_pref[njobs] = base + incl;
+  __syncthreads();
+  const int total = s_pref[njobs];
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    int lo = 0, hi = njobs - 1;   // last job with s_pref[j] <= t
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_pref[mid] <= t) lo = mid; else hi = mid - 1;
     }
-    __syncthreads();
+    const int64_t* d = desc + 6 * lo;
+    const int64_t so = d[0], dof = d[1], rows = d[2], cols = d[3], sld = d[4], dld = d[5];
+    const int lt = t - s_pref[lo], tc = (int)((cols + TP_T - 1) / TP_T);
+    const int64_t r0 = (int64_t)(lt / tc) * TP_T, c0 = (int64_t)(lt % tc) * TP_T;
+    if (((so | dof | rows | cols | sld | dld) & 7) == 0) {
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
-      const int c = c0 + ty + 8 * k, r = r0 + tx;
-      if (r < rows && c < cols) dst[dof + (int64_t)c * dld + r] = tile[tx][ty + 8 * k];
+      for (int h = 0; h < 2; h++) {
+        const int i = tid + 256 * h, r = i >> 3, ch = i & 7;
+        if (r0 + r < rows && c0 + ch * 8 < cols) {
+          const uint4 v = *reinterpret_cast<const uint4*>(src + so + (r0 + r) * sld + c0 + ch * 8);
+          const bf16* e = reinterpret_cast<const bf16*>(&v);
+          // element (r, c = 8ch + k) -> tile[c][8 * ((r >> 3) ^ ch) + (r & 7)]  (c >> 3 == ch)
+          const int col = (((r >> 3) ^ ch) << 3) | (r & 7);
+#pragma unroll
+          for (int k = 0; k < 8; k++) tile[ch * 8 + k][col] = e[k];
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int i = tid + 256 * h, c = i >> 3, rch = i & 7;
+        if (c0 + c < cols && r0 + rch * 8 < rows)
+          *reinterpret_cast<uint4*>(dst + dof + (c0 + c) * dld + r0 + rch * 8) =
+              *reinterpret_cast<const uint4*>(&tile[c][(rch ^ (c >> 3)) << 3]);
+      }
+      __syncthreads();
+    } else {
+      for (int i = tid; i < TP_T * TP_T; i += 256) {
+        const int64_t r = r0 + (i & (TP_T - 1)), c = c0 + (i >> 6);
+        if (r < rows && c < cols) dst[dof + c * dld + r] = src[so + r * sld + c];
+      }
     }
-    __syncthreads();
   }
 }
 
@@ -1182,12 +1236,21 @@ CVB_API int cvb_weight_flip_batched(const void* pb, void* fb, const int64_t* des
 CVB_API int cvb_transpose_batched(const void* src, void* dst, const int64_t* desc_dev, int njobs, int64_t max_elems,
                                   void* stream) {
   if (njobs <= 0) return CVB_OK;
-  if (njobs > 65535) { cvb_set_error("transpose_batched: too many jobs"); return CVB_EINVAL; }
-  unsigned gx = (unsigned)((max_elems + 1023) / 1024);
-  if (gx > 256) gx = 256;
-  if (gx < 1) gx = 1;
-  cvb_launch(transpose_batched, dim3(gx, njobs), 256, 0, STREAM, (const bf16*)src, (bf16*)dst, desc_dev);
-  CVB_CHECK_LAUNCH();
+  static bool attr = false;
+  if (!attr) {
+    CVB_CUDA(cudaFuncSetAttribute(transpose_batched, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (TP_MAX_JOBS + 1) * (int)sizeof(int)));
+    attr = true;
+  }
+  for (int j = 0; j < njobs; j += TP_MAX_JOBS) {   // the tile prefix lives in shared memory
+    const int nj = njobs - j < TP_MAX_JOBS ? njobs - j : TP_MAX_JOBS;
+    const int64_t tiles = (int64_t)nj * ((max_elems + TP_T * TP_T - 1) / (TP_T * TP_T) + 1);
+    const int64_t cap = 4ll * cvb_num_sms();
+    const unsigned g = (unsigned)(tiles < cap ? tiles : cap);
+    cvb_launch(transpose_batched, dim3(g), 256, (size_t)(nj + 1) * sizeof(int), STREAM, (const bf16*)src,
+               (bf16*)dst, desc_dev + 6 * (int64_t)j, nj);
+    CVB_CHECK_LAUNCH();
+  }
   return CVB_OK;
 }
 

@@ -251,3 +251,38 @@ def test_weight_flip_batched_matches_torch():
         want = w.flip(1, 2).permute(3, 1, 2, 0).contiguous().reshape(-1)
         assert torch.equal(fb[off:off + n], want)
         off += n
+
+
+@pytest.mark.gpu
+def test_transpose_batched_matches_torch():
+    """Batched transposes in one launch (the per-step flipped / class dgrad weights): vector jobs
+    (everything a multiple of 8) and element jobs (odd extents / offsets / strides), tiles
+    partially outside the matrix, and more jobs than one launch's shared-memory prefix holds."""
+    g = torch.Generator().manual_seed(7)
+    shapes = [(64, 64), (512, 512), (32, 128), (8, 24), (72, 40), (13, 7), (130, 66), (1, 1), (200, 8)]
+    shapes += [(8 * int(torch.randint(1, 9, (1,), generator=g)), 8 * int(torch.randint(1, 9, (1,), generator=g)))
+               for _ in range(60)]
+    src = torch.randn(sum(r * c + 16 for r, c in shapes) + 8, device=dev).bfloat16()
+    dst = torch.zeros(sum(r * c + 16 for r, c in shapes) + 8, dtype=torch.bfloat16, device=dev)
+    up8 = lambda v: (v + 7) // 8 * 8
+    desc, so, do = [], 8, 0
+    for i, (r, c) in enumerate(shapes):
+        odd = i == 4   # an element job with an unaligned source offset
+        s0 = so + (1 if odd else 0)
+        desc += [s0, do, r, c, c, r]
+        so += up8(r * c + 5)
+        do += up8(r * c + 3)
+    desc_dev = torch.tensor(desc, dtype=torch.int64, device=dev)
+    max_elems = max(r * c for r, c in shapes)
+    K.transpose_batched(src, dst, desc_dev, len(shapes), max_elems, 0)
+    for j in range(len(shapes)):
+        s0, d0, r, c = desc[6 * j:6 * j + 4]
+        want = src[s0:s0 + r * c].view(r, c).t().contiguous().reshape(-1)
+        assert torch.equal(dst[d0:d0 + r * c], want), (j, r, c)
+    # > 8192 jobs: several launches
+    n = 9000
+    src2 = torch.randn(n * 64, device=dev).bfloat16()
+    dst2 = torch.zeros_like(src2)
+    desc2 = torch.tensor([[64 * j, 64 * j, 8, 8, 8, 8] for j in range(n)], dtype=torch.int64, device=dev).reshape(-1)
+    K.transpose_batched(src2, dst2, desc2, n, 64, 0)
+    assert torch.equal(dst2.view(n, 8, 8), src2.view(n, 8, 8).transpose(1, 2))
