@@ -697,7 +697,42 @@ struct GatherArgs {
 
 constexpr int GATHER_THREADS = 256, GATHER_CH = 64;   // a CTA: 64 channels (8 groups) x 32 row lanes
 
-__global__ void __launch_bounds__(GATHER_THREADS) bn_gather_dx(const __grid_constant__ GatherArgs a) {
+// one gather term: dz = dy * mask, acc += k * (dz - kb - xhat * kg)
+__device__ __forceinline__ void gather_term(const uint4& u, const float* cfl, int g, const float xh[8], float acc[8]) {
+  float d[8], kk[8], kb[8], kg[8], ga[8], be[8];
+  unpack8(u, d);
+  lds8(cfl + 0 * GATHER_CH + g * 8, kk);
+  lds8(cfl + 1 * GATHER_CH + g * 8, kb);
+  lds8(cfl + 2 * GATHER_CH + g * 8, kg);
+  lds8(cfl + 3 * GATHER_CH + g * 8, ga);
+  lds8(cfl + 4 * GATHER_CH + g * 8, be);
+#pragma unroll
+  for (int k = 0; k < 8; k++) {   // bwd_load + the accumulating pass-2 loop, same roundings
+    if (!(__fmaf_rn(xh[k], ga[k], be[k]) > 0.f)) d[k] = 0.f;
+    const float o = __fmul_rn(kk[k], __fmaf_rn(-xh[k], kg[k], __fsub_rn(d[k], kb[k])));
+    acc[k] = __fadd_rn(acc[k], o);
+  }
+}
+
+// Latency-bound (ncu: long-scoreboard stalls, 16 warps per SM at 110 registers): every load of a
+// row -- x, the fp32 base and the first GATHER_BATCH layers' dY -- is issued before any is used,
+// and three CTAs fit per SM.
+// the same term with the coefficients read per element (fewer live registers: 3 CTAs per SM)
+__device__ __forceinline__ void gather_term_s(const uint4& u, const float* cfl, int g, const float xh[8], float acc[8]) {
+  float d[8];
+  unpack8(u, d);
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const float* c = cfl + g * 8 + k;
+    if (!(__fmaf_rn(xh[k], c[3 * GATHER_CH], c[4 * GATHER_CH]) > 0.f)) d[k] = 0.f;
+    const float o = __fmul_rn(c[0], __fmaf_rn(-xh[k], c[2 * GATHER_CH], __fsub_rn(d[k], c[GATHER_CH])));
+    acc[k] = __fadd_rn(acc[k], o);
+  }
+}
+
+constexpr int GATHER_BATCH = 8;
+template <int OCC>
+__global__ void __launch_bounds__(GATHER_THREADS, OCC) bn_gather_dx(const __grid_constant__ GatherArgs a) {
   __shared__ __align__(16) float cf[GATHER_MAX_LAYERS][5][GATHER_CH];   // kk, kb, kg, gamma, beta
   __shared__ __align__(16) float cm[2][GATHER_CH];                      // mean, rstd
   CVB_PDL_PROLOGUE();
@@ -720,49 +755,42 @@ __global__ void __launch_bounds__(GATHER_THREADS) bn_gather_dx(const __grid_cons
   const int G = nch / 8, g = threadIdx.x % G, rl = threadIdx.x / G, RL = GATHER_THREADS / G;
   if (rl >= RL) return;
   const int cg = cbase + g * 8;
-  float mu[8], rs[8];
-#pragma unroll
-  for (int k = 0; k < 8; k++) { mu[k] = cm[0][g * 8 + k]; rs[k] = cm[1][g * 8 + k]; }
+  const int nb = a.nl < GATHER_BATCH ? a.nl : GATHER_BATCH;
   for (int64_t r = (int64_t)blockIdx.x * RL + rl; r < a.rows; r += (int64_t)gridDim.x * RL) {
-    float xh[8], acc[8];
-    {
-      float xv[8];
-      ld8(a.x + r * a.xcs + cg, xv);
-#pragma unroll
-      for (int k = 0; k < 8; k++) xh[k] = __fmul_rn(__fsub_rn(xv[k], mu[k]), rs[k]);
-    }
+    const uint4 ux = __ldcg(reinterpret_cast<const uint4*>(a.x + r * a.xcs + cg));
+    float4 b0 = make_float4(0.f, 0.f, 0.f, 0.f), b1 = b0;
     if (a.base) {
       const float4* b4 = reinterpret_cast<const float4*>(a.base + r * a.bcs + cg);
-      const float4 u = __ldcg(b4), w = __ldcg(b4 + 1);
-      acc[0] = u.x; acc[1] = u.y; acc[2] = u.z; acc[3] = u.w; acc[4] = w.x; acc[5] = w.y; acc[6] = w.z; acc[7] = w.w;
-    } else {
-#pragma unroll
-      for (int k = 0; k < 8; k++) acc[k] = 0.f;
+      b0 = __ldcg(b4);
+      b1 = __ldcg(b4 + 1);
     }
-    for (int l0 = 0; l0 < a.nl; l0 += 8) {   // eight layers' 16-byte dY loads in flight
-      uint4 u[8];
+    uint4 u[GATHER_BATCH];
 #pragma unroll
-      for (int j = 0; j < 8; j++)
+    for (int j = 0; j < GATHER_BATCH; j++)
+      if (j < nb) u[j] = __ldcg(reinterpret_cast<const uint4*>(a.dy[j] + r * a.dycs[j] + cg));
+    float xh[8], acc[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    {
+      float xv[8];
+      unpack8(ux, xv);
+#pragma unroll
+      for (int k = 0; k < 8; k++) xh[k] = __fmul_rn(__fsub_rn(xv[k], cm[0][g * 8 + k]), cm[1][g * 8 + k]);
+    }
+#pragma unroll
+    for (int j = 0; j < GATHER_BATCH; j++)
+      if (j < nb) {
+        if (OCC >= 3) gather_term_s(u[j], &cf[j][0][0], g, xh, acc);
+        else gather_term(u[j], &cf[j][0][0], g, xh, acc);
+      }
+    for (int l0 = GATHER_BATCH; l0 < a.nl; l0 += GATHER_BATCH) {   // later layers, a batch in flight
+#pragma unroll
+      for (int j = 0; j < GATHER_BATCH; j++)
         if (l0 + j < a.nl) u[j] = __ldcg(reinterpret_cast<const uint4*>(a.dy[l0 + j] + r * a.dycs[l0 + j] + cg));
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
-        if (l0 + j >= a.nl) break;
-        const int l = l0 + j;
-        float d[8];
-        unpack8(u[j], d);
-        float kk[8], kb[8], kg[8], ga[8], be[8];
-        lds8(&cf[l][0][g * 8], kk);
-        lds8(&cf[l][1][g * 8], kb);
-        lds8(&cf[l][2][g * 8], kg);
-        lds8(&cf[l][3][g * 8], ga);
-        lds8(&cf[l][4][g * 8], be);
-#pragma unroll
-        for (int k = 0; k < 8; k++) {   // bwd_load + the accumulating pass-2 loop, same roundings
-          if (!(__fmaf_rn(xh[k], ga[k], be[k]) > 0.f)) d[k] = 0.f;
-          const float o = __fmul_rn(kk[k], __fmaf_rn(-xh[k], kg[k], __fsub_rn(d[k], kb[k])));
-          acc[k] = __fadd_rn(acc[k], o);
+      for (int j = 0; j < GATHER_BATCH; j++)
+        if (l0 + j < a.nl) {
+          if (OCC >= 3) gather_term_s(u[j], &cf[l0 + j][0][0], g, xh, acc);
+          else gather_term(u[j], &cf[l0 + j][0][0], g, xh, acc);
         }
-      }
     }
     if (a.out_f32) {
       float4* o4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + r * a.ocs + cg);
@@ -799,7 +827,12 @@ CVB_API int cvb_bn_gather_dx(const void* x, int xcs, int64_t rows, int nc, const
   int64_t bx = (int64_t)cvb_num_sms() * 8 / chunks;
   if (bx < 1) bx = 1;
   if (bx > rblocks) bx = rblocks;
-  cvb_launch(bn_gather_dx, dim3((unsigned)bx, (unsigned)chunks), dim3(GATHER_THREADS), 0, (cudaStream_t)stream, a);
+  static int occ = -1;
+  if (occ < 0) { const char* e = getenv("CVB_GATHER_OCC"); occ = e ? atoi(e) : 2; }
+  if (occ >= 3)
+    cvb_launch(bn_gather_dx<3>, dim3((unsigned)bx, (unsigned)chunks), dim3(GATHER_THREADS), 0, (cudaStream_t)stream, a);
+  else
+    cvb_launch(bn_gather_dx<2>, dim3((unsigned)bx, (unsigned)chunks), dim3(GATHER_THREADS), 0, (cudaStream_t)stream, a);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
