@@ -85,6 +85,16 @@ int cvb_bn_backward_fused(const void* dy, int dycs, const void* x, int xcs, cons
                           int C, const float* mean, const float* rstd, const float* gamma, const float* beta, int relu,
                           float* ws, float* dgamma, float* dbeta, void* dx, int dxcs, float* dx32, int accum32,
                           void* dz_out, void* stream);
+/* ReLU mask instead of y (residual layers): cvb_bn_forward_mask also writes mask[rows][C/8] bytes,
+   bit k of byte g = (y[row][8g + k] > 0) exactly as stored in bf16; cvb_bn_backward_fused_mask
+   reads it in place of y (1/16 of the bytes). */
+int cvb_bn_forward_mask(const void* x, int64_t rows, int C, int xcs, float* ws, float* mean, float* rstd, float eps,
+                        float* run_mean, float* run_var, float momentum, const float* gamma, const float* beta,
+                        const void* res, int rcs, int relu, void* y, int ycs, int ycoff, void* mask, void* stream);
+int cvb_bn_backward_fused_mask(const void* dy, int dycs, const void* x, int xcs, const void* mask, int64_t rows,
+                               int C, const float* mean, const float* rstd, const float* gamma, const float* beta,
+                               int relu, float* ws, float* dgamma, float* dbeta, void* dx, int dxcs, float* dx32,
+                               int accum32, void* dz_out, void* stream);
 
 /* ---- pooling -------------------------------------------------------------------------------- */
 int cvb_maxpool_fwd(const void* x, int n, int h, int w, int C, int k, int s, int p, void* y, int oh, int ow, int ycs,

@@ -84,6 +84,10 @@ SIGNATURES = {
                                     _INT, _INT, _P, _INT, _INT, _INT, _INT, _P]),
     "cvb_bn_backward_fused": (_INT, [_P, _INT, _P, _INT, _P, _INT, _I64, _INT, _P, _P, _P, _P, _INT, _P, _P, _P, _P,
                                      _INT, _P, _INT, _P, _P]),
+    "cvb_bn_forward_mask": (_INT, [_P, _I64, _INT, _INT, _P, _P, _P, _c.c_float, _P, _P, _c.c_float, _P, _P, _P,
+                                   _INT, _INT, _P, _INT, _INT, _P, _P]),
+    "cvb_bn_backward_fused_mask": (_INT, [_P, _INT, _P, _INT, _P, _I64, _INT, _P, _P, _P, _P, _INT, _P, _P, _P, _P,
+                                          _INT, _P, _INT, _P, _P]),
     "cvb_weight_flip_batched": (_INT, [_P, _P, _P, _INT, _I64, _P]),
     "cvb_transpose_batched": (_INT, [_P, _P, _P, _INT, _I64, _P]),
     "cvb_space_to_depth2": (_INT, [_P, _INT, _INT, _INT, _INT, _P, _P]),

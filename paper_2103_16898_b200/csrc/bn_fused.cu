@@ -57,6 +57,12 @@ __device__ __forceinline__ uint64_t pol_drop() {
 __device__ __forceinline__ uint4 ldv(const void* p, bool hint, uint64_t pol) {
   return hint ? ldv_pol(p, pol) : __ldcg(reinterpret_cast<const uint4*>(p));
 }
+__device__ __forceinline__ unsigned ldg_u8(const unsigned char* p, bool hint, uint64_t pol) {
+  if (!hint) return __ldcg(p);
+  unsigned short r;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(r) : "l"(p), "l"(pol));
+  return r;
+}
 __device__ __forceinline__ void unpack8(const uint4& u, float v[8]) {
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
@@ -131,7 +137,18 @@ struct FwdArgs {
   int hint;                  // L2 residency hints + reversed pass 2 (see ldv)
   int st_off, st_C;          // st_C > 0: statistics of channels [st_off, st_off + st_C) only (the
                              // others' mean/rstd are given); pass 2 normalises all C channels
+  unsigned char* mask;       // optional ReLU mask out: byte [row][C/8], bit k = (bf16 y of channel 8g+k > 0)
 };
+
+// bf16 round-to-nearest-even of a non-negative fp32 value is > 0 iff the value exceeds 2^-134
+// (half the smallest bf16 subnormal; the tie rounds to 0): the mask bit equals (bf16(o) > 0)
+__device__ __forceinline__ unsigned relu_bits(const float o[8]) {
+  const float lim = __int_as_float(0x00008000);   // 2^-134
+  unsigned b = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) b |= (o[k] > lim ? 1u : 0u) << k;
+  return b;
+}
 
 // OCC = 2: two 512-thread CTAs per SM (<= 64 registers) -- more loads in flight for the
 // latency-bound wide-channel layers; OCC = 1 keeps 86 registers (measured better at C <= 64)
@@ -247,6 +264,29 @@ __global__ void __launch_bounds__(THREADS, OCC) bn_fwd_fused(const FwdArgs a) {
       st8(a.y + R(r + RL) * a.ycs + a.ycoff + g * 8, o);
     }
   }
+  if (a.res) {   // residual: two rows' x and res loads in flight per thread
+    for (; r + RL < r1; r += 2 * RL) {
+      const uint4 ux0 = ldv(a.x + R(r) * a.xcs + g * 8, hint, pd);
+      const uint4 ur0 = ldv(a.res + R(r) * a.rcs + g * 8, false, 0);
+      const uint4 ux1 = ldv(a.x + R(r + RL) * a.xcs + g * 8, hint, pd);
+      const uint4 ur1 = ldv(a.res + R(r + RL) * a.rcs + g * 8, false, 0);
+#pragma unroll
+      for (int j = 0; j < 2; j++) {
+        float v[8], rv[8], o[8];
+        unpack8(j ? ux1 : ux0, v);
+        unpack8(j ? ur1 : ur0, rv);
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          float z = (v[k] - mu[k]) * sc[k] + be[k];
+          z += rv[k];
+          o[k] = a.relu ? fmaxf(z, 0.f) : z;
+        }
+        const int64_t rr = R(r + j * RL);
+        st8(a.y + rr * a.ycs + a.ycoff + g * 8, o);
+        if (a.mask) a.mask[rr * G + g] = (unsigned char)relu_bits(o);
+      }
+    }
+  }
   for (; r < r1; r += RL) {
     float v[8], o[8], rv[8];
     ld8h(a.x + R(r) * a.xcs + g * 8, v, hint, pd);
@@ -258,6 +298,7 @@ __global__ void __launch_bounds__(THREADS, OCC) bn_fwd_fused(const FwdArgs a) {
       o[k] = a.relu ? fmaxf(z, 0.f) : z;
     }
     st8(a.y + R(r) * a.ycs + a.ycoff + g * 8, o);
+    if (a.mask) a.mask[R(r) * G + g] = (unsigned char)relu_bits(o);
   }
 #undef R
   bn_trace(a.trace, 6);
@@ -272,6 +313,7 @@ struct BwdArgs {
   int two_rows;              // pass 2: two rows' raw loads in flight (CVB_BN_BWD_ONE_ROW=1: off)
   long long* trace;          // CVB_BN_TRACE: per-CTA phase timestamps (globaltimer ns), debug only
   int hint;                  // L2 residency hints + reversed pass 2 (see ldv)
+  const unsigned char* mask; // optional ReLU mask (cvb_bn_forward_mask's), read instead of y
 };
 
 // Per-channel constants live in shared memory (8 consecutive floats per channel group, two
@@ -300,7 +342,11 @@ __device__ __forceinline__ void bwd_load(const BwdArgs& a, int64_t r, int g, con
 #pragma unroll
   for (int k = 0; k < 8; k++) xh[k] = __fmul_rn(__fsub_rn(xv[k], mu[k]), rs[k]);
   if (a.relu) {
-    if (a.y) {
+    if (a.mask) {
+      const unsigned b = ldg_u8(a.mask + r * (a.C / 8) + g, hint, pol);
+#pragma unroll
+      for (int k = 0; k < 8; k++) if (!((b >> k) & 1u)) d[k] = 0.f;
+    } else if (a.y) {
       float yv[8];
       ld8h(a.y + r * a.ycs + g * 8, yv, hint, pol);
 #pragma unroll
@@ -457,7 +503,7 @@ __global__ void __launch_bounds__(THREADS, OCC) bn_bwd_fused(const BwdArgs a) {
     bn_trace(a.trace, 6);
     return;
   }
-  if (a.two_rows && !a.dx32 && !a.y) {
+  if (a.two_rows && !a.dx32 && !a.y && !a.mask) {
     // bf16 dx, mask recomputed from x: two rows' raw 16-byte loads in flight per thread (the
     // pass is load-latency bound), converted one row at a time (stays within 64 registers)
     for (; r + RL < r1; r += 2 * RL) {
@@ -611,10 +657,11 @@ CVB_API int cvb_bn_forward(const void* x, int64_t rows, int C, int xcs, float* w
 // st_off + st_C) (st_C > 0; multiple of 8); mean/rstd of the other channels are inputs.  DenseNet:
 // the statistics of the newest concat slice and the normalisation of the whole prefix in one
 // launch (no running statistics are updated for a partial range).
-CVB_API int cvb_bn_forward_range(const void* x, int64_t rows, int C, int xcs, float* ws, float* mean, float* rstd,
-                                 float eps, float* run_mean, float* run_var, float momentum, const float* gamma,
-                                 const float* beta, const void* res, int rcs, int relu, void* y, int ycs, int ycoff,
-                                 int st_off, int st_C, void* stream) {
+namespace {
+int bn_forward_impl(const void* x, int64_t rows, int C, int xcs, float* ws, float* mean, float* rstd, float eps,
+                    float* run_mean, float* run_var, float momentum, const float* gamma, const float* beta,
+                    const void* res, int rcs, int relu, void* y, int ycs, int ycoff, int st_off, int st_C,
+                    void* mask, void* stream) {
   if (st_C && (st_C % 8 || st_off % 8 || st_off < 0 || st_off + st_C > C || run_mean)) {
     cvb_set_error("bn_forward_range: bad statistics range");
     return CVB_EINVAL;
@@ -626,7 +673,8 @@ CVB_API int cvb_bn_forward_range(const void* x, int64_t rows, int C, int xcs, fl
   if (rc) return rc;
   FwdArgs a{(const bf16*)x, rows, C, xcs, ws, bar, mean, rstd, eps, run_mean, run_var, momentum, gamma, beta,
             (const bf16*)res, rcs, relu, (bf16*)y, ycs, ycoff, getenv("CVB_BN_FWD_TWO_ROWS") ? 0 : 1, trace_buf(),
-            l2hint_knob(), st_off, st_C};
+            l2hint_knob(), st_off, st_C, (unsigned char*)mask};
+  if (mask && !y) { cvb_set_error("bn_forward: a ReLU mask needs y"); return CVB_EINVAL; }
   // two CTAs per SM for large statistics passes (>= 12M elements: ResNet-18's stage-1..3
   // layers, +1.1% per step at 24M, +0.2% more at 12M); smaller ones measured better at one CTA
   // (fewer CTAs in the grid barriers).  Decided by the STATISTICS extent: the grid fixes the row partition of the
@@ -642,12 +690,32 @@ CVB_API int cvb_bn_forward_range(const void* x, int64_t rows, int C, int xcs, fl
   return two ? launch_coop(bn_fwd_fused<2>, a, gf, (cudaStream_t)stream)
              : launch_coop(bn_fwd_fused<1>, a, gf, (cudaStream_t)stream);
 }
+}  // namespace
+
+CVB_API int cvb_bn_forward_range(const void* x, int64_t rows, int C, int xcs, float* ws, float* mean, float* rstd,
+                                 float eps, float* run_mean, float* run_var, float momentum, const float* gamma,
+                                 const float* beta, const void* res, int rcs, int relu, void* y, int ycs, int ycoff,
+                                 int st_off, int st_C, void* stream) {
+  return bn_forward_impl(x, rows, C, xcs, ws, mean, rstd, eps, run_mean, run_var, momentum, gamma, beta, res, rcs,
+                         relu, y, ycs, ycoff, st_off, st_C, nullptr, stream);
+}
+
+// cvb_bn_forward that also writes the ReLU mask of y: mask[row][C/8] bytes, bit k of byte g =
+// (y[row][8g + k] > 0).  Read back by cvb_bn_backward_fused_mask instead of y: 1/16 of the bytes.
+CVB_API int cvb_bn_forward_mask(const void* x, int64_t rows, int C, int xcs, float* ws, float* mean, float* rstd,
+                                float eps, float* run_mean, float* run_var, float momentum, const float* gamma,
+                                const float* beta, const void* res, int rcs, int relu, void* y, int ycs, int ycoff,
+                                void* mask, void* stream) {
+  return bn_forward_impl(x, rows, C, xcs, ws, mean, rstd, eps, run_mean, run_var, momentum, gamma, beta, res, rcs,
+                         relu, y, ycs, ycoff, 0, 0, mask, stream);
+}
 
 // Batch-norm (+ReLU) backward in one launch (same contract as cvb_bn_backward).
-CVB_API int cvb_bn_backward_fused(const void* dy, int dycs, const void* x, int xcs, const void* y, int ycs, int64_t rows,
-                                  int C, const float* mean, const float* rstd, const float* gamma, const float* beta,
-                                  int relu, float* ws, float* dgamma, float* dbeta, void* dx, int dxcs, float* dx32,
-                                  int accum32, void* dz_out, void* stream) {
+namespace {
+int bn_backward_impl(const void* dy, int dycs, const void* x, int xcs, const void* y, int ycs, int64_t rows, int C,
+                     const float* mean, const float* rstd, const float* gamma, const float* beta, int relu, float* ws,
+                     float* dgamma, float* dbeta, void* dx, int dxcs, float* dx32, int accum32, void* dz_out,
+                     const void* mask, void* stream) {
   if (C % 8 || C / 8 > THREADS) { cvb_set_error("bn_backward: bad C"); return CVB_EINVAL; }
   unsigned* bar;
   int grid;
@@ -655,7 +723,7 @@ CVB_API int cvb_bn_backward_fused(const void* dy, int dycs, const void* x, int x
   if (rc) return rc;
   BwdArgs a{(const bf16*)dy, dycs, (const bf16*)x, xcs, (const bf16*)y, ycs, rows, C, mean, rstd, gamma, beta, relu,
             ws, bar, dgamma, dbeta, (bf16*)dx, dxcs, dx32, accum32, (bf16*)dz_out, two_rows_knob(), trace_buf(),
-            l2hint_knob()};
+            l2hint_knob(), (const unsigned char*)mask};
   // one CTA per SM below 12M elements (same rule and reason as the forward; 24M measured 0.3%
   // slower on both CNNs, 48M 2% slower on ResNet-18; the grid is fixed
   // by (rows, C), so DenseNet's statistics-only and full passes of a layer partition alike)
@@ -666,6 +734,25 @@ CVB_API int cvb_bn_backward_fused(const void* dy, int dycs, const void* x, int x
   if (C > 16 * gb) { cvb_set_error("bn_backward: more channels than finalising warps"); return CVB_EINVAL; }
   return one ? launch_coop(bn_bwd_fused<1>, a, gb, (cudaStream_t)stream)
              : launch_coop(bn_bwd_fused<2>, a, gb, (cudaStream_t)stream);
+}
+}  // namespace
+
+CVB_API int cvb_bn_backward_fused(const void* dy, int dycs, const void* x, int xcs, const void* y, int ycs, int64_t rows,
+                                  int C, const float* mean, const float* rstd, const float* gamma, const float* beta,
+                                  int relu, float* ws, float* dgamma, float* dbeta, void* dx, int dxcs, float* dx32,
+                                  int accum32, void* dz_out, void* stream) {
+  return bn_backward_impl(dy, dycs, x, xcs, y, ycs, rows, C, mean, rstd, gamma, beta, relu, ws, dgamma, dbeta, dx,
+                          dxcs, dx32, accum32, dz_out, nullptr, stream);
+}
+
+// cvb_bn_backward_fused with the ReLU mask written by cvb_bn_forward_mask in place of y
+CVB_API int cvb_bn_backward_fused_mask(const void* dy, int dycs, const void* x, int xcs, const void* mask,
+                                       int64_t rows, int C, const float* mean, const float* rstd, const float* gamma,
+                                       const float* beta, int relu, float* ws, float* dgamma, float* dbeta, void* dx,
+                                       int dxcs, float* dx32, int accum32, void* dz_out, void* stream) {
+  if (!mask) { cvb_set_error("bn_backward_mask: mask is NULL"); return CVB_EINVAL; }
+  return bn_backward_impl(dy, dycs, x, xcs, nullptr, 0, rows, C, mean, rstd, gamma, beta, relu, ws, dgamma, dbeta,
+                          dx, dxcs, dx32, accum32, dz_out, mask, stream);
 }
 
 // ---- DenseNet: deferred input gradient of the BNs over a concat prefix ------------------

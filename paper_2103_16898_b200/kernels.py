@@ -78,7 +78,8 @@ LAUNCH_CLASS = {
     **{n: "umma_gemm" for n in ("cvb_conv2d_fwd", "cvb_conv2d_wgrad", "cvb_gemm", "cvb_gemm_ex",
                                 "cvb_conv2d_dgrad_s2")},
     **{n: "bn" for n in ("cvb_bn_stats", "cvb_bn_forward", "cvb_bn_forward_range", "cvb_bn_apply", "cvb_bn_backward",
-                         "cvb_bn_backward_fused", "cvb_bn_gather_dx")},
+                         "cvb_bn_backward_fused", "cvb_bn_gather_dx", "cvb_bn_forward_mask",
+                         "cvb_bn_backward_fused_mask")},
     **{n: "pool" for n in ("cvb_maxpool_fwd", "cvb_maxpool_fwd_idx", "cvb_maxpool_bwd", "cvb_maxpool_bwd_idx",
                            "cvb_avgpool_fwd", "cvb_avgpool_bwd", "cvb_gap_fwd", "cvb_gap_bwd")},
     **{n: "head" for n in ("cvb_softmax_xent", "cvb_head_train")},
@@ -239,17 +240,26 @@ def bn_stats(x, rows, C, xcs, ws, mean, rstd, eps=1e-5, run_mean=None, run_var=N
 
 
 def bn_forward(x, rows, C, xcs, ws, mean, rstd, gamma, beta, y, ycs, ycoff=0, relu=True, res=None, rcs=0, eps=1e-5,
-               run_mean=None, run_var=None, momentum=0.1):
-    """Statistics + normalisation (+residual, +ReLU) of one BN layer in a single launch."""
+               run_mean=None, run_var=None, momentum=0.1, mask=None):
+    """Statistics + normalisation (+residual, +ReLU) of one BN layer in a single launch.
+    mask (uint8 [rows][C/8]): also write y's ReLU mask bits (for bn_backward(mask=...))."""
     if _UNFUSED_BN:
+        if mask is not None:
+            raise RuntimeError("bn_forward: the ReLU mask needs the fused BN kernels")
         bn_stats(x, rows, C, xcs, ws, mean, rstd, eps, run_mean, run_var, momentum)
         bn_apply(x, rows, C, xcs, mean, rstd, gamma, beta, y, ycs, ycoff, relu, res, rcs)
         return
-    # algorithmic bytes: x (+res) read once, y written once (the statistics pass's read of x is traffic)
-    tok = REC.begin(1, "bn", 0, rows * C * 2 * (3 if res is not None else 2))
-    rc = _lib_bound().cvb_bn_forward(x.data_ptr(), rows, C, xcs, ws.data_ptr(), mean.data_ptr(), rstd.data_ptr(), eps,
+    # algorithmic bytes: x (+res) read once, y (+mask) written once (the statistics pass's read of x is traffic)
+    tok = REC.begin(1, "bn", 0, rows * C * 2 * (3 if res is not None else 2) + (rows * C // 8 if mask is not None else 0))
+    lib = _lib_bound()
+    if mask is not None:
+        rc = lib.cvb_bn_forward_mask(x.data_ptr(), rows, C, xcs, ws.data_ptr(), mean.data_ptr(), rstd.data_ptr(), eps,
                                      _ptr(run_mean), _ptr(run_var), momentum, gamma.data_ptr(), beta.data_ptr(),
-                                     _ptr(res), rcs, int(relu), y.data_ptr(), ycs, ycoff, _stream())
+                                     _ptr(res), rcs, int(relu), y.data_ptr(), ycs, ycoff, mask.data_ptr(), _stream())
+    else:
+        rc = lib.cvb_bn_forward(x.data_ptr(), rows, C, xcs, ws.data_ptr(), mean.data_ptr(), rstd.data_ptr(), eps,
+                                _ptr(run_mean), _ptr(run_var), momentum, gamma.data_ptr(), beta.data_ptr(),
+                                _ptr(res), rcs, int(relu), y.data_ptr(), ycs, ycoff, _stream())
     REC.end(tok)
     _lib.check(rc, "bn_forward")
 
@@ -274,12 +284,23 @@ def bn_apply(x, rows, C, xcs, mean, rstd, gamma, beta, y, ycs, ycoff=0, relu=Tru
 
 
 def bn_backward(dy, dycs, x, xcs, rows, C, mean, rstd, gamma, beta, ws, dgamma, dbeta, relu=True, y=None, ycs=0,
-                dx=None, dxcs=0, dx32=None, accum32=False, dz_out=None):
+                dx=None, dxcs=0, dx32=None, accum32=False, dz_out=None, mask=None):
     # algorithmic bytes: dy, x (, y) read once, dz (bf16) and dx written once -- dx as bf16, fp32, or fp32
     # read-modify-write when accumulating. The kernel's second pass re-reads its inputs (mostly from L2);
     # those re-reads are traffic, not algorithmic bytes.
     dx_b = 8 if (dx32 is not None and accum32) else 4 if dx32 is not None else 2 if dx is not None else 0
     nb = rows * C * (2 * (3 if y is not None else 2) + (2 if dz_out is not None else 0) + dx_b)
+    if mask is not None:   # the ReLU mask of y (bn_forward(mask=...)) in place of y
+        if _UNFUSED_BN:
+            raise RuntimeError("bn_backward: the ReLU mask needs the fused BN kernels")
+        tok = REC.begin(1, "bn", 0, nb + rows * C // 8)
+        rc = _lib_bound().cvb_bn_backward_fused_mask(
+            dy.data_ptr(), dycs, x.data_ptr(), xcs, mask.data_ptr(), rows, C, mean.data_ptr(), rstd.data_ptr(),
+            gamma.data_ptr(), beta.data_ptr(), int(relu), ws.data_ptr(), dgamma.data_ptr(), dbeta.data_ptr(),
+            _ptr(dx), dxcs, _ptr(dx32), int(accum32), _ptr(dz_out), _stream())
+        REC.end(tok)
+        _lib.check(rc, "bn_backward_mask")
+        return
     fn = _lib_bound().cvb_bn_backward if _UNFUSED_BN else _lib_bound().cvb_bn_backward_fused
     tok = REC.begin((3 if (dx is not None or dx32 is not None) else 2) if _UNFUSED_BN else 1, "bn", 0, nb)
     rc = fn(dy.data_ptr(), dycs, x.data_ptr(), xcs, _ptr(y), ycs, rows, C, mean.data_ptr(),

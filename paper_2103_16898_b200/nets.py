@@ -28,6 +28,8 @@ from . import kernels as K
 BF16, F32 = torch.bfloat16, torch.float32
 _UNFUSED_HEAD = os.environ.get("CVB_UNFUSED_HEAD", "0") not in ("", "0")
 _NO_OVERLAP = os.environ.get("CVB_NO_OVERLAP", "0") not in ("", "0")
+# residual BN layers hand their ReLU mask to the backward as bits (A/B: CVB_NO_RELU_MASK=1 re-reads y)
+_RELU_MASK = not os.environ.get("CVB_NO_RELU_MASK") and not os.environ.get("CVB_BN_UNFUSED")
 
 
 class _nullctx:
@@ -209,6 +211,9 @@ class ConvBN:
         self.rstd = torch.zeros(self.cout, dtype=F32, device=device)
         self.run_mean = torch.zeros(self.cout, dtype=F32, device=device)
         self.run_var = torch.ones(self.cout, dtype=F32, device=device)
+        # residual layers keep y's ReLU mask as bits (rows x cout/8 bytes) for the backward instead
+        # of re-reading y (1/16 of the bytes); allocated on the first residual forward
+        self.mask = None
         self.wcount = self.cout * self.k * self.k * self.cin
         scratch.part_floats = max(scratch.part_floats, min(MAX_SPLITS * self.wcount, max(PART_CAP, 8 * self.wcount)))
         scratch.bn_floats = max(scratch.bn_floats, K._lib_bound().cvb_bn_workspace_floats(self.rows, self.cout))
@@ -228,9 +233,12 @@ class ConvBN:
         else:
             K.conv2d_fwd(x, ps.b[self.W], self.s, self.pad, out=self.z, cin=cin if cin is not None else self.cin,
                          acct_flops=self.flops)
+        if res is not None and self.relu and self.mask is None and _RELU_MASK:
+            self.mask = torch.empty(self.rows, self.cout // 8, dtype=torch.uint8, device=self.z.device)
         K.bn_forward(self.z, self.rows, self.cout, self.cout, self.scratch.bnws, self.mean, self.rstd, ps.p[self.G],
                      ps.p[self.B], out, out.shape[-1], out_coff, relu=self.relu, res=res,
-                     rcs=res.shape[-1] if res is not None else 0, run_mean=self.run_mean, run_var=self.run_var)
+                     rcs=res.shape[-1] if res is not None else 0, run_mean=self.run_mean, run_var=self.run_var,
+                     mask=self.mask if res is not None else None)
 
     def backward(self, ps: ParamStore, dout, x, dx=None, y=None, dres=None, dx_accumulate=False, cin=None,
                  dout_coff=0):
@@ -241,7 +249,8 @@ class ConvBN:
         dsrc = dout if dout_coff == 0 else dout[..., dout_coff:]
         K.bn_backward(dsrc, dcs, self.z, self.cout, self.rows, self.cout, self.mean, self.rstd, ps.p[self.G],
                       ps.p[self.B], self.scratch.bnws, ps.g[self.G], ps.g[self.B], relu=self.relu,
-                      y=y, ycs=y.shape[-1] if y is not None else 0, dx=self.dz, dxcs=self.cout, dz_out=dres)
+                      y=y if self.mask is None else None, ycs=y.shape[-1] if y is not None else 0, dx=self.dz,
+                      dxcs=self.cout, dz_out=dres, mask=self.mask if y is not None else None)
         if self.s2d:   # wgrad of the 4x4 s2d conv, mapped back onto the 7x7 weights
             count = self.cout * 16 * 4 * self.cin
             maxs = max(1, min(MAX_SPLITS, self.scratch.part.numel() // count))

@@ -286,3 +286,34 @@ def test_transpose_batched_matches_torch():
     desc2 = torch.tensor([[64 * j, 64 * j, 8, 8, 8, 8] for j in range(n)], dtype=torch.int64, device=dev).reshape(-1)
     K.transpose_batched(src2, dst2, desc2, n, 64, 0)
     assert torch.equal(dst2.view(n, 8, 8), src2.view(n, 8, 8).transpose(1, 2))
+
+
+@pytest.mark.parametrize("rows,C", [(512 * 32 * 32, 64), (3000, 128), (77, 512)])
+def test_bn_relu_mask_replaces_y(rows, C):
+    """Residual BN: the forward's ReLU mask bits equal (y > 0) of the stored bf16 y, and the
+    backward reading the mask is bit-identical to the backward reading y."""
+    g = torch.Generator(device=dev).manual_seed(rows * 3 + C)
+    z = (torch.randn(rows, C, device=dev, generator=g) * 1.5).bfloat16()
+    res = torch.randn(rows, C, device=dev, generator=g).bfloat16()
+    res[0, :8] = 0   # exact zeros around the ReLU edge
+    gamma = torch.rand(C, device=dev, generator=g) + 0.5
+    beta = torch.randn(C, device=dev, generator=g) * 0.1
+    mean, rstd, ws = torch.empty(C, device=dev), torch.empty(C, device=dev), K.bn_workspace(rows, C)
+    y = torch.empty(rows, C, device=dev, dtype=torch.bfloat16)
+    mask = torch.full((rows, C // 8), 0xA5, dtype=torch.uint8, device=dev)
+    K.bn_forward(z, rows, C, C, ws, mean, rstd, gamma, beta, y, C, relu=True, res=res, rcs=C, mask=mask)
+    y2 = torch.empty_like(y)
+    K.bn_forward(z, rows, C, C, ws, mean, rstd, gamma, beta, y2, C, relu=True, res=res, rcs=C)
+    assert torch.equal(y, y2)
+    bits = (y.view(rows, C // 8, 8) > 0).to(torch.int32) << torch.arange(8, device=dev, dtype=torch.int32)
+    assert torch.equal(bits.sum(-1).to(torch.uint8), mask)
+    dy = torch.randn(rows, C, device=dev, generator=g).bfloat16()
+    outs = []
+    for use_mask in (False, True):
+        dg, db = torch.empty(C, device=dev), torch.empty(C, device=dev)
+        dx, dres = torch.empty_like(z), torch.empty_like(z)
+        K.bn_backward(dy, C, z, C, rows, C, mean, rstd, gamma, beta, ws, dg, db, relu=True,
+                      y=None if use_mask else y, ycs=C, dx=dx, dxcs=C, dz_out=dres, mask=mask if use_mask else None)
+        outs.append((dg, db, dx, dres))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
