@@ -33,6 +33,14 @@ int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs, const v
 int cvb_conv2d_dgrad_s2(const void* dy, int n, int oh, int ow, int cout, int dycs, const void* w, int cin, int kh,
                         int kw, int pad, void* dx, int h, int wd, int dxcs, int accumulate, void* wscratch,
                         void* stream);
+/* dX of a 3x3 pad-1 stride-2 conv as two gather convs of dY, one per output ROW parity a, each
+   producing both column parities (N = 2*cin: dx[2i+a][2j+b][ci] as channel b*cin+ci of output
+   pixel (i, j)); dY taps (dh, dw): conv 0 (0,0) (0,1); conv 1 (0,0) (0,1) (1,0) (1,1).  wrows =
+   conv 0's [2cin][2][cout] then conv 1's [2cin][4][cout] bf16, rows (b, ci) of tap (dh, dw) =
+   w[co][a+1-2dh][b+1-2dw][ci], zero where that tap does not exist.  Needs dx [n][2oh][2ow][cin]
+   contiguous (dxcs == cin), else CVB_EINVAL without launching. */
+int cvb_conv2d_dgrad_s2_rows(const void* dy, int n, int oh, int ow, int cout, int dycs, int cin, void* dx, int h,
+                             int wd, int dxcs, int accumulate, const void* wrows, void* stream);
 int cvb_conv2d_wgrad(const void* dy, int n, int oh, int ow, int cout, int dycs, const void* x, int h, int w, int cin,
                      int xcs, int kh, int kw, int stride, int pad, float* part, int max_splits, int* splits_out,
                      void* stream);

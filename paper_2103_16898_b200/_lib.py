@@ -84,6 +84,7 @@ SIGNATURES = {
                                     _INT, _INT, _P, _INT, _INT, _INT, _INT, _P]),
     "cvb_bn_backward_fused": (_INT, [_P, _INT, _P, _INT, _P, _INT, _I64, _INT, _P, _P, _P, _P, _INT, _P, _P, _P, _P,
                                      _INT, _P, _INT, _P, _P]),
+    "cvb_conv2d_dgrad_s2_rows": (_INT, [_P, _INT, _INT, _INT, _INT, _INT, _INT, _P, _INT, _INT, _INT, _INT, _P, _P]),
     "cvb_bn_forward_mask": (_INT, [_P, _I64, _INT, _INT, _P, _P, _P, _c.c_float, _P, _P, _c.c_float, _P, _P, _P,
                                    _INT, _INT, _P, _INT, _INT, _P, _P]),
     "cvb_bn_backward_fused_mask": (_INT, [_P, _INT, _P, _INT, _P, _I64, _INT, _P, _P, _P, _P, _INT, _P, _P, _P, _P,

@@ -118,7 +118,8 @@ struct GemmParams {
   int two_cta;              // launched with two CTAs per SM (half the shared memory each)
   uint32_t stg_warp;        // staging bytes per epilogue warp (two buffers)
   int st_rows;              // valid rows of an M tile (multiple of 32); warps past it store nothing
-  int out_par;              // NHWC output is the parity sub-grid (out_ph, out_pw) of an out_H x out_W image
+  int out_par;              // 1: NHWC output is the parity sub-grid (out_ph, out_pw) of an out_H x out_W image;
+                            // 2: rows out_ph::2 only (every column) of an out_H x out_W image
   int out_ph, out_pw, out_H, out_W;
   CUtensorMap mapC;
   int dbg;                  // profiling knobs: 1 = skip MMA, 2 = skip TMA (results invalid)
@@ -1288,8 +1289,10 @@ int plan_tma_store(GemmParams& p) {
     }
     dims[0] = (uint64_t)(p.col_off + p.N); dims[1] = p.OW; dims[2] = p.OH; dims[3] = p.NIMG;
     st[0] = ld; st[1] = ld * p.OW; st[2] = ld * p.OW * p.OH;
-    if (p.out_par) {   // rows out_ph::2, cols out_pw::2 of the full image
+    if (p.out_par == 1) {   // rows out_ph::2, cols out_pw::2 of the full image
       st[0] = 2 * ld; st[1] = 2 * ld * p.out_W; st[2] = ld * p.out_W * p.out_H;
+    } else if (p.out_par == 2) {   // rows out_ph::2 of the full image
+      st[0] = ld; st[1] = 2 * ld * p.out_W; st[2] = ld * p.out_W * p.out_H;
     }
   } else if (p.out_mode == OUT_ROWS) {
     dims[0] = (uint64_t)(p.col_off + p.N); dims[1] = (uint64_t)p.M; dims[2] = 1; dims[3] = 1;
@@ -1303,7 +1306,7 @@ int plan_tma_store(GemmParams& p) {
   const int rowbytes = ch * es;
   void* base = p.out;
   if (p.out_mode == OUT_NHWC && p.out_par)
-    base = (char*)p.out + ((int64_t)p.out_ph * p.out_W + p.out_pw) * (int64_t)ld;
+    base = (char*)p.out + ((int64_t)p.out_ph * p.out_W + (p.out_par == 1 ? p.out_pw : 0)) * (int64_t)ld;
   CUresult r = g_encode(&p.mapC, p.out_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
                         base, dims, st, box, ones, CU_TENSOR_MAP_INTERLEAVE_NONE, swz_of(rowbytes),
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1779,11 +1782,11 @@ __global__ void dgrad_class_weights(const __nv_bfloat16* __restrict__ w, int cou
 // output through the parity view (ph, pw) of y [n][H][W][ycs].
 int plan_gather_conv(GemmParams& p, const void* x, int n, int h, int w, int cin, int xcs, const void* wt, int cout,
                      int ntaps, const int* dh, const int* dw, void* y, int H, int W, int ycs, int ph, int pw,
-                     int accumulate) {
+                     int accumulate, int rows_only = 0) {
   const int acel = pick_cel(cin);
   if (!acel || cout % 8) { cvb_set_error("dgrad: unsupported channels"); return CVB_EINVAL; }
   memset(&p, 0, sizeof(p));
-  const int oh = (H - ph + 1) / 2, ow = (W - pw + 1) / 2;
+  const int oh = (H - ph + 1) / 2, ow = rows_only ? W : (W - pw + 1) / 2;
   p.mode = MODE_FWD;
   p.a_cel = acel;
   p.b_cel = 64;
@@ -1822,7 +1825,7 @@ int plan_gather_conv(GemmParams& p, const void* x, int n, int h, int w, int cin,
   p.b_ptr = wt; p.b_rows = cout; p.b_cols = K; p.b_ld = K;
   p.out_mode = OUT_NHWC; p.out_f32 = 0; p.out = y; p.ldc = ycs; p.col_off = 0; p.bias = nullptr;
   p.accum = accumulate;
-  p.out_par = 1; p.out_ph = ph; p.out_pw = pw; p.out_H = H; p.out_W = W;
+  p.out_par = rows_only ? 2 : 1; p.out_ph = ph; p.out_pw = pw; p.out_H = H; p.out_W = W;
   plan_tma_store(p);
   if (!p.st_tma) { cvb_set_error("dgrad: parity class geometry needs direct stores"); return CVB_EINVAL; }
   return CVB_OK;
@@ -1877,6 +1880,37 @@ CVB_API int cvb_conv2d_dgrad_s2(const void* dy, int n, int oh, int ow, int cout,
       int rc = launch(plans[c], (cudaStream_t)stream);
       if (rc) return rc;
     }
+  return CVB_OK;
+}
+
+// dX of a 3x3 pad-1 stride-2 conv as TWO gather convs of dY, one per output ROW parity a, each
+// producing both column parities at once: output "pixel" (i, j) of conv a holds the 2*cin
+// channels (b, ci) = dx[2i + a][2j + b][ci] (adjacent in dx when dxcs == cin), so N = 2*cin
+// and the four parity classes' 9 taps become 2 + 4 tap boxes of dY (dh-major, dw in {0, 1}):
+//   conv 0: (dh, dw) = (0,0) (0,1);   conv 1: (0,0) (0,1) (1,0) (1,1)
+// with weight rows (b, ci) of tap (dh, dw) = w[co][a + 1 - 2dh][b + 1 - 2dw][ci] (zero where that
+// tap does not exist).  wrows = conv 0's [2cin][2][cout] then conv 1's [2cin][4][cout] bf16
+// (written by cvb_transpose_batched jobs; the zero entries stay zero).  Against the four class
+// convs (N = cin): half the dY box loads per output element and twice the MMA width.
+CVB_API int cvb_conv2d_dgrad_s2_rows(const void* dy, int n, int oh, int ow, int cout, int dycs, int cin, void* dx,
+                                     int h, int wd, int dxcs, int accumulate, const void* wrows, void* stream) {
+  if (get_encoder()) return CVB_ECUDA;
+  if (dxcs != cin || h != 2 * oh || wd != 2 * ow || cin % 8) {
+    cvb_set_error("dgrad_s2_rows: needs dx [n][2oh][2ow][cin] contiguous");
+    return CVB_EINVAL;
+  }
+  static GemmParams plans[2];
+  static const int dh0[2] = {0, 0}, dw0[2] = {0, 1};
+  static const int dh1[4] = {0, 0, 1, 1}, dw1[4] = {0, 1, 0, 1};
+  const void* w1 = (const char*)wrows + (size_t)2 * cin * 2 * cout * 2;
+  int rc = plan_gather_conv(plans[0], dy, n, oh, ow, cout, dycs, wrows, 2 * cin, 2, dh0, dw0, dx, h, ow, 2 * dxcs, 0, 0,
+                            accumulate, 1);
+  if (rc) return rc;
+  rc = plan_gather_conv(plans[1], dy, n, oh, ow, cout, dycs, w1, 2 * cin, 4, dh1, dw1, dx, h, ow, 2 * dxcs, 1, 0,
+                        accumulate, 1);
+  if (rc) return rc;
+  for (int a = 0; a < 2; a++)
+    if ((rc = launch(plans[a], (cudaStream_t)stream))) return rc;
   return CVB_OK;
 }
 

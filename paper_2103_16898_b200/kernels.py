@@ -75,7 +75,7 @@ def _stream():
 
 # launch entry point -> kernel class (the roofline / per-class timing vocabulary of bench.py)
 LAUNCH_CLASS = {
-    **{n: "umma_gemm" for n in ("cvb_conv2d_fwd", "cvb_conv2d_wgrad", "cvb_gemm", "cvb_gemm_ex",
+    **{n: "umma_gemm" for n in ("cvb_conv2d_dgrad_s2_rows", "cvb_conv2d_fwd", "cvb_conv2d_wgrad", "cvb_gemm", "cvb_gemm_ex",
                                 "cvb_conv2d_dgrad_s2")},
     **{n: "bn" for n in ("cvb_bn_stats", "cvb_bn_forward", "cvb_bn_forward_range", "cvb_bn_apply", "cvb_bn_backward",
                          "cvb_bn_backward_fused", "cvb_bn_gather_dx", "cvb_bn_forward_mask",
@@ -95,6 +95,10 @@ LAUNCH_CLASS = {
 # become no-ops, so a CUDA graph captured under the filter replays exactly that class's
 # kernels of a step -- their in-graph time without the rest of the step in between.
 ONLY_CLASSES = None
+# Measurement only (scripts/graph_layer_times.py): with ONLY_CLASSES set, keep just the
+# ONLY_INDEX-th launch call of the kept classes (ONLY_SEEN counts and names the calls).
+ONLY_INDEX = None
+ONLY_SEEN = []
 
 
 class _ClassFilter:
@@ -103,8 +107,14 @@ class _ClassFilter:
 
     def __getattr__(self, name):
         cls = LAUNCH_CLASS.get(name)
-        if cls is None or cls in self._keep:
+        if cls is None:
             return getattr(self._lib, name)
+        if cls in self._keep:
+            if ONLY_INDEX is None:
+                return getattr(self._lib, name)
+            ONLY_SEEN.append(name)
+            if len(ONLY_SEEN) - 1 == ONLY_INDEX:
+                return getattr(self._lib, name)
         return lambda *args: 0
 
 
@@ -170,6 +180,46 @@ def conv2d_dgrad_s2(dy, w, pad, dx, accumulate=False, wscratch=None, acct_flops=
     if rc == -1:
         return False
     _lib.check(rc, "conv2d_dgrad_s2")
+    return True
+
+
+# cvb_conv2d_dgrad_s2_rows: the dY taps (dh, dw) of the two row-parity convs (3x3, pad 1)
+DGRAD_S2_ROW_TAPS = ([(0, 0), (0, 1)], [(0, 0), (0, 1), (1, 0), (1, 1)])
+
+
+def dgrad_s2_row_jobs(w_off, kh, kw, cin, cout, pad, dst_off):
+    """Transpose jobs {src, dst, rows, cols, src ld, dst ld} writing the row-parity weight
+    matrices of cvb_conv2d_dgrad_s2_rows (rows (b, ci) of tap (dh, dw) = w[co][a + pad - 2dh]
+    [b + pad - 2dw][ci]) from w [cout][kh][kw][cin] at w_off into a ZEROED buffer at dst_off
+    (12 * cin * cout elements; taps that do not exist stay zero)."""
+    jobs, off = [], dst_off
+    for a, taps in enumerate(DGRAD_S2_ROW_TAPS):
+        nt = len(taps)
+        for t, (dh, dw) in enumerate(taps):
+            for b in (0, 1):
+                y, x = a + pad - 2 * dh, b + pad - 2 * dw
+                if 0 <= y < kh and 0 <= x < kw:
+                    jobs += [w_off + (y * kw + x) * cin, off + b * cin * nt * cout + t * cout, cout, cin,
+                             kh * kw * cin, nt * cout]
+        off += 2 * cin * nt * cout
+    return jobs
+
+
+def conv2d_dgrad_s2_rows(dy, wrows, cin, dx, accumulate=False, acct_flops=None):
+    """dX of a 3x3 pad-1 stride-2 conv as two row-parity gather convs (csrc/umma_gemm.cu
+    cvb_conv2d_dgrad_s2_rows) from the weights dgrad_s2_row_jobs wrote.  Returns False,
+    launching nothing, when dx is not [n][2oh][2ow][cin] contiguous."""
+    n, oh, ow, cout = dy.shape
+    _, h, wd, dcs = dx.shape
+    nbytes = 2 * (dy.numel() + 9 * cin * cout + n * h * wd * cin * (2 if accumulate else 1))
+    tok = REC.begin(2, "umma_gemm", acct_flops if acct_flops is not None else 2 * n * h * wd * cout * 9 * cin // 4,
+                    nbytes)
+    rc = _lib_bound().cvb_conv2d_dgrad_s2_rows(dy.data_ptr(), n, oh, ow, cout, dy.stride(2), cin, dx.data_ptr(), h, wd,
+                                               dx.stride(2), int(accumulate), wrows.data_ptr(), _stream())
+    REC.end(tok)
+    if rc == -1:
+        return False
+    _lib.check(rc, "conv2d_dgrad_s2_rows")
     return True
 
 

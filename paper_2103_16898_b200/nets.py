@@ -30,6 +30,8 @@ _UNFUSED_HEAD = os.environ.get("CVB_UNFUSED_HEAD", "0") not in ("", "0")
 _NO_OVERLAP = os.environ.get("CVB_NO_OVERLAP", "0") not in ("", "0")
 # residual BN layers hand their ReLU mask to the backward as bits (A/B: CVB_NO_RELU_MASK=1 re-reads y)
 _RELU_MASK = not os.environ.get("CVB_NO_RELU_MASK") and not os.environ.get("CVB_BN_UNFUSED")
+# 3x3 stride-2 dgrads as two row-parity convs (A/B: CVB_NO_DGRAD_ROWS=1 keeps the four parity classes)
+_DGRAD_ROWS = not os.environ.get("CVB_NO_DGRAD_ROWS")
 
 
 class _nullctx:
@@ -76,6 +78,12 @@ class ParamStore:
         (csrc/umma_gemm.cu cvb_conv2d_dgrad_s2 layout), refreshed by the same batched launch."""
         if name not in dict(getattr(self, "class_names", [])):
             self.class_names = getattr(self, "class_names", []) + [(name, pad)]
+
+    def want_row_weights(self, name, pad):
+        """Keep the row-parity weight matrices of a 3x3 pad-1 stride-2 conv (cvb_conv2d_dgrad_s2_rows
+        layout), refreshed by the same batched launch."""
+        if name not in dict(getattr(self, "row_names", [])):
+            self.row_names = getattr(self, "row_names", []) + [(name, pad)]
 
     def flip_all(self):
         if self.flip_n:
@@ -130,11 +138,20 @@ class ParamStore:
             self.cw[name] = (foff, (n,))
             foff += (n + ALIGN - 1) // ALIGN * ALIGN
             self.flip_max = max(self.flip_max, cout * cin)
+        self.rw = {}
+        for name, pad in getattr(self, "row_names", []):
+            cout, kh, kw, cin = shapes[name]
+            desc += K.dgrad_s2_row_jobs(offs[name], kh, kw, cin, cout, pad, foff)
+            self.rw[name] = (foff, (12 * cin * cout,))
+            foff += (12 * cin * cout + ALIGN - 1) // ALIGN * ALIGN
+            self.flip_max = max(self.flip_max, cout * cin)
         self.fb = torch.zeros(max(1, foff), dtype=BF16, device=device)
         for name, (o, shp) in list(self.f.items()):
             self.f[name] = self.fb[o:o + math.prod(shp)].view(shp)
         for name, (o, shp) in list(self.cw.items()):
             self.cw[name] = self.fb[o:o + shp[0]]
+        for name, (o, shp) in list(self.rw.items()):
+            self.rw[name] = self.fb[o:o + shp[0]]
         self.flip_n = len(desc) // 6
         self.flip_bytes = 4 * foff
         self.flip_desc = torch.tensor(desc if desc else [0], dtype=torch.int64, device=device)
@@ -193,6 +210,8 @@ class ConvBN:
             ps.want_flip(self.W)
         elif need_dgrad and stride == 2:
             ps.want_class_weights(self.W, pad)
+            if k == 3 and pad == 1 and _DGRAD_ROWS:
+                ps.want_row_weights(self.W, pad)
         self.G = ps.add(f"{name}.gamma", torch.ones(cout))
         self.B = ps.add(f"{name}.beta", torch.zeros(cout))
 
@@ -280,6 +299,10 @@ class ConvBN:
             ps.grad_ready(self.W, self.G, self.B)
         if dx is not None:
             wt = self.scratch.flip[:self.cout * self.k * self.k * cin].view(cin, self.k, self.k, self.cout)
+            if self.s == 2 and cin == self.cin and self.W in getattr(ps, "rw", {}):
+                if K.conv2d_dgrad_s2_rows(self.dz, ps.rw[self.W], cin, dx, accumulate=dx_accumulate,
+                                          acct_flops=self.flops):
+                    return
             if self.s == 2 and cin == self.cin:
                 ready = self.W in ps.cw   # class weights refreshed by ParamStore.flip_all
                 if K.conv2d_dgrad_s2(self.dz, ps.b[self.W], self.pad, dx, accumulate=dx_accumulate,

@@ -235,3 +235,31 @@ def test_dgrad_s2_with_batched_class_weights(cin, cout, k, p):
     dx = torch.zeros_like(dx_ref)
     assert K.conv2d_dgrad_s2(dy, wt, p, dx, accumulate=acc, wscratch=cw, class_weights_ready=True)
     assert torch.equal(dx, dx_ref)
+
+
+@pytest.mark.parametrize("n,h,cin,cout", [(8, 32, 64, 128), (8, 16, 128, 256), (16, 8, 256, 512), (4, 32, 32, 64)])
+@pytest.mark.parametrize("acc", [False, True])
+def test_dgrad_s2_rows_matches_torch(n, h, cin, cout, acc):
+    """3x3 pad-1 stride-2 dgrad as two row-parity convs (cvb_conv2d_dgrad_s2_rows, weights from
+    the batched transpose jobs) vs the fp32 transposed convolution; accumulate adds into dx."""
+    g = torch.Generator(device="cuda").manual_seed(n + h + cin + cout)
+    wt = (torch.randn(cout, 3, 3, cin, device="cuda", generator=g) / (9 * cin) ** 0.5).to(torch.bfloat16)
+    oh = h // 2
+    dy = torch.randn(n, oh, oh, cout, device="cuda", generator=g).to(torch.bfloat16)
+    wrows = torch.zeros(12 * cin * cout, device="cuda", dtype=torch.bfloat16)
+    desc = K.dgrad_s2_row_jobs(0, 3, 3, cin, cout, 1, 0)
+    K.transpose_batched(wt.reshape(-1), wrows, torch.tensor(desc, dtype=torch.int64, device="cuda"), len(desc) // 6,
+                        cout * cin, 0)
+    base = torch.randn(n, h, h, cin, device="cuda", generator=g).to(torch.bfloat16)
+    dx = base.clone() if acc else torch.zeros_like(base)
+    assert K.conv2d_dgrad_s2_rows(dy, wrows, cin, dx, accumulate=acc)
+    ref = torch.nn.functional.conv_transpose2d(dy.permute(0, 3, 1, 2).float(), wt.permute(0, 3, 1, 2).float(),
+                                               stride=2, padding=1, output_padding=1).permute(0, 2, 3, 1)
+    if acc:
+        ref = ref + base.float()
+    err = (dx.float() - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 8e-3, err
+    # against the four-class form on the same inputs (same products, other summation order)
+    dxc = base.clone() if acc else torch.zeros_like(base)
+    assert K.conv2d_dgrad_s2(dy, wt, 1, dxc, accumulate=acc)
+    assert (dx.float() - dxc.float()).abs().max().item() / ref.abs().max().item() < 8e-3
