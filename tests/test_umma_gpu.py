@@ -58,6 +58,10 @@ CONV_CASES = [
     (3, 16, 8, 128, 128, 3, 1, 1),
     (2, 32, 16, 128, 256, 3, 1, 1),
     (2, 16, 16, 192, 64, 3, 1, 1),
+    # 1x1 stride-1 convs as plain row GEMMs: DenseNet widths, a partial last row tile, 32 channels
+    (2, 56, 56, 64, 128, 1, 1, 0),
+    (3, 7, 7, 512, 128, 1, 1, 0),
+    (1, 10, 10, 32, 96, 1, 1, 0),
 ]
 
 
@@ -81,6 +85,22 @@ def test_conv_fwd_channel_slices():
     K.conv2d_fwd(x_full, wt, 1, 1, out=out, cin=96, out_coff=64)
     _close(out[..., 64:96], _ref_conv(x_full[..., :96].contiguous(), wt, 1, 1), tol=1e-2)
     assert out[..., :64].abs().max().item() == 0 and out[..., 96:].abs().max().item() == 0
+
+
+@pytest.mark.parametrize("acc", [False, True])
+def test_conv1x1_row_gemm_slices(acc):
+    # 1x1 conv (row-GEMM plan) reading channels [0, cin) of a wider buffer and writing / adding
+    # at a channel offset of another
+    g = torch.Generator(device="cuda").manual_seed(5 + acc)
+    x_full = torch.randn(2, 28, 28, 192, device="cuda", generator=g).to(torch.bfloat16)
+    wt = (torch.randn(128, 1, 1, 160, device="cuda", generator=g) * 0.1).to(torch.bfloat16)
+    base = torch.randn(2, 28, 28, 256, device="cuda", generator=g)
+    out = base.clone() if acc else torch.zeros_like(base)
+    K.conv2d_fwd(x_full, wt, 1, 0, out=out, out_f32=True, cin=160, out_coff=64, accumulate=acc)
+    ref = _ref_conv(x_full[..., :160].contiguous(), wt, 1, 0)
+    _close(out[..., 64:192] - (base[..., 64:192] if acc else 0), ref)
+    want_rest = base if acc else torch.zeros_like(base)
+    assert torch.equal(out[..., :64], want_rest[..., :64]) and torch.equal(out[..., 192:], want_rest[..., 192:])
 
 
 @pytest.mark.parametrize("k,p", [(3, 1), (4, 2)])
