@@ -536,12 +536,16 @@ __device__ __forceinline__ void release_acc_t(uint32_t tempty0, int acc) {
 // PAIR = 1: CTA-pair instantiation (MODE_FWD with streamed weights only; see the cta_group::2
 // helpers above).  Every tcgen05 instruction of a kernel must use one cta_group, hence the
 // separate instantiation.
-template <int PAIR>
+// MODE: the kernel is instantiated per GEMM mode (code of the other modes is dead and dropped):
+// the single all-mode kernel was ~150 KB of SASS and its epilogue / issue loops stalled on
+// instruction fetch (ncu: "no instruction" stalls; ~1,800 cycles per short-K tile epilogue).
+#define PMODE (MODE)
+template <int PAIR, int MODE>
 __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_constant__ GemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t a_stage = p.a_stage_bytes;         // 16 KB (halo mode: planes * plane stride)
-  const uint32_t b_stage = (p.b_res || p.hs) ? 0u : (p.b_stage_bytes ? p.b_stage_bytes : p.BN * p.kr * 2);
+  const uint32_t b_stage = (p.b_res || (PMODE == MODE_HALO && p.hs)) ? 0u : (p.b_stage_bytes ? p.b_stage_bytes : p.BN * p.kr * 2);
   const uint32_t stage_bytes = a_stage + b_stage;
   const uint32_t b_kb_bytes = p.BN * BK * 2;        // resident B: one K-block slab
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes + p.b_res_bytes +
@@ -630,7 +634,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       const int sp = (int)p.fd_n.div((uint32_t)rest), nt = rest - sp * p.n_tiles;
       const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
       int tw0 = 0, th0 = 0, tn0 = 0;
-      if (p.mode == MODE_FWD || p.mode == MODE_HALO) {
+      if (PMODE == MODE_FWD || PMODE == MODE_HALO) {
         const int r2 = (int)p.fd_pw.div((uint32_t)mt), r3 = (int)p.fd_ph.div((uint32_t)r2);
         tw0 = (mt - r2 * p.ptiles_w) * p.tw;
         th0 = (r2 - r3 * p.ptiles_h) * p.th;
@@ -638,14 +642,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       }
       // WGRAD: K-block kb is a pixel box; walk it incrementally
       int pw = 0, ph0 = 0, pn = 0;
-      if (p.mode == MODE_WGRAD) {
+      if (PMODE == MODE_WGRAD) {
         pw = (kb0 % p.ptiles_w) * p.tw;
         const int r2 = kb0 / p.ptiles_w;
         ph0 = (r2 % p.ptiles_h) * p.th;
         pn = (r2 / p.ptiles_h) * p.tn;
       }
       const int m0 = mt * BM, n0 = nt * p.BN;
-      if (p.hs) {   // per channel group: the halo (3 kw boxes), then the 9 taps' weight boxes
+      if ((PMODE == MODE_HALO && p.hs)) {   // per channel group: the halo (3 kw boxes), then the 9 taps' weight boxes
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait_lazy(&empty[s], ph ^ 1, false);
           if (leader) {
@@ -689,10 +693,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       // rows are never stored.
       int ga_eff = p.ga;
       uint32_t tx = p.tx_bytes;
-      if (p.mode == MODE_WGRAD) {
+      if (PMODE == MODE_WGRAD) {
         ga_eff = min(p.ga, (p.M - m0 + p.a_cel - 1) / p.a_cel);
         tx = p.tx_bytes - (uint32_t)(p.ga - ga_eff) * p.a_box_bytes;
-        if (p.w_pair) { ga_eff = p.w_pair == 2 ? 2 : 1; tx = p.tx_bytes; }   // kh-paired / kh-quad dY boxes
+        if ((PMODE == MODE_WGRAD ? p.w_pair : 0)) { ga_eff = (PMODE == MODE_WGRAD ? p.w_pair : 0) == 2 ? 2 : 1; tx = p.tx_bytes; }   // kh-paired / kh-quad dY boxes
       }
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
         mbar_wait_lazy(&empty[s], ph ^ 1, (p.dbg & 256) != 0);
@@ -703,7 +707,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
             // both CTAs' boxes complete on the leader's barrier; the leader expects both halves
             const uint32_t bar_c = mapa_rank0(smem_u32(&full[s]));
             if (rank == 0) mbar_expect_tx(&full[s], 2u * tx);
-            if (p.mode == MODE_WGRAD) {   // own 128 Cout rows of dY, this CTA's half of the input boxes
+            if (PMODE == MODE_WGRAD) {   // own 128 Cout rows of dY, this CTA's half of the input boxes
               for (int b = 0; b < p.ga; b++)
                 tma_load_4d_pair(&p.mapA[0], sa + b * p.a_box_stride, bar_c, m0 + b * p.a_cel, pw, ph0, pn);
               const int gh = p.gb >> 1;
@@ -713,9 +717,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
                 tma_load_4d_pair(&p.mapB[e & 3], sb + j * p.b_box_stride, bar_c, (int)((e >> 2) & 0xFFFF),
                                  pw + (int)((e >> 18) & 127) - 64, ph0 + (int)(e >> 25) - 64, pn);
               }
-            } else if (p.mode == MODE_HALO) {   // this CTA's halo tile (weights are resident)
+            } else if (PMODE == MODE_HALO) {   // this CTA's halo tile (weights are resident)
               for (int j = 0; j < p.h_planes; j++) {
-                if (p.h_kwbox)
+                if ((PMODE == MODE_HALO && p.h_kwbox))
                   tma_load_4d_pair(&p.mapA[0], sa + j * p.h_plane_stride, bar_c, kb * p.h_cg, tw0 - p.h_pad + j,
                                    th0 - p.h_pad, tn0);
                 else
@@ -737,8 +741,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
             mbar_arrive(&full[s]);
           } else {
             mbar_expect_tx(&full[s], tx);
-            if (p.mode == MODE_HALO) {
-              if (p.h_kwbox) {
+            if (PMODE == MODE_HALO) {
+              if ((PMODE == MODE_HALO && p.h_kwbox)) {
                 for (int j = 0; j < p.h_planes; j++)
                   tma_load_4d(&p.mapA[0], sa + j * p.h_plane_stride, &full[s], kb * p.h_cg, tw0 - p.h_pad + j,
                               th0 - p.h_pad, tn0);
@@ -747,7 +751,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
                   tma_load_4d(&p.mapA[0], sa + j * p.h_plane_stride, &full[s], kb * p.h_cg + 8 * j, tw0 - p.h_pad,
                               th0 - p.h_pad, tn0);
               }
-            } else if (p.mode == MODE_FWD) {
+            } else if (PMODE == MODE_FWD) {
               const uint32_t* tab = p.boxtab + kb * p.ga;
               for (int g = 0; g < p.ga; g++) {
                 const uint32_t e = tab[g];
@@ -757,14 +761,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
               if (!p.b_res)
                 for (int g = 0; g < p.gb; g++)
                   tma_load_2d(&p.mapB[0], sb + g * p.b_box_stride, &full[s], kb * BK + g * p.b_cel, n0);
-            } else if (p.mode == MODE_WGRAD) {
-              if (p.w_pair == 2) {   // M atom 0 = dY rows one up (kh 2t+1), atom 1 = dY rows (kh 2t)
+            } else if (PMODE == MODE_WGRAD) {
+              if ((PMODE == MODE_WGRAD ? p.w_pair : 0) == 2) {   // M atom 0 = dY rows one up (kh 2t+1), atom 1 = dY rows (kh 2t)
                 for (int b = 0; b < 2; b++)
                   tma_load_4d(&p.mapA[0], sa + b * p.a_box_stride, &full[s], 0, pw, ph0 - 1 + b, pn);
               } else {
                 for (int b = 0; b < ga_eff; b++)
                   tma_load_4d(&p.mapA[0], sa + b * p.a_box_stride, &full[s], m0 + b * p.a_cel, pw,
-                              p.w_pair == 3 ? ph0 - (p.w_kh - 1) : p.w_pair ? ph0 - 1 : ph0, pn);
+                              (PMODE == MODE_WGRAD ? p.w_pair : 0) == 3 ? ph0 - (p.w_kh - 1) : (PMODE == MODE_WGRAD ? p.w_pair : 0) ? ph0 - 1 : ph0, pn);
               }
               const uint32_t* tab = p.boxtab + nt * p.gb;
               for (int j = 0; j < p.gb; j++) {
@@ -785,7 +789,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           }
         }
         __syncwarp();
-        if (p.mode == MODE_WGRAD) {
+        if (PMODE == MODE_WGRAD) {
           pw += p.tw;
           if (pw >= p.ptiles_w * p.tw) {
             pw = 0;
@@ -831,7 +835,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
       if ((p.dbg & 32) && !(p.dbg & 64) && leader) TRACE(0, it);   // debug: slot 0 = accumulator wait passed
       tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * p.BN;
-      if (p.hs) {
+      if ((PMODE == MODE_HALO && p.hs)) {
         // per channel group: wait the halo, then per tap the weight box -> 4 MMAs (64 channels),
         // the tap's A start = kw box + kh KB (aligned SW128 starts, as in halo_kw_issue)
         uint32_t acc_flag = 0u;
@@ -898,7 +902,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           if (leader) mbar_arrive(&empty[s]);
         } else {
           const uint64_t sa = (smem0 + s * stage_bytes) >> 4;
-          if (p.mode == MODE_HALO) {
+          if (PMODE == MODE_HALO) {
             {
             // every tap of this channel group reads the same halo planes at a row offset.
             // Offsets are plain uniform arithmetic (no table loads: with N = 64 an MMA is
@@ -911,8 +915,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
             uint32_t acc_flag = kb > kb0 ? 1u : 0u;
             const int geo = p.h_kh * 100 + p.h_kw * 10 + (int)nj;
             const uint32_t box16 = p.h_plane_stride >> 4;
-            if (p.h_kwbox && geo == 334) halo_kw_issue<3, 3, 4, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16, box16);
-            else if (p.h_kwbox && geo == 332) halo_kw_issue<3, 3, 2, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16, box16);
+            if ((PMODE == MODE_HALO && p.h_kwbox) && geo == 334) halo_kw_issue<3, 3, 4, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16, box16);
+            else if ((PMODE == MODE_HALO && p.h_kwbox) && geo == 332) halo_kw_issue<3, 3, 2, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16, box16);
             else if (p.h_cg == 8) halo8_issue<3, 3, PAIR>(tmem_d, a0, p.adesc[1] + sa, b0, p.idesc, leader, slab16);
             else if (p.h_pitch == 16 && p.h_rowpad && geo == 332) halo_rows_issue_t<3, 3, 2, 8, 16, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
             else if (p.h_pitch == 16 && p.h_rowpad && geo == 442) halo_rows_issue_t<4, 4, 2, 8, 16, PAIR>(tmem_d, a0, b0, p.idesc, acc_flag, leader, kb, cin16, slab16);
@@ -1007,7 +1011,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
         const int m = mt * BM + row;
         valid = m < p.M;
         dst_row = m;
-      } else if (p.w_pair) {
+      } else if ((PMODE == MODE_WGRAD ? p.w_pair : 0)) {
         valid = 2 * nt + (quarter < 2 ? 1 : 0) < p.w_kh;
         dst_row = (int64_t)sp * p.part_rows + (row & 63);
       } else {
@@ -1038,22 +1042,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
         }
         // kh-paired wgrad: lane quarters 0-1 hold kh 2nt+1, quarters 2-3 kh 2nt, both for Cout 0..63;
         // kh-quad (Cout 32): lane quarter q holds kh = KH-1-q (q = KH.. unused), channel group nt
-        const int pair_kh = p.w_pair == 3 ? p.w_kh - 1 - quarter : 2 * nt + (quarter < 2 ? 1 : 0);
-        const int colbase = p.w_pair ? pair_kh * p.BN : nt * p.BN;
-        if (p.w_pair) c1 = p.w_pair == 3 ? 0 : (quarter & 1) * 32;
+        const int pair_kh = (PMODE == MODE_WGRAD ? p.w_pair : 0) == 3 ? p.w_kh - 1 - quarter : 2 * nt + (quarter < 2 ? 1 : 0);
+        const int colbase = (PMODE == MODE_WGRAD ? p.w_pair : 0) ? pair_kh * p.BN : nt * p.BN;
+        if ((PMODE == MODE_WGRAD ? p.w_pair : 0)) c1 = (PMODE == MODE_WGRAD ? p.w_pair : 0) == 3 ? 0 : (quarter & 1) * 32;
         const uint32_t stg = smem0 + p.stg_off + (uint32_t)(warp - 2) * p.stg_warp;
         const int span = p.n_epi == 8 && !p.epi_alt ? p.BN >> 1 : p.BN;   // columns this warp stores
         const int cbeg = p.n_epi == 8 && !p.epi_alt && warp >= 6 ? span : 0;
-        const bool rows_real = p.w_pair ? (pair_kh >= 0 && pair_kh < p.w_kh) : quarter * 32 < p.st_rows;
+        const bool rows_real = (PMODE == MODE_WGRAD ? p.w_pair : 0) ? (pair_kh >= 0 && pair_kh < p.w_kh) : quarter * 32 < p.st_rows;
         const int cend = rows_real ? cbeg + span : cbeg;   // short tile: nothing to store
         const bool one_chunk = span <= p.st_ch;
         bool released = false;
         for (int c = cbeg; c < cend; c += p.st_ch, ++stg_it) {
-          if (p.w_halo && (c & 63) >= p.w_cin) { --stg_it; continue; }   // zero-fill channels: nothing to store
+          if ((PMODE == MODE_WGRAD && p.w_halo) && (c & 63) >= p.w_cin) { --stg_it; continue; }   // zero-fill channels: nothing to store
           const uint32_t buf = stg + (stg_it & 1) * (p.stg_warp >> 1);
           // TMEM first: a single-chunk tile hands its accumulator back to the MMA warp before
           // waiting for the staging buffer
           uint32_t r[64];
+          if (warp == 2 && lane == 0 && (p.dbg & 8192)) TRACE(6, lt);   // debug: before the TMEM load
           if (p.st_ch == 64) { tmem_ld32(tbase + c, *reinterpret_cast<uint32_t(*)[32]>(r));
                                tmem_ld32(tbase + c + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32)); }
           else if (p.st_ch == 32) tmem_ld32(tbase + c, *reinterpret_cast<uint32_t(*)[32]>(r));
@@ -1068,14 +1073,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           }
           if (lane == 0) bulk_wait_read1();        // the store that last used this buffer has read it
           __syncwarp();
-          if (warp == 2 && lane == 0) TRACE(6, lt);
+          if (warp == 2 && lane == 0 && !(p.dbg & 8192)) TRACE(6, lt);
           if (p.st_ch == 8) {   // 8 fp32 columns (32-byte rows): zero-padded 8-channel halo wgrad
             const uint32_t off0 = (uint32_t)lane * 32u, off1 = off0 + 16u;
             st_shared_v4(buf + (off0 ^ (((off0 >> 7) & p.st_swz) << 4)), has_k ? r[0] : 0u, has_k ? r[1] : 0u,
                          has_k ? r[2] : 0u, has_k ? r[3] : 0u);
             st_shared_v4(buf + (off1 ^ (((off1 >> 7) & p.st_swz) << 4)), has_k ? r[4] : 0u, has_k ? r[5] : 0u,
                          has_k ? r[6] : 0u, has_k ? r[7] : 0u);
-          } else {
+          } else if (!(p.dbg & 4096)) {   // knob 4096: no staging (profiling, results invalid)
 #pragma unroll
           for (int cc = 0; cc < 64; cc += 16)
             if (cc < p.st_ch) stage16(p, buf, lane, cc, nt * p.BN + c + cc, r + cc, has_k);
@@ -1084,12 +1089,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           __syncwarp();
           if (lane == 0) {
             int c0 = p.col_off + colbase + c;
-            if (p.w_halo) {   // halo wgrad tile: 64-column kw segments of the [kh][kw][cin] output row
-              const int khh = p.w_pair ? pair_kh : nt / p.w_groups;
-              const int gg = p.w_pair == 3 ? nt : p.w_pair ? 0 : nt - (nt / p.w_groups) * p.w_groups;
+            if ((PMODE == MODE_WGRAD && p.w_halo)) {   // halo wgrad tile: 64-column kw segments of the [kh][kw][cin] output row
+              const int khh = (PMODE == MODE_WGRAD ? p.w_pair : 0) ? pair_kh : nt / p.w_groups;
+              const int gg = (PMODE == MODE_WGRAD ? p.w_pair : 0) == 3 ? nt : (PMODE == MODE_WGRAD ? p.w_pair : 0) ? 0 : nt - (nt / p.w_groups) * p.w_groups;
               c0 = (khh * p.h_kw + (c >> 6)) * p.w_cin + gg * 64 + (c & 63);
             }
-            if (p.accum) tma_red_add_4d(&p.mapC, buf, c0, c1, c2, c3);
+            if (p.dbg & 2048) {   // profiling knob: no output store (results invalid)
+            } else if (p.accum) tma_red_add_4d(&p.mapC, buf, c0, c1, c2, c3);
             else tma_store_4d(&p.mapC, buf, c0, c1, c2, c3);
             bulk_commit();
           }
@@ -1104,7 +1110,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
         continue;
       }
       const int64_t rowoff = dst_row * p.ldc + p.col_off +
-                             (p.w_pair ? (2 * nt + (quarter < 2 ? 1 : 0)) * p.BN : nt * p.BN);
+                             ((PMODE == MODE_WGRAD ? p.w_pair : 0) ? (2 * nt + (quarter < 2 ? 1 : 0)) * p.BN : nt * p.BN);
       int c = 0;
       for (; c + 32 <= p.BN; c += 32) {
         uint32_t r[32];
@@ -1137,6 +1143,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
     if (PAIR) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
     else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
   }
+}
+#undef PMODE
+
+using GemmKernel = void (*)(const GemmParams);
+GemmKernel kernel_for(int pair, int mode) {
+  static const GemmKernel k[2][4] = {
+      {umma_gemm_kernel<0, MODE_FWD>, umma_gemm_kernel<0, MODE_WGRAD>, umma_gemm_kernel<0, MODE_DENSE>,
+       umma_gemm_kernel<0, MODE_HALO>},
+      {umma_gemm_kernel<1, MODE_FWD>, umma_gemm_kernel<1, MODE_WGRAD>, umma_gemm_kernel<1, MODE_DENSE>,
+       umma_gemm_kernel<1, MODE_HALO>}};
+  return k[pair ? 1 : 0][mode & 3];
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1446,8 +1463,9 @@ int launch(GemmParams& p, cudaStream_t stream) {
   p.stg_off = (uint32_t)p.stages * stage_bytes + p.b_res_bytes;   // 1024-aligned (stages, slabs are)
   size_t smem = (size_t)p.stages * stage_bytes + p.b_res_bytes + stg + 1024 + 512;   // barriers: 64 words
   if (cvb_first_on_device(&g_attr_done)) {
-    CVB_CUDA(cudaFuncSetAttribute(umma_gemm_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    CVB_CUDA(cudaFuncSetAttribute(umma_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    for (int m = 0; m < 4; m++)
+      for (int pr = 0; pr < 2; pr++)
+        CVB_CUDA(cudaFuncSetAttribute(kernel_for(pr, m), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   }
   p.idesc = make_idesc(p.a_major, p.b_major, p.BN, p.pair ? 2 * BM : BM);
   // smem box strides and descriptor templates
@@ -1505,9 +1523,9 @@ int launch(GemmParams& p, cudaStream_t stream) {
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = cvb_pdl_enabled() ? 2 : 1;
-    cudaLaunchKernelEx(&cfg, umma_gemm_kernel<1>, p);
+    cudaLaunchKernelEx(&cfg, kernel_for(1, p.mode), p);
   } else {
-    cvb_launch(umma_gemm_kernel<0>, grid, (2 + p.n_epi) * 32, smem, stream, p);
+    cvb_launch(kernel_for(0, p.mode), grid, (2 + p.n_epi) * 32, smem, stream, p);
   }
   CVB_CHECK_LAUNCH();
   return CVB_OK;
