@@ -385,9 +385,31 @@ __device__ __forceinline__ void store16(const GemmParams& p, int64_t off, int co
   }
 }
 
+// Loop-invariant epilogue parameters, copied once into registers through opaque movs: left to
+// the compiler they are re-loaded from the kernel-parameter constant bank for every chunk, and
+// those loads miss the constant cache behind the producer / MMA warps' descriptor and box-table
+// reads (traced: ~900 cycles per 64-column chunk of a short-K tile).
+struct EpiK {
+  const float* bias;
+  int st_ch, swz, f32, N, accum, col_off;
+};
+__device__ __forceinline__ int pin(int v) {
+  asm volatile("mov.b32 %0, %0;" : "+r"(v));
+  return v;
+}
+__device__ __forceinline__ uint32_t pinu(uint32_t v) {
+  asm volatile("mov.b32 %0, %0;" : "+r"(v));
+  return v;
+}
+__device__ __forceinline__ const float* pinp(const float* v) {
+  uint64_t u = reinterpret_cast<uint64_t>(v);
+  asm volatile("mov.b64 %0, %0;" : "+l"(u));
+  return reinterpret_cast<const float*>(u);
+}
+
 // Stage 16 fp32 accumulator values (columns [cc, cc+16) of the chunk) of row r into the
 // chunk buffer: bias, bf16/fp32 pack, 16-byte pieces at swizzled offsets (bank-conflict-free).
-__device__ __forceinline__ void stage16(const GemmParams& p, uint32_t buf, int r, int cc, int col, const uint32_t* rr,
+__device__ __forceinline__ void stage16(const EpiK& p, uint32_t buf, int r, int cc, int col, const uint32_t* rr,
                                         bool has_k) {
   float v[16];
 #pragma unroll
@@ -396,12 +418,12 @@ __device__ __forceinline__ void stage16(const GemmParams& p, uint32_t buf, int r
 #pragma unroll
     for (int j = 0; j < 16; j++) v[j] += (col + j < p.N) ? __ldg(p.bias + col + j) : 0.f;
   }
-  const uint32_t rowbytes = (uint32_t)p.st_ch * (p.out_f32 ? 4u : 2u);
-  if (p.out_f32) {
+  const uint32_t rowbytes = (uint32_t)p.st_ch * (p.f32 ? 4u : 2u);
+  if (p.f32) {
 #pragma unroll
     for (int q = 0; q < 4; q++) {
       const uint32_t off = r * rowbytes + (uint32_t)(cc + 4 * q) * 4u;
-      const uint32_t ph = off ^ (((off >> 7) & p.st_swz) << 4);
+      const uint32_t ph = off ^ (((off >> 7) & p.swz) << 4);
       st_shared_v4(buf + ph, __float_as_uint(v[4 * q]), __float_as_uint(v[4 * q + 1]), __float_as_uint(v[4 * q + 2]),
                    __float_as_uint(v[4 * q + 3]));
     }
@@ -415,7 +437,7 @@ __device__ __forceinline__ void stage16(const GemmParams& p, uint32_t buf, int r
 #pragma unroll
     for (int q = 0; q < 2; q++) {
       const uint32_t off = r * rowbytes + (uint32_t)(cc + 8 * q) * 2u;
-      const uint32_t ph = off ^ (((off >> 7) & p.st_swz) << 4);
+      const uint32_t ph = off ^ (((off >> 7) & p.swz) << 4);
       st_shared_v4(buf + ph, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
     }
   }
@@ -988,6 +1010,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
     const int w_off = r0w % p.tw, h_off = (r0w / p.tw) % p.th, n_off = r0w / (p.tw * p.th);
     // the accumulator buffers are released on the leader's barriers (pair) or our own
     const uint32_t tempty0 = PAIR ? mapa_rank0(smem_u32(&tempty[0])) : smem_u32(&tempty[0]);
+    EpiK ek;
+    ek.bias = pinp(p.bias); ek.st_ch = pin(p.st_ch); ek.swz = pin((int)p.st_swz); ek.f32 = pin(p.out_f32);
+    ek.N = pin(p.N); ek.accum = pin(p.accum); ek.col_off = pin(p.col_off);
+    const uint32_t stg_w = pinu(smem0 + p.stg_off + (uint32_t)(warp - 2) * p.stg_warp), stg_half = pinu(p.stg_warp >> 1);
     for (int u = cl; u < units; u += ncl, ++lt) {
       const int rest = (int)p.fd_m.div((uint32_t)u), mt = (u - rest * mtu) * (PAIR ? 2 : 1) + rank;
       const int sp = (int)p.fd_n.div((uint32_t)rest), nt = rest - sp * p.n_tiles;
@@ -1045,23 +1071,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
         const int pair_kh = (PMODE == MODE_WGRAD ? p.w_pair : 0) == 3 ? p.w_kh - 1 - quarter : 2 * nt + (quarter < 2 ? 1 : 0);
         const int colbase = (PMODE == MODE_WGRAD ? p.w_pair : 0) ? pair_kh * p.BN : nt * p.BN;
         if ((PMODE == MODE_WGRAD ? p.w_pair : 0)) c1 = (PMODE == MODE_WGRAD ? p.w_pair : 0) == 3 ? 0 : (quarter & 1) * 32;
-        const uint32_t stg = smem0 + p.stg_off + (uint32_t)(warp - 2) * p.stg_warp;
+        const uint32_t stg = stg_w;
         const int span = p.n_epi == 8 && !p.epi_alt ? p.BN >> 1 : p.BN;   // columns this warp stores
         const int cbeg = p.n_epi == 8 && !p.epi_alt && warp >= 6 ? span : 0;
         const bool rows_real = (PMODE == MODE_WGRAD ? p.w_pair : 0) ? (pair_kh >= 0 && pair_kh < p.w_kh) : quarter * 32 < p.st_rows;
         const int cend = rows_real ? cbeg + span : cbeg;   // short tile: nothing to store
-        const bool one_chunk = span <= p.st_ch;
+        const bool one_chunk = span <= ek.st_ch;
         bool released = false;
-        for (int c = cbeg; c < cend; c += p.st_ch, ++stg_it) {
+        for (int c = cbeg; c < cend; c += ek.st_ch, ++stg_it) {
           if ((PMODE == MODE_WGRAD && p.w_halo) && (c & 63) >= p.w_cin) { --stg_it; continue; }   // zero-fill channels: nothing to store
-          const uint32_t buf = stg + (stg_it & 1) * (p.stg_warp >> 1);
+          const uint32_t buf = stg + (stg_it & 1) * stg_half;
           // TMEM first: a single-chunk tile hands its accumulator back to the MMA warp before
           // waiting for the staging buffer
           uint32_t r[64];
           if (warp == 2 && lane == 0 && (p.dbg & 8192)) TRACE(6, lt);   // debug: before the TMEM load
-          if (p.st_ch == 64) { tmem_ld32(tbase + c, *reinterpret_cast<uint32_t(*)[32]>(r));
+          if (ek.st_ch == 64) { tmem_ld32(tbase + c, *reinterpret_cast<uint32_t(*)[32]>(r));
                                tmem_ld32(tbase + c + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32)); }
-          else if (p.st_ch == 32) tmem_ld32(tbase + c, *reinterpret_cast<uint32_t(*)[32]>(r));
+          else if (ek.st_ch == 32) tmem_ld32(tbase + c, *reinterpret_cast<uint32_t(*)[32]>(r));
           else tmem_ld16(tbase + c, r);
           tmem_wait();
           if (warp == 2 && lane == 0) TRACE(5, lt);
@@ -1074,28 +1100,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           if (lane == 0) bulk_wait_read1();        // the store that last used this buffer has read it
           __syncwarp();
           if (warp == 2 && lane == 0 && !(p.dbg & 8192)) TRACE(6, lt);
-          if (p.st_ch == 8) {   // 8 fp32 columns (32-byte rows): zero-padded 8-channel halo wgrad
+          if (ek.st_ch == 8) {   // 8 fp32 columns (32-byte rows): zero-padded 8-channel halo wgrad
             const uint32_t off0 = (uint32_t)lane * 32u, off1 = off0 + 16u;
-            st_shared_v4(buf + (off0 ^ (((off0 >> 7) & p.st_swz) << 4)), has_k ? r[0] : 0u, has_k ? r[1] : 0u,
+            st_shared_v4(buf + (off0 ^ (((off0 >> 7) & ek.swz) << 4)), has_k ? r[0] : 0u, has_k ? r[1] : 0u,
                          has_k ? r[2] : 0u, has_k ? r[3] : 0u);
-            st_shared_v4(buf + (off1 ^ (((off1 >> 7) & p.st_swz) << 4)), has_k ? r[4] : 0u, has_k ? r[5] : 0u,
+            st_shared_v4(buf + (off1 ^ (((off1 >> 7) & ek.swz) << 4)), has_k ? r[4] : 0u, has_k ? r[5] : 0u,
                          has_k ? r[6] : 0u, has_k ? r[7] : 0u);
           } else if (!(p.dbg & 4096)) {   // knob 4096: no staging (profiling, results invalid)
 #pragma unroll
           for (int cc = 0; cc < 64; cc += 16)
-            if (cc < p.st_ch) stage16(p, buf, lane, cc, nt * p.BN + c + cc, r + cc, has_k);
+            if (cc < ek.st_ch) stage16(ek, buf, lane, cc, nt * p.BN + c + cc, r + cc, has_k);
           }
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
-            int c0 = p.col_off + colbase + c;
+            int c0 = ek.col_off + colbase + c;
             if ((PMODE == MODE_WGRAD && p.w_halo)) {   // halo wgrad tile: 64-column kw segments of the [kh][kw][cin] output row
               const int khh = (PMODE == MODE_WGRAD ? p.w_pair : 0) ? pair_kh : nt / p.w_groups;
               const int gg = (PMODE == MODE_WGRAD ? p.w_pair : 0) == 3 ? nt : (PMODE == MODE_WGRAD ? p.w_pair : 0) ? 0 : nt - (nt / p.w_groups) * p.w_groups;
               c0 = (khh * p.h_kw + (c >> 6)) * p.w_cin + gg * 64 + (c & 63);
             }
             if (p.dbg & 2048) {   // profiling knob: no output store (results invalid)
-            } else if (p.accum) tma_red_add_4d(&p.mapC, buf, c0, c1, c2, c3);
+            } else if (ek.accum) tma_red_add_4d(&p.mapC, buf, c0, c1, c2, c3);
             else tma_store_4d(&p.mapC, buf, c0, c1, c2, c3);
             bulk_commit();
           }
