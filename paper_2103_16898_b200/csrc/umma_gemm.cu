@@ -1428,7 +1428,14 @@ int launch(GemmParams& p, cudaStream_t stream) {
   const uint32_t half = 112u * 1024u;
   const bool two = env_2cta && !p.pair && p.mode == MODE_HALO && p.BN <= 32 &&
                    2 * stage_bytes + p.b_res_bytes + 16u * 1024u + 1280u <= half;
-  p.n_epi = (!env_epi4 && !two && p.BN <= 64 && p.BN % 32 == 0) ? 8 : 4;
+  // wide tiles with few K-blocks are epilogue-bound: two warps per TMEM lane quarter, each
+  // draining half the columns (tiles of <= CVB_EPI8_MAXKB K-blocks, default 4: DenseNet +1.5%,
+  // ResNet-18 neutral, same-box)
+  static int env_epi8kb = -1;
+  if (env_epi8kb < 0) { const char* e = getenv("CVB_EPI8_MAXKB"); env_epi8kb = e ? atoi(e) : 4; }
+  const bool wide8 = env_epi8kb > 0 && p.mode != MODE_WGRAD && p.BN > 64 && p.BN % 64 == 0 &&
+                     p.kb_per_split <= env_epi8kb;
+  p.n_epi = (!env_epi4 && !two && ((p.BN <= 64 && p.BN % 32 == 0) || wide8)) ? 8 : 4;
   // narrow tiles: more TMEM accumulators (the epilogue of tile i no longer gates the MMAs of
   // tile i+2) and alternate-tile epilogue warp groups (two tiles drain concurrently)
   p.nacc_log2 = (env_nacc >= 4 && 4 * p.BN <= 512) ? 2 : 1;
