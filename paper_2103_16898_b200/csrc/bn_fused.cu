@@ -361,6 +361,30 @@ __device__ __forceinline__ void bwd_load(const BwdArgs& a, int64_t r, int g, con
   }
 }
 
+// pass-1 body for one row from raw loads (mask recomputed from x): the bwd_load arithmetic,
+// accumulated into s = sum(dz), q = sum(dz * xhat) in the same order (bit-identical)
+__device__ __forceinline__ void bwd_stats_raw(const BwdArgs& a, const ChanSmem& cs, int g, const uint4& ud,
+                                              const uint4& ux, float s[8], float q[8]) {
+  // one bf16 pair at a time, per-channel constants read as scalars: few live registers (the
+  // two-CTA instantiation's 64-register cap otherwise spilled s / q every iteration)
+  const uint32_t* hd = reinterpret_cast<const uint32_t*>(&ud);
+  const uint32_t* hx = reinterpret_cast<const uint32_t*>(&ux);
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const float2 fd = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hd[i]));
+    const float2 fx = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hx[i]));
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+      const int k = 2 * i + j, c = g * 8 + k;
+      float d = j ? fd.y : fd.x;
+      const float xh = __fmul_rn(__fsub_rn(j ? fx.y : fx.x, cs.mu[c]), cs.rs[c]);
+      if (a.relu && !(__fmaf_rn(xh, cs.ga[c], cs.be[c]) > 0.f)) d = 0.f;
+      s[k] += d;
+      q[k] += d * xh;
+    }
+  }
+}
+
 // pass-2 body for one row from raw loads: dz = dy * relu-mask(x), dx = gamma*rstd*(dz - mean(dz)
 // - xhat*mean(dz*xhat)) (same arithmetic as bwd_load + the generic loop)
 __device__ __forceinline__ void bwd_apply_raw(const BwdArgs& a, const ChanSmem& cs, const float* sh, int C, int g,
@@ -437,6 +461,28 @@ __global__ void __launch_bounds__(THREADS, OCC) bn_bwd_fused(const BwdArgs a) {
   float s[8] = {0}, q[8] = {0};
   if (rl < RL) {
     int64_t r = r0 + rl;
+    if (!a.y && !a.mask && !a.dz_out) {
+      // raw 16-byte loads of two (one CTA per SM: four) rows in flight, converted one row at a
+      // time
+      if (OCC == 1)
+        for (; r + 3 * RL < r1; r += 4 * RL) {
+          uint4 ud[4], ux[4];
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            ud[j] = ldv(a.dy + (r + j * RL) * a.dycs + g * 8, hint, pk);
+            ux[j] = ldv(a.x + (r + j * RL) * a.xcs + g * 8, hint, pk);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; j++) bwd_stats_raw(a, cs, g, ud[j], ux[j], s, q);
+        }
+      for (; r + RL < r1; r += 2 * RL) {
+        const uint4 ud0 = ldv(a.dy + r * a.dycs + g * 8, hint, pk), ux0 = ldv(a.x + r * a.xcs + g * 8, hint, pk);
+        const uint4 ud1 = ldv(a.dy + (r + RL) * a.dycs + g * 8, hint, pk);
+        const uint4 ux1 = ldv(a.x + (r + RL) * a.xcs + g * 8, hint, pk);
+        bwd_stats_raw(a, cs, g, ud0, ux0, s, q);
+        bwd_stats_raw(a, cs, g, ud1, ux1, s, q);
+      }
+    }
     for (; r + RL < r1; r += 2 * RL) {
       float d0[8], x0[8], d1[8], x1[8];
       bwd_load(a, r, g, cs, d0, x0, hint, pk);
@@ -486,7 +532,19 @@ __global__ void __launch_bounds__(THREADS, OCC) bn_bwd_fused(const BwdArgs a) {
 #define R(x) (hint ? r0 + r1 - 1 - (x) : (x))
   if (a.dz_out && !a.dx32) {
     // pass 1 stored dz = dy * mask (the residual branch's gradient): pass 2 reads it instead of
-    // dy and y -- two tensors per row instead of three -- two rows' loads in flight
+    // dy and y -- two tensors per row instead of three -- two (one CTA per SM: four) rows' loads
+    // in flight
+    if (OCC == 1)
+      for (; r + 3 * RL < r1; r += 4 * RL) {
+        uint4 uz[4], ux[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          uz[j] = ldv(a.dz_out + R(r + j * RL) * C + g * 8, hint, pd);
+          ux[j] = ldv(a.x + R(r + j * RL) * a.xcs + g * 8, hint, pd);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++) bwd_apply_dz(cs, sh, C, g, uz[j], ux[j], a.dx + R(r + j * RL) * a.dxcs + g * 8);
+      }
     for (; r + RL < r1; r += 2 * RL) {
       const uint4 uz0 = ldv(a.dz_out + R(r) * C + g * 8, hint, pd);
       const uint4 ux0 = ldv(a.x + R(r) * a.xcs + g * 8, hint, pd);
@@ -504,8 +562,19 @@ __global__ void __launch_bounds__(THREADS, OCC) bn_bwd_fused(const BwdArgs a) {
     return;
   }
   if (a.two_rows && !a.dx32 && !a.y && !a.mask) {
-    // bf16 dx, mask recomputed from x: two rows' raw 16-byte loads in flight per thread (the
-    // pass is load-latency bound), converted one row at a time (stays within 64 registers)
+    // bf16 dx, mask recomputed from x: two (one CTA per SM: four) rows' raw 16-byte loads in
+    // flight per thread (the pass is load-latency bound), converted one row at a time
+    if (OCC == 1)
+      for (; r + 3 * RL < r1; r += 4 * RL) {
+        uint4 ud[4], ux[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          ud[j] = ldv(a.dy + R(r + j * RL) * a.dycs + g * 8, hint, pd);
+          ux[j] = ldv(a.x + R(r + j * RL) * a.xcs + g * 8, hint, pd);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++) bwd_apply_raw(a, cs, sh, C, g, ud[j], ux[j], a.dx + R(r + j * RL) * a.dxcs + g * 8);
+      }
     for (; r + RL < r1; r += 2 * RL) {
       const uint4 ud0 = ldv(a.dy + R(r) * a.dycs + g * 8, hint, pd);
       const uint4 ux0 = ldv(a.x + R(r) * a.xcs + g * 8, hint, pd);
@@ -724,11 +793,14 @@ int bn_backward_impl(const void* dy, int dycs, const void* x, int xcs, const voi
   BwdArgs a{(const bf16*)dy, dycs, (const bf16*)x, xcs, (const bf16*)y, ycs, rows, C, mean, rstd, gamma, beta, relu,
             ws, bar, dgamma, dbeta, (bf16*)dx, dxcs, dx32, accum32, (bf16*)dz_out, two_rows_knob(), trace_buf(),
             l2hint_knob(), (const unsigned char*)mask};
-  // one CTA per SM below 12M elements (same rule and reason as the forward; 24M measured 0.3%
-  // slower on both CNNs, 48M 2% slower on ResNet-18; the grid is fixed
-  // by (rows, C), so DenseNet's statistics-only and full passes of a layer partition alike)
+  // one CTA per SM (116+ registers, no spills; pass 1 with four rows' raw loads in flight).  The
+  // two-CTA instantiation (64 registers) spilled its statistics accumulators inside the pass-1
+  // loop; with pass 1 reworked, one CTA per SM at every size measured best (ResNet-18 +0.6% over
+  // two CTAs above 12M elements, same-box).  CVB_BN_BWD_OCC1_MAX_ELEMS: two CTAs from that size.
+  // (The grid is fixed by (rows, C): DenseNet's statistics-only and full passes of a layer
+  // partition alike.)
   static long long one_max = -1;
-  if (one_max < 0) { const char* e = getenv("CVB_BN_BWD_OCC1_MAX_ELEMS"); one_max = e ? atoll(e) : 12000000ll; }
+  if (one_max < 0) { const char* e = getenv("CVB_BN_BWD_OCC1_MAX_ELEMS"); one_max = e ? atoll(e) : (1ll << 62); }
   const bool one = rows * (int64_t)C < one_max;
   const int gb = size_grid(one ? cvb_num_sms() : grid, rows, C);
   if (C > 16 * gb) { cvb_set_error("bn_backward: more channels than finalising warps"); return CVB_EINVAL; }
