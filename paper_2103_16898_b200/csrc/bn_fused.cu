@@ -385,6 +385,30 @@ __device__ __forceinline__ void bwd_stats_raw(const BwdArgs& a, const ChanSmem& 
   }
 }
 
+// pass-1 body with the forward's ReLU mask bits (residual layers): dz = dy * mask stored to
+// dz_out (the residual branch's gradient), statistics as bwd_stats_raw
+__device__ __forceinline__ void bwd_stats_mask(const ChanSmem& cs, int g, const uint4& ud, const uint4& ux,
+                                               unsigned mb, float s[8], float q[8], bf16* dz_dst) {
+  const uint32_t* hd = reinterpret_cast<const uint32_t*>(&ud);
+  const uint32_t* hx = reinterpret_cast<const uint32_t*>(&ux);
+  float dz[8];
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const float2 fd = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hd[i]));
+    const float2 fx = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hx[i]));
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+      const int k = 2 * i + j, c = g * 8 + k;
+      const float d = ((mb >> k) & 1u) ? (j ? fd.y : fd.x) : 0.f;
+      const float xh = __fmul_rn(__fsub_rn(j ? fx.y : fx.x, cs.mu[c]), cs.rs[c]);
+      s[k] += d;
+      q[k] += d * xh;
+      dz[k] = d;
+    }
+  }
+  if (dz_dst) st8(dz_dst, dz);
+}
+
 // pass-2 body for one row from raw loads: dz = dy * relu-mask(x), dx = gamma*rstd*(dz - mean(dz)
 // - xhat*mean(dz*xhat)) (same arithmetic as bwd_load + the generic loop)
 __device__ __forceinline__ void bwd_apply_raw(const BwdArgs& a, const ChanSmem& cs, const float* sh, int C, int g,
@@ -481,6 +505,22 @@ __global__ void __launch_bounds__(THREADS, OCC) bn_bwd_fused(const BwdArgs a) {
         const uint4 ux1 = ldv(a.x + (r + RL) * a.xcs + g * 8, hint, pk);
         bwd_stats_raw(a, cs, g, ud0, ux0, s, q);
         bwd_stats_raw(a, cs, g, ud1, ux1, s, q);
+      }
+    }
+    if (OCC == 1 && a.mask && a.relu && !a.y) {   // residual layers: the forward's mask bits
+      const int Gm = C / 8;
+      for (; r + 3 * RL < r1; r += 4 * RL) {
+        uint4 ud[4], ux[4];
+        unsigned mb[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          ud[j] = ldv(a.dy + (r + j * RL) * a.dycs + g * 8, hint, pk);
+          ux[j] = ldv(a.x + (r + j * RL) * a.xcs + g * 8, hint, pk);
+          mb[j] = ldg_u8(a.mask + (r + j * RL) * Gm + g, hint, pk);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+          bwd_stats_mask(cs, g, ud[j], ux[j], mb[j], s, q, a.dz_out ? a.dz_out + (r + j * RL) * C + g * 8 : nullptr);
       }
     }
     for (; r + RL < r1; r += 2 * RL) {
