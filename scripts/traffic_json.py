@@ -7,7 +7,9 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 KIND = {"umma_gemm_kernel": "umma_gemm", "bn_bwd_fused": "bn", "bn_fwd_fused": "bn", "bn_apply": "bn",
-        "chan_stats_partial": "bn", "bn_finalize": "bn", "head_train_kernel": "head", "softmax_xent_mean": "head"}
+        "chan_stats_partial": "bn", "bn_finalize": "bn", "bn_gather_dx": "bn", "head_train_kernel": "head",
+        "softmax_xent_mean": "head", "transpose_batched": "layout", "adam_step_dev": "optimizer",
+        "reduce_splits": "reduce", "reduce_splits_flat": "reduce", "reduce_splits_flat4": "reduce"}
 
 
 def summarize(path):
