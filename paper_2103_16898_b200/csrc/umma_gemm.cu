@@ -866,8 +866,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) umma_gemm_kernel(const __grid_
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint64_t a0 = adr[0] + ((smem0 + s * stage_bytes) >> 4);
-          for (int t = 0; t < p.h_kh * p.h_kw; t++) {
-            const int kh = t / 3, kw = t - kh * 3;   // host plans 3x3 only
+          const int hkw = p.h_kw, ntap = p.h_kh * hkw;
+          for (int t = 0, kh = 0, kw = 0; t < ntap; t++, kw = kw + 1 == hkw ? 0 : kw + 1, kh += kw == 0 ? 1 : 0) {
             mbar_wait(&full_b[sbm], phbm);
             tc_fence_after();
             const uint64_t b0 = bdr[0] + ((bres + sbm * p.b_tap_bytes) >> 4);
@@ -1617,6 +1617,47 @@ uint32_t gather_entry(int k_elem, int cin, int ntaps, int KW, int pad, int strid
 //   y[n,oh,ow, yoff+co] = bias[co] + sum_{kh,kw,ci} x[n, oh*s-pad+kh, ow*s-pad+kw, ci] * w[co][kh][kw][ci]
 // x: NHWC bf16 (channel stride xcs, channels [0,cin)), cin multiple of 8.
 // w: bf16 [cout][kh*kw*cin] (K-major).  y: NHWC (bf16, or fp32 if y_f32) with channel stride ycs.
+// Halo conv with streamed weights (see cvb_conv2d_fwd): stride 1, any KH x KW <= 3 x 3 with
+// top/left padding pad (bottom/right overflow is TMA zero fill), 8 x 16 pixel tiles, the kw-box
+// halo of one 64-channel group per K-block, one weight-tap box per ring slot.
+static bool hs_fits(int n, int oh, int ow, int cin, int xcs, int cout) {
+  return cin % 64 == 0 && cin >= 128 && cout % 32 == 0 && cout <= 256 && ow % 8 == 0 && oh % 16 == 0 && xcs % 8 == 0 &&
+         n > 0;
+}
+static int plan_hs(GemmParams& p, const void* x, int n, int h, int w, int cin, int xcs, const void* wt, int cout, int kh, int kw,
+            int pad, void* y, int oh, int ow, int ycs, int yoff, const float* bias, int y_f32, int accumulate) {
+  memset(&p, 0, sizeof(p));
+  const int Kh = kh * kw * cin, BNh = pick_bn(cout), hrows = 16 + kh - 1;
+  p.mode = MODE_HALO;
+  p.hs = 1;
+  p.a_major = 0; p.b_major = 0;
+  p.a_cel = 8; p.b_cel = 64;
+  p.gb = 1;
+  p.BN = BNh;
+  p.M = n * oh * ow; p.N = cout;
+  p.tw = 8; p.th = 16; p.tn = 1;
+  p.ptiles_w = ow / 8; p.ptiles_h = oh / 16;
+  p.m_tiles = p.ptiles_w * p.ptiles_h * n;
+  p.n_tiles = 1; p.splits = 1;
+  p.h_cin = cin; p.h_cg = 64; p.h_pad = pad; p.h_kh = kh; p.h_kw = kw;
+  p.h_rows = 1; p.h_kwbox = 1; p.h_planes = kw; p.h_pitch = 8;
+  p.h_box_bytes = 8u * (uint32_t)hrows * 128u;
+  p.h_plane_stride = (p.h_box_bytes + 1023) / 1024 * 1024;
+  p.a_stage_bytes = (uint32_t)kw * p.h_plane_stride;
+  p.num_kb = cin / 64; p.kb_per_split = p.num_kb;
+  p.OH = oh; p.OW = ow; p.NIMG = n;
+  p.b_res = 0; p.b_res_bytes = 0;
+  p.tx_bytes = (uint32_t)kw * p.h_box_bytes;
+  p.b_tap_bytes = (uint32_t)BNh * 128u;   // launch(): halved for the CTA pair
+  int rc;
+  if ((rc = encode_nhwc(&p.mapA[0], x, n, h, w, cin, xcs, 64, 8, hrows, 1))) return rc;
+  if ((rc = encode_2d(&p.mapB[0], wt, cout, Kh, Kh, 64, BNh))) return rc;
+  p.b_ptr = wt; p.b_rows = cout; p.b_cols = Kh; p.b_ld = Kh;
+  p.out_mode = OUT_NHWC; p.out_f32 = y_f32; p.out = y; p.ldc = ycs; p.col_off = yoff; p.bias = bias;
+  p.accum = accumulate;
+  return CVB_OK;
+}
+
 CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs, const void* wt, int cout, int kh,
                            int kw, int stride, int pad, void* y, int oh, int ow, int ycs, int yoff, const float* bias,
                            int y_f32, int accumulate, void* stream) {
@@ -1756,35 +1797,10 @@ CVB_API int cvb_conv2d_fwd(const void* x, int n, int h, int w, int cin, int xcs,
     if (no_hs < 0) no_hs = getenv("CVB_NO_HALO_STREAM") ? 1 : 0;
     const int Kh = kh * kw * cin, BNh = pick_bn(cout);
     const uint32_t b_all_h = (uint32_t)((Kh + BK - 1) / BK) * BNh * BK * 2;
-    if (!no_hs && stride == 1 && kh == 3 && kw == 3 && pad == 1 && cin % 64 == 0 && cin >= 128 && cout % 32 == 0 &&
-        cout <= 256 && b_all_h > 96u * 1024u && ow % 8 == 0 && oh % 16 == 0 && xcs % 8 == 0) {
-      p.mode = MODE_HALO;
-      p.hs = 1;
-      p.a_major = 0; p.b_major = 0;
-      p.a_cel = 8; p.b_cel = 64;
-      p.gb = 1;
-      p.BN = BNh;
-      p.M = n * oh * ow; p.N = cout;
-      p.tw = 8; p.th = 16; p.tn = 1;
-      p.ptiles_w = ow / 8; p.ptiles_h = oh / 16;
-      p.m_tiles = p.ptiles_w * p.ptiles_h * n;
-      p.n_tiles = 1; p.splits = 1;
-      p.h_cin = cin; p.h_cg = 64; p.h_pad = pad; p.h_kh = kh; p.h_kw = kw;
-      p.h_rows = 1; p.h_kwbox = 1; p.h_planes = kw; p.h_pitch = 8;
-      p.h_box_bytes = 8u * 18u * 128u;
-      p.h_plane_stride = (p.h_box_bytes + 1023) / 1024 * 1024;
-      p.a_stage_bytes = (uint32_t)kw * p.h_plane_stride;
-      p.num_kb = cin / 64; p.kb_per_split = p.num_kb;
-      p.OH = oh; p.OW = ow; p.NIMG = n;
-      p.b_res = 0; p.b_res_bytes = 0;
-      p.tx_bytes = (uint32_t)kw * p.h_box_bytes;
-      p.b_tap_bytes = (uint32_t)BNh * 128u;   // launch(): halved for the CTA pair
-      int rc;
-      if ((rc = encode_nhwc(&p.mapA[0], x, n, h, w, cin, xcs, 64, 8, 18, 1))) return rc;
-      if ((rc = encode_2d(&p.mapB[0], wt, cout, Kh, Kh, 64, BNh))) return rc;
-      p.b_ptr = wt; p.b_rows = cout; p.b_cols = Kh; p.b_ld = Kh;
-      p.out_mode = OUT_NHWC; p.out_f32 = y_f32; p.out = y; p.ldc = ycs; p.col_off = yoff; p.bias = bias;
-      p.accum = accumulate;
+    if (!no_hs && stride == 1 && kh == 3 && kw == 3 && pad == 1 && b_all_h > 96u * 1024u &&
+        hs_fits(n, oh, ow, cin, xcs, cout)) {
+      int rc = plan_hs(p, x, n, h, w, cin, xcs, wt, cout, kh, kw, pad, y, oh, ow, ycs, yoff, bias, y_f32, accumulate);
+      if (rc) return rc;
       return launch(p, (cudaStream_t)stream);
     }
   }
@@ -1988,12 +2004,27 @@ CVB_API int cvb_conv2d_dgrad_s2_rows(const void* dy, int n, int oh, int ow, int 
   static const int dh0[2] = {0, 0}, dw0[2] = {0, 1};
   static const int dh1[4] = {0, 0, 1, 1}, dw1[4] = {0, 1, 0, 1};
   const void* w1 = (const char*)wrows + (size_t)2 * cin * 2 * cout * 2;
-  int rc = plan_gather_conv(plans[0], dy, n, oh, ow, cout, dycs, wrows, 2 * cin, 2, dh0, dw0, dx, h, ow, 2 * dxcs, 0, 0,
-                            accumulate, 1);
-  if (rc) return rc;
-  rc = plan_gather_conv(plans[1], dy, n, oh, ow, cout, dycs, w1, 2 * cin, 4, dh1, dw1, dx, h, ow, 2 * dxcs, 1, 0,
-                        accumulate, 1);
-  if (rc) return rc;
+  // dY maps of 16 x 16 and larger (ResNet-18 stage 2): the halo plan with streamed weights --
+  // conv 0 is a 1 x 2 and conv 1 a 2 x 2 stride-1 conv of dY, no top/left padding (the
+  // bottom/right overflow is TMA zero fill); the dY halo is read once per channel group
+  static int no_hs = -1;
+  if (no_hs < 0) no_hs = getenv("CVB_NO_DGRAD_ROWS_HS") ? 1 : 0;
+  int rc;
+  if (!no_hs && hs_fits(n, oh, ow, cout, dycs, 2 * cin)) {
+    for (int a = 0; a < 2; a++) {
+      if ((rc = plan_hs(plans[a], dy, n, oh, ow, cout, dycs, a ? w1 : wrows, 2 * cin, a ? 2 : 1, 2, 0, dx, oh, ow,
+                        2 * dxcs, 0, nullptr, 0, accumulate)))
+        return rc;
+      plans[a].out_par = 2; plans[a].out_ph = a; plans[a].out_pw = 0; plans[a].out_H = h; plans[a].out_W = ow;
+    }
+  } else {
+    rc = plan_gather_conv(plans[0], dy, n, oh, ow, cout, dycs, wrows, 2 * cin, 2, dh0, dw0, dx, h, ow, 2 * dxcs, 0, 0,
+                          accumulate, 1);
+    if (rc) return rc;
+    rc = plan_gather_conv(plans[1], dy, n, oh, ow, cout, dycs, w1, 2 * cin, 4, dh1, dw1, dx, h, ow, 2 * dxcs, 1, 0,
+                          accumulate, 1);
+    if (rc) return rc;
+  }
   for (int a = 0; a < 2; a++)
     if ((rc = launch(plans[a], (cudaStream_t)stream))) return rc;
   return CVB_OK;
