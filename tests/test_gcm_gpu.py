@@ -80,6 +80,30 @@ def test_large_message_tag_and_tamper_at_end():
         crypto.aead_open(key, iv, b"x", bytes(m))
 
 
+@pytest.mark.parametrize("extra", [-1, 0, 17])
+@pytest.mark.parametrize("alen", [0, 13, 200])
+def test_multi_pass_messages_around_pass_boundaries(extra, alen):
+    """Messages of two and three passes (one pass = 148 SMs x 1024 threads x 16 B): the GHASH
+    digit tables, the folded AES round 1 and the per-thread round-2 lookups of the fixed counter
+    byte are only used here; seal and open both bit-exact against `cryptography`."""
+    from cryptography.hazmat.primitives.ciphers.aead import AESGCM
+
+    import torch
+
+    per_pass = torch.cuda.get_device_properties(0).multi_processor_count * 1024 * 16
+    rng = np.random.default_rng(alen * 7 + extra + 3)
+    key, iv, aad = rng.bytes(32), rng.bytes(12), rng.bytes(alen)
+    for passes in (2, 3):
+        pt = rng.integers(0, 256, size=passes * per_pass + extra, dtype=np.uint8).tobytes()
+        blob = AESGCM(key).encrypt(iv, pt, aad)
+        assert crypto.aead_seal(key, iv, aad, pt) == blob
+        assert crypto.aead_open(key, iv, aad, blob) == pt
+        bad = bytearray(blob)
+        bad[-1] ^= 1
+        with pytest.raises(crypto.AuthenticationFailure):
+            crypto.aead_open(key, iv, aad, bytes(bad))
+
+
 def test_device_open_poisons_on_failure():
     import torch
 
@@ -128,7 +152,7 @@ def test_volume_round_trip_and_reference_interop(tmp_path):
     assert Volume.open(tmp_path / "v").get(key, "ref.bin") == b"written by the reference"
 
 
-@pytest.mark.parametrize("c,h,w,nrec", [(3, 32, 32, 37), (1, 224, 224, 3), (3, 32, 32, 1)])
+@pytest.mark.parametrize("c,h,w,nrec", [(3, 32, 32, 37), (1, 224, 224, 3), (3, 32, 32, 1), (1, 224, 224, 128)])
 def test_fused_decrypt_normalise_matches_two_kernel_path(c, h, w, nrec):
     """K1b: cvb_gcm_open_records_dev (one kernel) == GCM open + records_to_nhwc, bit for bit,
     and a tampered shard leaves an all-zero tile and labels."""
