@@ -371,6 +371,30 @@ __global__ void maxpool_bwd_idx(const uint8_t* __restrict__ idx, const bf16* __r
 
 // 2x2 / stride-2 windows do not overlap: one thread per output pixel and 8-channel group
 // routes dy to the window's first arg-max and writes zeros to the other three inputs.
+// 2x2 stride-2 max-pool forward: the four window loads issued together (the generic kernel's
+// runtime k loop issues them one after another); same comparison order -> identical output
+__global__ void maxpool2_fwd(const bf16* __restrict__ x, int n, int h, int w, int C, int oh, int ow,
+                             bf16* __restrict__ y, int ycs) {
+  CVB_PDL_PROLOGUE();
+  const int G = C / 8;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * oh * ow * G) return;
+  const int g = (int)(i % G);
+  const int64_t pix = i / G;
+  const int ox = (int)(pix % ow), oy = (int)((pix / ow) % oh), b = (int)(pix / ((int64_t)ow * oh));
+  float v[4][8], m[8];
+#pragma unroll
+  for (int q = 0; q < 4; q++)
+    load8(x + (((int64_t)b * h + 2 * oy + (q >> 1)) * w + 2 * ox + (q & 1)) * C + g * 8, v[q]);
+#pragma unroll
+  for (int c = 0; c < 8; c++) {
+    m[c] = -INFINITY;
+#pragma unroll
+    for (int q = 0; q < 4; q++) if (v[q][c] > m[c]) m[c] = v[q][c];
+  }
+  store8(y + pix * ycs + g * 8, m);
+}
+
 __global__ void maxpool2_bwd(const bf16* __restrict__ x, const bf16* __restrict__ dyp, int n, int h, int w, int C,
                              int oh, int ow, bf16* __restrict__ dx) {
   CVB_PDL_PROLOGUE();
@@ -1114,8 +1138,12 @@ CVB_API int cvb_bn_backward(const void* dy, int dycs, const void* x, int xcs, co
 
 CVB_API int cvb_maxpool_fwd(const void* x, int n, int h, int w, int C, int k, int s, int p, void* y, int oh, int ow,
                             int ycs, void* stream) {
-  cvb_launch(maxpool_fwd, nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM, (const bf16*)x, n, h, w, C, k, s, p, oh, ow,
-                                                                          (bf16*)y, ycs);
+  if (k == 2 && s == 2 && p == 0 && h == 2 * oh && w == 2 * ow)
+    cvb_launch(maxpool2_fwd, nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM, (const bf16*)x, n, h, w, C, oh, ow,
+               (bf16*)y, ycs);
+  else
+    cvb_launch(maxpool_fwd, nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM, (const bf16*)x, n, h, w, C, k, s, p, oh,
+               ow, (bf16*)y, ycs);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
