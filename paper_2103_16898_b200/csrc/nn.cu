@@ -340,6 +340,88 @@ __global__ void maxpool_fwd_idx(const bf16* __restrict__ x, int n, int h, int w,
 }
 
 // gather: input (iy, ix) takes dy of every window (oy, ox) whose stored arg-max is it
+// 3x3 / stride-2 / pad-1 (the DenseNet stem pool) with every window load in flight: the generic
+// kernels walk runtime-k loops with runtime divisions, one dependent load at a time.  Same
+// comparison / accumulation order as the generic forms -> identical outputs.
+__global__ void maxpool3s2_fwd_idx(const bf16* __restrict__ x, int n, int h, int w, int C, int oh, int ow,
+                                   bf16* __restrict__ y, int ycs, uint8_t* __restrict__ idx) {
+  CVB_PDL_PROLOGUE();
+  const int G = C / 8;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * oh * ow * G) return;
+  const int g = (int)(i % G);
+  const int64_t pix = i / G;
+  const int ox = (int)(pix % ow), oy = (int)((pix / ow) % oh), b = (int)(pix / ((int64_t)ow * oh));
+  uint4 u[9];
+#pragma unroll
+  for (int q = 0; q < 9; q++) {
+    const int iy = 2 * oy - 1 + q / 3, ix = 2 * ox - 1 + q % 3;
+    u[q] = (iy >= 0 && iy < h && ix >= 0 && ix < w)
+               ? *reinterpret_cast<const uint4*>(x + (((int64_t)b * h + iy) * w + ix) * C + g * 8)
+               : make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u);   // -inf: never > m
+  }
+  float m[8];
+  uint32_t am[8];
+#pragma unroll
+  for (int c = 0; c < 8; c++) { m[c] = -INFINITY; am[c] = 0; }
+#pragma unroll
+  for (int q = 0; q < 9; q++) {
+    const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&u[q]);
+#pragma unroll
+    for (int c2 = 0; c2 < 4; c2++) {
+      const float2 f = __bfloat1622float2(hv[c2]);
+      if (f.x > m[2 * c2]) { m[2 * c2] = f.x; am[2 * c2] = (uint32_t)q; }
+      if (f.y > m[2 * c2 + 1]) { m[2 * c2 + 1] = f.y; am[2 * c2 + 1] = (uint32_t)q; }
+    }
+  }
+  store8(y + pix * ycs + g * 8, m);
+  uint2 packed = make_uint2(am[0] | (am[1] << 8) | (am[2] << 16) | (am[3] << 24),
+                            am[4] | (am[5] << 8) | (am[6] << 16) | (am[7] << 24));
+  *reinterpret_cast<uint2*>(idx + pix * C + g * 8) = packed;
+}
+
+__global__ void maxpool3s2_bwd_idx(const uint8_t* __restrict__ idx, const bf16* __restrict__ dyp, int n, int h, int w,
+                                   int C, int oh, int ow, bf16* __restrict__ dx) {
+  CVB_PDL_PROLOGUE();
+  const int G = C / 8;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * h * w * G) return;
+  const int g = (int)(i % G);
+  const int64_t pix = i / G;
+  const int ix = (int)(pix % w), iy = (int)((pix / w) % h), b = (int)(pix / ((int64_t)w * h));
+  // windows covering (iy, ix): oy in [iy >> 1, (iy + 1) >> 1], ox likewise (clipped)
+  const int oy0 = iy >> 1, oy1 = min(oh - 1, (iy + 1) >> 1), ox0 = ix >> 1, ox1 = min(ow - 1, (ix + 1) >> 1);
+  uint2 a[4];
+  uint4 d[4];
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const int oy = oy0 + (q >> 1), ox = ox0 + (q & 1);
+    if (oy <= oy1 && ox <= ox1) {
+      const int64_t o = (((int64_t)b * oh + oy) * ow + ox) * C + g * 8;
+      a[q] = *reinterpret_cast<const uint2*>(idx + o);
+      d[q] = *reinterpret_cast<const uint4*>(dyp + o);
+    }
+  }
+  float acc[8] = {0};
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const int oy = oy0 + (q >> 1), ox = ox0 + (q & 1);
+    if (oy <= oy1 && ox <= ox1) {
+      const uint32_t me = (uint32_t)((iy - (oy * 2 - 1)) * 3 + (ix - (ox * 2 - 1)));
+      float dv[8];
+      const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&d[q]);
+#pragma unroll
+      for (int c2 = 0; c2 < 4; c2++) { const float2 f = __bfloat1622float2(hv[c2]); dv[2 * c2] = f.x; dv[2 * c2 + 1] = f.y; }
+#pragma unroll
+      for (int c = 0; c < 8; c++) {
+        const uint32_t am = ((c < 4 ? a[q].x : a[q].y) >> (8 * (c & 3))) & 0xffu;
+        if (am == me) acc[c] += dv[c];
+      }
+    }
+  }
+  store8(dx + pix * C + g * 8, acc);
+}
+
 __global__ void maxpool_bwd_idx(const uint8_t* __restrict__ idx, const bf16* __restrict__ dyp, int n, int h, int w,
                                 int C, int k, int s, int p, int oh, int ow, bf16* __restrict__ dx) {
   CVB_PDL_PROLOGUE();
@@ -369,8 +451,6 @@ __global__ void maxpool_bwd_idx(const uint8_t* __restrict__ idx, const bf16* __r
   store8(dx + pix * C + g * 8, acc);
 }
 
-// 2x2 / stride-2 windows do not overlap: one thread per output pixel and 8-channel group
-// routes dy to the window's first arg-max and writes zeros to the other three inputs.
 // 2x2 stride-2 max-pool forward: the four window loads issued together (the generic kernel's
 // runtime k loop issues them one after another); same comparison order -> identical output
 __global__ void maxpool2_fwd(const bf16* __restrict__ x, int n, int h, int w, int C, int oh, int ow,
@@ -395,6 +475,8 @@ __global__ void maxpool2_fwd(const bf16* __restrict__ x, int n, int h, int w, in
   store8(y + pix * ycs + g * 8, m);
 }
 
+// 2x2 / stride-2 windows do not overlap: one thread per output pixel and 8-channel group
+// routes dy to the window's first arg-max and writes zeros to the other three inputs.
 __global__ void maxpool2_bwd(const bf16* __restrict__ x, const bf16* __restrict__ dyp, int n, int h, int w, int C,
                              int oh, int ow, bf16* __restrict__ dx) {
   CVB_PDL_PROLOGUE();
@@ -1163,16 +1245,24 @@ CVB_API int cvb_maxpool_bwd(const void* x, const void* dy, int n, int h, int w, 
 CVB_API int cvb_maxpool_fwd_idx(const void* x, int n, int h, int w, int C, int k, int s, int p, void* y, int oh, int ow,
                                 int ycs, void* idx, void* stream) {
   if (C % 8 || k * k > 256) { cvb_set_error("maxpool_fwd_idx: bad shape"); return CVB_EINVAL; }
-  cvb_launch(maxpool_fwd_idx, nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM, (const bf16*)x, n, h, w, C, k, s, p, oh,
-                                                                              ow, (bf16*)y, ycs, (uint8_t*)idx);
+  if (k == 3 && s == 2 && p == 1 && oh == (h - 1) / 2 + 1 && ow == (w - 1) / 2 + 1)
+    cvb_launch(maxpool3s2_fwd_idx, nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM, (const bf16*)x, n, h, w, C, oh,
+               ow, (bf16*)y, ycs, (uint8_t*)idx);
+  else
+    cvb_launch(maxpool_fwd_idx, nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM, (const bf16*)x, n, h, w, C, k, s, p,
+               oh, ow, (bf16*)y, ycs, (uint8_t*)idx);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }
 
 CVB_API int cvb_maxpool_bwd_idx(const void* idx, const void* dy, int n, int h, int w, int C, int k, int s, int p, int oh,
                                 int ow, void* dx, void* stream) {
-  cvb_launch(maxpool_bwd_idx, nblocks((int64_t)n * h * w * (C / 8)), 256, 0, STREAM, (const uint8_t*)idx, (const bf16*)dy, n, h,
-                                                                            w, C, k, s, p, oh, ow, (bf16*)dx);
+  if (k == 3 && s == 2 && p == 1 && oh == (h - 1) / 2 + 1 && ow == (w - 1) / 2 + 1)
+    cvb_launch(maxpool3s2_bwd_idx, nblocks((int64_t)n * h * w * (C / 8)), 256, 0, STREAM, (const uint8_t*)idx,
+               (const bf16*)dy, n, h, w, C, oh, ow, (bf16*)dx);
+  else
+    cvb_launch(maxpool_bwd_idx, nblocks((int64_t)n * h * w * (C / 8)), 256, 0, STREAM, (const uint8_t*)idx, (const bf16*)dy,
+               n, h, w, C, k, s, p, oh, ow, (bf16*)dx);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }

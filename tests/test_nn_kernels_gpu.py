@@ -119,7 +119,7 @@ def test_bn_single_launch_forward_backward(rows, C, xcs, res):
     assert torch.equal(dx32[:, C:], base[:, C:])
 
 
-@pytest.mark.parametrize("k,s,p,h", [(2, 2, 0, 32), (3, 2, 1, 112), (2, 2, 0, 8)])
+@pytest.mark.parametrize("k,s,p,h", [(2, 2, 0, 32), (3, 2, 1, 112), (2, 2, 0, 8), (3, 2, 1, 9), (3, 2, 1, 8)])
 def test_maxpool_exact(k, s, p, h):
     x = torch.randn(4, h, h, 64, device=dev).bfloat16()
     x[0, :4, :4] = 1.0   # ties: first max wins, like torch
