@@ -531,6 +531,29 @@ __global__ void avgpool_fwd(const bf16* __restrict__ x, int n, int h, int w, int
   store8(y + pix * ycs + g * 8, a);
 }
 
+// 2x2 average pool (DenseNet transitions): the four window loads in flight, same summation order
+__global__ void avgpool2_fwd(const bf16* __restrict__ x, int n, int h, int w, int C, int xcs, int oh, int ow,
+                             bf16* __restrict__ y, int ycs) {
+  CVB_PDL_PROLOGUE();
+  const int G = C / 8;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * oh * ow * G) return;
+  const int g = (int)(i % G);
+  const int64_t pix = i / G;
+  const int ox = (int)(pix % ow), oy = (int)((pix / ow) % oh), b = (int)(pix / ((int64_t)ow * oh));
+  float v[4][8], a[8] = {0};
+#pragma unroll
+  for (int q = 0; q < 4; q++)
+    load8(x + (((int64_t)b * h + oy * 2 + (q >> 1)) * w + ox * 2 + (q & 1)) * xcs + g * 8, v[q]);
+#pragma unroll
+  for (int q = 0; q < 4; q++)
+#pragma unroll
+    for (int c = 0; c < 8; c++) a[c] += v[q][c];
+#pragma unroll
+  for (int c = 0; c < 8; c++) a[c] *= 0.25f;
+  store8(y + pix * ycs + g * 8, a);
+}
+
 __global__ void avgpool_bwd(const bf16* __restrict__ dy, int n, int h, int w, int C, int k, int oh, int ow,
                             bf16* __restrict__ dx, int dxcs) {
   CVB_PDL_PROLOGUE();
@@ -1269,8 +1292,12 @@ CVB_API int cvb_maxpool_bwd_idx(const void* idx, const void* dy, int n, int h, i
 
 CVB_API int cvb_avgpool_fwd(const void* x, int n, int h, int w, int C, int xcs, int k, void* y, int ycs, void* stream) {
   const int oh = h / k, ow = w / k;
-  cvb_launch(avgpool_fwd, nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM, (const bf16*)x, n, h, w, C, xcs, k, oh, ow,
-                                                                          (bf16*)y, ycs);
+  if (k == 2)
+    cvb_launch(avgpool2_fwd, nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM, (const bf16*)x, n, h, w, C, xcs, oh, ow,
+               (bf16*)y, ycs);
+  else
+    cvb_launch(avgpool_fwd, nblocks((int64_t)n * oh * ow * (C / 8)), 256, 0, STREAM, (const bf16*)x, n, h, w, C, xcs, k, oh,
+               ow, (bf16*)y, ycs);
   CVB_CHECK_LAUNCH();
   return CVB_OK;
 }

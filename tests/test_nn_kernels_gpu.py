@@ -149,6 +149,9 @@ def test_avgpool_and_gap():
     y = torch.empty(4, 7, 7, 128, device=dev, dtype=torch.bfloat16)
     K.avgpool_fwd(x, 4, 14, 14, 128, 128, 2, y)
     assert rel(nchw(y), F.avg_pool2d(nchw(x), 2)) < 4e-3
+    xf = x.float()   # the kernel's exact arithmetic: fp32 sum in window order, * 0.25, bf16 round
+    ref2 = ((((xf[:, 0::2, 0::2] + xf[:, 0::2, 1::2]) + xf[:, 1::2, 0::2]) + xf[:, 1::2, 1::2]) * 0.25).bfloat16()
+    assert torch.equal(y, ref2)
     dy = torch.randn(4, 7, 7, 128, device=dev).bfloat16()
     dx = torch.empty_like(x)
     K.avgpool_bwd(dy, 4, 14, 14, 128, 2, dx, 128)
